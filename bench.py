@@ -1,0 +1,449 @@
+#!/usr/bin/env python
+"""bench.py -- one step = one pass of the whole TQP hot path
+over one TPC-H-shaped batch, timed on B200.
+
+Step (per rank, BASELINE.json configs[2] size: SF10 = 15M orders / ~60M lineitem):
+  1. tqp_pkfk_join   lineitem.l_orderkey -> orders.o_orderkey      (a1-a4: build radix sort,
+                                                                      bracket probe, compaction)
+  2. tqp_smj_*       generic m:n sort-merge join of the same keys  (a1-a2, a5-a7)
+  3. tqp_groupby_agg TPC-H Q1: filter + group by (returnflag, linestatus), 8 aggregates (a8-a10)
+  4. tqp_filter_compact  TPC-H Q6 predicates -> bitmap + selection vector (a10)
+  5. tqp_groupby_agg Q6 revenue: fused filter + sum (n_keys = 0)
+Multi-GPU (torchrun, one process per GPU): each rank holds an SF10-sized co-partitioned slice
+of an SF(10*N) dataset (lineitem range-partitioned with its orders), so the
+joins need no exchange; the Q1/Q6 partial aggregates are all-gathered over NCCL and merged by
+libtqp (tqp_groupby_merge). scaling = "weak".
+
+value = lineitem rows processed per second by the whole job (all ranks), device-timed with
+CUDA events, max over ranks. Inputs (2.8 GB/rank) are larger than L2 (126 MB).
+`--impl reference` times the CPU oracle (oracle/, single-threaded C) on a bounded sample.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from datagen import tpch_orders_lineitem                                    # noqa: E402
+from datagen.queries import (Q1_AGGS, Q1_COLS, Q1_KEYS, Q1_PREDS, Q6_AGGS,  # noqa: E402
+                             Q6_COLS, Q6_PREDS, columns)
+from datagen.tpch import orders_count                                       # noqa: E402
+
+BASE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASE["metric"]
+SF_PER_RANK = 10.0
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, ValueError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, mx, reasons = [], [], set()
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx.append(float(s[1]))
+                for i, n in enumerate(names):
+                    if s[2 + i].lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ data
+
+def make_data(rank, world, device, layout):
+    n_o = orders_count(SF_PER_RANK)
+    orders, li = tpch_orders_lineitem(SF_PER_RANK * world, seed=42, device=device, layout=layout,
+                                      order_range=(rank * n_o, (rank + 1) * n_o))
+    return orders, li
+
+
+def q_avg_rewrite(aggs):
+    """Distributed AVG: compute SUM (same expression) + one COUNT per rank; merge recomputes AVG."""
+    out = []
+    for op, f in aggs:
+        out.append(("sum", f) if op == "avg" else (op, f))
+    out.append(("count", []))
+    return out
+
+
+# ------------------------------------------------------------------ GPU step
+
+class HotPath:
+    def __init__(self, T, orders, li, world):
+        self.T = T
+        self.ctx = T.context()
+        self.world = world
+        self.ok = orders["o_orderkey"]
+        self.lk = li["l_orderkey"]
+        self.q1 = columns(li, Q1_COLS)
+        self.q6 = columns(li, Q6_COLS)
+        self.n = self.lk.numel()
+        self.op_ms = {}
+        self._ev = []
+
+    def _mark(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self._ev.append((name, e))
+
+    def groupby(self, cols, keys, aggs, preds):
+        T = self.T
+        if self.world == 1:
+            return T.groupby_agg(cols, keys, aggs, preds)
+        from paper_2203_01877_b200 import dist
+        return dist.groupby_agg(self.ctx, cols, keys, aggs, preds)
+
+    def step(self, ok=None, lk=None, q1=None, q6=None):
+        ok = self.ok if ok is None else ok
+        lk = self.lk if lk is None else lk
+        q1 = self.q1 if q1 is None else q1
+        q6 = self.q6 if q6 is None else q6
+        c = self.ctx
+        self._mark("start")
+        lo, ro = c.pkfk_join(ok, lk)
+        self._mark("pkfk_join")
+        plan = c.smj_prepare(ok, lk)
+        sl, sr = plan.expand(0, plan.size)
+        plan.release()
+        self._mark("smj_join")
+        r1 = self.groupby(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS)
+        self._mark("q1_groupby")
+        mask, sel = c.filter_compact(q6, Q6_PREDS)
+        self._mark("q6_filter")
+        r6 = self.groupby(q6, [], Q6_AGGS, Q6_PREDS)
+        self._mark("q6_sum")
+        return {"pkfk": (lo, ro), "smj": (sl, sr), "q1": r1, "q6_mask": mask, "q6_sel": sel, "q6": r6}
+
+    def collect_ops(self):
+        torch.cuda.synchronize()
+        for i in range(1, len(self._ev)):
+            name, e = self._ev[i]
+            if name == "start":
+                continue
+            self.op_ms[name] = self.op_ms.get(name, 0.0) + self._ev[i - 1][1].elapsed_time(e)
+        self._ev = []
+
+
+def result_to_host(res, pinned_out):
+    """D2H of every result of the step into pinned host buffers (e2e leg). Returns bytes."""
+    nbytes = 0
+    flat = [res["pkfk"][0], res["pkfk"][1], res["smj"][0], res["smj"][1], res["q6_mask"], res["q6_sel"]]
+    for r in (res["q1"], res["q6"]):
+        flat += list(r["keys"]) + list(r["results"])
+    for i, t in enumerate(flat):
+        buf = pinned_out.get(i)
+        if buf is None or buf.numel() < t.numel() or buf.dtype != t.dtype:
+            buf = torch.empty(max(t.numel(), 1) * 2, dtype=t.dtype, pin_memory=True)
+            pinned_out[i] = buf
+        buf.view(-1)[:t.numel()].copy_(t.reshape(-1), non_blocking=True)
+        nbytes += t.numel() * t.element_size()
+    return nbytes
+
+
+def run_gpu(args):
+    import paper_2203_01877_b200 as T
+    rank, world, local = env_rank()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    orders, li = make_data(rank, world, dev, args.layout)
+    hp = HotPath(T, orders, li, world)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        hp.step()
+    torch.cuda.synchronize()
+    hp._ev, hp.op_ms = [], {}
+
+    # ---------------- device-timed region: inputs resident in HBM
+    clk = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clk.start()
+    hp.ctx.reset_counters()
+    hp.ctx.set_profiling(True)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        hp.step()
+    t1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clocks = clk.stop()
+    ms_local = t0.elapsed_time(t1)
+    kstats = hp.ctx.kernel_stats()
+    hp.ctx.set_profiling(False)
+    launches = hp.ctx.launch_count()
+    hp.collect_ops()
+    op_ms = {k: v / args.steps for k, v in hp.op_ms.items()}
+
+    # ---------------- end to end: pinned host inputs -> device -> step -> pinned host results
+    host_cols = {"o_orderkey": orders["o_orderkey"]}
+    for name in set(Q1_COLS) | set(Q6_COLS) | {"l_orderkey"}:
+        host_cols[name] = li[name]
+    host = {k: v.cpu().pin_memory() for k, v in host_cols.items()}
+    del orders, li
+    h2d = sum(v.numel() * v.element_size() for v in host.values())
+    pinned_out = {}
+    e2e_steps = max(1, min(args.steps, 5))
+    d2h = 0
+
+    def e2e_step():
+        dv = {k: v.to(dev, non_blocking=True) for k, v in host.items()}
+        res = hp.step(dv["o_orderkey"], dv["l_orderkey"], [dv[c] for c in Q1_COLS], [dv[c] for c in Q6_COLS])
+        return result_to_host(res, pinned_out)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    hp._ev = []
+    barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(e2e_steps):
+        d2h = e2e_step()
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    hp._ev = []
+    e2e_ms_local = e0.elapsed_time(e1) / e2e_steps
+
+    # ---------------- max over ranks
+    vals = torch.tensor([ms_local, e2e_ms_local, float(launches)], dtype=torch.float64, device=dev)
+    if dist:
+        mx = vals.clone()
+        dist.all_reduce(mx[:2], op=dist.ReduceOp.MAX)
+        sm = vals.clone()
+        dist.all_reduce(sm[2:], op=dist.ReduceOp.SUM)
+        ms_total, e2e_ms, launches_all = float(mx[0]), float(mx[1]), int(sm[2])
+    else:
+        ms_total, e2e_ms, launches_all = ms_local, e2e_ms_local, launches
+    ms_step = ms_total / args.steps
+    rows_total = hp.n * world      # identical partition sizes are not guaranteed: use the sum
+    if dist:
+        t = torch.tensor([float(hp.n)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        rows_total = float(t)
+    value = rows_total / (ms_step / 1e3)
+
+    if rank == 0:
+        peak, peak_src = peaks()
+        dom = max(kstats.items(), key=lambda kv: kv[1][0])
+        name, (kms, klaunch, kbytes) = dom
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            traffic = json.load(open(tp)).get(name)
+        achieved = (kbytes / klaunch) / (kms / klaunch / 1e3) / 1e9 if kms > 0 else 0.0
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "rows/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "int64",
+            "data": "synthetic (in-repo TPC-H-shaped generator, seed 42; dbgen unavailable offline)",
+            "config": {
+                "workload": "tpch_sf10_hot_path: pkfk_join + smj_join(orders x lineitem) + Q1 groupby + Q6 filter/sum",
+                "sf_per_rank": SF_PER_RANK,
+                "lineitem_rows_per_rank": hp.n,
+                "orders_rows_per_rank": hp.ok.numel(),
+                "layout": f"{args.layout}; ranks co-partitioned (lineitem range-partitioned with its orders)",
+                "parallelism": f"dp{world}",
+                "l2": "inputs larger than L2: 2.8 GB of columns per rank per step vs 126 MB L2 (no flush needed)",
+            },
+            "clocks": clocks,
+            "e2e": {"value": rows_total / (e2e_ms / 1e3), "unit": "rows/s", "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world,
+                    "how": "pinned host columns -> H2D -> same step via the public API -> D2H of every result"},
+            "gpu_launches": launches_all,
+            "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": kbytes / max(klaunch, 1),
+                         "avg_launch_ms": kms / max(klaunch, 1), "launches": klaunch,
+                         "share_of_step": kms / ms_total if ms_total else None},
+            "operators_ms": op_ms,
+            "probe_rows_per_s": hp.n / (op_ms.get("pkfk_join", float("nan")) / 1e3),
+            "groupby_rows_per_s": hp.n / (op_ms.get("q1_groupby", float("nan")) / 1e3),
+            "kernels": {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                            "algorithmic_GBps": (v[2] / v[0] / 1e6) if v[0] > 0 else None}
+                        for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+        }
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(hp, args)
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ CPU oracle leg
+
+def oracle_sample(orders, li, sf_sample):
+    """A bounded sample of the same workload: the first orders rows and their lineitems."""
+    n_s = orders_count(sf_sample)
+    m = li["l_parent"] < n_s
+    ok = orders["o_orderkey"][:n_s].cpu().numpy()
+    lcols = {k: v[m].cpu().numpy().astype(np.int64) for k, v in li.items()
+             if k in set(Q1_COLS) | set(Q6_COLS) | {"l_orderkey"}}
+    return ok, lcols
+
+
+def oracle_step(ok, lc):
+    import oracle
+    oracle.pkfk_join(ok, lc["l_orderkey"])
+    oracle.smj_join(ok, lc["l_orderkey"])
+    oracle.groupby_agg([lc[c] for c in Q1_COLS], Q1_KEYS, Q1_AGGS, Q1_PREDS)
+    oracle.filter_compact([lc[c] for c in Q6_COLS], Q6_PREDS)
+    oracle.groupby_agg([lc[c] for c in Q6_COLS], [], Q6_AGGS, Q6_PREDS)
+
+
+def cpu_baseline(hp, args):
+    """The oracle as it stands (single-threaded C), rank 0 only, bounded sample."""
+    sfs = args.cpu_sample_sf
+    orders = {"o_orderkey": hp.ok}
+    li = {"l_orderkey": hp.lk, **{c: t for c, t in zip(Q1_COLS, hp.q1)}, **{c: t for c, t in zip(Q6_COLS, hp.q6)}}
+    # l_parent is needed for the sample mask: rebuild it from the generator (bookkeeping, not method)
+    _, li_full = tpch_orders_lineitem(sfs, seed=42, device="cpu", layout="shuffled")
+    orders_s, _ = tpch_orders_lineitem(sfs, seed=42, device="cpu", layout="shuffled")
+    ok = orders_s["o_orderkey"].numpy()
+    lc = {k: v.numpy().astype(np.int64) for k, v in li_full.items()
+          if k in set(Q1_COLS) | set(Q6_COLS) | {"l_orderkey"}}
+    del orders, li
+    t0 = time.perf_counter()
+    oracle_step(ok, lc)
+    one = time.perf_counter() - t0
+    reps = max(1, min(int(20.0 // max(one, 1e-3)), 5))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle_step(ok, lc)
+    dt = (time.perf_counter() - t0) / reps
+    n = lc["l_orderkey"].size
+    return {"value": n / dt, "unit": "rows/s", "cores": 1, "kind": "oracle",
+            "sample": f"TPC-H-shaped SF{sfs} ({n} lineitem rows, same generator/queries), "
+                      f"{reps} timed oracle steps after 1 untimed, host cores available: {os.cpu_count()}",
+            "ms_per_step": dt * 1e3}
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    sfs = args.cpu_sample_sf
+    orders, li = tpch_orders_lineitem(sfs, seed=42, device="cpu", layout="shuffled")
+    ok = orders["o_orderkey"].numpy()
+    lc = {k: v.numpy().astype(np.int64) for k, v in li.items() if k in set(Q1_COLS) | set(Q6_COLS) | {"l_orderkey"}}
+    for _ in range(args.warmup):
+        oracle_step(ok, lc)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_step(ok, lc)
+    dt = (time.perf_counter() - t0) / args.steps
+    n = lc["l_orderkey"].size
+    v = n / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "rows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (in-repo TPC-H-shaped generator, seed 42)",
+        "config": {"workload": "tpch_sf10_hot_path: pkfk_join + smj_join(orders x lineitem) + Q1 groupby + "
+                               "Q6 filter/sum", "sf_per_rank": SF_PER_RANK, "parallelism": "host oracle"},
+        "cpu_baseline": {"value": v, "unit": "rows/s", "cores": 1, "kind": "oracle",
+                         "sample": f"TPC-H-shaped SF{sfs} ({n} lineitem rows) per step; single-threaded C oracle"},
+        "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tqp", choices=["tqp", "reference"])
+    ap.add_argument("--layout", default="shuffled", choices=["shuffled", "clustered"])
+    ap.add_argument("--cpu-sample-sf", type=float, default=0.25)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "tqp":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    run_gpu(args)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,209 @@
+/*
+ * tqp.h -- C ABI of libtqp: the data-parallel hot path of TQP
+ * ("Query Processing on Tensor Computation Runtimes", He et al., PVLDB 2022,
+ * arXiv 2203.01877; PAPER.md = the paper's LaTeX source) on NVIDIA B200 (sm_100a).
+ *
+ * The paper states each operator as forward(self, x) over "input columns passed
+ * as an array of tensors" returning "an array of tensors representing the join
+ * output". Here the arguments are key / payload
+ * columns and the results are index pairs and aggregate columns.
+ *
+ * Conventions (apply to every entry point)
+ *  - Pointers are CUDA DEVICE pointers (HBM) unless the parameter name ends in
+ *    `_host`. Lengths are int64_t. Index outputs are int64 row numbers into the
+ *    caller's input columns.
+ *  - Ownership: inputs are borrowed and never modified. Outputs are
+ *    caller-allocated (the bound is stated per function). Temporaries come from a
+ *    stream-ordered memory pool owned by the context.
+ *  - Ordering: all work is enqueued on the context's stream. A `*_host` output
+ *    costs one stream synchronisation; functions that need a data-dependent size
+ *    (sort pass plan, join sizes, group count) synchronise internally and say so.
+ *  - Errors: a status code; the message is available from tqp_last_error().
+ *    No C++ exception crosses the ABI. Outputs are unspecified on error. After
+ *    TQP_ERR_CUDA the context should be destroyed.
+ *  - Determinism: identical inputs give bit-identical outputs (every scan and
+ *    compaction is order-preserving; integer sums are associative).
+ *  - Threading: one context per host thread / stream.
+ */
+#ifndef TQP_H_
+#define TQP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TQP_ABI_VERSION 1
+
+typedef enum {
+    TQP_OK = 0,
+    TQP_ERR_INVALID_ARGUMENT = 1,
+    TQP_ERR_DUPLICATE_BUILD_KEY = 2,   /* PK-FK build side has a repeated key (reading R10) */
+    TQP_ERR_OUT_OF_MEMORY = 3,
+    TQP_ERR_CUDA = 4,
+    TQP_ERR_OVERFLOW = 5,              /* int64 aggregate value / join size >= 2^62 */
+    TQP_ERR_CAPACITY = 6               /* output buffer too small; required size reported */
+} tqp_status;
+
+/* Column element types ("§4.1 Data Representation": numeric
+ * n x 1 tensors; 1-character strings as uint8 (reading R19); dates as int32 days
+ * or int64 microseconds (reading R18)). Comparisons: u8 unsigned, ints signed. */
+typedef enum { TQP_U8 = 1, TQP_I32 = 2, TQP_I64 = 3 } tqp_dtype;
+
+/* A column: `data` points to n elements of `dtype`, contiguous. */
+typedef struct {
+    const void* data;
+    int32_t dtype;      /* tqp_dtype */
+    int32_t reserved;   /* must be 0 */
+} tqp_col;
+
+typedef struct tqp_ctx tqp_ctx;
+
+/* Create a context on CUDA device `device` issuing work on `stream`
+ * (a cudaStream_t; NULL = legacy default stream). */
+tqp_status tqp_ctx_create(int device, void* stream, tqp_ctx** out);
+void tqp_ctx_destroy(tqp_ctx* ctx);
+tqp_status tqp_ctx_set_stream(tqp_ctx* ctx, void* stream);
+const char* tqp_last_error(const tqp_ctx* ctx);
+int tqp_abi_version(void);
+
+/* Instrumentation. Every kernel launch is counted; with profiling enabled each
+ * launch is bracketed by CUDA events on the context stream and the device time
+ * is accumulated per kernel name. Each kernel's ALGORITHMIC bytes (the
+ * compulsory HBM traffic of the work it did) are
+ * accounted on the host per launch. tqp_ctx_kernel_stats synchronises the
+ * stream; per kernel k: ms_host[k] (profiled device time), launches_host[k]
+ * (profiled launches), bytes_host[k] (algorithmic bytes, all launches).
+ * names_host: '\n'-separated kernel names written into a caller buffer. */
+int64_t tqp_ctx_launch_count(const tqp_ctx* ctx);
+void tqp_ctx_reset_counters(tqp_ctx* ctx);
+tqp_status tqp_ctx_set_profiling(tqp_ctx* ctx, int enable);
+tqp_status tqp_ctx_kernel_stats(tqp_ctx* ctx, char* names_host, size_t names_cap, double* ms_host,
+                                int64_t* launches_host, double* bytes_host, int max_kernels, int* n_kernels_host);
+
+/* ------------------------------------------------------------------ sort */
+/* (1) Stable sort with permutation -- Alg. 1 l.2-3, Alg. 2
+ * l.3 "radix sort" (prose :1148); reading R1 (stable).
+ * keys: n elements (I32 or I64; U8 also accepted).
+ * perm_out[i] = input row of the i-th element of the stable (key, row) order
+ * (n x int64, caller-allocated). descending != 0 orders keys descending with
+ * ties still in ascending row order (descending is NOT the reverse).
+ * sorted_keys_out: nullable; if given, n elements of the input dtype = keys[perm].
+ * Implementation: onesweep LSD radix sort; digits that are constant across all
+ * keys are skipped. Synchronises once (pass plan). Requires n < 2^31. */
+tqp_status tqp_sort(tqp_ctx* ctx, tqp_col keys, int64_t n, int descending,
+                    void* sorted_keys_out, int64_t* perm_out);
+
+/* ------------------------------------------------------------ PK-FK join */
+/* (2) Primary-key / foreign-key join -- PAPER.md:55-100 ("Find matches using
+ * binary search"). build = unique-key side (the paper's `left`), probe = FK side
+ * (`right`). Output: one pair per matching probe row, in ascending probe-row
+ * order (reading R7): left_out_idx[j] = build row, right_out_idx[j] = probe row.
+ * Buffers: capacity n_probe each (caller-allocated). *n_out_host = pairs.
+ * The build side is radix-sorted; each probe key is located by a radix bracket
+ * table plus a branch-free lower_bound (reading R8: the answer equals
+ * lower_bound on the unpadded sorted build keys), matched by equality and
+ * compacted order-preservingly. Duplicate build keys -> TQP_ERR_DUPLICATE_BUILD_KEY.
+ * Key dtypes may differ (compared as int64). Synchronises twice. */
+tqp_status tqp_pkfk_join(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
+                         int64_t* left_out_idx, int64_t* right_out_idx, int64_t* n_out_host);
+
+/* Left-semi / left-anti variant ("left-semi, and left-anti
+ * joins"): match_out (nullable, n_probe x u8) = 1 iff the probe row has a build
+ * match; sel_out (nullable, capacity n_probe x int64) = ascending probe rows
+ * with a match (anti != 0: without a match); *n_sel_host = their count. */
+tqp_status tqp_pkfk_semi(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
+                         int anti, uint8_t* match_out, int64_t* sel_out, int64_t* n_sel_host);
+
+/* ------------------------------------------------ m:n sort-merge join */
+/* (3) Generic sort-merge join -- Alg. 1 (prose :1114-1137)
+ * with readings R2 (ascending sort), R3 (bucketize right=True),
+ * R4 (div and remainder by rightHist), R5 (histograms over the
+ * keys present on both sides). Output order: key ascending, then left row
+ * ascending, then right row ascending (reading R6).
+ * prepare: sorts both sides, run-length encodes them (the "bincount"), forms
+ * histMul = L*R and cumHistMul over the common keys; *out_size_host = outSize
+ * (synchronises; TQP_ERR_OVERFLOW if >= 2^62). The plan lives on the device.
+ * expand: writes pairs for output offsets [begin, end) into left_out_idx /
+ * right_out_idx ((end - begin) elements each); asynchronous, may be called on
+ * any windows of [0, outSize). */
+typedef struct tqp_smj_plan tqp_smj_plan;
+tqp_status tqp_smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t n_left, tqp_col right, int64_t n_right,
+                           tqp_smj_plan** plan, int64_t* out_size_host);
+tqp_status tqp_smj_expand(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin, int64_t end,
+                          int64_t* left_out_idx, int64_t* right_out_idx);
+void tqp_smj_release(tqp_ctx* ctx, tqp_smj_plan* plan);
+/* prepare + expand of everything into caller buffers of `capacity` pairs.
+ * If capacity < outSize: TQP_ERR_CAPACITY and *n_out_host = outSize. */
+tqp_status tqp_smj_join(tqp_ctx* ctx, tqp_col left, int64_t n_left, tqp_col right, int64_t n_right,
+                        int64_t* left_out_idx, int64_t* right_out_idx, int64_t capacity, int64_t* n_out_host);
+
+/* ---------------------------------------------------- filter/compaction */
+/* (4) Filter -- Listing 1 (bitmap) and Listing 2 (selection
+ * vector, reading R20). A row passes iff every predicate
+ * `cols[col] <op> value` holds (conjunction, "intersecting the
+ * masks using logical_and"). mask_out (nullable): n x u8 in {0,1}; sel_out
+ * (nullable): ascending passing rows (capacity n x int64); at least one given.
+ * n_sel_host (nullable): number of passing rows (synchronises if given). */
+typedef enum { TQP_LT = 0, TQP_LE = 1, TQP_GT = 2, TQP_GE = 3, TQP_EQ = 4, TQP_NE = 5 } tqp_cmp;
+typedef struct {
+    int32_t col;     /* index into cols */
+    int32_t op;      /* tqp_cmp */
+    int64_t value;   /* compared as int64 with the column value */
+} tqp_pred;
+#define TQP_MAX_PREDS 16
+tqp_status tqp_filter_compact(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols, int64_t n,
+                              const tqp_pred* preds_host, int n_preds,
+                              uint8_t* mask_out, int64_t* sel_out, int64_t* n_sel_host);
+
+/* -------------------------------------------------------------- group-by */
+/* (5) Sort-based group-by aggregation -- Alg. 2 (prose
+ * :1146-1152) with an optional fused pre-filter (same predicate form as (4)).
+ * Group keys: up to 8 columns, concatenated column 0 most significant
+ * (reading R12) into at most 64 bits (u8: 8, i32: 32, i64: 64 bits).
+ * Aggregate value per row = prod_{f < n_factors} (add[f] + sign[f] * cols[col[f]])
+ * in int64 fixed point (reading R16; the expression form of PAPER.md:1103-1110
+ * "sum(l_extendedprice * (1 - l_discount))"); overflow -> TQP_ERR_OVERFLOW.
+ * Results: SUM -> int128 (16 bytes, little-endian two's complement, exact);
+ * COUNT -> int64 rows of the group (COUNT(*), n_factors ignored);
+ * MIN / MAX -> int64; AVG -> double = rn((double)sum / (double)count) (R15/R17).
+ * Groups come out in ascending key order. n_keys == 0 -> exactly one group even
+ * if no row passes (SUM 0, COUNT 0, MIN INT64_MAX, MAX INT64_MIN, AVG NaN).
+ * Method: each tile of rows is radix-sorted by key in shared memory and reduced
+ * per run (segment boundaries + segmented sums); the per-tile partials are
+ * radix-sorted globally and reduced again (two-level sort-based aggregation).
+ * prepare synchronises and reports *n_groups_host = G; fetch writes:
+ *   keys_out[k]   : G elements of key column k's dtype (nullable each)
+ *   results_out[a]: G elements of the aggregate's result type (nullable each). */
+typedef enum { TQP_SUM = 0, TQP_COUNT = 1, TQP_MIN = 2, TQP_MAX = 3, TQP_AVG = 4 } tqp_aggop;
+typedef struct {
+    int32_t op;          /* tqp_aggop */
+    int32_t n_factors;   /* 0..3 */
+    int32_t col[3];
+    int32_t sign[3];     /* +1 or -1 */
+    int64_t add[3];
+} tqp_agg;
+#define TQP_MAX_KEYS 8
+#define TQP_MAX_AGGS 16
+typedef struct tqp_groupby_plan tqp_groupby_plan;
+tqp_status tqp_groupby_prepare(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols, int64_t n,
+                               const int32_t* key_idx_host, int n_keys,
+                               const tqp_pred* preds_host, int n_preds,
+                               const tqp_agg* aggs_host, int n_aggs,
+                               tqp_groupby_plan** plan, int64_t* n_groups_host);
+tqp_status tqp_groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* plan, void* const* keys_out_host,
+                             void* const* results_out_host);
+void tqp_groupby_release(tqp_ctx* ctx, tqp_groupby_plan* plan);
+/* prepare + fetch into caller buffers of `capacity` groups; if capacity < G:
+ * TQP_ERR_CAPACITY and *n_groups_host = G. */
+tqp_status tqp_groupby_agg(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols, int64_t n,
+                           const int32_t* key_idx_host, int n_keys, const tqp_pred* preds_host, int n_preds,
+                           const tqp_agg* aggs_host, int n_aggs, void* const* keys_out_host,
+                           void* const* results_out_host, int64_t capacity, int64_t* n_groups_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQP_H_ */

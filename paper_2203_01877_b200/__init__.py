@@ -1,0 +1,385 @@
+"""paper_2203_01877_b200 -- B200-native hot path of TQP (arXiv 2203.01877).
+
+Thin Python binding over libtqp.so (C ABI in include/tqp.h). This module only
+marshals arguments: torch tensors in (device memory, streams), raw pointers and
+sizes across the ABI, torch tensors out. Every step of the hot path runs in the
+library's CUDA kernels; there is no CPU fallback. Importing the package without
+a built libtqp.so raises ImportError.
+
+Operators (same names as the C ABI, PAPER.md citations in include/tqp.h):
+  sort, pkfk_join, pkfk_semi, smj_prepare / SmjPlan.expand, smj_join,
+  filter_compact, groupby_agg
+"""
+
+import ctypes
+import os
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libtqp.so")
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(f"libtqp.so not built ({_LIB_PATH}); run `python -m paper_2203_01877_b200.build` "
+                      "or __graft_entry__.build()")
+
+_lib = ctypes.CDLL(_LIB_PATH)
+
+TQP_OK, TQP_ERR_INVALID_ARGUMENT, TQP_ERR_DUPLICATE_BUILD_KEY, TQP_ERR_OUT_OF_MEMORY, TQP_ERR_CUDA, \
+    TQP_ERR_OVERFLOW, TQP_ERR_CAPACITY = range(7)
+TQP_U8, TQP_I32, TQP_I64 = 1, 2, 3
+OPS = {"lt": 0, "le": 1, "gt": 2, "ge": 3, "eq": 4, "ne": 5, "<": 0, "<=": 1, ">": 2, ">=": 3, "==": 4, "!=": 5}
+AGGS = {"sum": 0, "count": 1, "min": 2, "max": 3, "avg": 4}
+MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
+
+EXPORTED = [
+    "tqp_abi_version", "tqp_ctx_create", "tqp_ctx_destroy", "tqp_ctx_set_stream", "tqp_last_error",
+    "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_kernel_stats",
+    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
+    "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
+    "tqp_groupby_agg",
+]
+
+
+class Col(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class Pred(ctypes.Structure):
+    _fields_ = [("col", ctypes.c_int32), ("op", ctypes.c_int32), ("value", ctypes.c_int64)]
+
+
+class Agg(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int32), ("n_factors", ctypes.c_int32), ("col", ctypes.c_int32 * 3),
+                ("sign", ctypes.c_int32 * 3), ("add", ctypes.c_int64 * 3)]
+
+
+_vp, _i64, _int = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+_P = ctypes.POINTER
+_sig = {
+    "tqp_abi_version": ([], _int),
+    "tqp_ctx_create": ([_int, _vp, _P(_vp)], _int),
+    "tqp_ctx_destroy": ([_vp], None),
+    "tqp_ctx_set_stream": ([_vp, _vp], _int),
+    "tqp_last_error": ([_vp], ctypes.c_char_p),
+    "tqp_ctx_launch_count": ([_vp], _i64),
+    "tqp_ctx_reset_counters": ([_vp], None),
+    "tqp_ctx_set_profiling": ([_vp, _int], _int),
+    "tqp_ctx_kernel_stats": ([_vp, ctypes.c_char_p, ctypes.c_size_t, _P(ctypes.c_double), _P(_i64),
+                              _P(ctypes.c_double), _int, _P(_int)], _int),
+    "tqp_sort": ([_vp, Col, _i64, _int, _vp, _vp], _int),
+    "tqp_pkfk_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
+    "tqp_pkfk_semi": ([_vp, Col, _i64, Col, _i64, _int, _vp, _vp, _P(_i64)], _int),
+    "tqp_smj_prepare": ([_vp, Col, _i64, Col, _i64, _P(_vp), _P(_i64)], _int),
+    "tqp_smj_expand": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
+    "tqp_smj_release": ([_vp, _vp], None),
+    "tqp_smj_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _i64, _P(_i64)], _int),
+    "tqp_filter_compact": ([_vp, _P(Col), _int, _i64, _P(Pred), _int, _vp, _vp, _P(_i64)], _int),
+    "tqp_groupby_prepare": ([_vp, _P(Col), _int, _i64, _P(ctypes.c_int32), _int, _P(Pred), _int, _P(Agg), _int,
+                             _P(_vp), _P(_i64)], _int),
+    "tqp_groupby_fetch": ([_vp, _vp, _P(_vp), _P(_vp)], _int),
+    "tqp_groupby_release": ([_vp, _vp], None),
+    "tqp_groupby_agg": ([_vp, _P(Col), _int, _i64, _P(ctypes.c_int32), _int, _P(Pred), _int, _P(Agg), _int,
+                         _P(_vp), _P(_vp), _i64, _P(_i64)], _int),
+}
+for _name, (_args, _res) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+class TqpError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"libtqp status {status}: {msg}")
+        self.status = status
+
+
+def lib_path():
+    return _LIB_PATH
+
+
+def abi_version():
+    return _lib.tqp_abi_version()
+
+
+_DT = {torch.uint8: TQP_U8, torch.bool: TQP_U8, torch.int32: TQP_I32, torch.int64: TQP_I64}
+
+
+def _dev_tensor(t, device):
+    """Marshal an input column: CUDA tensors pass through; host tensors are staged to the device."""
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(t)
+    if t.dtype not in _DT:
+        raise TypeError(f"unsupported column dtype {t.dtype}")
+    if t.dim() != 1:
+        t = t.reshape(-1)
+    if t.device.type != "cuda":
+        src = t if t.is_pinned() else t.contiguous()
+        t = src.to(device, non_blocking=src.is_pinned())
+    elif t.device != device:
+        t = t.to(device)
+    return t.contiguous()
+
+
+def _col(t):
+    return Col(t.data_ptr() if t.numel() else 0, _DT[t.dtype], 0)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else None)
+
+
+class Context:
+    """A libtqp context bound to one CUDA device; work goes on torch's current stream."""
+
+    def __init__(self, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libtqp needs a CUDA device (B200); no CPU fallback exists")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   torch.device(device).index or 0)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            s = torch.cuda.current_stream(self.device).cuda_stream
+            self._check(_lib.tqp_ctx_create(self.device.index, ctypes.c_void_p(s), ctypes.byref(h)), None)
+        self._h = h
+        self._stream = s
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.tqp_ctx_destroy(h)
+            self._h = None
+
+    # ------------------------------------------------------------ plumbing
+    def _check(self, st, h=-1):
+        if st != TQP_OK:
+            hh = self._h if h == -1 else h
+            msg = _lib.tqp_last_error(hh).decode() if hh else "context creation failed"
+            raise TqpError(st, msg)
+
+    def _sync_stream(self):
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if s != self._stream:
+            self._check(_lib.tqp_ctx_set_stream(self._h, ctypes.c_void_p(s)))
+            self._stream = s
+
+    def launch_count(self):
+        return _lib.tqp_ctx_launch_count(self._h)
+
+    def reset_counters(self):
+        _lib.tqp_ctx_reset_counters(self._h)
+
+    def set_profiling(self, on=True):
+        self._check(_lib.tqp_ctx_set_profiling(self._h, int(bool(on))))
+
+    def kernel_stats(self):
+        """{kernel name: (profiled device ms, profiled launches, algorithmic bytes)} since the
+        last reset (synchronises)."""
+        cap = 64
+        names = ctypes.create_string_buffer(8192)
+        ms = (ctypes.c_double * cap)()
+        ln = (ctypes.c_int64 * cap)()
+        by = (ctypes.c_double * cap)()
+        k = ctypes.c_int(0)
+        self._check(_lib.tqp_ctx_kernel_stats(self._h, names, 8192, ms, ln, by, cap, ctypes.byref(k)))
+        nm = names.value.decode().split("\n")
+        return {nm[i]: (ms[i], ln[i], by[i]) for i in range(k.value)}
+
+    # ----------------------------------------------------------- operators
+    def sort(self, keys, descending=False, return_keys=True):
+        """Stable sort -> (sorted_keys | None, perm int64). PAPER.md:296-297, :352."""
+        self._sync_stream()
+        k = _dev_tensor(keys, self.device)
+        n = k.numel()
+        perm = torch.empty(n, dtype=torch.int64, device=self.device)
+        out = torch.empty_like(k) if return_keys else None
+        self._check(_lib.tqp_sort(self._h, _col(k), n, int(bool(descending)), _ptr(out), _ptr(perm)))
+        return out, perm
+
+    def pkfk_join(self, build_keys, probe_keys):
+        """PK-FK join -> (left_idx, right_idx) int64, ascending probe row. PAPER.md:55-100."""
+        self._sync_stream()
+        b = _dev_tensor(build_keys, self.device)
+        p = _dev_tensor(probe_keys, self.device)
+        lo = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        ro = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_pkfk_join(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(lo), _ptr(ro),
+                                       ctypes.byref(m)))
+        return lo[:m.value], ro[:m.value]
+
+    def pkfk_semi(self, build_keys, probe_keys, anti=False, return_mask=False):
+        """Left-semi (anti=False) / left-anti selection of probe rows."""
+        self._sync_stream()
+        b = _dev_tensor(build_keys, self.device)
+        p = _dev_tensor(probe_keys, self.device)
+        sel = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        mask = torch.empty(p.numel(), dtype=torch.uint8, device=self.device) if return_mask else None
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_pkfk_semi(self._h, _col(b), b.numel(), _col(p), p.numel(), int(bool(anti)),
+                                       _ptr(mask), _ptr(sel), ctypes.byref(m)))
+        return (sel[:m.value], mask) if return_mask else sel[:m.value]
+
+    def smj_prepare(self, left, right):
+        """Alg. 1 lines 1-9: sort, histograms, products, prefix sums -> SmjPlan (size known)."""
+        self._sync_stream()
+        l = _dev_tensor(left, self.device)
+        r = _dev_tensor(right, self.device)
+        plan = ctypes.c_void_p()
+        size = ctypes.c_int64(0)
+        self._check(_lib.tqp_smj_prepare(self._h, _col(l), l.numel(), _col(r), r.numel(), ctypes.byref(plan),
+                                         ctypes.byref(size)))
+        return SmjPlan(self, plan, size.value)
+
+    def smj_join(self, left, right):
+        """Generic m:n sort-merge join -> (left_idx, right_idx) in (key, l, r) order. PAPER.md:286-338."""
+        plan = self.smj_prepare(left, right)
+        try:
+            return plan.expand(0, plan.size)
+        finally:
+            plan.release()
+
+    def filter_compact(self, cols, preds, mask=True, sel=True):
+        """Listing 1 bitmap and/or Listing 2 selection vector -> (mask u8 | None, sel int64 | None)."""
+        self._sync_stream()
+        cs = [_dev_tensor(c, self.device) for c in cols]
+        n = cs[0].numel() if cs else 0
+        ca = (Col * max(len(cs), 1))(*[_col(c) for c in cs])
+        pa = _preds(preds)
+        mk = torch.empty(n, dtype=torch.uint8, device=self.device) if mask else None
+        sv = torch.empty(n, dtype=torch.int64, device=self.device) if sel else None
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_filter_compact(self._h, ca, len(cs), n, pa, len(preds), _ptr(mk), _ptr(sv),
+                                            ctypes.byref(m)))
+        return mk, (sv[:m.value] if sv is not None else None)
+
+    def groupby_agg(self, cols, key_idx, aggs, preds=()):
+        """Sort-based group-by (Alg. 2) with fused pre-filter.
+
+        aggs: [(op, [(col, add, sign), ...])]. Returns dict(n_groups, keys=[tensor per key col],
+        results=[SUM: int64 (G,2) = (lo, hi) of the int128 | COUNT/MIN/MAX: int64 | AVG: float64])."""
+        self._sync_stream()
+        cs = [_dev_tensor(c, self.device) for c in cols]
+        n = cs[0].numel() if cs else 0
+        ca = (Col * max(len(cs), 1))(*[_col(c) for c in cs])
+        ki = (ctypes.c_int32 * max(len(key_idx), 1))(*key_idx)
+        pa = _preds(preds)
+        aa = _aggs(aggs)
+        plan = ctypes.c_void_p()
+        G = ctypes.c_int64(0)
+        self._check(_lib.tqp_groupby_prepare(self._h, ca, len(cs), n, ki, len(key_idx), pa, len(preds), aa,
+                                             len(aggs), ctypes.byref(plan), ctypes.byref(G)))
+        try:
+            g = G.value
+            keys = [torch.empty(g, dtype=cs[k].dtype if cs[k].dtype != torch.bool else torch.uint8,
+                                device=self.device) for k in key_idx]
+            res = []
+            for op, _ in aggs:
+                o = AGGS[op] if isinstance(op, str) else int(op)
+                if o == 0:
+                    res.append(torch.empty((g, 2), dtype=torch.int64, device=self.device))
+                elif o == 4:
+                    res.append(torch.empty(g, dtype=torch.float64, device=self.device))
+                else:
+                    res.append(torch.empty(g, dtype=torch.int64, device=self.device))
+            kp = (ctypes.c_void_p * max(len(keys), 1))(*[t.data_ptr() if g else None for t in keys])
+            rp = (ctypes.c_void_p * max(len(res), 1))(*[t.data_ptr() if g else None for t in res])
+            self._check(_lib.tqp_groupby_fetch(self._h, plan, kp, rp))
+        finally:
+            _lib.tqp_groupby_release(self._h, plan)
+        return {"n_groups": g, "keys": keys, "results": res}
+
+
+class SmjPlan:
+    """Device-resident Alg. 1 state after line 9 (outSize known); expand() runs lines 10-14 on windows."""
+
+    def __init__(self, ctx, handle, size):
+        self.ctx, self._h, self.size = ctx, handle, size
+
+    def expand(self, begin, end, out=None):
+        self.ctx._sync_stream()
+        k = end - begin
+        if out is None:
+            lo = torch.empty(k, dtype=torch.int64, device=self.ctx.device)
+            ro = torch.empty(k, dtype=torch.int64, device=self.ctx.device)
+        else:
+            lo, ro = out
+        self.ctx._check(_lib.tqp_smj_expand(self.ctx._h, self._h, begin, end, _ptr(lo), _ptr(ro)))
+        return lo, ro
+
+    def release(self):
+        if self._h:
+            _lib.tqp_smj_release(self.ctx._h, self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def _preds(preds):
+    if len(preds) > MAX_PREDS:
+        raise ValueError("too many predicates")
+    arr = (Pred * max(len(preds), 1))()
+    for i, (c, op, v) in enumerate(preds):
+        arr[i].col, arr[i].op, arr[i].value = c, OPS[op] if isinstance(op, str) else int(op), int(v)
+    return arr
+
+
+def _aggs(aggs):
+    if len(aggs) > MAX_AGGS:
+        raise ValueError("too many aggregates")
+    arr = (Agg * max(len(aggs), 1))()
+    for i, (op, factors) in enumerate(aggs):
+        arr[i].op = AGGS[op] if isinstance(op, str) else int(op)
+        arr[i].n_factors = len(factors)
+        for f, (c, add, sign) in enumerate(factors):
+            arr[i].col[f], arr[i].add[f], arr[i].sign[f] = c, int(add), int(sign)
+    return arr
+
+
+def int128_to_ints(t):
+    """(G, 2) int64 [lo, hi] tensor -> list of exact Python ints."""
+    t = t.cpu()
+    return [(int(lo) & ((1 << 64) - 1)) + (int(hi) << 64) for lo, hi in t.tolist()]
+
+
+_default = {}
+
+
+def context(device=None):
+    """Process-wide default Context per device."""
+    d = torch.cuda.current_device() if device is None else torch.device(device).index or 0
+    if d not in _default:
+        _default[d] = Context(d)
+    return _default[d]
+
+
+def sort(keys, descending=False, return_keys=True):
+    return context().sort(keys, descending, return_keys)
+
+
+def pkfk_join(build_keys, probe_keys):
+    return context().pkfk_join(build_keys, probe_keys)
+
+
+def pkfk_semi(build_keys, probe_keys, anti=False, return_mask=False):
+    return context().pkfk_semi(build_keys, probe_keys, anti, return_mask)
+
+
+def smj_prepare(left, right):
+    return context().smj_prepare(left, right)
+
+
+def smj_join(left, right):
+    return context().smj_join(left, right)
+
+
+def filter_compact(cols, preds, mask=True, sel=True):
+    return context().filter_compact(cols, preds, mask, sel)
+
+
+def groupby_agg(cols, key_idx, aggs, preds=()):
+    return context().groupby_agg(cols, key_idx, aggs, preds)

@@ -1,0 +1,265 @@
+// api.cu -- the extern "C" boundary of libtqp (declared in include/tqp.h).
+// Every entry point converts internal exceptions into a tqp_status and a
+// message; nothing C++ crosses the ABI.
+#include <cstring>
+
+#include "internal.h"
+
+namespace tqp {
+void pkfk_join(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
+void pkfk_semi(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int, uint8_t*, int64_t*, int64_t*);
+void filter_compact(tqp_ctx*, const tqp_col*, int, int64_t, const tqp_pred*, int, uint8_t*, int64_t*, int64_t*);
+tqp_smj_plan* smj_prepare(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*);
+void smj_expand(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, int64_t*, int64_t*);
+void smj_release(tqp_ctx*, tqp_smj_plan*);
+tqp_groupby_plan* groupby_prepare(tqp_ctx*, const tqp_col*, int, int64_t, const int32_t*, int, const tqp_pred*, int,
+                                  const tqp_agg*, int, int64_t*);
+void groupby_fetch(tqp_ctx*, const tqp_groupby_plan*, void* const*, void* const*);
+void groupby_release(tqp_ctx*, tqp_groupby_plan*);
+}  // namespace tqp
+
+static_assert(sizeof(tqp_col) == 16, "tqp_col layout");
+static_assert(sizeof(tqp_pred) == 16, "tqp_pred layout");
+static_assert(sizeof(tqp_agg) == 56, "tqp_agg layout");
+
+void tqp_ctx::drain_profile() {
+    if (pending.empty()) return;
+    TQP_CUDA(cudaStreamSynchronize(stream));
+    for (auto& p : pending) {
+        float ms = 0.f;
+        TQP_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        auto& st = stats[p.name];
+        st.ms += ms;
+        st.launches += 1;
+        free_events.push_back(p.a);
+        free_events.push_back(p.b);
+    }
+    pending.clear();
+}
+
+#define TQP_GUARD(ctx, body)                                                   \
+    do {                                                                       \
+        if (!(ctx)) return TQP_ERR_INVALID_ARGUMENT;                           \
+        try {                                                                  \
+            int cur_ = -1;                                                     \
+            cudaGetDevice(&cur_);                                              \
+            if (cur_ != (ctx)->device) cudaSetDevice((ctx)->device);           \
+            body;                                                              \
+            (ctx)->err.clear();                                                \
+            return TQP_OK;                                                     \
+        } catch (const ::tqp::Error& e) {                                      \
+            (ctx)->err = e.msg;                                                \
+            return e.status;                                                   \
+        } catch (const std::bad_alloc&) {                                      \
+            (ctx)->err = "host out of memory";                                 \
+            return TQP_ERR_OUT_OF_MEMORY;                                      \
+        } catch (...) {                                                        \
+            (ctx)->err = "unknown error";                                      \
+            return TQP_ERR_CUDA;                                               \
+        }                                                                      \
+    } while (0)
+
+extern "C" {
+
+int tqp_abi_version(void) { return TQP_ABI_VERSION; }
+
+tqp_status tqp_ctx_create(int device, void* stream, tqp_ctx** out) {
+    if (!out) return TQP_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    tqp_ctx* c = new (std::nothrow) tqp_ctx();
+    if (!c) return TQP_ERR_OUT_OF_MEMORY;
+    try {
+        c->device = device;
+        TQP_CUDA(cudaSetDevice(device));
+        TQP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+        c->stream = static_cast<cudaStream_t>(stream);
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        TQP_CUDA(cudaMemPoolCreate(&c->pool, &props));
+        uint64_t thr = ~0ull;   // keep freed blocks cached in the pool
+        TQP_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        TQP_CUDA(cudaMallocHost(&c->pinned, 4096));
+    } catch (const tqp::Error& e) {
+        if (c->pool) cudaMemPoolDestroy(c->pool);
+        delete c;
+        return e.status;
+    }
+    *out = c;
+    return TQP_OK;
+}
+
+void tqp_ctx_destroy(tqp_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    for (auto e : c->free_events) cudaEventDestroy(e);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->pool) cudaMemPoolDestroy(c->pool);
+    delete c;
+}
+
+tqp_status tqp_ctx_set_stream(tqp_ctx* c, void* stream) {
+    TQP_GUARD(c, { c->drain_profile(); c->stream = static_cast<cudaStream_t>(stream); });
+}
+
+const char* tqp_last_error(const tqp_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t tqp_ctx_launch_count(const tqp_ctx* c) { return c ? c->launches : 0; }
+
+void tqp_ctx_reset_counters(tqp_ctx* c) {
+    if (!c) return;
+    try { c->drain_profile(); } catch (...) {}
+    c->launches = 0;
+    c->stats.clear();
+}
+
+tqp_status tqp_ctx_set_profiling(tqp_ctx* c, int enable) {
+    TQP_GUARD(c, { c->drain_profile(); c->profiling = enable != 0; });
+}
+
+tqp_status tqp_ctx_kernel_stats(tqp_ctx* c, char* names, size_t names_cap, double* ms, int64_t* launches,
+                                double* bytes, int max_kernels, int* n_kernels) {
+    TQP_GUARD(c, {
+        c->drain_profile();
+        std::string all;
+        int k = 0;
+        for (auto& kv : c->stats) {
+            if (k < max_kernels) {
+                if (ms) ms[k] = kv.second.ms;
+                if (launches) launches[k] = kv.second.launches;
+                if (bytes) bytes[k] = kv.second.bytes;
+                all += kv.first;
+                all += '\n';
+            }
+            k++;
+        }
+        if (n_kernels) *n_kernels = k < max_kernels ? k : max_kernels;
+        if (names && names_cap) {
+            size_t m = all.size() < names_cap - 1 ? all.size() : names_cap - 1;
+            memcpy(names, all.data(), m);
+            names[m] = 0;
+        }
+    });
+}
+
+tqp_status tqp_sort(tqp_ctx* c, tqp_col keys, int64_t n, int descending, void* sorted_keys_out, int64_t* perm_out) {
+    TQP_GUARD(c, {
+        tqp::check_col(keys, n, "sort keys");
+        if (n > 0 && !perm_out) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "sort: null perm_out");
+        tqp::SortOut o;
+        o.sorted_orig = sorted_keys_out;
+        o.perm64 = perm_out;
+        tqp::radix_sort(c, keys.data, keys.dtype, n, descending != 0, o);
+    });
+}
+
+tqp_status tqp_pkfk_join(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int64_t* lo, int64_t* ro,
+                         int64_t* n_out_host) {
+    TQP_GUARD(c, {
+        if (!n_out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null n_out_host");
+        tqp::pkfk_join(c, b, nb, p, np, lo, ro, n_out_host);
+    });
+}
+
+tqp_status tqp_pkfk_semi(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int anti, uint8_t* match_out,
+                         int64_t* sel_out, int64_t* n_sel_host) {
+    TQP_GUARD(c, { tqp::pkfk_semi(c, b, nb, p, np, anti, match_out, sel_out, n_sel_host); });
+}
+
+tqp_status tqp_smj_prepare(tqp_ctx* c, tqp_col l, int64_t nl, tqp_col r, int64_t nr, tqp_smj_plan** plan,
+                           int64_t* out_size_host) {
+    TQP_GUARD(c, {
+        if (!plan || !out_size_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_prepare: null output");
+        *plan = tqp::smj_prepare(c, l, nl, r, nr, out_size_host);
+    });
+}
+
+tqp_status tqp_smj_expand(tqp_ctx* c, const tqp_smj_plan* plan, int64_t begin, int64_t end, int64_t* lo,
+                          int64_t* ro) {
+    TQP_GUARD(c, {
+        if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: null plan");
+        tqp::smj_expand(c, plan, begin, end, lo, ro);
+    });
+}
+
+void tqp_smj_release(tqp_ctx* c, tqp_smj_plan* plan) {
+    if (plan) tqp::smj_release(c, plan);
+}
+
+tqp_status tqp_smj_join(tqp_ctx* c, tqp_col l, int64_t nl, tqp_col r, int64_t nr, int64_t* lo, int64_t* ro,
+                        int64_t capacity, int64_t* n_out_host) {
+    TQP_GUARD(c, {
+        if (!n_out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_join: null n_out_host");
+        int64_t size = 0;
+        tqp_smj_plan* P = tqp::smj_prepare(c, l, nl, r, nr, &size);
+        *n_out_host = size;
+        if (size > capacity) {
+            tqp::smj_release(c, P);
+            tqp::fail(TQP_ERR_CAPACITY, "smj_join: capacity smaller than the join size");
+        }
+        try {
+            tqp::smj_expand(c, P, 0, size, lo, ro);
+        } catch (...) {
+            tqp::smj_release(c, P);
+            throw;
+        }
+        tqp::smj_release(c, P);
+    });
+}
+
+tqp_status tqp_filter_compact(tqp_ctx* c, const tqp_col* cols, int n_cols, int64_t n, const tqp_pred* preds,
+                              int n_preds, uint8_t* mask_out, int64_t* sel_out, int64_t* n_sel_host) {
+    TQP_GUARD(c, { tqp::filter_compact(c, cols, n_cols, n, preds, n_preds, mask_out, sel_out, n_sel_host); });
+}
+
+tqp_status tqp_groupby_prepare(tqp_ctx* c, const tqp_col* cols, int n_cols, int64_t n, const int32_t* key_idx,
+                               int n_keys, const tqp_pred* preds, int n_preds, const tqp_agg* aggs, int n_aggs,
+                               tqp_groupby_plan** plan, int64_t* n_groups_host) {
+    TQP_GUARD(c, {
+        if (!plan || !n_groups_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_prepare: null output");
+        if ((n_cols && !cols) || (n_keys && !key_idx) || (n_preds && !preds) || (n_aggs && !aggs))
+            tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_prepare: null array");
+        *plan = tqp::groupby_prepare(c, cols, n_cols, n, key_idx, n_keys, preds, n_preds, aggs, n_aggs, n_groups_host);
+    });
+}
+
+tqp_status tqp_groupby_fetch(tqp_ctx* c, const tqp_groupby_plan* plan, void* const* keys_out,
+                             void* const* results_out) {
+    TQP_GUARD(c, {
+        if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_fetch: null plan");
+        tqp::groupby_fetch(c, plan, keys_out, results_out);
+    });
+}
+
+void tqp_groupby_release(tqp_ctx* c, tqp_groupby_plan* plan) {
+    if (plan) tqp::groupby_release(c, plan);
+}
+
+tqp_status tqp_groupby_agg(tqp_ctx* c, const tqp_col* cols, int n_cols, int64_t n, const int32_t* key_idx,
+                           int n_keys, const tqp_pred* preds, int n_preds, const tqp_agg* aggs, int n_aggs,
+                           void* const* keys_out, void* const* results_out, int64_t capacity,
+                           int64_t* n_groups_host) {
+    TQP_GUARD(c, {
+        if (!n_groups_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_agg: null n_groups_host");
+        if ((n_cols && !cols) || (n_keys && !key_idx) || (n_preds && !preds) || (n_aggs && !aggs))
+            tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_agg: null array");
+        tqp_groupby_plan* P =
+            tqp::groupby_prepare(c, cols, n_cols, n, key_idx, n_keys, preds, n_preds, aggs, n_aggs, n_groups_host);
+        if (*n_groups_host > capacity) {
+            tqp::groupby_release(c, P);
+            tqp::fail(TQP_ERR_CAPACITY, "groupby_agg: capacity smaller than the group count");
+        }
+        try {
+            tqp::groupby_fetch(c, P, keys_out, results_out);
+        } catch (...) {
+            tqp::groupby_release(c, P);
+            throw;
+        }
+        tqp::groupby_release(c, P);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,247 @@
+// common.cuh -- context, errors, stream-ordered temporaries, instrumented launches,
+// and the device helpers shared by every libtqp kernel (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/tqp.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libtqp is written for sm_100a (B200) only"
+#endif
+
+namespace tqp {
+
+struct Error {
+    tqp_status status;
+    std::string msg;
+};
+
+[[noreturn]] inline void fail(tqp_status s, const std::string& m) { throw Error{s, m}; }
+
+#define TQP_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            ::tqp::fail(e_ == cudaErrorMemoryAllocation ? TQP_ERR_OUT_OF_MEMORY : TQP_ERR_CUDA, \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                 \
+    } while (0)
+
+}  // namespace tqp
+
+struct tqp_ctx {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;
+    std::string err;
+    int64_t launches = 0;
+    bool profiling = false;
+    struct Pending { const char* name; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+    std::vector<cudaEvent_t> free_events;
+    struct Stat { double ms = 0; int64_t launches = 0; double bytes = 0; };
+    std::map<std::string, Stat> stats;
+    // algorithmic (compulsory) bytes per kernel name, accounted on the host at
+    // launch time; independent of profiling
+    void add_bytes(const char* name, double b) { stats[name].bytes += b; }
+    void* pinned = nullptr;   // 4 KB pinned host scratch for scalar readbacks
+
+    cudaEvent_t get_event() {
+        if (!free_events.empty()) {
+            cudaEvent_t e = free_events.back();
+            free_events.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        TQP_CUDA(cudaEventCreate(&e));
+        return e;
+    }
+    void drain_profile();   // synchronises; folds pending events into stats
+};
+
+namespace tqp {
+
+// ------------------------------------------------------------------ memory
+// Device temporaries from the context's stream-ordered pool (cudaMallocFromPoolAsync);
+// freed stream-ordered on destruction, so RAII is safe on every error path.
+template <typename T>
+struct DevBuf {
+    tqp_ctx* ctx = nullptr;
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(tqp_ctx* c, size_t count) { alloc(c, count); }
+    void alloc(tqp_ctx* c, size_t count) {
+        release();
+        ctx = c;
+        n = count;
+        if (count == 0) return;
+        void* q = nullptr;
+        TQP_CUDA(cudaMallocFromPoolAsync(&q, count * sizeof(T), c->pool, c->stream));
+        p = static_cast<T*>(q);
+    }
+    void release() {
+        if (p && ctx) cudaFreeAsync(p, ctx->stream);
+        p = nullptr;
+        n = 0;
+    }
+    void zero() {
+        if (p) TQP_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), ctx->stream));
+    }
+    T* get() const { return p; }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); ctx = o.ctx; p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+};
+
+// Read `bytes` from device memory into host memory: one stream synchronisation.
+inline void read_back(tqp_ctx* ctx, void* host, const void* dev, size_t bytes) {
+    if (bytes > 4096) fail(TQP_ERR_INVALID_ARGUMENT, "read_back too large");
+    TQP_CUDA(cudaMemcpyAsync(ctx->pinned, dev, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    TQP_CUDA(cudaStreamSynchronize(ctx->stream));
+    memcpy(host, ctx->pinned, bytes);
+}
+
+// -------------------------------------------------------------- launching
+template <typename... KArgs, typename... Args>
+inline void launch(tqp_ctx* ctx, const char* name, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                   Args... args) {
+    if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (ctx->profiling) {
+        a = ctx->get_event();
+        b = ctx->get_event();
+        TQP_CUDA(cudaEventRecord(a, ctx->stream));
+    }
+    k<<<grid, block, smem, ctx->stream>>>(args...);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(TQP_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+    ctx->launches++;
+    if (ctx->profiling) {
+        TQP_CUDA(cudaEventRecord(b, ctx->stream));
+        ctx->pending.push_back({name, a, b});
+    }
+}
+
+template <typename K>
+inline void set_smem(K* k, size_t bytes) {
+    TQP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------------------ key helpers
+// Order-preserving map of a signed value to unsigned (sign-bit flip).
+__host__ __device__ inline uint64_t ordered_u64(int64_t k) { return (uint64_t)k ^ 0x8000000000000000ull; }
+__host__ __device__ inline int64_t unordered_i64(uint64_t u) { return (int64_t)(u ^ 0x8000000000000000ull); }
+
+// Internal dtype code for unsigned 64-bit packed keys (not part of the ABI).
+constexpr int DT_U64 = 100;
+
+__device__ __forceinline__ int64_t load_as_i64(const void* p, int dtype, int64_t i) {
+    switch (dtype) {
+        case TQP_U8: return (int64_t)__ldg((const uint8_t*)p + i);
+        case TQP_I32: return (int64_t)__ldg((const int32_t*)p + i);
+        default: return (int64_t)__ldg((const long long*)p + i);
+    }
+}
+
+inline size_t dtype_size(int dt) {
+    switch (dt) {
+        case TQP_U8: return 1;
+        case TQP_I32: return 4;
+        case TQP_I64: return 8;
+        case DT_U64: return 8;
+    }
+    return 0;
+}
+inline void check_col(const tqp_col& c, int64_t n, const char* what) {
+    if (n < 0) fail(TQP_ERR_INVALID_ARGUMENT, std::string(what) + ": negative length");
+    if (c.dtype != TQP_U8 && c.dtype != TQP_I32 && c.dtype != TQP_I64)
+        fail(TQP_ERR_INVALID_ARGUMENT, std::string(what) + ": unsupported dtype");
+    if (n > 0 && c.data == nullptr) fail(TQP_ERR_INVALID_ARGUMENT, std::string(what) + ": null data");
+}
+
+// --------------------------------------------------- decoupled look-back
+// Single-pass chained scan across tiles (Merrill & Garland's decoupled
+// look-back). Status word: bits [63:62] flag (0 = not ready, 1 = tile aggregate,
+// 2 = inclusive prefix), bits [61:0] value. Value and flag live in one aligned
+// 64-bit word, so relaxed gpu-scope loads/stores are sufficient.
+constexpr uint64_t LB_AGG = 1ull << 62;
+constexpr uint64_t LB_PRE = 2ull << 62;
+constexpr uint64_t LB_VAL = (1ull << 62) - 1;
+
+__device__ __forceinline__ void lb_store(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t lb_load(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Called by ALL lanes of ONE warp. Publishes `agg` for `tile` and returns the
+// exclusive prefix (sum of all earlier tiles' aggregates) in every lane.
+// Dynamic tile ids (taken in launch order) guarantee forward progress.
+template <typename Op>
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile, uint64_t agg, Op op,
+                                                  uint64_t identity) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) lb_store(status, LB_PRE | (agg & LB_VAL));
+        return identity;
+    }
+    if (lane == 0) lb_store(status + tile, LB_AGG | (agg & LB_VAL));
+    uint64_t excl = identity;
+    int64_t win = tile - 1;   // the closest earlier tile this lane group looks at
+    while (true) {
+        int64_t idx = win - lane;
+        uint64_t w = (idx >= 0) ? lb_load(status + idx) : (LB_PRE | (identity & LB_VAL));
+        // all lanes must have a ready word before reducing
+        while (__any_sync(0xffffffffu, (w >> 62) == 0)) {
+            if ((w >> 62) == 0) w = lb_load(status + idx);
+        }
+        unsigned pre = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+        int stop = pre ? (__ffs(pre) - 1) : 31;   // lanes 0..stop contribute
+        uint64_t v = (lane <= stop) ? (w & LB_VAL) : identity;
+        for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+        excl = op(excl, v);
+        if (pre) break;
+        win -= 32;
+    }
+    if (lane == 0) lb_store(status + tile, LB_PRE | (op(excl, agg) & LB_VAL));
+    return excl;
+}
+
+struct OpAdd {
+    __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const { return a + b; }
+};
+struct OpMax {
+    __device__ __forceinline__ uint64_t operator()(uint64_t a, uint64_t b) const { return a > b ? a : b; }
+};
+
+// Dynamic tile id: taken by thread 0 and broadcast through shared memory.
+__device__ __forceinline__ int64_t take_tile(unsigned long long* counter, int64_t* smem_slot) {
+    if (threadIdx.x == 0) *smem_slot = (int64_t)atomicAdd(counter, 1ull);
+    __syncthreads();
+    return *smem_slot;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+}  // namespace tqp

@@ -1,0 +1,32 @@
+// internal.h -- interfaces shared between libtqp translation units (not part of the ABI).
+#pragma once
+
+#include "common.cuh"
+
+namespace tqp {
+
+// Radix sort of one key column (stable; "radix sort" :256/:1148).
+// Sort domain value u = ordered_u64(key) (DT_U64: the key itself); descending: u = ~u.
+// Requested outputs (all nullable / optional):
+struct SortOut {
+    void* sorted_orig = nullptr;       // n elements of the input dtype = keys[perm]
+    int64_t* perm64 = nullptr;         // n x int64 permutation
+    uint64_t* sorted_u = nullptr;      // n x sort-domain values u (ascending)
+    bool want_internal = false;        // keep internal sorted keys + u32 permutation below
+    bool want_perm32 = false;          // keep the u32 permutation only
+    // results
+    bool k32 = false;                  // internal keys are the low 32 bits of u
+    uint64_t and_bits = 0, or_bits = 0;   // AND / OR of all u (varying-bit mask = and ^ or)
+    int passes = 0;
+    DevBuf<uint32_t> keys32;           // internal sorted keys (k32)
+    DevBuf<uint64_t> keys64;           // internal sorted keys (!k32)
+    DevBuf<uint32_t> perm32;           // internal permutation
+};
+
+void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& out);
+
+// Exclusive / inclusive scans over device arrays (decoupled look-back).
+void iota_i64(tqp_ctx* ctx, int64_t* p, int64_t n);
+void scan_max_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n);
+
+}  // namespace tqp

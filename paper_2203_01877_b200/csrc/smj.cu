@@ -1,0 +1,371 @@
+// smj.cu -- generic many-to-many sort-merge join, Alg. 1 (
+// prose :1114-1137) with readings R2 (ascending), R3 (bucketize right=True),
+// R4 (div and remainder by rightHist), R5 (histograms over present keys), R6
+// (output order key asc, left row asc, right row asc).
+//
+// Paper step -> kernel here:
+//   l.2-3  sort both key columns with permutation       -> radix_sort (sort.cu)
+//   l.4    bincount left / right                          -> rle_kernel: run-length
+//          encoding of the sorted keys (unique key, run start); counts are run
+//          lengths, so no domain-sized histogram is ever materialised
+//   l.5-8  histMul = L*R; cumsums                         -> intersect_kernel (merge
+//          of the two unique-key lists, compaction of the common keys with
+//          L, R, startL = cumL - L, startR = cumR - R) + cum_kernel (inclusive
+//          scan of L*R by decoupled look-back = cumHistMul)
+//   l.9    outSize = cumHistMul[-1]                       -> one 8-byte readback
+//   l.10-14 arange, bucketize, in-bucket offset, div/rem -> expand_kernel: each CTA
+//          owns a fixed output range, finds its first bucket with one
+//          upper_bound (= bucketize right=True), and walks (q, r) incrementally
+//          (o' = q*R + r) instead of a 64-bit division per output.
+#include "internal.h"
+
+struct tqp_smj_plan {
+    int64_t n_left = 0, n_right = 0, K = 0, out_size = 0;
+    tqp::DevBuf<uint32_t> perm_l, perm_r;
+    tqp::DevBuf<int64_t> mL, mR, msL, msR, mcum;
+};
+
+namespace tqp {
+
+namespace {
+constexpr int JNT = 256;
+constexpr int JNW = JNT / 32;
+constexpr int JIPT = 8;
+constexpr int JTILE = JNT * JIPT;
+
+// Compaction helper shared by the RLE / intersection kernels: thread-ordered
+// (item i, thread) flags -> exclusive positions; returns the tile's exclusive
+// prefix. flags are block-striped: item i of thread t is tile position i*JNT + t.
+struct CompactTile {
+    uint32_t s_cnt[JIPT * JNW];
+    uint64_t s_excl;
+    uint32_t s_tot;
+};
+
+__device__ __forceinline__ void compact_scan(CompactTile& s, const unsigned* bal, int64_t tile, uint64_t* status) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int i = 0; i < JIPT; i++)
+        if (lane == 0) s.s_cnt[i * JNW + warp] = __popc(bal[i]);
+    __syncthreads();
+    if (warp == 0) {
+        constexpr int PER = JIPT * JNW / 32;
+        uint32_t c[PER], local = 0;
+#pragma unroll
+        for (int j = 0; j < PER; j++) { c[j] = s.s_cnt[lane * PER + j]; local += c[j]; }
+        uint32_t x = local;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
+        uint32_t run = x - local;
+#pragma unroll
+        for (int j = 0; j < PER; j++) { s.s_cnt[lane * PER + j] = run; run += c[j]; }
+        const uint64_t e = lookback_warp(status, tile, tot, OpAdd(), 0ull);
+        if (lane == 0) { s.s_excl = e; s.s_tot = tot; }
+    }
+    __syncthreads();
+}
+
+// Run-length encoding of sorted keys: heads -> (unique key, run start).
+// Writes ustart[U] = n and *U_out (last tile).
+__global__ void __launch_bounds__(JNT) rle_kernel(const uint64_t* __restrict__ u, int64_t n, uint64_t* ukey,
+                                                  int64_t* ustart, int64_t* U_out, uint64_t* status,
+                                                  unsigned long long* counter, int64_t n_tiles) {
+    __shared__ int64_t s_tile;
+    __shared__ CompactTile s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tile = take_tile(counter, &s_tile);
+    const int64_t base = tile * JTILE;
+    unsigned bal[JIPT];
+    uint64_t key[JIPT];
+#pragma unroll
+    for (int i = 0; i < JIPT; i++) {
+        const int64_t p = base + i * JNT + tid;
+        bool head = false;
+        if (p < n) {
+            key[i] = u[p];
+            head = (p == 0) || (u[p - 1] != key[i]);
+        }
+        bal[i] = __ballot_sync(0xffffffffu, head);
+    }
+    compact_scan(s, bal, tile, status);
+    const int64_t excl = (int64_t)s.s_excl;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < JIPT; i++) {
+        if (bal[i] & (1u << lane)) {
+            const int64_t j = excl + s.s_cnt[i * JNW + warp] + __popc(bal[i] & lt);
+            ukey[j] = key[i];
+            ustart[j] = base + i * JNT + tid;
+        }
+    }
+    if (tile == n_tiles - 1 && tid == 0) {
+        const int64_t U = excl + s.s_tot;
+        *U_out = U;
+        ustart[U] = n;
+    }
+}
+
+__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t k) {
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// For each left unique key: find it among the right unique keys; compact the
+// common keys with (L, R, startL, startR). Grid covers n_left (an upper bound
+// of U_l); tiles past U_l exit.
+__global__ void __launch_bounds__(JNT) intersect_kernel(const uint64_t* __restrict__ ukl, const int64_t* __restrict__ usl,
+                                                        const int64_t* U_l_p, const uint64_t* __restrict__ ukr,
+                                                        const int64_t* __restrict__ usr, const int64_t* U_r_p,
+                                                        int64_t* mL, int64_t* mR, int64_t* msL, int64_t* msR,
+                                                        int64_t* K_out, uint64_t* status, unsigned long long* counter) {
+    __shared__ int64_t s_tile, s_rlo, s_rhi;
+    __shared__ CompactTile s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tile = take_tile(counter, &s_tile);
+    const int64_t U_l = *U_l_p, U_r = *U_r_p;
+    const int64_t base = tile * JTILE;
+    if (base >= U_l) return;
+    const int64_t last = min(base + JTILE, U_l) - 1;
+    if (tid == 0) s_rlo = lower_bound_u64(ukr, 0, U_r, ukl[base]);
+    if (tid == 32) s_rhi = lower_bound_u64(ukr, 0, U_r, ukl[last]) + 1;
+    __syncthreads();
+    const int64_t rlo = s_rlo, rhi = min(s_rhi, U_r);
+    unsigned bal[JIPT];
+    int64_t L[JIPT], R[JIPT], sL[JIPT], sR[JIPT];
+#pragma unroll
+    for (int i = 0; i < JIPT; i++) {
+        const int64_t j = base + i * JNT + tid;
+        bool hit = false;
+        if (j < U_l) {
+            const uint64_t k = ukl[j];
+            const int64_t p = lower_bound_u64(ukr, rlo, rhi, k);
+            if (p < rhi && ukr[p] == k) {
+                hit = true;
+                sL[i] = usl[j];
+                L[i] = usl[j + 1] - sL[i];
+                sR[i] = usr[p];
+                R[i] = usr[p + 1] - sR[i];
+            }
+        }
+        bal[i] = __ballot_sync(0xffffffffu, hit);
+    }
+    compact_scan(s, bal, tile, status);
+    const int64_t excl = (int64_t)s.s_excl;
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int i = 0; i < JIPT; i++) {
+        if (bal[i] & (1u << lane)) {
+            const int64_t m = excl + s.s_cnt[i * JNW + warp] + __popc(bal[i] & lt);
+            mL[m] = L[i];
+            mR[m] = R[i];
+            msL[m] = sL[i];
+            msR[m] = sR[i];
+        }
+    }
+    if (tid == 0 && last == U_l - 1) *K_out = excl + s.s_tot;
+}
+
+// cumHistMul = inclusive scan of histMul = L*R over the K common keys.
+__global__ void __launch_bounds__(JNT) cum_kernel(const int64_t* __restrict__ mL, const int64_t* __restrict__ mR,
+                                                  const int64_t* K_p, int64_t* mcum, int64_t* out_size,
+                                                  int* overflow, uint64_t* status, unsigned long long* counter) {
+    __shared__ int64_t s_tile;
+    __shared__ uint64_t s_w[JNW], s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t tile = take_tile(counter, &s_tile);
+    const int64_t K = *K_p;
+    const int64_t base = tile * JTILE + (int64_t)tid * JIPT;   // blocked: 8 consecutive per thread
+    if (tile * JTILE >= K) return;
+    uint64_t v[JIPT], t = 0;
+#pragma unroll
+    for (int i = 0; i < JIPT; i++) {
+        v[i] = (base + i < K) ? (uint64_t)mL[base + i] * (uint64_t)mR[base + i] : 0;
+        t += v[i];
+    }
+    uint64_t x = t;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint64_t wpre = 0, tot = 0;
+    for (int w = 0; w < JNW; w++) {
+        if (w < warp) wpre += s_w[w];
+        tot += s_w[w];
+    }
+    if (warp == 0) {
+        const uint64_t e = lookback_warp(status, tile, tot, OpAdd(), 0ull);
+        if (lane == 0) {
+            s_excl = e;
+            if (e + tot >= LB_VAL || tot >= LB_VAL) *overflow = 1;
+            if ((tile + 1) * JTILE >= K) *out_size = (int64_t)(e + tot);
+        }
+    }
+    __syncthreads();
+    uint64_t run = s_excl + wpre + x - t;
+#pragma unroll
+    for (int i = 0; i < JIPT; i++) {
+        run += v[i];
+        if (base + i < K) mcum[base + i] = (int64_t)run;
+    }
+}
+
+constexpr int ENT = 256;
+constexpr int EIPT = 8;
+constexpr int ETILE = ENT * EIPT;
+
+__device__ __forceinline__ int64_t upper_bound_i64(const int64_t* a, int64_t lo, int64_t hi, int64_t x) {
+    while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// Output offsets [begin, end): bucket b = upper_bound(cumHistMul, o) (bucketize
+// right=True); o' = o - (cumHistMul[b] - histMul[b]); q = o' / R, r = o' % R;
+// left = leftIdx[startL + q], right = rightIdx[startR + r].
+__global__ void __launch_bounds__(ENT) expand_kernel(const int64_t* __restrict__ mL, const int64_t* __restrict__ mR,
+                                                     const int64_t* __restrict__ msL, const int64_t* __restrict__ msR,
+                                                     const int64_t* __restrict__ mcum, int64_t K,
+                                                     const uint32_t* __restrict__ perm_l,
+                                                     const uint32_t* __restrict__ perm_r, int64_t begin, int64_t end,
+                                                     int64_t* __restrict__ lo_out, int64_t* __restrict__ ro_out) {
+    __shared__ int64_t s_b0, s_b1;
+    const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
+    const int64_t c1 = min(c0 + ETILE, end);
+    if (threadIdx.x == 0) s_b0 = upper_bound_i64(mcum, 0, K, c0);
+    if (threadIdx.x == 32) s_b1 = upper_bound_i64(mcum, 0, K, c1 - 1);
+    __syncthreads();
+    const int64_t o0 = c0 + (int64_t)threadIdx.x * EIPT;
+    if (o0 >= c1) return;
+    int64_t b = upper_bound_i64(mcum, s_b0, s_b1 + 1, o0);
+    int64_t L = mL[b], R = mR[b], sL = msL[b], sR = msR[b];
+    int64_t off = o0 - (mcum[b] - L * R);
+    int64_t q = off / R, r = off - q * R;
+    const int cnt = (int)min((int64_t)EIPT, c1 - o0);
+    for (int j = 0; j < cnt; j++) {
+        const int64_t o = o0 + j - begin;
+        lo_out[o] = (int64_t)__ldg(perm_l + sL + q);
+        ro_out[o] = (int64_t)__ldg(perm_r + sR + r);
+        if (++r == R) {
+            r = 0;
+            if (++q == L) {
+                q = 0;
+                if (++b < K) { L = mL[b]; R = mR[b]; sL = msL[b]; sR = msR[b]; }
+            }
+        }
+    }
+}
+
+void sort_side(tqp_ctx* ctx, const tqp_col& c, int64_t n, DevBuf<uint64_t>& sorted_u, DevBuf<uint32_t>& perm) {
+    SortOut so;
+    so.want_perm32 = true;
+    sorted_u.alloc(ctx, n);
+    so.sorted_u = sorted_u.get();
+    radix_sort(ctx, c.data, c.dtype, n, false, so);
+    perm = std::move(so.perm32);
+}
+
+void rle(tqp_ctx* ctx, const uint64_t* u, int64_t n, DevBuf<uint64_t>& ukey, DevBuf<int64_t>& ustart,
+         int64_t* U_dev) {
+    ukey.alloc(ctx, n);
+    ustart.alloc(ctx, n + 1);
+    const int64_t tiles = ceil_div(n, JTILE);
+    DevBuf<uint64_t> status(ctx, tiles);
+    DevBuf<unsigned long long> counter(ctx, 1);
+    status.zero();
+    counter.zero();
+    ctx->add_bytes("tqp_smj_rle", 8.0 * (double)n);
+    launch(ctx, "tqp_smj_rle", rle_kernel, dim3((unsigned)tiles), dim3(JNT), 0, u, n, ukey.get(), ustart.get(), U_dev,
+           status.get(), counter.get(), tiles);
+}
+}  // namespace
+
+tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right, int64_t nr, int64_t* out_size_host) {
+    check_col(left, nl, "smj left");
+    check_col(right, nr, "smj right");
+    auto* P = new tqp_smj_plan();
+    try {
+        P->n_left = nl;
+        P->n_right = nr;
+        if (nl == 0 || nr == 0) {
+            *out_size_host = 0;
+            return P;
+        }
+        DevBuf<uint64_t> ul, ur;
+        sort_side(ctx, left, nl, ul, P->perm_l);
+        sort_side(ctx, right, nr, ur, P->perm_r);
+        DevBuf<int64_t> scal(ctx, 4);   // U_l, U_r, K, out_size
+        DevBuf<int> ovf(ctx, 1);
+        scal.zero();
+        ovf.zero();
+        DevBuf<uint64_t> ukl, ukr;
+        DevBuf<int64_t> usl, usr;
+        rle(ctx, ul.get(), nl, ukl, usl, scal.get() + 0);
+        rle(ctx, ur.get(), nr, ukr, usr, scal.get() + 1);
+        ul.release();
+        ur.release();
+        const int64_t cap = std::min(nl, nr);
+        P->mL.alloc(ctx, cap);
+        P->mR.alloc(ctx, cap);
+        P->msL.alloc(ctx, cap);
+        P->msR.alloc(ctx, cap);
+        P->mcum.alloc(ctx, cap);
+        {
+            const int64_t tiles = ceil_div(nl, JTILE);
+            DevBuf<uint64_t> status(ctx, tiles);
+            DevBuf<unsigned long long> counter(ctx, 1);
+            status.zero();
+            counter.zero();
+            launch(ctx, "tqp_smj_intersect", intersect_kernel, dim3((unsigned)tiles), dim3(JNT), 0, ukl.get(), usl.get(),
+                   scal.get() + 0, ukr.get(), usr.get(), scal.get() + 1, P->mL.get(), P->mR.get(), P->msL.get(),
+                   P->msR.get(), scal.get() + 2, status.get(), counter.get());
+        }
+        {
+            const int64_t tiles = ceil_div(cap, JTILE);
+            DevBuf<uint64_t> status(ctx, tiles);
+            DevBuf<unsigned long long> counter(ctx, 1);
+            status.zero();
+            counter.zero();
+            launch(ctx, "tqp_smj_cumsum", cum_kernel, dim3((unsigned)tiles), dim3(JNT), 0, P->mL.get(), P->mR.get(),
+                   scal.get() + 2, P->mcum.get(), scal.get() + 3, ovf.get(), status.get(), counter.get());
+        }
+        int64_t h[4];
+        int o = 0;
+        read_back(ctx, h, scal.get(), 32);
+        read_back(ctx, &o, ovf.get(), 4);
+        if (o) fail(TQP_ERR_OVERFLOW, "smj: output size exceeds 2^62");
+        ctx->add_bytes("tqp_smj_intersect", 16.0 * (double)std::min(nl, nr) + 32.0 * (double)h[2]);
+        ctx->add_bytes("tqp_smj_cumsum", 24.0 * (double)h[2]);
+        P->K = h[2];
+        P->out_size = h[2] > 0 ? h[3] : 0;
+        *out_size_host = P->out_size;
+        return P;
+    } catch (...) {
+        delete P;
+        throw;
+    }
+}
+
+void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end, int64_t* lo, int64_t* ro) {
+    if (begin < 0 || end < begin || end > P->out_size) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: bad window");
+    if (end == begin) return;
+    if (!lo || !ro) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: null output");
+    const int64_t blocks = ceil_div(end - begin, ETILE);
+    if (blocks >= (int64_t(1) << 31)) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: window too large");
+    ctx->add_bytes("tqp_smj_expand", 16.0 * (double)(end - begin));
+    launch(ctx, "tqp_smj_expand", expand_kernel, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(), P->mR.get(),
+           P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->perm_l.get(), P->perm_r.get(), begin, end, lo, ro);
+}
+
+void smj_release(tqp_ctx*, tqp_smj_plan* P) { delete P; }
+
+}  // namespace tqp

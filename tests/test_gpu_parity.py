@@ -1,0 +1,420 @@
+"""GPU parity: libtqp (through the C ABI) vs the CPU oracle, element by element.
+
+Bars: indices, counts, keys and int128 sums bit-exact;
+fp64 averages within 1e-12 relative (north star). Where several outputs are
+correct the ABI fixes a canonical order (stable sort, probe-row order, (key, l, r)
+order), so whole arrays are compared. Sizes span several tiles and ragged tails;
+full-size cases (BASELINE configs[2]) use closed forms that hold at any size.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from conftest import golden
+from datagen import random_small_keys, tpch_orders_lineitem, uniform_keys, zipf_keys
+from datagen.queries import Q1_AGGS, Q1_COLS, Q1_KEYS, Q1_PREDS, Q6_AGGS, Q6_COLS, Q6_PREDS, columns
+
+pytestmark = pytest.mark.gpu
+
+I64_MIN, I64_MAX = -(1 << 63), (1 << 63) - 1
+
+
+@pytest.fixture(scope="module")
+def T():
+    import paper_2203_01877_b200 as T
+    assert torch.cuda.is_available()
+    return T
+
+
+def cu(x, dtype=torch.int64):
+    return torch.as_tensor(np.asarray(x)).to(dtype).cuda()
+
+
+def npy(t):
+    return t.cpu().numpy()
+
+
+# ------------------------------------------------------------------- sort
+
+def _sort_keys(kind, n, seed):
+    if kind == "i64_wide":
+        return random_small_keys(n, I64_MIN, I64_MAX, seed)
+    if kind == "i64_narrow":
+        return random_small_keys(n, 10**12, 10**12 + 5_000_000, seed)
+    if kind == "i64_33bit":
+        return random_small_keys(n, -(1 << 32), 1 << 32, seed)
+    if kind == "i32":
+        return random_small_keys(n, -(1 << 31), (1 << 31) - 1, seed, dtype=torch.int32)
+    if kind == "u8":
+        return random_small_keys(n, 0, 255, seed, dtype=torch.uint8)
+    if kind == "dups":
+        return random_small_keys(n, -3, 3, seed)
+    if kind == "extremes":
+        return torch.tensor([I64_MIN, I64_MAX, 0, -1], dtype=torch.int64)[random_small_keys(n, 0, 3, seed)]
+    if kind == "const":
+        return torch.full((n,), 42, dtype=torch.int64)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 33, 3071, 3072, 3073, 4095, 4096, 4097, 100_003])
+@pytest.mark.parametrize("kind", ["i64_wide", "i64_narrow", "i64_33bit", "i32", "u8", "dups", "extremes", "const"])
+@pytest.mark.parametrize("desc", [False, True])
+def test_sort_parity(T, n, kind, desc):
+    k = _sort_keys(kind, n, seed=n + 7)
+    s, p = T.sort(k.cuda(), descending=desc)
+    os_, op = oracle.sort(k.numpy(), descending=desc)
+    assert np.array_equal(npy(p), op)
+    assert np.array_equal(npy(s).astype(np.int64), os_)
+    assert s.dtype == k.dtype
+
+
+@pytest.mark.parametrize("kind,n", [("i64_narrow", 2_000_003), ("i64_wide", 1_000_001), ("i32", 1_500_000)])
+def test_sort_parity_large(T, kind, n):
+    k = _sort_keys(kind, n, seed=99)
+    s, p = T.sort(k.cuda())
+    _, op = oracle.sort(k.numpy())
+    assert np.array_equal(npy(p), op)
+
+
+# ------------------------------------------------------------------ PK-FK
+
+def test_pkfk_spec_example(T):
+    g = golden("spec_pkfk.json")
+    lo, ro = T.pkfk_join(cu(g["build"]), cu(g["probe"]))
+    assert [list(x) for x in zip(npy(lo), npy(ro))] == g["pairs"]
+
+
+def test_pkfk_duplicate_build_key(T):
+    g = golden("spec_pkfk.json")
+    with pytest.raises(T.TqpError) as e:
+        T.pkfk_join(cu(g["duplicate_build"]), cu(g["duplicate_probe"]))
+    assert e.value.status == T.TQP_ERR_DUPLICATE_BUILD_KEY
+
+
+@pytest.mark.parametrize("nb,np_,span,bd,pd", [
+    (0, 0, 10, torch.int64, torch.int64), (0, 100, 10, torch.int64, torch.int64), (1, 5, 3, torch.int64, torch.int64),
+    (100, 1000, 300, torch.int64, torch.int32), (5000, 100_001, 20_000, torch.int32, torch.int64),
+    (2047, 2049, 4096, torch.int64, torch.int64), (300_000, 4_000_037, 1_000_000, torch.int64, torch.int64),
+])
+def test_pkfk_random_parity(T, nb, np_, span, bd, pd):
+    rng = np.random.default_rng(nb + np_)
+    build = (rng.permutation(span)[:nb] - span // 3).astype(np.int64)
+    probe = rng.integers(-span // 2, span, np_).astype(np.int64)
+    lo, ro = T.pkfk_join(cu(build, bd), cu(probe, pd))
+    olo, oro = oracle.pkfk_join(build, probe)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+def test_pkfk_wide_and_extreme_keys(T):
+    build = np.array([I64_MIN, I64_MAX, 0, -1, 1 << 40, -(1 << 50)], np.int64)
+    probe = np.array([I64_MAX, 5, I64_MIN, -1, 1 << 40, 0, I64_MAX, -(1 << 50) + 1], np.int64)
+    lo, ro = T.pkfk_join(cu(build), cu(probe))
+    olo, oro = oracle.pkfk_join(build, probe)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+def test_pkfk_tpch_sf1_parity_and_closed_form(T):
+    orders, li = tpch_orders_lineitem(1.0, seed=42, device="cuda")
+    lo, ro = T.pkfk_join(orders["o_orderkey"], li["l_orderkey"])
+    n = li["l_orderkey"].numel()
+    assert torch.equal(ro, torch.arange(n, device="cuda"))
+    assert torch.equal(lo, li["l_parent"])
+    olo, oro = oracle.pkfk_join(npy(orders["o_orderkey"]), npy(li["l_orderkey"]))
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+def test_pkfk_tpch_filtered_build(T):
+    orders, li = tpch_orders_lineitem(0.01, seed=42, device="cuda")
+    _, sel = T.filter_compact([orders["o_orderdate"]], [(0, "lt", 9204)], mask=False)
+    bk = orders["o_orderkey"][sel]
+    lo, ro = T.pkfk_join(bk, li["l_orderkey"])
+    olo, oro = oracle.pkfk_join(npy(bk), npy(li["l_orderkey"]))
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+def test_pkfk_sf10_full_size_closed_form(T):
+    """BASELINE configs[2] at full size (15M x 60M), in bench.py's launch configuration:
+    every lineitem row matches exactly its parent order (generator closed form)."""
+    orders, li = tpch_orders_lineitem(10.0, seed=42, device="cuda")
+    lo, ro = T.pkfk_join(orders["o_orderkey"], li["l_orderkey"])
+    assert lo.numel() == li["l_orderkey"].numel()
+    assert torch.equal(ro, torch.arange(lo.numel(), device="cuda"))
+    assert torch.equal(lo, li["l_parent"])
+    # sampled rows against the oracle's definition, one by one
+    idx = torch.randint(0, lo.numel(), (64,), generator=torch.Generator().manual_seed(1)).tolist()
+    ok = npy(orders["o_orderkey"])
+    for i in idx:
+        key = int(li["l_orderkey"][i])
+        blo, _ = oracle.pkfk_join(ok, np.array([key]))
+        assert int(lo[i]) == int(blo[0])
+
+
+@pytest.mark.parametrize("anti", [False, True])
+def test_pkfk_semi_anti(T, anti):
+    rng = np.random.default_rng(5)
+    build = rng.integers(0, 5000, 3000)      # duplicates allowed for semi/anti
+    probe = rng.integers(-100, 6000, 50_001)
+    sel, mask = T.pkfk_semi(cu(build), cu(probe), anti=anti, return_mask=True)
+    member = np.isin(probe, build)
+    assert np.array_equal(npy(mask).astype(bool), member)
+    want = np.nonzero(~member if anti else member)[0]
+    assert np.array_equal(npy(sel), want)
+    # cross-check against the oracle join on the de-duplicated build side
+    _, r = oracle.pkfk_join(np.unique(build), probe)
+    assert np.array_equal(np.nonzero(member)[0], r)
+
+
+def test_pkfk_semi_empty_build(T):
+    sel = T.pkfk_semi(cu(np.array([], np.int64)), cu(np.arange(10)), anti=True)
+    assert npy(sel).tolist() == list(range(10))
+    assert T.pkfk_semi(cu(np.array([], np.int64)), cu(np.arange(10))).numel() == 0
+
+
+# -------------------------------------------------------------------- SMJ
+
+def test_smj_alg1_trace(T):
+    g = golden("spec_alg1_trace.json")
+    plan = T.smj_prepare(cu(g["left"]), cu(g["right"]))
+    assert plan.size == g["outSize"]
+    lo, ro = plan.expand(0, plan.size)
+    assert npy(lo).tolist() == g["leftOutIdx"] and npy(ro).tolist() == g["rightOutIdx"]
+
+
+def test_smj_r4_pin(T):
+    g = golden("r4_remainder_pin.json")
+    lo, ro = T.smj_join(cu(g["left"]), cu(g["right"]))
+    assert [list(x) for x in zip(npy(lo), npy(ro))] == g["pairs"]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_smj_random_parity(T, seed):
+    rng = np.random.default_rng(seed)
+    nl = int(rng.integers(0, 6000))
+    nr = int(rng.integers(0, 6000))
+    kmax = int(rng.choice([3, 50, 2000, 10**6]))
+    left = rng.integers(-kmax, kmax, nl)
+    right = rng.integers(-kmax, kmax, nr)
+    lo, ro = T.smj_join(cu(left), cu(right))
+    olo, oro = oracle.smj_join(left, right)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+def test_smj_dtypes_and_extremes(T):
+    left = np.array([I64_MAX, I64_MIN, 0, I64_MAX, -3, 7], np.int64)
+    right = np.array([-3, I64_MAX, I64_MAX, I64_MIN, 7, 7], np.int64)
+    lo, ro = T.smj_join(cu(left), cu(right))
+    olo, oro = oracle.smj_join(left, right)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    l32 = np.array([1, 2, 2, 300], np.int64)
+    lo, ro = T.smj_join(cu(l32, torch.int32), cu(np.array([2, 300, 2]), torch.int64))
+    olo, oro = oracle.smj_join(l32, [2, 300, 2])
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+def test_smj_zipf_uniform_parity(T):
+    """Config-4 shape (Zipf(s=1) left x uniform right) at 400K x 400K."""
+    left = zipf_keys(400_000, 400_000, seed=42, device="cuda")
+    right = uniform_keys(400_000, 400_000, seed=43, device="cuda")
+    plan = T.smj_prepare(left, right)
+    assert plan.size == oracle.smj_count(npy(left), npy(right))
+    lo, ro = plan.expand(0, plan.size)
+    olo, oro = oracle.smj_join(npy(left), npy(right))
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    # windows, including ragged ones crossing the heavy key's bucket
+    rng = np.random.default_rng(3)
+    for _ in range(4):
+        b = int(rng.integers(0, plan.size))
+        e = int(min(plan.size, b + rng.integers(1, 50_000)))
+        wl, wr = plan.expand(b, e)
+        assert np.array_equal(npy(wl), olo[b:e]) and np.array_equal(npy(wr), oro[b:e])
+    plan.release()
+
+
+def test_smj_both_zipf_windows(T):
+    """Config-4 as stated (both sides Zipf): outSize exact; windows by the oracle's per-offset route."""
+    left = zipf_keys(200_000, 10**6, seed=42, device="cuda")
+    right = zipf_keys(200_000, 10**6, seed=43, stream=101, device="cuda")
+    plan = T.smj_prepare(left, right)
+    assert plan.size == oracle.smj_count(npy(left), npy(right))
+    rng = np.random.default_rng(4)
+    for b in [0] + [int(x) for x in rng.integers(0, plan.size - 5000, 3)]:
+        wl, wr = plan.expand(b, b + 5000)
+        olo, oro = oracle.smj_window(npy(left), npy(right), b, b + 5000)
+        assert np.array_equal(npy(wl), olo) and np.array_equal(npy(wr), oro)
+    plan.release()
+
+
+def test_smj_empty(T):
+    for l, r in [([], []), ([1, 2], []), ([], [3]), ([1], [2])]:
+        lo, ro = T.smj_join(cu(np.array(l, np.int64)), cu(np.array(r, np.int64)))
+        assert lo.numel() == 0 and ro.numel() == 0
+
+
+# ----------------------------------------------------------------- filter
+
+def test_filter_spec_listing(T):
+    g = golden("spec_filter.json")
+    mask, sel = T.filter_compact([cu(g["l_quantity"])], [(0, "lt", 24)])
+    assert npy(mask).tolist() == g["mask"] and npy(sel).tolist() == g["sel"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2047, 2048, 2049, 1_000_003])
+def test_filter_random_parity(T, n):
+    rng = np.random.default_rng(n)
+    a = rng.integers(-50, 50, n)
+    b = rng.integers(0, 256, n).astype(np.uint8)
+    c = rng.integers(-10**6, 10**6, n).astype(np.int32)
+    cols = [a, b, c]
+    preds = [(0, "ge", -20), (1, "ne", 7), (2, "lt", 500_000), (0, "le", 45)]
+    mask, sel = T.filter_compact([cu(a), cu(b, torch.uint8), cu(c, torch.int32)], preds)
+    om, os_ = oracle.filter_compact(cols, preds)
+    assert np.array_equal(npy(mask), om) and np.array_equal(npy(sel), os_)
+
+
+@pytest.mark.parametrize("preds", [[], [(0, "lt", -100)], [(0, "ge", -100)]])
+def test_filter_all_or_none(T, preds):
+    a = np.arange(-50, 50)
+    mask, sel = T.filter_compact([cu(a)], preds)
+    om, os_ = oracle.filter_compact([a], preds)
+    assert np.array_equal(npy(mask), om) and np.array_equal(npy(sel), os_)
+
+
+def test_filter_q6_sf1(T):
+    _, li = tpch_orders_lineitem(1.0, seed=42, device="cuda")
+    cols = columns(li, Q6_COLS)
+    mask, sel = T.filter_compact(cols, Q6_PREDS)
+    om, os_ = oracle.filter_compact([npy(c) for c in cols], Q6_PREDS)
+    assert np.array_equal(npy(mask), om) and np.array_equal(npy(sel), os_)
+
+
+# ---------------------------------------------------------------- group-by
+
+def check_groupby(T, got, want, aggs):
+    assert got["n_groups"] == want["n_groups"]
+    for k in range(len(got["keys"])):
+        assert np.array_equal(npy(got["keys"][k]).astype(np.int64), want["keys"][k])
+    for a, (op, _) in enumerate(aggs):
+        w = want["results"][a]
+        if op == "sum":
+            assert T.int128_to_ints(got["results"][a]) == w
+        elif op == "avg":
+            g = npy(got["results"][a]).tolist()
+            for x, y in zip(g, w):
+                if math.isnan(y):
+                    assert math.isnan(x)
+                else:
+                    assert abs(x - y) <= 1e-12 * max(abs(y), 1e-300)
+        else:
+            assert npy(got["results"][a]).tolist() == w
+
+
+def test_groupby_spec_example(T):
+    g = golden("spec_groupby.json")
+    aggs = [("sum", [(1, 0, 1)])]
+    got = T.groupby_agg([cu(g["keys"]), cu(g["values"])], [0], aggs)
+    assert npy(got["keys"][0]).tolist() == g["group_keys"]
+    assert T.int128_to_ints(got["results"][0]) == g["sums"]
+
+
+@pytest.mark.parametrize("sf", [0.01, 1.0])
+def test_groupby_q1_parity(T, sf):
+    _, li = tpch_orders_lineitem(sf, seed=42, device="cuda")
+    cols = columns(li, Q1_COLS)
+    got = T.groupby_agg(cols, Q1_KEYS, Q1_AGGS, Q1_PREDS)
+    want = oracle.groupby_agg([npy(c) for c in cols], Q1_KEYS, Q1_AGGS, Q1_PREDS)
+    check_groupby(T, got, want, Q1_AGGS)
+
+
+def test_groupby_q6_fused_sum(T):
+    _, li = tpch_orders_lineitem(1.0, seed=42, device="cuda")
+    cols = columns(li, Q6_COLS)
+    got = T.groupby_agg(cols, [], Q6_AGGS, Q6_PREDS)
+    want = oracle.groupby_agg([npy(c) for c in cols], [], Q6_AGGS, Q6_PREDS)
+    check_groupby(T, got, want, Q6_AGGS)
+
+
+AGGS_ALL = [("sum", [(2, 0, 1)]), ("count", []), ("min", [(2, 0, 1)]), ("max", [(2, 3, -1)]),
+            ("avg", [(2, 0, 1)]), ("sum", [(2, 7, -1), (1, 1, 1)]), ("min", [(3, 0, 1)]), ("max", [(3, 5, 1)])]
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_groupby_random_parity(T, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.choice([0, 1, 2047, 2048, 2049, 50_000, 300_001]))
+    card = int(rng.choice([1, 3, 200, 100_000]))
+    k0 = rng.integers(0, min(card, 256), n).astype(np.uint8)
+    k1 = rng.integers(-card, card, n).astype(np.int32)
+    v = rng.integers(-10**12, 10**12, n)
+    w = rng.integers(-(1 << 62), 1 << 62, n)
+    k2 = rng.integers(-card, card, n)
+    cols = [k0, k1, v, w, k2]
+    key_idx = [[0], [1], [0, 1], [1, 0], [], [4], [1, 0, 0]][seed % 7]
+    preds = [] if seed % 3 else [(2, "gt", -10**11)]
+    gcols = [cu(k0, torch.uint8), cu(k1, torch.int32), cu(v), cu(w), cu(k2)]
+    got = T.groupby_agg(gcols, key_idx, AGGS_ALL, preds)
+    want = oracle.groupby_agg(cols, key_idx, AGGS_ALL, preds)
+    check_groupby(T, got, want, AGGS_ALL)
+
+
+def test_groupby_key_wider_than_64_bits_rejected(T):
+    x = cu(np.arange(10))
+    with pytest.raises(T.TqpError) as e:
+        T.groupby_agg([x, cu(np.arange(10), torch.uint8)], [0, 1], [("count", [])])
+    assert e.value.status == T.TQP_ERR_INVALID_ARGUMENT
+
+
+def test_groupby_high_cardinality(T):
+    _, li = tpch_orders_lineitem(0.01, seed=42, device="cuda")
+    cols = [li["l_orderkey"], li["l_quantity"], li["l_extendedprice"]]
+    aggs = [("sum", [(1, 0, 1)]), ("count", []), ("max", [(2, 0, 1)]), ("avg", [(2, 0, 1)])]
+    got = T.groupby_agg(cols, [0], aggs)
+    want = oracle.groupby_agg([npy(c) for c in cols], [0], aggs)
+    check_groupby(T, got, want, aggs)
+
+
+def test_groupby_empty_and_global(T):
+    e = cu(np.array([], np.int64))
+    got = T.groupby_agg([e], [0], [("sum", [(0, 0, 1)])])
+    assert got["n_groups"] == 0
+    aggs = [("sum", [(0, 0, 1)]), ("count", []), ("min", [(0, 0, 1)]), ("max", [(0, 0, 1)]), ("avg", [(0, 0, 1)])]
+    got = T.groupby_agg([e], [], aggs)
+    want = oracle.groupby_agg([np.array([], np.int64)], [], aggs)
+    check_groupby(T, got, want, aggs)
+    x = cu(np.arange(5000))
+    got = T.groupby_agg([x], [], aggs, preds=[(0, "lt", -1)])      # nothing passes
+    want = oracle.groupby_agg([np.arange(5000)], [], aggs, preds=[(0, "lt", -1)])
+    check_groupby(T, got, want, aggs)
+
+
+def test_groupby_int128_and_overflow(T):
+    v = np.full(100_000, (1 << 62) + 12345, np.int64)
+    got = T.groupby_agg([cu(v)], [], [("sum", [(0, 0, 1)]), ("avg", [(0, 0, 1)])])
+    want = oracle.groupby_agg([v], [], [("sum", [(0, 0, 1)]), ("avg", [(0, 0, 1)])])
+    check_groupby(T, got, want, [("sum", []), ("avg", [])])
+    with pytest.raises(T.TqpError) as e:
+        T.groupby_agg([cu(v)], [], [("sum", [(0, 0, 1), (0, 0, 1)])])
+    assert e.value.status == T.TQP_ERR_OVERFLOW
+
+
+def test_groupby_q1_sf10_full_size(T):
+    """BASELINE configs[2]-sized lineitem (60M rows) Q1, bench launch configuration, vs the oracle."""
+    _, li = tpch_orders_lineitem(10.0, seed=42, device="cuda")
+    cols = columns(li, Q1_COLS)
+    got = T.groupby_agg(cols, Q1_KEYS, Q1_AGGS, Q1_PREDS)
+    want = oracle.groupby_agg([npy(c) for c in cols], Q1_KEYS, Q1_AGGS, Q1_PREDS)
+    check_groupby(T, got, want, Q1_AGGS)
+
+
+def test_launch_counter_and_profiling(T):
+    ctx = T.context()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    T.sort(cu(np.arange(10_000)[::-1].copy()))
+    st = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    assert ctx.launch_count() >= 3
+    assert "tqp_onesweep" in st and st["tqp_onesweep"][1] >= 1
