@@ -14,7 +14,9 @@
  *    caller's input columns.
  *  - Ownership: inputs are borrowed and never modified. Outputs are
  *    caller-allocated (the bound is stated per function). Temporaries come from a
- *    stream-ordered memory pool owned by the context.
+ *    caching device allocator owned by the context (blocks are reused
+ *    stream-ordered on the context stream and returned on tqp_ctx_destroy).
+ *    Plans (tqp_smj_plan, tqp_groupby_plan) must be released before their context.
  *  - Ordering: all work is enqueued on the context's stream. A `*_host` output
  *    costs one stream synchronisation; functions that need a data-dependent size
  *    (sort pass plan, join sizes, group count) synchronise internally and say so.
@@ -196,6 +198,19 @@ tqp_status tqp_groupby_prepare(tqp_ctx* ctx, const tqp_col* cols_host, int n_col
 tqp_status tqp_groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* plan, void* const* keys_out_host,
                              void* const* results_out_host);
 void tqp_groupby_release(tqp_ctx* ctx, tqp_groupby_plan* plan);
+/* Merge partial group-by results -- the "gather and final reduce" of
+ * multi-GPU aggregation (the paper's data-parallel future work,
+ * PAPER.md:1076). Inputs: m partial rows (e.g. the tqp_groupby_fetch outputs of
+ * R ranks, concatenated): key_cols_host[k] = device column of key k (dtype of
+ * the original key column); counts = COUNT(*) of each partial row (device,
+ * m x int64); partial_host[a] = device array per aggregate a: SUM and AVG ->
+ * the exact int128 SUM of aggregate a's expression (m x 16 bytes, fetch
+ * layout), MIN / MAX -> m x int64, COUNT -> ignored (may be NULL). The merged
+ * groups are fetched with tqp_groupby_fetch; AVG = rn(merged SUM / merged
+ * COUNT) -- averages are never averaged. Synchronises once. */
+tqp_status tqp_groupby_merge(tqp_ctx* ctx, int64_t m, const tqp_col* key_cols_host, int n_keys,
+                             const tqp_agg* aggs_host, int n_aggs, const void* const* partial_host,
+                             const int64_t* counts, tqp_groupby_plan** plan, int64_t* n_groups_host);
 /* prepare + fetch into caller buffers of `capacity` groups; if capacity < G:
  * TQP_ERR_CAPACITY and *n_groups_host = G. */
 tqp_status tqp_groupby_agg(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols, int64_t n,

@@ -37,7 +37,7 @@ EXPORTED = [
     "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_kernel_stats",
     "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
     "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
-    "tqp_groupby_agg",
+    "tqp_groupby_agg", "tqp_groupby_merge",
 ]
 
 
@@ -81,6 +81,7 @@ _sig = {
     "tqp_groupby_release": ([_vp, _vp], None),
     "tqp_groupby_agg": ([_vp, _P(Col), _int, _i64, _P(ctypes.c_int32), _int, _P(Pred), _int, _P(Agg), _int,
                          _P(_vp), _P(_vp), _i64, _P(_i64)], _int),
+    "tqp_groupby_merge": ([_vp, _i64, _P(Col), _int, _P(Agg), _int, _P(_vp), _vp, _P(_vp), _P(_i64)], _int),
 }
 for _name, (_args, _res) in _sig.items():
     _f = getattr(_lib, _name)
@@ -146,8 +147,11 @@ class Context:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            _lib.tqp_ctx_destroy(h)
+        if h and _lib is not None:
+            try:
+                _lib.tqp_ctx_destroy(h)
+            except Exception:
+                pass
             self._h = None
 
     # ------------------------------------------------------------ plumbing
@@ -288,6 +292,41 @@ class Context:
         finally:
             _lib.tqp_groupby_release(self._h, plan)
         return {"n_groups": g, "keys": keys, "results": res}
+
+    def _fetch(self, plan, G, key_dtypes, aggs):
+        try:
+            g = G
+            keys = [torch.empty(g, dtype=dt, device=self.device) for dt in key_dtypes]
+            res = []
+            for op, _ in aggs:
+                o = AGGS[op] if isinstance(op, str) else int(op)
+                shape, dt = ((g, 2), torch.int64) if o == 0 else ((g,), torch.float64 if o == 4 else torch.int64)
+                res.append(torch.empty(shape, dtype=dt, device=self.device))
+            kp = (ctypes.c_void_p * max(len(keys), 1))(*[t.data_ptr() if g else None for t in keys])
+            rp = (ctypes.c_void_p * max(len(res), 1))(*[t.data_ptr() if g else None for t in res])
+            self._check(_lib.tqp_groupby_fetch(self._h, plan, kp, rp))
+        finally:
+            _lib.tqp_groupby_release(self._h, plan)
+        return {"n_groups": g, "keys": keys, "results": res}
+
+    def groupby_merge(self, key_cols, aggs, partials, counts):
+        """Merge partial group-by rows (tqp_groupby_merge): key_cols = [tensor per key], partials[a] =
+        int128 (m,2) SUM of aggregate a's expression (SUM/AVG) or int64 (MIN/MAX) or None (COUNT),
+        counts = COUNT(*) per partial row. Returns the same dict as groupby_agg."""
+        self._sync_stream()
+        ks = [_dev_tensor(k, self.device) for k in key_cols]
+        cnt = _dev_tensor(counts, self.device)
+        m = cnt.numel()
+        ca = (Col * max(len(ks), 1))(*[_col(k) for k in ks])
+        aa = _aggs(aggs)
+        ps = [None if p is None else p.to(self.device).contiguous() for p in partials]
+        pp = (ctypes.c_void_p * max(len(ps), 1))(*[p.data_ptr() if p is not None and p.numel() else None
+                                                     for p in ps])
+        plan = ctypes.c_void_p()
+        G = ctypes.c_int64(0)
+        self._check(_lib.tqp_groupby_merge(self._h, m, ca, len(ks), aa, len(aggs), pp, _ptr(cnt),
+                                           ctypes.byref(plan), ctypes.byref(G)))
+        return self._fetch(plan, G.value, [k.dtype for k in ks], aggs)
 
 
 class SmjPlan:

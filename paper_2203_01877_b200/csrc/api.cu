@@ -16,11 +16,60 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx*, const tqp_col*, int, int64_t, const 
                                   const tqp_agg*, int, int64_t*);
 void groupby_fetch(tqp_ctx*, const tqp_groupby_plan*, void* const*, void* const*);
 void groupby_release(tqp_ctx*, tqp_groupby_plan*);
+tqp_groupby_plan* groupby_merge(tqp_ctx*, int64_t, const tqp_col*, int, const tqp_agg*, int, const void* const*,
+                                const int64_t*, int64_t*);
 }  // namespace tqp
 
 static_assert(sizeof(tqp_col) == 16, "tqp_col layout");
 static_assert(sizeof(tqp_pred) == 16, "tqp_pred layout");
 static_assert(sizeof(tqp_agg) == 56, "tqp_agg layout");
+
+static size_t round_block(size_t b) {
+    if (b <= (1u << 20)) return (b + 511) & ~size_t(511);
+    return (b + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+}
+
+void* tqp_ctx::dalloc(size_t bytes) {
+    if (bytes == 0) return nullptr;
+    const size_t sz = round_block(bytes);
+    auto it = free_blocks.lower_bound(sz);
+    if (it != free_blocks.end() && it->first <= sz + sz / 4) {   // best fit within 25 %
+        void* p = it->second;
+        const size_t have = it->first;
+        free_blocks.erase(it);
+        cached_bytes -= have;
+        live_blocks[p] = have;
+        return p;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, sz);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        trim();
+        e = cudaMalloc(&p, sz);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        tqp::fail(TQP_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    }
+    live_blocks[p] = sz;
+    return p;
+}
+
+void tqp_ctx::dfree(void* p) {
+    auto it = live_blocks.find(p);
+    if (it == live_blocks.end()) return;
+    free_blocks.emplace(it->second, p);
+    cached_bytes += it->second;
+    live_blocks.erase(it);
+}
+
+void tqp_ctx::trim() {
+    cudaStreamSynchronize(stream);
+    for (auto& kv : free_blocks) cudaFree(kv.second);
+    free_blocks.clear();
+    cached_bytes = 0;
+}
 
 void tqp_ctx::drain_profile() {
     if (pending.empty()) return;
@@ -73,16 +122,8 @@ tqp_status tqp_ctx_create(int device, void* stream, tqp_ctx** out) {
         TQP_CUDA(cudaSetDevice(device));
         TQP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         c->stream = static_cast<cudaStream_t>(stream);
-        cudaMemPoolProps props{};
-        props.allocType = cudaMemAllocationTypePinned;
-        props.location.type = cudaMemLocationTypeDevice;
-        props.location.id = device;
-        TQP_CUDA(cudaMemPoolCreate(&c->pool, &props));
-        uint64_t thr = ~0ull;   // keep freed blocks cached in the pool
-        TQP_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
         TQP_CUDA(cudaMallocHost(&c->pinned, 4096));
     } catch (const tqp::Error& e) {
-        if (c->pool) cudaMemPoolDestroy(c->pool);
         delete c;
         return e.status;
     }
@@ -97,12 +138,18 @@ void tqp_ctx_destroy(tqp_ctx* c) {
     for (auto& p : c->pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     for (auto e : c->free_events) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
-    if (c->pool) cudaMemPoolDestroy(c->pool);
+    c->trim();
+    for (auto& kv : c->live_blocks) cudaFree(kv.first);
     delete c;
 }
 
 tqp_status tqp_ctx_set_stream(tqp_ctx* c, void* stream) {
-    TQP_GUARD(c, { c->drain_profile(); c->stream = static_cast<cudaStream_t>(stream); });
+    // cached blocks were last used on the old stream: order the switch
+    TQP_GUARD(c, {
+        c->drain_profile();
+        TQP_CUDA(cudaStreamSynchronize(c->stream));
+        c->stream = static_cast<cudaStream_t>(stream);
+    });
 }
 
 const char* tqp_last_error(const tqp_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -231,6 +278,16 @@ tqp_status tqp_groupby_fetch(tqp_ctx* c, const tqp_groupby_plan* plan, void* con
     TQP_GUARD(c, {
         if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_fetch: null plan");
         tqp::groupby_fetch(c, plan, keys_out, results_out);
+    });
+}
+
+tqp_status tqp_groupby_merge(tqp_ctx* c, int64_t m, const tqp_col* key_cols, int n_keys, const tqp_agg* aggs,
+                             int n_aggs, const void* const* partial, const int64_t* counts, tqp_groupby_plan** plan,
+                             int64_t* n_groups_host) {
+    TQP_GUARD(c, {
+        if (!plan || !n_groups_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: null output");
+        if ((n_keys && !key_cols) || (n_aggs && !aggs)) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: null array");
+        *plan = tqp::groupby_merge(c, m, key_cols, n_keys, aggs, n_aggs, partial, counts, n_groups_host);
     });
 }
 

@@ -7,6 +7,7 @@
 
 #include <map>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/tqp.h"
@@ -38,7 +39,15 @@ struct tqp_ctx {
     int device = 0;
     int num_sms = 148;
     cudaStream_t stream = nullptr;
-    cudaMemPool_t pool = nullptr;
+    // caching device allocator: blocks are reused stream-ordered on `stream`
+    // (all libtqp work of a context is on that one stream), never returned
+    // until tqp_ctx_destroy / an out-of-memory retry.
+    std::multimap<size_t, void*> free_blocks;
+    std::unordered_map<void*, size_t> live_blocks;
+    size_t cached_bytes = 0;
+    void* dalloc(size_t bytes);
+    void dfree(void* p);
+    void trim();
     std::string err;
     int64_t launches = 0;
     bool profiling = false;
@@ -68,8 +77,8 @@ struct tqp_ctx {
 namespace tqp {
 
 // ------------------------------------------------------------------ memory
-// Device temporaries from the context's stream-ordered pool (cudaMallocFromPoolAsync);
-// freed stream-ordered on destruction, so RAII is safe on every error path.
+// Device temporaries from the context's caching allocator; released back to it
+// on destruction (reuse is stream-ordered), so RAII is safe on every error path.
 template <typename T>
 struct DevBuf {
     tqp_ctx* ctx = nullptr;
@@ -82,12 +91,10 @@ struct DevBuf {
         ctx = c;
         n = count;
         if (count == 0) return;
-        void* q = nullptr;
-        TQP_CUDA(cudaMallocFromPoolAsync(&q, count * sizeof(T), c->pool, c->stream));
-        p = static_cast<T*>(q);
+        p = static_cast<T*>(c->dalloc(count * sizeof(T)));
     }
     void release() {
-        if (p && ctx) cudaFreeAsync(p, ctx->stream);
+        if (p && ctx) ctx->dfree(p);
         p = nullptr;
         n = 0;
     }
@@ -244,4 +251,38 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
+}  // namespace tqp
+
+namespace tqp {
+// ------------------------------------------- TMA bulk copies + mbarriers
+// 1-D bulk copies global -> shared (cp.async.bulk, the TMA engine's non-tensor
+// path) completing on an mbarrier transaction count.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 }  // namespace tqp

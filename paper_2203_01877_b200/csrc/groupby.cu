@@ -6,27 +6,34 @@
 // The paper materialises every step as a whole-tensor op (and names
 // uniqueConsecutive as a bottleneck). Here it is two
 // levels of the same sort-based algorithm:
-//   phase 1 (one kernel, one pass over the input columns): each CTA tile of
-//     2048 rows evaluates the predicates, packs the key columns into one
-//     64-bit key (column 0 most significant, reading R12), radix-sorts its
-//     passing rows by key in shared memory (stable LSD passes with warp
-//     match_any ranking), marks segment boundaries (the unique/inverse step),
-//     and reduces every aggregate per segment in registers/shared memory
-//     (int64 values split into 32-bit halves so partial sums are exact),
-//     emitting one partial record per (tile, distinct key);
+//   phase 1 (persistent kernel, one pass over the referenced columns): every
+//     tile of 1024 rows is streamed into shared memory with TMA bulk copies
+//     (cp.async.bulk, mbarrier completion, double-buffered so tile k+2 loads
+//     while tile k is reduced). The tile's predicates are evaluated, key columns
+//     packed into one 64-bit key (column 0 most significant, reading R12), the
+//     passing rows radix-sorted in shared memory over the bits that vary in the
+//     tile (stable LSD, warp match_any ranking), segment boundaries marked (the
+//     uniqueConsecutive / inverse step) and every distinct (op, expression) pair
+//     reduced per segment in registers, reading the values in sorted order
+//     straight from the staged columns; one partial record per (tile, key);
 //   phase 2: the partial records are radix-sorted by key (sort.cu), segment
 //     boundaries give the final groups, and partials are added into exact
-//     int128 accumulators (64-bit atomics with explicit carry, order
-//     independent => bit-exact), then finalised (AVG = rn(sum / count)).
+//     int128 accumulators (64-bit atomics with explicit carry; integer addition
+//     is associative, so any order gives bit-identical sums), then finalised
+//     (AVG = rn(sum / count), reading R15/R17).
+#include <vector>
+
 #include "internal.h"
 
 struct tqp_groupby_plan {
     int64_t G = 0;
-    int n_keys = 0, n_aggs = 0;
+    int n_keys = 0, n_aggs = 0, n_pairs = 0;
     int kdt[TQP_MAX_KEYS];
     int kshift[TQP_MAX_KEYS];
     int aop[TQP_MAX_AGGS];
-    bool empty_global = false;   // n_keys == 0 and no passing row
+    int apair[TQP_MAX_AGGS];      // aggregate -> (op, expression) pair (-1 for COUNT)
+    int pop[TQP_MAX_AGGS];        // pair op: 0 sum, 1 min, 2 max
+    bool empty_global = false;    // n_keys == 0 and no passing row
     tqp::DevBuf<uint64_t> gkey;
     tqp::DevBuf<int64_t> gcount;
     tqp::DevBuf<uint64_t> glo[TQP_MAX_AGGS];
@@ -38,37 +45,40 @@ namespace tqp {
 namespace {
 constexpr int GNT = 256;
 constexpr int GNW = GNT / 32;
-constexpr int GIPT = 8;
-constexpr int GTILE = GNT * GIPT;   // 2048 rows per tile (fits u16 indices)
+constexpr int GPT = 4;
+constexpr int GTILE = GNT * GPT;   // 1024 rows per tile
+constexpr int MAXU = 16;           // distinct referenced columns
+constexpr int P_SUM = 0, P_MIN = 1, P_MAX = 2;
 
-struct GBArgs {
+struct Phase1Args {
+    int n_ucols;
+    const void* ucol[MAXU];
+    int udt[MAXU];
+    int uoff[MAXU];               // byte offset of the column inside a stage
+    int stage_bytes;
     int n_keys;
-    const void* kcol[TQP_MAX_KEYS];
-    int kdt[TQP_MAX_KEYS];
+    int kcol[TQP_MAX_KEYS];
     int kshift[TQP_MAX_KEYS];
     int n_preds;
-    const void* pcol[TQP_MAX_PREDS];
-    int pdt[TQP_MAX_PREDS];
+    int pcol[TQP_MAX_PREDS];
     int pop[TQP_MAX_PREDS];
     int64_t pval[TQP_MAX_PREDS];
-    int n_aggs;
-    int aop[TQP_MAX_AGGS];
-    int anf[TQP_MAX_AGGS];
-    const void* acol[TQP_MAX_AGGS][3];
-    int adt[TQP_MAX_AGGS][3];
-    int asign[TQP_MAX_AGGS][3];
-    int64_t aadd[TQP_MAX_AGGS][3];
+    int n_pairs;
+    int prop[TQP_MAX_AGGS];
+    int pnf[TQP_MAX_AGGS];
+    int pfc[TQP_MAX_AGGS][3];
+    int psign[TQP_MAX_AGGS][3];
+    int64_t padd[TQP_MAX_AGGS][3];
     int64_t n;
-    // phase-1 partial records
+    int64_t n_tiles;
+    int bulk_ok;
     uint64_t* pkey;
     int64_t* pcount;
-    uint64_t* plo[TQP_MAX_AGGS];   // SUM/AVG: low 64 bits of the int128 partial; MIN/MAX: value
-    int64_t* phi[TQP_MAX_AGGS];    // SUM/AVG: high 64 bits
-    uint64_t* status;
-    unsigned long long* counter;
-    int64_t* P_out;
-    int64_t n_tiles;
-    int* overflow;
+    uint64_t* plo[TQP_MAX_AGGS];
+    int64_t* phi[TQP_MAX_AGGS];
+    unsigned long long* P_counter;
+    int64_t cap;
+    int* overflow;                // bit 0: value overflow, bit 1: partial capacity exceeded
 };
 
 __device__ __forceinline__ bool cmp_op(int64_t x, int op, int64_t v) {
@@ -90,21 +100,12 @@ __device__ __forceinline__ uint64_t key_part(int64_t v, int dt) {
     }
 }
 
-// value = prod_f (add_f + sign_f * col_f[row]) in int64; sets *ovf on overflow.
-__device__ __forceinline__ int64_t agg_value(const GBArgs& a, int ag, int64_t row, int* ovf) {
-    int64_t v = 1;
-    for (int f = 0; f < a.anf[ag]; f++) {
-        const int64_t x = load_as_i64(a.acol[ag][f], a.adt[ag][f], row);
-        const int64_t sx = a.asign[ag][f] < 0 ? -x : x;
-        if (a.asign[ag][f] < 0 && x == INT64_MIN) *ovf = 1;
-        const int64_t t = a.aadd[ag][f] + sx;
-        if (((a.aadd[ag][f] ^ t) & (sx ^ t)) < 0) *ovf = 1;   // signed add overflow
-        const int64_t lo = v * t;
-        const int64_t hi = __mul64hi(v, t);
-        if (hi != (lo >> 63)) *ovf = 1;                       // signed mul overflow
-        v = lo;
+__device__ __forceinline__ int64_t scol(const uint8_t* stage, int off, int dt, int row) {
+    switch (dt) {
+        case TQP_U8: return (int64_t)stage[off + row];
+        case TQP_I32: return (int64_t)reinterpret_cast<const int32_t*>(stage + off)[row];
+        default: return (int64_t)reinterpret_cast<const long long*>(stage + off)[row];
     }
-    return v;
 }
 
 __device__ __forceinline__ uint32_t bscan256(uint32_t v, uint32_t* s_w) {
@@ -122,291 +123,349 @@ __device__ __forceinline__ uint32_t bscan256(uint32_t v, uint32_t* s_w) {
     return add + x - v;
 }
 
-struct GBSmem {
-    uint64_t skey[2][GTILE];        // 32 KB: sort ping-pong; the spare buffer holds per-row values
-    uint64_t acc_lo[GTILE];         // 16 KB: per-segment accumulators
-    int64_t acc_hi[GTILE];          // 16 KB
-    uint16_t sidx[2][GTILE + 2];    // 8 KB: local row of each sorted element / run starts
-    uint16_t inv[GTILE];            // 4 KB: local row -> sorted position
-    uint16_t srun[GTILE];           // 4 KB: segment id of each sorted position
-    uint32_t whist[GNW][256];       // 8 KB: per-warp digit counters
+// exact 128-bit atomic accumulation: the carry out of the low word is detected
+// from the value atomicAdd returns, so the total is exact for any order.
+__device__ __forceinline__ void atomic_add_i128(uint64_t* lo_p, int64_t* hi_p, unsigned __int128 v) {
+    const uint64_t lo = (uint64_t)v;
+    const uint64_t old = atomicAdd((unsigned long long*)lo_p, (unsigned long long)lo);
+    const uint64_t h = (uint64_t)(v >> 64) + ((old + lo < old) ? 1ull : 0ull);
+    if (h) atomicAdd((unsigned long long*)hi_p, (unsigned long long)h);
+}
+
+struct Work {   // shared-memory working set of one tile (after the two column stages)
+    uint64_t skey[2][GTILE];
+    uint16_t sidx[2][GTILE];
+    uint16_t srun[GTILE];
+    uint16_t rstart[GTILE + 2];
+    uint32_t whist[GNW][256];
     uint32_t tstart[256];
     uint32_t s_w[GNW];
-    uint32_t s_cnt[GNW * GIPT];
     uint64_t s_min[GNW], s_max[GNW];
-    int64_t s_tile;
-    uint64_t s_pbase;
+    uint64_t mbar[2];
+    int64_t s_pb;
     uint32_t s_m, s_U;
 };
 
 // One stable LSD pass over positions [0, m) of the tile: rank by the 8-bit digit
-// at `shift` with warp match_any (warp-striped positions keep warp-local order
-// equal to position order), then scatter to dst.
-__device__ __forceinline__ void tile_pass(GBSmem& s, int src, int m, int shift) {
+// at `shift` with warp match_any, then scatter to the other buffer.
+__device__ __forceinline__ void tile_pass(Work& w, int src, int m, int shift) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int dst = src ^ 1;
-    for (int d = lane; d < 256; d += 32) s.whist[warp][d] = 0;
+    for (int d = lane; d < 256; d += 32) w.whist[warp][d] = 0;
     __syncwarp();
-    uint64_t k[GIPT];
-    uint16_t ix[GIPT];
-    uint32_t rk[GIPT];
+    uint64_t k[GPT];
+    uint16_t ix[GPT];
+    uint32_t rk[GPT];
     const unsigned lt = lanemask_lt();
 #pragma unroll
-    for (int i = 0; i < GIPT; i++) {
-        const int q = warp * 32 * GIPT + i * 32 + lane;
+    for (int i = 0; i < GPT; i++) {
+        const int q = warp * 32 * GPT + i * 32 + lane;
         const bool valid = q < m;
-        if (valid) { k[i] = s.skey[src][q]; ix[i] = s.sidx[src][q]; }
+        if (valid) { k[i] = w.skey[src][q]; ix[i] = w.sidx[src][q]; }
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
         if (valid) {
             const uint32_t d = (uint32_t)(k[i] >> shift) & 255u;
             const unsigned peers = __match_any_sync(vm, d);
-            const uint32_t before = s.whist[warp][d];
+            const uint32_t before = w.whist[warp][d];
             rk[i] = before + __popc(peers & lt);
             __syncwarp(vm);
-            if (lane == 31 - __clz(peers)) s.whist[warp][d] = before + __popc(peers);
+            if (lane == 31 - __clz(peers)) w.whist[warp][d] = before + __popc(peers);
             __syncwarp(vm);
         }
     }
     __syncthreads();
     uint32_t cnt = 0;
 #pragma unroll
-    for (int w = 0; w < GNW; w++) {
-        const uint32_t c = s.whist[w][tid];
-        s.whist[w][tid] = cnt;
+    for (int ww = 0; ww < GNW; ww++) {
+        const uint32_t c = w.whist[ww][tid];
+        w.whist[ww][tid] = cnt;
         cnt += c;
     }
-    s.tstart[tid] = bscan256(cnt, s.s_w);
+    w.tstart[tid] = bscan256(cnt, w.s_w);
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < GIPT; i++) {
-        const int q = warp * 32 * GIPT + i * 32 + lane;
+    for (int i = 0; i < GPT; i++) {
+        const int q = warp * 32 * GPT + i * 32 + lane;
         if (q < m) {
             const uint32_t d = (uint32_t)(k[i] >> shift) & 255u;
-            const uint32_t p = s.tstart[d] + s.whist[warp][d] + rk[i];
-            s.skey[dst][p] = k[i];
-            s.sidx[dst][p] = ix[i];
+            const uint32_t p = w.tstart[d] + w.whist[warp][d] + rk[i];
+            w.skey[dst][p] = k[i];
+            w.sidx[dst][p] = ix[i];
         }
     }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(GNT) gb_phase1_kernel(GBArgs a) {
-    extern __shared__ __align__(16) uint8_t smem_raw[];
-    GBSmem& s = *reinterpret_cast<GBSmem*>(smem_raw);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s.s_tile = (int64_t)atomicAdd(a.counter, 1ull);
-    __syncthreads();
-    const int64_t tile = s.s_tile;
-    const int64_t base = tile * GTILE;
-    const unsigned lt = lanemask_lt();
+__device__ __forceinline__ int64_t pair_value(const Phase1Args& a, const uint8_t* st, int j, int row, int& ovf) {
+    int64_t v = 1;
+    for (int f = 0; f < a.pnf[j]; f++) {
+        const int c = a.pfc[j][f];
+        const int64_t x = scol(st, a.uoff[c], a.udt[c], row);
+        const int64_t sx = a.psign[j][f] < 0 ? -x : x;
+        if (a.psign[j][f] < 0 && x == INT64_MIN) ovf = 1;
+        const int64_t t = a.padd[j][f] + sx;
+        if (((a.padd[j][f] ^ t) & (sx ^ t)) < 0) ovf = 1;   // signed add overflow
+        const int64_t lo = v * t;
+        if (__mul64hi(v, t) != (lo >> 63)) ovf = 1;        // signed mul overflow
+        v = lo;
+    }
+    return v;
+}
 
-    // 1. predicates + packed key (rows are warp-striped: local row = warp*256 + i*32 + lane)
-    uint64_t key[GIPT];
-    unsigned bal[GIPT];
+__device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, int64_t t) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t row0 = t * GTILE;
+    const int nrows = (int)min((int64_t)GTILE, a.n - row0);
+    // 1. predicates + packed key; rows r = i*GNT + tid
+    uint64_t key[GPT];
+    unsigned bal[GPT];
     uint64_t kmin = ~0ull, kmax = 0;
+    if (tid == 0) w.s_m = 0;
 #pragma unroll
-    for (int i = 0; i < GIPT; i++) {
-        const int64_t row = base + warp * 32 * GIPT + i * 32 + lane;
-        bool pass = row < a.n;
+    for (int i = 0; i < GPT; i++) {
+        const int r = i * GNT + tid;
+        bool pass = r < nrows;
         key[i] = 0;
         if (pass) {
-            for (int q = 0; q < a.n_preds; q++)
-                pass = pass && cmp_op(load_as_i64(a.pcol[q], a.pdt[q], row), a.pop[q], a.pval[q]);
+            for (int q = 0; q < a.n_preds; q++) {
+                const int c = a.pcol[q];
+                pass = pass & cmp_op(scol(st, a.uoff[c], a.udt[c], r), a.pop[q], a.pval[q]);
+            }
         }
         if (pass) {
             uint64_t kk = 0;
-            for (int c = 0; c < a.n_keys; c++)
-                kk |= key_part(load_as_i64(a.kcol[c], a.kdt[c], row), a.kdt[c]) << a.kshift[c];
+            for (int c = 0; c < a.n_keys; c++) {
+                const int u = a.kcol[c];
+                kk |= key_part(scol(st, a.uoff[u], a.udt[u], r), a.udt[u]) << a.kshift[c];
+            }
             key[i] = kk;
             kmin = min(kmin, kk);
             kmax = max(kmax, kk);
         }
         bal[i] = __ballot_sync(0xffffffffu, pass);
-        if (lane == 0) s.s_cnt[warp * GIPT + i] = __popc(bal[i]);
     }
     for (int o = 16; o > 0; o >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
         kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
     }
-    if (lane == 0) { s.s_min[warp] = kmin; s.s_max[warp] = kmax; }
+    if (lane == 0) { w.s_min[warp] = kmin; w.s_max[warp] = kmax; }
     __syncthreads();
-    if (warp == 0) {   // exclusive scan over the 64 (warp, item) counts in row order
-        const uint32_t c0 = s.s_cnt[2 * lane], c1 = s.s_cnt[2 * lane + 1];
-        uint32_t x = c0 + c1;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        const uint32_t ex = x - c0 - c1;
-        s.s_cnt[2 * lane] = ex;
-        s.s_cnt[2 * lane + 1] = ex + c0;
-        if (lane == 31) s.s_m = x;
-    }
     kmin = ~0ull;
     kmax = 0;
-    for (int w = 0; w < GNW; w++) { kmin = min(kmin, s.s_min[w]); kmax = max(kmax, s.s_max[w]); }
-    __syncthreads();
-    const int m = (int)s.s_m;
-    // 2. compact passing rows (in row order) into sort buffer 0 as (key - kmin, local row)
+    for (int ww = 0; ww < GNW; ww++) { kmin = min(kmin, w.s_min[ww]); kmax = max(kmax, w.s_max[ww]); }
+    // 2. compact passing rows into sort buffer 0 (warp-aggregated slot claims)
+    const unsigned lt = lanemask_lt();
 #pragma unroll
-    for (int i = 0; i < GIPT; i++) {
+    for (int i = 0; i < GPT; i++) {
+        if (!bal[i]) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&w.s_m, (uint32_t)__popc(bal[i]));
+        base = __shfl_sync(0xffffffffu, base, 0);
         if (bal[i] & (1u << lane)) {
-            const uint32_t c = s.s_cnt[warp * GIPT + i] + __popc(bal[i] & lt);
-            s.skey[0][c] = key[i] - kmin;
-            s.sidx[0][c] = (uint16_t)(warp * 32 * GIPT + i * 32 + lane);
+            const uint32_t c = base + __popc(bal[i] & lt);
+            w.skey[0][c] = key[i] - kmin;
+            w.sidx[0][c] = (uint16_t)(i * GNT + tid);
         }
     }
     __syncthreads();
+    const int m = (int)w.s_m;
     // 3. in-tile stable LSD radix sort over the bits that vary in this tile
     const int bits = (m > 0 && kmax != kmin) ? 64 - __clzll(kmax - kmin) : 0;
     const int passes = (bits + 7) / 8;
-    for (int p = 0; p < passes; p++) tile_pass(s, p & 1, m, 8 * p);
+    for (int p = 0; p < passes; p++) tile_pass(w, p & 1, m, 8 * p);
     const int fin = passes & 1;
-    const uint64_t* sk = s.skey[fin];
-    uint64_t* sval = s.skey[fin ^ 1];           // spare buffer: per-row values in sorted order
-    uint16_t* rstart = s.sidx[fin ^ 1];         // spare buffer: segment starts
-    // 4. inverse map and segment boundaries (uniqueConsecutive)
-    for (int p = tid; p < m; p += GNT) s.inv[s.sidx[fin][p]] = (uint16_t)p;
+    const uint64_t* sk = w.skey[fin];
+    const uint16_t* si = w.sidx[fin];
+    // 4. segment boundaries (uniqueConsecutive): blocked positions p = tid*GPT + q
+    const int p0 = tid * GPT;
     uint32_t heads = 0;
 #pragma unroll
-    for (int j = 0; j < GIPT; j++) {
-        const int p = tid * GIPT + j;
+    for (int q = 0; q < GPT; q++) {
+        const int p = p0 + q;
         if (p < m && (p == 0 || sk[p] != sk[p - 1])) heads++;
     }
-    uint32_t hex = bscan256(heads, s.s_w);
+    const uint32_t hex = bscan256(heads, w.s_w);
     {
         uint32_t r = hex;
 #pragma unroll
-        for (int j = 0; j < GIPT; j++) {
-            const int p = tid * GIPT + j;
+        for (int q = 0; q < GPT; q++) {
+            const int p = p0 + q;
             if (p < m) {
-                if (p == 0 || sk[p] != sk[p - 1]) { rstart[r] = (uint16_t)p; r++; }
-                s.srun[p] = (uint16_t)(r - 1);
+                if (p == 0 || sk[p] != sk[p - 1]) { w.rstart[r] = (uint16_t)p; r++; }
+                w.srun[p] = (uint16_t)(r - 1);
             }
         }
-        if (tid == GNT - 1) s.s_U = r;
-    }
-    __syncthreads();
-    const int U = (int)s.s_U;
-    if (tid == 0) rstart[U] = (uint16_t)m;
-    // 5. place of this tile's partial records: decoupled look-back over U
-    if (warp == 0) {
-        const uint64_t e = lookback_warp(a.status, tile, (uint64_t)U, OpAdd(), 0ull);
-        if (lane == 0) {
-            s.s_pbase = e;
-            if (tile == a.n_tiles - 1) *a.P_out = (int64_t)(e + U);
+        if (tid == GNT - 1) {
+            w.s_U = r;
+            w.rstart[r] = (uint16_t)m;
+            int64_t pb = r ? (int64_t)atomicAdd(a.P_counter, (unsigned long long)r) : 0;
+            if (pb + r > a.cap) { atomicOr(a.overflow, 2); pb = -1; }
+            w.s_pb = pb;
         }
     }
     __syncthreads();
-    const int64_t pb = (int64_t)s.s_pbase;
+    const int U = (int)w.s_U;
+    const int64_t pb = w.s_pb;
+    if (U == 0 || pb < 0) return;
+    // 5. partial records: key, count, accumulator init
     for (int u = tid; u < U; u += GNT) {
-        a.pkey[pb + u] = sk[rstart[u]] + kmin;
-        a.pcount[pb + u] = (int64_t)rstart[u + 1] - rstart[u];
+        a.pkey[pb + u] = sk[w.rstart[u]] + kmin;
+        a.pcount[pb + u] = (int64_t)w.rstart[u + 1] - w.rstart[u];
+        for (int j = 0; j < a.n_pairs; j++) {
+            const int op = a.prop[j];
+            a.plo[j][pb + u] = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+            if (op == P_SUM) a.phi[j][pb + u] = 0;
+        }
     }
-    // 6. segmented reduction of every aggregate
+    __syncthreads();
+    // 6. segmented reduction of every (op, expression) pair in sorted order
+    const bool any = p0 < m;
+    const int pl = min(p0 + GPT, m) - 1;
+    const int r0 = any ? w.srun[p0] : -1;
+    const int rl = any ? w.srun[pl] : -1;
+    const int wr0 = __shfl_sync(0xffffffffu, r0, 0);
+    const bool uniform = __all_sync(0xffffffffu, any && r0 == rl && r0 == wr0);
     int ovf = 0;
-    for (int ag = 0; ag < a.n_aggs; ag++) {
-        const int op = a.aop[ag];
-        if (op == TQP_COUNT) continue;
-        const bool is_sum = (op == TQP_SUM || op == TQP_AVG);
-#pragma unroll
-        for (int i = 0; i < GIPT; i++) {
-            if (bal[i] & (1u << lane)) {
-                const int lr = warp * 32 * GIPT + i * 32 + lane;
-                const int64_t row = base + lr;
-                sval[s.inv[lr]] = (uint64_t)agg_value(a, ag, row, &ovf);
-            }
-        }
-        for (int u = tid; u < U; u += GNT) {
-            s.acc_lo[u] = is_sum ? 0ull : (op == TQP_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
-            s.acc_hi[u] = 0;
-        }
-        __syncthreads();
-        // thread t reduces the blocked positions [t*8, t*8+8)
-        const int p0 = tid * GIPT;
-        const int pl = min(p0 + GIPT, m) - 1;
-        const bool any = p0 < m;
-        const int r0 = any ? s.srun[p0] : -1;
-        const int rl = any ? s.srun[pl] : -1;
-        const int wr0 = __shfl_sync(0xffffffffu, r0, 0);
-        const bool uniform = __all_sync(0xffffffffu, any && r0 == rl && r0 == wr0);
-        uint64_t lo = 0;
-        int64_t hi = 0;
-        int64_t mm = op == TQP_MIN ? INT64_MAX : INT64_MIN;
+    for (int j = 0; j < a.n_pairs; j++) {
+        const int op = a.prop[j];
+        uint64_t lo = 0;      // sum of the low 32-bit halves
+        int64_t hi = 0;       // sum of the high 32-bit halves (signed)
+        int64_t mm = op == P_MIN ? INT64_MAX : INT64_MIN;
         int cur = r0;
+        auto flush = [&](int run) {
+            if (op == P_SUM) {
+                const unsigned __int128 v = (unsigned __int128)(((__int128)hi << 32) + (__int128)lo);
+                atomic_add_i128(&a.plo[j][pb + run], &a.phi[j][pb + run], v);
+            } else if (op == P_MIN) {
+                atomicMin((long long*)&a.plo[j][pb + run], (long long)mm);
+            } else {
+                atomicMax((long long*)&a.plo[j][pb + run], (long long)mm);
+            }
+        };
         for (int p = p0; p <= pl; p++) {
-            const int r = s.srun[p];
+            const int r = w.srun[p];
             if (r != cur) {
-                if (is_sum) {
-                    atomicAdd((unsigned long long*)&s.acc_lo[cur], (unsigned long long)lo);
-                    atomicAdd((unsigned long long*)&s.acc_hi[cur], (unsigned long long)hi);
-                } else if (op == TQP_MIN) atomicMin((long long*)&s.acc_lo[cur], (long long)mm);
-                else atomicMax((long long*)&s.acc_lo[cur], (long long)mm);
-                lo = 0; hi = 0; mm = op == TQP_MIN ? INT64_MAX : INT64_MIN;
+                flush(cur);
+                lo = 0;
+                hi = 0;
+                mm = op == P_MIN ? INT64_MAX : INT64_MIN;
                 cur = r;
             }
-            const int64_t v = (int64_t)sval[p];
-            if (is_sum) { lo += (uint64_t)(uint32_t)v; hi += (v >> 32); }
-            else mm = op == TQP_MIN ? min(mm, v) : max(mm, v);
+            const int64_t v = pair_value(a, st, j, si[p], ovf);
+            if (op == P_SUM) { lo += (uint64_t)(uint32_t)v; hi += (v >> 32); }
+            else mm = op == P_MIN ? min(mm, v) : max(mm, v);
         }
         if (uniform) {
             for (int o = 16; o > 0; o >>= 1) {
-                if (is_sum) {
+                if (op == P_SUM) {
                     lo += __shfl_xor_sync(0xffffffffu, lo, o);
                     hi += __shfl_xor_sync(0xffffffffu, hi, o);
                 } else {
-                    const int64_t t = __shfl_xor_sync(0xffffffffu, mm, o);
-                    mm = op == TQP_MIN ? min(mm, t) : max(mm, t);
+                    const int64_t x = __shfl_xor_sync(0xffffffffu, mm, o);
+                    mm = op == P_MIN ? min(mm, x) : max(mm, x);
                 }
             }
+            if (lane == 0) flush(cur);
+        } else if (any) {
+            flush(cur);
         }
-        if (any && (!uniform || lane == 0)) {
-            if (is_sum) {
-                atomicAdd((unsigned long long*)&s.acc_lo[cur], (unsigned long long)lo);
-                atomicAdd((unsigned long long*)&s.acc_hi[cur], (unsigned long long)hi);
-            } else if (op == TQP_MIN) atomicMin((long long*)&s.acc_lo[cur], (long long)mm);
-            else atomicMax((long long*)&s.acc_lo[cur], (long long)mm);
-        }
-        __syncthreads();
-        for (int u = tid; u < U; u += GNT) {
-            if (is_sum) {
-                // exact: value = acc_hi * 2^32 + acc_lo  (|acc_hi| < 2^43, acc_lo < 2^43)
-                const __int128 t = ((__int128)s.acc_hi[u] << 32) + (__int128)s.acc_lo[u];
-                a.plo[ag][pb + u] = (uint64_t)t;
-                a.phi[ag][pb + u] = (int64_t)(t >> 64);
-            } else {
-                a.plo[ag][pb + u] = s.acc_lo[u];
-            }
-        }
-        __syncthreads();
     }
     if (ovf) atomicOr(a.overflow, 1);
 }
 
+__global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* stage[2] = {smem, smem + a.stage_bytes};
+    Work& w = *reinterpret_cast<Work*>(smem + 2 * a.stage_bytes);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        mbar_init(&w.mbar[0], 1);
+        mbar_init(&w.mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto eligible = [&](int64_t t) { return a.bulk_ok && (t + 1) * GTILE <= a.n; };
+    auto issue = [&](int64_t t, int s) {   // thread 0 only
+        mbar_expect_tx(&w.mbar[s], (uint32_t)a.stage_bytes);
+        for (int c = 0; c < a.n_ucols; c++) {
+            const uint32_t es = a.udt[c] == TQP_U8 ? 1 : a.udt[c] == TQP_I32 ? 4 : 8;
+            bulk_g2s(stage[s] + a.uoff[c], (const uint8_t*)a.ucol[c] + t * GTILE * es, GTILE * es, &w.mbar[s]);
+        }
+    };
+    uint32_t uses[2] = {0, 0};
+    for (int s = 0; s < 2; s++) {
+        const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
+        if (t < a.n_tiles && eligible(t)) {
+            if (tid == 0) issue(t, s);
+            uses[s]++;
+        }
+    }
+    for (int64_t k = 0;; k++) {
+        const int64_t t = blockIdx.x + k * gridDim.x;
+        if (t >= a.n_tiles) break;
+        const int s = (int)(k & 1);
+        if (eligible(t)) {
+            mbar_wait(&w.mbar[s], (uses[s] - 1) & 1);
+        } else {   // tail tile or unaligned columns: plain cooperative loads
+            const int64_t row0 = t * GTILE;
+            const int nrows = (int)min((int64_t)GTILE, a.n - row0);
+            for (int c = 0; c < a.n_ucols; c++) {
+                for (int r = tid; r < nrows; r += GNT) {
+                    switch (a.udt[c]) {
+                        case TQP_U8: stage[s][a.uoff[c] + r] = ((const uint8_t*)a.ucol[c])[row0 + r]; break;
+                        case TQP_I32:
+                            reinterpret_cast<int32_t*>(stage[s] + a.uoff[c])[r] = ((const int32_t*)a.ucol[c])[row0 + r];
+                            break;
+                        default:
+                            reinterpret_cast<long long*>(stage[s] + a.uoff[c])[r] =
+                                ((const long long*)a.ucol[c])[row0 + r];
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        process_tile(a, stage[s], w, t);
+        __syncthreads();   // every thread is done with stage s
+        const int64_t t2 = t + 2 * (int64_t)gridDim.x;
+        if (t2 < a.n_tiles && eligible(t2)) {
+            if (tid == 0) {
+                fence_proxy_async();
+                issue(t2, s);
+            }
+            uses[s]++;
+        }
+    }
+}
+
 // Phase 2a: group ids over the sorted partial keys (segment boundaries).
-__global__ void __launch_bounds__(GNT) gb_gid_kernel(const uint64_t* __restrict__ sk, int64_t P, uint32_t* gid,
+constexpr int QNT = 256;
+constexpr int QNW = QNT / 32;
+constexpr int QIPT = 8;
+constexpr int QTILE = QNT * QIPT;
+
+__global__ void __launch_bounds__(QNT) gb_gid_kernel(const uint64_t* __restrict__ sk, int64_t P, uint32_t* gid,
                                                      uint64_t* gkey, int64_t* G_out, uint64_t* status,
                                                      unsigned long long* counter, int64_t n_tiles) {
     __shared__ int64_t s_tile;
-    __shared__ uint32_t s_cnt[GIPT * GNW];
+    __shared__ uint32_t s_cnt[QIPT * QNW];
     __shared__ uint64_t s_excl;
     __shared__ uint32_t s_tot;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tile = take_tile(counter, &s_tile);
-    const int64_t base = tile * GTILE;
-    unsigned bal[GIPT];
-    uint64_t k[GIPT];
+    const int64_t base = tile * QTILE;
+    unsigned bal[QIPT];
+    uint64_t k[QIPT];
 #pragma unroll
-    for (int i = 0; i < GIPT; i++) {
-        const int64_t p = base + i * GNT + tid;
+    for (int i = 0; i < QIPT; i++) {
+        const int64_t p = base + i * QNT + tid;
         bool head = false;
         if (p < P) { k[i] = sk[p]; head = p == 0 || sk[p - 1] != k[i]; }
         bal[i] = __ballot_sync(0xffffffffu, head);
-        if (lane == 0) s_cnt[i * GNW + warp] = __popc(bal[i]);
+        if (lane == 0) s_cnt[i * QNW + warp] = __popc(bal[i]);
     }
     __syncthreads();
     if (warp == 0) {
-        constexpr int PER = GIPT * GNW / 32;
+        constexpr int PER = QIPT * QNW / 32;
         uint32_t c[PER], local = 0;
 #pragma unroll
         for (int j = 0; j < PER; j++) { c[j] = s_cnt[lane * PER + j]; local += c[j]; }
@@ -426,10 +485,10 @@ __global__ void __launch_bounds__(GNT) gb_gid_kernel(const uint64_t* __restrict_
     const int64_t excl = (int64_t)s_excl;
     const unsigned le = lanemask_lt() | (1u << lane);
 #pragma unroll
-    for (int i = 0; i < GIPT; i++) {
-        const int64_t p = base + i * GNT + tid;
+    for (int i = 0; i < QIPT; i++) {
+        const int64_t p = base + i * QNT + tid;
         if (p < P) {
-            const int64_t g = excl + s_cnt[i * GNW + warp] + __popc(bal[i] & le) - 1;
+            const int64_t g = excl + s_cnt[i * QNW + warp] + __popc(bal[i] & le) - 1;
             gid[p] = (uint32_t)g;
             if (bal[i] & (1u << lane)) gkey[g] = k[i];
         }
@@ -438,8 +497,8 @@ __global__ void __launch_bounds__(GNT) gb_gid_kernel(const uint64_t* __restrict_
 }
 
 struct AccArgs {
-    int n_aggs;
-    int aop[TQP_MAX_AGGS];
+    int n_pairs;
+    int pop[TQP_MAX_AGGS];
     const uint64_t* plo[TQP_MAX_AGGS];
     const int64_t* phi[TQP_MAX_AGGS];
     uint64_t* glo[TQP_MAX_AGGS];
@@ -451,18 +510,9 @@ struct AccArgs {
     int64_t P;
 };
 
-// exact 128-bit atomic accumulation: the carry out of the low word is detected
-// from the value atomicAdd returns, so the total is exact for any order.
-__device__ __forceinline__ void atomic_add_i128(uint64_t* lo_p, int64_t* hi_p, uint64_t lo, int64_t hi) {
-    const uint64_t old = atomicAdd((unsigned long long*)lo_p, (unsigned long long)lo);
-    const int64_t carry = (old + lo < old) ? 1 : 0;
-    const int64_t h = hi + carry;
-    if (h) atomicAdd((unsigned long long*)hi_p, (unsigned long long)h);
-}
-
-__global__ void __launch_bounds__(GNT) gb_acc_kernel(AccArgs a) {
+__global__ void __launch_bounds__(QNT) gb_acc_kernel(AccArgs a) {
     const int lane = threadIdx.x & 31;
-    for (int64_t p0 = blockIdx.x * (int64_t)GNT; p0 < a.P; p0 += (int64_t)gridDim.x * GNT) {
+    for (int64_t p0 = blockIdx.x * (int64_t)QNT; p0 < a.P; p0 += (int64_t)gridDim.x * QNT) {
         const int64_t p = p0 + threadIdx.x;
         const bool valid = p < a.P;
         const uint32_t rec = valid ? a.perm[p] : 0;
@@ -476,44 +526,41 @@ __global__ void __launch_bounds__(GNT) gb_acc_kernel(AccArgs a) {
         } else if (valid) {
             atomicAdd((unsigned long long*)&a.gcount[g], (unsigned long long)cnt);
         }
-        for (int ag = 0; ag < a.n_aggs; ag++) {
-            const int op = a.aop[ag];
-            if (op == TQP_COUNT) continue;
-            if (op == TQP_SUM || op == TQP_AVG) {
+        for (int j = 0; j < a.n_pairs; j++) {
+            const int op = a.pop[j];
+            if (op == P_SUM) {
                 unsigned __int128 v = 0;
-                if (valid) v = ((unsigned __int128)(uint64_t)a.phi[ag][rec] << 64) | a.plo[ag][rec];
+                if (valid) v = ((unsigned __int128)(uint64_t)a.phi[j][rec] << 64) | a.plo[j][rec];
                 if (uniform) {
                     for (int o = 16; o > 0; o >>= 1) {
                         const uint64_t l = __shfl_xor_sync(0xffffffffu, (uint64_t)v, o);
                         const uint64_t h = __shfl_xor_sync(0xffffffffu, (uint64_t)(v >> 64), o);
                         v += ((unsigned __int128)h << 64) | l;
                     }
-                    if (lane == 0) atomic_add_i128(&a.glo[ag][g], &a.ghi[ag][g], (uint64_t)v, (int64_t)(v >> 64));
+                    if (lane == 0) atomic_add_i128(&a.glo[j][g], &a.ghi[j][g], v);
                 } else if (valid) {
-                    atomic_add_i128(&a.glo[ag][g], &a.ghi[ag][g], (uint64_t)v, (int64_t)(v >> 64));
+                    atomic_add_i128(&a.glo[j][g], &a.ghi[j][g], v);
                 }
             } else {
-                int64_t v = valid ? (int64_t)a.plo[ag][rec] : (op == TQP_MIN ? INT64_MAX : INT64_MIN);
+                int64_t v = valid ? (int64_t)a.plo[j][rec] : (op == P_MIN ? INT64_MAX : INT64_MIN);
                 if (uniform) {
                     for (int o = 16; o > 0; o >>= 1) {
-                        const int64_t t = __shfl_xor_sync(0xffffffffu, v, o);
-                        v = op == TQP_MIN ? min(v, t) : max(v, t);
+                        const int64_t x = __shfl_xor_sync(0xffffffffu, v, o);
+                        v = op == P_MIN ? min(v, x) : max(v, x);
                     }
                 }
                 if (valid && (!uniform || lane == 0)) {
-                    if (op == TQP_MIN) atomicMin((long long*)&a.glo[ag][g], (long long)v);
-                    else atomicMax((long long*)&a.glo[ag][g], (long long)v);
+                    if (op == P_MIN) atomicMin((long long*)&a.glo[j][g], (long long)v);
+                    else atomicMax((long long*)&a.glo[j][g], (long long)v);
                 }
             }
         }
     }
 }
 
-__global__ void gb_init_kernel(uint64_t* lo, int64_t* hi, int64_t n, uint64_t init) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+__global__ void gb_init_kernel(uint64_t* lo, int64_t n, uint64_t init) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         lo[i] = init;
-        if (hi) hi[i] = 0;
-    }
 }
 
 // correctly rounded signed int128 -> double
@@ -544,6 +591,7 @@ struct FinArgs {
     int kshift[TQP_MAX_KEYS];
     void* kout[TQP_MAX_KEYS];
     int aop[TQP_MAX_AGGS];
+    int apair[TQP_MAX_AGGS];
     void* rout[TQP_MAX_AGGS];
     const uint64_t* glo[TQP_MAX_AGGS];
     const int64_t* ghi[TQP_MAX_AGGS];
@@ -568,9 +616,15 @@ __global__ void gb_finalize_kernel(FinArgs a) {
         for (int ag = 0; ag < a.n_aggs; ag++) {
             if (!a.rout[ag]) continue;
             const int op = a.aop[ag];
-            const uint64_t lo = a.empty_global ? (op == TQP_MIN ? (uint64_t)INT64_MAX : op == TQP_MAX ? (uint64_t)INT64_MIN : 0)
-                                               : (op == TQP_COUNT ? 0 : a.glo[ag][g]);
-            const int64_t hi = (a.empty_global || op == TQP_COUNT || op == TQP_MIN || op == TQP_MAX) ? 0 : a.ghi[ag][g];
+            const int j = a.apair[ag];
+            uint64_t lo = 0;
+            int64_t hi = 0;
+            if (op == TQP_MIN) lo = (uint64_t)INT64_MAX;
+            if (op == TQP_MAX) lo = (uint64_t)INT64_MIN;
+            if (!a.empty_global && j >= 0) {
+                lo = a.glo[j][g];
+                if (op == TQP_SUM || op == TQP_AVG) hi = a.ghi[j][g];
+            }
             switch (op) {
                 case TQP_SUM:
                     ((uint64_t*)a.rout[ag])[2 * g] = lo;
@@ -587,6 +641,104 @@ __global__ void gb_finalize_kernel(FinArgs a) {
         }
     }
 }
+
+struct Partials {   // phase-1 output / phase-2 input
+    DevBuf<uint64_t> pkey;
+    DevBuf<int64_t> pcount;
+    DevBuf<uint64_t> plo[TQP_MAX_AGGS];
+    DevBuf<int64_t> phi[TQP_MAX_AGGS];
+    int64_t P = 0;
+};
+
+// Phase 2: global sort of partial keys, segment ids, exact accumulation.
+void phase2(tqp_ctx* ctx, tqp_groupby_plan* PL, Partials& pr) {
+    const int64_t P = pr.P;
+    SortOut so;
+    so.want_perm32 = true;
+    DevBuf<uint64_t> sk(ctx, P);
+    so.sorted_u = sk.get();
+    radix_sort(ctx, pr.pkey.get(), DT_U64, P, false, so);
+    DevBuf<uint32_t> gid(ctx, P);
+    DevBuf<int64_t> Gd(ctx, 1);
+    Gd.zero();
+    PL->gkey.alloc(ctx, P);
+    {
+        const int64_t t2 = ceil_div(P, QTILE);
+        DevBuf<uint64_t> status(ctx, t2);
+        DevBuf<unsigned long long> counter(ctx, 1);
+        status.zero();
+        counter.zero();
+        launch(ctx, "tqp_groupby_gid", gb_gid_kernel, dim3((unsigned)t2), dim3(QNT), 0, sk.get(), P, gid.get(),
+               PL->gkey.get(), Gd.get(), status.get(), counter.get(), t2);
+        ctx->add_bytes("tqp_groupby_gid", 12.0 * (double)P);
+    }
+    AccArgs c{};
+    c.n_pairs = PL->n_pairs;
+    PL->gcount.alloc(ctx, P);
+    PL->gcount.zero();
+    const int ig = (int)std::min<int64_t>(ceil_div(P, 256), (int64_t)ctx->num_sms * 8);
+    double rec = 8;
+    for (int j = 0; j < PL->n_pairs; j++) {
+        c.pop[j] = PL->pop[j];
+        c.plo[j] = pr.plo[j].get();
+        c.phi[j] = pr.phi[j].get();
+        PL->glo[j].alloc(ctx, P);
+        c.glo[j] = PL->glo[j].get();
+        if (PL->pop[j] == P_SUM) {
+            PL->ghi[j].alloc(ctx, P);
+            c.ghi[j] = PL->ghi[j].get();
+            PL->glo[j].zero();
+            PL->ghi[j].zero();
+            rec += 16;
+        } else {
+            launch(ctx, "tqp_groupby_init", gb_init_kernel, dim3(ig), dim3(256), 0, PL->glo[j].get(), P,
+                   PL->pop[j] == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+            rec += 8;
+        }
+    }
+    c.pcount = pr.pcount.get();
+    c.gcount = PL->gcount.get();
+    c.perm = so.perm32.get();
+    c.gid = gid.get();
+    c.P = P;
+    const int ag = (int)std::min<int64_t>(ceil_div(P, QNT), (int64_t)ctx->num_sms * 8);
+    launch(ctx, "tqp_groupby_accumulate", gb_acc_kernel, dim3(ag), dim3(QNT), 0, c);
+    ctx->add_bytes("tqp_groupby_accumulate", (rec + 8) * (double)P);
+    int64_t G = 0;
+    read_back(ctx, &G, Gd.get(), 8);
+    PL->G = G;
+}
+
+// Distinct (op, expression) pairs: SUM and AVG of the same expression share one.
+void make_pairs(tqp_groupby_plan* PL, const tqp_agg* aggs, int n_aggs, int (*pf)[3], int (*ps)[3],
+                int64_t (*pa)[3], int* pnf) {
+    PL->n_pairs = 0;
+    for (int g = 0; g < n_aggs; g++) {
+        const int op = aggs[g].op;
+        PL->aop[g] = op;
+        if (op == TQP_COUNT) { PL->apair[g] = -1; continue; }
+        const int pop = (op == TQP_SUM || op == TQP_AVG) ? P_SUM : op == TQP_MIN ? P_MIN : P_MAX;
+        int found = -1;
+        for (int j = 0; j < PL->n_pairs && found < 0; j++) {
+            if (PL->pop[j] != pop || pnf[j] != aggs[g].n_factors) continue;
+            bool same = true;
+            for (int f = 0; f < pnf[j]; f++)
+                same = same && pf[j][f] == aggs[g].col[f] && ps[j][f] == aggs[g].sign[f] && pa[j][f] == aggs[g].add[f];
+            if (same) found = j;
+        }
+        if (found < 0) {
+            found = PL->n_pairs++;
+            PL->pop[found] = pop;
+            pnf[found] = aggs[g].n_factors;
+            for (int f = 0; f < pnf[found]; f++) {
+                pf[found][f] = aggs[g].col[f];
+                ps[found][f] = aggs[g].sign[f];
+                pa[found][f] = aggs[g].add[f];
+            }
+        }
+        PL->apair[g] = found;
+    }
+}
 }  // namespace
 
 tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, const int32_t* key_idx,
@@ -597,164 +749,131 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         fail(TQP_ERR_INVALID_ARGUMENT, "groupby: bad sizes");
     if (n >= (int64_t(1) << 40)) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: n too large");
     for (int c = 0; c < n_cols; c++) check_col(cols[c], n, "groupby column");
-    GBArgs a{};
-    a.n = n;
-    a.n_keys = n_keys;
-    int off = 0;
-    for (int k = n_keys - 1; k >= 0; k--) {   // column 0 most significant
-        const int c = key_idx[k];
-        if (c < 0 || c >= n_cols) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: key column");
-        a.kcol[k] = cols[c].data;
-        a.kdt[k] = cols[c].dtype;
-        a.kshift[k] = off;
-        off += 8 * (int)dtype_size(cols[c].dtype);
-    }
-    if (off > 64) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: packed key wider than 64 bits");
-    a.n_preds = n_preds;
-    for (int q = 0; q < n_preds; q++) {
+    for (int k = 0; k < n_keys; k++)
+        if (key_idx[k] < 0 || key_idx[k] >= n_cols) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: key column");
+    for (int q = 0; q < n_preds; q++)
         if (preds[q].col < 0 || preds[q].col >= n_cols || preds[q].op < TQP_LT || preds[q].op > TQP_NE)
             fail(TQP_ERR_INVALID_ARGUMENT, "groupby: predicate");
-        a.pcol[q] = cols[preds[q].col].data;
-        a.pdt[q] = cols[preds[q].col].dtype;
-        a.pop[q] = preds[q].op;
-        a.pval[q] = preds[q].value;
-    }
-    a.n_aggs = n_aggs;
     for (int g = 0; g < n_aggs; g++) {
         if (aggs[g].op < TQP_SUM || aggs[g].op > TQP_AVG || aggs[g].n_factors < 0 || aggs[g].n_factors > 3)
             fail(TQP_ERR_INVALID_ARGUMENT, "groupby: aggregate");
-        a.aop[g] = aggs[g].op;
-        a.anf[g] = aggs[g].op == TQP_COUNT ? 0 : aggs[g].n_factors;
-        for (int f = 0; f < a.anf[g]; f++) {
-            const int c = aggs[g].col[f];
-            if (c < 0 || c >= n_cols || (aggs[g].sign[f] != 1 && aggs[g].sign[f] != -1))
+        if (aggs[g].op == TQP_COUNT) continue;
+        for (int f = 0; f < aggs[g].n_factors; f++)
+            if (aggs[g].col[f] < 0 || aggs[g].col[f] >= n_cols || (aggs[g].sign[f] != 1 && aggs[g].sign[f] != -1))
                 fail(TQP_ERR_INVALID_ARGUMENT, "groupby: aggregate factor");
-            a.acol[g][f] = cols[c].data;
-            a.adt[g][f] = cols[c].dtype;
-            a.asign[g][f] = aggs[g].sign[f];
-            a.aadd[g][f] = aggs[g].add[f];
-        }
     }
+    Phase1Args a{};
+    a.n = n;
+    // distinct referenced columns (one stage slot each)
+    std::vector<int> ucols;
+    auto uidx = [&](int c) {
+        for (size_t i = 0; i < ucols.size(); i++) if (ucols[i] == c) return (int)i;
+        ucols.push_back(c);
+        return (int)ucols.size() - 1;
+    };
     auto* PL = new tqp_groupby_plan();
     try {
         PL->n_keys = n_keys;
         PL->n_aggs = n_aggs;
-        for (int k = 0; k < n_keys; k++) { PL->kdt[k] = a.kdt[k]; PL->kshift[k] = a.kshift[k]; }
-        for (int g = 0; g < n_aggs; g++) PL->aop[g] = a.aop[g];
-
-        // ---- phase 1: per-tile sort + segmented reduce -> partial records
+        int off = 0;
+        a.n_keys = n_keys;
+        for (int k = n_keys - 1; k >= 0; k--) {   // column 0 most significant
+            const int c = key_idx[k];
+            a.kcol[k] = uidx(c);
+            a.kshift[k] = off;
+            PL->kdt[k] = cols[c].dtype;
+            PL->kshift[k] = off;
+            off += 8 * (int)dtype_size(cols[c].dtype);
+        }
+        if (off > 64) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: packed key wider than 64 bits");
+        a.n_preds = n_preds;
+        for (int q = 0; q < n_preds; q++) {
+            a.pcol[q] = uidx(preds[q].col);
+            a.pop[q] = preds[q].op;
+            a.pval[q] = preds[q].value;
+        }
+        int pf[TQP_MAX_AGGS][3], ps[TQP_MAX_AGGS][3], pnf[TQP_MAX_AGGS];
+        int64_t pa[TQP_MAX_AGGS][3];
+        make_pairs(PL, aggs, n_aggs, pf, ps, pa, pnf);
+        a.n_pairs = PL->n_pairs;
+        for (int j = 0; j < PL->n_pairs; j++) {
+            a.prop[j] = PL->pop[j];
+            a.pnf[j] = pnf[j];
+            for (int f = 0; f < pnf[j]; f++) {
+                a.pfc[j][f] = uidx(pf[j][f]);
+                a.psign[j][f] = ps[j][f];
+                a.padd[j][f] = pa[j][f];
+            }
+        }
+        if ((int)ucols.size() > MAXU) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: more than 16 distinct columns");
+        a.n_ucols = (int)ucols.size();
+        int sb = 0;
+        bool aligned = true;
+        for (int i = 0; i < a.n_ucols; i++) {
+            a.ucol[i] = cols[ucols[i]].data;
+            a.udt[i] = cols[ucols[i]].dtype;
+            a.uoff[i] = sb;
+            sb += GTILE * (int)dtype_size(a.udt[i]);
+            aligned = aligned && ((uintptr_t)a.ucol[i] % 16 == 0);
+        }
+        a.stage_bytes = std::max(sb, 16);
+        a.bulk_ok = (aligned && a.n_ucols > 0) ? 1 : 0;
         const int64_t tiles = ceil_div(n, GTILE);
-        const int64_t cap = std::max<int64_t>(n, 1);
-        DevBuf<uint64_t> pkey(ctx, cap);
-        DevBuf<int64_t> pcount(ctx, cap);
-        DevBuf<uint64_t> plo[TQP_MAX_AGGS];
-        DevBuf<int64_t> phi[TQP_MAX_AGGS];
-        for (int g = 0; g < n_aggs; g++) {
-            if (a.aop[g] == TQP_COUNT) continue;
-            plo[g].alloc(ctx, cap);
-            a.plo[g] = plo[g].get();
-            if (a.aop[g] == TQP_SUM || a.aop[g] == TQP_AVG) { phi[g].alloc(ctx, cap); a.phi[g] = phi[g].get(); }
-        }
-        DevBuf<int64_t> scal(ctx, 2);   // P, G
+        a.n_tiles = tiles;
+
+        // ---- phase 1 (retried once with full capacity if the partial estimate is exceeded)
+        Partials pr;
+        DevBuf<unsigned long long> Pc(ctx, 1);
         DevBuf<int> ovf(ctx, 1);
-        scal.zero();
-        ovf.zero();
-        a.pkey = pkey.get();
-        a.pcount = pcount.get();
-        a.P_out = scal.get();
-        a.overflow = ovf.get();
-        if (n > 0) {
-            DevBuf<uint64_t> status(ctx, tiles);
-            DevBuf<unsigned long long> counter(ctx, 1);
-            status.zero();
-            counter.zero();
-            a.status = status.get();
-            a.counter = counter.get();
-            a.n_tiles = tiles;
-            const size_t sm = sizeof(GBSmem);
-            set_smem(gb_phase1_kernel, sm);
-            launch(ctx, "tqp_groupby_tile", gb_phase1_kernel, dim3((unsigned)tiles), dim3(GNT), sm, a);
-        }
-        int64_t P = 0;
-        {
-            int64_t h[2];
+        int64_t cap = std::min<int64_t>(std::max<int64_t>(n, 1), std::max<int64_t>(tiles * 64, 1 << 16));
+        for (int attempt = 0; attempt < 2; attempt++) {
+            pr.pkey.alloc(ctx, cap);
+            pr.pcount.alloc(ctx, cap);
+            for (int j = 0; j < PL->n_pairs; j++) {
+                pr.plo[j].alloc(ctx, cap);
+                if (PL->pop[j] == P_SUM) pr.phi[j].alloc(ctx, cap);
+                a.plo[j] = pr.plo[j].get();
+                a.phi[j] = pr.phi[j].get();
+            }
+            a.pkey = pr.pkey.get();
+            a.pcount = pr.pcount.get();
+            a.cap = cap;
+            Pc.zero();
+            ovf.zero();
+            a.P_counter = Pc.get();
+            a.overflow = ovf.get();
+            if (n > 0) {
+                const size_t smem = 2 * (size_t)a.stage_bytes + sizeof(Work);
+                if (smem > 227 * 1024) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: referenced columns too wide");
+                set_smem(gb_phase1_kernel, smem);
+                int occ = 1;
+                TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_phase1_kernel, GNT, smem));
+                const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
+                launch(ctx, "tqp_groupby_tile", gb_phase1_kernel, dim3((unsigned)grid), dim3(GNT), smem, a);
+            }
+            int64_t h[2] = {0, 0};
+            read_back(ctx, &h[0], Pc.get(), 8);
             int o = 0;
-            read_back(ctx, h, scal.get(), 16);
             read_back(ctx, &o, ovf.get(), 4);
-            if (o) fail(TQP_ERR_OVERFLOW, "groupby: int64 overflow in an aggregate expression");
-            P = h[0];
-            // distinct referenced columns read once; partial records written
-            double in = 0;
-            std::vector<const void*> seen;
-            auto note = [&](const void* d, int dt) {
-                for (auto x : seen) if (x == d) return;
-                seen.push_back(d);
-                in += (double)dtype_size(dt);
-            };
-            for (int k = 0; k < n_keys; k++) note(a.kcol[k], a.kdt[k]);
-            for (int q = 0; q < n_preds; q++) note(a.pcol[q], a.pdt[q]);
-            for (int g = 0; g < n_aggs; g++)
-                for (int f = 0; f < a.anf[g]; f++) note(a.acol[g][f], a.adt[g][f]);
-            double rec = 16;
-            for (int g = 0; g < n_aggs; g++)
-                rec += a.aop[g] == TQP_COUNT ? 0 : (a.aop[g] == TQP_SUM || a.aop[g] == TQP_AVG) ? 16 : 8;
-            if (n > 0) ctx->add_bytes("tqp_groupby_tile", in * (double)n + rec * (double)P);
+            if (o & 1) fail(TQP_ERR_OVERFLOW, "groupby: int64 overflow in an aggregate expression");
+            pr.P = h[0];
+            if (!(o & 2)) break;
+            cap = std::max<int64_t>(n, 1);   // more distinct keys per tile than estimated: full capacity
         }
-        // ---- phase 2: sort partial keys, segment, accumulate exactly
-        if (P == 0) {
+        {   // algorithmic bytes: distinct referenced columns read once, partial records written
+            double in = 0;
+            for (int i = 0; i < a.n_ucols; i++) in += (double)dtype_size(a.udt[i]);
+            double rec = 16;
+            for (int j = 0; j < PL->n_pairs; j++) rec += PL->pop[j] == P_SUM ? 16 : 8;
+            if (n > 0) ctx->add_bytes("tqp_groupby_tile", in * (double)n + rec * (double)pr.P);
+        }
+        if (pr.P == 0) {
             PL->G = n_keys == 0 ? 1 : 0;
             PL->empty_global = n_keys == 0;
             *n_groups_host = PL->G;
             return PL;
         }
-        SortOut so;
-        so.want_perm32 = true;
-        DevBuf<uint64_t> sk(ctx, P);
-        so.sorted_u = sk.get();
-        radix_sort(ctx, pkey.get(), DT_U64, P, false, so);
-        DevBuf<uint32_t> gid(ctx, P);
-        PL->gkey.alloc(ctx, P);
-        {
-            const int64_t t2 = ceil_div(P, GTILE);
-            DevBuf<uint64_t> status(ctx, t2);
-            DevBuf<unsigned long long> counter(ctx, 1);
-            status.zero();
-            counter.zero();
-            launch(ctx, "tqp_groupby_gid", gb_gid_kernel, dim3((unsigned)t2), dim3(GNT), 0, sk.get(), P, gid.get(),
-                   PL->gkey.get(), scal.get() + 1, status.get(), counter.get(), t2);
-        }
-        AccArgs c{};
-        c.n_aggs = n_aggs;
-        PL->gcount.alloc(ctx, P);
-        PL->gcount.zero();
-        const int ig = (int)std::min<int64_t>(ceil_div(P, 256), (int64_t)ctx->num_sms * 8);
-        for (int g = 0; g < n_aggs; g++) {
-            c.aop[g] = a.aop[g];
-            if (a.aop[g] == TQP_COUNT) continue;
-            c.plo[g] = plo[g].get();
-            c.phi[g] = phi[g].get();
-            PL->glo[g].alloc(ctx, P);
-            c.glo[g] = PL->glo[g].get();
-            if (a.aop[g] == TQP_SUM || a.aop[g] == TQP_AVG) {
-                PL->ghi[g].alloc(ctx, P);
-                c.ghi[g] = PL->ghi[g].get();
-                PL->glo[g].zero();
-                PL->ghi[g].zero();
-            } else {
-                launch(ctx, "tqp_groupby_init", gb_init_kernel, dim3(ig), dim3(256), 0, PL->glo[g].get(),
-                       (int64_t*)nullptr, P, a.aop[g] == TQP_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
-            }
-        }
-        c.pcount = pcount.get();
-        c.gcount = PL->gcount.get();
-        c.perm = so.perm32.get();
-        c.gid = gid.get();
-        c.P = P;
-        const int ag = (int)std::min<int64_t>(ceil_div(P, GNT), (int64_t)ctx->num_sms * 8);
-        launch(ctx, "tqp_groupby_accumulate", gb_acc_kernel, dim3(ag), dim3(GNT), 0, c);
-        int64_t h[2];
-        read_back(ctx, h, scal.get(), 16);
-        PL->G = h[1];
+        phase2(ctx, PL, pr);
         *n_groups_host = PL->G;
         return PL;
     } catch (...) {
@@ -775,9 +894,12 @@ void groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* PL, void* const* keys_o
     }
     for (int g = 0; g < PL->n_aggs; g++) {
         f.aop[g] = PL->aop[g];
+        f.apair[g] = PL->apair[g];
         f.rout[g] = results_out ? results_out[g] : nullptr;
-        f.glo[g] = PL->glo[g].get();
-        f.ghi[g] = PL->ghi[g].get();
+    }
+    for (int j = 0; j < PL->n_pairs; j++) {
+        f.glo[j] = PL->glo[j].get();
+        f.ghi[j] = PL->ghi[j].get();
     }
     f.gkey = PL->gkey.get();
     f.gcount = PL->gcount.get();
@@ -788,5 +910,106 @@ void groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* PL, void* const* keys_o
 }
 
 void groupby_release(tqp_ctx*, tqp_groupby_plan* PL) { delete PL; }
+
+namespace {
+struct MergeArgs {
+    int n_keys;
+    const void* kcol[TQP_MAX_KEYS];
+    int kdt[TQP_MAX_KEYS];
+    int kshift[TQP_MAX_KEYS];
+    int n_pairs;
+    int pop[TQP_MAX_AGGS];
+    const void* src[TQP_MAX_AGGS];   // SUM pair: int128 (lo, hi) rows; MIN/MAX: int64 rows
+    uint64_t* plo[TQP_MAX_AGGS];
+    int64_t* phi[TQP_MAX_AGGS];
+    uint64_t* pkey;
+    int64_t m;
+};
+
+__global__ void gb_merge_pack_kernel(MergeArgs a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.m; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t kk = 0;
+        for (int c = 0; c < a.n_keys; c++) kk |= key_part(load_as_i64(a.kcol[c], a.kdt[c], i), a.kdt[c]) << a.kshift[c];
+        a.pkey[i] = kk;
+        for (int j = 0; j < a.n_pairs; j++) {
+            if (a.pop[j] == P_SUM) {
+                a.plo[j][i] = ((const uint64_t*)a.src[j])[2 * i];
+                a.phi[j][i] = ((const int64_t*)a.src[j])[2 * i + 1];
+            } else {
+                a.plo[j][i] = ((const uint64_t*)a.src[j])[i];
+            }
+        }
+    }
+}
+}  // namespace
+
+// Merge of partial group-by results (e.g. one fetch output per rank, concatenated):
+// partial row i has key columns key_cols[k][i], COUNT(*) counts[i], and per
+// aggregate a partial[a][i] (SUM and AVG: the int128 SUM of the aggregate's
+// expression; MIN / MAX: int64; COUNT: ignored). Phase 2 of the group-by
+// (global radix sort of packed keys, segment ids, exact int128 merge) is
+// applied; AVG is recomputed from the merged SUM and COUNT.
+tqp_groupby_plan* groupby_merge(tqp_ctx* ctx, int64_t m, const tqp_col* key_cols, int n_keys, const tqp_agg* aggs,
+                                int n_aggs, const void* const* partial, const int64_t* counts, int64_t* n_groups_host) {
+    if (m < 0 || n_keys < 0 || n_keys > TQP_MAX_KEYS || n_aggs < 0 || n_aggs > TQP_MAX_AGGS)
+        fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: bad sizes");
+    if (m > 0 && !counts) fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: null counts");
+    for (int k = 0; k < n_keys; k++) check_col(key_cols[k], m, "groupby_merge key");
+    for (int g = 0; g < n_aggs; g++)
+        if (aggs[g].op < TQP_SUM || aggs[g].op > TQP_AVG || aggs[g].n_factors < 0 || aggs[g].n_factors > 3)
+            fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: aggregate");
+    auto* PL = new tqp_groupby_plan();
+    try {
+        PL->n_keys = n_keys;
+        PL->n_aggs = n_aggs;
+        MergeArgs a{};
+        a.n_keys = n_keys;
+        a.m = m;
+        int off = 0;
+        for (int k = n_keys - 1; k >= 0; k--) {
+            a.kcol[k] = key_cols[k].data;
+            a.kdt[k] = key_cols[k].dtype;
+            a.kshift[k] = off;
+            PL->kdt[k] = key_cols[k].dtype;
+            PL->kshift[k] = off;
+            off += 8 * (int)dtype_size(key_cols[k].dtype);
+        }
+        if (off > 64) fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: packed key wider than 64 bits");
+        int pf[TQP_MAX_AGGS][3], ps[TQP_MAX_AGGS][3], pnf[TQP_MAX_AGGS];
+        int64_t pa[TQP_MAX_AGGS][3];
+        make_pairs(PL, aggs, n_aggs, pf, ps, pa, pnf);
+        Partials pr;
+        pr.P = m;
+        if (m == 0) {
+            PL->G = n_keys == 0 ? 1 : 0;
+            PL->empty_global = n_keys == 0;
+            *n_groups_host = PL->G;
+            return PL;
+        }
+        pr.pkey.alloc(ctx, m);
+        pr.pcount.alloc(ctx, m);
+        TQP_CUDA(cudaMemcpyAsync(pr.pcount.get(), counts, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        a.pkey = pr.pkey.get();
+        a.n_pairs = PL->n_pairs;
+        for (int j = 0; j < PL->n_pairs; j++) {
+            a.pop[j] = PL->pop[j];
+            a.src[j] = nullptr;
+            for (int g = 0; g < n_aggs && !a.src[j]; g++)
+                if (PL->apair[g] == j) a.src[j] = partial ? partial[g] : nullptr;
+            if (!a.src[j]) fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: missing partial array");
+            pr.plo[j].alloc(ctx, m);
+            a.plo[j] = pr.plo[j].get();
+            if (PL->pop[j] == P_SUM) { pr.phi[j].alloc(ctx, m); a.phi[j] = pr.phi[j].get(); }
+        }
+        const int g = (int)std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->num_sms * 8);
+        launch(ctx, "tqp_groupby_merge_pack", gb_merge_pack_kernel, dim3(g), dim3(256), 0, a);
+        phase2(ctx, PL, pr);
+        *n_groups_host = PL->G;
+        return PL;
+    } catch (...) {
+        delete PL;
+        throw;
+    }
+}
 
 }  // namespace tqp

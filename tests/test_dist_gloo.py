@@ -1,0 +1,146 @@
+"""World-size-2 gloo tests (CPU) of the multi-GPU exchange logic in
+paper_2203_01877_b200/dist.py. The local operators are the oracle (CPU), so the
+test checks the partitioning, all-gather, AVG rewrite and exact merge, and the
+broadcast-build join's global row numbering against the single-process oracle
+on the whole table."""
+
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+# ---- oracle-backed stand-ins for the CUDA operators (same dict layout as the binding)
+
+def oracle_local(cols, key_idx, aggs, preds):
+    import oracle
+    r = oracle.groupby_agg([c.numpy() for c in cols], key_idx, aggs, preds)
+    G = r["n_groups"]
+    res = []
+    for (op, _), v in zip(aggs, r["results"]):
+        if op == "sum":
+            res.append(torch.tensor([[x & ((1 << 64) - 1) if x & ((1 << 64) - 1) < (1 << 63)
+                                      else (x & ((1 << 64) - 1)) - (1 << 64), x >> 64] for x in v],
+                                    dtype=torch.int64).reshape(G, 2))
+        elif op == "avg":
+            res.append(torch.tensor(v, dtype=torch.float64))
+        else:
+            res.append(torch.tensor(v, dtype=torch.int64))
+    keys = [torch.tensor(k, dtype=cols[key_idx[i]].dtype) for i, k in enumerate(r["keys"])]
+    return {"n_groups": G, "keys": keys, "results": res}
+
+
+def oracle_merge(keys, aggs, partials, counts):
+    """Plain merge by dictionary (Python big ints) -- mirrors tqp_groupby_merge's contract."""
+    m = counts.numel()
+    groups = {}
+    for i in range(m):
+        k = tuple(int(t[i]) for t in keys)
+        g = groups.setdefault(k, {"count": 0, "vals": [None] * len(aggs)})
+        g["count"] += int(counts[i])
+        for a, (op, _) in enumerate(aggs):
+            p = partials[a]
+            if op in ("sum", "avg"):
+                lo, hi = int(p[i, 0]) & ((1 << 64) - 1), int(p[i, 1])
+                v = (hi << 64) + lo
+                g["vals"][a] = v if g["vals"][a] is None else g["vals"][a] + v
+            elif op == "min":
+                g["vals"][a] = int(p[i]) if g["vals"][a] is None else min(g["vals"][a], int(p[i]))
+            elif op == "max":
+                g["vals"][a] = int(p[i]) if g["vals"][a] is None else max(g["vals"][a], int(p[i]))
+    out_keys = sorted(groups)
+    results = []
+    for a, (op, _) in enumerate(aggs):
+        col = []
+        for k in out_keys:
+            g = groups[k]
+            if op == "count":
+                col.append(g["count"])
+            elif op == "avg":
+                col.append(float(g["vals"][a]) / g["count"] if g["count"] else float("nan"))
+            else:
+                col.append(g["vals"][a])
+        results.append(col)
+    return {"n_groups": len(out_keys), "keys": [[k[j] for k in out_keys] for j in range(len(keys))],
+            "results": results}
+
+
+def _worker(rank, world, port, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from datagen import tpch_orders_lineitem
+        from datagen.tpch import orders_count
+        from datagen.queries import Q1_AGGS, Q1_COLS, Q1_KEYS, Q1_PREDS, Q6_AGGS, Q6_COLS, Q6_PREDS, columns
+        from paper_2203_01877_b200 import dist as D   # noqa: imports the binding (CPU: no kernels run)
+        sf = 0.01
+        n_o = orders_count(sf) // world
+        orders, li = tpch_orders_lineitem(sf, seed=42, device="cpu", layout="shuffled",
+                                          order_range=(rank * n_o, (rank + 1) * n_o))
+        q1 = D.groupby_agg(None, columns(li, Q1_COLS), Q1_KEYS, Q1_AGGS, Q1_PREDS,
+                           local_fn=oracle_local, merge_fn=oracle_merge)
+        q6 = D.groupby_agg(None, columns(li, Q6_COLS), [], Q6_AGGS, Q6_PREDS,
+                           local_fn=oracle_local, merge_fn=oracle_merge)
+        # shuffled layout: each rank probes with a different lineitem slice than its orders
+        import oracle
+        def join_fn(b, p):
+            lo, ro = oracle.pkfk_join(b.numpy(), p.numpy())
+            return torch.as_tensor(lo), torch.as_tensor(ro)
+        other = (rank + 1) % world
+        _, li_other = tpch_orders_lineitem(sf, seed=42, device="cpu", layout="shuffled",
+                                           order_range=(other * n_o, (other + 1) * n_o))
+        lo, ro = D.pkfk_join_broadcast(None, orders["o_orderkey"], li_other["l_orderkey"], join_fn=join_fn)
+        out_q.put((rank, q1, q6, lo.numpy(), ro.numpy(), li_other["l_parent"].numpy() + other * n_o))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_world2_groupby_and_broadcast_join():
+    import oracle
+    from datagen import tpch_orders_lineitem
+    from datagen.queries import Q1_AGGS, Q1_COLS, Q1_KEYS, Q1_PREDS, Q6_AGGS, Q6_COLS, Q6_PREDS, columns
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    # single-process oracle over the whole table (the union of both ranks' slices)
+    sf = 0.01
+    _, full = tpch_orders_lineitem(sf, seed=42, device="cpu", layout="shuffled")
+    want1 = oracle.groupby_agg([c.numpy() for c in columns(full, Q1_COLS)], Q1_KEYS, Q1_AGGS, Q1_PREDS)
+    want6 = oracle.groupby_agg([c.numpy() for c in columns(full, Q6_COLS)], [], Q6_AGGS, Q6_PREDS)
+    for rank, q1, q6, lo, ro, parent_global in outs:
+        assert q1["n_groups"] == want1["n_groups"]
+        assert [list(map(int, k)) for k in q1["keys"]] == [k.tolist() for k in want1["keys"]]
+        for a, (op, _) in enumerate(Q1_AGGS):
+            if op == "avg":
+                assert np.allclose(q1["results"][a], want1["results"][a], rtol=1e-12, atol=0)
+            else:
+                assert q1["results"][a] == want1["results"][a]
+        assert q6["results"][0] == want6["results"][0]
+        # broadcast build: global orders row of every probed lineitem, probe-row order
+        assert np.array_equal(ro, np.arange(len(ro)))
+        assert np.array_equal(lo, parent_global)

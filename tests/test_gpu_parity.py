@@ -418,3 +418,24 @@ def test_launch_counter_and_profiling(T):
     ctx.set_profiling(False)
     assert ctx.launch_count() >= 3
     assert "tqp_onesweep" in st and st["tqp_onesweep"][1] >= 1
+
+
+def test_groupby_merge_partials(T):
+    """tqp_groupby_merge over 3 row slices (the multi-GPU gather + final reduce, one process):
+    equals the oracle on the whole table, AVG recomputed from merged SUM / COUNT."""
+    from paper_2203_01877_b200.dist import _rewrite_aggs
+    _, li = tpch_orders_lineitem(0.01, seed=42, device="cuda")
+    cols = columns(li, Q1_COLS)
+    aggs = Q1_AGGS + [("min", [(3, 0, 1)]), ("max", [(2, 0, 1)])]
+    raggs = _rewrite_aggs(aggs)
+    n = cols[0].numel()
+    cuts = [0, n // 3, (2 * n) // 3, n]
+    parts = [T.groupby_agg([c[a:b] for c in cols], Q1_KEYS, raggs, Q1_PREDS) for a, b in zip(cuts, cuts[1:])]
+    keys = [torch.cat([p["keys"][k] for p in parts]) for k in range(len(Q1_KEYS))]
+    partials = []
+    for a, (op, _) in enumerate(aggs):
+        partials.append(None if op == "count" else torch.cat([p["results"][a] for p in parts]))
+    counts = torch.cat([p["results"][-1] for p in parts])
+    got = T.context().groupby_merge(keys, aggs, partials, counts)
+    want = oracle.groupby_agg([npy(c) for c in cols], Q1_KEYS, aggs, Q1_PREDS)
+    check_groupby(T, got, want, aggs)

@@ -1,0 +1,61 @@
+"""Per-operator timing on SF10 (dev tool): each operator alone, repeated, with the
+library's per-kernel CUDA-event stats and host wall time, to separate kernel time
+from host-side gaps (syncs, allocations)."""
+
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2203_01877_b200 as T                                   # noqa: E402
+from datagen import tpch_orders_lineitem                            # noqa: E402
+from datagen.queries import (Q1_AGGS, Q1_COLS, Q1_KEYS, Q1_PREDS,   # noqa: E402
+                             Q6_AGGS, Q6_COLS, Q6_PREDS, columns)
+
+
+def main():
+    sf = float(sys.argv[1]) if len(sys.argv) > 1 else 10.0
+    reps = 5
+    orders, li = tpch_orders_lineitem(sf, seed=42, device="cuda")
+    ok, lk = orders["o_orderkey"], li["l_orderkey"]
+    q1, q6 = columns(li, Q1_COLS), columns(li, Q6_COLS)
+    ctx = T.context()
+    ops = {
+        "sort_build": lambda: ctx.sort(ok),
+        "sort_probe": lambda: ctx.sort(lk),
+        "pkfk_join": lambda: ctx.pkfk_join(ok, lk),
+        "smj_join": lambda: ctx.smj_join(ok, lk),
+        "q1_groupby": lambda: ctx.groupby_agg(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS),
+        "q6_filter": lambda: ctx.filter_compact(q6, Q6_PREDS),
+        "q6_sum": lambda: ctx.groupby_agg(q6, [], Q6_AGGS, Q6_PREDS),
+    }
+    out = {}
+    for name, f in ops.items():
+        for _ in range(2):
+            f()
+        torch.cuda.synchronize()
+        ctx.reset_counters()
+        ctx.set_profiling(True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        for _ in range(reps):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / reps * 1e3
+        st = ctx.kernel_stats()
+        ctx.set_profiling(False)
+        out[name] = {"event_ms": e0.elapsed_time(e1) / reps, "wall_ms": wall,
+                     "kernel_ms": sum(v[0] for v in st.values()) / reps,
+                     "kernels": {k: [round(v[0] / reps, 4), v[1] / reps, round(v[2] / max(v[0], 1e-9) / 1e6, 1)]
+                                 for k, v in sorted(st.items(), key=lambda kv: -kv[1][0])}}
+        print(name, json.dumps(out[name]), flush=True)
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
