@@ -50,18 +50,65 @@ __global__ void __launch_bounds__(FNT) filter_kernel(FilterArgs a) {
     const int64_t tile = take_tile(a.counter, &s_tile);
     const int64_t base = tile * FTILE;
     unsigned bal[FIPT];
+    bool pass[FIPT];
+#pragma unroll
+    for (int i = 0; i < FIPT; i++) pass[i] = base + i * FNT + tid < a.n;
+    const bool full = base + FTILE <= a.n;
+    // predicates: descriptor and dtype/op dispatch hoisted out of the row loop; all
+    // loads of a predicate column are independent (no short-circuit), 8 in flight
+    for (int q = 0; q < a.n_preds; q++) {
+        int64_t x[FIPT];
+        switch (a.pdt[q]) {
+            case TQP_U8: {
+                const uint8_t* c = (const uint8_t*)a.pcol[q] + base + tid;
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) x[i] = (full || pass[i]) ? (int64_t)__ldg(c + i * FNT) : 0;
+                break;
+            }
+            case TQP_I32: {
+                const int32_t* c = (const int32_t*)a.pcol[q] + base + tid;
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) x[i] = (full || pass[i]) ? (int64_t)__ldg(c + i * FNT) : 0;
+                break;
+            }
+            default: {
+                const long long* c = (const long long*)a.pcol[q] + base + tid;
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) x[i] = (full || pass[i]) ? (int64_t)__ldg(c + i * FNT) : 0;
+            }
+        }
+        const int64_t v = a.val[q];
+        switch (a.op[q]) {
+            case TQP_LT:
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] < v;
+                break;
+            case TQP_LE:
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] <= v;
+                break;
+            case TQP_GT:
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] > v;
+                break;
+            case TQP_GE:
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] >= v;
+                break;
+            case TQP_EQ:
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] == v;
+                break;
+            default:
+#pragma unroll
+                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] != v;
+        }
+    }
 #pragma unroll
     for (int i = 0; i < FIPT; i++) {
         const int64_t row = base + i * FNT + tid;
-        bool pass = row < a.n;
-        if (pass) {
-            for (int q = 0; q < a.n_preds; q++) {
-                int64_t x = load_as_i64(a.pcol[q], a.pdt[q], row);
-                pass = pass && cmp(x, a.op[q], a.val[q]);
-            }
-            if (a.mask) a.mask[row] = (uint8_t)pass;
-        }
-        bal[i] = __ballot_sync(0xffffffffu, pass);
+        if (a.mask && row < a.n) a.mask[row] = (uint8_t)pass[i];
+        bal[i] = __ballot_sync(0xffffffffu, pass[i]);
         if (lane == 0) s_cnt[i * FNW + warp] = __popc(bal[i]);
     }
     __syncthreads();

@@ -49,6 +49,8 @@ constexpr int GPT = 4;
 constexpr int GTILE = GNT * GPT;   // 1024 rows per tile
 constexpr int MAXU = 16;           // distinct referenced columns
 constexpr int P_SUM = 0, P_MIN = 1, P_MAX = 2;
+constexpr int PCH = 8;             // (op, expression) pairs reduced per traversal
+constexpr int UCAP = 64;           // runs per tile with shared-memory accumulators
 
 struct Phase1Args {
     int n_ucols;
@@ -137,7 +139,13 @@ struct Work {   // shared-memory working set of one tile (after the two column s
     uint16_t sidx[2][GTILE];
     uint16_t srun[GTILE];
     uint16_t rstart[GTILE + 2];
-    uint32_t whist[GNW][256];
+    union {
+        uint32_t whist[GNW][256];   // in-tile sort: per-warp digit counters
+        struct {
+            uint64_t alo[PCH][UCAP];   // reduction: per-run split sums (low halves) / min / max
+            int64_t ahi[PCH][UCAP];    //            per-run split sums (high halves)
+        };
+    };
     uint32_t tstart[256];
     uint32_t s_w[GNW];
     uint64_t s_min[GNW], s_max[GNW];
@@ -163,9 +171,16 @@ __device__ __forceinline__ void tile_pass(Work& w, int src, int m, int shift) {
         const bool valid = q < m;
         if (valid) { k[i] = w.skey[src][q]; ix[i] = w.sidx[src][q]; }
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        const uint32_t dd = valid ? ((uint32_t)(k[i] >> shift) & 255u) : 0u;
+        unsigned pe = vm;
+#pragma unroll
+        for (int b = 0; b < 8; b++) {   // peers by one ballot per digit bit
+            const unsigned bb = __ballot_sync(0xffffffffu, (dd >> b) & 1u);
+            pe &= ((dd >> b) & 1u) ? bb : ~bb;
+        }
         if (valid) {
-            const uint32_t d = (uint32_t)(k[i] >> shift) & 255u;
-            const unsigned peers = __match_any_sync(vm, d);
+            const uint32_t d = dd;
+            const unsigned peers = pe;
             const uint32_t before = w.whist[warp][d];
             rk[i] = before + __popc(peers & lt);
             __syncwarp(vm);
@@ -196,22 +211,6 @@ __device__ __forceinline__ void tile_pass(Work& w, int src, int m, int shift) {
     __syncthreads();
 }
 
-__device__ __forceinline__ int64_t pair_value(const Phase1Args& a, const uint8_t* st, int j, int row, int& ovf) {
-    int64_t v = 1;
-    for (int f = 0; f < a.pnf[j]; f++) {
-        const int c = a.pfc[j][f];
-        const int64_t x = scol(st, a.uoff[c], a.udt[c], row);
-        const int64_t sx = a.psign[j][f] < 0 ? -x : x;
-        if (a.psign[j][f] < 0 && x == INT64_MIN) ovf = 1;
-        const int64_t t = a.padd[j][f] + sx;
-        if (((a.padd[j][f] ^ t) & (sx ^ t)) < 0) ovf = 1;   // signed add overflow
-        const int64_t lo = v * t;
-        if (__mul64hi(v, t) != (lo >> 63)) ovf = 1;        // signed mul overflow
-        v = lo;
-    }
-    return v;
-}
-
 __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, int64_t t) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t row0 = t * GTILE;
@@ -221,28 +220,85 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
     unsigned bal[GPT];
     uint64_t kmin = ~0ull, kmax = 0;
     if (tid == 0) w.s_m = 0;
+    bool pass[GPT];
 #pragma unroll
     for (int i = 0; i < GPT; i++) {
-        const int r = i * GNT + tid;
-        bool pass = r < nrows;
+        pass[i] = i * GNT + tid < nrows;
         key[i] = 0;
-        if (pass) {
-            for (int q = 0; q < a.n_preds; q++) {
-                const int c = a.pcol[q];
-                pass = pass & cmp_op(scol(st, a.uoff[c], a.udt[c], r), a.pop[q], a.pval[q]);
-            }
+    }
+    // predicates: descriptor and dtype/op dispatch hoisted out of the row loop
+    for (int q = 0; q < a.n_preds; q++) {
+        const int c = a.pcol[q];
+        int64_t x[GPT];
+        const uint8_t* col = st + a.uoff[c];
+        switch (a.udt[c]) {
+            case TQP_U8:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) x[i] = (int64_t)col[i * GNT + tid];
+                break;
+            case TQP_I32:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid];
+                break;
+            default:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid];
         }
-        if (pass) {
-            uint64_t kk = 0;
-            for (int c = 0; c < a.n_keys; c++) {
-                const int u = a.kcol[c];
-                kk |= key_part(scol(st, a.uoff[u], a.udt[u], r), a.udt[u]) << a.kshift[c];
-            }
-            key[i] = kk;
-            kmin = min(kmin, kk);
-            kmax = max(kmax, kk);
+        const int64_t v = a.pval[q];
+        switch (a.pop[q]) {
+            case TQP_LT:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] < v;
+                break;
+            case TQP_LE:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] <= v;
+                break;
+            case TQP_GT:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] > v;
+                break;
+            case TQP_GE:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] >= v;
+                break;
+            case TQP_EQ:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] == v;
+                break;
+            default:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] != v;
         }
-        bal[i] = __ballot_sync(0xffffffffu, pass);
+    }
+    // packed key, column 0 most significant (reading R12)
+    for (int c = 0; c < a.n_keys; c++) {
+        const int u = a.kcol[c];
+        const uint8_t* col = st + a.uoff[u];
+        const int sh = a.kshift[c];
+        switch (a.udt[u]) {
+            case TQP_U8:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) key[i] |= (uint64_t)col[i * GNT + tid] << sh;
+                break;
+            case TQP_I32:
+#pragma unroll
+                for (int i = 0; i < GPT; i++)
+                    key[i] |= (uint64_t)((uint32_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid] ^ 0x80000000u) << sh;
+                break;
+            default:
+#pragma unroll
+                for (int i = 0; i < GPT; i++)
+                    key[i] |= ((uint64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid] ^ 0x8000000000000000ull) << sh;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < GPT; i++) {
+        if (pass[i]) {
+            kmin = min(kmin, key[i]);
+            kmax = max(kmax, key[i]);
+        }
+        bal[i] = __ballot_sync(0xffffffffu, pass[i]);
     }
     for (int o = 16; o > 0; o >>= 1) {
         kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
@@ -307,67 +363,164 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
     const int U = (int)w.s_U;
     const int64_t pb = w.s_pb;
     if (U == 0 || pb < 0) return;
-    // 5. partial records: key, count, accumulator init
+    // 5. partial records: key and count; per-run accumulators live in shared memory
+    //    when the tile has few runs (the partial slots are private to this tile),
+    //    else directly in the tile's global partial slots
     for (int u = tid; u < U; u += GNT) {
         a.pkey[pb + u] = sk[w.rstart[u]] + kmin;
         a.pcount[pb + u] = (int64_t)w.rstart[u + 1] - w.rstart[u];
-        for (int j = 0; j < a.n_pairs; j++) {
-            const int op = a.prop[j];
-            a.plo[j][pb + u] = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
-            if (op == P_SUM) a.phi[j][pb + u] = 0;
-        }
     }
-    __syncthreads();
-    // 6. segmented reduction of every (op, expression) pair in sorted order
+    const bool sm_acc = U <= UCAP;
+    // 6. per (op, expression) pair: (A) evaluate the expression for this thread's
+    //    rows in row order into the spare sort buffer, (B) reduce it in sorted
+    //    order per run. Sums are kept split (sum of low 32-bit halves, sum of high
+    //    halves): exact for a tile and independent of the order of additions.
     const bool any = p0 < m;
     const int pl = min(p0 + GPT, m) - 1;
-    const int r0 = any ? w.srun[p0] : -1;
+    int prow[GPT], prun[GPT];
+#pragma unroll
+    for (int q = 0; q < GPT; q++) {
+        const int p = p0 + q;
+        prow[q] = p < m ? si[p] : 0;
+        prun[q] = p < m ? w.srun[p] : -1;
+    }
+    const int r0 = prun[0];
     const int rl = any ? w.srun[pl] : -1;
     const int wr0 = __shfl_sync(0xffffffffu, r0, 0);
     const bool uniform = __all_sync(0xffffffffu, any && r0 == rl && r0 == wr0);
     int ovf = 0;
     for (int j = 0; j < a.n_pairs; j++) {
         const int op = a.prop[j];
-        uint64_t lo = 0;      // sum of the low 32-bit halves
-        int64_t hi = 0;       // sum of the high 32-bit halves (signed)
-        int64_t mm = op == P_MIN ? INT64_MAX : INT64_MIN;
-        int cur = r0;
+        const int jj = j % PCH;
+        // (A) evaluate the expression at this thread's sorted positions (passing rows
+        //     only; the in-tile sort is stable, so rows ascend within a run)
+        int64_t vv[GPT];
+        bool ov[GPT];
+#pragma unroll
+        for (int q = 0; q < GPT; q++) { vv[q] = 1; ov[q] = false; }
+        const int nf = a.pnf[j];
+        if (any) {
+            for (int f = 0; f < nf; f++) {
+                const int c = a.pfc[j][f];
+                const uint8_t* col = st + a.uoff[c];
+                const int64_t add = a.padd[j][f];
+                const bool neg = a.psign[j][f] < 0;
+                int64_t x[GPT];
+                switch (a.udt[c]) {
+                    case TQP_U8:
+#pragma unroll
+                        for (int q = 0; q < GPT; q++) x[q] = (int64_t)col[prow[q]];
+                        break;
+                    case TQP_I32:
+#pragma unroll
+                        for (int q = 0; q < GPT; q++) x[q] = (int64_t)reinterpret_cast<const int32_t*>(col)[prow[q]];
+                        break;
+                    default:
+#pragma unroll
+                        for (int q = 0; q < GPT; q++) x[q] = (int64_t)reinterpret_cast<const long long*>(col)[prow[q]];
+                }
+#pragma unroll
+                for (int q = 0; q < GPT; q++) {
+                    int64_t t;
+                    if (neg) {
+                        t = add - x[q];
+                        ov[q] |= ((add ^ x[q]) & (add ^ t)) < 0;   // signed sub overflow
+                    } else {
+                        t = add + x[q];
+                        ov[q] |= ((add ^ t) & (x[q] ^ t)) < 0;     // signed add overflow
+                    }
+                    if (f == 0) {
+                        vv[q] = t;
+                    } else if ((uint64_t)(vv[q] + 0x80000000ll) < 0x100000000ull &&
+                               (uint64_t)(t + 0x80000000ll) < 0x100000000ull) {
+                        vv[q] = (int64_t)(int32_t)vv[q] * (int64_t)(int32_t)t;   // both fit int32: exact
+                    } else {
+                        const int64_t lo = vv[q] * t;
+                        ov[q] |= __mul64hi(vv[q], t) != (lo >> 63);             // signed mul overflow
+                        vv[q] = lo;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < GPT; q++)
+                if (ov[q] && prun[q] >= 0) ovf = 1;
+        }
+        if (jj == 0) {   // (re)initialise the accumulators of this chunk of pairs
+            const int np = min(PCH, a.n_pairs - j);
+            if (sm_acc) {
+                for (int idx = tid; idx < np * U; idx += GNT) {
+                    const int k2 = idx / U, u = idx - k2 * U;
+                    const int op2 = a.prop[j + k2];
+                    w.alo[k2][u] = op2 == P_SUM ? 0ull : (op2 == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+                    w.ahi[k2][u] = 0;
+                }
+            } else {
+                for (int u = tid; u < U; u += GNT)
+                    for (int k2 = 0; k2 < np; k2++) {
+                        const int op2 = a.prop[j + k2];
+                        a.plo[j + k2][pb + u] =
+                            op2 == P_SUM ? 0ull : (op2 == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+                        if (op2 == P_SUM) a.phi[j + k2][pb + u] = 0;
+                    }
+            }
+            __syncthreads();
+        }
+        // (B) reduce in sorted order
+        uint64_t lo = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+        int64_t hi = 0;
+        unsigned long long* dl = sm_acc ? (unsigned long long*)&w.alo[jj][0] : (unsigned long long*)&a.plo[j][pb];
+        unsigned long long* dh = sm_acc ? (unsigned long long*)&w.ahi[jj][0]
+                                        : (unsigned long long*)(op == P_SUM ? &a.phi[j][pb] : nullptr);
         auto flush = [&](int run) {
             if (op == P_SUM) {
-                const unsigned __int128 v = (unsigned __int128)(((__int128)hi << 32) + (__int128)lo);
-                atomic_add_i128(&a.plo[j][pb + run], &a.phi[j][pb + run], v);
+                atomicAdd(dl + run, (unsigned long long)lo);
+                atomicAdd(dh + run, (unsigned long long)hi);
             } else if (op == P_MIN) {
-                atomicMin((long long*)&a.plo[j][pb + run], (long long)mm);
+                atomicMin((long long*)(dl + run), (long long)lo);
             } else {
-                atomicMax((long long*)&a.plo[j][pb + run], (long long)mm);
+                atomicMax((long long*)(dl + run), (long long)lo);
             }
         };
-        for (int p = p0; p <= pl; p++) {
-            const int r = w.srun[p];
-            if (r != cur) {
+        int cur = r0;
+#pragma unroll
+        for (int q = 0; q < GPT; q++) {
+            if (prun[q] < 0) break;
+            if (prun[q] != cur) {
                 flush(cur);
-                lo = 0;
+                lo = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
                 hi = 0;
-                mm = op == P_MIN ? INT64_MAX : INT64_MIN;
-                cur = r;
+                cur = prun[q];
             }
-            const int64_t v = pair_value(a, st, j, si[p], ovf);
+            const int64_t v = vv[q];
             if (op == P_SUM) { lo += (uint64_t)(uint32_t)v; hi += (v >> 32); }
-            else mm = op == P_MIN ? min(mm, v) : max(mm, v);
+            else if (op == P_MIN) lo = (uint64_t)min((int64_t)lo, v);
+            else lo = (uint64_t)max((int64_t)lo, v);
         }
         if (uniform) {
             for (int o = 16; o > 0; o >>= 1) {
+                const uint64_t xl = __shfl_xor_sync(0xffffffffu, lo, o);
                 if (op == P_SUM) {
-                    lo += __shfl_xor_sync(0xffffffffu, lo, o);
+                    lo += xl;
                     hi += __shfl_xor_sync(0xffffffffu, hi, o);
+                } else if (op == P_MIN) {
+                    lo = (uint64_t)min((int64_t)lo, (int64_t)xl);
                 } else {
-                    const int64_t x = __shfl_xor_sync(0xffffffffu, mm, o);
-                    mm = op == P_MIN ? min(mm, x) : max(mm, x);
+                    lo = (uint64_t)max((int64_t)lo, (int64_t)xl);
                 }
             }
             if (lane == 0) flush(cur);
         } else if (any) {
             flush(cur);
+        }
+        if (jj == PCH - 1 || j == a.n_pairs - 1) __syncthreads();
+        if (sm_acc && (jj == PCH - 1 || j == a.n_pairs - 1)) {   // chunk complete: write its partials
+            const int jb = j - jj, np = jj + 1;
+            for (int idx = tid; idx < np * U; idx += GNT) {
+                const int k2 = idx / U, u = idx - k2 * U;
+                a.plo[jb + k2][pb + u] = w.alo[k2][u];
+                if (a.prop[jb + k2] == P_SUM) a.phi[jb + k2][pb + u] = w.ahi[k2][u];
+            }
+            __syncthreads();
         }
     }
     if (ovf) atomicOr(a.overflow, 1);
@@ -508,6 +661,7 @@ struct AccArgs {
     const uint32_t* perm;
     const uint32_t* gid;
     int64_t P;
+    int split;   // 1: phase-1 partials (sum of low / high 32-bit halves); 0: int128 (lo, hi)
 };
 
 __global__ void __launch_bounds__(QNT) gb_acc_kernel(AccArgs a) {
@@ -530,7 +684,12 @@ __global__ void __launch_bounds__(QNT) gb_acc_kernel(AccArgs a) {
             const int op = a.pop[j];
             if (op == P_SUM) {
                 unsigned __int128 v = 0;
-                if (valid) v = ((unsigned __int128)(uint64_t)a.phi[j][rec] << 64) | a.plo[j][rec];
+                if (valid) {
+                    if (a.split)
+                        v = (unsigned __int128)(((__int128)a.phi[j][rec] << 32) + (__int128)a.plo[j][rec]);
+                    else
+                        v = ((unsigned __int128)(uint64_t)a.phi[j][rec] << 64) | a.plo[j][rec];
+                }
                 if (uniform) {
                     for (int o = 16; o > 0; o >>= 1) {
                         const uint64_t l = __shfl_xor_sync(0xffffffffu, (uint64_t)v, o);
@@ -651,7 +810,7 @@ struct Partials {   // phase-1 output / phase-2 input
 };
 
 // Phase 2: global sort of partial keys, segment ids, exact accumulation.
-void phase2(tqp_ctx* ctx, tqp_groupby_plan* PL, Partials& pr) {
+void phase2(tqp_ctx* ctx, tqp_groupby_plan* PL, Partials& pr, bool split) {
     const int64_t P = pr.P;
     SortOut so;
     so.want_perm32 = true;
@@ -701,6 +860,7 @@ void phase2(tqp_ctx* ctx, tqp_groupby_plan* PL, Partials& pr) {
     c.perm = so.perm32.get();
     c.gid = gid.get();
     c.P = P;
+    c.split = split ? 1 : 0;
     const int ag = (int)std::min<int64_t>(ceil_div(P, QNT), (int64_t)ctx->num_sms * 8);
     launch(ctx, "tqp_groupby_accumulate", gb_acc_kernel, dim3(ag), dim3(QNT), 0, c);
     ctx->add_bytes("tqp_groupby_accumulate", (rec + 8) * (double)P);
@@ -873,7 +1033,7 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             *n_groups_host = PL->G;
             return PL;
         }
-        phase2(ctx, PL, pr);
+        phase2(ctx, PL, pr, true);
         *n_groups_host = PL->G;
         return PL;
     } catch (...) {
@@ -1003,7 +1163,7 @@ tqp_groupby_plan* groupby_merge(tqp_ctx* ctx, int64_t m, const tqp_col* key_cols
         }
         const int g = (int)std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->num_sms * 8);
         launch(ctx, "tqp_groupby_merge_pack", gb_merge_pack_kernel, dim3(g), dim3(256), 0, a);
-        phase2(ctx, PL, pr);
+        phase2(ctx, PL, pr, false);
         *n_groups_host = PL->G;
         return PL;
     } catch (...) {

@@ -44,12 +44,26 @@ __global__ void bucket_ends_kernel(const KT* __restrict__ keys, int64_t n, KT ba
     }
 }
 
+// Packed build records: rec = ((key - base) mod 2^shift) << pbits | source row. The
+// bracket bucket supplies the key bits above `shift`, so one u32 per build row
+// carries both the residual key and the permutation (keeps the build side
+// L2-resident: 15M orders -> 60 MB of records + an 8 MB bracket table).
+template <typename KT>
+__global__ void pack_records_kernel(const KT* __restrict__ keys, const uint32_t* __restrict__ perm, int64_t n,
+                                    KT base, uint32_t lowmask, int pbits, uint32_t* __restrict__ rec) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        rec[i] = (((uint32_t)(KT)(keys[i] - base) & lowmask) << pbits) | perm[i];
+}
+
 struct ProbeArgs {
     const void* probe;
     int64_t n_probe;
     const void* bkeys;        // sorted internal build keys (KT)
     const uint32_t* bperm;    // their source rows
     const uint32_t* T;        // bracket table, 2^B + 1 entries
+    const uint32_t* rec;      // packed records (PACKED)
+    uint32_t lowmask;         // 2^shift - 1
+    int pbits;                // bits of the row number in a record
     uint64_t base;            // internal-domain base (= AND of all build keys)
     int vbits;                // (k - base) must be < 2^vbits
     uint64_t hi_bits;         // k32: required high 32 bits of u
@@ -65,12 +79,12 @@ struct ProbeArgs {
     int64_t n_tiles;
 };
 
-template <typename KT, int PDT>
+template <typename KT, int PDT, bool PACKED>
 __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint32_t& left) {
-    int64_t v;
-    if (PDT == TQP_I64) v = (int64_t)__ldg((const long long*)a.probe + row);
-    else if (PDT == TQP_I32) v = (int64_t)__ldg((const int*)a.probe + row);
-    else v = (int64_t)__ldg((const unsigned char*)a.probe + row);
+    int64_t v;   // probe keys are streamed once: evict-first
+    if (PDT == TQP_I64) v = (int64_t)__ldcs((const long long*)a.probe + row);
+    else if (PDT == TQP_I32) v = (int64_t)__ldcs((const int*)a.probe + row);
+    else v = (int64_t)__ldcs((const unsigned char*)a.probe + row);
     uint64_t u = ordered_u64(v);
     KT k;
     if (sizeof(KT) == 4) {
@@ -83,19 +97,37 @@ __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint3
     if (k < (KT)a.base || (a.vbits < 64 && ((uint64_t)rel >> a.vbits) != 0)) return false;
     uint64_t b = (uint64_t)rel >> a.shift;
     uint32_t lo = __ldg(a.T + b), hi = __ldg(a.T + b + 1);
+    if (PACKED) {
+        const uint32_t low = (uint32_t)rel & a.lowmask;
+        const uint32_t target = low << a.pbits;
+        const uint32_t end = hi;
+        while (lo < hi) {   // lower_bound of the residual inside the bucket
+            uint32_t mid = (lo + hi) >> 1;
+            if (__ldg(a.rec + mid) < target) lo = mid + 1; else hi = mid;
+        }
+        if (lo < end) {
+            const uint32_t r = __ldg(a.rec + lo);
+            if ((r >> a.pbits) == low) {
+                left = r & ((1u << a.pbits) - 1u);
+                return true;
+            }
+        }
+        return false;
+    }
     const KT* keys = (const KT*)a.bkeys;
+    const uint32_t end = hi;
     while (lo < hi) {   // lower_bound inside the bucket (a few elements)
         uint32_t mid = (lo + hi) >> 1;
         if (__ldg(keys + mid) < k) lo = mid + 1; else hi = mid;
     }
-    if (lo < __ldg(a.T + b + 1) && __ldg(keys + lo) == k) {
+    if (lo < end && __ldg(keys + lo) == k) {
         left = __ldg(a.bperm + lo);
         return true;
     }
     return false;
 }
 
-template <typename KT, int PDT>
+template <typename KT, int PDT, bool PACKED>
 __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
     __shared__ int64_t s_tile;
     __shared__ uint32_t s_cnt[PIPT * PNW];
@@ -110,7 +142,7 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
     for (int i = 0; i < PIPT; i++) {
         int64_t row = base + i * PNT + tid;
         m[i] = false;
-        if (row < a.n_probe) m[i] = probe_one<KT, PDT>(a, row, left[i]);
+        if (row < a.n_probe) m[i] = probe_one<KT, PDT, PACKED>(a, row, left[i]);
     }
 #pragma unroll
     for (int i = 0; i < PIPT; i++) {
@@ -150,11 +182,11 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
         if (bal[i] & (1u << lane)) {
             int64_t row = base + i * PNT + tid;
             int64_t j = excl + s_cnt[i * PNW + warp] + __popc(bal[i] & lt);
-            if (a.mode == 0) {
-                a.left_out[j] = (int64_t)left[i];
-                a.right_out[j] = row;
+            if (a.mode == 0) {   // outputs are streamed: evict-first stores
+                __stcs((long long*)a.left_out + j, (long long)left[i]);
+                __stcs((long long*)a.right_out + j, (long long)row);
             } else if (a.right_out) {
-                a.right_out[j] = row;
+                __stcs((long long*)a.right_out + j, (long long)row);
             }
         }
     }
@@ -163,9 +195,12 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
 struct Built {
     SortOut so;
     DevBuf<uint32_t> T;
+    DevBuf<uint32_t> rec;
     DevBuf<int> dup;
     uint64_t base = 0, hi_bits = 0;
-    int shift = 0, vbits = 0;
+    int shift = 0, vbits = 0, pbits = 0;
+    bool packed = false;
+    int64_t nb = 0;
 };
 
 void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
@@ -178,9 +213,22 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
     const int vbits = diff ? 64 - __builtin_clzll(diff) : 0;
     int lg = 0;
     while ((int64_t(1) << (lg + 1)) <= nb) lg++;
-    int Bbits = std::max(0, std::min(vbits, lg - 1));
-    Bbits = std::min(Bbits, 26);
-    if (vbits > 0) Bbits = std::max(Bbits, 1);   // keeps shift <= 63
+    int pbits = 1;
+    while ((int64_t(1) << pbits) < nb) pbits++;
+    // packed records need shift = vbits - B <= 32 - pbits; aim at ~4 keys per bucket
+    const int bmax = std::min(vbits, 26);
+    const int bmin_packed = vbits - (32 - pbits);
+    int Bbits;
+    if (vbits > 0 && bmin_packed <= bmax) {
+        Bbits = std::max(std::max(std::min(bmax, std::max(lg - 2, 1)), bmin_packed), 1);
+        B.packed = true;
+        B.pbits = pbits;
+    } else {
+        Bbits = std::max(0, std::min(vbits, lg - 1));
+        Bbits = std::min(Bbits, 26);
+        if (vbits > 0) Bbits = std::max(Bbits, 1);   // keeps shift <= 63
+    }
+    B.nb = nb;
     B.shift = vbits - Bbits;
     B.vbits = vbits;
     if (B.so.k32) {
@@ -202,13 +250,27 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
                nb, (uint64_t)B.base, B.shift, H.get(), B.dup.get());
     ctx->add_bytes("tqp_pkfk_bucket_ends", (double)nb * (B.so.k32 ? 4 : 8) + 4.0 * (double)std::min<int64_t>(nb, nbk));
     scan_max_u32_exclusive(ctx, H.get(), B.T.get(), nbk + 1);
+    if (B.packed) {
+        B.rec.alloc(ctx, nb);
+        const uint32_t lowmask = B.shift >= 32 ? 0xFFFFFFFFu : ((1u << B.shift) - 1u);
+        if (B.so.k32)
+            launch(ctx, "tqp_pkfk_records", pack_records_kernel<uint32_t>, dim3(g), dim3(256), 0, B.so.keys32.get(),
+                   B.so.perm32.get(), nb, (uint32_t)B.base, lowmask, B.pbits, B.rec.get());
+        else
+            launch(ctx, "tqp_pkfk_records", pack_records_kernel<uint64_t>, dim3(g), dim3(256), 0, B.so.keys64.get(),
+                   B.so.perm32.get(), nb, (uint64_t)B.base, lowmask, B.pbits, B.rec.get());
+        ctx->add_bytes("tqp_pkfk_records", (double)nb * ((B.so.k32 ? 4 : 8) + 8));
+        B.so.keys32.release();
+        B.so.keys64.release();
+        B.so.perm32.release();
+    }
 }
 
 void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, int anti, int64_t* left_out,
                int64_t* right_out, uint8_t* match_out, int64_t* n_out_host) {
     DevBuf<int64_t> total(ctx, 1);
     total.zero();
-    const int64_t nb = B.so.keys32.n + B.so.keys64.n;
+    const int64_t nb = B.nb;
     if (np > 0 && nb > 0) {
         const int64_t tiles = ceil_div(np, PTILE);
         DevBuf<uint64_t> status(ctx, tiles);
@@ -221,6 +283,9 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         a.bkeys = B.so.k32 ? (const void*)B.so.keys32.get() : (const void*)B.so.keys64.get();
         a.bperm = B.so.perm32.get();
         a.T = B.T.get();
+        a.rec = B.rec.get();
+        a.pbits = B.pbits;
+        a.lowmask = B.shift >= 32 ? 0xFFFFFFFFu : ((1u << B.shift) - 1u);
         a.base = B.base;
         a.vbits = B.vbits;
         a.hi_bits = B.hi_bits;
@@ -234,15 +299,20 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         a.counter = counter.get();
         a.total = total.get();
         a.n_tiles = tiles;
-        auto go = [&](auto kt) {
+        auto go = [&](auto kt, auto pk_) {
             using KT = decltype(kt);
+            constexpr bool PK = decltype(pk_)::value;
             switch (pk.dtype) {
-                case TQP_I64: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_I64>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
-                case TQP_I32: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_I32>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
-                default: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_U8>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                case TQP_I64: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_I64, PK>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                case TQP_I32: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_I32, PK>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                default: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_U8, PK>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
             }
         };
-        if (B.so.k32) go(uint32_t{}); else go(uint64_t{});
+        if (B.so.k32) {
+            if (B.packed) go(uint32_t{}, std::true_type{}); else go(uint32_t{}, std::false_type{});
+        } else {
+            if (B.packed) go(uint64_t{}, std::true_type{}); else go(uint64_t{}, std::false_type{});
+        }
     } else if (np > 0 && mode == 1) {
         // empty build side: nothing matches
         if (match_out) TQP_CUDA(cudaMemsetAsync(match_out, 0, np, ctx->stream));

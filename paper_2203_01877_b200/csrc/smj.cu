@@ -22,7 +22,8 @@
 struct tqp_smj_plan {
     int64_t n_left = 0, n_right = 0, K = 0, out_size = 0;
     tqp::DevBuf<uint32_t> perm_l, perm_r;
-    tqp::DevBuf<int64_t> mL, mR, msL, msR, mcum;
+    tqp::DevBuf<uint32_t> mL, mR, msL, msR;   // per common key: counts and run starts (< 2^30)
+    tqp::DevBuf<int64_t> mcum;                 // cumHistMul (inclusive)
 };
 
 namespace tqp {
@@ -119,13 +120,16 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo
 // For each left unique key: find it among the right unique keys; compact the
 // common keys with (L, R, startL, startR). Grid covers n_left (an upper bound
 // of U_l); tiles past U_l exit.
+constexpr int ICAP = 4096;   // right unique keys staged in shared memory per tile
+
 __global__ void __launch_bounds__(JNT) intersect_kernel(const uint64_t* __restrict__ ukl, const int64_t* __restrict__ usl,
                                                         const int64_t* U_l_p, const uint64_t* __restrict__ ukr,
                                                         const int64_t* __restrict__ usr, const int64_t* U_r_p,
-                                                        int64_t* mL, int64_t* mR, int64_t* msL, int64_t* msR,
+                                                        uint32_t* mL, uint32_t* mR, uint32_t* msL, uint32_t* msR,
                                                         int64_t* K_out, uint64_t* status, unsigned long long* counter) {
     __shared__ int64_t s_tile, s_rlo, s_rhi;
     __shared__ CompactTile s;
+    __shared__ uint64_t s_r[ICAP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tile = take_tile(counter, &s_tile);
     const int64_t U_l = *U_l_p, U_r = *U_r_p;
@@ -136,21 +140,40 @@ __global__ void __launch_bounds__(JNT) intersect_kernel(const uint64_t* __restri
     if (tid == 32) s_rhi = lower_bound_u64(ukr, 0, U_r, ukl[last]) + 1;
     __syncthreads();
     const int64_t rlo = s_rlo, rhi = min(s_rhi, U_r);
+    // the right unique keys this tile can match: staged in shared memory if they fit
+    const bool staged = rhi - rlo <= ICAP;
+    if (staged) {
+        for (int64_t i = rlo + tid; i < rhi; i += JNT) s_r[i - rlo] = ukr[i];
+        __syncthreads();
+    }
     unsigned bal[JIPT];
-    int64_t L[JIPT], R[JIPT], sL[JIPT], sR[JIPT];
+    uint32_t L[JIPT], R[JIPT], sL[JIPT], sR[JIPT];
 #pragma unroll
     for (int i = 0; i < JIPT; i++) {
         const int64_t j = base + i * JNT + tid;
         bool hit = false;
         if (j < U_l) {
             const uint64_t k = ukl[j];
-            const int64_t p = lower_bound_u64(ukr, rlo, rhi, k);
-            if (p < rhi && ukr[p] == k) {
+            int64_t p;
+            bool eq;
+            if (staged) {
+                int64_t lo = 0, hi = rhi - rlo;
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi) >> 1;
+                    if (s_r[mid] < k) lo = mid + 1; else hi = mid;
+                }
+                eq = lo < rhi - rlo && s_r[lo] == k;
+                p = lo + rlo;
+            } else {
+                p = lower_bound_u64(ukr, rlo, rhi, k);
+                eq = p < rhi && ukr[p] == k;
+            }
+            if (eq) {
                 hit = true;
-                sL[i] = usl[j];
-                L[i] = usl[j + 1] - sL[i];
-                sR[i] = usr[p];
-                R[i] = usr[p + 1] - sR[i];
+                sL[i] = (uint32_t)usl[j];
+                L[i] = (uint32_t)(usl[j + 1] - usl[j]);
+                sR[i] = (uint32_t)usr[p];
+                R[i] = (uint32_t)(usr[p + 1] - usr[p]);
             }
         }
         bal[i] = __ballot_sync(0xffffffffu, hit);
@@ -172,7 +195,7 @@ __global__ void __launch_bounds__(JNT) intersect_kernel(const uint64_t* __restri
 }
 
 // cumHistMul = inclusive scan of histMul = L*R over the K common keys.
-__global__ void __launch_bounds__(JNT) cum_kernel(const int64_t* __restrict__ mL, const int64_t* __restrict__ mR,
+__global__ void __launch_bounds__(JNT) cum_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
                                                   const int64_t* K_p, int64_t* mcum, int64_t* out_size,
                                                   int* overflow, uint64_t* status, unsigned long long* counter) {
     __shared__ int64_t s_tile;
@@ -232,36 +255,46 @@ __device__ __forceinline__ int64_t upper_bound_i64(const int64_t* a, int64_t lo,
 // Output offsets [begin, end): bucket b = upper_bound(cumHistMul, o) (bucketize
 // right=True); o' = o - (cumHistMul[b] - histMul[b]); q = o' / R, r = o' % R;
 // left = leftIdx[startL + q], right = rightIdx[startR + r].
-__global__ void __launch_bounds__(ENT) expand_kernel(const int64_t* __restrict__ mL, const int64_t* __restrict__ mR,
-                                                     const int64_t* __restrict__ msL, const int64_t* __restrict__ msR,
+__global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
+                                                     const uint32_t* __restrict__ msL, const uint32_t* __restrict__ msR,
                                                      const int64_t* __restrict__ mcum, int64_t K,
                                                      const uint32_t* __restrict__ perm_l,
                                                      const uint32_t* __restrict__ perm_r, int64_t begin, int64_t end,
                                                      int64_t* __restrict__ lo_out, int64_t* __restrict__ ro_out) {
     __shared__ int64_t s_b0, s_b1;
+    __shared__ uint32_t s_l[ETILE], s_r[ETILE];
     const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
     const int64_t c1 = min(c0 + ETILE, end);
     if (threadIdx.x == 0) s_b0 = upper_bound_i64(mcum, 0, K, c0);
     if (threadIdx.x == 32) s_b1 = upper_bound_i64(mcum, 0, K, c1 - 1);
     __syncthreads();
     const int64_t o0 = c0 + (int64_t)threadIdx.x * EIPT;
-    if (o0 >= c1) return;
-    int64_t b = upper_bound_i64(mcum, s_b0, s_b1 + 1, o0);
-    int64_t L = mL[b], R = mR[b], sL = msL[b], sR = msR[b];
-    int64_t off = o0 - (mcum[b] - L * R);
-    int64_t q = off / R, r = off - q * R;
-    const int cnt = (int)min((int64_t)EIPT, c1 - o0);
-    for (int j = 0; j < cnt; j++) {
-        const int64_t o = o0 + j - begin;
-        lo_out[o] = (int64_t)__ldg(perm_l + sL + q);
-        ro_out[o] = (int64_t)__ldg(perm_r + sR + r);
-        if (++r == R) {
-            r = 0;
-            if (++q == L) {
-                q = 0;
-                if (++b < K) { L = mL[b]; R = mR[b]; sL = msL[b]; sR = msR[b]; }
+    if (o0 < c1) {   // thread: EIPT consecutive outputs, incremental (q, r)
+        int64_t b = upper_bound_i64(mcum, s_b0, s_b1 + 1, o0);
+        int64_t L = mL[b], R = mR[b], sL = msL[b], sR = msR[b];
+        int64_t off = o0 - (mcum[b] - L * R);
+        int64_t q = off / R, r = off - q * R;
+        const int cnt = (int)min((int64_t)EIPT, c1 - o0);
+        for (int j = 0; j < cnt; j++) {
+            const int o = threadIdx.x * EIPT + j;
+            s_l[o] = __ldg(perm_l + sL + q);
+            s_r[o] = __ldg(perm_r + sR + r);
+            if (++r == R) {
+                r = 0;
+                if (++q == L) {
+                    q = 0;
+                    if (++b < K) { L = mL[b]; R = mR[b]; sL = msL[b]; sR = msR[b]; }
+                }
             }
         }
+    }
+    __syncthreads();
+    const int n = (int)(c1 - c0);
+    int64_t* lo = lo_out + (c0 - begin);
+    int64_t* ro = ro_out + (c0 - begin);
+    for (int o = threadIdx.x; o < n; o += ENT) {   // coalesced, streamed (evict-first) stores
+        __stcs((long long*)lo + o, (long long)s_l[o]);
+        __stcs((long long*)ro + o, (long long)s_r[o]);
     }
 }
 

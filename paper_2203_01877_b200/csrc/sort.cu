@@ -124,7 +124,7 @@ __device__ __forceinline__ uint64_t to_u(KT k, uint64_t hi_bits) {
 }
 
 template <typename KT, int IN, int IPT>
-__global__ void __launch_bounds__(NT) onesweep_kernel(OnesweepArgs a) {
+__global__ void __launch_bounds__(NT, 3) onesweep_kernel(OnesweepArgs a) {
     constexpr int TILE = NT * IPT;
     __shared__ union {
         uint32_t whist[NW][256];
@@ -163,21 +163,34 @@ __global__ void __launch_bounds__(NT) onesweep_kernel(OnesweepArgs a) {
         }
     }
     __syncwarp();
+    // Stable warp-level ranking: the leader of each match_any peer group claims
+    // popc(peers) slots of its warp's digit counter with a shared-memory atomicAdd
+    // (items are issued in order, so the claimed ranges follow item order); the
+    // 16 atomics pipeline without waiting on each other. rk packs the claimed
+    // base (bits 0-15), the leader lane (16-20) and the lane's rank among its
+    // peers (24-28) until the bases are broadcast.
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
-        int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        bool valid = pos < a.n;
-        unsigned vm = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-            uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
-            unsigned peers = __match_any_sync(vm, d);
-            uint32_t before = s.whist[warp][d];
-            rk[i] = before + __popc(peers & lt);
-            __syncwarp(vm);
-            if (lane == 31 - __clz(peers)) s.whist[warp][d] = before + __popc(peers);
-            __syncwarp(vm);
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        const bool valid = pos < a.n;
+        const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
+        // peers = lanes with the same digit: one ballot per digit bit (cheaper than MATCH.ANY)
+        unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int b = 0; b < 8; b++) {
+            const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+            peers &= ((d >> b) & 1u) ? bb : ~bb;
         }
+        const uint32_t leader = 31 - __clz(peers);
+        uint32_t old = 0;
+        if (valid && lane == leader) old = atomicAdd(&s.whist[warp][d], (uint32_t)__popc(peers));
+        rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; i++) {
+        const uint32_t b = __shfl_sync(0xffffffffu, rk[i] & 0xFFFFu, (rk[i] >> 16) & 31u);
+        rk[i] = b + (rk[i] >> 24);
     }
     __syncthreads();
     // per digit (thread d): exclusive prefix over warps and the tile count
@@ -192,31 +205,14 @@ __global__ void __launch_bounds__(NT) onesweep_kernel(OnesweepArgs a) {
         }
     }
     s_tstart[tid] = block_excl_scan256(cnt, s_w);
-    // decoupled look-back along this digit's chain of tiles
+    // publish this tile's digit counts as early as possible (successors sum them)
     {
         const int d = tid;
         uint32_t* st = a.lb + d;
-        uint32_t g;
-        if (tile == 0) {
-            g = s_base[d];
-            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st), "r"(SLB_PRE | (g + cnt)) : "memory");
-        } else {
+        if (tile == 0)
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st), "r"(SLB_PRE | (s_base[d] + cnt)) : "memory");
+        else
             asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st + tile * 256), "r"(SLB_AGG | cnt) : "memory");
-            uint32_t excl = 0;
-            int64_t t = tile - 1;
-            while (true) {
-                uint32_t w;
-                do {
-                    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(w) : "l"(st + t * 256) : "memory");
-                } while ((w >> 30) == 0);
-                excl += w & SLB_VAL;
-                if ((w >> 30) == 2) break;
-                t--;
-            }
-            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st + tile * 256), "r"(SLB_PRE | (excl + cnt)) : "memory");
-            g = excl;
-        }
-        s_gstart[d] = g;
     }
     __syncthreads();
 #pragma unroll
@@ -235,6 +231,51 @@ __global__ void __launch_bounds__(NT) onesweep_kernel(OnesweepArgs a) {
             s.stage.keys[rk[i]] = key[i];
             s.stage.perm[rk[i]] = pm[i];
         }
+    }
+    // decoupled look-back along this digit's chain of tiles, after the keys are
+    // staged (their registers are free): LBW independent loads per round
+    {
+        const int d = tid;
+        uint32_t* st = a.lb + d;
+        uint32_t g;
+        if (tile == 0) {
+            g = s_base[d];
+        } else {
+            constexpr int LBW = 8;
+            uint32_t excl = 0;
+            int64_t t = tile - 1;
+            while (true) {
+                uint32_t wv[LBW];
+#pragma unroll
+                for (int i = 0; i < LBW; i++) {
+                    const int64_t ti = t - i;
+                    if (ti >= 0)
+                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(wv[i]) : "l"(st + ti * 256) : "memory");
+                    else
+                        wv[i] = SLB_PRE;
+                }
+                uint32_t sum = 0;
+                bool done = false, stall = false;
+#pragma unroll
+                for (int i = 0; i < LBW; i++) {
+                    if (!done && !stall) {
+                        const uint32_t f = wv[i] >> 30;
+                        if (f == 0) stall = true;
+                        else {
+                            sum += wv[i] & SLB_VAL;
+                            done = f == 2;
+                        }
+                    }
+                }
+                if (stall) continue;
+                excl += sum;
+                if (done) break;
+                t -= LBW;
+            }
+            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st + tile * 256), "r"(SLB_PRE | (excl + cnt)) : "memory");
+            g = excl;
+        }
+        s_gstart[d] = g;
     }
     __syncthreads();
     const int tile_n = (int)min((int64_t)TILE, a.n - base);
