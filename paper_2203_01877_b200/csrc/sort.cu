@@ -1,28 +1,29 @@
-// sort.cu -- onesweep LSD radix sort with permutation (stable), sm_100a.
+// sort.cu -- LSD radix sort with permutation (stable), sm_100a.
 //
 // Paper: the join sorts its keys (Alg. 1 l.2-3) and the
 // aggregation sorts the concatenated group keys with "radix sort" (PAPER.md:256,
-// prose :1148). The paper composes torch.sort; here the sort is one upfront
-// AND/OR pass (which digits vary), one digit-histogram pass, and one onesweep
-// pass per varying 8-bit digit:
-//   - each CTA takes a dynamic tile id, ranks its tile by digit with warp-level
-//     __match_any_sync (stable within the warp's contiguous slice),
-//   - per-warp digit counters give the tile-local stable order,
-//   - the tile's 256-bin histogram is chained across tiles by decoupled
-//     look-back (one thread per digit) to get global output offsets,
-//   - keys and permutation are staged in shared memory in sorted order and
-//     written out so that consecutive threads write consecutive addresses.
-// Digits that are constant across all keys are skipped; when every varying bit
-// lies in the low 32 bits the passes carry 32-bit keys (half the traffic).
+// prose :1148). The paper composes torch.sort; here:
+//   - one AND/OR pass finds the bits that vary; 8-bit digits that are constant
+//     across all keys are skipped, and when every varying bit lies in the low
+//     32 bits the passes carry 32-bit keys (half the traffic);
+//   - every digit pass is reduce-then-scan, with no inter-tile waiting:
+//       tile_hist   per tile of 4096 (u32) / 3072 (u64) keys: 256 digit counts
+//       scan_tiles  per chunk of 128 tiles: exclusive prefix over tiles, per digit
+//       scan_chunks prefix over chunks + global bin bases (one CTA)
+//       scatter     stable tile ranking (one ballot per digit bit gives each
+//                   key's peers; warp counters claimed with shared atomics in item
+//                   order), keys staged in shared memory in digit order, written
+//                   out so consecutive threads write consecutive addresses.
+//     (A decoupled look-back "onesweep" variant was measured at 0.74 ms per
+//     60M-key pass on B200: its inclusive-prefix frontier serialises the tiles;
+//     see DESIGN.md.)
 #include "internal.h"
 
 namespace tqp {
 
-constexpr int NT = 256;                 // threads per CTA in the sort kernels
+constexpr int NT = 256;   // threads per CTA in the sort kernels
 constexpr int NW = NT / 32;
-constexpr uint32_t SLB_AGG = 1u << 30;  // 32-bit look-back words for the digit chains
-constexpr uint32_t SLB_PRE = 2u << 30;
-constexpr uint32_t SLB_VAL = (1u << 30) - 1;
+constexpr int CHUNK = 128;   // tiles per scan chunk
 
 enum InMode { IN_INTERNAL = 0, IN_I64 = 1, IN_I32 = 2, IN_U8 = 3, IN_U64 = 4 };
 
@@ -59,30 +60,6 @@ __global__ void __launch_bounds__(NT) andor_kernel(const void* keys, int64_t n, 
     }
 }
 
-struct PassPlan {
-    int n;
-    int shift[8];
-};
-
-template <int IN>
-__global__ void __launch_bounds__(NT) hist_kernel(const void* keys, int64_t n, bool desc, PassPlan pp,
-                                                  uint32_t* ghist) {
-    __shared__ uint32_t h[8][256];
-    for (int i = threadIdx.x; i < 8 * 256; i += NT) (&h[0][0])[i] = 0;
-    __syncthreads();
-    for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
-        uint64_t u = load_u<IN>(keys, i, desc);
-#pragma unroll
-        for (int p = 0; p < 8; p++)
-            if (p < pp.n) atomicAdd(&h[p][(u >> pp.shift[p]) & 255], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < pp.n * 256; i += NT) {
-        uint32_t c = (&h[0][0])[i];
-        if (c) atomicAdd(&ghist[i], c);
-    }
-}
-
 // Exclusive scan of one value per thread across a 256-thread block.
 __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* s_w) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -99,7 +76,80 @@ __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* s_w
     return add + x - v;
 }
 
-struct OnesweepArgs {
+template <typename KT, int IN>
+__device__ __forceinline__ KT load_key(const void* in_keys, int64_t pos, bool desc) {
+    if (IN == IN_INTERNAL) return ((const KT*)in_keys)[pos];
+    return (KT)load_u<IN>(in_keys, pos, desc);
+}
+
+// (1) per-tile digit counts -> th[tile * 256 + d]
+template <typename KT, int IN, int IPT>
+__global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int64_t n, int shift, bool desc,
+                                                       uint32_t* __restrict__ th) {
+    constexpr int TILE = NT * IPT;
+    __shared__ uint32_t h[NW][256];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int d = lane; d < 256; d += 32) h[warp][d] = 0;
+    __syncwarp();
+    const int64_t base = (int64_t)blockIdx.x * TILE;
+    KT k[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; i++) {
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        k[i] = pos < n ? load_key<KT, IN>(in_keys, pos, desc) : (KT)0;
+    }
+#pragma unroll
+    for (int i = 0; i < IPT; i++) {
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        if (pos < n) atomicAdd(&h[warp][(uint32_t)(k[i] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    uint32_t c = 0;
+#pragma unroll
+    for (int w = 0; w < NW; w++) c += h[w][tid];
+    th[(int64_t)blockIdx.x * 256 + tid] = c;
+}
+
+// (2) per chunk of CHUNK tiles: th[t][d] <- exclusive prefix within the chunk; ct[c][d] = chunk total
+__global__ void __launch_bounds__(NT) scan_tiles_kernel(uint32_t* __restrict__ th, int64_t n_tiles,
+                                                        uint32_t* __restrict__ ct) {
+    const int d = threadIdx.x;
+    const int64_t t0 = (int64_t)blockIdx.x * CHUNK;
+    const int cnt = (int)min((int64_t)CHUNK, n_tiles - t0);
+    uint32_t run = 0;
+    for (int b = 0; b < cnt; b += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) v[i] = (b + i < cnt) ? th[(t0 + b + i) * 256 + d] : 0u;   // 16 loads in flight
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (b + i < cnt) th[(t0 + b + i) * 256 + d] = run;
+            run += v[i];
+        }
+    }
+    ct[(int64_t)blockIdx.x * 256 + d] = run;
+}
+
+// (3) one CTA: ct[c][d] <- global start of digit d in chunk c (bin base + earlier chunks)
+__global__ void __launch_bounds__(NT) scan_chunks_kernel(uint32_t* __restrict__ ct, int64_t n_chunks) {
+    __shared__ uint32_t s_w[NW];
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+    for (int64_t b = 0; b < n_chunks; b += 16) {
+        uint32_t v[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * 256 + d] : 0u;
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (b + i < n_chunks) ct[(b + i) * 256 + d] = run;
+            run += v[i];
+        }
+    }
+    const uint32_t base = block_excl_scan256(run, s_w);   // global bin bases
+    for (int64_t c = 0; c < n_chunks; c++) ct[c * 256 + d] += base;
+}
+
+struct ScatterArgs {
     const void* in_keys;
     const uint32_t* in_perm;      // IN_INTERNAL only
     void* out_keys;               // internal KT (nullable on the last pass)
@@ -108,9 +158,8 @@ struct OnesweepArgs {
     int orig_dtype;
     int64_t* out_perm64;          // last pass
     uint64_t* out_u;              // last pass: sort-domain values
-    const uint32_t* ghist;        // this pass's 256 global digit counts
-    uint32_t* lb;                 // tiles x 256 look-back words (zeroed)
-    unsigned long long* counter;  // dynamic tile counter (zeroed)
+    const uint32_t* th;           // per tile, per digit: exclusive prefix within the chunk
+    const uint32_t* ct;           // per chunk, per digit: global start
     int64_t n;
     int shift;
     bool desc;
@@ -123,8 +172,9 @@ __device__ __forceinline__ uint64_t to_u(KT k, uint64_t hi_bits) {
     return (uint64_t)k;
 }
 
+// (4) stable scatter of one tile
 template <typename KT, int IN, int IPT>
-__global__ void __launch_bounds__(NT, 3) onesweep_kernel(OnesweepArgs a) {
+__global__ void __launch_bounds__(NT, 3) scatter_kernel(ScatterArgs a) {
     constexpr int TILE = NT * IPT;
     __shared__ union {
         uint32_t whist[NW][256];
@@ -133,49 +183,39 @@ __global__ void __launch_bounds__(NT, 3) onesweep_kernel(OnesweepArgs a) {
             uint32_t perm[TILE];
         } stage;
     } s;
-    __shared__ uint32_t s_tstart[256], s_gstart[256], s_base[256], s_w[NW];
-    __shared__ int64_t s_tile;
+    __shared__ uint32_t s_tstart[256], s_gstart[256], s_w[NW];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = take_tile(a.counter, &s_tile);
+    const int64_t tile = blockIdx.x;
     const int64_t base = tile * TILE;
 
     for (int d = lane; d < 256; d += 32) s.whist[warp][d] = 0;
-    // global start of each digit's bin = exclusive scan of the pass histogram
-    s_base[tid] = block_excl_scan256(a.ghist[tid], s_w);
+    s_gstart[tid] = a.ct[(tile / CHUNK) * 256 + tid] + a.th[tile * 256 + tid];
 
     KT key[IPT];
     uint32_t pm[IPT], rk[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
-        int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
         if (pos < a.n) {
-            if (IN == IN_INTERNAL) {
-                key[i] = ((const KT*)a.in_keys)[pos];
-                pm[i] = a.in_perm[pos];
-            } else {
-                key[i] = (KT)load_u<IN>(a.in_keys, pos, a.desc);
-                pm[i] = (uint32_t)pos;
-            }
+            key[i] = load_key<KT, IN>(a.in_keys, pos, a.desc);
+            pm[i] = IN == IN_INTERNAL ? a.in_perm[pos] : (uint32_t)pos;
         } else {
             key[i] = 0;
             pm[i] = 0;
         }
     }
     __syncwarp();
-    // Stable warp-level ranking: the leader of each match_any peer group claims
-    // popc(peers) slots of its warp's digit counter with a shared-memory atomicAdd
-    // (items are issued in order, so the claimed ranges follow item order); the
-    // 16 atomics pipeline without waiting on each other. rk packs the claimed
-    // base (bits 0-15), the leader lane (16-20) and the lane's rank among its
-    // peers (24-28) until the bases are broadcast.
+    // Stable warp-level ranking: peers (same digit) from one ballot per digit bit;
+    // the highest peer claims popc(peers) slots of its warp's digit counter with a
+    // shared-memory atomicAdd, in item order. rk packs the claimed base (bits
+    // 0-15), the leader lane (16-20) and the rank among peers (24-28).
     const unsigned lt = lanemask_lt();
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
         const bool valid = pos < a.n;
         const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
-        // peers = lanes with the same digit: one ballot per digit bit (cheaper than MATCH.ANY)
         unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
         for (int b = 0; b < 8; b++) {
@@ -193,105 +233,47 @@ __global__ void __launch_bounds__(NT, 3) onesweep_kernel(OnesweepArgs a) {
         rk[i] = b + (rk[i] >> 24);
     }
     __syncthreads();
-    // per digit (thread d): exclusive prefix over warps and the tile count
     uint32_t cnt = 0;
-    {
-        const int d = tid;
 #pragma unroll
-        for (int w = 0; w < NW; w++) {
-            uint32_t c = s.whist[w][d];
-            s.whist[w][d] = cnt;
-            cnt += c;
-        }
+    for (int w = 0; w < NW; w++) {   // per digit (thread d): exclusive prefix over warps
+        const uint32_t c = s.whist[w][tid];
+        s.whist[w][tid] = cnt;
+        cnt += c;
     }
     s_tstart[tid] = block_excl_scan256(cnt, s_w);
-    // publish this tile's digit counts as early as possible (successors sum them)
-    {
-        const int d = tid;
-        uint32_t* st = a.lb + d;
-        if (tile == 0)
-            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st), "r"(SLB_PRE | (s_base[d] + cnt)) : "memory");
-        else
-            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st + tile * 256), "r"(SLB_AGG | cnt) : "memory");
-    }
-    __syncthreads();
+    __syncthreads();   // s_tstart / whist prefixes visible to every thread
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
-        int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
         if (pos < a.n) {
-            uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
+            const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
             rk[i] = s_tstart[d] + s.whist[warp][d] + rk[i];
         }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
-        int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
         if (pos < a.n) {
             s.stage.keys[rk[i]] = key[i];
             s.stage.perm[rk[i]] = pm[i];
         }
     }
-    // decoupled look-back along this digit's chain of tiles, after the keys are
-    // staged (their registers are free): LBW independent loads per round
-    {
-        const int d = tid;
-        uint32_t* st = a.lb + d;
-        uint32_t g;
-        if (tile == 0) {
-            g = s_base[d];
-        } else {
-            constexpr int LBW = 8;
-            uint32_t excl = 0;
-            int64_t t = tile - 1;
-            while (true) {
-                uint32_t wv[LBW];
-#pragma unroll
-                for (int i = 0; i < LBW; i++) {
-                    const int64_t ti = t - i;
-                    if (ti >= 0)
-                        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(wv[i]) : "l"(st + ti * 256) : "memory");
-                    else
-                        wv[i] = SLB_PRE;
-                }
-                uint32_t sum = 0;
-                bool done = false, stall = false;
-#pragma unroll
-                for (int i = 0; i < LBW; i++) {
-                    if (!done && !stall) {
-                        const uint32_t f = wv[i] >> 30;
-                        if (f == 0) stall = true;
-                        else {
-                            sum += wv[i] & SLB_VAL;
-                            done = f == 2;
-                        }
-                    }
-                }
-                if (stall) continue;
-                excl += sum;
-                if (done) break;
-                t -= LBW;
-            }
-            asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st + tile * 256), "r"(SLB_PRE | (excl + cnt)) : "memory");
-            g = excl;
-        }
-        s_gstart[d] = g;
-    }
     __syncthreads();
     const int tile_n = (int)min((int64_t)TILE, a.n - base);
     for (int j = tid; j < tile_n; j += NT) {
-        KT k = s.stage.keys[j];
-        uint32_t p = s.stage.perm[j];
-        uint32_t d = (uint32_t)(k >> a.shift) & 255u;
-        int64_t dst = (int64_t)s_gstart[d] + (j - (int64_t)s_tstart[d]);
+        const KT k = s.stage.keys[j];
+        const uint32_t p = s.stage.perm[j];
+        const uint32_t d = (uint32_t)(k >> a.shift) & 255u;
+        const int64_t dst = (int64_t)s_gstart[d] + (j - (int64_t)s_tstart[d]);
         if (a.out_keys) ((KT*)a.out_keys)[dst] = k;
         if (a.out_perm) a.out_perm[dst] = p;
         if (a.out_perm64) a.out_perm64[dst] = (int64_t)p;
         if (a.out_u || a.out_orig) {
-            uint64_t u = to_u<KT>(k, a.hi_bits);
+            const uint64_t u = to_u<KT>(k, a.hi_bits);
             if (a.out_u) a.out_u[dst] = u;
             if (a.out_orig) {
-                uint64_t v = a.desc ? ~u : u;
+                const uint64_t v = a.desc ? ~u : u;
                 switch (a.orig_dtype) {
                     case TQP_U8: ((uint8_t*)a.out_orig)[dst] = (uint8_t)unordered_i64(v); break;
                     case TQP_I32: ((int32_t*)a.out_orig)[dst] = (int32_t)unordered_i64(v); break;
@@ -300,6 +282,198 @@ __global__ void __launch_bounds__(NT, 3) onesweep_kernel(OnesweepArgs a) {
                 }
             }
         }
+    }
+}
+
+// (4') the same stable scatter as a persistent kernel whose input tiles (keys and
+// permutation) are streamed into shared memory by TMA bulk copies
+// (cp.async.bulk + mbarrier), double-buffered: the stage of tile k is released as
+// soon as its keys are in registers, and tile k+2's copy is issued right away, so
+// HBM reads overlap ranking and write-out. Tail tile: plain loads.
+template <int IN, typename KT>
+struct InKey { using T = KT; };
+template <typename KT> struct InKey<IN_I64, KT> { using T = long long; };
+template <typename KT> struct InKey<IN_I32, KT> { using T = int; };
+template <typename KT> struct InKey<IN_U8, KT> { using T = unsigned char; };
+template <typename KT> struct InKey<IN_U64, KT> { using T = unsigned long long; };
+
+template <typename KT, int IN>
+__device__ __forceinline__ KT conv_key(typename InKey<IN, KT>::T v, bool desc) {
+    if (IN == IN_INTERNAL) return (KT)v;
+    uint64_t u = IN == IN_U64 ? (uint64_t)v : ordered_u64((int64_t)v);
+    return (KT)(desc ? ~u : u);
+}
+
+template <typename KT, int IN, int IPT>
+struct ScatterWork {
+    union {
+        uint32_t whist[NW][256];
+        struct {
+            KT keys[NT * IPT];
+            uint32_t perm[NT * IPT];
+        } sorted;
+    } u;
+    uint32_t tstart[256], gstart[256], w[NW];
+    uint64_t mbar[2];
+};
+
+template <typename KT, int IN, int IPT>
+constexpr int scatter_stage_bytes() {
+    return NT * IPT * (int)sizeof(typename InKey<IN, KT>::T) + (IN == IN_INTERNAL ? NT * IPT * 4 : 0);
+}
+
+template <typename KT, int IN, int IPT>
+constexpr size_t scatter_tma_smem() {
+    return 2 * (size_t)scatter_stage_bytes<KT, IN, IPT>() + sizeof(ScatterWork<KT, IN, IPT>);
+}
+
+template <typename KT, int IN, int IPT>
+__global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles) {
+    constexpr int TILE = NT * IPT;
+    using KIN = typename InKey<IN, KT>::T;
+    constexpr bool HAS_PERM = IN == IN_INTERNAL;
+    constexpr int STAGE_BYTES = scatter_stage_bytes<KT, IN, IPT>();
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t* stage0 = smem;
+    uint8_t* stage1 = smem + STAGE_BYTES;
+    ScatterWork<KT, IN, IPT>& s = *reinterpret_cast<ScatterWork<KT, IN, IPT>*>(smem + 2 * STAGE_BYTES);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(&s.mbar[0], 1);
+        mbar_init(&s.mbar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto full = [&](int64_t t) { return (t + 1) * TILE <= a.n; };
+    auto issue = [&](int64_t t, int st) {   // thread 0
+        uint8_t* dst = st ? stage1 : stage0;
+        mbar_expect_tx(&s.mbar[st], (uint32_t)STAGE_BYTES);
+        bulk_g2s(dst, (const KIN*)a.in_keys + t * TILE, TILE * (uint32_t)sizeof(KIN), &s.mbar[st]);
+        if (HAS_PERM) bulk_g2s(dst + TILE * sizeof(KIN), a.in_perm + t * TILE, TILE * 4u, &s.mbar[st]);
+    };
+    uint32_t uses0 = 0, uses1 = 0;
+    for (int st = 0; st < 2; st++) {
+        const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
+        if (t < n_tiles && full(t)) {
+            if (tid == 0) issue(t, st);
+            if (st) uses1++; else uses0++;
+        }
+    }
+    const unsigned lt = lanemask_lt();
+    for (int64_t k = 0;; k++) {
+        const int64_t tile = blockIdx.x + k * gridDim.x;
+        if (tile >= n_tiles) break;
+        const int st = (int)(k & 1);
+        const int64_t base = tile * TILE;
+        KT key[IPT];
+        uint32_t pm[IPT], rk[IPT];
+        for (int d = lane; d < 256; d += 32) s.u.whist[warp][d] = 0;
+        s.gstart[tid] = a.ct[(tile / CHUNK) * 256 + tid] + a.th[tile * 256 + tid];
+        if (full(tile)) {
+            mbar_wait(&s.mbar[st], ((st ? uses1 : uses0) - 1) & 1);
+            const uint8_t* sp = st ? stage1 : stage0;
+            const KIN* sk = reinterpret_cast<const KIN*>(sp);
+            const uint32_t* spm = reinterpret_cast<const uint32_t*>(sp + TILE * sizeof(KIN));
+#pragma unroll
+            for (int i = 0; i < IPT; i++) {
+                const int q = warp * 32 * IPT + i * 32 + lane;
+                key[i] = conv_key<KT, IN>(sk[q], a.desc);
+                pm[i] = HAS_PERM ? spm[q] : (uint32_t)(base + q);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < IPT; i++) {
+                const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+                if (pos < a.n) {
+                    key[i] = conv_key<KT, IN>(((const KIN*)a.in_keys)[pos], a.desc);
+                    pm[i] = HAS_PERM ? a.in_perm[pos] : (uint32_t)pos;
+                } else {
+                    key[i] = 0;
+                    pm[i] = 0;
+                }
+            }
+        }
+        __syncthreads();   // stage st consumed by every thread; whist zeroed
+        {
+            const int64_t t2 = tile + 2 * (int64_t)gridDim.x;
+            if (t2 < n_tiles && full(t2)) {
+                if (tid == 0) {
+                    fence_proxy_async();
+                    issue(t2, st);
+                }
+                if (st) uses1++; else uses0++;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < IPT; i++) {
+            const bool valid = base + warp * 32 * IPT + i * 32 + lane < a.n;
+            const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
+            unsigned peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+            for (int b = 0; b < 8; b++) {
+                const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+                peers &= ((d >> b) & 1u) ? bb : ~bb;
+            }
+            const uint32_t leader = 31 - __clz(peers);
+            uint32_t old = 0;
+            if (valid && lane == leader) old = atomicAdd(&s.u.whist[warp][d], (uint32_t)__popc(peers));
+            rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
+        }
+#pragma unroll
+        for (int i = 0; i < IPT; i++) {
+            const uint32_t b = __shfl_sync(0xffffffffu, rk[i] & 0xFFFFu, (rk[i] >> 16) & 31u);
+            rk[i] = b + (rk[i] >> 24);
+        }
+        __syncthreads();
+        uint32_t cnt = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) {
+            const uint32_t c = s.u.whist[w][tid];
+            s.u.whist[w][tid] = cnt;
+            cnt += c;
+        }
+        s.tstart[tid] = block_excl_scan256(cnt, s.w);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; i++) {
+            if (base + warp * 32 * IPT + i * 32 + lane < a.n) {
+                const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
+                rk[i] = s.tstart[d] + s.u.whist[warp][d] + rk[i];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < IPT; i++) {
+            if (base + warp * 32 * IPT + i * 32 + lane < a.n) {
+                s.u.sorted.keys[rk[i]] = key[i];
+                s.u.sorted.perm[rk[i]] = pm[i];
+            }
+        }
+        __syncthreads();
+        const int tile_n = (int)min((int64_t)TILE, a.n - base);
+        for (int j = tid; j < tile_n; j += NT) {
+            const KT kk = s.u.sorted.keys[j];
+            const uint32_t p = s.u.sorted.perm[j];
+            const uint32_t d = (uint32_t)(kk >> a.shift) & 255u;
+            const int64_t dst = (int64_t)s.gstart[d] + (j - (int64_t)s.tstart[d]);
+            if (a.out_keys) ((KT*)a.out_keys)[dst] = kk;
+            if (a.out_perm) a.out_perm[dst] = p;
+            if (a.out_perm64) a.out_perm64[dst] = (int64_t)p;
+            if (a.out_u || a.out_orig) {
+                const uint64_t u = to_u<KT>(kk, a.hi_bits);
+                if (a.out_u) a.out_u[dst] = u;
+                if (a.out_orig) {
+                    const uint64_t v = a.desc ? ~u : u;
+                    switch (a.orig_dtype) {
+                        case TQP_U8: ((uint8_t*)a.out_orig)[dst] = (uint8_t)unordered_i64(v); break;
+                        case TQP_I32: ((int32_t*)a.out_orig)[dst] = (int32_t)unordered_i64(v); break;
+                        case TQP_I64: ((int64_t*)a.out_orig)[dst] = unordered_i64(v); break;
+                        default: ((uint64_t*)a.out_orig)[dst] = v; break;
+                    }
+                }
+            }
+        }
+        __syncthreads();   // sorted/whist/gstart reused by the next tile
     }
 }
 
@@ -341,17 +515,18 @@ static void dispatch_in(int mode, F&& f) {
         case IN_I64: f(std::integral_constant<int, IN_I64>()); break;
         case IN_I32: f(std::integral_constant<int, IN_I32>()); break;
         case IN_U8: f(std::integral_constant<int, IN_U8>()); break;
+        case IN_INTERNAL: f(std::integral_constant<int, IN_INTERNAL>()); break;
         default: f(std::integral_constant<int, IN_U64>()); break;
     }
 }
 
 template <typename KT>
 static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o,
-                       const PassPlan& pp, const uint32_t* ghist) {
+                       const int* shifts, int P) {
     constexpr int IPT = sizeof(KT) == 4 ? 16 : 12;
     constexpr int TILE = NT * IPT;
     const int64_t tiles = ceil_div(n, TILE);
-    const int P = pp.n;
+    const int64_t chunks = ceil_div(tiles, CHUNK);
     DevBuf<KT> kb[2];
     DevBuf<uint32_t> pb[2];
     const bool need_key_final = o.want_internal;
@@ -367,14 +542,23 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         if (kused) kb[b].alloc(ctx, n);
         if (pused) pb[b].alloc(ctx, n);
     }
-    DevBuf<uint32_t> lb(ctx, (size_t)P * tiles * 256);
-    DevBuf<unsigned long long> counters(ctx, P);
-    lb.zero();
-    counters.zero();
-    const int mode = in_mode(dtype);
+    DevBuf<uint32_t> th(ctx, (size_t)tiles * 256);
+    DevBuf<uint32_t> ct(ctx, (size_t)chunks * 256);
+    const int mode0 = in_mode(dtype);
     for (int p = 0; p < P; p++) {
-        OnesweepArgs a{};
-        a.in_keys = p == 0 ? keys : kb[(p - 1) % 2].get();
+        const void* in = p == 0 ? keys : kb[(p - 1) % 2].get();
+        const int mode = p == 0 ? mode0 : (int)IN_INTERNAL;
+        const double kin = p == 0 ? (double)dtype_size(dtype) : (double)sizeof(KT);
+        dispatch_in(mode, [&](auto m) {
+            launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT>, dim3((unsigned)tiles),
+                   dim3(NT), 0, in, n, shifts[p], desc, th.get());
+        });
+        ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 1024.0 * (double)tiles);
+        launch(ctx, "tqp_sort_scan", scan_tiles_kernel, dim3((unsigned)chunks), dim3(NT), 0, th.get(), tiles, ct.get());
+        launch(ctx, "tqp_sort_scan", scan_chunks_kernel, dim3(1), dim3(NT), 0, ct.get(), chunks);
+        ctx->add_bytes("tqp_sort_scan", 2048.0 * (double)tiles + 3072.0 * (double)chunks);
+        ScatterArgs a{};
+        a.in_keys = in;
         a.in_perm = p == 0 ? nullptr : pb[(p - 1) % 2].get();
         const bool last = p == P - 1;
         a.out_keys = (!last || need_key_final) ? kb[p % 2].get() : nullptr;
@@ -385,28 +569,33 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
             a.out_perm64 = o.perm64;
             a.out_u = o.sorted_u;
         }
-        a.ghist = ghist + p * 256;
-        a.lb = lb.get() + (size_t)p * tiles * 256;
-        a.counter = counters.get() + p;
+        a.th = th.get();
+        a.ct = ct.get();
         a.n = n;
-        a.shift = pp.shift[p];
+        a.shift = shifts[p];
         a.desc = desc;
         a.hi_bits = o.and_bits & 0xFFFFFFFF00000000ull;
         {   // algorithmic bytes of this pass: keys + permutation in, requested outputs out
-            double rd = p == 0 ? (double)dtype_size(dtype) : (double)(sizeof(KT) + 4);
-            double wr = (a.out_keys ? sizeof(KT) : 0) + (a.out_perm ? 4 : 0) + (a.out_orig ? dtype_size(dtype) : 0) +
-                        (a.out_perm64 ? 8 : 0) + (a.out_u ? 8 : 0);
-            ctx->add_bytes("tqp_onesweep", (rd + wr) * (double)n);
+            const double rd = kin + (p == 0 ? 0.0 : 4.0);
+            const double wr = (a.out_keys ? sizeof(KT) : 0) + (a.out_perm ? 4 : 0) +
+                              (a.out_orig ? dtype_size(dtype) : 0) + (a.out_perm64 ? 8 : 0) + (a.out_u ? 8 : 0);
+            ctx->add_bytes("tqp_sort_scatter", (rd + wr) * (double)n);
         }
-        if (p == 0) {
-            dispatch_in(mode, [&](auto m) {
-                launch(ctx, "tqp_onesweep", onesweep_kernel<KT, decltype(m)::value, IPT>, dim3((unsigned)tiles),
-                       dim3(NT), 0, a);
-            });
-        } else {
-            launch(ctx, "tqp_onesweep", onesweep_kernel<KT, IN_INTERNAL, IPT>, dim3((unsigned)tiles), dim3(NT), 0,
-                   a);
-        }
+        const bool aligned = ((uintptr_t)in % 16 == 0) && (p == 0 || (uintptr_t)a.in_perm % 16 == 0);
+        dispatch_in(mode, [&](auto m) {
+            constexpr int INM = decltype(m)::value;
+            if (aligned) {
+                constexpr size_t smem = scatter_tma_smem<KT, INM, IPT>();
+                auto* kfn = scatter_tma_kernel<KT, INM, IPT>;
+                set_smem(kfn, smem);
+                int occ = 1;
+                TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem));
+                const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
+                launch(ctx, "tqp_sort_scatter", kfn, dim3((unsigned)grid), dim3(NT), smem, a, tiles);
+            } else {
+                launch(ctx, "tqp_sort_scatter", scatter_kernel<KT, INM, IPT>, dim3((unsigned)tiles), dim3(NT), 0, a);
+            }
+        });
     }
     const int fb = (P - 1) % 2;
     if (need_key_final) {
@@ -425,8 +614,9 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     TQP_CUDA(cudaMemsetAsync(ao.get(), 0xFF, 8, ctx->stream));
     TQP_CUDA(cudaMemsetAsync(ao.get() + 1, 0, 8, ctx->stream));
     dispatch_in(mode, [&](auto m) {
-        launch(ctx, "tqp_sort_andor", andor_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc,
-               ao.get());
+        if constexpr (decltype(m)::value != IN_INTERNAL)
+            launch(ctx, "tqp_sort_andor", andor_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc,
+                   ao.get());
     });
     ctx->add_bytes("tqp_sort_andor", (double)n * dtype_size(dtype));
     uint64_t h[2];
@@ -435,11 +625,11 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     o.or_bits = h[1];
     const uint64_t diff = h[0] ^ h[1];
     o.k32 = (diff >> 32) == 0;
-    PassPlan pp{};
+    int shifts[8], P = 0;
     for (int b = 0; b < 8; b++)
-        if ((diff >> (8 * b)) & 0xFF) pp.shift[pp.n++] = 8 * b;
-    o.passes = pp.n;
-    if (pp.n == 0) {
+        if ((diff >> (8 * b)) & 0xFF) shifts[P++] = 8 * b;
+    o.passes = P;
+    if (P == 0) {
         if (o.want_internal || o.want_perm32) o.perm32.alloc(ctx, n);
         if (o.want_internal) {
             if (o.k32) o.keys32.alloc(ctx, n); else o.keys64.alloc(ctx, n);
@@ -449,24 +639,21 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
                        (double)n * (dtype_size(dtype) + (o.sorted_orig ? dtype_size(dtype) : 0) + (o.perm64 ? 8 : 0) +
                                     (o.sorted_u ? 8 : 0) + (o.perm32.n ? 4 : 0) + (o.want_internal ? (o.k32 ? 4 : 8) : 0)));
         dispatch_in(mode, [&](auto m) {
-            if (o.k32)
-                launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint32_t, decltype(m)::value>, dim3(g), dim3(NT),
-                       0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys32.get(), o.perm32.get());
-            else
-                launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint64_t, decltype(m)::value>, dim3(g), dim3(NT),
-                       0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys64.get(), o.perm32.get());
+            if constexpr (decltype(m)::value != IN_INTERNAL) {
+                if (o.k32)
+                    launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint32_t, decltype(m)::value>, dim3(g),
+                           dim3(NT), 0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys32.get(),
+                           o.perm32.get());
+                else
+                    launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint64_t, decltype(m)::value>, dim3(g),
+                           dim3(NT), 0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys64.get(),
+                           o.perm32.get());
+            }
         });
         return;
     }
-    DevBuf<uint32_t> ghist(ctx, (size_t)pp.n * 256);
-    ghist.zero();
-    dispatch_in(mode, [&](auto m) {
-        launch(ctx, "tqp_sort_hist", hist_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc, pp,
-               ghist.get());
-    });
-    ctx->add_bytes("tqp_sort_hist", (double)n * dtype_size(dtype));
-    if (o.k32) run_passes<uint32_t>(ctx, keys, dtype, n, desc, o, pp, ghist.get());
-    else run_passes<uint64_t>(ctx, keys, dtype, n, desc, o, pp, ghist.get());
+    if (o.k32) run_passes<uint32_t>(ctx, keys, dtype, n, desc, o, shifts, P);
+    else run_passes<uint64_t>(ctx, keys, dtype, n, desc, o, shifts, P);
 }
 
 }  // namespace tqp
