@@ -215,8 +215,10 @@ __device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, int64_t tile
     while (true) {
         int64_t idx = win - lane;
         uint64_t w = (idx >= 0) ? lb_load(status + idx) : (LB_PRE | (identity & LB_VAL));
-        // all lanes must have a ready word before reducing
+        // all lanes must have a ready word before reducing; back off while waiting so
+        // spinning warps do not steal issue slots and L2 bandwidth from the producers
         while (__any_sync(0xffffffffu, (w >> 62) == 0)) {
+            __nanosleep(64);
             if ((w >> 62) == 0) w = lb_load(status + idx);
         }
         unsigned pre = __ballot_sync(0xffffffffu, (w >> 62) == 2);

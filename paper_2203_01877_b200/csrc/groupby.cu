@@ -526,6 +526,192 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
     if (ovf) atomicOr(a.overflow, 1);
 }
 
+// No group keys (e.g. Q6's fused filter + sum): the tile sort is the identity and
+// there is one segment, so every thread keeps its (op, expression) accumulators in
+// registers across all the tiles of the persistent loop; one partial record per CTA.
+struct NoKeyAcc {
+    uint64_t lo[PCH];
+    int64_t hi[PCH];
+    int64_t count;
+    int ovf;
+};
+
+__device__ __forceinline__ void process_tile_nokey(const Phase1Args& a, const uint8_t* st, int64_t t, NoKeyAcc& acc) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int nrows = (int)min((int64_t)GTILE, a.n - t * GTILE);
+    bool pass[GPT];
+#pragma unroll
+    for (int i = 0; i < GPT; i++) pass[i] = i * GNT + tid < nrows;
+    for (int q = 0; q < a.n_preds; q++) {
+        const int c = a.pcol[q];
+        int64_t x[GPT];
+        const uint8_t* col = st + a.uoff[c];
+        switch (a.udt[c]) {
+            case TQP_U8:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) x[i] = (int64_t)col[i * GNT + tid];
+                break;
+            case TQP_I32:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid];
+                break;
+            default:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid];
+        }
+        const int64_t v = a.pval[q];
+        switch (a.pop[q]) {
+            case TQP_LT:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] < v;
+                break;
+            case TQP_LE:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] <= v;
+                break;
+            case TQP_GT:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] > v;
+                break;
+            case TQP_GE:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] >= v;
+                break;
+            case TQP_EQ:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] == v;
+                break;
+            default:
+#pragma unroll
+                for (int i = 0; i < GPT; i++) pass[i] &= x[i] != v;
+        }
+    }
+    bool anyp = false;
+#pragma unroll
+    for (int i = 0; i < GPT; i++) {
+        acc.count += pass[i] ? 1 : 0;
+        anyp |= pass[i];
+    }
+    if (!__any_sync(0xffffffffu, anyp)) return;   // nothing passes in this warp's rows
+#pragma unroll
+    for (int jj = 0; jj < PCH; jj++) {
+        if (jj >= a.n_pairs) break;
+        const int op = a.prop[jj];
+        const int nf = a.pnf[jj];
+        int64_t vv[GPT];
+        bool ov[GPT];
+#pragma unroll
+        for (int i = 0; i < GPT; i++) { vv[i] = 1; ov[i] = false; }
+        for (int f = 0; f < nf; f++) {
+            const int c = a.pfc[jj][f];
+            const uint8_t* col = st + a.uoff[c];
+            const int64_t add = a.padd[jj][f];
+            const bool neg = a.psign[jj][f] < 0;
+            int64_t x[GPT];
+            switch (a.udt[c]) {
+                case TQP_U8:
+#pragma unroll
+                    for (int i = 0; i < GPT; i++) x[i] = (int64_t)col[i * GNT + tid];
+                    break;
+                case TQP_I32:
+#pragma unroll
+                    for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid];
+                    break;
+                default:
+#pragma unroll
+                    for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid];
+            }
+#pragma unroll
+            for (int i = 0; i < GPT; i++) {
+                int64_t tt;
+                if (neg) {
+                    tt = add - x[i];
+                    ov[i] |= ((add ^ x[i]) & (add ^ tt)) < 0;
+                } else {
+                    tt = add + x[i];
+                    ov[i] |= ((add ^ tt) & (x[i] ^ tt)) < 0;
+                }
+                if (f == 0) {
+                    vv[i] = tt;
+                } else if ((uint64_t)(vv[i] + 0x80000000ll) < 0x100000000ull &&
+                           (uint64_t)(tt + 0x80000000ll) < 0x100000000ull) {
+                    vv[i] = (int64_t)(int32_t)vv[i] * (int64_t)(int32_t)tt;
+                } else {
+                    const int64_t lo = vv[i] * tt;
+                    ov[i] |= __mul64hi(vv[i], tt) != (lo >> 63);
+                    vv[i] = lo;
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < GPT; i++) {
+            if (!pass[i]) continue;
+            if (ov[i]) acc.ovf = 1;
+            const int64_t v = vv[i];
+            if (op == P_SUM) { acc.lo[jj] += (uint64_t)(uint32_t)v; acc.hi[jj] += (v >> 32); }
+            else if (op == P_MIN) acc.lo[jj] = (uint64_t)min((int64_t)acc.lo[jj], v);
+            else acc.lo[jj] = (uint64_t)max((int64_t)acc.lo[jj], v);
+        }
+    }
+    (void)lane;
+}
+
+// End of the persistent loop: reduce the CTA's register accumulators and emit one
+// partial record (key 0) if any row passed.
+__device__ void flush_nokey(const Phase1Args& a, NoKeyAcc& acc, Work& w) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ int64_t s_cnt[GNW];
+    __shared__ uint64_t s_lo[GNW][PCH];
+    __shared__ int64_t s_hi[GNW][PCH];
+    __shared__ int64_t s_pb;
+    int64_t cnt = acc.count;
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+#pragma unroll
+    for (int jj = 0; jj < PCH; jj++) {
+        const int op = jj < a.n_pairs ? a.prop[jj] : P_SUM;
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t xl = __shfl_xor_sync(0xffffffffu, acc.lo[jj], o);
+            const int64_t xh = __shfl_xor_sync(0xffffffffu, acc.hi[jj], o);
+            if (op == P_SUM) { acc.lo[jj] += xl; acc.hi[jj] += xh; }
+            else if (op == P_MIN) acc.lo[jj] = (uint64_t)min((int64_t)acc.lo[jj], (int64_t)xl);
+            else acc.lo[jj] = (uint64_t)max((int64_t)acc.lo[jj], (int64_t)xl);
+        }
+        if (lane == 0) { s_lo[warp][jj] = acc.lo[jj]; s_hi[warp][jj] = acc.hi[jj]; }
+    }
+    if (lane == 0) s_cnt[warp] = cnt;
+    if (acc.ovf) atomicOr(a.overflow, 1);
+    __syncthreads();
+    if (tid == 0) {
+        int64_t c = 0;
+        for (int ww = 0; ww < GNW; ww++) c += s_cnt[ww];
+        int64_t pb = -1;
+        if (c > 0) {
+            pb = (int64_t)atomicAdd(a.P_counter, 1ull);
+            if (pb + 1 > a.cap) { atomicOr(a.overflow, 2); pb = -1; }
+        }
+        if (pb >= 0) {
+            a.pkey[pb] = 0;
+            a.pcount[pb] = c;
+        }
+        s_pb = pb;
+    }
+    __syncthreads();
+    const int64_t pb = s_pb;
+    if (pb >= 0 && tid < a.n_pairs && tid < PCH) {
+        const int jj = tid, op = a.prop[jj];
+        uint64_t lo = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+        int64_t hi = 0;
+        for (int ww = 0; ww < GNW; ww++) {
+            if (op == P_SUM) { lo += s_lo[ww][jj]; hi += s_hi[ww][jj]; }
+            else if (op == P_MIN) lo = (uint64_t)min((int64_t)lo, (int64_t)s_lo[ww][jj]);
+            else lo = (uint64_t)max((int64_t)lo, (int64_t)s_lo[ww][jj]);
+        }
+        a.plo[jj][pb] = lo;
+        if (op == P_SUM) a.phi[jj][pb] = hi;
+    }
+    (void)w;
+}
+
 __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* stage[2] = {smem, smem + a.stage_bytes};
@@ -545,6 +731,16 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
             bulk_g2s(stage[s] + a.uoff[c], (const uint8_t*)a.ucol[c] + t * GTILE * es, GTILE * es, &w.mbar[s]);
         }
     };
+    const bool nokey = a.n_keys == 0 && a.n_pairs <= PCH;
+    NoKeyAcc nacc;
+#pragma unroll
+    for (int jj = 0; jj < PCH; jj++) {
+        const int op = jj < a.n_pairs ? a.prop[jj] : P_SUM;
+        nacc.lo[jj] = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+        nacc.hi[jj] = 0;
+    }
+    nacc.count = 0;
+    nacc.ovf = 0;
     uint32_t uses[2] = {0, 0};
     for (int s = 0; s < 2; s++) {
         const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
@@ -577,7 +773,8 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
             }
             __syncthreads();
         }
-        process_tile(a, stage[s], w, t);
+        if (nokey) process_tile_nokey(a, stage[s], t, nacc);
+        else process_tile(a, stage[s], w, t);
         __syncthreads();   // every thread is done with stage s
         const int64_t t2 = t + 2 * (int64_t)gridDim.x;
         if (t2 < a.n_tiles && eligible(t2)) {
@@ -588,6 +785,7 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
             uses[s]++;
         }
     }
+    if (nokey) flush_nokey(a, nacc, w);
 }
 
 // Phase 2a: group ids over the sorted partial keys (segment boundaries).

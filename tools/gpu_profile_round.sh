@@ -1,0 +1,12 @@
+# Round profiling: full bench line, ncu launch list, ncu --set full of the top kernels.
+# Usage (on the GPU box via gpurun): bash tools/gpu_profile_round.sh <tag>
+TAG=${1:-r01}
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/${TAG}_smi.txt
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/${TAG}_bench_ref.json 2>> gpurun_out/${TAG}_bench.err
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
+timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
+timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
+for K in gb_phase1 scatter_tma probe_kernel expand_kernel filter_kernel rle_kernel intersect_kernel; do timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -c 2 -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_full_$K.log 2>&1; done
+echo done

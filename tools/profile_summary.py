@@ -1,0 +1,87 @@
+"""Turn a round's ncu captures into profiles/: ncu_traffic.json (dram bytes per launch per
+libtqp kernel name, read by bench.py for roofline.traffic), a launch-share table and a
+markdown summary. Usage: python tools/profile_summary.py <tag>"""
+import csv, io, json, os, subprocess, sys, collections
+
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
+G = "gpurun_out"
+NAME = [("gb_phase1", "tqp_groupby_tile"), ("scatter_tma", "tqp_sort_scatter"), ("scatter_kernel", "tqp_sort_scatter"),
+        ("probe_kernel", "tqp_pkfk_probe"), ("expand_kernel", "tqp_smj_expand"), ("filter_kernel", "tqp_filter"),
+        ("tile_hist", "tqp_sort_tile_hist"), ("scan_tiles", "tqp_sort_scan"), ("scan_chunks", "tqp_sort_scan"),
+        ("rle_kernel", "tqp_smj_rle"), ("intersect_kernel", "tqp_smj_intersect"), ("cum_kernel", "tqp_smj_cumsum"),
+        ("andor_kernel", "tqp_sort_andor"), ("gb_gid", "tqp_groupby_gid"), ("gb_acc", "tqp_groupby_accumulate"),
+        ("gb_finalize", "tqp_groupby_finalize"), ("bucket_ends", "tqp_pkfk_bucket_ends"), ("scan_max", "tqp_scan_max"),
+        ("pack_records", "tqp_pkfk_records"), ("trivial_sort", "tqp_sort_trivial"), ("gb_init", "tqp_groupby_init")]
+
+
+def tqp_name(k):
+    for pat, n in NAME:
+        if pat in k:
+            return n
+    return None
+
+
+def launches():
+    rows = list(csv.reader(open(f"{G}/{TAG}_launches.csv")))
+    h = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    hdr = rows[h]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.OrderedDict()
+    for r in rows[h + 1:]:
+        if len(r) <= vi:
+            continue
+        v = float(r[vi].replace(",", ""))
+        v *= {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
+        n = tqp_name(r[ki]) or ("torch/other: " + r[ki].split("(")[0][-50:])
+        a = agg.setdefault(n, [0.0, 0])
+        a[0] += v
+        a[1] += 1
+    return agg
+
+
+def full(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    hdr, units = rows[0], rows[1]
+    col = lambda k: hdr.index(k)
+    res = collections.defaultdict(list)
+    for d in rows[2:]:
+        n = tqp_name(d[col("Kernel Name")])
+        def val(k):
+            v = float(d[col(k)].replace(",", ""))
+            u = units[col(k)]
+            return v * {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "ms": 1e3, "msecond": 1e3,
+                        "us": 1.0, "usecond": 1.0, "ns": 1e-3, "nsecond": 1e-3}.get(u, 1.0)
+        res[n].append({"time_us": val("gpu__time_duration.sum"), "dram_read": val("dram__bytes_read.sum"),
+                       "dram_write": val("dram__bytes_write.sum"),
+                       "warps_active_pct": float(d[col("sm__warps_active.avg.pct_of_peak_sustained_active")]),
+                       "issue_active_pct": float(d[col("smsp__issue_active.avg.pct_of_peak_sustained_active")]),
+                       "regs": d[col("launch__registers_per_thread")], "grid": d[col("launch__grid_size")]})
+    return res
+
+
+os.makedirs("profiles", exist_ok=True)
+L = launches()
+tot = sum(v[0] for v in L.values())
+tq = sum(v[0] for k, v in L.items() if not k.startswith("torch"))
+import glob
+F = collections.defaultdict(list)
+for rep in sorted(glob.glob(f"{G}/{TAG}_full*.ncu-rep")):
+    for k, v in full(rep).items():
+        F[k] += v
+traffic = {k: sum(x["dram_read"] + x["dram_write"] for x in v) / len(v) for k, v in F.items() if k}
+json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
+with open(f"profiles/ncu_summary_{TAG}.md", "w") as f:
+    f.write(f"# ncu summary ({TAG})\n\nCommand: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline` on one B200 "
+            f"(ncu, `--clock-control none`; cold-cache serialised launches: compare shares, not absolutes).\n\n")
+    f.write("## Launch list: device time by libtqp kernel (share of libtqp time)\n\n| kernel | us | launches | share |\n|---|---|---|---|\n")
+    for k, (v, c) in sorted(L.items(), key=lambda kv: -kv[1][0]):
+        if not k.startswith("torch"):
+            f.write(f"| {k} | {v:.0f} | {c} | {100*v/tq:.1f}% |\n")
+    f.write(f"\nlibtqp kernels: {tq:.0f} us of {tot:.0f} us total (rest: torch data generation / copies in the bench harness).\n\n")
+    f.write("## `--set full` captures (per launch)\n\n| kernel | time us | DRAM read MB | DRAM write MB | warps active % | issue active % | regs | grid |\n|---|---|---|---|---|---|---|---|\n")
+    for k, v in F.items():
+        for x in v:
+            f.write(f"| {k} | {x['time_us']:.0f} | {x['dram_read']/1e6:.1f} | {x['dram_write']/1e6:.1f} | "
+                    f"{x['warps_active_pct']:.1f} | {x['issue_active_pct']:.1f} | {x['regs']} | {x['grid']} |\n")
+print(open(f"profiles/ncu_summary_{TAG}.md").read())
