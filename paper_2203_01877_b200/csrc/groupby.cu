@@ -29,9 +29,9 @@ struct tqp_groupby_plan {
     int64_t G = 0;
     int n_keys = 0, n_aggs = 0, n_pairs = 0;
     int kdt[TQP_MAX_KEYS];
-    int kshift[TQP_MAX_KEYS];
     int aop[TQP_MAX_AGGS];
     int apair[TQP_MAX_AGGS];      // aggregate -> (op, expression) pair (-1 for COUNT)
+    tqp::DevBuf<unsigned long long> krange;   // per key column min (0..7) / max (8..15)
     int pop[TQP_MAX_AGGS];        // pair op: 0 sum, 1 min, 2 max
     bool empty_global = false;    // n_keys == 0 and no passing row
     tqp::DevBuf<uint64_t> gkey;
@@ -51,6 +51,7 @@ constexpr int MAXU = 16;           // distinct referenced columns
 constexpr int P_SUM = 0, P_MIN = 1, P_MAX = 2;
 constexpr int PCH = 8;             // (op, expression) pairs reduced per traversal
 constexpr int UCAP = 64;           // runs per tile with shared-memory accumulators
+constexpr int CBINS = 2048;        // key range of a tile sorted by a one-pass counting sort
 
 struct Phase1Args {
     int n_ucols;
@@ -60,7 +61,7 @@ struct Phase1Args {
     int stage_bytes;
     int n_keys;
     int kcol[TQP_MAX_KEYS];
-    int kshift[TQP_MAX_KEYS];
+    const unsigned long long* krange;   // per key column min / max (device)
     int n_preds;
     int pcol[TQP_MAX_PREDS];
     int pop[TQP_MAX_PREDS];
@@ -99,6 +100,87 @@ __device__ __forceinline__ uint64_t key_part(int64_t v, int dt) {
         case TQP_U8: return (uint64_t)v & 0xFFull;
         case TQP_I32: return (uint64_t)((uint32_t)v ^ 0x80000000u);
         default: return (uint64_t)v ^ 0x8000000000000000ull;
+    }
+}
+
+// Per key column: min / max of the order-preserving unsigned key value, so each
+// column is packed as (value - min) in bits(max - min) bits (column 0 most
+// significant). Monotone per column, so the packed order is the lexicographic
+// order of the tuples (reading R12) and small-domain keys become small bins.
+struct KRArgs {
+    int n_keys;
+    const void* kcol[TQP_MAX_KEYS];
+    int kdt[TQP_MAX_KEYS];
+    int64_t n;
+};
+
+__global__ void key_range_kernel(KRArgs a, unsigned long long* kr) {   // kr[k] = min, kr[8 + k] = max
+    __shared__ unsigned long long smin[TQP_MAX_KEYS][GNT / 32], smax[TQP_MAX_KEYS][GNT / 32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+    for (int k = 0; k < a.n_keys; k++) {
+        unsigned long long mn = ~0ull, mx = 0;
+        const int dt = a.kdt[k];
+        const int per = dt == TQP_U8 ? 16 : dt == TQP_I32 ? 4 : 2;   // elements per 16-byte load
+        const int64_t nv = ((uintptr_t)a.kcol[k] % 16 == 0) ? a.n / per : 0;
+        for (int64_t v = gt; v < nv; v += gs) {   // vectorised body: 16 bytes per load, streamed
+            const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + v);
+            const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
+            if (dt == TQP_U8) {
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const unsigned long long x = (wd[j >> 2] >> (8 * (j & 3))) & 0xFFu;
+                    mn = min(mn, x);
+                    mx = max(mx, x);
+                }
+            } else if (dt == TQP_I32) {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const unsigned long long x = wd[j] ^ 0x80000000u;
+                    mn = min(mn, x);
+                    mx = max(mx, x);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 2; j++) {
+                    const unsigned long long x = (((unsigned long long)wd[2 * j + 1] << 32) | wd[2 * j]) ^ 0x8000000000000000ull;
+                    mn = min(mn, x);
+                    mx = max(mx, x);
+                }
+            }
+        }
+        for (int64_t i = nv * per + gt; i < a.n; i += gs) {   // tail (or unaligned column)
+            const unsigned long long x = key_part(load_as_i64(a.kcol[k], dt, i), dt);
+            mn = min(mn, x);
+            mx = max(mx, x);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (lane == 0) { smin[k][warp] = mn; smax[k][warp] = mx; }
+    }
+    __syncthreads();
+    if (threadIdx.x < a.n_keys) {
+        const int k = threadIdx.x;
+        unsigned long long mn = ~0ull, mx = 0;
+        for (int w = 0; w < (int)(blockDim.x / 32); w++) { mn = min(mn, smin[k][w]); mx = max(mx, smax[k][w]); }
+        atomicMin(&kr[k], mn);
+        atomicMax(&kr[8 + k], mx);
+    }
+}
+
+// shift / width / min of every key column from the device-resident ranges
+__device__ __forceinline__ void key_layout(const unsigned long long* kr, int n_keys, uint64_t* kmin, int* shift,
+                                           int* width) {
+    int off = 0;
+    for (int k = n_keys - 1; k >= 0; k--) {
+        const uint64_t mn = kr[k], mx = kr[8 + k];
+        const int wdt = mx > mn ? 64 - __clzll(mx - mn) : 0;
+        kmin[k] = mx >= mn ? mn : 0;
+        width[k] = wdt;
+        shift[k] = off;
+        off += wdt;
     }
 }
 
@@ -149,6 +231,8 @@ struct Work {   // shared-memory working set of one tile (after the two column s
     uint32_t tstart[256];
     uint32_t s_w[GNW];
     uint64_t s_min[GNW], s_max[GNW];
+    uint64_t s_kmin[TQP_MAX_KEYS];
+    int s_kshift[TQP_MAX_KEYS];
     uint64_t mbar[2];
     int64_t s_pb;
     uint32_t s_m, s_U;
@@ -271,25 +355,28 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
                 for (int i = 0; i < GPT; i++) pass[i] &= x[i] != v;
         }
     }
-    // packed key, column 0 most significant (reading R12)
+    // packed key: column 0 most significant (reading R12), each column as (value - min)
     for (int c = 0; c < a.n_keys; c++) {
         const int u = a.kcol[c];
         const uint8_t* col = st + a.uoff[u];
-        const int sh = a.kshift[c];
+        const int sh = w.s_kshift[c];
+        const uint64_t mn = w.s_kmin[c];
         switch (a.udt[u]) {
             case TQP_U8:
 #pragma unroll
-                for (int i = 0; i < GPT; i++) key[i] |= (uint64_t)col[i * GNT + tid] << sh;
+                for (int i = 0; i < GPT; i++) key[i] |= ((uint64_t)col[i * GNT + tid] - mn) << sh;
                 break;
             case TQP_I32:
 #pragma unroll
                 for (int i = 0; i < GPT; i++)
-                    key[i] |= (uint64_t)((uint32_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid] ^ 0x80000000u) << sh;
+                    key[i] |= ((uint64_t)((uint32_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid] ^ 0x80000000u) - mn)
+                              << sh;
                 break;
             default:
 #pragma unroll
                 for (int i = 0; i < GPT; i++)
-                    key[i] |= ((uint64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid] ^ 0x8000000000000000ull) << sh;
+                    key[i] |= (((uint64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid] ^ 0x8000000000000000ull) - mn)
+                              << sh;
         }
     }
 #pragma unroll
@@ -309,9 +396,85 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
     kmin = ~0ull;
     kmax = 0;
     for (int ww = 0; ww < GNW; ww++) { kmin = min(kmin, w.s_min[ww]); kmax = max(kmax, w.s_max[ww]); }
-    // 2. compact passing rows into sort buffer 0 (warp-aggregated slot claims)
     const unsigned lt = lanemask_lt();
+    const int p0 = tid * GPT;
+    int m;
+    const uint64_t* sk;
+    const uint16_t* si;
+    if (kmax >= kmin && kmax - kmin < (uint64_t)CBINS) {
+        // 2'-4'. small key range: one-pass counting sort. Each passing row claims a
+        //        rank in its key's bin (warp-aggregated shared atomics), the bin scan
+        //        gives bin starts, and the non-empty bins are exactly the segments
+        //        (uniqueConsecutive) -- no compaction pass, no LSD passes, no head scan.
+        uint32_t* cnt = &w.whist[0][0];
+        uint16_t* rid = reinterpret_cast<uint16_t*>(w.skey[1]);
+        const int R = (int)(kmax - kmin) + 1;
+        for (int b = tid; b < R; b += GNT) cnt[b] = 0;
+        __syncthreads();
+        uint32_t rk[GPT], dk[GPT];
 #pragma unroll
+        for (int i = 0; i < GPT; i++) {
+            dk[i] = pass[i] ? (uint32_t)(key[i] - kmin) : (0x80000000u | (uint32_t)lane);
+            const unsigned peers = __match_any_sync(0xffffffffu, dk[i]);
+            const uint32_t leader = 31 - __clz(peers);
+            uint32_t old = 0;
+            if (pass[i] && lane == leader) old = atomicAdd(&cnt[dk[i]], (uint32_t)__popc(peers));
+            rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
+        }
+#pragma unroll
+        for (int i = 0; i < GPT; i++) {
+            const uint32_t b = __shfl_sync(0xffffffffu, rk[i] & 0xFFFFu, (rk[i] >> 16) & 31u);
+            rk[i] = b + (rk[i] >> 24);
+        }
+        __syncthreads();
+        // bin scan: thread t owns bins [8t, 8t+8); (rows, non-empty bins) packed in one word
+        constexpr int BPT = CBINS / GNT;
+        uint32_t c[BPT], rows = 0, runs = 0;
+#pragma unroll
+        for (int j = 0; j < BPT; j++) {
+            const int bidx = tid * BPT + j;
+            c[j] = bidx < R ? cnt[bidx] : 0u;
+            rows += c[j];
+            runs += c[j] ? 1u : 0u;
+        }
+        const uint32_t ex = bscan256(rows | (runs << 16), w.s_w);
+        uint32_t start = ex & 0xFFFFu, run = ex >> 16;
+#pragma unroll
+        for (int j = 0; j < BPT; j++) {
+            const int bidx = tid * BPT + j;
+            if (c[j]) {
+                w.rstart[run] = (uint16_t)start;
+                rid[bidx] = (uint16_t)run;
+                run++;
+            }
+            if (bidx < R) cnt[bidx] = start;
+            start += c[j];
+        }
+        if (tid == GNT - 1) {
+            w.s_m = start;
+            w.s_U = run;
+            w.rstart[run] = (uint16_t)start;
+            int64_t pb = run ? (int64_t)atomicAdd(a.P_counter, (unsigned long long)run) : 0;
+            if (pb + run > a.cap) { atomicOr(a.overflow, 2); pb = -1; }
+            w.s_pb = pb;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < GPT; i++) {
+            if (pass[i]) {
+                const uint32_t pos = cnt[dk[i]] + rk[i];
+                w.skey[0][pos] = dk[i];
+                w.sidx[0][pos] = (uint16_t)(i * GNT + tid);
+                w.srun[pos] = rid[dk[i]];
+            }
+        }
+        __syncthreads();
+        m = (int)w.s_m;
+        sk = w.skey[0];
+        si = w.sidx[0];
+    } else {
+    // 2. compact passing rows into sort buffer 0 (warp-aggregated slot claims)
+    #pragma unroll
     for (int i = 0; i < GPT; i++) {
         if (!bal[i]) continue;
         uint32_t base = 0;
@@ -324,16 +487,15 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
         }
     }
     __syncthreads();
-    const int m = (int)w.s_m;
+    m = (int)w.s_m;
     // 3. in-tile stable LSD radix sort over the bits that vary in this tile
     const int bits = (m > 0 && kmax != kmin) ? 64 - __clzll(kmax - kmin) : 0;
     const int passes = (bits + 7) / 8;
     for (int p = 0; p < passes; p++) tile_pass(w, p & 1, m, 8 * p);
     const int fin = passes & 1;
-    const uint64_t* sk = w.skey[fin];
-    const uint16_t* si = w.sidx[fin];
+    sk = w.skey[fin];
+    si = w.sidx[fin];
     // 4. segment boundaries (uniqueConsecutive): blocked positions p = tid*GPT + q
-    const int p0 = tid * GPT;
     uint32_t heads = 0;
 #pragma unroll
     for (int q = 0; q < GPT; q++) {
@@ -360,6 +522,7 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
         }
     }
     __syncthreads();
+    }
     const int U = (int)w.s_U;
     const int64_t pb = w.s_pb;
     if (U == 0 || pb < 0) return;
@@ -721,6 +884,10 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
         mbar_init(&w.mbar[0], 1);
         mbar_init(&w.mbar[1], 1);
         fence_mbar_init();
+        if (a.n_keys > 0) {
+            int wd[TQP_MAX_KEYS];
+            key_layout(a.krange, a.n_keys, w.s_kmin, w.s_kshift, wd);
+        }
     }
     __syncthreads();
     auto eligible = [&](int64_t t) { return a.bulk_ok && (t + 1) * GTILE <= a.n; };
@@ -945,7 +1112,7 @@ __device__ __forceinline__ double i128_to_double(uint64_t lo, int64_t hi) {
 struct FinArgs {
     int n_keys, n_aggs;
     int kdt[TQP_MAX_KEYS];
-    int kshift[TQP_MAX_KEYS];
+    const unsigned long long* krange;
     void* kout[TQP_MAX_KEYS];
     int aop[TQP_MAX_AGGS];
     int apair[TQP_MAX_AGGS];
@@ -961,12 +1128,19 @@ struct FinArgs {
 __global__ void gb_finalize_kernel(FinArgs a) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < a.G; g += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t key = a.empty_global ? 0 : a.gkey[g];
-        for (int k = 0; k < a.n_keys; k++) {
-            if (!a.kout[k]) continue;
-            switch (a.kdt[k]) {
-                case TQP_U8: ((uint8_t*)a.kout[k])[g] = (uint8_t)(key >> a.kshift[k]); break;
-                case TQP_I32: ((int32_t*)a.kout[k])[g] = (int32_t)((uint32_t)(key >> a.kshift[k]) ^ 0x80000000u); break;
-                default: ((int64_t*)a.kout[k])[g] = (int64_t)(key ^ 0x8000000000000000ull); break;
+        if (a.n_keys > 0) {
+            uint64_t kmin[TQP_MAX_KEYS];
+            int shift[TQP_MAX_KEYS], width[TQP_MAX_KEYS];
+            key_layout(a.krange, a.n_keys, kmin, shift, width);
+            for (int k = 0; k < a.n_keys; k++) {
+                if (!a.kout[k]) continue;
+                const uint64_t msk = width[k] >= 64 ? ~0ull : ((1ull << width[k]) - 1);
+                const uint64_t part = (width[k] ? ((key >> shift[k]) & msk) : 0ull) + kmin[k];
+                switch (a.kdt[k]) {
+                    case TQP_U8: ((uint8_t*)a.kout[k])[g] = (uint8_t)part; break;
+                    case TQP_I32: ((int32_t*)a.kout[k])[g] = (int32_t)((uint32_t)part ^ 0x80000000u); break;
+                    default: ((int64_t*)a.kout[k])[g] = (int64_t)(part ^ 0x8000000000000000ull); break;
+                }
             }
         }
         const int64_t cnt = a.empty_global ? 0 : a.gcount[g];
@@ -1067,6 +1241,27 @@ void phase2(tqp_ctx* ctx, tqp_groupby_plan* PL, Partials& pr, bool split) {
     PL->G = G;
 }
 
+// Key-column ranges on the device (no host sync): min in kr[0..7], max in kr[8..15].
+void key_ranges(tqp_ctx* ctx, const void* const* kcol, const int* kdt, int n_keys, int64_t n,
+                DevBuf<unsigned long long>& kr) {
+    kr.alloc(ctx, 16);
+    TQP_CUDA(cudaMemsetAsync(kr.get(), 0xFF, 8 * 8, ctx->stream));
+    TQP_CUDA(cudaMemsetAsync(kr.get() + 8, 0, 8 * 8, ctx->stream));
+    if (n_keys == 0 || n == 0) return;
+    KRArgs a{};
+    a.n_keys = n_keys;
+    a.n = n;
+    double bytes = 0;
+    for (int k = 0; k < n_keys; k++) {
+        a.kcol[k] = kcol[k];
+        a.kdt[k] = kdt[k];
+        bytes += (double)dtype_size(kdt[k]) * (double)n;
+    }
+    const int g = (int)std::min<int64_t>(ceil_div(n, GNT * 16), (int64_t)ctx->num_sms * 8);
+    launch(ctx, "tqp_groupby_keyrange", key_range_kernel, dim3(g), dim3(GNT), 0, a, kr.get());
+    ctx->add_bytes("tqp_groupby_keyrange", bytes);
+}
+
 // Distinct (op, expression) pairs: SUM and AVG of the same expression share one.
 void make_pairs(tqp_groupby_plan* PL, const tqp_agg* aggs, int n_aggs, int (*pf)[3], int (*ps)[3],
                 int64_t (*pa)[3], int* pnf) {
@@ -1135,15 +1330,19 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         PL->n_aggs = n_aggs;
         int off = 0;
         a.n_keys = n_keys;
+        const void* kc[TQP_MAX_KEYS];
+        int kd[TQP_MAX_KEYS];
         for (int k = n_keys - 1; k >= 0; k--) {   // column 0 most significant
             const int c = key_idx[k];
             a.kcol[k] = uidx(c);
-            a.kshift[k] = off;
             PL->kdt[k] = cols[c].dtype;
-            PL->kshift[k] = off;
+            kc[k] = cols[c].data;
+            kd[k] = cols[c].dtype;
             off += 8 * (int)dtype_size(cols[c].dtype);
         }
         if (off > 64) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: packed key wider than 64 bits");
+        key_ranges(ctx, kc, kd, n_keys, n, PL->krange);
+        a.krange = PL->krange.get();
         a.n_preds = n_preds;
         for (int q = 0; q < n_preds; q++) {
             a.pcol[q] = uidx(preds[q].col);
@@ -1247,7 +1446,6 @@ void groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* PL, void* const* keys_o
     f.n_aggs = PL->n_aggs;
     for (int k = 0; k < PL->n_keys; k++) {
         f.kdt[k] = PL->kdt[k];
-        f.kshift[k] = PL->kshift[k];
         f.kout[k] = keys_out ? keys_out[k] : nullptr;
     }
     for (int g = 0; g < PL->n_aggs; g++) {
@@ -1259,6 +1457,7 @@ void groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* PL, void* const* keys_o
         f.glo[j] = PL->glo[j].get();
         f.ghi[j] = PL->ghi[j].get();
     }
+    f.krange = PL->krange.get();
     f.gkey = PL->gkey.get();
     f.gcount = PL->gcount.get();
     f.G = PL->G;
@@ -1274,7 +1473,7 @@ struct MergeArgs {
     int n_keys;
     const void* kcol[TQP_MAX_KEYS];
     int kdt[TQP_MAX_KEYS];
-    int kshift[TQP_MAX_KEYS];
+    const unsigned long long* krange;
     int n_pairs;
     int pop[TQP_MAX_AGGS];
     const void* src[TQP_MAX_AGGS];   // SUM pair: int128 (lo, hi) rows; MIN/MAX: int64 rows
@@ -1287,7 +1486,13 @@ struct MergeArgs {
 __global__ void gb_merge_pack_kernel(MergeArgs a) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.m; i += (int64_t)gridDim.x * blockDim.x) {
         uint64_t kk = 0;
-        for (int c = 0; c < a.n_keys; c++) kk |= key_part(load_as_i64(a.kcol[c], a.kdt[c], i), a.kdt[c]) << a.kshift[c];
+        if (a.n_keys > 0) {
+            uint64_t kmin[TQP_MAX_KEYS];
+            int shift[TQP_MAX_KEYS], width[TQP_MAX_KEYS];
+            key_layout(a.krange, a.n_keys, kmin, shift, width);
+            for (int c = 0; c < a.n_keys; c++)
+                kk |= (key_part(load_as_i64(a.kcol[c], a.kdt[c], i), a.kdt[c]) - kmin[c]) << shift[c];
+        }
         a.pkey[i] = kk;
         for (int j = 0; j < a.n_pairs; j++) {
             if (a.pop[j] == P_SUM) {
@@ -1324,15 +1529,19 @@ tqp_groupby_plan* groupby_merge(tqp_ctx* ctx, int64_t m, const tqp_col* key_cols
         a.n_keys = n_keys;
         a.m = m;
         int off = 0;
+        int kd[TQP_MAX_KEYS];
+        const void* kc[TQP_MAX_KEYS];
         for (int k = n_keys - 1; k >= 0; k--) {
             a.kcol[k] = key_cols[k].data;
             a.kdt[k] = key_cols[k].dtype;
-            a.kshift[k] = off;
             PL->kdt[k] = key_cols[k].dtype;
-            PL->kshift[k] = off;
+            kc[k] = key_cols[k].data;
+            kd[k] = key_cols[k].dtype;
             off += 8 * (int)dtype_size(key_cols[k].dtype);
         }
         if (off > 64) fail(TQP_ERR_INVALID_ARGUMENT, "groupby_merge: packed key wider than 64 bits");
+        key_ranges(ctx, kc, kd, n_keys, m, PL->krange);
+        a.krange = PL->krange.get();
         int pf[TQP_MAX_AGGS][3], ps[TQP_MAX_AGGS][3], pnf[TQP_MAX_AGGS];
         int64_t pa[TQP_MAX_AGGS][3];
         make_pairs(PL, aggs, n_aggs, pf, ps, pa, pnf);
