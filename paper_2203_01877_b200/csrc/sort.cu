@@ -82,14 +82,14 @@ __device__ __forceinline__ KT load_key(const void* in_keys, int64_t pos, bool de
     return (KT)load_u<IN>(in_keys, pos, desc);
 }
 
-// (1) per-tile digit counts -> th[tile * 256 + d]
-template <typename KT, int IN, int IPT>
+// (1) per-tile digit counts -> th[tile * BINS + d]
+template <typename KT, int IN, int IPT, int RB>
 __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int64_t n, int shift, bool desc,
                                                        uint32_t* __restrict__ th) {
-    constexpr int TILE = NT * IPT;
-    __shared__ uint32_t h[NW][256];
+    constexpr int TILE = NT * IPT, BINS = 1 << RB;
+    __shared__ uint32_t h[NW][BINS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int d = lane; d < 256; d += 32) h[warp][d] = 0;
+    for (int d = lane; d < BINS; d += 32) h[warp][d] = 0;
     __syncwarp();
     const int64_t base = (int64_t)blockIdx.x * TILE;
     KT k[IPT];
@@ -101,52 +101,71 @@ __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int6
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        if (pos < n) atomicAdd(&h[warp][(uint32_t)(k[i] >> shift) & 255u], 1u);
+        if (pos < n) atomicAdd(&h[warp][(uint32_t)(k[i] >> shift) & (BINS - 1u)], 1u);
     }
     __syncthreads();
-    uint32_t c = 0;
+    for (int d = tid; d < BINS; d += NT) {
+        uint32_t c = 0;
 #pragma unroll
-    for (int w = 0; w < NW; w++) c += h[w][tid];
-    th[(int64_t)blockIdx.x * 256 + tid] = c;
+        for (int w = 0; w < NW; w++) c += h[w][d];
+        th[(int64_t)blockIdx.x * BINS + d] = c;
+    }
 }
 
 // (2) per chunk of CHUNK tiles: th[t][d] <- exclusive prefix within the chunk; ct[c][d] = chunk total
+template <int RB>
 __global__ void __launch_bounds__(NT) scan_tiles_kernel(uint32_t* __restrict__ th, int64_t n_tiles,
                                                         uint32_t* __restrict__ ct) {
-    const int d = threadIdx.x;
+    constexpr int BINS = 1 << RB;
     const int64_t t0 = (int64_t)blockIdx.x * CHUNK;
     const int cnt = (int)min((int64_t)CHUNK, n_tiles - t0);
-    uint32_t run = 0;
-    for (int b = 0; b < cnt; b += 16) {
-        uint32_t v[16];
+    for (int d = threadIdx.x; d < BINS; d += NT) {
+        uint32_t run = 0;
+        for (int b = 0; b < cnt; b += 16) {
+            uint32_t v[16];
 #pragma unroll
-        for (int i = 0; i < 16; i++) v[i] = (b + i < cnt) ? th[(t0 + b + i) * 256 + d] : 0u;   // 16 loads in flight
+            for (int i = 0; i < 16; i++) v[i] = (b + i < cnt) ? th[(t0 + b + i) * BINS + d] : 0u;   // 16 loads in flight
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            if (b + i < cnt) th[(t0 + b + i) * 256 + d] = run;
-            run += v[i];
+            for (int i = 0; i < 16; i++) {
+                if (b + i < cnt) th[(t0 + b + i) * BINS + d] = run;
+                run += v[i];
+            }
         }
+        ct[(int64_t)blockIdx.x * BINS + d] = run;
     }
-    ct[(int64_t)blockIdx.x * 256 + d] = run;
 }
 
-// (3) one CTA: ct[c][d] <- global start of digit d in chunk c (bin base + earlier chunks)
+// (3) one CTA: ct[c][d] <- global start of digit d in chunk c (bin base + earlier chunks);
+// thread t owns the consecutive digits [t*BPT, t*BPT + BPT)
+template <int RB>
 __global__ void __launch_bounds__(NT) scan_chunks_kernel(uint32_t* __restrict__ ct, int64_t n_chunks) {
+    constexpr int BINS = 1 << RB, BPT = BINS / NT;
     __shared__ uint32_t s_w[NW];
-    const int d = threadIdx.x;
-    uint32_t run = 0;
-    for (int64_t b = 0; b < n_chunks; b += 16) {
-        uint32_t v[16];
+    uint32_t tot[BPT], local = 0;
 #pragma unroll
-        for (int i = 0; i < 16; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * 256 + d] : 0u;
+    for (int j = 0; j < BPT; j++) {
+        const int d = threadIdx.x * BPT + j;
+        uint32_t run = 0;
+        for (int64_t b = 0; b < n_chunks; b += 16) {
+            uint32_t v[16];
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            if (b + i < n_chunks) ct[(b + i) * 256 + d] = run;
-            run += v[i];
+            for (int i = 0; i < 16; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * BINS + d] : 0u;
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                if (b + i < n_chunks) ct[(b + i) * BINS + d] = run;
+                run += v[i];
+            }
         }
+        tot[j] = run;
+        local += run;
     }
-    const uint32_t base = block_excl_scan256(run, s_w);   // global bin bases
-    for (int64_t c = 0; c < n_chunks; c++) ct[c * 256 + d] += base;
+    uint32_t base = block_excl_scan256(local, s_w);   // global bin bases, digits in order
+#pragma unroll
+    for (int j = 0; j < BPT; j++) {
+        const int d = threadIdx.x * BPT + j;
+        for (int64_t c = 0; c < n_chunks; c++) ct[c * BINS + d] += base;
+        base += tot[j];
+    }
 }
 
 struct ScatterArgs {
@@ -172,119 +191,6 @@ __device__ __forceinline__ uint64_t to_u(KT k, uint64_t hi_bits) {
     return (uint64_t)k;
 }
 
-// (4) stable scatter of one tile
-template <typename KT, int IN, int IPT>
-__global__ void __launch_bounds__(NT, 3) scatter_kernel(ScatterArgs a) {
-    constexpr int TILE = NT * IPT;
-    __shared__ union {
-        uint32_t whist[NW][256];
-        struct {
-            KT keys[TILE];
-            uint32_t perm[TILE];
-        } stage;
-    } s;
-    __shared__ uint32_t s_tstart[256], s_gstart[256], s_w[NW];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = blockIdx.x;
-    const int64_t base = tile * TILE;
-
-    for (int d = lane; d < 256; d += 32) s.whist[warp][d] = 0;
-    s_gstart[tid] = a.ct[(tile / CHUNK) * 256 + tid] + a.th[tile * 256 + tid];
-
-    KT key[IPT];
-    uint32_t pm[IPT], rk[IPT];
-#pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        if (pos < a.n) {
-            key[i] = load_key<KT, IN>(a.in_keys, pos, a.desc);
-            pm[i] = IN == IN_INTERNAL ? a.in_perm[pos] : (uint32_t)pos;
-        } else {
-            key[i] = 0;
-            pm[i] = 0;
-        }
-    }
-    __syncwarp();
-    // Stable warp-level ranking: peers (same digit) from one ballot per digit bit;
-    // the highest peer claims popc(peers) slots of its warp's digit counter with a
-    // shared-memory atomicAdd, in item order. rk packs the claimed base (bits
-    // 0-15), the leader lane (16-20) and the rank among peers (24-28).
-    const unsigned lt = lanemask_lt();
-#pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        const bool valid = pos < a.n;
-        const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
-        unsigned peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int b = 0; b < 8; b++) {
-            const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-            peers &= ((d >> b) & 1u) ? bb : ~bb;
-        }
-        const uint32_t leader = 31 - __clz(peers);
-        uint32_t old = 0;
-        if (valid && lane == leader) old = atomicAdd(&s.whist[warp][d], (uint32_t)__popc(peers));
-        rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
-    }
-#pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const uint32_t b = __shfl_sync(0xffffffffu, rk[i] & 0xFFFFu, (rk[i] >> 16) & 31u);
-        rk[i] = b + (rk[i] >> 24);
-    }
-    __syncthreads();
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int w = 0; w < NW; w++) {   // per digit (thread d): exclusive prefix over warps
-        const uint32_t c = s.whist[w][tid];
-        s.whist[w][tid] = cnt;
-        cnt += c;
-    }
-    s_tstart[tid] = block_excl_scan256(cnt, s_w);
-    __syncthreads();   // s_tstart / whist prefixes visible to every thread
-#pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        if (pos < a.n) {
-            const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
-            rk[i] = s_tstart[d] + s.whist[warp][d] + rk[i];
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        if (pos < a.n) {
-            s.stage.keys[rk[i]] = key[i];
-            s.stage.perm[rk[i]] = pm[i];
-        }
-    }
-    __syncthreads();
-    const int tile_n = (int)min((int64_t)TILE, a.n - base);
-    for (int j = tid; j < tile_n; j += NT) {
-        const KT k = s.stage.keys[j];
-        const uint32_t p = s.stage.perm[j];
-        const uint32_t d = (uint32_t)(k >> a.shift) & 255u;
-        const int64_t dst = (int64_t)s_gstart[d] + (j - (int64_t)s_tstart[d]);
-        if (a.out_keys) ((KT*)a.out_keys)[dst] = k;
-        if (a.out_perm) a.out_perm[dst] = p;
-        if (a.out_perm64) a.out_perm64[dst] = (int64_t)p;
-        if (a.out_u || a.out_orig) {
-            const uint64_t u = to_u<KT>(k, a.hi_bits);
-            if (a.out_u) a.out_u[dst] = u;
-            if (a.out_orig) {
-                const uint64_t v = a.desc ? ~u : u;
-                switch (a.orig_dtype) {
-                    case TQP_U8: ((uint8_t*)a.out_orig)[dst] = (uint8_t)unordered_i64(v); break;
-                    case TQP_I32: ((int32_t*)a.out_orig)[dst] = (int32_t)unordered_i64(v); break;
-                    case TQP_I64: ((int64_t*)a.out_orig)[dst] = unordered_i64(v); break;
-                    default: ((uint64_t*)a.out_orig)[dst] = v; break;
-                }
-            }
-        }
-    }
-}
-
 // (4') the same stable scatter as a persistent kernel whose input tiles (keys and
 // permutation) are streamed into shared memory by TMA bulk copies
 // (cp.async.bulk + mbarrier), double-buffered: the stage of tile k is released as
@@ -304,16 +210,16 @@ __device__ __forceinline__ KT conv_key(typename InKey<IN, KT>::T v, bool desc) {
     return (KT)(desc ? ~u : u);
 }
 
-template <typename KT, int IN, int IPT>
+template <typename KT, int IN, int IPT, int RB>
 struct ScatterWork {
     union {
-        uint32_t whist[NW][256];
+        uint32_t whist[NW][1 << RB];
         struct {
             KT keys[NT * IPT];
             uint32_t perm[NT * IPT];
         } sorted;
     } u;
-    uint32_t tstart[256], gstart[256], w[NW];
+    uint32_t tstart[1 << RB], gstart[1 << RB], w[NW];
     uint64_t mbar[2];
 };
 
@@ -322,21 +228,22 @@ constexpr int scatter_stage_bytes() {
     return NT * IPT * (int)sizeof(typename InKey<IN, KT>::T) + (IN == IN_INTERNAL ? NT * IPT * 4 : 0);
 }
 
-template <typename KT, int IN, int IPT>
+template <typename KT, int IN, int IPT, int RB>
 constexpr size_t scatter_tma_smem() {
-    return 2 * (size_t)scatter_stage_bytes<KT, IN, IPT>() + sizeof(ScatterWork<KT, IN, IPT>);
+    return 2 * (size_t)scatter_stage_bytes<KT, IN, IPT>() + sizeof(ScatterWork<KT, IN, IPT, RB>);
 }
 
-template <typename KT, int IN, int IPT>
-__global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles) {
-    constexpr int TILE = NT * IPT;
+template <typename KT, int IN, int IPT, int RB>
+__global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
+    constexpr int TILE = NT * IPT, BINS = 1 << RB, BPT = BINS / NT;
+    constexpr uint32_t DM = BINS - 1u;
     using KIN = typename InKey<IN, KT>::T;
     constexpr bool HAS_PERM = IN == IN_INTERNAL;
     constexpr int STAGE_BYTES = scatter_stage_bytes<KT, IN, IPT>();
     extern __shared__ __align__(128) uint8_t smem[];
     uint8_t* stage0 = smem;
     uint8_t* stage1 = smem + STAGE_BYTES;
-    ScatterWork<KT, IN, IPT>& s = *reinterpret_cast<ScatterWork<KT, IN, IPT>*>(smem + 2 * STAGE_BYTES);
+    ScatterWork<KT, IN, IPT, RB>& s = *reinterpret_cast<ScatterWork<KT, IN, IPT, RB>*>(smem + 2 * STAGE_BYTES);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         mbar_init(&s.mbar[0], 1);
@@ -344,7 +251,7 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
         fence_mbar_init();
     }
     __syncthreads();
-    auto full = [&](int64_t t) { return (t + 1) * TILE <= a.n; };
+    auto full = [&](int64_t t) { return use_tma && (t + 1) * TILE <= a.n; };
     auto issue = [&](int64_t t, int st) {   // thread 0
         uint8_t* dst = st ? stage1 : stage0;
         mbar_expect_tx(&s.mbar[st], (uint32_t)STAGE_BYTES);
@@ -367,8 +274,8 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
         const int64_t base = tile * TILE;
         KT key[IPT];
         uint32_t pm[IPT], rk[IPT];
-        for (int d = lane; d < 256; d += 32) s.u.whist[warp][d] = 0;
-        s.gstart[tid] = a.ct[(tile / CHUNK) * 256 + tid] + a.th[tile * 256 + tid];
+        for (int d = lane; d < BINS; d += 32) s.u.whist[warp][d] = 0;
+        for (int d = tid; d < BINS; d += NT) s.gstart[d] = a.ct[(tile / CHUNK) * BINS + d] + a.th[tile * BINS + d];
         if (full(tile)) {
             mbar_wait(&s.mbar[st], ((st ? uses1 : uses0) - 1) & 1);
             const uint8_t* sp = st ? stage1 : stage0;
@@ -407,10 +314,10 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
             const bool valid = base + warp * 32 * IPT + i * 32 + lane < a.n;
-            const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
+            const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
             unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-            for (int b = 0; b < 8; b++) {
+            for (int b = 0; b < RB; b++) {
                 const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
                 peers &= ((d >> b) & 1u) ? bb : ~bb;
             }
@@ -425,19 +332,33 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
             rk[i] = b + (rk[i] >> 24);
         }
         __syncthreads();
-        uint32_t cnt = 0;
+        {   // per digit: exclusive prefix over warps; tile-local digit starts (thread owns BPT digits)
+            uint32_t cnt[BPT], local = 0;
 #pragma unroll
-        for (int w = 0; w < NW; w++) {
-            const uint32_t c = s.u.whist[w][tid];
-            s.u.whist[w][tid] = cnt;
-            cnt += c;
+            for (int j = 0; j < BPT; j++) {
+                const int d = tid * BPT + j;
+                uint32_t run = 0;
+#pragma unroll
+                for (int w = 0; w < NW; w++) {
+                    const uint32_t c = s.u.whist[w][d];
+                    s.u.whist[w][d] = run;
+                    run += c;
+                }
+                cnt[j] = run;
+                local += run;
+            }
+            uint32_t ex = block_excl_scan256(local, s.w);
+#pragma unroll
+            for (int j = 0; j < BPT; j++) {
+                s.tstart[tid * BPT + j] = ex;
+                ex += cnt[j];
+            }
         }
-        s.tstart[tid] = block_excl_scan256(cnt, s.w);
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
             if (base + warp * 32 * IPT + i * 32 + lane < a.n) {
-                const uint32_t d = (uint32_t)(key[i] >> a.shift) & 255u;
+                const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
                 rk[i] = s.tstart[d] + s.u.whist[warp][d] + rk[i];
             }
         }
@@ -454,7 +375,7 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
         for (int j = tid; j < tile_n; j += NT) {
             const KT kk = s.u.sorted.keys[j];
             const uint32_t p = s.u.sorted.perm[j];
-            const uint32_t d = (uint32_t)(kk >> a.shift) & 255u;
+            const uint32_t d = (uint32_t)(kk >> a.shift) & DM;
             const int64_t dst = (int64_t)s.gstart[d] + (j - (int64_t)s.tstart[d]);
             if (a.out_keys) ((KT*)a.out_keys)[dst] = kk;
             if (a.out_perm) a.out_perm[dst] = p;
@@ -520,9 +441,10 @@ static void dispatch_in(int mode, F&& f) {
     }
 }
 
-template <typename KT>
+template <typename KT, int RB>
 static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o,
                        const int* shifts, int P) {
+    constexpr int BINS = 1 << RB;
     constexpr int IPT = sizeof(KT) == 4 ? 16 : 12;
     constexpr int TILE = NT * IPT;
     const int64_t tiles = ceil_div(n, TILE);
@@ -542,21 +464,22 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         if (kused) kb[b].alloc(ctx, n);
         if (pused) pb[b].alloc(ctx, n);
     }
-    DevBuf<uint32_t> th(ctx, (size_t)tiles * 256);
-    DevBuf<uint32_t> ct(ctx, (size_t)chunks * 256);
+    DevBuf<uint32_t> th(ctx, (size_t)tiles * BINS);
+    DevBuf<uint32_t> ct(ctx, (size_t)chunks * BINS);
     const int mode0 = in_mode(dtype);
     for (int p = 0; p < P; p++) {
         const void* in = p == 0 ? keys : kb[(p - 1) % 2].get();
         const int mode = p == 0 ? mode0 : (int)IN_INTERNAL;
         const double kin = p == 0 ? (double)dtype_size(dtype) : (double)sizeof(KT);
         dispatch_in(mode, [&](auto m) {
-            launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT>, dim3((unsigned)tiles),
-                   dim3(NT), 0, in, n, shifts[p], desc, th.get());
+            launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT, RB>,
+                   dim3((unsigned)tiles), dim3(NT), 0, in, n, shifts[p], desc, th.get());
         });
-        ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 1024.0 * (double)tiles);
-        launch(ctx, "tqp_sort_scan", scan_tiles_kernel, dim3((unsigned)chunks), dim3(NT), 0, th.get(), tiles, ct.get());
-        launch(ctx, "tqp_sort_scan", scan_chunks_kernel, dim3(1), dim3(NT), 0, ct.get(), chunks);
-        ctx->add_bytes("tqp_sort_scan", 2048.0 * (double)tiles + 3072.0 * (double)chunks);
+        ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
+        launch(ctx, "tqp_sort_scan", scan_tiles_kernel<RB>, dim3((unsigned)chunks), dim3(NT), 0, th.get(), tiles,
+               ct.get());
+        launch(ctx, "tqp_sort_scan", scan_chunks_kernel<RB>, dim3(1), dim3(NT), 0, ct.get(), chunks);
+        ctx->add_bytes("tqp_sort_scan", 8.0 * BINS * (double)tiles + 12.0 * BINS * (double)chunks);
         ScatterArgs a{};
         a.in_keys = in;
         a.in_perm = p == 0 ? nullptr : pb[(p - 1) % 2].get();
@@ -584,17 +507,13 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         const bool aligned = ((uintptr_t)in % 16 == 0) && (p == 0 || (uintptr_t)a.in_perm % 16 == 0);
         dispatch_in(mode, [&](auto m) {
             constexpr int INM = decltype(m)::value;
-            if (aligned) {
-                constexpr size_t smem = scatter_tma_smem<KT, INM, IPT>();
-                auto* kfn = scatter_tma_kernel<KT, INM, IPT>;
-                set_smem(kfn, smem);
-                int occ = 1;
-                TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem));
-                const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
-                launch(ctx, "tqp_sort_scatter", kfn, dim3((unsigned)grid), dim3(NT), smem, a, tiles);
-            } else {
-                launch(ctx, "tqp_sort_scatter", scatter_kernel<KT, INM, IPT>, dim3((unsigned)tiles), dim3(NT), 0, a);
-            }
+            constexpr size_t smem = scatter_tma_smem<KT, INM, IPT, RB>();
+            auto* kfn = scatter_tma_kernel<KT, INM, IPT, RB>;
+            set_smem(kfn, smem);
+            int occ = 1;
+            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem));
+            const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
+            launch(ctx, "tqp_sort_scatter", kfn, dim3((unsigned)grid), dim3(NT), smem, a, tiles, aligned);
         });
     }
     const int fb = (P - 1) % 2;
@@ -625,9 +544,20 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     o.or_bits = h[1];
     const uint64_t diff = h[0] ^ h[1];
     o.k32 = (diff >> 32) == 0;
-    int shifts[8], P = 0;
+    // digit plan: 8-bit digits over the bytes that vary, or 9-bit digits over the
+    // varying bit span when that takes fewer passes (e.g. 26-bit order keys: 3 not 4)
+    int shifts[8], P = 0, rb = 8;
     for (int b = 0; b < 8; b++)
         if ((diff >> (8 * b)) & 0xFF) shifts[P++] = 8 * b;
+    if (diff) {
+        const int lo = __builtin_ctzll(diff), hi = 64 - __builtin_clzll(diff);
+        const int p9 = (hi - lo + 8) / 9;
+        if (p9 < P) {
+            rb = 9;
+            P = p9;
+            for (int p = 0; p < P; p++) shifts[p] = lo + 9 * p;
+        }
+    }
     o.passes = P;
     if (P == 0) {
         if (o.want_internal || o.want_perm32) o.perm32.alloc(ctx, n);
@@ -652,8 +582,13 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
         });
         return;
     }
-    if (o.k32) run_passes<uint32_t>(ctx, keys, dtype, n, desc, o, shifts, P);
-    else run_passes<uint64_t>(ctx, keys, dtype, n, desc, o, shifts, P);
+    if (o.k32) {
+        if (rb == 9) run_passes<uint32_t, 9>(ctx, keys, dtype, n, desc, o, shifts, P);
+        else run_passes<uint32_t, 8>(ctx, keys, dtype, n, desc, o, shifts, P);
+    } else {
+        if (rb == 9) run_passes<uint64_t, 9>(ctx, keys, dtype, n, desc, o, shifts, P);
+        else run_passes<uint64_t, 8>(ctx, keys, dtype, n, desc, o, shifts, P);
+    }
 }
 
 }  // namespace tqp
