@@ -121,12 +121,12 @@ __global__ void __launch_bounds__(NT) scan_tiles_kernel(uint32_t* __restrict__ t
     const int cnt = (int)min((int64_t)CHUNK, n_tiles - t0);
     for (int d = threadIdx.x; d < BINS; d += NT) {
         uint32_t run = 0;
-        for (int b = 0; b < cnt; b += 16) {
-            uint32_t v[16];
+        for (int b = 0; b < cnt; b += 32) {
+            uint32_t v[32];
 #pragma unroll
-            for (int i = 0; i < 16; i++) v[i] = (b + i < cnt) ? th[(t0 + b + i) * BINS + d] : 0u;   // 16 loads in flight
+            for (int i = 0; i < 32; i++) v[i] = (b + i < cnt) ? th[(t0 + b + i) * BINS + d] : 0u;   // 32 loads in flight
 #pragma unroll
-            for (int i = 0; i < 16; i++) {
+            for (int i = 0; i < 32; i++) {
                 if (b + i < cnt) th[(t0 + b + i) * BINS + d] = run;
                 run += v[i];
             }
@@ -135,37 +135,35 @@ __global__ void __launch_bounds__(NT) scan_tiles_kernel(uint32_t* __restrict__ t
     }
 }
 
-// (3) one CTA: ct[c][d] <- global start of digit d in chunk c (bin base + earlier chunks);
-// thread t owns the consecutive digits [t*BPT, t*BPT + BPT)
+// (3) one CTA of BINS threads (one digit each): ct[c][d] <- global start of digit d
+// in chunk c (bin base + earlier chunks)
 template <int RB>
-__global__ void __launch_bounds__(NT) scan_chunks_kernel(uint32_t* __restrict__ ct, int64_t n_chunks) {
-    constexpr int BINS = 1 << RB, BPT = BINS / NT;
-    __shared__ uint32_t s_w[NW];
-    uint32_t tot[BPT], local = 0;
+__global__ void __launch_bounds__(1 << RB) scan_chunks_kernel(uint32_t* __restrict__ ct, int64_t n_chunks) {
+    constexpr int BINS = 1 << RB, NWB = BINS / 32;
+    __shared__ uint32_t s_w[NWB];
+    const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    uint32_t run = 0;
+    for (int64_t b = 0; b < n_chunks; b += 32) {
+        uint32_t v[32];
 #pragma unroll
-    for (int j = 0; j < BPT; j++) {
-        const int d = threadIdx.x * BPT + j;
-        uint32_t run = 0;
-        for (int64_t b = 0; b < n_chunks; b += 16) {
-            uint32_t v[16];
+        for (int i = 0; i < 32; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * BINS + d] : 0u;   // 32 loads in flight
 #pragma unroll
-            for (int i = 0; i < 16; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * BINS + d] : 0u;
-#pragma unroll
-            for (int i = 0; i < 16; i++) {
-                if (b + i < n_chunks) ct[(b + i) * BINS + d] = run;
-                run += v[i];
-            }
+        for (int i = 0; i < 32; i++) {
+            if (b + i < n_chunks) ct[(b + i) * BINS + d] = run;
+            run += v[i];
         }
-        tot[j] = run;
-        local += run;
     }
-    uint32_t base = block_excl_scan256(local, s_w);   // global bin bases, digits in order
-#pragma unroll
-    for (int j = 0; j < BPT; j++) {
-        const int d = threadIdx.x * BPT + j;
-        for (int64_t c = 0; c < n_chunks; c++) ct[c * BINS + d] += base;
-        base += tot[j];
+    // exclusive scan of the digit totals across the block (global bin bases)
+    uint32_t x = run;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
     }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t base = x - run;
+    for (int w = 0; w < warp; w++) base += s_w[w];
+    for (int64_t c = 0; c < n_chunks; c++) ct[c * BINS + d] += base;
 }
 
 struct ScatterArgs {
@@ -478,7 +476,7 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
         launch(ctx, "tqp_sort_scan", scan_tiles_kernel<RB>, dim3((unsigned)chunks), dim3(NT), 0, th.get(), tiles,
                ct.get());
-        launch(ctx, "tqp_sort_scan", scan_chunks_kernel<RB>, dim3(1), dim3(NT), 0, ct.get(), chunks);
+        launch(ctx, "tqp_sort_scan", scan_chunks_kernel<RB>, dim3(1), dim3(BINS), 0, ct.get(), chunks);
         ctx->add_bytes("tqp_sort_scan", 8.0 * BINS * (double)tiles + 12.0 * BINS * (double)chunks);
         ScatterArgs a{};
         a.in_keys = in;
