@@ -556,13 +556,18 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
         const int op = a.prop[j];
         const int jj = j % PCH;
         // (A) evaluate the expression at this thread's sorted positions (passing rows
-        //     only; the in-tile sort is stable, so rows ascend within a run)
+        //     only; the in-tile sort is stable, so rows ascend within a run). Products
+        //     wrap; overflow is excluded by magnitude bounds: with b_f = bit length of
+        //     max |term f| over the thread's rows, |prod| < 2^(sum b_f), so sum b_f <= 63
+        //     (and no add overflow) proves every product exact. Otherwise the rows are
+        //     re-evaluated with exact per-operation checks.
         int64_t vv[GPT];
-        bool ov[GPT];
 #pragma unroll
-        for (int q = 0; q < GPT; q++) { vv[q] = 1; ov[q] = false; }
+        for (int q = 0; q < GPT; q++) vv[q] = 1;
         const int nf = a.pnf[j];
         if (any) {
+            int bsum = 0;
+            bool addsafe = true;
             for (int f = 0; f < nf; f++) {
                 const int c = a.pfc[j][f];
                 const uint8_t* col = st + a.uoff[c];
@@ -582,31 +587,50 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
 #pragma unroll
                         for (int q = 0; q < GPT; q++) x[q] = (int64_t)reinterpret_cast<const long long*>(col)[prow[q]];
                 }
+                uint64_t mx = 0, mt = 0;
 #pragma unroll
                 for (int q = 0; q < GPT; q++) {
-                    int64_t t;
-                    if (neg) {
-                        t = add - x[q];
-                        ov[q] |= ((add ^ x[q]) & (add ^ t)) < 0;   // signed sub overflow
-                    } else {
-                        t = add + x[q];
-                        ov[q] |= ((add ^ t) & (x[q] ^ t)) < 0;     // signed add overflow
-                    }
-                    if (f == 0) {
-                        vv[q] = t;
-                    } else if ((uint64_t)(vv[q] + 0x80000000ll) < 0x100000000ull &&
-                               (uint64_t)(t + 0x80000000ll) < 0x100000000ull) {
-                        vv[q] = (int64_t)(int32_t)vv[q] * (int64_t)(int32_t)t;   // both fit int32: exact
-                    } else {
-                        const int64_t lo = vv[q] * t;
-                        ov[q] |= __mul64hi(vv[q], t) != (lo >> 63);             // signed mul overflow
-                        vv[q] = lo;
+                    const int64_t t = neg ? add - x[q] : add + x[q];
+                    mx |= (uint64_t)(x[q] ^ (x[q] >> 63));
+                    mt |= (uint64_t)(t ^ (t >> 63));
+                    vv[q] = f == 0 ? t : vv[q] * t;
+                }
+                // |x| <= mx + 1 and |add| < 2^61 keep add +- x exact
+                addsafe = addsafe && (64 - __clzll(mx)) <= 61 && add < (1ll << 61) && add > -(1ll << 61);
+                bsum += (64 - __clzll(mt)) + 1;
+            }
+            if (!addsafe || bsum > 63) {   // rare: exact re-evaluation with checks
+                bool ov[GPT];
+#pragma unroll
+                for (int q = 0; q < GPT; q++) { vv[q] = 1; ov[q] = false; }
+                for (int f = 0; f < nf; f++) {
+                    const int c = a.pfc[j][f];
+                    const int64_t add = a.padd[j][f];
+                    const bool neg = a.psign[j][f] < 0;
+#pragma unroll
+                    for (int q = 0; q < GPT; q++) {
+                        const int64_t x = scol(st, a.uoff[c], a.udt[c], prow[q]);
+                        int64_t t;
+                        if (neg) {
+                            t = add - x;
+                            ov[q] |= ((add ^ x) & (add ^ t)) < 0;
+                        } else {
+                            t = add + x;
+                            ov[q] |= ((add ^ t) & (x ^ t)) < 0;
+                        }
+                        if (f == 0) {
+                            vv[q] = t;
+                        } else {
+                            const int64_t lo = vv[q] * t;
+                            ov[q] |= __mul64hi(vv[q], t) != (lo >> 63);
+                            vv[q] = lo;
+                        }
                     }
                 }
-            }
 #pragma unroll
-            for (int q = 0; q < GPT; q++)
-                if (ov[q] && prun[q] >= 0) ovf = 1;
+                for (int q = 0; q < GPT; q++)
+                    if (ov[q] && prun[q] >= 0) ovf = 1;
+            }
         }
         if (jj == 0) {   // (re)initialise the accumulators of this chunk of pairs
             const int np = min(PCH, a.n_pairs - j);

@@ -232,7 +232,7 @@ constexpr size_t scatter_tma_smem() {
 }
 
 template <typename KT, int IN, int IPT, int RB>
-__global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
+__global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
     constexpr int TILE = NT * IPT, BINS = 1 << RB, BPT = BINS / NT;
     constexpr uint32_t DM = BINS - 1u;
     using KIN = typename InKey<IN, KT>::T;
@@ -273,7 +273,12 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
         KT key[IPT];
         uint32_t pm[IPT], rk[IPT];
         for (int d = lane; d < BINS; d += 32) s.u.whist[warp][d] = 0;
-        for (int d = tid; d < BINS; d += NT) s.gstart[d] = a.ct[(tile / CHUNK) * BINS + d] + a.th[tile * BINS + d];
+        uint32_t gs[BPT];   // this tile's global digit starts: loaded now, used after ranking
+#pragma unroll
+        for (int j = 0; j < BPT; j++) {
+            const int d = tid + j * NT;
+            gs[j] = __ldg(a.ct + (tile / CHUNK) * BINS + d) + __ldg(a.th + tile * BINS + d);
+        }
         if (full(tile)) {
             mbar_wait(&s.mbar[st], ((st ? uses1 : uses0) - 1) & 1);
             const uint8_t* sp = st ? stage1 : stage0;
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
             const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
             unsigned peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-            for (int b = 0; b < RB; b++) {
+            for (int b = 0; b < RB; b++) {   // peers = lanes with the same digit: one ballot per digit bit
                 const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
                 peers &= ((d >> b) & 1u) ? bb : ~bb;
             }
@@ -368,6 +373,8 @@ __global__ void __launch_bounds__(NT, 2) scatter_tma_kernel(ScatterArgs a, int64
                 s.u.sorted.perm[rk[i]] = pm[i];
             }
         }
+#pragma unroll
+        for (int j = 0; j < BPT; j++) s.gstart[tid + j * NT] = gs[j];
         __syncthreads();
         const int tile_n = (int)min((int64_t)TILE, a.n - base);
         for (int j = tid; j < tile_n; j += NT) {
@@ -443,7 +450,7 @@ template <typename KT, int RB>
 static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o,
                        const int* shifts, int P) {
     constexpr int BINS = 1 << RB;
-    constexpr int IPT = sizeof(KT) == 4 ? 16 : 12;
+    constexpr int IPT = sizeof(KT) == 4 ? 16 : 12;   // 4096 / 3072 keys per tile
     constexpr int TILE = NT * IPT;
     const int64_t tiles = ceil_div(n, TILE);
     const int64_t chunks = ceil_div(tiles, CHUNK);

@@ -22,10 +22,13 @@ def main():
     orders, li = tpch_orders_lineitem(sf, seed=42, device="cuda")
     ok, lk = orders["o_orderkey"], li["l_orderkey"]
     q1, q6 = columns(li, Q1_COLS), columns(li, Q6_COLS)
+    lk32 = lk.to(torch.int32)
     ctx = T.context()
     ops = {
         "sort_build": lambda: ctx.sort(ok),
         "sort_probe": lambda: ctx.sort(lk),
+        "cub_sort_probe_i64": lambda: torch.sort(lk, stable=True),
+        "cub_sort_probe_i32": lambda: torch.sort(lk32, stable=True),
         "pkfk_join": lambda: ctx.pkfk_join(ok, lk),
         "smj_join": lambda: ctx.smj_join(ok, lk),
         "q1_groupby": lambda: ctx.groupby_agg(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS),
