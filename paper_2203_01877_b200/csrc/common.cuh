@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <map>
 #include <string>
 #include <unordered_map>
@@ -178,6 +179,82 @@ inline void check_col(const tqp_col& c, int64_t n, const char* what) {
     if (c.dtype != TQP_U8 && c.dtype != TQP_I32 && c.dtype != TQP_I64)
         fail(TQP_ERR_INVALID_ARGUMENT, std::string(what) + ": unsupported dtype");
     if (n > 0 && c.data == nullptr) fail(TQP_ERR_INVALID_ARGUMENT, std::string(what) + ": null data");
+}
+
+// ------------------------------------------------- predicate conjunctions
+// The filter of PAPER.md:829 is an AND of column-vs-constant comparisons. The host
+// folds the conjunction into one closed interval per column (lo <= x <= hi, the
+// intersection of the <, <=, >, >=, == bounds, clamped to the column's dtype) and
+// keeps each != as a negated point interval. A row passes a term iff
+// ((x - lo) mod 2^b <= (hi - lo) mod 2^b) != neg, b = 32 for u8/i32 columns and 64 for
+// i64: one subtract + one unsigned compare per term and row. Same truth value as the
+// predicates taken one by one; never reorders or drops a row.
+struct Term {
+    int col;          // column index (caller's numbering)
+    int dt;           // column dtype
+    int neg;          // 1: the row passes iff x is outside [lo, hi]
+    uint64_t lo;      // interval start (two's complement bits; 32-bit terms use the low half)
+    uint64_t width;   // hi - lo (mod 2^64)
+};
+struct TermSet {
+    int n = 0;
+    bool never = false;   // the conjunction is unsatisfiable: no row passes
+    Term t[TQP_MAX_PREDS];
+};
+
+inline void dtype_domain(int dt, int64_t& lo, int64_t& hi) {
+    if (dt == TQP_U8) { lo = 0; hi = 255; }
+    else if (dt == TQP_I32) { lo = INT32_MIN; hi = INT32_MAX; }
+    else { lo = INT64_MIN; hi = INT64_MAX; }
+}
+
+// col_dt(c) gives the dtype of column c; predicates are validated by the caller.
+template <typename DtOf>
+inline TermSet make_terms(const tqp_pred* preds, int n_preds, DtOf col_dt) {
+    TermSet s;
+    for (int q = 0; q < n_preds; q++) {   // one range term per distinct column, first-use order
+        if (preds[q].op == TQP_NE) continue;
+        const int c = preds[q].col;
+        bool seen = false;
+        for (int r = 0; r < q; r++) seen = seen || (preds[r].op != TQP_NE && preds[r].col == c);
+        if (seen) continue;
+        const int dt = col_dt(c);
+        int64_t dlo, dhi;
+        dtype_domain(dt, dlo, dhi);
+        int64_t lo = dlo, hi = dhi;
+        bool empty = false;
+        for (int r = q; r < n_preds; r++) {
+            if (preds[r].col != c || preds[r].op == TQP_NE) continue;
+            const int64_t v = preds[r].value;
+            switch (preds[r].op) {
+                case TQP_LT: if (v == INT64_MIN) empty = true; else hi = std::min(hi, v - 1); break;
+                case TQP_LE: hi = std::min(hi, v); break;
+                case TQP_GT: if (v == INT64_MAX) empty = true; else lo = std::max(lo, v + 1); break;
+                case TQP_GE: lo = std::max(lo, v); break;
+                default: lo = std::max(lo, v); hi = std::min(hi, v); break;   // TQP_EQ
+            }
+        }
+        if (empty || lo > hi) { s.never = true; s.n = 0; return s; }
+        if (lo == dlo && hi == dhi) continue;   // the whole domain: always true
+        s.t[s.n++] = Term{c, dt, 0, (uint64_t)lo, (uint64_t)hi - (uint64_t)lo};
+    }
+    for (int q = 0; q < n_preds; q++) {
+        if (preds[q].op != TQP_NE) continue;
+        const int dt = col_dt(preds[q].col);
+        int64_t dlo, dhi;
+        dtype_domain(dt, dlo, dhi);
+        const int64_t v = preds[q].value;
+        if (v < dlo || v > dhi) continue;        // no value of the column equals v: always true
+        s.t[s.n++] = Term{preds[q].col, dt, 1, (uint64_t)v, 0};
+    }
+    return s;
+}
+
+__device__ __forceinline__ bool term32(uint32_t x, uint32_t lo, uint32_t width, bool neg) {
+    return (x - lo <= width) != neg;
+}
+__device__ __forceinline__ bool term64(uint64_t x, uint64_t lo, uint64_t width, bool neg) {
+    return (x - lo <= width) != neg;
 }
 
 // --------------------------------------------------- decoupled look-back

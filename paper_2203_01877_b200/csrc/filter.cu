@@ -2,10 +2,11 @@
 //
 // Listing 1 (bitmap): mask = lt(col, c) [AND-ed over predicates, PAPER.md:829];
 // Listing 2 (selection vector): idx = nonzero(mask). One kernel evaluates the
-// conjunction per row, writes the u8 mask, and compacts passing row numbers in
-// ascending order: warp ballots -> per-(item, warp) counts -> block scan ->
-// decoupled look-back across tiles -> coalesced writes. No atomics whose order
-// could leak into the output.
+// conjunction per row (folded to one interval term per column, common.cuh), writes
+// the u8 mask, and compacts passing row numbers in ascending order: each thread owns
+// 8 consecutive rows (vector loads) -> warp scan of per-thread counts -> block scan ->
+// decoupled look-back across tiles -> rows staged in shared memory -> coalesced
+// writes. No atomics whose order could leak into the output.
 #include "internal.h"
 
 namespace tqp {
@@ -13,15 +14,13 @@ namespace tqp {
 namespace {
 constexpr int FNT = 256;
 constexpr int FNW = FNT / 32;
-constexpr int FIPT = 8;
+constexpr int FIPT = 8;                 // consecutive rows per thread (vector loads)
 constexpr int FTILE = FNT * FIPT;
 
 struct FilterArgs {
-    int n_preds;
-    const void* pcol[TQP_MAX_PREDS];
-    int pdt[TQP_MAX_PREDS];
-    int op[TQP_MAX_PREDS];
-    int64_t val[TQP_MAX_PREDS];
+    TermSet ts;                          // the conjunction, folded per column (common.cuh)
+    const void* tcol[TQP_MAX_PREDS];
+    int vec;                             // every term column and the mask are 16-byte aligned
     int64_t n;
     uint8_t* mask;
     int64_t* sel;
@@ -31,118 +30,113 @@ struct FilterArgs {
     int64_t n_tiles;
 };
 
-__device__ __forceinline__ bool cmp(int64_t x, int op, int64_t v) {
-    switch (op) {
-        case TQP_LT: return x < v;
-        case TQP_LE: return x <= v;
-        case TQP_GT: return x > v;
-        case TQP_GE: return x >= v;
-        case TQP_EQ: return x == v;
-        default: return x != v;
+// Rows r0 .. r0+FIPT-1 of a column; vector loads on full aligned tiles.
+template <typename T, typename V>
+__device__ __forceinline__ void load_rows(const T* c, int64_t r0, int64_t n, bool vec, T (&x)[FIPT]) {
+    if (vec) {
+        const V* v = reinterpret_cast<const V*>(c + r0);
+        constexpr int PER = sizeof(V) / sizeof(T);
+#pragma unroll
+        for (int j = 0; j < FIPT / PER; j++) {
+            const V u = __ldcs(v + j);
+            memcpy(&x[j * PER], &u, sizeof(V));
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < FIPT; i++) x[i] = r0 + i < n ? c[r0 + i] : T(0);
     }
 }
 
 __global__ void __launch_bounds__(FNT) filter_kernel(FilterArgs a) {
     __shared__ int64_t s_tile;
-    __shared__ uint32_t s_cnt[FIPT * FNW];
+    __shared__ uint32_t s_woff[FNW];
     __shared__ uint64_t s_excl;
+    __shared__ uint32_t s_tot;
+    __shared__ int64_t s_out[FTILE];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tile = take_tile(a.counter, &s_tile);
     const int64_t base = tile * FTILE;
-    unsigned bal[FIPT];
+    const int64_t r0 = base + (int64_t)tid * FIPT;
+    const bool full = base + FTILE <= a.n;
+    const bool vec = full && a.vec;
     bool pass[FIPT];
 #pragma unroll
-    for (int i = 0; i < FIPT; i++) pass[i] = base + i * FNT + tid < a.n;
-    const bool full = base + FTILE <= a.n;
-    // predicates: descriptor and dtype/op dispatch hoisted out of the row loop; all
-    // loads of a predicate column are independent (no short-circuit), 8 in flight
-    for (int q = 0; q < a.n_preds; q++) {
-        int64_t x[FIPT];
-        switch (a.pdt[q]) {
-            case TQP_U8: {
-                const uint8_t* c = (const uint8_t*)a.pcol[q] + base + tid;
+    for (int i = 0; i < FIPT; i++) pass[i] = !a.ts.never && r0 + i < a.n;
+    // one interval term per column: one load per row, subtract + unsigned compare
+    for (int q = 0; q < a.ts.n; q++) {
+        const Term& tm = a.ts.t[q];
+        const bool neg = tm.neg;
+        if (tm.dt == TQP_I64) {
+            unsigned long long x[FIPT];
+            load_rows<unsigned long long, ulonglong2>((const unsigned long long*)a.tcol[q], r0, a.n, vec, x);
 #pragma unroll
-                for (int i = 0; i < FIPT; i++) x[i] = (full || pass[i]) ? (int64_t)__ldg(c + i * FNT) : 0;
-                break;
-            }
-            case TQP_I32: {
-                const int32_t* c = (const int32_t*)a.pcol[q] + base + tid;
+            for (int i = 0; i < FIPT; i++) pass[i] &= term64(x[i], tm.lo, tm.width, neg);
+        } else if (tm.dt == TQP_I32) {
+            unsigned int x[FIPT];
+            load_rows<unsigned int, uint4>((const unsigned int*)a.tcol[q], r0, a.n, vec, x);
 #pragma unroll
-                for (int i = 0; i < FIPT; i++) x[i] = (full || pass[i]) ? (int64_t)__ldg(c + i * FNT) : 0;
-                break;
-            }
-            default: {
-                const long long* c = (const long long*)a.pcol[q] + base + tid;
+            for (int i = 0; i < FIPT; i++) pass[i] &= term32(x[i], (uint32_t)tm.lo, (uint32_t)tm.width, neg);
+        } else {
+            unsigned char x[FIPT];
+            load_rows<unsigned char, uint2>((const unsigned char*)a.tcol[q], r0, a.n, vec, x);
 #pragma unroll
-                for (int i = 0; i < FIPT; i++) x[i] = (full || pass[i]) ? (int64_t)__ldg(c + i * FNT) : 0;
-            }
-        }
-        const int64_t v = a.val[q];
-        switch (a.op[q]) {
-            case TQP_LT:
-#pragma unroll
-                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] < v;
-                break;
-            case TQP_LE:
-#pragma unroll
-                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] <= v;
-                break;
-            case TQP_GT:
-#pragma unroll
-                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] > v;
-                break;
-            case TQP_GE:
-#pragma unroll
-                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] >= v;
-                break;
-            case TQP_EQ:
-#pragma unroll
-                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] == v;
-                break;
-            default:
-#pragma unroll
-                for (int i = 0; i < FIPT; i++) pass[i] &= x[i] != v;
+            for (int i = 0; i < FIPT; i++) pass[i] &= term32(x[i], (uint32_t)tm.lo, (uint32_t)tm.width, neg);
         }
     }
+    uint32_t cnt = 0;
 #pragma unroll
-    for (int i = 0; i < FIPT; i++) {
-        const int64_t row = base + i * FNT + tid;
-        if (a.mask && row < a.n) a.mask[row] = (uint8_t)pass[i];
-        bal[i] = __ballot_sync(0xffffffffu, pass[i]);
-        if (lane == 0) s_cnt[i * FNW + warp] = __popc(bal[i]);
+    for (int i = 0; i < FIPT; i++) cnt += pass[i];
+    if (a.mask) {   // Listing 1's bitmap, one byte per row
+        if (vec) {
+            uint2 m;
+            m.x = (uint32_t)pass[0] | (uint32_t)pass[1] << 8 | (uint32_t)pass[2] << 16 | (uint32_t)pass[3] << 24;
+            m.y = (uint32_t)pass[4] | (uint32_t)pass[5] << 8 | (uint32_t)pass[6] << 16 | (uint32_t)pass[7] << 24;
+            __stcs(reinterpret_cast<uint2*>(a.mask + r0), m);
+        } else {
+#pragma unroll
+            for (int i = 0; i < FIPT; i++)
+                if (r0 + i < a.n) a.mask[r0 + i] = (uint8_t)pass[i];
+        }
     }
+    // rank of each passing row in the tile: thread-exclusive scan within the warp
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    const uint32_t texcl = x - cnt;
+    if (lane == 31) s_woff[warp] = x;
     __syncthreads();
     if (warp == 0) {
-        constexpr int PER = FIPT * FNW / 32;
-        uint32_t c[PER], local = 0;
+        const uint32_t wt = lane < FNW ? s_woff[lane] : 0;
+        uint32_t y = wt;
 #pragma unroll
-        for (int j = 0; j < PER; j++) { c[j] = s_cnt[lane * PER + j]; local += c[j]; }
-        uint32_t x = local;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+        for (int o = 1; o < FNW; o <<= 1) {
+            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
         }
-        const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
-        uint32_t run = x - local;
-#pragma unroll
-        for (int j = 0; j < PER; j++) { s_cnt[lane * PER + j] = run; run += c[j]; }
+        const uint32_t tot = __shfl_sync(0xffffffffu, y, FNW - 1);
         const uint64_t e = lookback_warp(a.status, tile, tot, OpAdd(), 0ull);
+        if (lane < FNW) s_woff[lane] = y - wt;
         if (lane == 0) {
             s_excl = e;
+            s_tot = tot;
             if (tile == a.n_tiles - 1) *a.total = (int64_t)(e + tot);
         }
     }
     __syncthreads();
     if (!a.sel) return;
-    const int64_t excl = (int64_t)s_excl;
-    const unsigned lt = lanemask_lt();
+    // Listing 2's selection vector: stage the tile's passing row numbers in shared
+    // memory in row order, then write them out coalesced
+    uint32_t lp = s_woff[warp] + texcl;
 #pragma unroll
-    for (int i = 0; i < FIPT; i++) {
-        if (bal[i] & (1u << lane)) {
-            const int64_t row = base + i * FNT + tid;
-            a.sel[excl + s_cnt[i * FNW + warp] + __popc(bal[i] & lt)] = row;
-        }
-    }
+    for (int i = 0; i < FIPT; i++)
+        if (pass[i]) s_out[lp++] = r0 + i;
+    __syncthreads();
+    const uint32_t tot = s_tot;
+    int64_t* dst = a.sel + s_excl;
+    for (uint32_t k = tid; k < tot; k += FNT) __stcs(reinterpret_cast<long long*>(dst + k), (long long)s_out[k]);
 }
 }  // namespace
 
@@ -154,15 +148,16 @@ void filter_compact(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, co
     if (n_preds > 0 && !preds) fail(TQP_ERR_INVALID_ARGUMENT, "filter: null preds");
     if (!mask_out && !sel_out && !n_sel_host) fail(TQP_ERR_INVALID_ARGUMENT, "filter: no output requested");
     for (int c = 0; c < n_cols; c++) check_col(cols[c], n, "filter column");
-    FilterArgs a{};
-    a.n_preds = n_preds;
     for (int q = 0; q < n_preds; q++) {
         if (preds[q].col < 0 || preds[q].col >= n_cols) fail(TQP_ERR_INVALID_ARGUMENT, "filter: predicate column");
         if (preds[q].op < TQP_LT || preds[q].op > TQP_NE) fail(TQP_ERR_INVALID_ARGUMENT, "filter: predicate op");
-        a.pcol[q] = cols[preds[q].col].data;
-        a.pdt[q] = cols[preds[q].col].dtype;
-        a.op[q] = preds[q].op;
-        a.val[q] = preds[q].value;
+    }
+    FilterArgs a{};
+    a.ts = make_terms(preds, n_preds, [&](int c) { return cols[c].dtype; });
+    a.vec = mask_out == nullptr || (uintptr_t)mask_out % 16 == 0;
+    for (int q = 0; q < a.ts.n; q++) {
+        a.tcol[q] = cols[a.ts.t[q].col].data;
+        a.vec = a.vec && (uintptr_t)a.tcol[q] % 16 == 0;
     }
     DevBuf<int64_t> total(ctx, 1);
     total.zero();

@@ -59,13 +59,11 @@ struct Phase1Args {
     int udt[MAXU];
     int uoff[MAXU];               // byte offset of the column inside a stage
     int stage_bytes;
+    int n_stages;
     int n_keys;
     int kcol[TQP_MAX_KEYS];
     const unsigned long long* krange;   // per key column min / max (device)
-    int n_preds;
-    int pcol[TQP_MAX_PREDS];
-    int pop[TQP_MAX_PREDS];
-    int64_t pval[TQP_MAX_PREDS];
+    TermSet ts;                   // predicate conjunction, one interval per column (Term.col = stage slot)
     int n_pairs;
     int prop[TQP_MAX_AGGS];
     int pnf[TQP_MAX_AGGS];
@@ -83,17 +81,6 @@ struct Phase1Args {
     int64_t cap;
     int* overflow;                // bit 0: value overflow, bit 1: partial capacity exceeded
 };
-
-__device__ __forceinline__ bool cmp_op(int64_t x, int op, int64_t v) {
-    switch (op) {
-        case TQP_LT: return x < v;
-        case TQP_LE: return x <= v;
-        case TQP_GT: return x > v;
-        case TQP_GE: return x >= v;
-        case TQP_EQ: return x == v;
-        default: return x != v;
-    }
-}
 
 __device__ __forceinline__ uint64_t key_part(int64_t v, int dt) {
     switch (dt) {
@@ -216,7 +203,8 @@ __device__ __forceinline__ void atomic_add_i128(uint64_t* lo_p, int64_t* hi_p, u
     if (h) atomicAdd((unsigned long long*)hi_p, (unsigned long long)h);
 }
 
-struct Work {   // shared-memory working set of one tile (after the two column stages)
+struct Work {   // shared-memory working set of one tile (after the column stages)
+    uint64_t mbar[4];               // first: the no-key path allocates only these
     uint64_t skey[2][GTILE];
     uint16_t sidx[2][GTILE];
     uint16_t srun[GTILE];
@@ -233,7 +221,6 @@ struct Work {   // shared-memory working set of one tile (after the two column s
     uint64_t s_min[GNW], s_max[GNW];
     uint64_t s_kmin[TQP_MAX_KEYS];
     int s_kshift[TQP_MAX_KEYS];
-    uint64_t mbar[2];
     int64_t s_pb;
     uint32_t s_m, s_U;
 };
@@ -307,52 +294,27 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
     bool pass[GPT];
 #pragma unroll
     for (int i = 0; i < GPT; i++) {
-        pass[i] = i * GNT + tid < nrows;
+        pass[i] = !a.ts.never && i * GNT + tid < nrows;
         key[i] = 0;
     }
-    // predicates: descriptor and dtype/op dispatch hoisted out of the row loop
-    for (int q = 0; q < a.n_preds; q++) {
-        const int c = a.pcol[q];
-        int64_t x[GPT];
-        const uint8_t* col = st + a.uoff[c];
-        switch (a.udt[c]) {
-            case TQP_U8:
+    // predicates: one interval term per column (common.cuh), dtype dispatch hoisted
+    for (int q = 0; q < a.ts.n; q++) {
+        const Term& tm = a.ts.t[q];
+        const uint8_t* col = st + a.uoff[tm.col];
+        const bool neg = tm.neg;
+        if (tm.dt == TQP_I64) {
 #pragma unroll
-                for (int i = 0; i < GPT; i++) x[i] = (int64_t)col[i * GNT + tid];
-                break;
-            case TQP_I32:
+            for (int i = 0; i < GPT; i++)
+                pass[i] &= term64(reinterpret_cast<const unsigned long long*>(col)[i * GNT + tid], tm.lo, tm.width, neg);
+        } else if (tm.dt == TQP_I32) {
 #pragma unroll
-                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid];
-                break;
-            default:
+            for (int i = 0; i < GPT; i++)
+                pass[i] &= term32(reinterpret_cast<const uint32_t*>(col)[i * GNT + tid], (uint32_t)tm.lo,
+                                  (uint32_t)tm.width, neg);
+        } else {
 #pragma unroll
-                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid];
-        }
-        const int64_t v = a.pval[q];
-        switch (a.pop[q]) {
-            case TQP_LT:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] < v;
-                break;
-            case TQP_LE:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] <= v;
-                break;
-            case TQP_GT:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] > v;
-                break;
-            case TQP_GE:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] >= v;
-                break;
-            case TQP_EQ:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] == v;
-                break;
-            default:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] != v;
+            for (int i = 0; i < GPT; i++)
+                pass[i] &= term32(col[i * GNT + tid], (uint32_t)tm.lo, (uint32_t)tm.width, neg);
         }
     }
     // packed key: column 0 most significant (reading R12), each column as (value - min)
@@ -723,124 +685,113 @@ struct NoKeyAcc {
     int ovf;
 };
 
-__device__ __forceinline__ void process_tile_nokey(const Phase1Args& a, const uint8_t* st, int64_t t, NoKeyAcc& acc) {
-    const int tid = threadIdx.x, lane = tid & 31;
+struct NoKeyWork {   // the no-key path's shared memory after the stages (aliases Work)
+    uint64_t mbar[4];
+    uint64_t pad[4];
+    uint16_t list[GNW][GTILE / GNW];   // per warp: the tile rows that passed the predicates
+};
+static_assert(offsetof(Work, mbar) == 0 && offsetof(NoKeyWork, mbar) == 0, "mbarriers lead both layouts");
+
+// One (op, expression) pair on one row: prod_f (add_f + sign_f * x_f), 64-bit with
+// overflow detection (the exact fallback re-runs on int128).
+__device__ __forceinline__ int64_t pair_value(const Phase1Args& a, const uint8_t* st, int jj, int row, bool& ov) {
+    int64_t vv = 1;
+    const int nf = a.pnf[jj];
+    for (int f = 0; f < nf; f++) {
+        const int c = a.pfc[jj][f];
+        const uint8_t* col = st + a.uoff[c];
+        const int64_t add = a.padd[jj][f];
+        int64_t x;
+        switch (a.udt[c]) {
+            case TQP_U8: x = (int64_t)col[row]; break;
+            case TQP_I32: x = (int64_t)reinterpret_cast<const int32_t*>(col)[row]; break;
+            default: x = (int64_t)reinterpret_cast<const long long*>(col)[row];
+        }
+        int64_t tt;
+        if (a.psign[jj][f] < 0) {
+            tt = add - x;
+            ov |= ((add ^ x) & (add ^ tt)) < 0;
+        } else {
+            tt = add + x;
+            ov |= ((add ^ tt) & (x ^ tt)) < 0;
+        }
+        if (f == 0) {
+            vv = tt;
+        } else if ((uint64_t)(vv + 0x80000000ll) < 0x100000000ull && (uint64_t)(tt + 0x80000000ll) < 0x100000000ull) {
+            vv = (int64_t)(int32_t)vv * (int64_t)(int32_t)tt;
+        } else {
+            const int64_t lo = vv * tt;
+            ov |= __mul64hi(vv, tt) != (lo >> 63);
+            vv = lo;
+        }
+    }
+    return vv;
+}
+
+// Each thread owns GPT consecutive rows of the stage (vector shared-memory loads);
+// rows that pass are listed per warp, and the aggregate expressions are evaluated on
+// the listed rows only (one lane per row), so a selective filter (Q6) pays for the
+// predicates on every row and for the arithmetic on the passing ones.
+__device__ __forceinline__ void process_tile_nokey(const Phase1Args& a, const uint8_t* st, int64_t t, NoKeyAcc& acc,
+                                                   NoKeyWork& nw) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int nrows = (int)min((int64_t)GTILE, a.n - t * GTILE);
+    const int r0 = tid * GPT;
+    static_assert(GPT == 4, "vector loads below assume 4 rows per thread");
     bool pass[GPT];
 #pragma unroll
-    for (int i = 0; i < GPT; i++) pass[i] = i * GNT + tid < nrows;
-    for (int q = 0; q < a.n_preds; q++) {
-        const int c = a.pcol[q];
-        int64_t x[GPT];
-        const uint8_t* col = st + a.uoff[c];
-        switch (a.udt[c]) {
-            case TQP_U8:
+    for (int i = 0; i < GPT; i++) pass[i] = !a.ts.never && r0 + i < nrows;
+    for (int q = 0; q < a.ts.n; q++) {
+        const Term& tm = a.ts.t[q];
+        const uint8_t* col = st + a.uoff[tm.col];
+        const bool neg = tm.neg;
+        if (tm.dt == TQP_I64) {
+            const ulonglong2 u0 = reinterpret_cast<const ulonglong2*>(col)[2 * tid];
+            const ulonglong2 u1 = reinterpret_cast<const ulonglong2*>(col)[2 * tid + 1];
+            pass[0] &= term64(u0.x, tm.lo, tm.width, neg);
+            pass[1] &= term64(u0.y, tm.lo, tm.width, neg);
+            pass[2] &= term64(u1.x, tm.lo, tm.width, neg);
+            pass[3] &= term64(u1.y, tm.lo, tm.width, neg);
+        } else if (tm.dt == TQP_I32) {
+            const uint4 u = reinterpret_cast<const uint4*>(col)[tid];
+            const uint32_t lo = (uint32_t)tm.lo, wd = (uint32_t)tm.width;
+            pass[0] &= term32(u.x, lo, wd, neg);
+            pass[1] &= term32(u.y, lo, wd, neg);
+            pass[2] &= term32(u.z, lo, wd, neg);
+            pass[3] &= term32(u.w, lo, wd, neg);
+        } else {
+            const uint32_t u = reinterpret_cast<const uint32_t*>(col)[tid];
+            const uint32_t lo = (uint32_t)tm.lo, wd = (uint32_t)tm.width;
 #pragma unroll
-                for (int i = 0; i < GPT; i++) x[i] = (int64_t)col[i * GNT + tid];
-                break;
-            case TQP_I32:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid];
-                break;
-            default:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid];
-        }
-        const int64_t v = a.pval[q];
-        switch (a.pop[q]) {
-            case TQP_LT:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] < v;
-                break;
-            case TQP_LE:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] <= v;
-                break;
-            case TQP_GT:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] > v;
-                break;
-            case TQP_GE:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] >= v;
-                break;
-            case TQP_EQ:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] == v;
-                break;
-            default:
-#pragma unroll
-                for (int i = 0; i < GPT; i++) pass[i] &= x[i] != v;
+            for (int i = 0; i < GPT; i++) pass[i] &= term32((u >> (8 * i)) & 0xFFu, lo, wd, neg);
         }
     }
-    bool anyp = false;
+    uint16_t* L = nw.list[warp];
+    const unsigned lt = lanemask_lt();
+    int cnt = 0;
 #pragma unroll
     for (int i = 0; i < GPT; i++) {
+        const unsigned b = __ballot_sync(0xffffffffu, pass[i]);
+        if (pass[i]) L[cnt + __popc(b & lt)] = (uint16_t)(r0 + i);
+        cnt += __popc(b);
         acc.count += pass[i] ? 1 : 0;
-        anyp |= pass[i];
     }
-    if (!__any_sync(0xffffffffu, anyp)) return;   // nothing passes in this warp's rows
+    if (cnt == 0) return;
+    __syncwarp();
+    for (int k = lane; k < cnt; k += 32) {
+        const int row = L[k];
+        bool ov = false;
 #pragma unroll
-    for (int jj = 0; jj < PCH; jj++) {
-        if (jj >= a.n_pairs) break;
-        const int op = a.prop[jj];
-        const int nf = a.pnf[jj];
-        int64_t vv[GPT];
-        bool ov[GPT];
-#pragma unroll
-        for (int i = 0; i < GPT; i++) { vv[i] = 1; ov[i] = false; }
-        for (int f = 0; f < nf; f++) {
-            const int c = a.pfc[jj][f];
-            const uint8_t* col = st + a.uoff[c];
-            const int64_t add = a.padd[jj][f];
-            const bool neg = a.psign[jj][f] < 0;
-            int64_t x[GPT];
-            switch (a.udt[c]) {
-                case TQP_U8:
-#pragma unroll
-                    for (int i = 0; i < GPT; i++) x[i] = (int64_t)col[i * GNT + tid];
-                    break;
-                case TQP_I32:
-#pragma unroll
-                    for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const int32_t*>(col)[i * GNT + tid];
-                    break;
-                default:
-#pragma unroll
-                    for (int i = 0; i < GPT; i++) x[i] = (int64_t)reinterpret_cast<const long long*>(col)[i * GNT + tid];
-            }
-#pragma unroll
-            for (int i = 0; i < GPT; i++) {
-                int64_t tt;
-                if (neg) {
-                    tt = add - x[i];
-                    ov[i] |= ((add ^ x[i]) & (add ^ tt)) < 0;
-                } else {
-                    tt = add + x[i];
-                    ov[i] |= ((add ^ tt) & (x[i] ^ tt)) < 0;
-                }
-                if (f == 0) {
-                    vv[i] = tt;
-                } else if ((uint64_t)(vv[i] + 0x80000000ll) < 0x100000000ull &&
-                           (uint64_t)(tt + 0x80000000ll) < 0x100000000ull) {
-                    vv[i] = (int64_t)(int32_t)vv[i] * (int64_t)(int32_t)tt;
-                } else {
-                    const int64_t lo = vv[i] * tt;
-                    ov[i] |= __mul64hi(vv[i], tt) != (lo >> 63);
-                    vv[i] = lo;
-                }
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < GPT; i++) {
-            if (!pass[i]) continue;
-            if (ov[i]) acc.ovf = 1;
-            const int64_t v = vv[i];
+        for (int jj = 0; jj < PCH; jj++) {
+            if (jj >= a.n_pairs) break;
+            const int op = a.prop[jj];
+            const int64_t v = pair_value(a, st, jj, row, ov);
             if (op == P_SUM) { acc.lo[jj] += (uint64_t)(uint32_t)v; acc.hi[jj] += (v >> 32); }
             else if (op == P_MIN) acc.lo[jj] = (uint64_t)min((int64_t)acc.lo[jj], v);
             else acc.lo[jj] = (uint64_t)max((int64_t)acc.lo[jj], v);
         }
+        if (ov) acc.ovf = 1;
     }
-    (void)lane;
 }
 
 // End of the persistent loop: reduce the CTA's register accumulators and emit one
@@ -901,12 +852,12 @@ __device__ void flush_nokey(const Phase1Args& a, NoKeyAcc& acc, Work& w) {
 
 __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
     extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t* stage[2] = {smem, smem + a.stage_bytes};
-    Work& w = *reinterpret_cast<Work*>(smem + 2 * a.stage_bytes);
+    const int NS = a.n_stages;   // 2..4 stages in flight per CTA
+    Work& w = *reinterpret_cast<Work*>(smem + (size_t)NS * a.stage_bytes);
+    auto stage_ptr = [&](int s) { return smem + (size_t)s * a.stage_bytes; };
     const int tid = threadIdx.x;
     if (tid == 0) {
-        mbar_init(&w.mbar[0], 1);
-        mbar_init(&w.mbar[1], 1);
+        for (int s = 0; s < NS; s++) mbar_init(&w.mbar[s], 1);
         fence_mbar_init();
         if (a.n_keys > 0) {
             int wd[TQP_MAX_KEYS];
@@ -919,7 +870,7 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
         mbar_expect_tx(&w.mbar[s], (uint32_t)a.stage_bytes);
         for (int c = 0; c < a.n_ucols; c++) {
             const uint32_t es = a.udt[c] == TQP_U8 ? 1 : a.udt[c] == TQP_I32 ? 4 : 8;
-            bulk_g2s(stage[s] + a.uoff[c], (const uint8_t*)a.ucol[c] + t * GTILE * es, GTILE * es, &w.mbar[s]);
+            bulk_g2s(stage_ptr(s) + a.uoff[c], (const uint8_t*)a.ucol[c] + t * GTILE * es, GTILE * es, &w.mbar[s]);
         }
     };
     const bool nokey = a.n_keys == 0 && a.n_pairs <= PCH;
@@ -932,8 +883,8 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
     }
     nacc.count = 0;
     nacc.ovf = 0;
-    uint32_t uses[2] = {0, 0};
-    for (int s = 0; s < 2; s++) {
+    uint32_t uses[4] = {0, 0, 0, 0};
+    for (int s = 0; s < NS; s++) {
         const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
         if (t < a.n_tiles && eligible(t)) {
             if (tid == 0) issue(t, s);
@@ -943,7 +894,7 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
     for (int64_t k = 0;; k++) {
         const int64_t t = blockIdx.x + k * gridDim.x;
         if (t >= a.n_tiles) break;
-        const int s = (int)(k & 1);
+        const int s = (int)(k % NS);
         if (eligible(t)) {
             mbar_wait(&w.mbar[s], (uses[s] - 1) & 1);
         } else {   // tail tile or unaligned columns: plain cooperative loads
@@ -952,22 +903,22 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
             for (int c = 0; c < a.n_ucols; c++) {
                 for (int r = tid; r < nrows; r += GNT) {
                     switch (a.udt[c]) {
-                        case TQP_U8: stage[s][a.uoff[c] + r] = ((const uint8_t*)a.ucol[c])[row0 + r]; break;
+                        case TQP_U8: stage_ptr(s)[a.uoff[c] + r] = ((const uint8_t*)a.ucol[c])[row0 + r]; break;
                         case TQP_I32:
-                            reinterpret_cast<int32_t*>(stage[s] + a.uoff[c])[r] = ((const int32_t*)a.ucol[c])[row0 + r];
+                            reinterpret_cast<int32_t*>(stage_ptr(s) + a.uoff[c])[r] = ((const int32_t*)a.ucol[c])[row0 + r];
                             break;
                         default:
-                            reinterpret_cast<long long*>(stage[s] + a.uoff[c])[r] =
+                            reinterpret_cast<long long*>(stage_ptr(s) + a.uoff[c])[r] =
                                 ((const long long*)a.ucol[c])[row0 + r];
                     }
                 }
             }
             __syncthreads();
         }
-        if (nokey) process_tile_nokey(a, stage[s], t, nacc);
-        else process_tile(a, stage[s], w, t);
+        if (nokey) process_tile_nokey(a, stage_ptr(s), t, nacc, reinterpret_cast<NoKeyWork&>(w));
+        else process_tile(a, stage_ptr(s), w, t);
         __syncthreads();   // every thread is done with stage s
-        const int64_t t2 = t + 2 * (int64_t)gridDim.x;
+        const int64_t t2 = t + (int64_t)NS * gridDim.x;
         if (t2 < a.n_tiles && eligible(t2)) {
             if (tid == 0) {
                 fence_proxy_async();
@@ -1367,12 +1318,8 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         if (off > 64) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: packed key wider than 64 bits");
         key_ranges(ctx, kc, kd, n_keys, n, PL->krange);
         a.krange = PL->krange.get();
-        a.n_preds = n_preds;
-        for (int q = 0; q < n_preds; q++) {
-            a.pcol[q] = uidx(preds[q].col);
-            a.pop[q] = preds[q].op;
-            a.pval[q] = preds[q].value;
-        }
+        a.ts = make_terms(preds, n_preds, [&](int c) { return cols[c].dtype; });
+        for (int q = 0; q < a.ts.n; q++) a.ts.t[q].col = uidx(a.ts.t[q].col);
         int pf[TQP_MAX_AGGS][3], ps[TQP_MAX_AGGS][3], pnf[TQP_MAX_AGGS];
         int64_t pa[TQP_MAX_AGGS][3];
         make_pairs(PL, aggs, n_aggs, pf, ps, pa, pnf);
@@ -1424,7 +1371,11 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             a.P_counter = Pc.get();
             a.overflow = ovf.get();
             if (n > 0) {
-                const size_t smem = 2 * (size_t)a.stage_bytes + sizeof(Work);
+                // pipeline depth: light per-row work (no group keys) is bandwidth-bound and
+                // wants more bytes in flight; keyed tiles are compute-heavy and prefer 2 CTAs/SM
+                const bool nokey_path = n_keys == 0 && PL->n_pairs <= PCH;
+                a.n_stages = (nokey_path && (size_t)4 * a.stage_bytes + sizeof(NoKeyWork) <= 112 * 1024) ? 4 : 2;
+                const size_t smem = (size_t)a.n_stages * a.stage_bytes + (nokey_path ? sizeof(NoKeyWork) : sizeof(Work));
                 if (smem > 227 * 1024) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: referenced columns too wide");
                 set_smem(gb_phase1_kernel, smem);
                 int occ = 1;

@@ -283,6 +283,64 @@ def test_filter_all_or_none(T, preds):
     assert np.array_equal(npy(mask), om) and np.array_equal(npy(sel), os_)
 
 
+I64_MIN, I64_MAX = -(1 << 63), (1 << 63) - 1
+FOLD_CASES = [   # the library folds each column's predicates into one interval (common.cuh make_terms)
+    [(0, "gt", 10), (0, "lt", 5)],                          # contradiction: nothing passes
+    [(0, "lt", I64_MIN)], [(0, "gt", I64_MAX)],             # empty at the int64 ends
+    [(0, "le", I64_MAX), (0, "ge", I64_MIN)],               # the whole domain
+    [(1, "eq", 300)], [(1, "ne", 300)], [(1, "lt", 0)], [(1, "ge", -5)],   # u8 beyond its domain
+    [(2, "gt", 1 << 40)], [(2, "ge", -(1 << 40)), (2, "le", 1 << 40)],     # i32 beyond its domain
+    [(1, "ne", 0), (1, "ne", 255), (1, "gt", 3), (1, "le", 200), (1, "ne", 100)],
+    [(0, "eq", 7), (0, "ge", 7), (0, "le", 7), (2, "ne", 0)],
+    [(0, "ge", -20), (0, "le", 45), (0, "gt", -30), (0, "lt", 40), (2, "lt", 0), (2, "gt", -500_000)],
+    [(2, "eq", 12345), (2, "ne", 12345)],
+]
+
+
+def fold_inputs(n, seed=5):
+    rng = np.random.default_rng(seed)
+    a = rng.integers(-50, 50, n)
+    a[:4] = [I64_MIN, I64_MAX, 7, -7]
+    b = rng.integers(0, 256, n).astype(np.uint8)
+    c = rng.integers(-10**6, 10**6, n).astype(np.int32)
+    c[:3] = [np.iinfo(np.int32).min, np.iinfo(np.int32).max, 12345]
+    return [a, b, c]
+
+
+@pytest.mark.parametrize("k", range(len(FOLD_CASES)))
+def test_filter_predicate_folding(T, k):
+    cols = fold_inputs(100_003)
+    preds = FOLD_CASES[k]
+    mask, sel = T.filter_compact([cu(cols[0]), cu(cols[1], torch.uint8), cu(cols[2], torch.int32)], preds)
+    om, os_ = oracle.filter_compact(cols, preds)
+    assert np.array_equal(npy(mask), om) and np.array_equal(npy(sel), os_)
+
+
+@pytest.mark.parametrize("k", range(len(FOLD_CASES)))
+def test_groupby_predicate_folding(T, k):
+    """Both group-by tile paths (keyed: strided rows; no key: vector rows + pass lists)."""
+    cols = fold_inputs(50_001)
+    g = (cols[0] & 3).astype(np.int64)
+    dcols = [cu(cols[0]), cu(cols[1], torch.uint8), cu(cols[2], torch.int32), cu(g)]
+    hcols = cols + [g]
+    aggs = [("sum", [(2, 0, 1)]), ("count", []), ("max", [(1, 0, 1)]), ("min", [(2, 1, -1)])]
+    for keys in ([3], []):
+        got = T.groupby_agg(dcols, keys, aggs, FOLD_CASES[k])
+        want = oracle.groupby_agg(hcols, keys, aggs, FOLD_CASES[k])
+        check_groupby(T, got, want, aggs)
+
+
+def test_filter_unaligned_columns(T):
+    """Columns starting 8 bytes into an allocation take the scalar loads."""
+    base = torch.randint(-100, 100, (300_001,), dtype=torch.int64, device="cuda")
+    x = base[1:]
+    assert x.data_ptr() % 16 != 0
+    preds = [(0, "ge", -20), (0, "lt", 60)]
+    mask, sel = T.filter_compact([x], preds)
+    om, os_ = oracle.filter_compact([npy(x)], preds)
+    assert np.array_equal(npy(mask), om) and np.array_equal(npy(sel), os_)
+
+
 def test_filter_q6_sf1(T):
     _, li = tpch_orders_lineitem(1.0, seed=42, device="cuda")
     cols = columns(li, Q6_COLS)

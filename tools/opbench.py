@@ -30,13 +30,17 @@ def main():
         "cub_sort_probe_i64": lambda: torch.sort(lk, stable=True),
         "cub_sort_probe_i32": lambda: torch.sort(lk32, stable=True),
         "pkfk_join": lambda: ctx.pkfk_join(ok, lk),
+        "pkfk_small_build": lambda: ctx.pkfk_join(ok[:65536], lk),
         "smj_join": lambda: ctx.smj_join(ok, lk),
         "q1_groupby": lambda: ctx.groupby_agg(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS),
         "q6_filter": lambda: ctx.filter_compact(q6, Q6_PREDS),
         "q6_sum": lambda: ctx.groupby_agg(q6, [], Q6_AGGS, Q6_PREDS),
     }
     out = {}
+    only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
     for name, f in ops.items():
+        if only and name not in only:
+            continue
         for _ in range(2):
             f()
         torch.cuda.synchronize()
