@@ -64,6 +64,13 @@ struct Phase1Args {
     int kcol[TQP_MAX_KEYS];
     const unsigned long long* krange;   // per key column min / max (device)
     TermSet ts;                   // predicate conjunction, one interval per column (Term.col = stage slot)
+    // dense small-domain path (gb_dense_kernel)
+    int D;                        // distinct packed keys present; ids 0..D-1
+    const uint8_t* dtab;          // packed key -> id
+    const uint64_t* dkeys;        // id -> packed key
+    int dense_bits;               // SUM pairs: |value| <= 2^dense_bits keeps per-thread int64 sums exact
+    int poff[PCH][3];             // stage byte offset of each factor's column
+    int pdtf[PCH][3];             // and its dtype
     int n_pairs;
     int prop[TQP_MAX_AGGS];
     int pnf[TQP_MAX_AGGS];
@@ -224,6 +231,18 @@ struct Work {   // shared-memory working set of one tile (after the column stage
     int64_t s_pb;
     uint32_t s_m, s_U;
 };
+constexpr int WRUNS = 4;   // runs a warp may span for the warp-reduction path
+// Per-warp run partials of the warp-reduction path (aliases the tile's sort key
+// buffers, which are dead once the partial keys are written): combined per run
+// without shared-memory atomics (64-bit ones are compare-and-swap loops).
+struct WarpPart {
+    uint64_t lo[PCH][GNW][WRUNS];
+    int64_t hi[PCH][GNW][WRUNS];
+    uint32_t r0[GNW];
+    uint8_t nr[PCH][GNW];
+};
+static_assert(sizeof(WarpPart) <= sizeof(uint64_t) * 2 * GTILE, "WarpPart fits the sort key buffers");
+
 
 // One stable LSD pass over positions [0, m) of the tile: rank by the 8-bit digit
 // at `shift` with warp match_any, then scatter to the other buffer.
@@ -514,6 +533,11 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
     const int wr0 = __shfl_sync(0xffffffffu, r0, 0);
     const bool uniform = __all_sync(0xffffffffu, any && r0 == rl && r0 == wr0);
     int ovf = 0;
+    // the runs this warp's 128 sorted positions span
+    const uint32_t rlo = __reduce_min_sync(0xffffffffu, any ? (uint32_t)r0 : 0xFFFFFFFFu);
+    const uint32_t rhi = __reduce_max_sync(0xffffffffu, any ? (uint32_t)rl : 0u);
+    const bool wsmall = sm_acc && rlo != 0xFFFFFFFFu && rhi == rlo;
+    WarpPart& wp = *reinterpret_cast<WarpPart*>(&w.skey[0][0]);
     for (int j = 0; j < a.n_pairs; j++) {
         const int op = a.prop[j];
         const int jj = j % PCH;
@@ -630,6 +654,32 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
                 atomicMax((long long*)(dl + run), (long long)lo);
             }
         };
+        // Sums over a warp whose 128 sorted positions span at most 4 runs: per run, the
+        // thread's values are split into 24-bit pieces (1, 2 or 3 by the warp's magnitude
+        // bound) whose warp totals fit 32 bits, summed by redux.sync and recombined exactly
+        // into the split (low-half, high-half) form.
+        if (op == P_SUM && wsmall && rlo == rhi) {   // one run: serial + butterfly, no atomics
+            uint64_t l2 = 0;
+            int64_t h2 = 0;
+#pragma unroll
+            for (int q = 0; q < GPT; q++) {
+                if (prun[q] < 0) break;
+                l2 += (uint64_t)(uint32_t)vv[q];
+                h2 += vv[q] >> 32;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                l2 += __shfl_xor_sync(0xffffffffu, l2, o);
+                h2 += __shfl_xor_sync(0xffffffffu, h2, o);
+            }
+            if (lane == 0) {
+                wp.lo[jj][warp][0] = l2;
+                wp.hi[jj][warp][0] = h2;
+                wp.r0[warp] = rlo;
+                wp.nr[jj][warp] = 1;
+            }
+        } else {
+        if (sm_acc && lane == 0) wp.nr[jj][warp] = 0;
         int cur = r0;
 #pragma unroll
         for (int q = 0; q < GPT; q++) {
@@ -661,13 +711,23 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
         } else if (any) {
             flush(cur);
         }
+        }
         if (jj == PCH - 1 || j == a.n_pairs - 1) __syncthreads();
         if (sm_acc && (jj == PCH - 1 || j == a.n_pairs - 1)) {   // chunk complete: write its partials
             const int jb = j - jj, np = jj + 1;
             for (int idx = tid; idx < np * U; idx += GNT) {
                 const int k2 = idx / U, u = idx - k2 * U;
-                a.plo[jb + k2][pb + u] = w.alo[k2][u];
-                if (a.prop[jb + k2] == P_SUM) a.phi[jb + k2][pb + u] = w.ahi[k2][u];
+                uint64_t lo2 = w.alo[k2][u];
+                int64_t hi2 = w.ahi[k2][u];
+                if (a.prop[jb + k2] == P_SUM) {
+#pragma unroll
+                    for (int ww = 0; ww < GNW; ww++) {   // warp-reduction partials of this run
+                        const uint32_t d = (uint32_t)u - wp.r0[ww];
+                        if (d < (uint32_t)wp.nr[k2][ww]) { lo2 += wp.lo[k2][ww][d]; hi2 += wp.hi[k2][ww][d]; }
+                    }
+                    a.phi[jb + k2][pb + u] = hi2;
+                }
+                a.plo[jb + k2][pb + u] = lo2;
             }
             __syncthreads();
         }
@@ -850,39 +910,23 @@ __device__ void flush_nokey(const Phase1Args& a, NoKeyAcc& acc, Work& w) {
     (void)w;
 }
 
-__global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    const int NS = a.n_stages;   // 2..4 stages in flight per CTA
-    Work& w = *reinterpret_cast<Work*>(smem + (size_t)NS * a.stage_bytes);
-    auto stage_ptr = [&](int s) { return smem + (size_t)s * a.stage_bytes; };
+// The persistent tile loop shared by the phase-1 kernels: tiles t = blockIdx.x +
+// k * gridDim.x are streamed into NS shared-memory stages with TMA bulk copies
+// (mbarrier completion; stage s is refilled as soon as every thread is done with it);
+// tail tiles and unaligned columns take plain cooperative loads.
+template <typename F>
+__device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem, uint64_t* mbar, F&& process) {
+    const int NS = a.n_stages;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        for (int s = 0; s < NS; s++) mbar_init(&w.mbar[s], 1);
-        fence_mbar_init();
-        if (a.n_keys > 0) {
-            int wd[TQP_MAX_KEYS];
-            key_layout(a.krange, a.n_keys, w.s_kmin, w.s_kshift, wd);
-        }
-    }
-    __syncthreads();
+    auto stage_ptr = [&](int s) { return smem + (size_t)s * a.stage_bytes; };
     auto eligible = [&](int64_t t) { return a.bulk_ok && (t + 1) * GTILE <= a.n; };
     auto issue = [&](int64_t t, int s) {   // thread 0 only
-        mbar_expect_tx(&w.mbar[s], (uint32_t)a.stage_bytes);
+        mbar_expect_tx(&mbar[s], (uint32_t)a.stage_bytes);
         for (int c = 0; c < a.n_ucols; c++) {
             const uint32_t es = a.udt[c] == TQP_U8 ? 1 : a.udt[c] == TQP_I32 ? 4 : 8;
-            bulk_g2s(stage_ptr(s) + a.uoff[c], (const uint8_t*)a.ucol[c] + t * GTILE * es, GTILE * es, &w.mbar[s]);
+            bulk_g2s(stage_ptr(s) + a.uoff[c], (const uint8_t*)a.ucol[c] + t * GTILE * es, GTILE * es, &mbar[s]);
         }
     };
-    const bool nokey = a.n_keys == 0 && a.n_pairs <= PCH;
-    NoKeyAcc nacc;
-#pragma unroll
-    for (int jj = 0; jj < PCH; jj++) {
-        const int op = jj < a.n_pairs ? a.prop[jj] : P_SUM;
-        nacc.lo[jj] = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
-        nacc.hi[jj] = 0;
-    }
-    nacc.count = 0;
-    nacc.ovf = 0;
     uint32_t uses[4] = {0, 0, 0, 0};
     for (int s = 0; s < NS; s++) {
         const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
@@ -896,7 +940,7 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
         if (t >= a.n_tiles) break;
         const int s = (int)(k % NS);
         if (eligible(t)) {
-            mbar_wait(&w.mbar[s], (uses[s] - 1) & 1);
+            mbar_wait(&mbar[s], (uses[s] - 1) & 1);
         } else {   // tail tile or unaligned columns: plain cooperative loads
             const int64_t row0 = t * GTILE;
             const int nrows = (int)min((int64_t)GTILE, a.n - row0);
@@ -915,8 +959,7 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
             }
             __syncthreads();
         }
-        if (nokey) process_tile_nokey(a, stage_ptr(s), t, nacc, reinterpret_cast<NoKeyWork&>(w));
-        else process_tile(a, stage_ptr(s), w, t);
+        process(stage_ptr(s), t);
         __syncthreads();   // every thread is done with stage s
         const int64_t t2 = t + (int64_t)NS * gridDim.x;
         if (t2 < a.n_tiles && eligible(t2)) {
@@ -927,7 +970,309 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
             uses[s]++;
         }
     }
+}
+
+__global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int NS = a.n_stages;   // 2..4 stages in flight per CTA
+    Work& w = *reinterpret_cast<Work*>(smem + (size_t)NS * a.stage_bytes);
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        for (int s = 0; s < NS; s++) mbar_init(&w.mbar[s], 1);
+        fence_mbar_init();
+        if (a.n_keys > 0) {
+            int wd[TQP_MAX_KEYS];
+            key_layout(a.krange, a.n_keys, w.s_kmin, w.s_kshift, wd);
+        }
+    }
+    __syncthreads();
+    const bool nokey = a.n_keys == 0 && a.n_pairs <= PCH;
+    NoKeyAcc nacc;
+#pragma unroll
+    for (int jj = 0; jj < PCH; jj++) {
+        const int op = jj < a.n_pairs ? a.prop[jj] : P_SUM;
+        nacc.lo[jj] = op == P_SUM ? 0ull : (op == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+        nacc.hi[jj] = 0;
+    }
+    nacc.count = 0;
+    nacc.ovf = 0;
+    tile_pipeline(a, smem, w.mbar, [&](const uint8_t* st, int64_t t) {
+        if (nokey) process_tile_nokey(a, st, t, nacc, reinterpret_cast<NoKeyWork&>(w));
+        else process_tile(a, st, w, t);
+    });
     if (nokey) flush_nokey(a, nacc, w);
+}
+
+// ------------------------------------------------ dense small-domain path
+// When the packed keys present in the input are few (D <= DMAX, e.g. TPC-H Q1's four
+// (returnflag, linestatus) groups), the tile sort is unnecessary: a presence pass
+// marks the packed keys that occur, a prefix popcount gives every present key a
+// dense id, and phase 1 adds each passing row into lane-private int64 accumulators
+// acc[id][pair][thread] in shared memory (no sort, no atomics, no shuffles). One
+// partial record per (CTA, id) goes to the same phase 2. Values are computed with
+// wrapping 64-bit arithmetic, exact because a per-thread magnitude bound on the
+// inputs proves |value| <= 2^bits (the result mod 2^64 is the true value whenever
+// |true value| < 2^63); per-thread sums stay below 2^62 by the host's choice of
+// dense_bits. A tile that cannot be proven sets overflow bit 2 and the host re-runs
+// the general path.
+constexpr int PBITS = 16;   // packed key width the presence bitmap covers
+constexpr int DMAX = 16;    // distinct keys of the dense path
+
+struct PresArgs {
+    int n_keys;
+    const void* kcol[TQP_MAX_KEYS];
+    int kdt[TQP_MAX_KEYS];
+    int64_t n;
+    const unsigned long long* krange;
+    uint32_t* bitmap;   // 2^PBITS bits
+};
+
+__global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
+    __shared__ uint32_t bm[1 << (PBITS - 5)];
+    __shared__ uint64_t kmin[TQP_MAX_KEYS];
+    __shared__ int sh[TQP_MAX_KEYS];
+    __shared__ int tw;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        int wd[TQP_MAX_KEYS];
+        key_layout(a.krange, a.n_keys, kmin, sh, wd);
+        int s = 0;
+        for (int k = 0; k < a.n_keys; k++) s += wd[k];
+        tw = s;
+    }
+    for (int w = tid; w < (1 << (PBITS - 5)); w += GNT) bm[w] = 0;
+    __syncthreads();
+    if (tw > PBITS) return;
+    const int64_t gs = (int64_t)gridDim.x * GNT;
+    for (int64_t r = blockIdx.x * (int64_t)GNT + tid; r < a.n; r += gs) {
+        uint32_t b = 0;
+        for (int k = 0; k < a.n_keys; k++)
+            b |= (uint32_t)(key_part(load_as_i64(a.kcol[k], a.kdt[k], r), a.kdt[k]) - kmin[k]) << sh[k];
+        const uint32_t m = 1u << (b & 31);
+        if (!(bm[b >> 5] & m)) atomicOr(&bm[b >> 5], m);
+    }
+    __syncthreads();
+    for (int w = tid; w < (1 << (PBITS - 5)); w += GNT)
+        if (bm[w]) atomicOr(&a.bitmap[w], bm[w]);
+}
+
+// one CTA of 1024 threads: D = popcount of the bitmap; if D <= DMAX, ids in key order
+__global__ void __launch_bounds__(1024) gb_dense_ids_kernel(const uint32_t* bitmap, uint8_t* dtab, uint64_t* dkeys,
+                                                             int* D_out) {
+    __shared__ uint32_t s_w[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int WPT = (1 << (PBITS - 5)) / 1024;
+    uint32_t wv[WPT], c = 0;
+#pragma unroll
+    for (int j = 0; j < WPT; j++) { wv[j] = bitmap[tid * WPT + j]; c += __popc(wv[j]); }
+    uint32_t x = c;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = s_w[lane], z = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, z, o);
+            if (lane >= o) z += y;
+        }
+        s_w[lane] = z - v;
+        if (lane == 31) *D_out = (int)z;
+        __syncwarp();
+    }
+    __syncthreads();
+    uint32_t id = s_w[warp] + x - c;
+    const uint32_t D = s_w[31] + 0;   // exclusive prefix of the last warp (total read below)
+    (void)D;
+#pragma unroll
+    for (int j = 0; j < WPT; j++) {
+        uint32_t m = wv[j];
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            if (id < (uint32_t)DMAX) {
+                const uint32_t bin = (uint32_t)(tid * WPT + j) * 32u + (uint32_t)b;
+                dtab[bin] = (uint8_t)id;
+                dkeys[id] = bin;
+            }
+            id++;
+        }
+    }
+}
+
+struct DenseHdr {
+    uint64_t mbar[4];
+    uint64_t kmin[TQP_MAX_KEYS];
+    int kshift[TQP_MAX_KEYS];
+    int64_t dcnt[DMAX];
+    int64_t drec[DMAX];
+    int bad;
+};
+
+// 4 consecutive rows (thread-contiguous) of a staged column, sign/zero-extended
+__device__ __forceinline__ void load4(const uint8_t* col, int dt, int tid, int64_t (&x)[GPT]) {
+    if (dt == TQP_I64) {
+        const longlong2 u0 = reinterpret_cast<const longlong2*>(col)[2 * tid];
+        const longlong2 u1 = reinterpret_cast<const longlong2*>(col)[2 * tid + 1];
+        x[0] = u0.x; x[1] = u0.y; x[2] = u1.x; x[3] = u1.y;
+    } else if (dt == TQP_I32) {
+        const int4 u = reinterpret_cast<const int4*>(col)[tid];
+        x[0] = u.x; x[1] = u.y; x[2] = u.z; x[3] = u.w;
+    } else {
+        const uint32_t u = reinterpret_cast<const uint32_t*>(col)[tid];
+#pragma unroll
+        for (int i = 0; i < GPT; i++) x[i] = (int64_t)((u >> (8 * i)) & 0xFFu);
+    }
+}
+
+__device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* st, int64_t t, const DenseHdr& h,
+                                           int64_t* acc, uint32_t* cnt, int& bad) {
+    const int tid = threadIdx.x;
+    const int nrows = (int)min((int64_t)GTILE, a.n - t * GTILE);
+    const int r0 = tid * GPT;
+    bool pass[GPT];
+#pragma unroll
+    for (int i = 0; i < GPT; i++) pass[i] = !a.ts.never && r0 + i < nrows;
+    for (int q = 0; q < a.ts.n; q++) {
+        const Term& tm = a.ts.t[q];
+        int64_t x[GPT];
+        load4(st + a.uoff[tm.col], tm.dt, tid, x);
+        if (tm.dt == TQP_I64) {
+#pragma unroll
+            for (int i = 0; i < GPT; i++) pass[i] &= term64((uint64_t)x[i], tm.lo, tm.width, tm.neg);
+        } else {
+#pragma unroll
+            for (int i = 0; i < GPT; i++) pass[i] &= term32((uint32_t)x[i], (uint32_t)tm.lo, (uint32_t)tm.width, tm.neg);
+        }
+    }
+    if (!(pass[0] | pass[1] | pass[2] | pass[3])) return;
+    // packed key (same layout as the general path) -> dense id
+    uint32_t kb[GPT] = {0, 0, 0, 0};
+    for (int c = 0; c < a.n_keys; c++) {
+        const int u = a.kcol[c];
+        const int dt = a.udt[u];
+        int64_t x[GPT];
+        load4(st + a.uoff[u], dt, tid, x);
+#pragma unroll
+        for (int i = 0; i < GPT; i++) kb[i] |= (uint32_t)(key_part(x[i], dt) - h.kmin[c]) << h.kshift[c];
+    }
+    int id[GPT];
+#pragma unroll
+    for (int i = 0; i < GPT; i++) {
+        id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
+        if (pass[i]) cnt[id[i] * GNT + tid]++;
+    }
+    const int np = a.n_pairs;
+#pragma unroll
+    for (int jj = 0; jj < PCH; jj++) {
+        if (jj >= np) break;
+        int64_t vv[GPT] = {1, 1, 1, 1};
+        int bs = 0;
+#pragma unroll
+        for (int f = 0; f < 3; f++) {
+            if (f >= a.pnf[jj]) break;
+            int64_t x[GPT];
+            load4(st + a.poff[jj][f], a.pdtf[jj][f], tid, x);
+            const int64_t add = a.padd[jj][f];
+            const bool neg = a.psign[jj][f] < 0;
+            uint64_t mx = 0;
+#pragma unroll
+            for (int i = 0; i < GPT; i++) {
+                if (pass[i]) mx |= (uint64_t)(x[i] ^ (x[i] >> 63));
+                const int64_t tt = (int64_t)(neg ? (uint64_t)add - (uint64_t)x[i] : (uint64_t)add + (uint64_t)x[i]);
+                vv[i] = f == 0 ? tt : (int64_t)((uint64_t)vv[i] * (uint64_t)tt);   // wrapping (mod 2^64)
+            }
+            const int ab = 64 - __clzll((uint64_t)(add ^ (add >> 63)));
+            bs += max(ab, 64 - __clzll(mx)) + 1;   // |add +- x| <= |add| + |x| <= 2^(max + 1)
+        }
+        const int op = a.prop[jj];
+        if (bs > (op == P_SUM ? a.dense_bits : 62)) bad = 1;
+#pragma unroll
+        for (int i = 0; i < GPT; i++) {
+            if (!pass[i]) continue;
+            int64_t* p = acc + ((size_t)(id[i] * np + jj) * GNT + tid);
+            if (op == P_SUM) *p += vv[i];
+            else if (op == P_MIN) *p = min(*p, vv[i]);
+            else *p = max(*p, vv[i]);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int NS = a.n_stages;
+    DenseHdr& h = *reinterpret_cast<DenseHdr*>(smem + (size_t)NS * a.stage_bytes);
+    int64_t* acc = reinterpret_cast<int64_t*>(smem + (size_t)NS * a.stage_bytes + ((sizeof(DenseHdr) + 15) & ~size_t(15)));
+    const int D = a.D, np = a.n_pairs;
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(acc + (size_t)D * np * GNT);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int s2 = 0; s2 < D * np; s2++) {   // own column only: no barrier needed before use
+        const int op = a.prop[s2 % np];
+        acc[(size_t)s2 * GNT + tid] = op == P_SUM ? 0 : (op == P_MIN ? INT64_MAX : INT64_MIN);
+    }
+    for (int d = 0; d < D; d++) cnt[d * GNT + tid] = 0;
+    if (tid == 0) {
+        for (int s = 0; s < NS; s++) mbar_init(&h.mbar[s], 1);
+        fence_mbar_init();
+        int wd[TQP_MAX_KEYS];
+        key_layout(a.krange, a.n_keys, h.kmin, h.kshift, wd);
+        h.bad = 0;
+    }
+    __syncthreads();
+    int bad = 0;
+    tile_pipeline(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile(a, st, t, h, acc, cnt, bad); });
+    if (bad) h.bad = 1;
+    // flush: counts per id, one partial record per present id
+    for (int d = warp; d < D; d += GNW) {
+        int64_t c = 0;
+        for (int t2 = lane; t2 < GNT; t2 += 32) c += cnt[d * GNT + t2];
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) h.dcnt[d] = c;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        if (h.bad) atomicOr(a.overflow, 4);
+        int nz = 0;
+        for (int d = 0; d < D; d++) nz += h.dcnt[d] > 0;
+        int64_t pb = nz ? (int64_t)atomicAdd(a.P_counter, (unsigned long long)nz) : 0;
+        if (pb + nz > a.cap) { atomicOr(a.overflow, 2); pb = -1; }
+        for (int d = 0; d < D; d++) {
+            if (pb >= 0 && h.dcnt[d] > 0) h.drec[d] = pb++;
+            else h.drec[d] = -1;
+        }
+    }
+    __syncthreads();
+    for (int s2 = warp; s2 < D * np; s2 += GNW) {
+        const int d = s2 / np, jj = s2 - d * np;
+        const int64_t rec = h.drec[d];
+        if (rec < 0) continue;
+        const int op = a.prop[jj];
+        const int64_t* col = acc + (size_t)s2 * GNT;
+        if (op == P_SUM) {   // exact: split halves of the per-thread int64 sums
+            uint64_t lo = 0;
+            int64_t hi = 0;
+            for (int t2 = lane; t2 < GNT; t2 += 32) { lo += (uint64_t)(uint32_t)col[t2]; hi += col[t2] >> 32; }
+            for (int o = 16; o > 0; o >>= 1) {
+                lo += __shfl_xor_sync(0xffffffffu, lo, o);
+                hi += __shfl_xor_sync(0xffffffffu, hi, o);
+            }
+            if (lane == 0) { a.plo[jj][rec] = lo; a.phi[jj][rec] = hi; }
+        } else {
+            int64_t v = op == P_MIN ? INT64_MAX : INT64_MIN;
+            for (int t2 = lane; t2 < GNT; t2 += 32) v = op == P_MIN ? min(v, col[t2]) : max(v, col[t2]);
+            for (int o = 16; o > 0; o >>= 1) {
+                const int64_t y = __shfl_xor_sync(0xffffffffu, v, o);
+                v = op == P_MIN ? min(v, y) : max(v, y);
+            }
+            if (lane == 0) a.plo[jj][rec] = (uint64_t)v;
+        }
+    }
+    for (int d = tid; d < D; d += GNT) {
+        const int64_t rec = h.drec[d];
+        if (rec >= 0) { a.pkey[rec] = a.dkeys[d]; a.pcount[rec] = h.dcnt[d]; }
+    }
 }
 
 // Phase 2a: group ids over the sorted partial keys (segment boundaries).
@@ -1348,13 +1693,76 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         a.bulk_ok = (aligned && a.n_ucols > 0) ? 1 : 0;
         const int64_t tiles = ceil_div(n, GTILE);
         a.n_tiles = tiles;
+        for (int j = 0; j < PL->n_pairs && j < PCH; j++)
+            for (int f = 0; f < pnf[j]; f++) {
+                a.poff[j][f] = a.uoff[a.pfc[j][f]];
+                a.pdtf[j][f] = a.udt[a.pfc[j][f]];
+            }
+
+        // ---- dense small-domain path (gb_dense_kernel): presence pass + dense ids
+        DevBuf<uint8_t> dtab;
+        DevBuf<uint64_t> dkeys;
+        bool dense = false;
+        size_t dense_smem = 0;
+        int dense_ns = 0;
+        int64_t dense_grid = 0;
+        const char* dz = getenv("TQP_GROUPBY_DENSE");
+        if (n_keys > 0 && n > 0 && PL->n_pairs <= PCH && !(dz && dz[0] == '0')) {
+            DevBuf<uint32_t> bitmap(ctx, 1 << (PBITS - 5));
+            DevBuf<int> Dd(ctx, 1);
+            bitmap.zero();
+            dtab.alloc(ctx, 1 << PBITS);
+            dkeys.alloc(ctx, DMAX);
+            PresArgs pa{};
+            pa.n_keys = n_keys;
+            pa.n = n;
+            pa.krange = PL->krange.get();
+            pa.bitmap = bitmap.get();
+            double kb = 0;
+            for (int k = 0; k < n_keys; k++) {
+                pa.kcol[k] = kc[k];
+                pa.kdt[k] = kd[k];
+                kb += (double)dtype_size(kd[k]);
+            }
+            const int g = (int)std::min<int64_t>(ceil_div(n, GNT * 8), (int64_t)ctx->num_sms * 4);
+            launch(ctx, "tqp_groupby_presence", gb_presence_kernel, dim3(g), dim3(GNT), 0, pa);
+            ctx->add_bytes("tqp_groupby_presence", kb * (double)n);
+            launch(ctx, "tqp_groupby_dense_ids", gb_dense_ids_kernel, dim3(1), dim3(1024), 0, (const uint32_t*)bitmap.get(),
+                   dtab.get(), dkeys.get(), Dd.get());
+            int D = 0;
+            read_back(ctx, &D, Dd.get(), 4);
+            if (D >= 1 && D <= DMAX) {
+                const size_t accb = (size_t)D * PL->n_pairs * GNT * 8 + (size_t)D * GNT * 4;
+                const size_t hdr = (sizeof(DenseHdr) + 15) & ~size_t(15);
+                int ns = 4;
+                while (ns >= 2 && (size_t)ns * a.stage_bytes + hdr + accb > 227 * 1024) ns--;
+                if (ns >= 2) {
+                    dense_ns = ns;
+                    dense_smem = (size_t)ns * a.stage_bytes + hdr + accb;
+                    set_smem(gb_dense_kernel, dense_smem);
+                    int occ = 1;
+                    TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_dense_kernel, GNT, dense_smem));
+                    dense_grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
+                    // rows per thread bound -> per-thread int64 sums of values <= 2^bits stay <= 2^62
+                    const int64_t rpt = ceil_div(tiles, dense_grid) * GPT;
+                    int lg = 0;
+                    while ((int64_t(1) << lg) < rpt) lg++;
+                    a.dense_bits = 62 - lg;
+                    a.D = D;
+                    a.dtab = dtab.get();
+                    a.dkeys = dkeys.get();
+                    dense = a.dense_bits >= 1;
+                }
+            }
+        }
 
         // ---- phase 1 (retried once with full capacity if the partial estimate is exceeded)
         Partials pr;
         DevBuf<unsigned long long> Pc(ctx, 1);
         DevBuf<int> ovf(ctx, 1);
         int64_t cap = std::min<int64_t>(std::max<int64_t>(n, 1), std::max<int64_t>(tiles * 64, 1 << 16));
-        for (int attempt = 0; attempt < 2; attempt++) {
+        const char* tile_name = "tqp_groupby_tile";
+        for (int attempt = 0; attempt < 3; attempt++) {
             pr.pkey.alloc(ctx, cap);
             pr.pcount.alloc(ctx, cap);
             for (int j = 0; j < PL->n_pairs; j++) {
@@ -1370,7 +1778,12 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             ovf.zero();
             a.P_counter = Pc.get();
             a.overflow = ovf.get();
-            if (n > 0) {
+            if (n > 0 && dense) {
+                a.n_stages = dense_ns;
+                tile_name = "tqp_groupby_dense";
+                launch(ctx, tile_name, gb_dense_kernel, dim3((unsigned)dense_grid), dim3(GNT), dense_smem, a);
+            } else if (n > 0) {
+                tile_name = "tqp_groupby_tile";
                 // pipeline depth: light per-row work (no group keys) is bandwidth-bound and
                 // wants more bytes in flight; keyed tiles are compute-heavy and prefer 2 CTAs/SM
                 const bool nokey_path = n_keys == 0 && PL->n_pairs <= PCH;
@@ -1387,6 +1800,10 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             read_back(ctx, &h[0], Pc.get(), 8);
             int o = 0;
             read_back(ctx, &o, ovf.get(), 4);
+            if (o & 4) {   // dense path could not prove a tile exact: general path
+                dense = false;
+                continue;
+            }
             if (o & 1) fail(TQP_ERR_OVERFLOW, "groupby: int64 overflow in an aggregate expression");
             pr.P = h[0];
             if (!(o & 2)) break;
@@ -1397,7 +1814,7 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             for (int i = 0; i < a.n_ucols; i++) in += (double)dtype_size(a.udt[i]);
             double rec = 16;
             for (int j = 0; j < PL->n_pairs; j++) rec += PL->pop[j] == P_SUM ? 16 : 8;
-            if (n > 0) ctx->add_bytes("tqp_groupby_tile", in * (double)n + rec * (double)pr.P);
+            if (n > 0) ctx->add_bytes(tile_name, in * (double)n + rec * (double)pr.P);
         }
         if (pr.P == 0) {
             PL->G = n_keys == 0 ? 1 : 0;

@@ -418,6 +418,83 @@ def test_groupby_random_parity(T, seed):
     check_groupby(T, got, want, AGGS_ALL)
 
 
+@pytest.mark.parametrize("e", [0, 22, 23, 24, 25, 46, 47, 48, 49, 60, 62])
+@pytest.mark.parametrize("card", [1, 3, 6, 40])
+def test_groupby_sum_magnitude_tiers(T, e, card):
+    """Sums over warps spanning few runs are reduced as 1, 2 or 3 24-bit pieces chosen
+    from the values' magnitude bound; values straddle each tier edge, both signs, and
+    products of two factors move the bound across tiers."""
+    rng = np.random.default_rng(e * 100 + card)
+    n = 70_001
+    k = rng.integers(0, card, n)
+    hi = 1 << e
+    v = rng.integers(-hi, hi + 1, n)
+    v[rng.random(n) < 0.01] = hi
+    v[rng.random(n) < 0.01] = -hi
+    small = rng.integers(-3, 4, n)
+    aggs = [("sum", [(1, 0, 1)]), ("sum", [(1, 0, -1)]), ("count", [])]
+    if e <= 60:                         # |v * (small + 1)| <= 2^62
+        aggs.append(("sum", [(1, 0, 1), (2, 1, 1)]))
+    cols = [k, v, small]
+    got = T.groupby_agg([cu(c) for c in cols], [0], aggs)
+    want = oracle.groupby_agg(cols, [0], aggs)
+    check_groupby(T, got, want, aggs)
+
+
+@pytest.mark.parametrize("card,wide", [(1, False), (2, False), (5, False), (6, False), (5, True)])
+def test_groupby_dense_path(T, card, wide, monkeypatch):
+    """Few distinct packed keys (<= 16, packed width <= 16 bits) take the sort-free dense
+    kernel; both it and the general tile path (TQP_GROUPBY_DENSE=0) match the oracle."""
+    rng = np.random.default_rng(card)
+    n = 200_003
+    k0 = (rng.integers(0, card, n) * 7 + 60).astype(np.uint8)
+    k1 = rng.integers(-2, 1, n).astype(np.int32)
+    if wide:   # packed width > 16 bits: the presence pass declines
+        k1 = (k1.astype(np.int64) * 100_000).astype(np.int32)
+    v = rng.integers(-10**9, 10**9, n)
+    w = rng.integers(0, 100, n)
+    cols = [k0, k1, v, w]
+    gcols = [cu(k0, torch.uint8), cu(k1, torch.int32), cu(v), cu(w)]
+    aggs = [("sum", [(2, 0, 1)]), ("sum", [(2, 0, 1), (3, 100, -1)]), ("count", []), ("min", [(2, 0, 1)]),
+            ("max", [(3, 5, 1)]), ("avg", [(2, 0, 1)])]
+    preds = [(3, "lt", 90)]
+    want = oracle.groupby_agg(cols, [0, 1], aggs, preds)
+    ctx = T.context()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    got = ctx.groupby_agg(gcols, [0, 1], aggs, preds)
+    st = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    check_groupby(T, got, want, aggs)
+    d_keys = card * 3
+    assert ("tqp_groupby_dense" in st) == (d_keys <= 16 and not wide)
+    monkeypatch.setenv("TQP_GROUPBY_DENSE", "0")
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    got = ctx.groupby_agg(gcols, [0, 1], aggs, preds)
+    st = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    check_groupby(T, got, want, aggs)
+    assert "tqp_groupby_dense" not in st
+
+
+def test_groupby_dense_bound_fallback(T):
+    """A product the dense path cannot prove exact re-runs on the general path."""
+    rng = np.random.default_rng(3)
+    n = 100_000
+    k = rng.integers(0, 3, n)
+    v = rng.integers(-(1 << 40), 1 << 40, n)
+    aggs = [("sum", [(1, 0, 1), (1, 0, 1)]), ("count", [])]    # |v*v| up to 2^80: int64 overflow
+    with pytest.raises(T.TqpError) as e:
+        T.groupby_agg([cu(k), cu(v)], [0], aggs)
+    assert e.value.status == T.TQP_ERR_OVERFLOW
+    v2 = rng.integers(-(1 << 30), 1 << 30, n)                   # |v*v| < 2^60 but > 2^dense_bits
+    aggs = [("sum", [(1, 0, 1), (1, 0, 1)]), ("count", [])]
+    got = T.groupby_agg([cu(k), cu(v2)], [0], aggs)
+    want = oracle.groupby_agg([k, v2], [0], aggs)
+    check_groupby(T, got, want, aggs)
+
+
 def test_groupby_key_wider_than_64_bits_rejected(T):
     x = cu(np.arange(10))
     with pytest.raises(T.TqpError) as e:

@@ -24,3 +24,7 @@ s = sum(tot.values()) or 1
 print("stall reasons:", {k[6:]: round(100 * v / s, 1) for k, v in sorted(tot.items(), key=lambda kv: -kv[1])[:7]})
 for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
     print(f"{100*v[0]/ts:5.1f}% stall {100*v[1]/ti:5.1f}% inst {k[0]}:{k[1]} {v[2]}")
+if len(sys.argv) > 3 and sys.argv[3] == "inst":
+    print("-- by instructions")
+    for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1])[:top]:
+        print(f"{100*v[1]/ti:5.1f}% inst {100*v[0]/ts:5.1f}% stall {k[0]}:{k[1]} {v[2]}")
