@@ -1043,13 +1043,54 @@ __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
     for (int w = tid; w < (1 << (PBITS - 5)); w += GNT) bm[w] = 0;
     __syncthreads();
     if (tw > PBITS) return;
+    auto mark = [&](uint32_t b) {
+        const uint32_t m = 1u << (b & 31);
+        if (!(bm[b >> 5] & m)) atomicOr(&bm[b >> 5], m);
+    };
+    // body: 16 consecutive rows per thread and step, 16-byte loads (aligned columns)
+    constexpr int R = 16;
+    bool vec = true;
+    for (int k = 0; k < a.n_keys; k++) vec = vec && (uintptr_t)a.kcol[k] % 16 == 0;
+    const int64_t nb = vec ? a.n / R : 0;
     const int64_t gs = (int64_t)gridDim.x * GNT;
-    for (int64_t r = blockIdx.x * (int64_t)GNT + tid; r < a.n; r += gs) {
+    for (int64_t g = blockIdx.x * (int64_t)GNT + tid; g < nb; g += gs) {
+        uint32_t b[R];
+#pragma unroll
+        for (int i = 0; i < R; i++) b[i] = 0;
+        for (int k = 0; k < a.n_keys; k++) {
+            const int dt = a.kdt[k];
+            const uint64_t mn = kmin[k];
+            const int s = sh[k];
+            if (dt == TQP_U8) {
+                const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g);
+                const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int i = 0; i < R; i++) b[i] |= (uint32_t)(((wv[i >> 2] >> (8 * (i & 3))) & 0xFFu) - (uint32_t)mn) << s;
+            } else if (dt == TQP_I32) {
+#pragma unroll
+                for (int j = 0; j < R / 4; j++) {
+                    const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g * 4 + j);
+                    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                    for (int i = 0; i < 4; i++) b[4 * j + i] |= ((wv[i] ^ 0x80000000u) - (uint32_t)mn) << s;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < R / 2; j++) {
+                    const ulonglong2 q = __ldcs(reinterpret_cast<const ulonglong2*>(a.kcol[k]) + g * 8 + j);
+                    b[2 * j] |= (uint32_t)((q.x ^ 0x8000000000000000ull) - mn) << s;
+                    b[2 * j + 1] |= (uint32_t)((q.y ^ 0x8000000000000000ull) - mn) << s;
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < R; i++) mark(b[i]);
+    }
+    for (int64_t r = nb * R + blockIdx.x * (int64_t)GNT + tid; r < a.n; r += gs) {   // tail / unaligned
         uint32_t b = 0;
         for (int k = 0; k < a.n_keys; k++)
             b |= (uint32_t)(key_part(load_as_i64(a.kcol[k], a.kdt[k], r), a.kdt[k]) - kmin[k]) << sh[k];
-        const uint32_t m = 1u << (b & 31);
-        if (!(bm[b >> 5] & m)) atomicOr(&bm[b >> 5], m);
+        mark(b);
     }
     __syncthreads();
     for (int w = tid; w < (1 << (PBITS - 5)); w += GNT)
@@ -1128,7 +1169,7 @@ __device__ __forceinline__ void load4(const uint8_t* col, int dt, int tid, int64
 }
 
 __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* st, int64_t t, const DenseHdr& h,
-                                           int64_t* acc, uint32_t* cnt, int& bad) {
+                                           int64_t* acc, uint32_t* cnt, uint64_t (&mt)[PCH][3]) {
     const int tid = threadIdx.x;
     const int nrows = (int)min((int64_t)GTILE, a.n - t * GTILE);
     const int r0 = tid * GPT;
@@ -1160,35 +1201,32 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     }
     int id[GPT];
 #pragma unroll
-    for (int i = 0; i < GPT; i++) {
-        id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
+    for (int i = 0; i < GPT; i++) id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
+#pragma unroll
+    for (int i = 0; i < GPT; i++)
         if (pass[i]) cnt[id[i] * GNT + tid]++;
-    }
     const int np = a.n_pairs;
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
         if (jj >= np) break;
         int64_t vv[GPT] = {1, 1, 1, 1};
-        int bs = 0;
 #pragma unroll
         for (int f = 0; f < 3; f++) {
             if (f >= a.pnf[jj]) break;
             int64_t x[GPT];
             load4(st + a.poff[jj][f], a.pdtf[jj][f], tid, x);
-            const int64_t add = a.padd[jj][f];
+            const uint64_t add = (uint64_t)a.padd[jj][f];
             const bool neg = a.psign[jj][f] < 0;
-            uint64_t mx = 0;
+            uint64_t m2 = mt[jj][f];
 #pragma unroll
             for (int i = 0; i < GPT; i++) {
-                if (pass[i]) mx |= (uint64_t)(x[i] ^ (x[i] >> 63));
-                const int64_t tt = (int64_t)(neg ? (uint64_t)add - (uint64_t)x[i] : (uint64_t)add + (uint64_t)x[i]);
-                vv[i] = f == 0 ? tt : (int64_t)((uint64_t)vv[i] * (uint64_t)tt);   // wrapping (mod 2^64)
+                const int64_t tt = (int64_t)(neg ? add - (uint64_t)x[i] : add + (uint64_t)x[i]);   // mod 2^64
+                if (pass[i]) m2 |= (uint64_t)(tt ^ (tt >> 63));
+                vv[i] = f == 0 ? tt : (int64_t)((uint64_t)vv[i] * (uint64_t)tt);                  // mod 2^64
             }
-            const int ab = 64 - __clzll((uint64_t)(add ^ (add >> 63)));
-            bs += max(ab, 64 - __clzll(mx)) + 1;   // |add +- x| <= |add| + |x| <= 2^(max + 1)
+            mt[jj][f] = m2;
         }
         const int op = a.prop[jj];
-        if (bs > (op == P_SUM ? a.dense_bits : 62)) bad = 1;
 #pragma unroll
         for (int i = 0; i < GPT; i++) {
             if (!pass[i]) continue;
@@ -1221,8 +1259,25 @@ __global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
         h.bad = 0;
     }
     __syncthreads();
-    int bad = 0;
-    tile_pipeline(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile(a, st, t, h, acc, cnt, bad); });
+    // per (pair, factor): OR of |add +- x| (as computed mod 2^64) over this thread's
+    // passing rows. |value| <= 2^(sum of bit lengths); a wrapped add +- x (|add| <
+    // 2^61, checked on the host) has |result| > 2^62 and so fails the bound below.
+    uint64_t mt[PCH][3];
+#pragma unroll
+    for (int jj = 0; jj < PCH; jj++)
+#pragma unroll
+        for (int f = 0; f < 3; f++) mt[jj][f] = 0;
+    tile_pipeline(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile(a, st, t, h, acc, cnt, mt); });
+    bool bad = false;
+#pragma unroll
+    for (int jj = 0; jj < PCH; jj++) {
+        if (jj >= np) break;
+        int bs = 0;
+#pragma unroll
+        for (int f = 0; f < 3; f++)
+            if (f < a.pnf[jj]) bs += 64 - __clzll(mt[jj][f]);
+        bad |= bs > (a.prop[jj] == P_SUM ? a.dense_bits : 62);
+    }
     if (bad) h.bad = 1;
     // flush: counts per id, one partial record per present id
     for (int d = warp; d < D; d += GNW) {
@@ -1707,7 +1762,10 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         int dense_ns = 0;
         int64_t dense_grid = 0;
         const char* dz = getenv("TQP_GROUPBY_DENSE");
-        if (n_keys > 0 && n > 0 && PL->n_pairs <= PCH && !(dz && dz[0] == '0')) {
+        bool small_add = true;   // the dense bound argument needs |add| < 2^61
+        for (int j = 0; j < PL->n_pairs && j < PCH; j++)
+            for (int f = 0; f < pnf[j]; f++) small_add = small_add && a.padd[j][f] < (1ll << 61) && a.padd[j][f] > -(1ll << 61);
+        if (n_keys > 0 && n > 0 && PL->n_pairs <= PCH && small_add && !(dz && dz[0] == '0')) {
             DevBuf<uint32_t> bitmap(ctx, 1 << (PBITS - 5));
             DevBuf<int> Dd(ctx, 1);
             bitmap.zero();
@@ -1724,7 +1782,7 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
                 pa.kdt[k] = kd[k];
                 kb += (double)dtype_size(kd[k]);
             }
-            const int g = (int)std::min<int64_t>(ceil_div(n, GNT * 8), (int64_t)ctx->num_sms * 4);
+            const int g = (int)std::min<int64_t>(ceil_div(n, GNT * 16), (int64_t)ctx->num_sms * 8);
             launch(ctx, "tqp_groupby_presence", gb_presence_kernel, dim3(g), dim3(GNT), 0, pa);
             ctx->add_bytes("tqp_groupby_presence", kb * (double)n);
             launch(ctx, "tqp_groupby_dense_ids", gb_dense_ids_kernel, dim3(1), dim3(1024), 0, (const uint32_t*)bitmap.get(),
