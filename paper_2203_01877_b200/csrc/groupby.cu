@@ -914,17 +914,18 @@ __device__ void flush_nokey(const Phase1Args& a, NoKeyAcc& acc, Work& w) {
 // k * gridDim.x are streamed into NS shared-memory stages with TMA bulk copies
 // (mbarrier completion; stage s is refilled as soon as every thread is done with it);
 // tail tiles and unaligned columns take plain cooperative loads.
-template <typename F>
+template <int NT, typename F>
 __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem, uint64_t* mbar, F&& process) {
+    constexpr int TR = NT * GPT;   // rows per tile
     const int NS = a.n_stages;
     const int tid = threadIdx.x;
     auto stage_ptr = [&](int s) { return smem + (size_t)s * a.stage_bytes; };
-    auto eligible = [&](int64_t t) { return a.bulk_ok && (t + 1) * GTILE <= a.n; };
+    auto eligible = [&](int64_t t) { return a.bulk_ok && (t + 1) * TR <= a.n; };
     auto issue = [&](int64_t t, int s) {   // thread 0 only
         mbar_expect_tx(&mbar[s], (uint32_t)a.stage_bytes);
         for (int c = 0; c < a.n_ucols; c++) {
             const uint32_t es = a.udt[c] == TQP_U8 ? 1 : a.udt[c] == TQP_I32 ? 4 : 8;
-            bulk_g2s(stage_ptr(s) + a.uoff[c], (const uint8_t*)a.ucol[c] + t * GTILE * es, GTILE * es, &mbar[s]);
+            bulk_g2s(stage_ptr(s) + a.uoff[c], (const uint8_t*)a.ucol[c] + t * TR * es, TR * es, &mbar[s]);
         }
     };
     uint32_t uses[4] = {0, 0, 0, 0};
@@ -942,10 +943,10 @@ __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem
         if (eligible(t)) {
             mbar_wait(&mbar[s], (uses[s] - 1) & 1);
         } else {   // tail tile or unaligned columns: plain cooperative loads
-            const int64_t row0 = t * GTILE;
-            const int nrows = (int)min((int64_t)GTILE, a.n - row0);
+            const int64_t row0 = t * TR;
+            const int nrows = (int)min((int64_t)TR, a.n - row0);
             for (int c = 0; c < a.n_ucols; c++) {
-                for (int r = tid; r < nrows; r += GNT) {
+                for (int r = tid; r < nrows; r += NT) {
                     switch (a.udt[c]) {
                         case TQP_U8: stage_ptr(s)[a.uoff[c] + r] = ((const uint8_t*)a.ucol[c])[row0 + r]; break;
                         case TQP_I32:
@@ -996,7 +997,7 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
     }
     nacc.count = 0;
     nacc.ovf = 0;
-    tile_pipeline(a, smem, w.mbar, [&](const uint8_t* st, int64_t t) {
+    tile_pipeline<GNT>(a, smem, w.mbar, [&](const uint8_t* st, int64_t t) {
         if (nokey) process_tile_nokey(a, st, t, nacc, reinterpret_cast<NoKeyWork&>(w));
         else process_tile(a, st, w, t);
     });
@@ -1168,10 +1169,11 @@ __device__ __forceinline__ void load4(const uint8_t* col, int dt, int tid, int64
     }
 }
 
+template <int NT>
 __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* st, int64_t t, const DenseHdr& h,
                                            int64_t* acc, uint32_t* cnt, uint64_t (&mt)[PCH][3]) {
     const int tid = threadIdx.x;
-    const int nrows = (int)min((int64_t)GTILE, a.n - t * GTILE);
+    const int nrows = (int)min((int64_t)NT * GPT, a.n - t * NT * GPT);
     const int r0 = tid * GPT;
     bool pass[GPT];
 #pragma unroll
@@ -1204,7 +1206,7 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     for (int i = 0; i < GPT; i++) id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
 #pragma unroll
     for (int i = 0; i < GPT; i++)
-        if (pass[i]) cnt[id[i] * GNT + tid]++;
+        if (pass[i]) cnt[id[i] * NT + tid]++;
     const int np = a.n_pairs;
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
@@ -1230,7 +1232,7 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
 #pragma unroll
         for (int i = 0; i < GPT; i++) {
             if (!pass[i]) continue;
-            int64_t* p = acc + ((size_t)(id[i] * np + jj) * GNT + tid);
+            int64_t* p = acc + ((size_t)(id[i] * np + jj) * NT + tid);
             if (op == P_SUM) *p += vv[i];
             else if (op == P_MIN) *p = min(*p, vv[i]);
             else *p = max(*p, vv[i]);
@@ -1238,19 +1240,21 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     }
 }
 
-__global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
+template <int NT>
+__global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
+    constexpr int NW = NT / 32;
     extern __shared__ __align__(128) uint8_t smem[];
     const int NS = a.n_stages;
     DenseHdr& h = *reinterpret_cast<DenseHdr*>(smem + (size_t)NS * a.stage_bytes);
     int64_t* acc = reinterpret_cast<int64_t*>(smem + (size_t)NS * a.stage_bytes + ((sizeof(DenseHdr) + 15) & ~size_t(15)));
     const int D = a.D, np = a.n_pairs;
-    uint32_t* cnt = reinterpret_cast<uint32_t*>(acc + (size_t)D * np * GNT);
+    uint32_t* cnt = reinterpret_cast<uint32_t*>(acc + (size_t)D * np * NT);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int s2 = 0; s2 < D * np; s2++) {   // own column only: no barrier needed before use
         const int op = a.prop[s2 % np];
-        acc[(size_t)s2 * GNT + tid] = op == P_SUM ? 0 : (op == P_MIN ? INT64_MAX : INT64_MIN);
+        acc[(size_t)s2 * NT + tid] = op == P_SUM ? 0 : (op == P_MIN ? INT64_MAX : INT64_MIN);
     }
-    for (int d = 0; d < D; d++) cnt[d * GNT + tid] = 0;
+    for (int d = 0; d < D; d++) cnt[d * NT + tid] = 0;
     if (tid == 0) {
         for (int s = 0; s < NS; s++) mbar_init(&h.mbar[s], 1);
         fence_mbar_init();
@@ -1267,7 +1271,7 @@ __global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
     for (int jj = 0; jj < PCH; jj++)
 #pragma unroll
         for (int f = 0; f < 3; f++) mt[jj][f] = 0;
-    tile_pipeline(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile(a, st, t, h, acc, cnt, mt); });
+    tile_pipeline<NT>(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile<NT>(a, st, t, h, acc, cnt, mt); });
     bool bad = false;
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
@@ -1280,9 +1284,9 @@ __global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
     }
     if (bad) h.bad = 1;
     // flush: counts per id, one partial record per present id
-    for (int d = warp; d < D; d += GNW) {
+    for (int d = warp; d < D; d += NW) {
         int64_t c = 0;
-        for (int t2 = lane; t2 < GNT; t2 += 32) c += cnt[d * GNT + t2];
+        for (int t2 = lane; t2 < NT; t2 += 32) c += cnt[d * NT + t2];
         for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
         if (lane == 0) h.dcnt[d] = c;
     }
@@ -1299,16 +1303,16 @@ __global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
         }
     }
     __syncthreads();
-    for (int s2 = warp; s2 < D * np; s2 += GNW) {
+    for (int s2 = warp; s2 < D * np; s2 += NW) {
         const int d = s2 / np, jj = s2 - d * np;
         const int64_t rec = h.drec[d];
         if (rec < 0) continue;
         const int op = a.prop[jj];
-        const int64_t* col = acc + (size_t)s2 * GNT;
+        const int64_t* col = acc + (size_t)s2 * NT;
         if (op == P_SUM) {   // exact: split halves of the per-thread int64 sums
             uint64_t lo = 0;
             int64_t hi = 0;
-            for (int t2 = lane; t2 < GNT; t2 += 32) { lo += (uint64_t)(uint32_t)col[t2]; hi += col[t2] >> 32; }
+            for (int t2 = lane; t2 < NT; t2 += 32) { lo += (uint64_t)(uint32_t)col[t2]; hi += col[t2] >> 32; }
             for (int o = 16; o > 0; o >>= 1) {
                 lo += __shfl_xor_sync(0xffffffffu, lo, o);
                 hi += __shfl_xor_sync(0xffffffffu, hi, o);
@@ -1316,7 +1320,7 @@ __global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
             if (lane == 0) { a.plo[jj][rec] = lo; a.phi[jj][rec] = hi; }
         } else {
             int64_t v = op == P_MIN ? INT64_MAX : INT64_MIN;
-            for (int t2 = lane; t2 < GNT; t2 += 32) v = op == P_MIN ? min(v, col[t2]) : max(v, col[t2]);
+            for (int t2 = lane; t2 < NT; t2 += 32) v = op == P_MIN ? min(v, col[t2]) : max(v, col[t2]);
             for (int o = 16; o > 0; o >>= 1) {
                 const int64_t y = __shfl_xor_sync(0xffffffffu, v, o);
                 v = op == P_MIN ? min(v, y) : max(v, y);
@@ -1324,7 +1328,7 @@ __global__ void __launch_bounds__(GNT, 1) gb_dense_kernel(Phase1Args a) {
             if (lane == 0) a.plo[jj][rec] = (uint64_t)v;
         }
     }
-    for (int d = tid; d < D; d += GNT) {
+    for (int d = tid; d < D; d += NT) {
         const int64_t rec = h.drec[d];
         if (rec >= 0) { a.pkey[rec] = a.dkeys[d]; a.pcount[rec] = h.dcnt[d]; }
     }
@@ -1759,7 +1763,7 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         DevBuf<uint64_t> dkeys;
         bool dense = false;
         size_t dense_smem = 0;
-        int dense_ns = 0;
+        int dense_ns = 0, dense_nt = GNT;
         int64_t dense_grid = 0;
         const char* dz = getenv("TQP_GROUPBY_DENSE");
         bool small_add = true;   // the dense bound argument needs |add| < 2^61
@@ -1790,19 +1794,40 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             int D = 0;
             read_back(ctx, &D, Dd.get(), 4);
             if (D >= 1 && D <= DMAX) {
-                const size_t accb = (size_t)D * PL->n_pairs * GNT * 8 + (size_t)D * GNT * 4;
+                // (threads per CTA, stages) with the most resident warps per SM; ties go to
+                // more stages per SM. Lane-private accumulators make occupancy smem-bound.
                 const size_t hdr = (sizeof(DenseHdr) + 15) & ~size_t(15);
-                int ns = 4;
-                while (ns >= 2 && (size_t)ns * a.stage_bytes + hdr + accb > 227 * 1024) ns--;
-                if (ns >= 2) {
-                    dense_ns = ns;
-                    dense_smem = (size_t)ns * a.stage_bytes + hdr + accb;
-                    set_smem(gb_dense_kernel, dense_smem);
-                    int occ = 1;
-                    TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_dense_kernel, GNT, dense_smem));
-                    dense_grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
+                int best_w = 0, best_st = 0;
+                for (int nt : {128, 256}) {
+                    const size_t stage = (size_t)a.stage_bytes * nt / GNT;
+                    const size_t accb = (size_t)D * PL->n_pairs * nt * 8 + (size_t)D * nt * 4;
+                    for (int ns = 1; ns <= 4; ns++) {
+                        const size_t sm = (size_t)ns * stage + hdr + accb;
+                        if (sm > 227 * 1024) continue;
+                        int occ = 0;
+                        if (nt == 128) {
+                            set_smem(gb_dense_kernel<128>, sm);
+                            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_dense_kernel<128>, nt, sm));
+                        } else {
+                            set_smem(gb_dense_kernel<256>, sm);
+                            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_dense_kernel<256>, nt, sm));
+                        }
+                        const int wps = occ * nt / 32, st = occ * ns;
+                        if (occ > 0 && (wps > best_w || (wps == best_w && st > best_st))) {
+                            best_w = wps;
+                            best_st = st;
+                            dense_nt = nt;
+                            dense_ns = ns;
+                            dense_smem = sm;
+                            dense_grid = (int64_t)ctx->num_sms * occ;
+                        }
+                    }
+                }
+                if (best_w > 0) {
+                    const int64_t tr = (int64_t)dense_nt * GPT;
+                    dense_grid = std::min<int64_t>(dense_grid, ceil_div(n, tr));
                     // rows per thread bound -> per-thread int64 sums of values <= 2^bits stay <= 2^62
-                    const int64_t rpt = ceil_div(tiles, dense_grid) * GPT;
+                    const int64_t rpt = ceil_div(ceil_div(n, tr), dense_grid) * GPT;
                     int lg = 0;
                     while ((int64_t(1) << lg) < rpt) lg++;
                     a.dense_bits = 62 - lg;
@@ -1837,9 +1862,20 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             a.P_counter = Pc.get();
             a.overflow = ovf.get();
             if (n > 0 && dense) {
-                a.n_stages = dense_ns;
+                // the stage layout scaled to tiles of dense_nt * GPT rows
+                Phase1Args ad = a;
+                const int64_t tr = (int64_t)dense_nt * GPT;
+                ad.n_stages = dense_ns;
+                ad.stage_bytes = (int)((int64_t)a.stage_bytes * dense_nt / GNT);
+                ad.n_tiles = ceil_div(n, tr);
+                for (int c = 0; c < a.n_ucols; c++) ad.uoff[c] = (int)((int64_t)a.uoff[c] * dense_nt / GNT);
+                for (int j = 0; j < PL->n_pairs && j < PCH; j++)
+                    for (int f = 0; f < pnf[j]; f++) ad.poff[j][f] = ad.uoff[a.pfc[j][f]];
                 tile_name = "tqp_groupby_dense";
-                launch(ctx, tile_name, gb_dense_kernel, dim3((unsigned)dense_grid), dim3(GNT), dense_smem, a);
+                if (dense_nt == 128)
+                    launch(ctx, tile_name, gb_dense_kernel<128>, dim3((unsigned)dense_grid), dim3(128), dense_smem, ad);
+                else
+                    launch(ctx, tile_name, gb_dense_kernel<256>, dim3((unsigned)dense_grid), dim3(256), dense_smem, ad);
             } else if (n > 0) {
                 tile_name = "tqp_groupby_tile";
                 // pipeline depth: light per-row work (no group keys) is bandwidth-bound and
