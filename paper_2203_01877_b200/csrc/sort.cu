@@ -211,7 +211,10 @@ __device__ __forceinline__ KT conv_key(typename InKey<IN, KT>::T v, bool desc) {
 template <typename KT, int IN, int IPT, int RB>
 struct ScatterWork {
     union {
-        uint32_t whist[NW][1 << RB];
+        struct {
+            uint32_t whist[NW][1 << RB];
+            uint32_t match[NW][1 << RB];   // per-warp digit -> lane bitmask (peer detection)
+        };
         struct {
             KT keys[NT * IPT];
             uint32_t perm[NT * IPT];
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         const int64_t base = tile * TILE;
         KT key[IPT];
         uint32_t pm[IPT], rk[IPT];
-        for (int d = lane; d < BINS; d += 32) s.u.whist[warp][d] = 0;
+        for (int d = lane; d < BINS; d += 32) { s.u.whist[warp][d] = 0; s.u.match[warp][d] = 0; }
         uint32_t gs[BPT];   // this tile's global digit starts: loaded now, used after ranking
 #pragma unroll
         for (int j = 0; j < BPT; j++) {
@@ -318,15 +321,19 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         for (int i = 0; i < IPT; i++) {
             const bool valid = base + warp * 32 * IPT + i * 32 + lane < a.n;
             const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
-            unsigned peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-            for (int b = 0; b < RB; b++) {   // peers = lanes with the same digit: one ballot per digit bit
-                const unsigned bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-                peers &= ((d >> b) & 1u) ? bb : ~bb;
-            }
+            // peers = lanes of this warp with the same digit: every lane ORs its bit into
+            // the digit's match word, reads the word back, and the leader clears it
+            uint32_t* mw = &s.u.match[warp][d];
+            if (valid) atomicOr(mw, 1u << lane);
+            __syncwarp();
+            const unsigned peers = valid ? *reinterpret_cast<volatile uint32_t*>(mw) : 0u;
+            __syncwarp();
             const uint32_t leader = 31 - __clz(peers);
             uint32_t old = 0;
-            if (valid && lane == leader) old = atomicAdd(&s.u.whist[warp][d], (uint32_t)__popc(peers));
+            if (valid && lane == leader) {
+                old = atomicAdd(&s.u.whist[warp][d], (uint32_t)__popc(peers));
+                *mw = 0;
+            }
             rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
         }
 #pragma unroll
