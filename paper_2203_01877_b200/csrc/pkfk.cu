@@ -101,7 +101,24 @@ __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint3
         const uint32_t low = (uint32_t)rel & a.lowmask;
         const uint32_t target = low << a.pbits;
         const uint32_t end = hi;
-        while (lo < hi) {   // lower_bound of the residual inside the bucket
+        const uint32_t s0 = lo & ~7u;   // the bucket's records from one aligned 64-byte fetch
+        if (hi <= s0 + 16u) {
+            const uint4* p4 = reinterpret_cast<const uint4*>(a.rec + s0);
+            const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1), q2 = __ldg(p4 + 2), q3 = __ldg(p4 + 3);
+            const uint32_t r16[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                                      q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+            bool hit = false;
+#pragma unroll
+            for (int j = 0; j < 16; j++) {   // residuals are distinct: at most one match
+                const uint32_t pos = s0 + (uint32_t)j;
+                if (pos >= lo && pos < end && (r16[j] >> a.pbits) == low) {
+                    left = r16[j] & ((1u << a.pbits) - 1u);
+                    hit = true;
+                }
+            }
+            return hit;
+        }
+        while (lo < hi) {   // long bucket: lower_bound of the residual
             uint32_t mid = (lo + hi) >> 1;
             if (__ldg(a.rec + mid) < target) lo = mid + 1; else hi = mid;
         }
@@ -194,8 +211,10 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
 
 struct Built {
     SortOut so;
-    DevBuf<uint32_t> T;
-    DevBuf<uint32_t> rec;
+    DevBuf<uint32_t> TR;      // bracket table T, then (packed) the records, one allocation
+    uint32_t* T = nullptr;
+    uint32_t* rec = nullptr;
+    size_t tr_bytes = 0;
     DevBuf<int> dup;
     uint64_t base = 0, hi_bits = 0;
     int shift = 0, vbits = 0, pbits = 0;
@@ -240,7 +259,11 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
     const int64_t nbk = int64_t(1) << Bbits;
     DevBuf<uint32_t> H(ctx, nbk + 1);
     H.zero();
-    B.T.alloc(ctx, nbk + 1);
+    const int64_t toff = (nbk + 1 + 15) & ~int64_t(15);   // records start 64-byte aligned
+    B.TR.alloc(ctx, toff + (B.packed ? nb + 16 : 0));     // +16: the probe reads whole aligned 64-byte groups
+    B.T = B.TR.get();
+    B.rec = B.packed ? B.TR.get() + toff : nullptr;
+    B.tr_bytes = (size_t)(toff + (B.packed ? nb + 16 : 0)) * 4;
     const int g = (int)std::min<int64_t>(ceil_div(nb, 256), (int64_t)ctx->num_sms * 8);
     if (B.so.k32)
         launch(ctx, "tqp_pkfk_bucket_ends", bucket_ends_kernel<uint32_t>, dim3(g), dim3(256), 0, B.so.keys32.get(),
@@ -249,16 +272,15 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
         launch(ctx, "tqp_pkfk_bucket_ends", bucket_ends_kernel<uint64_t>, dim3(g), dim3(256), 0, B.so.keys64.get(),
                nb, (uint64_t)B.base, B.shift, H.get(), B.dup.get());
     ctx->add_bytes("tqp_pkfk_bucket_ends", (double)nb * (B.so.k32 ? 4 : 8) + 4.0 * (double)std::min<int64_t>(nb, nbk));
-    scan_max_u32_exclusive(ctx, H.get(), B.T.get(), nbk + 1);
+    scan_max_u32_exclusive(ctx, H.get(), B.T, nbk + 1);
     if (B.packed) {
-        B.rec.alloc(ctx, nb);
         const uint32_t lowmask = B.shift >= 32 ? 0xFFFFFFFFu : ((1u << B.shift) - 1u);
         if (B.so.k32)
             launch(ctx, "tqp_pkfk_records", pack_records_kernel<uint32_t>, dim3(g), dim3(256), 0, B.so.keys32.get(),
-                   B.so.perm32.get(), nb, (uint32_t)B.base, lowmask, B.pbits, B.rec.get());
+                   B.so.perm32.get(), nb, (uint32_t)B.base, lowmask, B.pbits, B.rec);
         else
             launch(ctx, "tqp_pkfk_records", pack_records_kernel<uint64_t>, dim3(g), dim3(256), 0, B.so.keys64.get(),
-                   B.so.perm32.get(), nb, (uint64_t)B.base, lowmask, B.pbits, B.rec.get());
+                   B.so.perm32.get(), nb, (uint64_t)B.base, lowmask, B.pbits, B.rec);
         ctx->add_bytes("tqp_pkfk_records", (double)nb * ((B.so.k32 ? 4 : 8) + 8));
         B.so.keys32.release();
         B.so.keys64.release();
@@ -282,8 +304,8 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         a.n_probe = np;
         a.bkeys = B.so.k32 ? (const void*)B.so.keys32.get() : (const void*)B.so.keys64.get();
         a.bperm = B.so.perm32.get();
-        a.T = B.T.get();
-        a.rec = B.rec.get();
+        a.T = B.T;
+        a.rec = B.rec;
         a.pbits = B.pbits;
         a.lowmask = B.shift >= 32 ? 0xFFFFFFFFu : ((1u << B.shift) - 1u);
         a.base = B.base;
