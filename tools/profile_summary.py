@@ -5,7 +5,8 @@ import csv, io, json, os, subprocess, sys, collections
 
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
 G = "gpurun_out"
-NAME = [("gb_phase1", "tqp_groupby_tile"), ("scatter_tma", "tqp_sort_scatter"), ("scatter_kernel", "tqp_sort_scatter"),
+NAME = [("gb_phase1", "tqp_groupby_tile"), ("gb_dense_kernel", "tqp_groupby_dense"), ("gb_presence", "tqp_groupby_presence"),
+        ("gb_dense_ids", "tqp_groupby_dense_ids"), ("key_range", "tqp_groupby_keyrange"), ("scatter_tma", "tqp_sort_scatter"), ("scatter_kernel", "tqp_sort_scatter"),
         ("probe_kernel", "tqp_pkfk_probe"), ("expand_kernel", "tqp_smj_expand"), ("filter_kernel", "tqp_filter"),
         ("tile_hist", "tqp_sort_tile_hist"), ("scan_tiles", "tqp_sort_scan"), ("scan_chunks", "tqp_sort_scan"),
         ("rle_kernel", "tqp_smj_rle"), ("intersect_kernel", "tqp_smj_intersect"), ("cum_kernel", "tqp_smj_cumsum"),
