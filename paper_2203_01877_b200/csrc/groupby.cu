@@ -117,22 +117,21 @@ __global__ void key_range_kernel(KRArgs a, unsigned long long* kr) {   // kr[k] 
         const int dt = a.kdt[k];
         const int per = dt == TQP_U8 ? 16 : dt == TQP_I32 ? 4 : 2;   // elements per 16-byte load
         const int64_t nv = ((uintptr_t)a.kcol[k] % 16 == 0) ? a.n / per : 0;
+        uint32_t mn4 = 0xFFFFFFFFu, mx4 = 0;   // u8: per-byte-lane min / max; i32: 32-bit min / max
         for (int64_t v = gt; v < nv; v += gs) {   // vectorised body: 16 bytes per load, streamed
             const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + v);
             const uint32_t wd[4] = {q.x, q.y, q.z, q.w};
             if (dt == TQP_U8) {
 #pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const unsigned long long x = (wd[j >> 2] >> (8 * (j & 3))) & 0xFFu;
-                    mn = min(mn, x);
-                    mx = max(mx, x);
+                for (int j = 0; j < 4; j++) {
+                    mn4 = __vminu4(mn4, wd[j]);
+                    mx4 = __vmaxu4(mx4, wd[j]);
                 }
             } else if (dt == TQP_I32) {
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
-                    const unsigned long long x = wd[j] ^ 0x80000000u;
-                    mn = min(mn, x);
-                    mx = max(mx, x);
+                    mn4 = min(mn4, wd[j] ^ 0x80000000u);
+                    mx4 = max(mx4, wd[j] ^ 0x80000000u);
                 }
             } else {
 #pragma unroll
@@ -142,6 +141,16 @@ __global__ void key_range_kernel(KRArgs a, unsigned long long* kr) {   // kr[k] 
                     mx = max(mx, x);
                 }
             }
+        }
+        if (dt == TQP_U8) {
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                mn = min(mn, (unsigned long long)((mn4 >> (8 * j)) & 0xFFu));
+                mx = max(mx, (unsigned long long)((mx4 >> (8 * j)) & 0xFFu));
+            }
+        } else if (dt == TQP_I32 && nv > gt) {
+            mn = min(mn, (unsigned long long)mn4);
+            mx = max(mx, (unsigned long long)mx4);
         }
         for (int64_t i = nv * per + gt; i < a.n; i += gs) {   // tail (or unaligned column)
             const unsigned long long x = key_part(load_as_i64(a.kcol[k], dt, i), dt);
@@ -1841,8 +1850,8 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
 
         // ---- phase 1 (retried once with full capacity if the partial estimate is exceeded)
         Partials pr;
-        DevBuf<unsigned long long> Pc(ctx, 1);
-        DevBuf<int> ovf(ctx, 1);
+        DevBuf<unsigned long long> Pc(ctx, 2);   // [0] partial counter, [1] overflow flags: one readback
+        int* ovf = reinterpret_cast<int*>(Pc.get() + 1);
         int64_t cap = std::min<int64_t>(std::max<int64_t>(n, 1), std::max<int64_t>(tiles * 64, 1 << 16));
         const char* tile_name = "tqp_groupby_tile";
         for (int attempt = 0; attempt < 3; attempt++) {
@@ -1858,9 +1867,8 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             a.pcount = pr.pcount.get();
             a.cap = cap;
             Pc.zero();
-            ovf.zero();
             a.P_counter = Pc.get();
-            a.overflow = ovf.get();
+            a.overflow = ovf;
             if (n > 0 && dense) {
                 // the stage layout scaled to tiles of dense_nt * GPT rows
                 Phase1Args ad = a;
@@ -1890,16 +1898,15 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
                 const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
                 launch(ctx, "tqp_groupby_tile", gb_phase1_kernel, dim3((unsigned)grid), dim3(GNT), smem, a);
             }
-            int64_t h[2] = {0, 0};
-            read_back(ctx, &h[0], Pc.get(), 8);
-            int o = 0;
-            read_back(ctx, &o, ovf.get(), 4);
+            unsigned long long h[2] = {0, 0};
+            read_back(ctx, h, Pc.get(), 16);
+            const int o = (int)h[1];
             if (o & 4) {   // dense path could not prove a tile exact: general path
                 dense = false;
                 continue;
             }
             if (o & 1) fail(TQP_ERR_OVERFLOW, "groupby: int64 overflow in an aggregate expression");
-            pr.P = h[0];
+            pr.P = (int64_t)h[0];
             if (!(o & 2)) break;
             cap = std::max<int64_t>(n, 1);   // more distinct keys per tile than estimated: full capacity
         }

@@ -69,47 +69,90 @@ __device__ __forceinline__ void compact_scan(CompactTile& s, const unsigned* bal
     __syncthreads();
 }
 
-// Run-length encoding of sorted keys: heads -> (unique key, run start).
+// Run-length encoding of sorted keys: heads -> (unique key, run start). Each thread
+// owns JIPT consecutive keys (16-byte loads); heads are counted per thread, ranked by a
+// warp scan + block scan + decoupled look-back, staged in shared memory in key order
+// and written coalesced. Keys are read as KT (the sort's internal 32- or 64-bit key)
+// and written as KO = hi | key (the common domain of both join sides).
 // Writes ustart[U] = n and *U_out (last tile).
-__global__ void __launch_bounds__(JNT) rle_kernel(const uint64_t* __restrict__ u, int64_t n, uint64_t* ukey,
-                                                  int64_t* ustart, int64_t* U_out, uint64_t* status,
+template <typename KT, typename KO>
+__global__ void __launch_bounds__(JNT) rle_kernel(const KT* __restrict__ u, uint64_t hi, int64_t n, KO* ukey,
+                                                  uint32_t* ustart, int64_t* U_out, uint64_t* status,
                                                   unsigned long long* counter, int64_t n_tiles) {
     __shared__ int64_t s_tile;
-    __shared__ CompactTile s;
+    __shared__ uint32_t s_woff[JNW];
+    __shared__ uint64_t s_excl;
+    __shared__ uint32_t s_tot;
+    __shared__ KO s_key[JTILE];
+    __shared__ uint32_t s_pos[JTILE];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tile = take_tile(counter, &s_tile);
     const int64_t base = tile * JTILE;
-    unsigned bal[JIPT];
-    uint64_t key[JIPT];
+    const int64_t r0 = base + (int64_t)tid * JIPT;
+    KT k[JIPT];
+    if (base + JTILE <= n && (uintptr_t)u % 16 == 0) {
+        constexpr int PER = 16 / sizeof(KT);
 #pragma unroll
-    for (int i = 0; i < JIPT; i++) {
-        const int64_t p = base + i * JNT + tid;
-        bool head = false;
-        if (p < n) {
-            key[i] = u[p];
-            head = (p == 0) || (u[p - 1] != key[i]);
+        for (int q = 0; q < JIPT / PER; q++) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(u + r0) + q);
+            memcpy(&k[q * PER], &v, 16);
         }
-        bal[i] = __ballot_sync(0xffffffffu, head);
+    } else {
+#pragma unroll
+        for (int j = 0; j < JIPT; j++) k[j] = r0 + j < n ? u[r0 + j] : KT(0);
     }
-    compact_scan(s, bal, tile, status);
-    const int64_t excl = (int64_t)s.s_excl;
-    const unsigned lt = lanemask_lt();
+    // the key before this thread's first: the previous lane's last, or memory for lane 0
+    KT pk = __shfl_up_sync(0xffffffffu, k[JIPT - 1], 1);
+    if (lane == 0 && r0 > 0 && r0 <= n) pk = u[r0 - 1];
+    bool head[JIPT];
+    uint32_t cnt = 0;
 #pragma unroll
-    for (int i = 0; i < JIPT; i++) {
-        if (bal[i] & (1u << lane)) {
-            const int64_t j = excl + s.s_cnt[i * JNW + warp] + __popc(bal[i] & lt);
-            ukey[j] = key[i];
-            ustart[j] = base + i * JNT + tid;
+    for (int j = 0; j < JIPT; j++) {
+        head[j] = r0 + j < n && (j == 0 ? (r0 == 0 || k[0] != pk) : k[j] != k[j - 1]);
+        cnt += head[j];
+    }
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_woff[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t wt = lane < JNW ? s_woff[lane] : 0;
+        uint32_t y = wt;
+#pragma unroll
+        for (int o = 1; o < JNW; o <<= 1) {
+            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += z;
         }
+        const uint32_t tot = __shfl_sync(0xffffffffu, y, JNW - 1);
+        const uint64_t e = lookback_warp(status, tile, tot, OpAdd(), 0ull);
+        if (lane < JNW) s_woff[lane] = y - wt;
+        if (lane == 0) { s_excl = e; s_tot = tot; }
+    }
+    __syncthreads();
+    uint32_t lp = s_woff[warp] + x - cnt;
+#pragma unroll
+    for (int j = 0; j < JIPT; j++)
+        if (head[j]) { s_key[lp] = (KO)(hi | (uint64_t)k[j]); s_pos[lp] = (uint32_t)(r0 + j); lp++; }
+    __syncthreads();
+    const int64_t excl = (int64_t)s_excl;
+    const uint32_t tot = s_tot;
+    for (uint32_t q = tid; q < tot; q += JNT) {
+        ukey[excl + q] = s_key[q];
+        ustart[excl + q] = s_pos[q];
     }
     if (tile == n_tiles - 1 && tid == 0) {
-        const int64_t U = excl + s.s_tot;
+        const int64_t U = excl + tot;
         *U_out = U;
-        ustart[U] = n;
+        ustart[U] = (uint32_t)n;
     }
 }
 
-__device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo, int64_t hi, uint64_t k) {
+template <typename KO>
+__device__ __forceinline__ int64_t lower_bound_k(const KO* a, int64_t lo, int64_t hi, KO k) {
     while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
         if (a[mid] < k) lo = mid + 1; else hi = mid;
@@ -122,22 +165,23 @@ __device__ __forceinline__ int64_t lower_bound_u64(const uint64_t* a, int64_t lo
 // of U_l); tiles past U_l exit.
 constexpr int ICAP = 4096;   // right unique keys staged in shared memory per tile
 
-__global__ void __launch_bounds__(JNT) intersect_kernel(const uint64_t* __restrict__ ukl, const int64_t* __restrict__ usl,
-                                                        const int64_t* U_l_p, const uint64_t* __restrict__ ukr,
-                                                        const int64_t* __restrict__ usr, const int64_t* U_r_p,
+template <typename KO>
+__global__ void __launch_bounds__(JNT) intersect_kernel(const KO* __restrict__ ukl, const uint32_t* __restrict__ usl,
+                                                        const int64_t* U_l_p, const KO* __restrict__ ukr,
+                                                        const uint32_t* __restrict__ usr, const int64_t* U_r_p,
                                                         uint32_t* mL, uint32_t* mR, uint32_t* msL, uint32_t* msR,
                                                         int64_t* K_out, uint64_t* status, unsigned long long* counter) {
     __shared__ int64_t s_tile, s_rlo, s_rhi;
     __shared__ CompactTile s;
-    __shared__ uint64_t s_r[ICAP];
+    __shared__ KO s_r[ICAP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t tile = take_tile(counter, &s_tile);
     const int64_t U_l = *U_l_p, U_r = *U_r_p;
     const int64_t base = tile * JTILE;
     if (base >= U_l) return;
     const int64_t last = min(base + JTILE, U_l) - 1;
-    if (tid == 0) s_rlo = lower_bound_u64(ukr, 0, U_r, ukl[base]);
-    if (tid == 32) s_rhi = lower_bound_u64(ukr, 0, U_r, ukl[last]) + 1;
+    if (tid == 0) s_rlo = lower_bound_k(ukr, 0, U_r, ukl[base]);
+    if (tid == 32) s_rhi = lower_bound_k(ukr, 0, U_r, ukl[last]) + 1;
     __syncthreads();
     const int64_t rlo = s_rlo, rhi = min(s_rhi, U_r);
     // the right unique keys this tile can match: staged in shared memory if they fit
@@ -153,7 +197,7 @@ __global__ void __launch_bounds__(JNT) intersect_kernel(const uint64_t* __restri
         const int64_t j = base + i * JNT + tid;
         bool hit = false;
         if (j < U_l) {
-            const uint64_t k = ukl[j];
+            const KO k = ukl[j];
             int64_t p;
             bool eq;
             if (staged) {
@@ -165,15 +209,15 @@ __global__ void __launch_bounds__(JNT) intersect_kernel(const uint64_t* __restri
                 eq = lo < rhi - rlo && s_r[lo] == k;
                 p = lo + rlo;
             } else {
-                p = lower_bound_u64(ukr, rlo, rhi, k);
+                p = lower_bound_k(ukr, rlo, rhi, k);
                 eq = p < rhi && ukr[p] == k;
             }
             if (eq) {
                 hit = true;
-                sL[i] = (uint32_t)usl[j];
-                L[i] = (uint32_t)(usl[j + 1] - usl[j]);
-                sR[i] = (uint32_t)usr[p];
-                R[i] = (uint32_t)(usr[p + 1] - usr[p]);
+                sL[i] = usl[j];
+                L[i] = usl[j + 1] - usl[j];
+                sR[i] = usr[p];
+                R[i] = usr[p + 1] - usr[p];
             }
         }
         bal[i] = __ballot_sync(0xffffffffu, hit);
@@ -298,16 +342,8 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
     }
 }
 
-void sort_side(tqp_ctx* ctx, const tqp_col& c, int64_t n, DevBuf<uint64_t>& sorted_u, DevBuf<uint32_t>& perm) {
-    SortOut so;
-    so.want_perm32 = true;
-    sorted_u.alloc(ctx, n);
-    so.sorted_u = sorted_u.get();
-    radix_sort(ctx, c.data, c.dtype, n, false, so);
-    perm = std::move(so.perm32);
-}
-
-void rle(tqp_ctx* ctx, const uint64_t* u, int64_t n, DevBuf<uint64_t>& ukey, DevBuf<int64_t>& ustart,
+template <typename KT, typename KO>
+void rle(tqp_ctx* ctx, const KT* u, uint64_t hi, int64_t n, DevBuf<KO>& ukey, DevBuf<uint32_t>& ustart,
          int64_t* U_dev) {
     ukey.alloc(ctx, n);
     ustart.alloc(ctx, n + 1);
@@ -316,9 +352,35 @@ void rle(tqp_ctx* ctx, const uint64_t* u, int64_t n, DevBuf<uint64_t>& ukey, Dev
     DevBuf<unsigned long long> counter(ctx, 1);
     status.zero();
     counter.zero();
-    ctx->add_bytes("tqp_smj_rle", 8.0 * (double)n);
-    launch(ctx, "tqp_smj_rle", rle_kernel, dim3((unsigned)tiles), dim3(JNT), 0, u, n, ukey.get(), ustart.get(), U_dev,
-           status.get(), counter.get(), tiles);
+    launch(ctx, "tqp_smj_rle", rle_kernel<KT, KO>, dim3((unsigned)tiles), dim3(JNT), 0, u, hi, n, ukey.get(),
+           ustart.get(), U_dev, status.get(), counter.get(), tiles);
+}
+
+// Both sides' RLE in the common key domain KO, then the intersection of the unique
+// keys.
+template <typename KO>
+void rle_intersect(tqp_ctx* ctx, tqp_smj_plan* P, SortOut& sl, SortOut& sr, int64_t* scal) {
+    const int64_t nl = P->n_left, nr = P->n_right;
+    DevBuf<KO> ukl, ukr;
+    DevBuf<uint32_t> usl, usr;
+    auto side = [&](SortOut& so, int64_t n, DevBuf<KO>& uk, DevBuf<uint32_t>& us, int64_t* U) {
+        const uint64_t hi = (sizeof(KO) == 8 && so.k32) ? (so.and_bits & 0xFFFFFFFF00000000ull) : 0;
+        if (so.k32) rle<uint32_t, KO>(ctx, so.keys32.get(), hi, n, uk, us, U);
+        else rle<uint64_t, KO>(ctx, so.keys64.get(), 0, n, uk, us, U);
+        ctx->add_bytes("tqp_smj_rle", (double)n * (so.k32 ? 4 : 8));
+        so.keys32.release();
+        so.keys64.release();
+    };
+    side(sl, nl, ukl, usl, scal + 0);
+    side(sr, nr, ukr, usr, scal + 1);
+    const int64_t tiles = ceil_div(nl, JTILE);
+    DevBuf<uint64_t> status(ctx, tiles);
+    DevBuf<unsigned long long> counter(ctx, 1);
+    status.zero();
+    counter.zero();
+    launch(ctx, "tqp_smj_intersect", intersect_kernel<KO>, dim3((unsigned)tiles), dim3(JNT), 0, ukl.get(), usl.get(),
+           scal + 0, ukr.get(), usr.get(), scal + 1, P->mL.get(), P->mR.get(), P->msL.get(), P->msR.get(), scal + 2,
+           status.get(), counter.get());
 }
 }  // namespace
 
@@ -333,35 +395,28 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
             *out_size_host = 0;
             return P;
         }
-        DevBuf<uint64_t> ul, ur;
-        sort_side(ctx, left, nl, ul, P->perm_l);
-        sort_side(ctx, right, nr, ur, P->perm_r);
+        // sort both sides (l.2-3); keep the internal sorted keys and u32 permutations
+        SortOut sl, sr;
+        sl.want_internal = sr.want_internal = true;
+        radix_sort(ctx, left.data, left.dtype, nl, false, sl);
+        radix_sort(ctx, right.data, right.dtype, nr, false, sr);
+        P->perm_l = std::move(sl.perm32);
+        P->perm_r = std::move(sr.perm32);
         DevBuf<int64_t> scal(ctx, 4);   // U_l, U_r, K, out_size
         DevBuf<int> ovf(ctx, 1);
         scal.zero();
         ovf.zero();
-        DevBuf<uint64_t> ukl, ukr;
-        DevBuf<int64_t> usl, usr;
-        rle(ctx, ul.get(), nl, ukl, usl, scal.get() + 0);
-        rle(ctx, ur.get(), nr, ukr, usr, scal.get() + 1);
-        ul.release();
-        ur.release();
         const int64_t cap = std::min(nl, nr);
         P->mL.alloc(ctx, cap);
         P->mR.alloc(ctx, cap);
         P->msL.alloc(ctx, cap);
         P->msR.alloc(ctx, cap);
         P->mcum.alloc(ctx, cap);
-        {
-            const int64_t tiles = ceil_div(nl, JTILE);
-            DevBuf<uint64_t> status(ctx, tiles);
-            DevBuf<unsigned long long> counter(ctx, 1);
-            status.zero();
-            counter.zero();
-            launch(ctx, "tqp_smj_intersect", intersect_kernel, dim3((unsigned)tiles), dim3(JNT), 0, ukl.get(), usl.get(),
-                   scal.get() + 0, ukr.get(), usr.get(), scal.get() + 1, P->mL.get(), P->mR.get(), P->msL.get(),
-                   P->msR.get(), scal.get() + 2, status.get(), counter.get());
-        }
+        // 32-bit unique keys when both sides' keys differ only in one common low word
+        const bool k32 = sl.k32 && sr.k32 && (sl.and_bits >> 32) == (sr.and_bits >> 32);
+        const double kb = k32 ? 4.0 : 8.0;
+        if (k32) rle_intersect<uint32_t>(ctx, P, sl, sr, scal.get());
+        else rle_intersect<uint64_t>(ctx, P, sl, sr, scal.get());
         {
             const int64_t tiles = ceil_div(cap, JTILE);
             DevBuf<uint64_t> status(ctx, tiles);
@@ -376,7 +431,7 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         read_back(ctx, h, scal.get(), 32);
         read_back(ctx, &o, ovf.get(), 4);
         if (o) fail(TQP_ERR_OVERFLOW, "smj: output size exceeds 2^62");
-        ctx->add_bytes("tqp_smj_intersect", 16.0 * (double)std::min(nl, nr) + 32.0 * (double)h[2]);
+        ctx->add_bytes("tqp_smj_intersect", (kb + 4.0) * (double)std::min(nl, nr) + 16.0 * (double)h[2]);
         ctx->add_bytes("tqp_smj_cumsum", 24.0 * (double)h[2]);
         P->K = h[2];
         P->out_size = h[2] > 0 ? h[3] : 0;

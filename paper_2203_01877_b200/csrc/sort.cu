@@ -142,16 +142,13 @@ __global__ void __launch_bounds__(1 << RB) scan_chunks_kernel(uint32_t* __restri
     constexpr int BINS = 1 << RB, NWB = BINS / 32;
     __shared__ uint32_t s_w[NWB];
     const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
-    uint32_t run = 0;
+    uint32_t run = 0;   // pass 1: digit total over all chunks (32 loads in flight)
     for (int64_t b = 0; b < n_chunks; b += 32) {
         uint32_t v[32];
 #pragma unroll
-        for (int i = 0; i < 32; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * BINS + d] : 0u;   // 32 loads in flight
+        for (int i = 0; i < 32; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * BINS + d] : 0u;
 #pragma unroll
-        for (int i = 0; i < 32; i++) {
-            if (b + i < n_chunks) ct[(b + i) * BINS + d] = run;
-            run += v[i];
-        }
+        for (int i = 0; i < 32; i++) run += v[i];
     }
     // exclusive scan of the digit totals across the block (global bin bases)
     uint32_t x = run;
@@ -163,7 +160,17 @@ __global__ void __launch_bounds__(1 << RB) scan_chunks_kernel(uint32_t* __restri
     __syncthreads();
     uint32_t base = x - run;
     for (int w = 0; w < warp; w++) base += s_w[w];
-    for (int64_t c = 0; c < n_chunks; c++) ct[c * BINS + d] += base;
+    // pass 2: ct[c][d] <- bin base + exclusive prefix over earlier chunks
+    for (int64_t b = 0; b < n_chunks; b += 32) {
+        uint32_t v[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * BINS + d] : 0u;
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            if (b + i < n_chunks) ct[(b + i) * BINS + d] = base;
+            base += v[i];
+        }
+    }
 }
 
 struct ScatterArgs {

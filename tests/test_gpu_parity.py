@@ -215,6 +215,32 @@ def test_smj_dtypes_and_extremes(T):
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
 
 
+@pytest.mark.parametrize("case", ["same_hi", "diff_hi", "wide_left", "wide_right", "negative", "const_sides"])
+def test_smj_key_domains(T, case):
+    """The join compares sorted keys in a common domain: 32-bit unique keys when both
+    sides vary only in the same low word, 64-bit otherwise (mixed widths, different high
+    words, one-key sides)."""
+    rng = np.random.default_rng(len(case))
+    n = 30_011
+    base = {"same_hi": (5 << 32, 5 << 32), "diff_hi": (5 << 32, 6 << 32), "wide_left": (0, 0),
+            "wide_right": (0, 0), "negative": (-(1 << 33), -(1 << 33)), "const_sides": (7, 7)}[case]
+    left = base[0] + rng.integers(0, 5000, n)
+    right = base[1] + rng.integers(0, 5000, n)
+    if case == "wide_left":
+        left[::97] = rng.integers(1 << 40, 1 << 41, left[::97].size)
+    if case == "wide_right":
+        right[::89] = -rng.integers(1 << 40, 1 << 41, right[::89].size)
+    if case == "diff_hi":   # some keys shared across the two high words
+        right[::50] = left[::50][: right[::50].size]
+    if case == "const_sides":   # one distinct key on the left (trivial sort), ~45K pairs
+        left = np.full(300, 7, np.int64)
+        right = right[:301].copy()
+        right[::2] = 7
+    lo, ro = T.smj_join(cu(left), cu(right))
+    olo, oro = oracle.smj_join(left, right)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
 def test_smj_zipf_uniform_parity(T):
     """Config-4 shape (Zipf(s=1) left x uniform right) at 400K x 400K."""
     left = zipf_keys(400_000, 400_000, seed=42, device="cuda")
