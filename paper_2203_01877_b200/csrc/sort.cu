@@ -112,27 +112,37 @@ __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int6
     }
 }
 
-// (2) per chunk of CHUNK tiles: th[t][d] <- exclusive prefix within the chunk; ct[c][d] = chunk total
+// (2) per chunk of CHUNK tiles: th[t][d] <- exclusive prefix within the chunk; ct[c][d] = chunk total.
+// Grid (chunk, digit slice of SNT): the CTA stages its [CHUNK tiles x SNT digits] block
+// into shared memory with 16-byte cp.async copies (all in flight at once), then one
+// thread per digit scans its column and writes the prefixes back (coalesced rows).
+constexpr int SNT = 64;
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gmem_src) : "memory");
+}
 template <int RB>
-__global__ void __launch_bounds__(NT) scan_tiles_kernel(uint32_t* __restrict__ th, int64_t n_tiles,
-                                                        uint32_t* __restrict__ ct) {
+__global__ void __launch_bounds__(SNT) scan_tiles_kernel(uint32_t* __restrict__ th, int64_t n_tiles,
+                                                         uint32_t* __restrict__ ct) {
     constexpr int BINS = 1 << RB;
+    constexpr int V = SNT / 4;   // 16-byte vectors per tile row of the slice
+    __shared__ __align__(16) uint32_t blk[CHUNK][SNT];
     const int64_t t0 = (int64_t)blockIdx.x * CHUNK;
     const int cnt = (int)min((int64_t)CHUNK, n_tiles - t0);
-    for (int d = threadIdx.x; d < BINS; d += NT) {
-        uint32_t run = 0;
-        for (int b = 0; b < cnt; b += 32) {
-            uint32_t v[32];
-#pragma unroll
-            for (int i = 0; i < 32; i++) v[i] = (b + i < cnt) ? th[(t0 + b + i) * BINS + d] : 0u;   // 32 loads in flight
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                if (b + i < cnt) th[(t0 + b + i) * BINS + d] = run;
-                run += v[i];
-            }
-        }
-        ct[(int64_t)blockIdx.x * BINS + d] = run;
+    const int d0 = blockIdx.y * SNT;
+    for (int q = threadIdx.x; q < cnt * V; q += SNT) {
+        const int r = q / V, c = q - r * V;
+        cp_async16(&blk[r][c * 4], th + (t0 + r) * BINS + d0 + c * 4);
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    const int d = threadIdx.x;
+    uint32_t run = 0;
+    for (int r = 0; r < cnt; r++) {
+        const uint32_t v = blk[r][d];
+        th[(t0 + r) * BINS + d0 + d] = run;
+        run += v;
+    }
+    ct[(int64_t)blockIdx.x * BINS + d0 + d] = run;
 }
 
 // (3) one CTA of BINS threads (one digit each): ct[c][d] <- global start of digit d
@@ -165,6 +175,7 @@ __global__ void __launch_bounds__(1 << RB) scan_chunks_kernel(uint32_t* __restri
         uint32_t v[32];
 #pragma unroll
         for (int i = 0; i < 32; i++) v[i] = (b + i < n_chunks) ? ct[(b + i) * BINS + d] : 0u;
+        asm volatile("" ::: "memory");
 #pragma unroll
         for (int i = 0; i < 32; i++) {
             if (b + i < n_chunks) ct[(b + i) * BINS + d] = base;
@@ -495,8 +506,8 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
                    dim3((unsigned)tiles), dim3(NT), 0, in, n, shifts[p], desc, th.get());
         });
         ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
-        launch(ctx, "tqp_sort_scan", scan_tiles_kernel<RB>, dim3((unsigned)chunks), dim3(NT), 0, th.get(), tiles,
-               ct.get());
+        launch(ctx, "tqp_sort_scan", scan_tiles_kernel<RB>, dim3((unsigned)chunks, BINS / SNT), dim3(SNT), 0, th.get(),
+               tiles, ct.get());
         launch(ctx, "tqp_sort_scan", scan_chunks_kernel<RB>, dim3(1), dim3(BINS), 0, ct.get(), chunks);
         ctx->add_bytes("tqp_sort_scan", 8.0 * BINS * (double)tiles + 12.0 * BINS * (double)chunks);
         ScatterArgs a{};
