@@ -24,6 +24,7 @@ struct tqp_smj_plan {
     tqp::DevBuf<uint32_t> perm_l, perm_r;
     tqp::DevBuf<uint32_t> mL, mR, msL, msR;   // per common key: counts and run starts (< 2^30)
     tqp::DevBuf<int64_t> mcum;                 // cumHistMul (inclusive)
+    tqp::DevBuf<uint32_t> tb;                  // per output tile of ETILE: bucket of its first output (+ sentinel)
 };
 
 namespace tqp {
@@ -288,33 +289,54 @@ constexpr int ENT = 256;
 constexpr int EIPT = 8;
 constexpr int ETILE = ENT * EIPT;
 
-__device__ __forceinline__ int64_t upper_bound_i64(const int64_t* a, int64_t lo, int64_t hi, int64_t x) {
-    while (lo < hi) {
-        int64_t mid = (lo + hi) >> 1;
-        if (a[mid] <= x) lo = mid + 1; else hi = mid;
+
+// tb[c] = bucket (common key) containing output c * ETILE, for every output tile; the
+// sentinel tb[ceil(out / ETILE)] = K - 1. One thread per key writes the tiles whose
+// first output falls inside the key's output range.
+__global__ void tile_bucket_kernel(const int64_t* __restrict__ mcum, const uint32_t* __restrict__ mL,
+                                   const uint32_t* __restrict__ mR, int64_t K, uint32_t* tb, int64_t n_tb) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < K; b += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t end = mcum[b], start = end - (int64_t)mL[b] * (int64_t)mR[b];
+        for (int64_t c = (start + ETILE - 1) / ETILE; c * ETILE < end; c++) tb[c] = (uint32_t)b;
+        if (b == K - 1) tb[n_tb - 1] = (uint32_t)b;
     }
-    return lo;
 }
 
 // Output offsets [begin, end): bucket b = upper_bound(cumHistMul, o) (bucketize
 // right=True); o' = o - (cumHistMul[b] - histMul[b]); q = o' / R, r = o' % R;
-// left = leftIdx[startL + q], right = rightIdx[startR + r].
+// left = leftIdx[startL + q], right = rightIdx[startR + r]. The CTA's candidate
+// buckets come from the tile-bucket table (two loads); their cumulative ends,
+// clamped to the CTA's output window, are staged in shared memory where every
+// thread finds its first bucket.
 __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
                                                      const uint32_t* __restrict__ msL, const uint32_t* __restrict__ msR,
                                                      const int64_t* __restrict__ mcum, int64_t K,
+                                                     const uint32_t* __restrict__ tb,
                                                      const uint32_t* __restrict__ perm_l,
                                                      const uint32_t* __restrict__ perm_r, int64_t begin, int64_t end,
                                                      int64_t* __restrict__ lo_out, int64_t* __restrict__ ro_out) {
-    __shared__ int64_t s_b0, s_b1;
+    __shared__ int32_t s_cum[2 * ETILE + 2];
     __shared__ uint32_t s_l[ETILE], s_r[ETILE];
     const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
     const int64_t c1 = min(c0 + ETILE, end);
-    if (threadIdx.x == 0) s_b0 = upper_bound_i64(mcum, 0, K, c0);
-    if (threadIdx.x == 32) s_b1 = upper_bound_i64(mcum, 0, K, c1 - 1);
+    // buckets of outputs c0 and c1 - 1 lie in [b0, b1]: at most two output tiles' worth
+    const int64_t b0 = tb[c0 / ETILE];
+    const int64_t b1 = min((int64_t)tb[(c1 - 1) / ETILE + 1], K - 1);
+    const int nb = (int)(b1 - b0 + 1);
+    for (int i = threadIdx.x; i < nb; i += ENT) {
+        const int64_t v = mcum[b0 + i] - c0;
+        s_cum[i] = (int32_t)(v < 0 ? -1 : (v > ETILE ? ETILE + 1 : v));
+    }
     __syncthreads();
     const int64_t o0 = c0 + (int64_t)threadIdx.x * EIPT;
     if (o0 < c1) {   // thread: EIPT consecutive outputs, incremental (q, r)
-        int64_t b = upper_bound_i64(mcum, s_b0, s_b1 + 1, o0);
+        const int32_t rel = threadIdx.x * EIPT;
+        int lo = 0, hi = nb;
+        while (lo < hi) {   // upper_bound(rel) over the staged ends
+            const int mid = (lo + hi) >> 1;
+            if (s_cum[mid] <= rel) lo = mid + 1; else hi = mid;
+        }
+        int64_t b = b0 + lo;
         int64_t L = mL[b], R = mR[b], sL = msL[b], sR = msR[b];
         int64_t off = o0 - (mcum[b] - L * R);
         int64_t q = off / R, r = off - q * R;
@@ -334,11 +356,11 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
     }
     __syncthreads();
     const int n = (int)(c1 - c0);
-    int64_t* lo = lo_out + (c0 - begin);
-    int64_t* ro = ro_out + (c0 - begin);
+    int64_t* lo_p = lo_out + (c0 - begin);
+    int64_t* ro_p = ro_out + (c0 - begin);
     for (int o = threadIdx.x; o < n; o += ENT) {   // coalesced, streamed (evict-first) stores
-        __stcs((long long*)lo + o, (long long)s_l[o]);
-        __stcs((long long*)ro + o, (long long)s_r[o]);
+        __stcs((long long*)lo_p + o, (long long)s_l[o]);
+        __stcs((long long*)ro_p + o, (long long)s_r[o]);
     }
 }
 
@@ -435,6 +457,14 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         ctx->add_bytes("tqp_smj_cumsum", 24.0 * (double)h[2]);
         P->K = h[2];
         P->out_size = h[2] > 0 ? h[3] : 0;
+        if (P->out_size > 0) {   // tile -> bucket table for expand
+            const int64_t n_tb = ceil_div(P->out_size, ETILE) + 1;
+            P->tb.alloc(ctx, n_tb);
+            const int g = (int)std::min<int64_t>(ceil_div(P->K, 256), (int64_t)ctx->num_sms * 8);
+            launch(ctx, "tqp_smj_cumsum", tile_bucket_kernel, dim3(g), dim3(256), 0, (const int64_t*)P->mcum.get(),
+                   (const uint32_t*)P->mL.get(), (const uint32_t*)P->mR.get(), P->K, P->tb.get(), n_tb);
+            ctx->add_bytes("tqp_smj_cumsum", 16.0 * (double)P->K + 4.0 * (double)n_tb);
+        }
         *out_size_host = P->out_size;
         return P;
     } catch (...) {
@@ -451,7 +481,8 @@ void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end,
     if (blocks >= (int64_t(1) << 31)) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: window too large");
     ctx->add_bytes("tqp_smj_expand", 16.0 * (double)(end - begin));
     launch(ctx, "tqp_smj_expand", expand_kernel, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(), P->mR.get(),
-           P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->perm_l.get(), P->perm_r.get(), begin, end, lo, ro);
+           P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(), begin, end, lo,
+           ro);
 }
 
 void smj_release(tqp_ctx*, tqp_smj_plan* P) { delete P; }
