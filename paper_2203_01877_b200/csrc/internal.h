@@ -28,5 +28,7 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
 // Exclusive / inclusive scans over device arrays (decoupled look-back).
 void iota_i64(tqp_ctx* ctx, int64_t* p, int64_t n);
 void scan_max_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n);
+// out[i] = sum(in[0..i-1]), out[n] = total (out has n + 1 entries; sums must fit 32 bits)
+void scan_add_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n);
 
 }  // namespace tqp

@@ -70,82 +70,108 @@ __device__ __forceinline__ void compact_scan(CompactTile& s, const unsigned* bal
     __syncthreads();
 }
 
-// Run-length encoding of sorted keys: heads -> (unique key, run start). Each thread
-// owns JIPT consecutive keys (16-byte loads); heads are counted per thread, ranked by a
-// warp scan + block scan + decoupled look-back, staged in shared memory in key order
-// and written coalesced. Keys are read as KT (the sort's internal 32- or 64-bit key)
-// and written as KO = hi | key (the common domain of both join sides).
-// Writes ustart[U] = n and *U_out (last tile).
-template <typename KT, typename KO>
-__global__ void __launch_bounds__(JNT) rle_kernel(const KT* __restrict__ u, uint64_t hi, int64_t n, KO* ukey,
-                                                  uint32_t* ustart, int64_t* U_out, uint64_t* status,
-                                                  unsigned long long* counter, int64_t n_tiles) {
-    __shared__ int64_t s_tile;
-    __shared__ uint32_t s_woff[JNW];
-    __shared__ uint64_t s_excl;
-    __shared__ uint32_t s_tot;
-    __shared__ KO s_key[JTILE];
-    __shared__ uint32_t s_pos[JTILE];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = take_tile(counter, &s_tile);
-    const int64_t base = tile * JTILE;
-    const int64_t r0 = base + (int64_t)tid * JIPT;
-    KT k[JIPT];
-    if (base + JTILE <= n && (uintptr_t)u % 16 == 0) {
+// Run-length encoding of sorted keys: heads -> (unique key, run start), in two
+// passes with no inter-tile dependency (a decoupled look-back chain over 2048-key
+// tiles was measured to bound this step at ~1 TB/s): rle_count_kernel counts the
+// heads of every tile of RT keys, an exclusive add-scan turns counts into offsets,
+// and rle_write_kernel re-reads the keys, ranks the heads inside the tile and writes
+// them at their final positions (staged in shared memory, coalesced). Each thread
+// owns RIPT consecutive keys (16-byte loads). Keys are read as KT (the sort's
+// internal 32- or 64-bit key) and written as KO = hi | key (the common domain of
+// both join sides).
+constexpr int RIPT = 16;
+constexpr int RT = JNT * RIPT;
+
+template <typename KT>
+__device__ __forceinline__ void rle_heads(const KT* __restrict__ u, int64_t n, int64_t r0, KT (&k)[RIPT],
+                                          bool (&head)[RIPT], uint32_t& cnt) {
+    const int lane = threadIdx.x & 31;
+    if (r0 + RIPT <= n && (uintptr_t)u % 16 == 0) {
         constexpr int PER = 16 / sizeof(KT);
 #pragma unroll
-        for (int q = 0; q < JIPT / PER; q++) {
-            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(u + r0) + q);
+        for (int q = 0; q < RIPT / PER; q++) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(u + r0) + q);
             memcpy(&k[q * PER], &v, 16);
         }
     } else {
 #pragma unroll
-        for (int j = 0; j < JIPT; j++) k[j] = r0 + j < n ? u[r0 + j] : KT(0);
+        for (int j = 0; j < RIPT; j++) k[j] = r0 + j < n ? u[r0 + j] : KT(0);
     }
     // the key before this thread's first: the previous lane's last, or memory for lane 0
-    KT pk = __shfl_up_sync(0xffffffffu, k[JIPT - 1], 1);
+    KT pk = __shfl_up_sync(0xffffffffu, k[RIPT - 1], 1);
     if (lane == 0 && r0 > 0 && r0 <= n) pk = u[r0 - 1];
-    bool head[JIPT];
-    uint32_t cnt = 0;
+    cnt = 0;
 #pragma unroll
-    for (int j = 0; j < JIPT; j++) {
+    for (int j = 0; j < RIPT; j++) {
         head[j] = r0 + j < n && (j == 0 ? (r0 == 0 || k[0] != pk) : k[j] != k[j - 1]);
         cnt += head[j];
     }
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(JNT) rle_count_kernel(const KT* __restrict__ u, int64_t n, uint32_t* tcnt) {
+    __shared__ uint32_t s_w[JNW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * RT + (int64_t)tid * RIPT;
+    KT k[RIPT];
+    bool head[RIPT];
+    uint32_t cnt;
+    rle_heads(u, n, r0, k, head, cnt);
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < JNW; w++) t += s_w[w];
+        tcnt[blockIdx.x] = t;
+    }
+}
+
+template <typename KT, typename KO>
+__global__ void __launch_bounds__(JNT) rle_write_kernel(const KT* __restrict__ u, uint64_t hi, int64_t n,
+                                                        const uint32_t* __restrict__ toff, int64_t n_tiles, KO* ukey,
+                                                        uint32_t* ustart, int64_t* U_out) {
+    __shared__ uint32_t s_w[JNW];
+    constexpr int SCAP = sizeof(KO) == 4 ? RT : RT / 2;   // heads staged when they fit (else written directly)
+    __shared__ KO s_key[SCAP];
+    __shared__ uint32_t s_pos[SCAP];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * RT + (int64_t)tid * RIPT;
+    KT k[RIPT];
+    bool head[RIPT];
+    uint32_t cnt;
+    rle_heads(u, n, r0, k, head, cnt);
     uint32_t x = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    if (lane == 31) s_woff[warp] = x;
+    if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    if (warp == 0) {
-        const uint32_t wt = lane < JNW ? s_woff[lane] : 0;
-        uint32_t y = wt;
+    uint32_t wpre = 0, tot = 0;
 #pragma unroll
-        for (int o = 1; o < JNW; o <<= 1) {
-            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += z;
+    for (int w = 0; w < JNW; w++) {
+        if (w < warp) wpre += s_w[w];
+        tot += s_w[w];
+    }
+    const int64_t excl = toff[blockIdx.x];
+    uint32_t lp = wpre + x - cnt;
+    if (tot <= (uint32_t)SCAP) {
+#pragma unroll
+        for (int j = 0; j < RIPT; j++)
+            if (head[j]) { s_key[lp] = (KO)(hi | (uint64_t)k[j]); s_pos[lp] = (uint32_t)(r0 + j); lp++; }
+        __syncthreads();
+        for (uint32_t q = tid; q < tot; q += JNT) {
+            ukey[excl + q] = s_key[q];
+            ustart[excl + q] = s_pos[q];
         }
-        const uint32_t tot = __shfl_sync(0xffffffffu, y, JNW - 1);
-        const uint64_t e = lookback_warp(status, tile, tot, OpAdd(), 0ull);
-        if (lane < JNW) s_woff[lane] = y - wt;
-        if (lane == 0) { s_excl = e; s_tot = tot; }
-    }
-    __syncthreads();
-    uint32_t lp = s_woff[warp] + x - cnt;
+    } else {
 #pragma unroll
-    for (int j = 0; j < JIPT; j++)
-        if (head[j]) { s_key[lp] = (KO)(hi | (uint64_t)k[j]); s_pos[lp] = (uint32_t)(r0 + j); lp++; }
-    __syncthreads();
-    const int64_t excl = (int64_t)s_excl;
-    const uint32_t tot = s_tot;
-    for (uint32_t q = tid; q < tot; q += JNT) {
-        ukey[excl + q] = s_key[q];
-        ustart[excl + q] = s_pos[q];
+        for (int j = 0; j < RIPT; j++)
+            if (head[j]) { ukey[excl + lp] = (KO)(hi | (uint64_t)k[j]); ustart[excl + lp] = (uint32_t)(r0 + j); lp++; }
     }
-    if (tile == n_tiles - 1 && tid == 0) {
+    if (blockIdx.x == n_tiles - 1 && tid == 0) {
         const int64_t U = excl + tot;
         *U_out = U;
         ustart[U] = (uint32_t)n;
@@ -369,13 +395,12 @@ void rle(tqp_ctx* ctx, const KT* u, uint64_t hi, int64_t n, DevBuf<KO>& ukey, De
          int64_t* U_dev) {
     ukey.alloc(ctx, n);
     ustart.alloc(ctx, n + 1);
-    const int64_t tiles = ceil_div(n, JTILE);
-    DevBuf<uint64_t> status(ctx, tiles);
-    DevBuf<unsigned long long> counter(ctx, 1);
-    status.zero();
-    counter.zero();
-    launch(ctx, "tqp_smj_rle", rle_kernel<KT, KO>, dim3((unsigned)tiles), dim3(JNT), 0, u, hi, n, ukey.get(),
-           ustart.get(), U_dev, status.get(), counter.get(), tiles);
+    const int64_t tiles = ceil_div(n, RT);
+    DevBuf<uint32_t> tcnt(ctx, tiles), toff(ctx, tiles + 1);
+    launch(ctx, "tqp_smj_rle", rle_count_kernel<KT>, dim3((unsigned)tiles), dim3(JNT), 0, u, n, tcnt.get());
+    scan_add_u32_exclusive(ctx, tcnt.get(), toff.get(), tiles);
+    launch(ctx, "tqp_smj_rle", rle_write_kernel<KT, KO>, dim3((unsigned)tiles), dim3(JNT), 0, u, hi, n,
+           (const uint32_t*)toff.get(), tiles, ukey.get(), ustart.get(), U_dev);
 }
 
 // Both sides' RLE in the common key domain KO, then the intersection of the unique
@@ -389,7 +414,7 @@ void rle_intersect(tqp_ctx* ctx, tqp_smj_plan* P, SortOut& sl, SortOut& sr, int6
         const uint64_t hi = (sizeof(KO) == 8 && so.k32) ? (so.and_bits & 0xFFFFFFFF00000000ull) : 0;
         if (so.k32) rle<uint32_t, KO>(ctx, so.keys32.get(), hi, n, uk, us, U);
         else rle<uint64_t, KO>(ctx, so.keys64.get(), 0, n, uk, us, U);
-        ctx->add_bytes("tqp_smj_rle", (double)n * (so.k32 ? 4 : 8));
+        ctx->add_bytes("tqp_smj_rle", (double)n * (so.k32 ? 4 : 8));   // compulsory: keys read once
         so.keys32.release();
         so.keys64.release();
     };
