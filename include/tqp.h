@@ -148,7 +148,8 @@ tqp_status tqp_smj_join(tqp_ctx* ctx, tqp_col left, int64_t n_left, tqp_col righ
  * `cols[col] <op> value` holds (conjunction, "intersecting the
  * masks using logical_and"). mask_out (nullable): n x u8 in {0,1}; sel_out
  * (nullable): ascending passing rows (capacity n x int64); at least one given.
- * n_sel_host (nullable): number of passing rows (synchronises if given). */
+ * n_sel_host (nullable): number of passing rows (synchronises if given).
+ * n < 2^32, else TQP_ERR_INVALID_ARGUMENT. */
 typedef enum { TQP_LT = 0, TQP_LE = 1, TQP_GT = 2, TQP_GE = 3, TQP_EQ = 4, TQP_NE = 5 } tqp_cmp;
 typedef struct {
     int32_t col;     /* index into cols */

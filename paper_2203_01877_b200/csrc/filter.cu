@@ -1,12 +1,13 @@
 // filter.cu -- filter + order-preserving compaction.
 //
 // Listing 1 (bitmap): mask = lt(col, c) [AND-ed over predicates, PAPER.md:829];
-// Listing 2 (selection vector): idx = nonzero(mask). One kernel evaluates the
-// conjunction per row (folded to one interval term per column, common.cuh), writes
-// the u8 mask, and compacts passing row numbers in ascending order: each thread owns
-// 8 consecutive rows (vector loads) -> warp scan of per-thread counts -> block scan ->
-// decoupled look-back across tiles -> rows staged in shared memory -> coalesced
-// writes. No atomics whose order could leak into the output.
+// Listing 2 (selection vector): idx = nonzero(mask). Pass 1 evaluates the conjunction
+// per row (folded to one interval term per column, common.cuh), writes the u8 mask and
+// counts passing rows per tile; an exclusive add-scan gives tile offsets; pass 2 reads
+// only the mask and writes passing row numbers in ascending order (warp scan of
+// per-thread counts -> block scan -> staged in shared memory -> coalesced stores).
+// No inter-tile chain (a decoupled look-back was measured to leave the warps of a
+// tile idle at the barrier) and no atomics whose order could leak into the output.
 #include "internal.h"
 
 namespace tqp {
@@ -14,20 +15,16 @@ namespace tqp {
 namespace {
 constexpr int FNT = 256;
 constexpr int FNW = FNT / 32;
-constexpr int FIPT = 8;                 // consecutive rows per thread (vector loads)
+constexpr int FIPT = 16;                // consecutive rows per thread (vector loads)
 constexpr int FTILE = FNT * FIPT;
 
 struct FilterArgs {
     TermSet ts;                          // the conjunction, folded per column (common.cuh)
     const void* tcol[TQP_MAX_PREDS];
-    int vec;                             // every term column and the mask are 16-byte aligned
+    int vec;                             // every term column is 16-byte aligned
     int64_t n;
-    uint8_t* mask;
-    int64_t* sel;
-    uint64_t* status;
-    unsigned long long* counter;
-    int64_t* total;
-    int64_t n_tiles;
+    uint8_t* mask;                       // the output mask, or a temporary one
+    uint32_t* tcnt;                      // per tile: passing rows
 };
 
 // Rows r0 .. r0+FIPT-1 of a column; vector loads on full aligned tiles.
@@ -47,15 +44,12 @@ __device__ __forceinline__ void load_rows(const T* c, int64_t r0, int64_t n, boo
     }
 }
 
-__global__ void __launch_bounds__(FNT) filter_kernel(FilterArgs a) {
-    __shared__ int64_t s_tile;
-    __shared__ uint32_t s_woff[FNW];
-    __shared__ uint64_t s_excl;
-    __shared__ uint32_t s_tot;
-    __shared__ int64_t s_out[FTILE];
+// Pass 1 (Listing 1, the bitmap): the conjunction per row -> u8 mask, and the number
+// of passing rows per tile. No inter-tile dependency.
+__global__ void __launch_bounds__(FNT) filter_mask_kernel(FilterArgs a) {
+    __shared__ uint32_t s_w[FNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = take_tile(a.counter, &s_tile);
-    const int64_t base = tile * FTILE;
+    const int64_t base = (int64_t)blockIdx.x * FTILE;
     const int64_t r0 = base + (int64_t)tid * FIPT;
     const bool full = base + FTILE <= a.n;
     const bool vec = full && a.vec;
@@ -78,7 +72,7 @@ __global__ void __launch_bounds__(FNT) filter_kernel(FilterArgs a) {
             for (int i = 0; i < FIPT; i++) pass[i] &= term32(x[i], (uint32_t)tm.lo, (uint32_t)tm.width, neg);
         } else {
             unsigned char x[FIPT];
-            load_rows<unsigned char, uint2>((const unsigned char*)a.tcol[q], r0, a.n, vec, x);
+            load_rows<unsigned char, uint4>((const unsigned char*)a.tcol[q], r0, a.n, vec, x);
 #pragma unroll
             for (int i = 0; i < FIPT; i++) pass[i] &= term32(x[i], (uint32_t)tm.lo, (uint32_t)tm.width, neg);
         }
@@ -86,64 +80,77 @@ __global__ void __launch_bounds__(FNT) filter_kernel(FilterArgs a) {
     uint32_t cnt = 0;
 #pragma unroll
     for (int i = 0; i < FIPT; i++) cnt += pass[i];
-    if (a.mask) {   // Listing 1's bitmap, one byte per row
-        if (vec) {
-            uint2 m;
-            m.x = (uint32_t)pass[0] | (uint32_t)pass[1] << 8 | (uint32_t)pass[2] << 16 | (uint32_t)pass[3] << 24;
-            m.y = (uint32_t)pass[4] | (uint32_t)pass[5] << 8 | (uint32_t)pass[6] << 16 | (uint32_t)pass[7] << 24;
-            __stcs(reinterpret_cast<uint2*>(a.mask + r0), m);
-        } else {
+    if (full && (uintptr_t)a.mask % 16 == 0) {
+        uint32_t m[4];
 #pragma unroll
-            for (int i = 0; i < FIPT; i++)
-                if (r0 + i < a.n) a.mask[r0 + i] = (uint8_t)pass[i];
-        }
+        for (int w = 0; w < 4; w++)
+            m[w] = (uint32_t)pass[4 * w] | (uint32_t)pass[4 * w + 1] << 8 | (uint32_t)pass[4 * w + 2] << 16 |
+                   (uint32_t)pass[4 * w + 3] << 24;
+        __stcs(reinterpret_cast<uint4*>(a.mask + r0), make_uint4(m[0], m[1], m[2], m[3]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < FIPT; i++)
+            if (r0 + i < a.n) a.mask[r0 + i] = (uint8_t)pass[i];
     }
-    // rank of each passing row in the tile: thread-exclusive scan within the warp
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < FNW; w++) t += s_w[w];
+        a.tcnt[blockIdx.x] = t;
+    }
+}
+
+// Pass 2 (Listing 2, the selection vector): passing row numbers in ascending order at
+// the tile's offset; ranks by warp scan of per-thread counts + block scan; staged in
+// shared memory and written coalesced.
+__global__ void __launch_bounds__(FNT) filter_sel_kernel(const uint8_t* __restrict__ mask, int64_t n,
+                                                         const uint32_t* __restrict__ toff, int64_t* sel) {
+    __shared__ uint32_t s_w[FNW];
+    __shared__ int64_t s_out[FTILE];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * FTILE;
+    const int64_t excl = toff[blockIdx.x];
+    const uint32_t tot = toff[blockIdx.x + 1] - (uint32_t)excl;
+    if (tot == 0) return;
+    const int64_t r0 = base + (int64_t)tid * FIPT;
+    uint8_t m[FIPT];
+    if (base + FTILE <= n && (uintptr_t)mask % 16 == 0) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(mask + r0));
+        memcpy(m, &v, 16);
+    } else {
+#pragma unroll
+        for (int i = 0; i < FIPT; i++) m[i] = r0 + i < n ? mask[r0 + i] : 0;
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < FIPT; i++) cnt += m[i] != 0;
     uint32_t x = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    const uint32_t texcl = x - cnt;
-    if (lane == 31) s_woff[warp] = x;
+    if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    if (warp == 0) {
-        const uint32_t wt = lane < FNW ? s_woff[lane] : 0;
-        uint32_t y = wt;
+    uint32_t lp = x - cnt;
 #pragma unroll
-        for (int o = 1; o < FNW; o <<= 1) {
-            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
-            if (lane >= o) y += z;
-        }
-        const uint32_t tot = __shfl_sync(0xffffffffu, y, FNW - 1);
-        const uint64_t e = lookback_warp(a.status, tile, tot, OpAdd(), 0ull);
-        if (lane < FNW) s_woff[lane] = y - wt;
-        if (lane == 0) {
-            s_excl = e;
-            s_tot = tot;
-            if (tile == a.n_tiles - 1) *a.total = (int64_t)(e + tot);
-        }
-    }
-    __syncthreads();
-    if (!a.sel) return;
-    // Listing 2's selection vector: stage the tile's passing row numbers in shared
-    // memory in row order, then write them out coalesced
-    uint32_t lp = s_woff[warp] + texcl;
+    for (int w = 0; w < FNW; w++)
+        if (w < warp) lp += s_w[w];
 #pragma unroll
     for (int i = 0; i < FIPT; i++)
-        if (pass[i]) s_out[lp++] = r0 + i;
+        if (m[i]) s_out[lp++] = r0 + i;
     __syncthreads();
-    const uint32_t tot = s_tot;
-    int64_t* dst = a.sel + s_excl;
+    int64_t* dst = sel + excl;
     for (uint32_t k = tid; k < tot; k += FNT) __stcs(reinterpret_cast<long long*>(dst + k), (long long)s_out[k]);
 }
 }  // namespace
 
 void filter_compact(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, const tqp_pred* preds, int n_preds,
                     uint8_t* mask_out, int64_t* sel_out, int64_t* n_sel_host) {
-    if (n < 0 || n_cols < 0 || n_preds < 0 || n_preds > TQP_MAX_PREDS)
-        fail(TQP_ERR_INVALID_ARGUMENT, "filter: bad sizes");
+    if (n < 0 || n >= (int64_t(1) << 32) || n_cols < 0 || n_preds < 0 || n_preds > TQP_MAX_PREDS)
+        fail(TQP_ERR_INVALID_ARGUMENT, "filter: bad sizes (n must be < 2^32)");
     if (n_cols > 0 && !cols) fail(TQP_ERR_INVALID_ARGUMENT, "filter: null cols");
     if (n_preds > 0 && !preds) fail(TQP_ERR_INVALID_ARGUMENT, "filter: null preds");
     if (!mask_out && !sel_out && !n_sel_host) fail(TQP_ERR_INVALID_ARGUMENT, "filter: no output requested");
@@ -154,29 +161,34 @@ void filter_compact(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, co
     }
     FilterArgs a{};
     a.ts = make_terms(preds, n_preds, [&](int c) { return cols[c].dtype; });
-    a.vec = mask_out == nullptr || (uintptr_t)mask_out % 16 == 0;
+    a.vec = 1;
     for (int q = 0; q < a.ts.n; q++) {
         a.tcol[q] = cols[a.ts.t[q].col].data;
         a.vec = a.vec && (uintptr_t)a.tcol[q] % 16 == 0;
     }
-    DevBuf<int64_t> total(ctx, 1);
-    total.zero();
+    int64_t nsel = 0;
     if (n > 0) {
         const int64_t tiles = ceil_div(n, FTILE);
-        DevBuf<uint64_t> status(ctx, tiles);
-        DevBuf<unsigned long long> counter(ctx, 1);
-        status.zero();
-        counter.zero();
+        DevBuf<uint8_t> tmask;
+        if (!mask_out) tmask.alloc(ctx, n);
+        DevBuf<uint32_t> tcnt(ctx, tiles), toff(ctx, tiles + 1);
         a.n = n;
-        a.mask = mask_out;
-        a.sel = sel_out;
-        a.status = status.get();
-        a.counter = counter.get();
-        a.total = total.get();
-        a.n_tiles = tiles;
-        launch(ctx, "tqp_filter", filter_kernel, dim3((unsigned)tiles), dim3(FNT), 0, a);
+        a.mask = mask_out ? mask_out : tmask.get();
+        a.tcnt = tcnt.get();
+        launch(ctx, "tqp_filter", filter_mask_kernel, dim3((unsigned)tiles), dim3(FNT), 0, a);
+        scan_add_u32_exclusive(ctx, tcnt.get(), toff.get(), tiles);
+        if (sel_out)
+            launch(ctx, "tqp_filter_select", filter_sel_kernel, dim3((unsigned)tiles), dim3(FNT), 0,
+                   (const uint8_t*)a.mask, n, (const uint32_t*)toff.get(), sel_out);
+        if (n_sel_host) {
+            uint32_t t = 0;
+            read_back(ctx, &t, toff.get() + tiles, 4);
+            nsel = t;
+            *n_sel_host = nsel;
+        }
+    } else if (n_sel_host) {
+        *n_sel_host = 0;
     }
-    if (n_sel_host) read_back(ctx, n_sel_host, total.get(), 8);
     {   // distinct predicate columns in; mask and selection vector out
         double in = 0;
         for (int q = 0; q < n_preds; q++) {
@@ -184,8 +196,8 @@ void filter_compact(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, co
             for (int r = 0; r < q; r++) seen = seen || preds[r].col == preds[q].col;
             if (!seen) in += (double)dtype_size(cols[preds[q].col].dtype);
         }
-        double out = (mask_out ? 1.0 : 0.0) * (double)n + (sel_out && n_sel_host ? 8.0 * (double)*n_sel_host : 0.0);
-        if (n > 0) ctx->add_bytes("tqp_filter", in * (double)n + out);
+        if (n > 0) ctx->add_bytes("tqp_filter", in * (double)n + (mask_out ? (double)n : 0.0));
+        if (n > 0 && sel_out) ctx->add_bytes("tqp_filter_select", 8.0 * (double)nsel + (mask_out ? (double)n : 0.0));
     }
 }
 
