@@ -13,10 +13,13 @@
 //      T[b] = first sorted position whose bucket is >= b, built from the bucket
 //      end positions by an exclusive max-scan (no domain-sized bincount),
 //   3. per probe key: bucket -> [T[b], T[b+1]) -> lower_bound inside the bucket
-//      -> equality test (the paper's match mask) ->
-//      order-preserving compaction (ballot + block scan + decoupled look-back)
-//      writing leftOutputIndex = perm[pos], rightOutputIndex = probe row
-//       in ascending probe-row order (reading R7).
+//      -> equality test (the paper's match mask); the matching
+//      build row (or a no-match sentinel) is written per probe row as u32 with a
+//      per-tile count, an exclusive add-scan gives tile offsets, and an
+//      order-preserving compaction pass writes leftOutputIndex = perm[pos],
+//      rightOutputIndex = probe row in ascending probe-row order
+//      (reading R7). Two passes instead of one with a decoupled look-back: the
+//      look-back left a tile's warps idle at the barrier (measured).
 // Duplicate build keys (adjacent equal sorted keys) -> TQP_ERR_DUPLICATE_BUILD_KEY.
 #include "internal.h"
 
@@ -70,13 +73,9 @@ struct ProbeArgs {
     int shift;
     int mode;                 // 0 = join pairs, 1 = semi/anti
     int anti;
-    int64_t* left_out;
-    int64_t* right_out;       // join: probe rows; semi: selected rows
-    uint8_t* match_out;       // semi: per-row mask (nullable)
-    uint64_t* status;
-    unsigned long long* counter;
-    int64_t* total;           // written by the last tile
-    int64_t n_tiles;
+    uint32_t* lft;            // join: per probe row, the build row or NOMATCH
+    uint8_t* mask;            // semi: per probe row, 1 = the key is on the build side
+    uint32_t* tcnt;           // per tile: rows selected (join: matches; semi: match != anti)
 };
 
 template <typename KT, int PDT, bool PACKED>
@@ -144,68 +143,117 @@ __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint3
     return false;
 }
 
+constexpr uint32_t NOMATCH = 0xFFFFFFFFu;   // build rows are < 2^30
+
+// Pass 1: every probe row is looked up (no inter-tile dependency): join mode writes
+// the matching build row (or NOMATCH) as u32, semi mode the match byte; each tile
+// counts its selected rows.
 template <typename KT, int PDT, bool PACKED>
 __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
-    __shared__ int64_t s_tile;
-    __shared__ uint32_t s_cnt[PIPT * PNW];
-    __shared__ uint64_t s_excl;
+    __shared__ uint32_t s_w[PNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = take_tile(a.counter, &s_tile);
-    const int64_t base = tile * PTILE;
+    const int64_t base = (int64_t)blockIdx.x * PTILE;
     bool m[PIPT];
     uint32_t left[PIPT];
-    unsigned bal[PIPT];
 #pragma unroll
     for (int i = 0; i < PIPT; i++) {
-        int64_t row = base + i * PNT + tid;
+        const int64_t row = base + i * PNT + tid;
         m[i] = false;
+        left[i] = NOMATCH;
         if (row < a.n_probe) m[i] = probe_one<KT, PDT, PACKED>(a, row, left[i]);
     }
+    uint32_t cnt = 0;
 #pragma unroll
     for (int i = 0; i < PIPT; i++) {
-        int64_t row = base + i * PNT + tid;
-        bool sel = a.mode == 0 ? m[i] : (row < a.n_probe && (m[i] != (a.anti != 0)));
-        if (a.mode == 1 && a.match_out && row < a.n_probe) a.match_out[row] = (uint8_t)m[i];
-        bal[i] = __ballot_sync(0xffffffffu, sel);
-        if (lane == 0) s_cnt[i * PNW + warp] = __popc(bal[i]);
-    }
-    __syncthreads();
-    if (warp == 0) {
-        // exclusive scan over the PIPT*PNW (item, warp) counts, in tile order
-        uint32_t c[PIPT * PNW / 32];
-        uint32_t local = 0;
-#pragma unroll
-        for (int j = 0; j < PIPT * PNW / 32; j++) { c[j] = s_cnt[lane * (PIPT * PNW / 32) + j]; local += c[j]; }
-        uint32_t x = local;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
-        uint32_t run = x - local;
-#pragma unroll
-        for (int j = 0; j < PIPT * PNW / 32; j++) { s_cnt[lane * (PIPT * PNW / 32) + j] = run; run += c[j]; }
-        uint64_t e = lookback_warp(a.status, tile, tot, OpAdd(), 0ull);
-        if (lane == 0) {
-            s_excl = e;
-            if (tile == a.n_tiles - 1) *a.total = (int64_t)(e + tot);
+        const int64_t row = base + i * PNT + tid;
+        if (row >= a.n_probe) continue;
+        if (a.mode == 0) {
+            __stcs(a.lft + row, m[i] ? left[i] : NOMATCH);
+            cnt += m[i];
+        } else {
+            a.mask[row] = (uint8_t)m[i];
+            cnt += m[i] != (a.anti != 0);
         }
     }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_w[warp] = cnt;
     __syncthreads();
-    const int64_t excl = (int64_t)s_excl;
-    const unsigned lt = lanemask_lt();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < PNW; w++) t += s_w[w];
+        a.tcnt[blockIdx.x] = t;
+    }
+}
+
+// Pass 2: order-preserving compaction at the scanned tile offsets. Each thread owns
+// PIPT consecutive probe rows; ranks by warp scan of per-thread counts + block scan;
+// join pairs (leftOutputIndex = build row, rightOutputIndex = probe row)
+// or semi/anti rows are staged in shared memory and written coalesced.
+template <bool JOIN>
+__global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ lft, const uint8_t* __restrict__ mask,
+                                                   int anti, int64_t np, const uint64_t* __restrict__ toff,
+                                                   int64_t* left_out, int64_t* right_out) {
+    __shared__ uint32_t s_w[PNW];
+    __shared__ uint32_t s_l[PTILE];
+    __shared__ uint16_t s_r[PTILE];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * PTILE;
+    const int64_t excl = (int64_t)toff[blockIdx.x];
+    const uint32_t tot = (uint32_t)(toff[blockIdx.x + 1] - toff[blockIdx.x]);
+    if (tot == 0) return;
+    const int64_t r0 = base + (int64_t)tid * PIPT;
+    const bool full = base + PTILE <= np;
+    uint32_t l[PIPT];
+    bool sel[PIPT];
+    if (JOIN) {
+        if (full) {
+            const uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(lft + r0));
+            const uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(lft + r0) + 1);
+            l[0] = v0.x; l[1] = v0.y; l[2] = v0.z; l[3] = v0.w; l[4] = v1.x; l[5] = v1.y; l[6] = v1.z; l[7] = v1.w;
+        } else {
+#pragma unroll
+            for (int i = 0; i < PIPT; i++) l[i] = r0 + i < np ? lft[r0 + i] : NOMATCH;
+        }
+#pragma unroll
+        for (int i = 0; i < PIPT; i++) sel[i] = l[i] != NOMATCH;
+    } else {
+        uint8_t mb[PIPT];
+        if (full && (uintptr_t)mask % 8 == 0) {
+            const uint2 v = *reinterpret_cast<const uint2*>(mask + r0);
+            memcpy(mb, &v, 8);
+        } else {
+#pragma unroll
+            for (int i = 0; i < PIPT; i++) mb[i] = r0 + i < np ? mask[r0 + i] : (uint8_t)(anti != 0);
+        }
+#pragma unroll
+        for (int i = 0; i < PIPT; i++) sel[i] = (mb[i] != 0) != (anti != 0) && r0 + i < np;
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < PIPT; i++) cnt += sel[i];
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t lp = x - cnt;
+#pragma unroll
+    for (int w = 0; w < PNW; w++)
+        if (w < warp) lp += s_w[w];
 #pragma unroll
     for (int i = 0; i < PIPT; i++) {
-        if (bal[i] & (1u << lane)) {
-            int64_t row = base + i * PNT + tid;
-            int64_t j = excl + s_cnt[i * PNW + warp] + __popc(bal[i] & lt);
-            if (a.mode == 0) {   // outputs are streamed: evict-first stores
-                __stcs((long long*)a.left_out + j, (long long)left[i]);
-                __stcs((long long*)a.right_out + j, (long long)row);
-            } else if (a.right_out) {
-                __stcs((long long*)a.right_out + j, (long long)row);
-            }
-        }
+        if (!sel[i]) continue;
+        if (JOIN) s_l[lp] = l[i];
+        s_r[lp] = (uint16_t)(tid * PIPT + i);
+        lp++;
+    }
+    __syncthreads();
+    for (uint32_t k = tid; k < tot; k += PNT) {   // streamed (evict-first) coalesced stores
+        if (JOIN) __stcs((long long*)left_out + excl + k, (long long)s_l[k]);
+        if (right_out) __stcs((long long*)right_out + excl + k, (long long)(base + s_r[k]));
     }
 }
 
@@ -290,15 +338,17 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
 
 void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, int anti, int64_t* left_out,
                int64_t* right_out, uint8_t* match_out, int64_t* n_out_host) {
-    DevBuf<int64_t> total(ctx, 1);
-    total.zero();
+    DevBuf<int64_t> pack(ctx, 2);   // [0] selected rows, [1] duplicate-build-key flag: one readback
+    pack.zero();
     const int64_t nb = B.nb;
     if (np > 0 && nb > 0) {
         const int64_t tiles = ceil_div(np, PTILE);
-        DevBuf<uint64_t> status(ctx, tiles);
-        DevBuf<unsigned long long> counter(ctx, 1);
-        status.zero();
-        counter.zero();
+        DevBuf<uint32_t> tcnt(ctx, tiles);
+        DevBuf<uint64_t> toff(ctx, tiles + 1);
+        DevBuf<uint32_t> lft;
+        DevBuf<uint8_t> tmask;
+        if (mode == 0) lft.alloc(ctx, np);
+        else if (!match_out) tmask.alloc(ctx, np);
         ProbeArgs a{};
         a.probe = pk.data;
         a.n_probe = np;
@@ -314,13 +364,9 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         a.shift = B.shift;
         a.mode = mode;
         a.anti = anti;
-        a.left_out = left_out;
-        a.right_out = right_out;
-        a.match_out = match_out;
-        a.status = status.get();
-        a.counter = counter.get();
-        a.total = total.get();
-        a.n_tiles = tiles;
+        a.lft = lft.get();
+        a.mask = match_out ? match_out : tmask.get();
+        a.tcnt = tcnt.get();
         auto go = [&](auto kt, auto pk_) {
             using KT = decltype(kt);
             constexpr bool PK = decltype(pk_)::value;
@@ -335,6 +381,14 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         } else {
             if (B.packed) go(uint64_t{}, std::true_type{}); else go(uint64_t{}, std::false_type{});
         }
+        scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
+        if (mode == 0)
+            launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)lft.get(),
+                   (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out);
+        else if (right_out)
+            launch(ctx, "tqp_pkfk_emit", emit_kernel<false>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)nullptr,
+                   (const uint8_t*)a.mask, anti, np, (const uint64_t*)toff.get(), (int64_t*)nullptr, right_out);
+        TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
     } else if (np > 0 && mode == 1) {
         // empty build side: nothing matches
         if (match_out) TQP_CUDA(cudaMemsetAsync(match_out, 0, np, ctx->stream));
@@ -342,21 +396,18 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
             // every probe row is selected: sel = 0..np-1
             if (right_out) iota_i64(ctx, right_out, np);
             int64_t h = np;
-            TQP_CUDA(cudaMemcpyAsync(total.get(), &h, 8, cudaMemcpyHostToDevice, ctx->stream));
+            TQP_CUDA(cudaMemcpyAsync(pack.get(), &h, 8, cudaMemcpyHostToDevice, ctx->stream));
         }
     }
+    if (B.dup.get()) TQP_CUDA(cudaMemcpyAsync(pack.get() + 1, B.dup.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
     int64_t h[2];
-    DevBuf<int64_t> pack(ctx, 2);
-    TQP_CUDA(cudaMemcpyAsync(pack.get(), total.get(), 8, cudaMemcpyDeviceToDevice, ctx->stream));
-    TQP_CUDA(cudaMemsetAsync(pack.get() + 1, 0, 8, ctx->stream));
-    TQP_CUDA(cudaMemcpyAsync(pack.get() + 1, B.dup.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
     read_back(ctx, h, pack.get(), 16);
     if (h[1] && mode == 0) fail(TQP_ERR_DUPLICATE_BUILD_KEY, "pkfk: duplicate key on the build side");
     if (n_out_host) *n_out_host = h[0];
-    if (np > 0 && nb > 0)   // probe keys in; pairs (join) or mask + selection vector (semi) out
-        ctx->add_bytes("tqp_pkfk_probe", (double)np * dtype_size(pk.dtype) +
-                                         (mode == 0 ? 16.0 * (double)h[0]
-                                                    : (match_out ? (double)np : 0.0) + (right_out ? 8.0 * (double)h[0] : 0.0)));
+    if (np > 0 && nb > 0) {   // probe keys in; pairs (join) or mask + selection vector (semi) out
+        ctx->add_bytes("tqp_pkfk_probe", (double)np * dtype_size(pk.dtype) + (mode == 1 && match_out ? (double)np : 0.0));
+        ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? 16.0 * (double)h[0] : (right_out ? 8.0 * (double)h[0] : 0.0));
+    }
 }
 }  // namespace
 

@@ -10,11 +10,11 @@ constexpr int STILE = SNT * SIPT;
 
 // Exclusive scan of u32 values under max (out[i] = max(in[0..i-1])) or add
 // (out[i] = sum(in[0..i-1]), and out[n] = the total). out[0] = 0.
-template <bool ADD>
-__global__ void __launch_bounds__(SNT) scan_u32_kernel(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
+template <bool ADD, typename OT>
+__global__ void __launch_bounds__(SNT) scan_u32_kernel(const uint32_t* __restrict__ in, OT* __restrict__ out,
                                                        int64_t n, uint64_t* status, unsigned long long* counter) {
     __shared__ int64_t s_tile;
-    __shared__ uint32_t s_w[SNT / 32];
+    __shared__ OT s_w[SNT / 32];
     __shared__ uint64_t s_excl;
     const int64_t tile = take_tile(counter, &s_tile);
     const int64_t base = tile * STILE + (int64_t)threadIdx.x * SIPT;
@@ -27,32 +27,33 @@ __global__ void __launch_bounds__(SNT) scan_u32_kernel(const uint32_t* __restric
 #pragma unroll
         for (int i = 0; i < SIPT; i++) v[i] = (base + i < n) ? in[base + i] : 0u;
     }
-    auto op = [](uint32_t a, uint32_t b) { return ADD ? a + b : max(a, b); };
-    uint32_t t = 0;
+    auto op = [](OT a, OT b) -> OT { return ADD ? a + b : max(a, b); };
+    OT t = 0;
 #pragma unroll
     for (int i = 0; i < SIPT; i++) t = op(t, v[i]);
     // block exclusive max over threads
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t x = t;
+    OT x = t;
     for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        OT y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x = op(x, y);
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    uint32_t wpre = 0, tot = 0;
+    OT wpre = 0, tot = 0;
     for (int w = 0; w < SNT / 32; w++) {
         if (w < warp) wpre = op(wpre, s_w[w]);
         tot = op(tot, s_w[w]);
     }
-    const uint32_t xp = __shfl_up_sync(0xffffffffu, x, 1);
-    uint32_t texcl = op(wpre, lane > 0 ? xp : 0u);
+    const OT xp = __shfl_up_sync(0xffffffffu, x, 1);
+    OT texcl = op(wpre, lane > 0 ? xp : OT(0));
     if (warp == 0) {
-        uint64_t e = ADD ? lookback_warp(status, tile, tot, OpAdd(), 0ull) : lookback_warp(status, tile, tot, OpMax(), 0ull);
+        uint64_t e = ADD ? lookback_warp(status, tile, (uint64_t)tot, OpAdd(), 0ull)
+                         : lookback_warp(status, tile, (uint64_t)tot, OpMax(), 0ull);
         if (lane == 0) s_excl = e;
     }
     __syncthreads();
-    uint32_t run = op((uint32_t)s_excl, texcl);
+    OT run = op((OT)s_excl, texcl);
 #pragma unroll
     for (int i = 0; i < SIPT; i++) {
         if (base + i < n) out[base + i] = run;
@@ -81,7 +82,7 @@ void scan_max_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int
     status.zero();
     counter.zero();
     ctx->add_bytes("tqp_scan_max", 8.0 * (double)n);
-    launch(ctx, "tqp_scan_max", scan_u32_kernel<false>, dim3((unsigned)tiles), dim3(SNT), 0, in, out, n, status.get(),
+    launch(ctx, "tqp_scan_max", scan_u32_kernel<false, uint32_t>, dim3((unsigned)tiles), dim3(SNT), 0, in, out, n, status.get(),
            counter.get());
 }
 
@@ -93,8 +94,20 @@ void scan_add_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int
     status.zero();
     counter.zero();
     ctx->add_bytes("tqp_scan_add", 8.0 * (double)n);
-    launch(ctx, "tqp_scan_add", scan_u32_kernel<true>, dim3((unsigned)tiles), dim3(SNT), 0, in, out, n, status.get(),
+    launch(ctx, "tqp_scan_add", scan_u32_kernel<true, uint32_t>, dim3((unsigned)tiles), dim3(SNT), 0, in, out, n, status.get(),
            counter.get());
+}
+
+void scan_add_u32_to_u64_exclusive(tqp_ctx* ctx, const uint32_t* in, uint64_t* out, int64_t n) {
+    if (n <= 0) return;
+    const int64_t tiles = ceil_div(n, STILE);
+    DevBuf<uint64_t> status(ctx, tiles);
+    DevBuf<unsigned long long> counter(ctx, 1);
+    status.zero();
+    counter.zero();
+    ctx->add_bytes("tqp_scan_add", 12.0 * (double)n);
+    launch(ctx, "tqp_scan_add", scan_u32_kernel<true, uint64_t>, dim3((unsigned)tiles), dim3(SNT), 0, in, out, n,
+           status.get(), counter.get());
 }
 
 }  // namespace tqp
