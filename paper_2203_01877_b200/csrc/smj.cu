@@ -8,10 +8,11 @@
 //   l.4    bincount left / right                          -> rle_kernel: run-length
 //          encoding of the sorted keys (unique key, run start); counts are run
 //          lengths, so no domain-sized histogram is ever materialised
-//   l.5-8  histMul = L*R; cumsums                         -> intersect_kernel (merge
-//          of the two unique-key lists, compaction of the common keys with
-//          L, R, startL = cumL - L, startR = cumR - R) + cum_kernel (inclusive
-//          scan of L*R by decoupled look-back = cumHistMul)
+//   l.5-8  histMul = L*R; cumsums                         -> intersect_kernel (each
+//          left unique key located among the right unique keys by a merge walk)
+//          + common_kernel (compaction of the common keys with L, R,
+//          startL = cumL - L, startR = cumR - R) + cum_kernel (inclusive scan of
+//          L*R by decoupled look-back = cumHistMul)
 //   l.9    outSize = cumHistMul[-1]                       -> one 8-byte readback
 //   l.10-14 arange, bucketize, in-bucket offset, div/rem -> expand_kernel: each CTA
 //          owns a fixed output range, finds its first bucket with one
@@ -34,41 +35,6 @@ constexpr int JNT = 256;
 constexpr int JNW = JNT / 32;
 constexpr int JIPT = 8;
 constexpr int JTILE = JNT * JIPT;
-
-// Compaction helper shared by the RLE / intersection kernels: thread-ordered
-// (item i, thread) flags -> exclusive positions; returns the tile's exclusive
-// prefix. flags are block-striped: item i of thread t is tile position i*JNT + t.
-struct CompactTile {
-    uint32_t s_cnt[JIPT * JNW];
-    uint64_t s_excl;
-    uint32_t s_tot;
-};
-
-__device__ __forceinline__ void compact_scan(CompactTile& s, const unsigned* bal, int64_t tile, uint64_t* status) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int i = 0; i < JIPT; i++)
-        if (lane == 0) s.s_cnt[i * JNW + warp] = __popc(bal[i]);
-    __syncthreads();
-    if (warp == 0) {
-        constexpr int PER = JIPT * JNW / 32;
-        uint32_t c[PER], local = 0;
-#pragma unroll
-        for (int j = 0; j < PER; j++) { c[j] = s.s_cnt[lane * PER + j]; local += c[j]; }
-        uint32_t x = local;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        const uint32_t tot = __shfl_sync(0xffffffffu, x, 31);
-        uint32_t run = x - local;
-#pragma unroll
-        for (int j = 0; j < PER; j++) { s.s_cnt[lane * PER + j] = run; run += c[j]; }
-        const uint64_t e = lookback_warp(status, tile, tot, OpAdd(), 0ull);
-        if (lane == 0) { s.s_excl = e; s.s_tot = tot; }
-    }
-    __syncthreads();
-}
 
 // Run-length encoding of sorted keys: heads -> (unique key, run start), in two
 // passes with no inter-tile dependency (a decoupled look-back chain over 2048-key
@@ -187,82 +153,164 @@ __device__ __forceinline__ int64_t lower_bound_k(const KO* a, int64_t lo, int64_
     return lo;
 }
 
-// For each left unique key: find it among the right unique keys; compact the
-// common keys with (L, R, startL, startR). Grid covers n_left (an upper bound
-// of U_l); tiles past U_l exit.
+// For each left unique key: find it among the right unique keys (pass 1, no
+// inter-tile dependency: the matching right unique index or NOMATCH per left unique
+// key, and a per-tile count), then compact the common keys with (L, R, startL,
+// startR) at the scanned tile offsets (pass 2). Grid covers n_left (an upper bound
+// of U_l); tiles past U_l count zero.
 constexpr int ICAP = 4096;   // right unique keys staged in shared memory per tile
+constexpr uint32_t NOMATCH = 0xFFFFFFFFu;
+
+// tb[t] = lower_bound(right unique keys, first left unique key of tile t), all tiles
+// searched in parallel (one thread each); tb[n_tiles] = U_r.
+template <typename KO>
+__global__ void tile_bounds_kernel(const KO* __restrict__ ukl, const int64_t* U_l_p, const KO* __restrict__ ukr,
+                                   const int64_t* U_r_p, int64_t* tb, int64_t n_tiles) {
+    const int64_t U_l = *U_l_p, U_r = *U_r_p;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= n_tiles; t += (int64_t)gridDim.x * blockDim.x)
+        tb[t] = (t < n_tiles && t * JTILE < U_l) ? lower_bound_k(ukr, 0, U_r, ukl[t * JTILE]) : U_r;
+}
 
 template <typename KO>
-__global__ void __launch_bounds__(JNT) intersect_kernel(const KO* __restrict__ ukl, const uint32_t* __restrict__ usl,
-                                                        const int64_t* U_l_p, const KO* __restrict__ ukr,
-                                                        const uint32_t* __restrict__ usr, const int64_t* U_r_p,
-                                                        uint32_t* mL, uint32_t* mR, uint32_t* msL, uint32_t* msR,
-                                                        int64_t* K_out, uint64_t* status, unsigned long long* counter) {
-    __shared__ int64_t s_tile, s_rlo, s_rhi;
-    __shared__ CompactTile s;
+__global__ void __launch_bounds__(JNT) intersect_kernel(const KO* __restrict__ ukl, const int64_t* U_l_p,
+                                                        const KO* __restrict__ ukr, const int64_t* U_r_p,
+                                                        const int64_t* __restrict__ tb, uint32_t* __restrict__ pm,
+                                                        uint32_t* __restrict__ tcnt) {
+    __shared__ uint32_t s_w[JNW];
     __shared__ KO s_r[ICAP];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = take_tile(counter, &s_tile);
     const int64_t U_l = *U_l_p, U_r = *U_r_p;
-    const int64_t base = tile * JTILE;
-    if (base >= U_l) return;
-    const int64_t last = min(base + JTILE, U_l) - 1;
-    if (tid == 0) s_rlo = lower_bound_k(ukr, 0, U_r, ukl[base]);
-    if (tid == 32) s_rhi = lower_bound_k(ukr, 0, U_r, ukl[last]) + 1;
-    __syncthreads();
-    const int64_t rlo = s_rlo, rhi = min(s_rhi, U_r);
+    const int64_t base = (int64_t)blockIdx.x * JTILE;
+    if (base >= U_l) {
+        if (tid == 0) tcnt[blockIdx.x] = 0;
+        return;
+    }
+    // right unique keys <= this tile's last left key lie below tb[t + 1] + 1
+    const int64_t rlo = tb[blockIdx.x], rhi = min(tb[blockIdx.x + 1] + 1, U_r);
     // the right unique keys this tile can match: staged in shared memory if they fit
     const bool staged = rhi - rlo <= ICAP;
     if (staged) {
         for (int64_t i = rlo + tid; i < rhi; i += JNT) s_r[i - rlo] = ukr[i];
         __syncthreads();
     }
-    unsigned bal[JIPT];
-    uint32_t L[JIPT], R[JIPT], sL[JIPT], sR[JIPT];
+    // JIPT consecutive left unique keys per thread: one lower_bound for the first,
+    // then a merge walk (both lists are sorted and unique)
+    const int64_t jb = base + (int64_t)tid * JIPT;
+    uint32_t cnt = 0;
+    if (jb < U_l) {
+        KO k[JIPT];
 #pragma unroll
-    for (int i = 0; i < JIPT; i++) {
-        const int64_t j = base + i * JNT + tid;
-        bool hit = false;
-        if (j < U_l) {
-            const KO k = ukl[j];
-            int64_t p;
-            bool eq;
-            if (staged) {
-                int64_t lo = 0, hi = rhi - rlo;
-                while (lo < hi) {
-                    const int64_t mid = (lo + hi) >> 1;
-                    if (s_r[mid] < k) lo = mid + 1; else hi = mid;
-                }
-                eq = lo < rhi - rlo && s_r[lo] == k;
-                p = lo + rlo;
-            } else {
-                p = lower_bound_k(ukr, rlo, rhi, k);
-                eq = p < rhi && ukr[p] == k;
+        for (int i = 0; i < JIPT; i++) k[i] = jb + i < U_l ? ukl[jb + i] : KO(0);
+        uint32_t out[JIPT];
+        if (staged) {
+            const int64_t nr = rhi - rlo;
+            int64_t lo = 0, hi = nr;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (s_r[mid] < k[0]) lo = mid + 1; else hi = mid;
             }
-            if (eq) {
-                hit = true;
-                sL[i] = usl[j];
-                L[i] = usl[j + 1] - usl[j];
-                sR[i] = usr[p];
-                R[i] = usr[p + 1] - usr[p];
+#pragma unroll
+            for (int i = 0; i < JIPT; i++) {
+                while (lo < nr && s_r[lo] < k[i]) lo++;
+                const bool eq = jb + i < U_l && lo < nr && s_r[lo] == k[i];
+                out[i] = eq ? (uint32_t)(lo + rlo) : NOMATCH;
+                cnt += eq;
+            }
+        } else {
+            int64_t pos = lower_bound_k(ukr, rlo, rhi, k[0]);
+#pragma unroll
+            for (int i = 0; i < JIPT; i++) {
+                if (i > 0) pos = lower_bound_k(ukr, pos, rhi, k[i]);
+                const bool eq = jb + i < U_l && pos < rhi && ukr[pos] == k[i];
+                out[i] = eq ? (uint32_t)pos : NOMATCH;
+                cnt += eq;
             }
         }
-        bal[i] = __ballot_sync(0xffffffffu, hit);
+#pragma unroll
+        for (int i = 0; i < JIPT; i++)
+            if (jb + i < U_l) pm[jb + i] = out[i];
     }
-    compact_scan(s, bal, tile, status);
-    const int64_t excl = (int64_t)s.s_excl;
-    const unsigned lt = lanemask_lt();
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < JNW; w++) t += s_w[w];
+        tcnt[blockIdx.x] = t;
+    }
+}
+
+// pass 2: common keys in left-key order -> (L, R, startL, startR). Each thread owns
+// JIPT consecutive left unique keys (16-byte loads of pm and of the run starts);
+// the right run starts are gathered with all loads issued up front; outputs are
+// staged in shared memory and written coalesced.
+__global__ void __launch_bounds__(JNT) common_kernel(const uint32_t* __restrict__ pm, const uint32_t* __restrict__ usl,
+                                                     const uint32_t* __restrict__ usr, const int64_t* U_l_p,
+                                                     const uint32_t* __restrict__ toff, uint32_t* mL, uint32_t* mR,
+                                                     uint32_t* msL, uint32_t* msR, int64_t* K_out, int64_t n_tiles) {
+    __shared__ uint32_t s_w[JNW];
+    __shared__ uint32_t s_o[4][JTILE];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t U_l = *U_l_p;
+    const int64_t base = (int64_t)blockIdx.x * JTILE;
+    if (blockIdx.x == n_tiles - 1 && tid == 0) *K_out = toff[n_tiles];
+    const uint32_t t0 = toff[blockIdx.x];
+    const uint32_t tot = toff[blockIdx.x + 1] - t0;
+    if (base >= U_l || tot == 0) return;
+    const int64_t r0 = base + (int64_t)tid * JIPT;   // JIPT consecutive left unique keys per thread
+    uint32_t p[JIPT], ul[JIPT + 1];
+    if (r0 + JIPT <= U_l) {
+        const uint4 a0 = __ldcs(reinterpret_cast<const uint4*>(pm + r0));
+        const uint4 a1 = __ldcs(reinterpret_cast<const uint4*>(pm + r0) + 1);
+        p[0] = a0.x; p[1] = a0.y; p[2] = a0.z; p[3] = a0.w; p[4] = a1.x; p[5] = a1.y; p[6] = a1.z; p[7] = a1.w;
+        const uint4 b0 = __ldg(reinterpret_cast<const uint4*>(usl + r0));
+        const uint4 b1 = __ldg(reinterpret_cast<const uint4*>(usl + r0) + 1);
+        ul[0] = b0.x; ul[1] = b0.y; ul[2] = b0.z; ul[3] = b0.w; ul[4] = b1.x; ul[5] = b1.y; ul[6] = b1.z; ul[7] = b1.w;
+        ul[8] = usl[r0 + JIPT];
+    } else {
+#pragma unroll
+        for (int i = 0; i < JIPT; i++) {
+            p[i] = r0 + i < U_l ? pm[r0 + i] : NOMATCH;
+            ul[i] = r0 + i <= U_l ? usl[r0 + i] : 0u;
+        }
+        ul[JIPT] = r0 + JIPT <= U_l ? usl[r0 + JIPT] : 0u;
+    }
+    uint32_t ur0[JIPT], ur1[JIPT], cnt = 0;
+#pragma unroll
+    for (int i = 0; i < JIPT; i++) {   // right run start and end of every match, loads in flight together
+        const bool hit = p[i] != NOMATCH;
+        ur0[i] = hit ? __ldg(usr + p[i]) : 0u;
+        ur1[i] = hit ? __ldg(usr + p[i] + 1) : 0u;
+        cnt += hit;
+    }
+    uint32_t x = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t m = x - cnt;
+#pragma unroll
+    for (int w = 0; w < JNW; w++)
+        if (w < warp) m += s_w[w];
 #pragma unroll
     for (int i = 0; i < JIPT; i++) {
-        if (bal[i] & (1u << lane)) {
-            const int64_t m = excl + s.s_cnt[i * JNW + warp] + __popc(bal[i] & lt);
-            mL[m] = L[i];
-            mR[m] = R[i];
-            msL[m] = sL[i];
-            msR[m] = sR[i];
-        }
+        if (p[i] == NOMATCH) continue;
+        s_o[0][m] = ul[i + 1] - ul[i];
+        s_o[1][m] = ur1[i] - ur0[i];
+        s_o[2][m] = ul[i];
+        s_o[3][m] = ur0[i];
+        m++;
     }
-    if (tid == 0 && last == U_l - 1) *K_out = excl + s.s_tot;
+    __syncthreads();
+    for (uint32_t k = tid; k < tot; k += JNT) {
+        mL[t0 + k] = s_o[0][k];
+        mR[t0 + k] = s_o[1][k];
+        msL[t0 + k] = s_o[2][k];
+        msR[t0 + k] = s_o[3][k];
+    }
 }
 
 // cumHistMul = inclusive scan of histMul = L*R over the K common keys.
@@ -421,13 +469,18 @@ void rle_intersect(tqp_ctx* ctx, tqp_smj_plan* P, SortOut& sl, SortOut& sr, int6
     side(sl, nl, ukl, usl, scal + 0);
     side(sr, nr, ukr, usr, scal + 1);
     const int64_t tiles = ceil_div(nl, JTILE);
-    DevBuf<uint64_t> status(ctx, tiles);
-    DevBuf<unsigned long long> counter(ctx, 1);
-    status.zero();
-    counter.zero();
-    launch(ctx, "tqp_smj_intersect", intersect_kernel<KO>, dim3((unsigned)tiles), dim3(JNT), 0, ukl.get(), usl.get(),
-           scal + 0, ukr.get(), usr.get(), scal + 1, P->mL.get(), P->mR.get(), P->msL.get(), P->msR.get(), scal + 2,
-           status.get(), counter.get());
+    DevBuf<uint32_t> pm(ctx, nl), tcnt(ctx, tiles), toff(ctx, tiles + 1);
+    DevBuf<int64_t> tb(ctx, tiles + 1);
+    launch(ctx, "tqp_smj_intersect", tile_bounds_kernel<KO>, dim3((unsigned)ceil_div(tiles + 1, 128)), dim3(128), 0,
+           (const KO*)ukl.get(), (const int64_t*)(scal + 0), (const KO*)ukr.get(), (const int64_t*)(scal + 1), tb.get(),
+           tiles);
+    launch(ctx, "tqp_smj_intersect", intersect_kernel<KO>, dim3((unsigned)tiles), dim3(JNT), 0, (const KO*)ukl.get(),
+           (const int64_t*)(scal + 0), (const KO*)ukr.get(), (const int64_t*)(scal + 1), (const int64_t*)tb.get(),
+           pm.get(), tcnt.get());
+    scan_add_u32_exclusive(ctx, tcnt.get(), toff.get(), tiles);
+    launch(ctx, "tqp_smj_intersect", common_kernel, dim3((unsigned)tiles), dim3(JNT), 0, (const uint32_t*)pm.get(),
+           (const uint32_t*)usl.get(), (const uint32_t*)usr.get(), (const int64_t*)(scal + 0),
+           (const uint32_t*)toff.get(), P->mL.get(), P->mR.get(), P->msL.get(), P->msR.get(), scal + 2, tiles);
 }
 }  // namespace
 
