@@ -360,17 +360,17 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
             rk[i] = b + (rk[i] >> 24);
         }
         __syncthreads();
-        {   // per digit: exclusive prefix over warps; tile-local digit starts (thread owns BPT digits)
-            uint32_t cnt[BPT], local = 0;
+        {   // per digit: tile-local digit start + exclusive prefix over warps, folded into
+            // whist[w][d] (thread owns BPT digits); gdelta[d] = global - tile digit start
+            uint32_t c[BPT][NW], cnt[BPT], local = 0;
 #pragma unroll
             for (int j = 0; j < BPT; j++) {
                 const int d = tid * BPT + j;
                 uint32_t run = 0;
 #pragma unroll
                 for (int w = 0; w < NW; w++) {
-                    const uint32_t c = s.u.whist[w][d];
-                    s.u.whist[w][d] = run;
-                    run += c;
+                    c[j][w] = s.u.whist[w][d];
+                    run += c[j][w];
                 }
                 cnt[j] = run;
                 local += run;
@@ -378,7 +378,14 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
             uint32_t ex = block_excl_scan256(local, s.w);
 #pragma unroll
             for (int j = 0; j < BPT; j++) {
-                s.tstart[tid * BPT + j] = ex;
+                const int d = tid * BPT + j;
+                s.tstart[d] = ex;
+                uint32_t run = ex;
+#pragma unroll
+                for (int w = 0; w < NW; w++) {
+                    s.u.whist[w][d] = run;
+                    run += c[j][w];
+                }
                 ex += cnt[j];
             }
         }
@@ -387,7 +394,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         for (int i = 0; i < IPT; i++) {
             if (base + warp * 32 * IPT + i * 32 + lane < a.n) {
                 const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
-                rk[i] = s.tstart[d] + s.u.whist[warp][d] + rk[i];
+                rk[i] = s.u.whist[warp][d] + rk[i];
             }
         }
         __syncthreads();
@@ -399,14 +406,14 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
             }
         }
 #pragma unroll
-        for (int j = 0; j < BPT; j++) s.gstart[tid + j * NT] = gs[j];
+        for (int j = 0; j < BPT; j++) s.gstart[tid + j * NT] = gs[j] - s.tstart[tid + j * NT];   // global - tile start
         __syncthreads();
         const int tile_n = (int)min((int64_t)TILE, a.n - base);
         for (int j = tid; j < tile_n; j += NT) {
             const KT kk = s.u.sorted.keys[j];
             const uint32_t p = s.u.sorted.perm[j];
             const uint32_t d = (uint32_t)(kk >> a.shift) & DM;
-            const int64_t dst = (int64_t)s.gstart[d] + (j - (int64_t)s.tstart[d]);
+            const int64_t dst = (int64_t)(uint32_t)(s.gstart[d] + (uint32_t)j);   // gdelta[d] + j (mod 2^32, n < 2^30)
             if (a.out_keys) ((KT*)a.out_keys)[dst] = kk;
             if (a.out_perm) a.out_perm[dst] = p;
             if (a.out_perm64) a.out_perm64[dst] = (int64_t)p;
