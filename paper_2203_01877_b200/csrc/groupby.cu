@@ -71,6 +71,7 @@ struct Phase1Args {
     int dense_bits;               // SUM pairs: |value| <= 2^dense_bits keeps per-thread int64 sums exact
     int poff[PCH][3];             // stage byte offset of each factor's column
     int pdtf[PCH][3];             // and its dtype
+    int pext[PCH];                // leading factors shared with the previous pair (its whole list), else 0
     int n_pairs;
     int prop[TQP_MAX_AGGS];
     int pnf[TQP_MAX_AGGS];
@@ -955,7 +956,12 @@ __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem
             const int64_t row0 = t * TR;
             const int nrows = (int)min((int64_t)TR, a.n - row0);
             for (int c = 0; c < a.n_ucols; c++) {
-                for (int r = tid; r < nrows; r += NT) {
+                for (int r = tid; r < TR; r += NT) {   // rows past the end are zero-filled
+                    if (r >= nrows) {
+                        const uint32_t es = a.udt[c] == TQP_U8 ? 1 : a.udt[c] == TQP_I32 ? 4 : 8;
+                        for (uint32_t b = 0; b < es; b++) stage_ptr(s)[a.uoff[c] + r * es + b] = 0;
+                        continue;
+                    }
                     switch (a.udt[c]) {
                         case TQP_U8: stage_ptr(s)[a.uoff[c] + r] = ((const uint8_t*)a.ucol[c])[row0 + r]; break;
                         case TQP_I32:
@@ -1217,12 +1223,17 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     for (int i = 0; i < GPT; i++)
         if (pass[i]) cnt[id[i] * NT + tid]++;
     const int np = a.n_pairs;
+    int64_t vprev[GPT] = {1, 1, 1, 1};
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
         if (jj >= np) break;
-        int64_t vv[GPT] = {1, 1, 1, 1};
+        const int fx = a.pext[jj];   // factors already multiplied into the previous pair's value
+        int64_t vv[GPT];
+#pragma unroll
+        for (int i = 0; i < GPT; i++) vv[i] = fx ? vprev[i] : 1;
 #pragma unroll
         for (int f = 0; f < 3; f++) {
+            if (f < fx) continue;
             if (f >= a.pnf[jj]) break;
             int64_t x[GPT];
             load4(st + a.poff[jj][f], a.pdtf[jj][f], tid, x);
@@ -1232,11 +1243,13 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
 #pragma unroll
             for (int i = 0; i < GPT; i++) {
                 const int64_t tt = (int64_t)(neg ? add - (uint64_t)x[i] : add + (uint64_t)x[i]);   // mod 2^64
-                if (pass[i]) m2 |= (uint64_t)(tt ^ (tt >> 63));
+                m2 |= (uint64_t)(tt ^ (tt >> 63));   // every staged row (tail rows are zero-filled)
                 vv[i] = f == 0 ? tt : (int64_t)((uint64_t)vv[i] * (uint64_t)tt);                  // mod 2^64
             }
             mt[jj][f] = m2;
         }
+#pragma unroll
+        for (int i = 0; i < GPT; i++) vprev[i] = vv[i];
         const int op = a.prop[jj];
 #pragma unroll
         for (int i = 0; i < GPT; i++) {
@@ -1287,8 +1300,10 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
         if (jj >= np) break;
         int bs = 0;
 #pragma unroll
-        for (int f = 0; f < 3; f++)
+        for (int f = 0; f < 3; f++) {
+            if (jj > 0 && f < a.pext[jj]) mt[jj][f] = mt[jj - 1][f];   // reused factor: its bound
             if (f < a.pnf[jj]) bs += 64 - __clzll(mt[jj][f]);
+        }
         bad |= bs > (a.prop[jj] == P_SUM ? a.dense_bits : 62);
     }
     if (bad) h.bad = 1;
@@ -1679,6 +1694,38 @@ void make_pairs(tqp_groupby_plan* PL, const tqp_agg* aggs, int n_aggs, int (*pf)
         }
         PL->apair[g] = found;
     }
+    // order pairs by their factor lists (lexicographic, a prefix first), so that an
+    // expression extending the previous pair's (Q1: price, price*(1-disc),
+    // price*(1-disc)*(1+tax)) can reuse its value (dense path)
+    const int np = PL->n_pairs;
+    int ord[TQP_MAX_AGGS];
+    for (int j = 0; j < np; j++) ord[j] = j;
+    auto less = [&](int x, int y) {
+        for (int f = 0; f < 3; f++) {
+            if (f >= pnf[x] || f >= pnf[y]) return pnf[x] < pnf[y] || (pnf[x] == pnf[y] && PL->pop[x] < PL->pop[y]);
+            if (pf[x][f] != pf[y][f]) return pf[x][f] < pf[y][f];
+            if (ps[x][f] != ps[y][f]) return ps[x][f] < ps[y][f];
+            if (pa[x][f] != pa[y][f]) return pa[x][f] < pa[y][f];
+        }
+        return pnf[x] == pnf[y] && PL->pop[x] < PL->pop[y];
+    };
+    std::stable_sort(ord, ord + np, less);
+    int inv[TQP_MAX_AGGS], pop2[TQP_MAX_AGGS], pnf2[TQP_MAX_AGGS], pf2[TQP_MAX_AGGS][3], ps2[TQP_MAX_AGGS][3];
+    int64_t pa2[TQP_MAX_AGGS][3];
+    for (int j = 0; j < np; j++) {
+        const int o = ord[j];
+        inv[o] = j;
+        pop2[j] = PL->pop[o];
+        pnf2[j] = pnf[o];
+        for (int f = 0; f < 3; f++) { pf2[j][f] = pf[o][f]; ps2[j][f] = ps[o][f]; pa2[j][f] = pa[o][f]; }
+    }
+    for (int j = 0; j < np; j++) {
+        PL->pop[j] = pop2[j];
+        pnf[j] = pnf2[j];
+        for (int f = 0; f < 3; f++) { pf[j][f] = pf2[j][f]; ps[j][f] = ps2[j][f]; pa[j][f] = pa2[j][f]; }
+    }
+    for (int g = 0; g < n_aggs; g++)
+        if (PL->apair[g] >= 0) PL->apair[g] = inv[PL->apair[g]];
 }
 }  // namespace
 
@@ -1761,11 +1808,16 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         a.bulk_ok = (aligned && a.n_ucols > 0) ? 1 : 0;
         const int64_t tiles = ceil_div(n, GTILE);
         a.n_tiles = tiles;
-        for (int j = 0; j < PL->n_pairs && j < PCH; j++)
+        for (int j = 0; j < PL->n_pairs && j < PCH; j++) {
             for (int f = 0; f < pnf[j]; f++) {
                 a.poff[j][f] = a.uoff[a.pfc[j][f]];
                 a.pdtf[j][f] = a.udt[a.pfc[j][f]];
             }
+            bool pre = j > 0 && pnf[j - 1] > 0 && pnf[j - 1] <= pnf[j];
+            for (int f = 0; pre && f < pnf[j - 1]; f++)
+                pre = pf[j - 1][f] == pf[j][f] && ps[j - 1][f] == ps[j][f] && pa[j - 1][f] == pa[j][f];
+            a.pext[j] = pre ? pnf[j - 1] : 0;
+        }
 
         // ---- dense small-domain path (gb_dense_kernel): presence pass + dense ids
         DevBuf<uint8_t> dtab;
