@@ -100,10 +100,12 @@ __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint3
         const uint32_t low = (uint32_t)rel & a.lowmask;
         const uint32_t target = low << a.pbits;
         const uint32_t end = hi;
-        const uint32_t s0 = lo & ~7u;   // the bucket's records from one aligned 64-byte fetch
+        const uint32_t s0 = lo & ~7u;   // the bucket's records from the aligned 32-byte sector(s) holding it
         if (hi <= s0 + 16u) {
             const uint4* p4 = reinterpret_cast<const uint4*>(a.rec + s0);
-            const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1), q2 = __ldg(p4 + 2), q3 = __ldg(p4 + 3);
+            const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1);
+            uint4 q2 = make_uint4(0, 0, 0, 0), q3 = q2;
+            if (hi > s0 + 8u) { q2 = __ldg(p4 + 2); q3 = __ldg(p4 + 3); }   // second sector only when needed
             const uint32_t r16[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
                                       q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
             bool hit = false;
