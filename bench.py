@@ -479,7 +479,9 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="tqp", choices=["tqp", "reference"])
+    # tqp: this library; reference: the oracle on host cores (the driver's reference arm);
+    # paper-torch: the paper's tensor programs as torch ops on the same GPU (comparison only)
+    ap.add_argument("--impl", default="tqp", choices=["tqp", "reference", "paper-torch"])
     ap.add_argument("--layout", default="shuffled", choices=["shuffled", "clustered"])
     ap.add_argument("--cpu-sample-sf", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -488,6 +490,11 @@ def main():
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args)
+    if args.impl == "paper-torch":
+        sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), "tools"))
+        import paper_torch
+        print(json.dumps(paper_torch.run(max(args.steps, 1), max(args.warmup, 1), check=True)))
+        return 0
     run_gpu(args)
     return 0
 
