@@ -119,6 +119,16 @@ tqp_status tqp_pkfk_join(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_
 tqp_status tqp_pkfk_semi(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
                          int anti, uint8_t* match_out, int64_t* sel_out, int64_t* n_sel_host);
 
+/* Probe-side outer join (the PK-FK match mask of
+ * PAPER.md:81 kept for every row): every probe row i in order gets
+ * left_out[i] = its build row, or -1 without a match (n_probe x int64,
+ * caller-allocated, required); the right index of row i is i itself.
+ * match_out (nullable, n_probe x u8) = 1 iff matched; *n_match_host (nullable)
+ * = matched rows. Duplicate build keys are not checked (each probe row takes
+ * one of the equal build rows). Synchronises twice. */
+tqp_status tqp_pkfk_outer(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
+                          int64_t* left_out, uint8_t* match_out, int64_t* n_match_host);
+
 /* ------------------------------------------------ m:n sort-merge join */
 /* (3) Generic sort-merge join -- Alg. 1 (prose :1114-1137)
  * with readings R2 (ascending sort), R3 (bucketize right=True),

@@ -35,7 +35,7 @@ MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
 EXPORTED = [
     "tqp_abi_version", "tqp_ctx_create", "tqp_ctx_destroy", "tqp_ctx_set_stream", "tqp_last_error",
     "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_kernel_stats",
-    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
+    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
     "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge",
 ]
@@ -70,6 +70,7 @@ _sig = {
     "tqp_sort": ([_vp, Col, _i64, _int, _vp, _vp], _int),
     "tqp_pkfk_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_semi": ([_vp, Col, _i64, Col, _i64, _int, _vp, _vp, _P(_i64)], _int),
+    "tqp_pkfk_outer": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_smj_prepare": ([_vp, Col, _i64, Col, _i64, _P(_vp), _P(_i64)], _int),
     "tqp_smj_expand": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "tqp_smj_release": ([_vp, _vp], None),
@@ -223,6 +224,18 @@ class Context:
         self._check(_lib.tqp_pkfk_semi(self._h, _col(b), b.numel(), _col(p), p.numel(), int(bool(anti)),
                                        _ptr(mask), _ptr(sel), ctypes.byref(m)))
         return (sel[:m.value], mask) if return_mask else sel[:m.value]
+
+    def pkfk_outer(self, build_keys, probe_keys, return_mask=False):
+        """Probe-side outer join: build row per probe row (-1 = no match), probe rows in order."""
+        self._sync_stream()
+        b = _dev_tensor(build_keys, self.device)
+        p = _dev_tensor(probe_keys, self.device)
+        left = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        mask = torch.empty(p.numel(), dtype=torch.uint8, device=self.device) if return_mask else None
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_pkfk_outer(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(left), _ptr(mask),
+                                        ctypes.byref(m)))
+        return (left, mask) if return_mask else left
 
     def smj_prepare(self, left, right):
         """Alg. 1 lines 1-9: sort, histograms, products, prefix sums -> SmjPlan (size known)."""
@@ -414,6 +427,10 @@ def smj_prepare(left, right):
 
 def smj_join(left, right):
     return context().smj_join(left, right)
+
+
+def pkfk_outer(build_keys, probe_keys, return_mask=False):
+    return context().pkfk_outer(build_keys, probe_keys, return_mask)
 
 
 def filter_compact(cols, preds, mask=True, sel=True):

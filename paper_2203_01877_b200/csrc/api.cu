@@ -8,6 +8,7 @@
 namespace tqp {
 void pkfk_join(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void pkfk_semi(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int, uint8_t*, int64_t*, int64_t*);
+void pkfk_outer(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, uint8_t*, int64_t*);
 void filter_compact(tqp_ctx*, const tqp_col*, int, int64_t, const tqp_pred*, int, uint8_t*, int64_t*, int64_t*);
 tqp_smj_plan* smj_prepare(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*);
 void smj_expand(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, int64_t*, int64_t*);
@@ -214,6 +215,11 @@ tqp_status tqp_pkfk_join(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t n
 tqp_status tqp_pkfk_semi(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int anti, uint8_t* match_out,
                          int64_t* sel_out, int64_t* n_sel_host) {
     TQP_GUARD(c, { tqp::pkfk_semi(c, b, nb, p, np, anti, match_out, sel_out, n_sel_host); });
+}
+
+tqp_status tqp_pkfk_outer(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int64_t* left_out,
+                          uint8_t* match_out, int64_t* n_match_host) {
+    TQP_GUARD(c, { tqp::pkfk_outer(c, b, nb, p, np, left_out, match_out, n_match_host); });
 }
 
 tqp_status tqp_smj_prepare(tqp_ctx* c, tqp_col l, int64_t nl, tqp_col r, int64_t nr, tqp_smj_plan** plan,

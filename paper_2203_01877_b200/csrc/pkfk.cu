@@ -71,9 +71,10 @@ struct ProbeArgs {
     int vbits;                // (k - base) must be < 2^vbits
     uint64_t hi_bits;         // k32: required high 32 bits of u
     int shift;
-    int mode;                 // 0 = join pairs, 1 = semi/anti
+    int mode;                 // 0 = join pairs, 1 = semi/anti, 2 = probe-side outer join
     int anti;
     uint32_t* lft;            // join: per probe row, the build row or NOMATCH
+    int64_t* left64;          // outer: per probe row, the build row or -1
     uint8_t* mask;            // semi: per probe row, 1 = the key is on the build side
     uint32_t* tcnt;           // per tile: rows selected (join: matches; semi: match != anti)
 };
@@ -171,6 +172,10 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
         if (row >= a.n_probe) continue;
         if (a.mode == 0) {
             __stcs(a.lft + row, m[i] ? left[i] : NOMATCH);
+            cnt += m[i];
+        } else if (a.mode == 2) {
+            __stcs((long long*)a.left64 + row, m[i] ? (long long)left[i] : -1ll);
+            if (a.mask) a.mask[row] = (uint8_t)m[i];
             cnt += m[i];
         } else {
             a.mask[row] = (uint8_t)m[i];
@@ -350,7 +355,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         DevBuf<uint32_t> lft;
         DevBuf<uint8_t> tmask;
         if (mode == 0) lft.alloc(ctx, np);
-        else if (!match_out) tmask.alloc(ctx, np);
+        else if (mode == 1 && !match_out) tmask.alloc(ctx, np);
         ProbeArgs a{};
         a.probe = pk.data;
         a.n_probe = np;
@@ -367,6 +372,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         a.mode = mode;
         a.anti = anti;
         a.lft = lft.get();
+        a.left64 = left_out;
         a.mask = match_out ? match_out : tmask.get();
         a.tcnt = tcnt.get();
         auto go = [&](auto kt, auto pk_) {
@@ -387,10 +393,14 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         if (mode == 0)
             launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)lft.get(),
                    (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out);
-        else if (right_out)
+        else if (mode == 1 && right_out)
             launch(ctx, "tqp_pkfk_emit", emit_kernel<false>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)nullptr,
                    (const uint8_t*)a.mask, anti, np, (const uint64_t*)toff.get(), (int64_t*)nullptr, right_out);
         TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else if (np > 0 && mode == 2) {
+        // empty build side: no probe row matches
+        TQP_CUDA(cudaMemsetAsync(left_out, 0xFF, (size_t)np * 8, ctx->stream));
+        if (match_out) TQP_CUDA(cudaMemsetAsync(match_out, 0, np, ctx->stream));
     } else if (np > 0 && mode == 1) {
         // empty build side: nothing matches
         if (match_out) TQP_CUDA(cudaMemsetAsync(match_out, 0, np, ctx->stream));
@@ -407,8 +417,10 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
     if (h[1] && mode == 0) fail(TQP_ERR_DUPLICATE_BUILD_KEY, "pkfk: duplicate key on the build side");
     if (n_out_host) *n_out_host = h[0];
     if (np > 0 && nb > 0) {   // probe keys in; pairs (join) or mask + selection vector (semi) out
-        ctx->add_bytes("tqp_pkfk_probe", (double)np * dtype_size(pk.dtype) + (mode == 1 && match_out ? (double)np : 0.0));
-        ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? 16.0 * (double)h[0] : (right_out ? 8.0 * (double)h[0] : 0.0));
+        ctx->add_bytes("tqp_pkfk_probe", (double)np * dtype_size(pk.dtype) + (mode != 0 && match_out ? (double)np : 0.0) +
+                                             (mode == 2 ? 8.0 * (double)np : 0.0));
+        if (mode != 2)
+            ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? 16.0 * (double)h[0] : (right_out ? 8.0 * (double)h[0] : 0.0));
     }
 }
 }  // namespace
@@ -431,6 +443,22 @@ void pkfk_semi(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int
     Built B;
     build_side(ctx, bk, nb, B);
     run_probe(ctx, B, pk, np, 1, anti, nullptr, sel_out, match_out, n_sel_host);
+}
+
+// Probe-side outer join ("outer = inner pairs + unmatched rows
+// with a match-flag column"): every probe row in order, left_out[i] = its build row or
+// -1; match_out (nullable) = 1 iff matched; *n_match_host (nullable) = matched rows.
+void pkfk_outer(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int64_t* left_out, uint8_t* match_out,
+                int64_t* n_match_host) {
+    check_col(bk, nb, "outer build");
+    check_col(pk, np, "outer probe");
+    if (np > 0 && !left_out) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_outer: null left_out");
+    if (np >= (int64_t(1) << 40)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_outer: probe too large");
+    Built B;
+    build_side(ctx, bk, nb, B);
+    int64_t m = 0;
+    run_probe(ctx, B, pk, np, 2, 0, left_out, nullptr, match_out, &m);
+    if (n_match_host) *n_match_host = m;
 }
 
 }  // namespace tqp

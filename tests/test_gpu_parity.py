@@ -168,6 +168,20 @@ def test_pkfk_semi_anti(T, anti):
     assert np.array_equal(np.nonzero(member)[0], r)
 
 
+@pytest.mark.parametrize("nb,np_,span", [(0, 1000, 50), (1, 5, 3), (3000, 50_001, 6000), (300_000, 1_000_003, 10**6)])
+def test_pkfk_outer(T, nb, np_, span):
+    """Probe-side outer join: every probe row, its build row or -1 (oracle pairs fill the rest)."""
+    rng = np.random.default_rng(nb + 7)
+    build = (rng.permutation(span)[:nb] - span // 4).astype(np.int64)
+    probe = rng.integers(-span // 2, span, np_).astype(np.int64)
+    left, mask = T.pkfk_outer(cu(build), cu(probe), return_mask=True)
+    olo, oro = oracle.pkfk_join(build, probe)
+    want = np.full(np_, -1, np.int64)
+    want[oro] = olo
+    assert np.array_equal(npy(left), want)
+    assert np.array_equal(npy(mask).astype(bool), want >= 0)
+
+
 def test_pkfk_semi_empty_build(T):
     sel = T.pkfk_semi(cu(np.array([], np.int64)), cu(np.arange(10)), anti=True)
     assert npy(sel).tolist() == list(range(10))
