@@ -119,6 +119,21 @@ tqp_status tqp_pkfk_join(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_
 tqp_status tqp_pkfk_semi(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
                          int anti, uint8_t* match_out, int64_t* sel_out, int64_t* n_sel_host);
 
+/* PK-FK join with payload materialisation fused into the output (SURVEY.md
+ * §8(f) NEXT 2: the paper's GenerateOutput / createOutput, PAPER.md:89, :333,
+ * gathering payload columns by the index pairs). Same rows and order as
+ * tqp_pkfk_join; for each j < *n_out_host:
+ *   build_payload_out[c][j] = build_payload[c][left_j]   (n_build rows each)
+ *   probe_payload_out[c][j] = probe_payload[c][right_j]  (n_probe rows each)
+ * Outputs have the payload column's dtype and capacity n_probe (caller-allocated
+ * device buffers; host arrays of pointers). At most 8 payload columns per side.
+ * left_out_idx / right_out_idx are nullable here. Synchronises twice. */
+tqp_status tqp_pkfk_join_payload(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys,
+                                 int64_t n_probe, const tqp_col* build_payload_host, int n_build_payload,
+                                 void* const* build_payload_out_host, const tqp_col* probe_payload_host,
+                                 int n_probe_payload, void* const* probe_payload_out_host, int64_t* left_out_idx,
+                                 int64_t* right_out_idx, int64_t* n_out_host);
+
 /* Probe-side outer join (the PK-FK match mask of
  * PAPER.md:81 kept for every row): every probe row i in order gets
  * left_out[i] = its build row, or -1 without a match (n_probe x int64,

@@ -35,7 +35,7 @@ MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
 EXPORTED = [
     "tqp_abi_version", "tqp_ctx_create", "tqp_ctx_destroy", "tqp_ctx_set_stream", "tqp_last_error",
     "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_kernel_stats",
-    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
+    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
     "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge",
 ]
@@ -71,6 +71,8 @@ _sig = {
     "tqp_pkfk_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_semi": ([_vp, Col, _i64, Col, _i64, _int, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_outer": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
+    "tqp_pkfk_join_payload": ([_vp, Col, _i64, Col, _i64, _P(Col), _int, _P(_vp), _P(Col), _int, _P(_vp), _vp, _vp,
+                               _P(_i64)], _int),
     "tqp_smj_prepare": ([_vp, Col, _i64, Col, _i64, _P(_vp), _P(_i64)], _int),
     "tqp_smj_expand": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "tqp_smj_release": ([_vp, _vp], None),
@@ -224,6 +226,29 @@ class Context:
         self._check(_lib.tqp_pkfk_semi(self._h, _col(b), b.numel(), _col(p), p.numel(), int(bool(anti)),
                                        _ptr(mask), _ptr(sel), ctypes.byref(m)))
         return (sel[:m.value], mask) if return_mask else sel[:m.value]
+
+    def pkfk_join_payload(self, build_keys, probe_keys, build_payload=(), probe_payload=(), indices=True):
+        """PK-FK join with payload columns gathered into the output (GenerateOutput fused).
+        Returns (build payload outputs, probe payload outputs, (left, right) or None)."""
+        self._sync_stream()
+        b = _dev_tensor(build_keys, self.device)
+        p = _dev_tensor(probe_keys, self.device)
+        bps = [_dev_tensor(c, self.device) for c in build_payload]
+        pps = [_dev_tensor(c, self.device) for c in probe_payload]
+        np_ = p.numel()
+        bouts = [torch.empty(np_, dtype=c.dtype, device=self.device) for c in bps]
+        pouts = [torch.empty(np_, dtype=c.dtype, device=self.device) for c in pps]
+        lo = torch.empty(np_, dtype=torch.int64, device=self.device) if indices else None
+        ro = torch.empty(np_, dtype=torch.int64, device=self.device) if indices else None
+        ba = (Col * max(len(bps), 1))(*[_col(c) for c in bps])
+        pa = (Col * max(len(pps), 1))(*[_col(c) for c in pps])
+        bo = (_vp * max(len(bouts), 1))(*[t.data_ptr() for t in bouts])
+        po = (_vp * max(len(pouts), 1))(*[t.data_ptr() for t in pouts])
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_pkfk_join_payload(self._h, _col(b), b.numel(), _col(p), np_, ba, len(bps), bo, pa,
+                                               len(pps), po, _ptr(lo), _ptr(ro), ctypes.byref(m)))
+        n = m.value
+        return ([t[:n] for t in bouts], [t[:n] for t in pouts], (lo[:n], ro[:n]) if indices else None)
 
     def pkfk_outer(self, build_keys, probe_keys, return_mask=False):
         """Probe-side outer join: build row per probe row (-1 = no match), probe rows in order."""
@@ -427,6 +452,10 @@ def smj_prepare(left, right):
 
 def smj_join(left, right):
     return context().smj_join(left, right)
+
+
+def pkfk_join_payload(build_keys, probe_keys, build_payload=(), probe_payload=(), indices=True):
+    return context().pkfk_join_payload(build_keys, probe_keys, build_payload, probe_payload, indices)
 
 
 def pkfk_outer(build_keys, probe_keys, return_mask=False):

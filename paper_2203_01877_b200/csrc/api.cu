@@ -9,6 +9,8 @@ namespace tqp {
 void pkfk_join(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void pkfk_semi(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int, uint8_t*, int64_t*, int64_t*);
 void pkfk_outer(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, uint8_t*, int64_t*);
+void pkfk_join_payload(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, const tqp_col*, int, void* const*, const tqp_col*, int,
+                       void* const*, int64_t*, int64_t*, int64_t*);
 void filter_compact(tqp_ctx*, const tqp_col*, int, int64_t, const tqp_pred*, int, uint8_t*, int64_t*, int64_t*);
 tqp_smj_plan* smj_prepare(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*);
 void smj_expand(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, int64_t*, int64_t*);
@@ -215,6 +217,17 @@ tqp_status tqp_pkfk_join(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t n
 tqp_status tqp_pkfk_semi(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int anti, uint8_t* match_out,
                          int64_t* sel_out, int64_t* n_sel_host) {
     TQP_GUARD(c, { tqp::pkfk_semi(c, b, nb, p, np, anti, match_out, sel_out, n_sel_host); });
+}
+
+tqp_status tqp_pkfk_join_payload(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, const tqp_col* bp, int n_bp,
+                                 void* const* bp_out, const tqp_col* pp, int n_pp, void* const* pp_out, int64_t* lo,
+                                 int64_t* ro, int64_t* n_out_host) {
+    TQP_GUARD(c, {
+        if (!n_out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null n_out_host");
+        if ((n_bp > 0 && (!bp || !bp_out)) || (n_pp > 0 && (!pp || !pp_out)))
+            tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null payload arrays");
+        tqp::pkfk_join_payload(c, b, nb, p, np, bp, n_bp, bp_out, pp, n_pp, pp_out, lo, ro, n_out_host);
+    });
 }
 
 tqp_status tqp_pkfk_outer(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int64_t* left_out,

@@ -192,6 +192,27 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
     }
 }
 
+// Payload columns gathered into the join output by the emit pass (SURVEY §8(f) NEXT 2:
+// GenerateOutput / createOutput of PAPER.md:89, :333 fused with the compaction).
+constexpr int MAXPAY = 8;
+struct Payload {
+    int nb, np;                     // build-side / probe-side payload columns
+    const void* bsrc[MAXPAY];
+    int bdt[MAXPAY];
+    void* bdst[MAXPAY];
+    const void* psrc[MAXPAY];
+    int pdt[MAXPAY];
+    void* pdst[MAXPAY];
+};
+
+__device__ __forceinline__ void copy_elem(const void* src, int dt, int64_t from, void* dst, int64_t to) {
+    switch (dt) {
+        case TQP_U8: static_cast<uint8_t*>(dst)[to] = __ldg(static_cast<const uint8_t*>(src) + from); break;
+        case TQP_I32: __stcs(static_cast<int*>(dst) + to, __ldg(static_cast<const int*>(src) + from)); break;
+        default: __stcs(static_cast<long long*>(dst) + to, __ldg(static_cast<const long long*>(src) + from));
+    }
+}
+
 // Pass 2: order-preserving compaction at the scanned tile offsets. Each thread owns
 // PIPT consecutive probe rows; ranks by warp scan of per-thread counts + block scan;
 // join pairs (leftOutputIndex = build row, rightOutputIndex = probe row)
@@ -199,7 +220,7 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
 template <bool JOIN>
 __global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ lft, const uint8_t* __restrict__ mask,
                                                    int anti, int64_t np, const uint64_t* __restrict__ toff,
-                                                   int64_t* left_out, int64_t* right_out) {
+                                                   int64_t* left_out, int64_t* right_out, Payload pay) {
     __shared__ uint32_t s_w[PNW];
     __shared__ uint32_t s_l[PTILE];
     __shared__ uint16_t s_r[PTILE];
@@ -259,8 +280,12 @@ __global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ 
     }
     __syncthreads();
     for (uint32_t k = tid; k < tot; k += PNT) {   // streamed (evict-first) coalesced stores
-        if (JOIN) __stcs((long long*)left_out + excl + k, (long long)s_l[k]);
+        if (JOIN && left_out) __stcs((long long*)left_out + excl + k, (long long)s_l[k]);
         if (right_out) __stcs((long long*)right_out + excl + k, (long long)(base + s_r[k]));
+        if (JOIN) {
+            for (int c = 0; c < pay.nb; c++) copy_elem(pay.bsrc[c], pay.bdt[c], s_l[k], pay.bdst[c], excl + k);
+            for (int c = 0; c < pay.np; c++) copy_elem(pay.psrc[c], pay.pdt[c], base + s_r[k], pay.pdst[c], excl + k);
+        }
     }
 }
 
@@ -344,7 +369,7 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
 }
 
 void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, int anti, int64_t* left_out,
-               int64_t* right_out, uint8_t* match_out, int64_t* n_out_host) {
+               int64_t* right_out, uint8_t* match_out, int64_t* n_out_host, const Payload* pay = nullptr) {
     DevBuf<int64_t> pack(ctx, 2);   // [0] selected rows, [1] duplicate-build-key flag: one readback
     pack.zero();
     const int64_t nb = B.nb;
@@ -392,10 +417,12 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
         if (mode == 0)
             launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)lft.get(),
-                   (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out);
+                   (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out,
+                   pay ? *pay : Payload{});
         else if (mode == 1 && right_out)
             launch(ctx, "tqp_pkfk_emit", emit_kernel<false>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)nullptr,
-                   (const uint8_t*)a.mask, anti, np, (const uint64_t*)toff.get(), (int64_t*)nullptr, right_out);
+                   (const uint8_t*)a.mask, anti, np, (const uint64_t*)toff.get(), (int64_t*)nullptr, right_out,
+                   Payload{});
         TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
     } else if (np > 0 && mode == 2) {
         // empty build side: no probe row matches
@@ -419,8 +446,12 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
     if (np > 0 && nb > 0) {   // probe keys in; pairs (join) or mask + selection vector (semi) out
         ctx->add_bytes("tqp_pkfk_probe", (double)np * dtype_size(pk.dtype) + (mode != 0 && match_out ? (double)np : 0.0) +
                                              (mode == 2 ? 8.0 * (double)np : 0.0));
+        double pb = 0;   // payload: read + write per output row
+        for (int c = 0; pay && c < pay->nb; c++) pb += 2.0 * (double)dtype_size(pay->bdt[c]);
+        for (int c = 0; pay && c < pay->np; c++) pb += 2.0 * (double)dtype_size(pay->pdt[c]);
         if (mode != 2)
-            ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? 16.0 * (double)h[0] : (right_out ? 8.0 * (double)h[0] : 0.0));
+            ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? ((left_out ? 8.0 : 0.0) + (right_out ? 8.0 : 0.0) + pb) * (double)h[0]
+                                                    : (right_out ? 8.0 * (double)h[0] : 0.0));
     }
 }
 }  // namespace
@@ -434,6 +465,38 @@ void pkfk_join(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int
     Built B;
     build_side(ctx, bk, nb, B);
     run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host);
+}
+
+// PK-FK join with payload columns gathered into the output (one row per matching probe
+// row, ascending probe row): build_out[c][j] = build_payload[c][left_j],
+// probe_out[c][j] = probe_payload[c][right_j]; the index pairs are optional.
+void pkfk_join_payload(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, const tqp_col* bp, int n_bp,
+                       void* const* bp_out, const tqp_col* pp, int n_pp, void* const* pp_out, int64_t* left_out,
+                       int64_t* right_out, int64_t* n_out_host) {
+    check_col(bk, nb, "pkfk build");
+    check_col(pk, np, "pkfk probe");
+    if (n_bp < 0 || n_bp > MAXPAY || n_pp < 0 || n_pp > MAXPAY) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: at most 8 payload columns per side");
+    if (np >= (int64_t(1) << 40)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: probe too large");
+    Payload pay{};
+    pay.nb = n_bp;
+    pay.np = n_pp;
+    for (int c = 0; c < n_bp; c++) {
+        check_col(bp[c], nb, "pkfk build payload");
+        if (np > 0 && !bp_out[c]) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null payload output");
+        pay.bsrc[c] = bp[c].data;
+        pay.bdt[c] = bp[c].dtype;
+        pay.bdst[c] = bp_out[c];
+    }
+    for (int c = 0; c < n_pp; c++) {
+        check_col(pp[c], np, "pkfk probe payload");
+        if (np > 0 && !pp_out[c]) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null payload output");
+        pay.psrc[c] = pp[c].data;
+        pay.pdt[c] = pp[c].dtype;
+        pay.pdst[c] = pp_out[c];
+    }
+    Built B;
+    build_side(ctx, bk, nb, B);
+    run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host, &pay);
 }
 
 void pkfk_semi(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int anti, uint8_t* match_out,

@@ -168,6 +168,26 @@ def test_pkfk_semi_anti(T, anti):
     assert np.array_equal(np.nonzero(member)[0], r)
 
 
+@pytest.mark.parametrize("indices", [True, False])
+def test_pkfk_join_payload(T, indices):
+    """Payload columns gathered into the join output equal the columns gathered by the
+    oracle's index pairs (u8 / i32 / i64 payloads on both sides)."""
+    orders, li = tpch_orders_lineitem(0.05, seed=42, device="cuda")
+    ok, lk = orders["o_orderkey"], li["l_orderkey"]
+    keep = torch.arange(ok.numel(), device="cuda") % 3 != 0           # a third of the orders unmatched
+    bk = ok[keep]
+    bpay = [orders["o_orderdate"][keep], bk * 7 - 3]
+    ppay = [li["l_returnflag"], li["l_shipdate"], li["l_extendedprice"]]
+    bo, po, idx = T.pkfk_join_payload(bk, lk, bpay, ppay, indices=indices)
+    olo, oro = oracle.pkfk_join(npy(bk), npy(lk))
+    for got, col in zip(bo, bpay):
+        assert np.array_equal(npy(got), npy(col)[olo])
+    for got, col in zip(po, ppay):
+        assert np.array_equal(npy(got), npy(col)[oro])
+    if indices:
+        assert np.array_equal(npy(idx[0]), olo) and np.array_equal(npy(idx[1]), oro)
+
+
 @pytest.mark.parametrize("nb,np_,span", [(0, 1000, 50), (1, 5, 3), (3000, 50_001, 6000), (300_000, 1_000_003, 10**6)])
 def test_pkfk_outer(T, nb, np_, span):
     """Probe-side outer join: every probe row, its build row or -1 (oracle pairs fill the rest)."""
