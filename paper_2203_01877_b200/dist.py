@@ -8,9 +8,11 @@ execution as future work):
     averaged);
   * PK-FK join, co-partitioned layout (each rank holds its orders and exactly their
     lineitems): purely local, no exchange;
-  * PK-FK join, shuffled layout: the build side is all-gathered (broadcast build,
-    SURVEY.md §8(e)); the gathered rank-ordered concatenation is the global build table,
-    so build rows come out as global row numbers with no extra remapping.
+  * PK-FK join, shuffled layout: either the build side is all-gathered (broadcast
+    build) -- the gathered rank-ordered concatenation is the global
+    build table, so build rows come out as global row numbers with no remapping -- or
+    both sides are co-partitioned by key range (all_to_all of (key, global row)) and
+    joined locally; a byte cost model picks the cheaper exchange (pkfk_cost_bytes).
 Operators are injectable (`local_fn`, `merge_fn`, `join_fn`) so the exchange logic is
 tested on CPU with the gloo backend and the oracle as the local operator
 (tests/test_dist_gloo.py). The product path always uses the libtqp kernels.
@@ -82,3 +84,91 @@ def pkfk_join_broadcast(ctx, build_keys, probe_keys, group=None, join_fn=None):
     join_fn = join_fn or ctx.pkfk_join
     allb = _gather_rows(build_keys.reshape(-1, 1).to(torch.int64), group).reshape(-1)
     return join_fn(allb.to(build_keys.dtype), probe_keys)
+
+
+def _stable_order(dest, sort_fn):
+    """Stable permutation grouping rows by destination rank (libtqp's radix sort on GPUs)."""
+    if sort_fn is not None:
+        return sort_fn(dest)
+    return torch.argsort(dest, stable=True)
+
+
+def _exchange(cols, dest, world, group=None, sort_fn=None):
+    """Send row i of every column to rank dest[i] (all_to_all_single). Received rows are
+    in source-rank order, and in source row order within a source."""
+    order = _stable_order(dest, sort_fn)
+    send_counts = torch.bincount(dest, minlength=world).to(torch.int64)
+    recv_counts = torch.empty_like(send_counts)
+    dist.all_to_all_single(recv_counts, send_counts, group=group)
+    sc, rc = send_counts.tolist(), recv_counts.tolist()
+    out = []
+    for c in cols:
+        r = torch.empty(sum(rc), dtype=c.dtype, device=c.device)
+        dist.all_to_all_single(r, c[order].contiguous(), rc, sc, group=group)
+        out.append(r)
+    return out
+
+
+def _key_ranges(build_keys, probe_keys, world, group=None):
+    """Equal-width key ranges over the global [min, max] of both sides (the TPC-H key
+    domain is dense; a sampled splitter set would replace this for skewed keys)."""
+    dev = build_keys.device
+    big = torch.iinfo(torch.int64)
+    lo = torch.tensor([min(int(build_keys.min()) if build_keys.numel() else big.max,
+                           int(probe_keys.min()) if probe_keys.numel() else big.max)], dtype=torch.int64, device=dev)
+    hi = torch.tensor([max(int(build_keys.max()) if build_keys.numel() else big.min,
+                           int(probe_keys.max()) if probe_keys.numel() else big.min)], dtype=torch.int64, device=dev)
+    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
+    kmin, kmax = int(lo.item()), int(hi.item())
+    width = max((kmax - kmin) // world + 1, 1)
+    return kmin, width
+
+
+def pkfk_join_copartition(ctx, build_keys, build_rows, probe_keys, probe_rows, group=None, join_fn=None,
+                          sort_fn=None):
+    """Shuffled-layout PK-FK join by co-partitioning: both sides' (key, global row) are
+    sent to the rank owning the key's range, joined locally, and mapped back to global
+    rows. Returns (global build row, global probe row) pairs of this rank's key range,
+    ascending by global probe row (the union over ranks = the single-GPU result)."""
+    join_fn = join_fn or ctx.pkfk_join
+    if sort_fn is None and ctx is not None:
+        sort_fn = lambda d: ctx.sort(d)[1]   # noqa: E731
+    world = dist.get_world_size(group)
+    kmin, width = _key_ranges(build_keys, probe_keys, world, group)
+    bk, pk = build_keys.to(torch.int64), probe_keys.to(torch.int64)
+    dest_b = torch.clamp((bk - kmin) // width, 0, world - 1)
+    dest_p = torch.clamp((pk - kmin) // width, 0, world - 1)
+    rb_key, rb_row = _exchange([bk, build_rows.to(torch.int64)], dest_b, world, group, sort_fn)
+    rp_key, rp_row = _exchange([pk, probe_rows.to(torch.int64)], dest_p, world, group, sort_fn)
+    lo, ro = join_fn(rb_key, rp_key)
+    gl, gr = rb_row[lo], rp_row[ro]
+    order = _stable_order(gr, sort_fn)
+    return gl[order], gr[order]
+
+
+def pkfk_cost_bytes(n_build, n_probe, world, key_bytes=8, row_bytes=8):
+    """Bytes received per rank by each shuffled-layout strategy:
+    broadcast = every other rank's build keys; co-partition = the (key, row) pairs of
+    both sides that belong to another rank's key range."""
+    f = (world - 1) / world
+    return {"broadcast": n_build * key_bytes * f,
+            "copartition": (n_build + n_probe) / world * (key_bytes + row_bytes) * f}
+
+
+def pkfk_join_shuffled(ctx, build_keys, build_rows, probe_keys, probe_rows, group=None, strategy="auto",
+                       join_fn=None, sort_fn=None):
+    """Shuffled-layout PK-FK join with the cheaper exchange (or the one asked for).
+    Returns (strategy, global build rows, global probe rows); broadcast pairs come in
+    local probe order, co-partition pairs by global probe row within the rank's range."""
+    world = dist.get_world_size(group)
+    if strategy == "auto":
+        n = torch.tensor([build_keys.numel(), probe_keys.numel()], dtype=torch.int64, device=build_keys.device)
+        dist.all_reduce(n, group=group)
+        cost = pkfk_cost_bytes(int(n[0]), int(n[1]), world)
+        strategy = min(cost, key=cost.get)
+    if strategy == "broadcast":
+        lo, ro = pkfk_join_broadcast(ctx, build_keys, probe_keys, group, join_fn)
+        return strategy, lo, probe_rows.to(torch.int64)[ro]
+    gl, gr = pkfk_join_copartition(ctx, build_keys, build_rows, probe_keys, probe_rows, group, join_fn, sort_fn)
+    return strategy, gl, gr

@@ -144,3 +144,74 @@ def test_world2_groupby_and_broadcast_join():
         # broadcast build: global orders row of every probed lineitem, probe-row order
         assert np.array_equal(ro, np.arange(len(ro)))
         assert np.array_equal(lo, parent_global)
+
+
+def _worker_copart(rank, world, port, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from datagen import tpch_orders_lineitem
+        from datagen.tpch import orders_count
+        from paper_2203_01877_b200 import dist as D
+        sf = 0.01
+        n_o = orders_count(sf) // world
+        orders, _ = tpch_orders_lineitem(sf, seed=42, device="cpu", layout="shuffled",
+                                         order_range=(rank * n_o, (rank + 1) * n_o))
+        other = (rank + 1) % world   # shuffled layout: the probe slice belongs to another rank's orders
+        _, li = tpch_orders_lineitem(sf, seed=42, device="cpu", layout="shuffled",
+                                     order_range=(other * n_o, (other + 1) * n_o))
+
+        def join_fn(b, p):
+            lo, ro = oracle.pkfk_join(b.numpy(), p.numpy())
+            return torch.as_tensor(lo), torch.as_tensor(ro)
+
+        res = {}
+        for strategy in ("copartition", "broadcast", "auto"):
+            s, gl, gr = D.pkfk_join_shuffled(None, orders["o_orderkey"], orders["o_global_row"], li["l_orderkey"],
+                                             li["l_global_row"], strategy=strategy, join_fn=join_fn)
+            res[strategy] = (s, gl.numpy(), gr.numpy())
+        parent_global = li["l_parent"].numpy() + other * n_o
+        out_q.put((rank, res, li["l_global_row"].numpy(), parent_global,
+                   D.pkfk_cost_bytes(orders_count(sf), 0, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_world2_copartition_join_and_cost_model():
+    """Co-partitioned shuffled-layout PK-FK join: the union over ranks of (global build
+    row, global probe row), ordered by probe row, is the single-process join of the whole
+    table; broadcast gives the same pairs; 'auto' takes the cheaper exchange."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_copart, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    # expected: every lineitem row joins its parent order (generator closed form)
+    rows = np.concatenate([o[2] for o in outs])
+    parents = np.concatenate([o[3] for o in outs])
+    order = np.argsort(rows, kind="stable")
+    want_l, want_r = parents[order], rows[order]
+    gl = np.concatenate([o[1]["copartition"][1] for o in outs])
+    gr = np.concatenate([o[1]["copartition"][2] for o in outs])
+    o2 = np.argsort(gr, kind="stable")
+    assert np.array_equal(gr[o2], want_r) and np.array_equal(gl[o2], want_l)
+    for rank, res, *_ in outs:   # within a rank, co-partition pairs ascend by global probe row
+        assert np.all(np.diff(res["copartition"][2]) > 0)
+    bl = np.concatenate([o[1]["broadcast"][1] for o in outs])
+    br = np.concatenate([o[1]["broadcast"][2] for o in outs])
+    o3 = np.argsort(br, kind="stable")
+    assert np.array_equal(br[o3], want_r) and np.array_equal(bl[o3], want_l)
+    for _, res, *_ in outs:
+        s = res["auto"][0]
+        n_b, n_p = 15_000, len(rows)
+        cost = {"broadcast": n_b * 8 * 0.5, "copartition": (n_b + n_p) / 2 * 16 * 0.5}
+        assert s == min(cost, key=cost.get)
