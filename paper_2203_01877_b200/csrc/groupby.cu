@@ -72,6 +72,7 @@ struct Phase1Args {
     int poff[PCH][3];             // stage byte offset of each factor's column
     int pdtf[PCH][3];             // and its dtype
     int pext[PCH];                // leading factors shared with the previous pair (its whole list), else 0
+    int direct;                   // dense / no-key paths: record blockIdx.x * D + id (fixed slots, no counter)
     int n_pairs;
     int prop[TQP_MAX_AGGS];
     int pnf[TQP_MAX_AGGS];
@@ -893,7 +894,9 @@ __device__ void flush_nokey(const Phase1Args& a, NoKeyAcc& acc, Work& w) {
         int64_t c = 0;
         for (int ww = 0; ww < GNW; ww++) c += s_cnt[ww];
         int64_t pb = -1;
-        if (c > 0) {
+        if (a.direct) {
+            pb = blockIdx.x;   // fixed slot (count 0 when nothing passed)
+        } else if (c > 0) {
             pb = (int64_t)atomicAdd(a.P_counter, 1ull);
             if (pb + 1 > a.cap) { atomicOr(a.overflow, 2); pb = -1; }
         }
@@ -1317,14 +1320,7 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     __syncthreads();
     if (tid == 0) {
         if (h.bad) atomicOr(a.overflow, 4);
-        int nz = 0;
-        for (int d = 0; d < D; d++) nz += h.dcnt[d] > 0;
-        int64_t pb = nz ? (int64_t)atomicAdd(a.P_counter, (unsigned long long)nz) : 0;
-        if (pb + nz > a.cap) { atomicOr(a.overflow, 2); pb = -1; }
-        for (int d = 0; d < D; d++) {
-            if (pb >= 0 && h.dcnt[d] > 0) h.drec[d] = pb++;
-            else h.drec[d] = -1;
-        }
+        for (int d = 0; d < D; d++) h.drec[d] = (int64_t)blockIdx.x * D + d;   // fixed slots (direct merge)
     }
     __syncthreads();
     for (int s2 = warp; s2 < D * np; s2 += NW) {
@@ -1355,6 +1351,82 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     for (int d = tid; d < D; d += NT) {
         const int64_t rec = h.drec[d];
         if (rec >= 0) { a.pkey[rec] = a.dkeys[d]; a.pcount[rec] = h.dcnt[d]; }
+    }
+}
+
+// Direct merge of fixed-slot partials (dense ids / no keys): record b * D + d holds CTA
+// b's split sums for id d. One warp per id reduces over the CTAs (count, per pair the
+// sums of low / high 32-bit halves -> an exact int128, or min / max); ids with rows are
+// compacted in id order (= key order) into the final groups. No sort, one launch.
+struct DirectArgs {
+    int D, n_pairs, keep_empty;   // keep_empty: no group keys -> always one group
+    int64_t nblocks;
+    int pop[TQP_MAX_AGGS];
+    const uint64_t* plo[TQP_MAX_AGGS];
+    const int64_t* phi[TQP_MAX_AGGS];
+    const int64_t* pcount;
+    const uint64_t* dkeys;        // id -> packed key (dense path)
+    uint64_t* gkey;
+    int64_t* gcount;
+    uint64_t* glo[TQP_MAX_AGGS];
+    int64_t* ghi[TQP_MAX_AGGS];
+    unsigned long long* G_out;    // group count (device)
+};
+
+__global__ void __launch_bounds__(1024) gb_direct_kernel(DirectArgs a) {
+    __shared__ int64_t s_cnt[DMAX];
+    __shared__ unsigned __int128 s_sum[DMAX][PCH];
+    __shared__ int64_t s_mm[DMAX][PCH];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int per = a.n_pairs + 1;   // per id: the count and every pair, one warp each
+    for (int item = warp; item < a.D * per; item += 32) {
+        const int d = item / per, j = item - d * per - 1;   // j = -1: the count
+        if (j < 0) {
+            int64_t c = 0;
+            for (int64_t b = lane; b < a.nblocks; b += 32) c += a.pcount[b * a.D + d];
+            for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+            if (lane == 0) s_cnt[d] = c;
+        } else if (a.pop[j] == P_SUM) {
+            uint64_t lo = 0;
+            int64_t hi = 0;
+            for (int64_t b = lane; b < a.nblocks; b += 32) { lo += a.plo[j][b * a.D + d]; hi += a.phi[j][b * a.D + d]; }
+            for (int o = 16; o > 0; o >>= 1) {
+                lo += __shfl_xor_sync(0xffffffffu, lo, o);
+                hi += __shfl_xor_sync(0xffffffffu, hi, o);
+            }
+            if (lane == 0) s_sum[d][j] = (unsigned __int128)(((__int128)hi << 32) + (__int128)lo);
+        } else {
+            const int op = a.pop[j];
+            int64_t v = op == P_MIN ? INT64_MAX : INT64_MIN;
+            for (int64_t b = lane; b < a.nblocks; b += 32) {
+                const int64_t x = (int64_t)a.plo[j][b * a.D + d];
+                v = op == P_MIN ? min(v, x) : max(v, x);
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const int64_t x = __shfl_xor_sync(0xffffffffu, v, o);
+                v = op == P_MIN ? min(v, x) : max(v, x);
+            }
+            if (lane == 0) s_mm[d][j] = v;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long g = 0;
+        for (int dd = 0; dd < a.D; dd++) {
+            if (s_cnt[dd] == 0 && !a.keep_empty) continue;
+            if (a.gkey) a.gkey[g] = a.dkeys ? a.dkeys[dd] : 0;
+            a.gcount[g] = s_cnt[dd];
+            for (int j = 0; j < a.n_pairs; j++) {
+                if (a.pop[j] == P_SUM) {
+                    a.glo[j][g] = (uint64_t)s_sum[dd][j];
+                    a.ghi[j][g] = (int64_t)(s_sum[dd][j] >> 64);
+                } else {
+                    a.glo[j][g] = (uint64_t)s_mm[dd][j];
+                }
+            }
+            g++;
+        }
+        *a.G_out = g;
     }
 }
 
@@ -1906,7 +1978,26 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
         int* ovf = reinterpret_cast<int*>(Pc.get() + 1);
         int64_t cap = std::min<int64_t>(std::max<int64_t>(n, 1), std::max<int64_t>(tiles * 64, 1 << 16));
         const char* tile_name = "tqp_groupby_tile";
+        const bool nokey_path = n_keys == 0 && PL->n_pairs <= PCH;
+        int64_t nokey_grid = 0;
+        size_t nokey_smem = 0;
+        if (nokey_path && n > 0) {
+            // pipeline depth: light per-row work (no group keys) is bandwidth-bound and
+            // wants more bytes in flight; keyed tiles are compute-heavy and prefer 2 CTAs/SM
+            a.n_stages = ((size_t)4 * a.stage_bytes + sizeof(NoKeyWork) <= 112 * 1024) ? 4 : 2;
+            nokey_smem = (size_t)a.n_stages * a.stage_bytes + sizeof(NoKeyWork);
+            set_smem(gb_phase1_kernel, nokey_smem);
+            int occ = 1;
+            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_phase1_kernel, GNT, nokey_smem));
+            nokey_grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
+        }
         for (int attempt = 0; attempt < 3; attempt++) {
+            // dense ids / no keys: fixed per-CTA slots merged directly (no phase-2 sort)
+            const bool direct = n > 0 && (dense || nokey_path);
+            const int64_t dD = dense ? a.D : 1;
+            const int64_t nblocks = dense ? dense_grid : nokey_grid;
+            if (direct) cap = std::max<int64_t>(cap, nblocks * dD);
+            a.direct = direct ? 1 : 0;
             pr.pkey.alloc(ctx, cap);
             pr.pcount.alloc(ctx, cap);
             for (int j = 0; j < PL->n_pairs; j++) {
@@ -1936,19 +2027,49 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
                     launch(ctx, tile_name, gb_dense_kernel<128>, dim3((unsigned)dense_grid), dim3(128), dense_smem, ad);
                 else
                     launch(ctx, tile_name, gb_dense_kernel<256>, dim3((unsigned)dense_grid), dim3(256), dense_smem, ad);
+            } else if (n > 0 && nokey_path) {
+                tile_name = "tqp_groupby_tile";
+                if (nokey_smem > 227 * 1024) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: referenced columns too wide");
+                launch(ctx, "tqp_groupby_tile", gb_phase1_kernel, dim3((unsigned)nokey_grid), dim3(GNT), nokey_smem, a);
             } else if (n > 0) {
                 tile_name = "tqp_groupby_tile";
-                // pipeline depth: light per-row work (no group keys) is bandwidth-bound and
-                // wants more bytes in flight; keyed tiles are compute-heavy and prefer 2 CTAs/SM
-                const bool nokey_path = n_keys == 0 && PL->n_pairs <= PCH;
-                a.n_stages = (nokey_path && (size_t)4 * a.stage_bytes + sizeof(NoKeyWork) <= 112 * 1024) ? 4 : 2;
-                const size_t smem = (size_t)a.n_stages * a.stage_bytes + (nokey_path ? sizeof(NoKeyWork) : sizeof(Work));
+                a.n_stages = 2;
+                const size_t smem = (size_t)a.n_stages * a.stage_bytes + sizeof(Work);
                 if (smem > 227 * 1024) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: referenced columns too wide");
                 set_smem(gb_phase1_kernel, smem);
                 int occ = 1;
                 TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_phase1_kernel, GNT, smem));
                 const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
                 launch(ctx, "tqp_groupby_tile", gb_phase1_kernel, dim3((unsigned)grid), dim3(GNT), smem, a);
+            }
+            if (direct) {   // merge the fixed slots straight into the final groups
+                PL->gkey.alloc(ctx, dD);
+                PL->gcount.alloc(ctx, dD);
+                DirectArgs da{};
+                da.D = (int)dD;
+                da.n_pairs = PL->n_pairs;
+                da.keep_empty = dense ? 0 : 1;
+                da.nblocks = nblocks;
+                for (int j = 0; j < PL->n_pairs; j++) {
+                    da.pop[j] = PL->pop[j];
+                    da.plo[j] = pr.plo[j].get();
+                    da.phi[j] = pr.phi[j].get();
+                    PL->glo[j].alloc(ctx, dD);
+                    da.glo[j] = PL->glo[j].get();
+                    if (PL->pop[j] == P_SUM) {
+                        PL->ghi[j].alloc(ctx, dD);
+                        da.ghi[j] = PL->ghi[j].get();
+                    }
+                }
+                da.pcount = pr.pcount.get();
+                da.dkeys = dense ? a.dkeys : nullptr;
+                da.gkey = PL->gkey.get();
+                da.gcount = PL->gcount.get();
+                da.G_out = Pc.get();
+                launch(ctx, "tqp_groupby_accumulate", gb_direct_kernel, dim3(1), dim3(1024), 0, da);
+                double rb = 8;
+                for (int j = 0; j < PL->n_pairs; j++) rb += PL->pop[j] == P_SUM ? 16 : 8;
+                ctx->add_bytes("tqp_groupby_accumulate", rb * (double)(nblocks * dD));
             }
             unsigned long long h[2] = {0, 0};
             read_back(ctx, h, Pc.get(), 16);
@@ -1958,6 +2079,16 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
                 continue;
             }
             if (o & 1) fail(TQP_ERR_OVERFLOW, "groupby: int64 overflow in an aggregate expression");
+            if (direct) {
+                pr.P = nblocks * dD;
+                PL->G = (int64_t)h[0];
+                PL->empty_global = false;
+                double in = 0;
+                for (int i = 0; i < a.n_ucols; i++) in += (double)dtype_size(a.udt[i]);
+                ctx->add_bytes(tile_name, in * (double)n);
+                *n_groups_host = PL->G;
+                return PL;
+            }
             pr.P = (int64_t)h[0];
             if (!(o & 2)) break;
             cap = std::max<int64_t>(n, 1);   // more distinct keys per tile than estimated: full capacity
