@@ -389,7 +389,10 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
                                                      const uint32_t* __restrict__ perm_l,
                                                      const uint32_t* __restrict__ perm_r, int64_t begin, int64_t end,
                                                      int64_t* __restrict__ lo_out, int64_t* __restrict__ ro_out) {
-    __shared__ int32_t s_cum[2 * ETILE + 2];
+    // shared memory: the staged bucket ends, plus (when the CTA spans <= MCAP buckets)
+    // the buckets' (L, R, startL, startR) so that walking across keys needs no global loads
+    constexpr int MCAP = 1024;
+    __shared__ __align__(16) int32_t s_buf[2 * ETILE + 2 + 3 * MCAP];
     __shared__ uint32_t s_l[ETILE], s_r[ETILE];
     const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
     const int64_t c1 = min(c0 + ETILE, end);
@@ -397,9 +400,18 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
     const int64_t b0 = tb[c0 / ETILE];
     const int64_t b1 = min((int64_t)tb[(c1 - 1) / ETILE + 1], K - 1);
     const int nb = (int)(b1 - b0 + 1);
+    const bool meta = nb <= MCAP;
+    int32_t* s_cum = s_buf;
+    uint32_t* s_m = reinterpret_cast<uint32_t*>(s_buf + (meta ? MCAP : 0));   // [4][MCAP] when meta
     for (int i = threadIdx.x; i < nb; i += ENT) {
         const int64_t v = mcum[b0 + i] - c0;
         s_cum[i] = (int32_t)(v < 0 ? -1 : (v > ETILE ? ETILE + 1 : v));
+        if (meta) {
+            s_m[i] = mL[b0 + i];
+            s_m[MCAP + i] = mR[b0 + i];
+            s_m[2 * MCAP + i] = msL[b0 + i];
+            s_m[3 * MCAP + i] = msR[b0 + i];
+        }
     }
     __syncthreads();
     const int64_t o0 = c0 + (int64_t)threadIdx.x * EIPT;
@@ -410,9 +422,17 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
             const int mid = (lo + hi) >> 1;
             if (s_cum[mid] <= rel) lo = mid + 1; else hi = mid;
         }
-        int64_t b = b0 + lo;
-        int64_t L = mL[b], R = mR[b], sL = msL[b], sR = msR[b];
-        int64_t off = o0 - (mcum[b] - L * R);
+        int bi = lo;   // bucket index relative to b0
+        auto load = [&](int i, int64_t& L, int64_t& R, int64_t& sL, int64_t& sR) {
+            if (meta) {
+                L = s_m[i]; R = s_m[MCAP + i]; sL = s_m[2 * MCAP + i]; sR = s_m[3 * MCAP + i];
+            } else {
+                L = mL[b0 + i]; R = mR[b0 + i]; sL = msL[b0 + i]; sR = msR[b0 + i];
+            }
+        };
+        int64_t L, R, sL, sR;
+        load(bi, L, R, sL, sR);
+        int64_t off = o0 - (mcum[b0 + bi] - L * R);
         int64_t q = off / R, r = off - q * R;
         const int cnt = (int)min((int64_t)EIPT, c1 - o0);
         for (int j = 0; j < cnt; j++) {
@@ -423,7 +443,7 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
                 r = 0;
                 if (++q == L) {
                     q = 0;
-                    if (++b < K) { L = mL[b]; R = mR[b]; sL = msL[b]; sR = msR[b]; }
+                    if (b0 + ++bi < K && bi < nb) load(bi, L, R, sL, sR);
                 }
             }
         }
