@@ -23,7 +23,12 @@ struct SortOut {
     DevBuf<uint32_t> perm32;           // internal permutation
 };
 
-void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& out);
+// andor (nullable): the AND / OR of the sort-domain keys, already read back by the caller
+// from sort_andor (so several sorts share one host sync); null = computed here.
+void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& out,
+                const uint64_t* andor = nullptr);
+// AND / OR of the sort-domain keys into ao[0..1] (device, stream-ordered; no sync)
+void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao);
 
 // Exclusive / inclusive scans over device arrays (decoupled look-back).
 void iota_i64(tqp_ctx* ctx, int64_t* p, int64_t n);

@@ -518,8 +518,15 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         // sort both sides (l.2-3); keep the internal sorted keys and u32 permutations
         SortOut sl, sr;
         sl.want_internal = sr.want_internal = true;
-        radix_sort(ctx, left.data, left.dtype, nl, false, sl);
-        radix_sort(ctx, right.data, right.dtype, nr, false, sr);
+        {   // both digit plans with one host sync
+            DevBuf<unsigned long long> ao(ctx, 4);
+            sort_andor(ctx, left.data, left.dtype, nl, false, ao.get());
+            sort_andor(ctx, right.data, right.dtype, nr, false, ao.get() + 2);
+            uint64_t h[4];
+            read_back(ctx, h, ao.get(), 32);
+            radix_sort(ctx, left.data, left.dtype, nl, false, sl, h);
+            radix_sort(ctx, right.data, right.dtype, nr, false, sr, h + 2);
+        }
         P->perm_l = std::move(sl.perm32);
         P->perm_r = std::move(sr.perm32);
         DevBuf<int64_t> scal(ctx, 4);   // U_l, U_r, K, out_size

@@ -565,22 +565,32 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
     if (need_perm_final) o.perm32 = std::move(pb[fb]);
 }
 
-void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o) {
+void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao) {
+    TQP_CUDA(cudaMemsetAsync(ao, 0xFF, 8, ctx->stream));
+    TQP_CUDA(cudaMemsetAsync(ao + 1, 0, 8, ctx->stream));
+    if (n <= 0) return;
+    const int mode = in_mode(dtype);
+    const int grid = (int)std::min<int64_t>(ceil_div(n, NT * 8), (int64_t)ctx->num_sms * 4);
+    dispatch_in(mode, [&](auto m) {
+        if constexpr (decltype(m)::value != IN_INTERNAL)
+            launch(ctx, "tqp_sort_andor", andor_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc, ao);
+    });
+    ctx->add_bytes("tqp_sort_andor", (double)n * dtype_size(dtype));
+}
+
+void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o, const uint64_t* andor) {
     if (n < 0 || n >= (int64_t(1) << 30)) fail(TQP_ERR_INVALID_ARGUMENT, "sort: n must be in [0, 2^30)");
     if (n == 0) return;
     const int mode = in_mode(dtype);
-    const int grid = (int)std::min<int64_t>(ceil_div(n, NT * 8), (int64_t)ctx->num_sms * 4);
-    DevBuf<unsigned long long> ao(ctx, 2);
-    TQP_CUDA(cudaMemsetAsync(ao.get(), 0xFF, 8, ctx->stream));
-    TQP_CUDA(cudaMemsetAsync(ao.get() + 1, 0, 8, ctx->stream));
-    dispatch_in(mode, [&](auto m) {
-        if constexpr (decltype(m)::value != IN_INTERNAL)
-            launch(ctx, "tqp_sort_andor", andor_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc,
-                   ao.get());
-    });
-    ctx->add_bytes("tqp_sort_andor", (double)n * dtype_size(dtype));
     uint64_t h[2];
-    read_back(ctx, h, ao.get(), 16);
+    if (andor) {   // the caller launched sort_andor and read the plan back (one sync for several sorts)
+        h[0] = andor[0];
+        h[1] = andor[1];
+    } else {
+        DevBuf<unsigned long long> ao(ctx, 2);
+        sort_andor(ctx, keys, dtype, n, desc, ao.get());
+        read_back(ctx, h, ao.get(), 16);
+    }
     o.and_bits = h[0];
     o.or_bits = h[1];
     const uint64_t diff = h[0] ^ h[1];
