@@ -8,5 +8,5 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/$
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
 timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
-for K in gb_dense_kernel gb_phase1 scatter_tma probe_kernel expand_kernel filter_kernel rle_kernel intersect_kernel gb_presence; do timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -c $([ $K = scatter_tma ] && echo 10 || echo 2) -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_full_$K.log 2>&1; done
+for K in gb_dense_kernel gb_phase1 scatter_tma probe_kernel emit_kernel expand_kernel filter_mask rle_write intersect_kernel common_kernel; do timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -c $([ $K = scatter_tma ] && echo 10 || echo 2) -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_full_$K.log 2>&1; done
 echo done

@@ -7,7 +7,10 @@ TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
 G = "gpurun_out"
 NAME = [("gb_phase1", "tqp_groupby_tile"), ("gb_dense_kernel", "tqp_groupby_dense"), ("gb_presence", "tqp_groupby_presence"),
         ("gb_dense_ids", "tqp_groupby_dense_ids"), ("key_range", "tqp_groupby_keyrange"), ("scatter_tma", "tqp_sort_scatter"), ("scatter_kernel", "tqp_sort_scatter"),
-        ("probe_kernel", "tqp_pkfk_probe"), ("expand_kernel", "tqp_smj_expand"), ("filter_kernel", "tqp_filter"),
+        ("probe_kernel", "tqp_pkfk_probe"), ("emit_kernel", "tqp_pkfk_emit"), ("filter_mask", "tqp_filter"),
+        ("filter_sel", "tqp_filter_select"), ("rle_count", "tqp_smj_rle"), ("rle_write", "tqp_smj_rle"),
+        ("common_kernel", "tqp_smj_intersect"), ("tile_bounds", "tqp_smj_intersect"), ("tile_bucket", "tqp_smj_cumsum"),
+        ("scan_u32", "tqp_scan_add"), ("gb_direct", "tqp_groupby_accumulate"), ("expand_kernel", "tqp_smj_expand"), ("filter_kernel", "tqp_filter"),
         ("tile_hist", "tqp_sort_tile_hist"), ("scan_tiles", "tqp_sort_scan"), ("scan_chunks", "tqp_sort_scan"),
         ("rle_kernel", "tqp_smj_rle"), ("intersect_kernel", "tqp_smj_intersect"), ("cum_kernel", "tqp_smj_cumsum"),
         ("andor_kernel", "tqp_sort_andor"), ("gb_gid", "tqp_groupby_gid"), ("gb_acc", "tqp_groupby_accumulate"),
