@@ -172,3 +172,69 @@ def pkfk_join_shuffled(ctx, build_keys, build_rows, probe_keys, probe_rows, grou
         return strategy, lo, probe_rows.to(torch.int64)[ro]
     gl, gr = pkfk_join_copartition(ctx, build_keys, build_rows, probe_keys, probe_rows, group, join_fn, sort_fn)
     return strategy, gl, gr
+
+
+# ---------------------------------------------------------- distributed sort / SMJ
+# SURVEY.md §8(f) NEXT 3. Ranks hold contiguous global row ranges (rank order = global
+# row order). Keys are range-partitioned by splitters sampled from every rank's sorted
+# keys; (key, global row) pairs are exchanged with all_to_all and sorted / joined locally
+# with libtqp. Received blocks arrive in source-rank order, so a stable local sort (or
+# the SMJ's (key, left row, right row) order) reproduces the single-GPU order exactly:
+# the concatenation of the ranks' outputs, in rank order, is bit-identical to it.
+
+def _splitters(sorted_keys_list, world, group=None, per_rank=64):
+    """world - 1 splitters from evenly spaced samples of each rank's keys (exact local
+    quantiles when the keys are sorted, a position sample otherwise)."""
+    dev = sorted_keys_list[0].device
+    samples = []
+    for k in sorted_keys_list:
+        if k.numel():
+            idx = torch.linspace(0, k.numel() - 1, per_rank, device=dev).round().to(torch.int64)
+            samples.append(k.to(torch.int64)[idx])
+    loc = torch.cat(samples) if samples else torch.empty(0, dtype=torch.int64, device=dev)
+    allv = _gather_rows(loc.reshape(-1, 1), group).reshape(-1)
+    allv, _ = torch.sort(allv)   # a few thousand host-chosen samples: plumbing, not the operator
+    if allv.numel() == 0:
+        return torch.empty(0, dtype=torch.int64, device=dev)
+    pos = [(i * allv.numel()) // world for i in range(1, world)]
+    return allv[torch.tensor(pos, dtype=torch.int64, device=dev)]
+
+
+def _range_dest(keys, splitters):
+    """Rank owning each key: the number of splitters <= key (equal keys share a rank)."""
+    return torch.searchsorted(splitters, keys.to(torch.int64), right=True)
+
+
+def sort_samplesort(ctx, keys, global_rows, group=None, sort_fn=None):
+    """Distributed stable sort. Returns this rank's (sorted keys, their global rows); the
+    ranks' outputs concatenated in rank order are the stable (key, global row) order of
+    the whole column. sort_fn(k) -> (sorted keys, permutation); default libtqp."""
+    sort_fn = sort_fn or ctx.sort
+    world = dist.get_world_size(group)
+    sk, perm = sort_fn(keys)
+    rows = global_rows.to(torch.int64)[perm]
+    spl = _splitters([sk], world, group)
+    dest = _range_dest(sk, spl)
+    rk, rr = _exchange([sk.to(torch.int64), rows], dest, world, group,
+                       sort_fn=lambda d: torch.arange(d.numel(), device=d.device))   # sk is sorted: dest ascends
+    k2, p2 = sort_fn(rk)
+    return k2.to(keys.dtype), rr[p2]
+
+
+def smj_join_copartition(ctx, left_keys, left_rows, right_keys, right_rows, group=None, join_fn=None,
+                         sort_fn=None):
+    """Distributed generic sort-merge join (Alg. 1) by key-range co-partitioning with
+    sampled splitters. Returns this rank's (global left row, global right row) pairs in
+    (key, left row, right row) order; the concatenation over ranks in rank order is the
+    single-GPU result. A key's pairs are produced by one rank (Zipf-heavy keys are not
+    split across ranks; output-range splitting of heavy keys is not implemented)."""
+    join_fn = join_fn or ctx.smj_join
+    if sort_fn is None and ctx is not None:
+        sort_fn = lambda d: ctx.sort(d)[1]   # noqa: E731
+    world = dist.get_world_size(group)
+    lk, rk = left_keys.to(torch.int64), right_keys.to(torch.int64)
+    spl = _splitters([lk, rk], world, group, per_rank=256)
+    rl_key, rl_row = _exchange([lk, left_rows.to(torch.int64)], _range_dest(lk, spl), world, group, sort_fn)
+    rr_key, rr_row = _exchange([rk, right_rows.to(torch.int64)], _range_dest(rk, spl), world, group, sort_fn)
+    lo, ro = join_fn(rl_key, rr_key)
+    return rl_row[lo], rr_row[ro]

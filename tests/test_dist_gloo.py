@@ -215,3 +215,64 @@ def test_world2_copartition_join_and_cost_model():
         n_b, n_p = 15_000, len(rows)
         cost = {"broadcast": n_b * 8 * 0.5, "copartition": (n_b + n_p) / 2 * 16 * 0.5}
         assert s == min(cost, key=cost.get)
+
+
+def _worker_sort_smj(rank, world, port, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from datagen import uniform_keys, zipf_keys
+        from paper_2203_01877_b200 import dist as D
+
+        def sort_fn(k):
+            s, p = oracle.sort(k.numpy())
+            return torch.as_tensor(s), torch.as_tensor(p)
+
+        def join_fn(a, b):
+            lo, ro = oracle.smj_join(a.numpy(), b.numpy())
+            return torch.as_tensor(lo), torch.as_tensor(ro)
+
+        n = 20_000
+        keys = zipf_keys(world * n, 5_000, seed=42)            # global column, Zipf with duplicates
+        mine = keys[rank * n:(rank + 1) * n]
+        rows = torch.arange(rank * n, (rank + 1) * n, dtype=torch.int64)
+        sk, sr = D.sort_samplesort(None, mine, rows, sort_fn=sort_fn)
+        left = zipf_keys(world * n, 3_000, seed=7)
+        right = uniform_keys(world * n, 3_000, seed=8)
+        sl = left[rank * n:(rank + 1) * n]
+        sr2 = right[rank * n:(rank + 1) * n]
+        gl, gr = D.smj_join_copartition(None, sl, rows, sr2, rows, join_fn=join_fn, sort_fn=None)
+        out_q.put((rank, sk.numpy(), sr.numpy(), gl.numpy(), gr.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_world2_samplesort_and_smj():
+    """Distributed sample sort and co-partitioned SMJ: the ranks' outputs concatenated in
+    rank order equal the single-process stable sort / Alg.-1 join of the whole columns."""
+    import oracle
+    from datagen import uniform_keys, zipf_keys
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sort_smj, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=240) for _ in range(world)], key=lambda o: o[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    n = 20_000
+    keys = zipf_keys(world * n, 5_000, seed=42).numpy()
+    want_k, want_p = oracle.sort(keys)
+    assert np.array_equal(np.concatenate([o[1] for o in outs]), want_k)
+    assert np.array_equal(np.concatenate([o[2] for o in outs]), want_p)
+    left = zipf_keys(world * n, 3_000, seed=7).numpy()
+    right = uniform_keys(world * n, 3_000, seed=8).numpy()
+    olo, oro = oracle.smj_join(left, right)
+    assert np.array_equal(np.concatenate([o[3] for o in outs]), olo)
+    assert np.array_equal(np.concatenate([o[4] for o in outs]), oro)
