@@ -60,6 +60,10 @@ def test_pkfk_vs_macro_and_bruteforce(seed):
     if nb > 0 and probe.size > 0:
         mlo, mro = PL.pkfk_join_macro(build, probe, pad="safe")
         assert sorted(zip(lo, ro)) == sorted(zip(mlo, mro))
+        # reading R7: the paper's order (probe side sorted descending, stable) is our
+        # probe-row order re-sorted stably by probe key descending
+        order = np.lexsort((ro, -probe[ro]))
+        assert np.array_equal(lo[order], mlo) and np.array_equal(ro[order], mro)
 
 
 def test_pkfk_tpch_closed_form(sf001):
