@@ -36,5 +36,6 @@ void scan_max_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int
 // out[i] = sum(in[0..i-1]), out[n] = total (out has n + 1 entries; sums must fit 32 bits)
 void scan_add_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n);
 void scan_add_u32_to_u64_exclusive(tqp_ctx* ctx, const uint32_t* in, uint64_t* out, int64_t n);
+void scan_add_u64_exclusive(tqp_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t n);
 
 }  // namespace tqp

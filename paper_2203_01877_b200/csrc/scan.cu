@@ -10,22 +10,22 @@ constexpr int STILE = SNT * SIPT;
 
 // Exclusive scan of u32 values under max (out[i] = max(in[0..i-1])) or add
 // (out[i] = sum(in[0..i-1]), and out[n] = the total). out[0] = 0.
-template <bool ADD, typename OT>
-__global__ void __launch_bounds__(SNT) scan_u32_kernel(const uint32_t* __restrict__ in, OT* __restrict__ out,
+template <bool ADD, typename OT, typename IT = uint32_t>
+__global__ void __launch_bounds__(SNT) scan_u32_kernel(const IT* __restrict__ in, OT* __restrict__ out,
                                                        int64_t n, uint64_t* status, unsigned long long* counter) {
     __shared__ int64_t s_tile;
     __shared__ OT s_w[SNT / 32];
     __shared__ uint64_t s_excl;
     const int64_t tile = take_tile(counter, &s_tile);
     const int64_t base = tile * STILE + (int64_t)threadIdx.x * SIPT;
-    uint32_t v[SIPT];
-    if (base + SIPT <= n && (((uintptr_t)(in + base)) & 15) == 0) {
+    IT v[SIPT];
+    if (sizeof(IT) == 4 && base + SIPT <= n && (((uintptr_t)(in + base)) & 15) == 0) {
         uint4 a = *reinterpret_cast<const uint4*>(in + base);
         uint4 b = *reinterpret_cast<const uint4*>(in + base + 4);
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
     } else {
 #pragma unroll
-        for (int i = 0; i < SIPT; i++) v[i] = (base + i < n) ? in[base + i] : 0u;
+        for (int i = 0; i < SIPT; i++) v[i] = (base + i < n) ? in[base + i] : IT(0);
     }
     auto op = [](OT a, OT b) -> OT { return ADD ? a + b : max(a, b); };
     OT t = 0;
@@ -108,6 +108,19 @@ void scan_add_u32_to_u64_exclusive(tqp_ctx* ctx, const uint32_t* in, uint64_t* o
     ctx->add_bytes("tqp_scan_add", 12.0 * (double)n);
     launch(ctx, "tqp_scan_add", scan_u32_kernel<true, uint64_t>, dim3((unsigned)tiles), dim3(SNT), 0, in, out, n,
            status.get(), counter.get());
+}
+
+// 64-bit values (< 2^62 each and in total; the caller checks the total separately)
+void scan_add_u64_exclusive(tqp_ctx* ctx, const uint64_t* in, uint64_t* out, int64_t n) {
+    if (n <= 0) return;
+    const int64_t tiles = ceil_div(n, STILE);
+    DevBuf<uint64_t> status(ctx, tiles);
+    DevBuf<unsigned long long> counter(ctx, 1);
+    status.zero();
+    counter.zero();
+    ctx->add_bytes("tqp_scan_add", 16.0 * (double)n);
+    launch(ctx, "tqp_scan_add", scan_u32_kernel<true, uint64_t, uint64_t>, dim3((unsigned)tiles), dim3(SNT), 0, in, out,
+           n, status.get(), counter.get());
 }
 
 }  // namespace tqp

@@ -11,8 +11,8 @@
 //   l.5-8  histMul = L*R; cumsums                         -> intersect_kernel (each
 //          left unique key located among the right unique keys by a merge walk)
 //          + common_kernel (compaction of the common keys with L, R,
-//          startL = cumL - L, startR = cumR - R) + cum_kernel (inclusive scan of
-//          L*R by decoupled look-back = cumHistMul)
+//          startL = cumL - L, startR = cumR - R) + cum_tiles / add-scan /
+//          cum_write (inclusive scan of L*R = cumHistMul, two passes)
 //   l.9    outSize = cumHistMul[-1]                       -> one 8-byte readback
 //   l.10-14 arange, bucketize, in-bucket offset, div/rem -> expand_kernel: each CTA
 //          owns a fixed output range, finds its first bucket with one
@@ -313,68 +313,87 @@ __global__ void __launch_bounds__(JNT) common_kernel(const uint32_t* __restrict_
     }
 }
 
-// cumHistMul = inclusive scan of histMul = L*R over the K common keys.
-__global__ void __launch_bounds__(JNT) cum_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
-                                                  const int64_t* K_p, int64_t* mcum, int64_t* out_size,
-                                                  int* overflow, uint64_t* status, unsigned long long* counter) {
-    __shared__ int64_t s_tile;
-    __shared__ uint64_t s_w[JNW], s_excl;
+// cumHistMul = inclusive scan of histMul = L*R over the K common keys, in two passes
+// with no inter-tile chain: cum_tiles_kernel sums L*R per tile of JTILE keys (saturated at
+// 2^62, and also added into an fp64 running total that flags totals >= 2^62), an
+// exclusive 64-bit add-scan gives tile offsets, and cum_write_kernel writes cumHistMul
+// and, in the same pass, the per-output-tile bucket table expand needs.
+constexpr uint64_t SUM_CAP = 1ull << 62;
+constexpr int64_t ETILE_C = 256 * 8;   // == ETILE (expand's outputs per CTA), defined below
+
+__global__ void __launch_bounds__(JNT) cum_tiles_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
+                                                        const int64_t* K_p, uint64_t* tsum, double* dtot, int* overflow) {
+    __shared__ unsigned __int128 s_w[JNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tile = take_tile(counter, &s_tile);
     const int64_t K = *K_p;
-    const int64_t base = tile * JTILE + (int64_t)tid * JIPT;   // blocked: 8 consecutive per thread
-    if (tile * JTILE >= K) return;
+    const int64_t base = (int64_t)blockIdx.x * JTILE + (int64_t)tid * JIPT;
+    unsigned __int128 t = 0;
+#pragma unroll
+    for (int i = 0; i < JIPT; i++)
+        if (base + i < K) t += (uint64_t)mL[base + i] * (uint64_t)mR[base + i];
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t lo = __shfl_xor_sync(0xffffffffu, (uint64_t)t, o);
+        const uint64_t hi = __shfl_xor_sync(0xffffffffu, (uint64_t)(t >> 64), o);
+        t += ((unsigned __int128)hi << 64) | lo;
+    }
+    if (lane == 0) s_w[warp] = t;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned __int128 tot = 0;
+        for (int w = 0; w < JNW; w++) tot += s_w[w];
+        if (tot >= SUM_CAP) {
+            *overflow = 1;
+            tot = SUM_CAP - 1;
+        }
+        tsum[blockIdx.x] = (uint64_t)tot;
+        if (tot) atomicAdd(dtot, (double)(uint64_t)tot);
+    }
+}
+
+__global__ void __launch_bounds__(JNT) cum_write_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
+                                                        const int64_t* K_p, const uint64_t* __restrict__ toff,
+                                                        int64_t* mcum, uint32_t* tb, int64_t n_tb) {
+    __shared__ uint64_t s_w[JNW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t K = *K_p;
+    const int64_t base = (int64_t)blockIdx.x * JTILE + (int64_t)tid * JIPT;
+    if ((int64_t)blockIdx.x * JTILE >= K) return;
     uint64_t v[JIPT], t = 0;
 #pragma unroll
     for (int i = 0; i < JIPT; i++) {
-        v[i] = (base + i < K) ? (uint64_t)mL[base + i] * (uint64_t)mR[base + i] : 0;
+        v[i] = base + i < K ? (uint64_t)mL[base + i] * (uint64_t)mR[base + i] : 0;
         t += v[i];
     }
     uint64_t x = t;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    uint64_t wpre = 0, tot = 0;
-    for (int w = 0; w < JNW; w++) {
-        if (w < warp) wpre += s_w[w];
-        tot += s_w[w];
-    }
-    if (warp == 0) {
-        const uint64_t e = lookback_warp(status, tile, tot, OpAdd(), 0ull);
-        if (lane == 0) {
-            s_excl = e;
-            if (e + tot >= LB_VAL || tot >= LB_VAL) *overflow = 1;
-            if ((tile + 1) * JTILE >= K) *out_size = (int64_t)(e + tot);
-        }
-    }
-    __syncthreads();
-    uint64_t run = s_excl + wpre + x - t;
+    uint64_t run = toff[blockIdx.x] + x - t;
+#pragma unroll
+    for (int w = 0; w < JNW; w++)
+        if (w < warp) run += s_w[w];
 #pragma unroll
     for (int i = 0; i < JIPT; i++) {
+        const int64_t b = base + i;
+        if (b >= K) break;
+        const int64_t start = (int64_t)run;
         run += v[i];
-        if (base + i < K) mcum[base + i] = (int64_t)run;
+        mcum[b] = (int64_t)run;
+        // output tiles whose first output falls inside this key's range [start, run)
+        for (int64_t c = (start + ETILE_C - 1) / ETILE_C; c * ETILE_C < (int64_t)run; c++) tb[c] = (uint32_t)b;
+        if (b == K - 1) tb[n_tb - 1] = (uint32_t)b;
     }
 }
 
 constexpr int ENT = 256;
 constexpr int EIPT = 8;
 constexpr int ETILE = ENT * EIPT;
+static_assert(ETILE == ETILE_C, "cum_write_kernel's tile-bucket table uses expand's tile size");
 
-
-// tb[c] = bucket (common key) containing output c * ETILE, for every output tile; the
-// sentinel tb[ceil(out / ETILE)] = K - 1. One thread per key writes the tiles whose
-// first output falls inside the key's output range.
-__global__ void tile_bucket_kernel(const int64_t* __restrict__ mcum, const uint32_t* __restrict__ mL,
-                                   const uint32_t* __restrict__ mR, int64_t K, uint32_t* tb, int64_t n_tb) {
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < K; b += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t end = mcum[b], start = end - (int64_t)mL[b] * (int64_t)mR[b];
-        for (int64_t c = (start + ETILE - 1) / ETILE; c * ETILE < end; c++) tb[c] = (uint32_t)b;
-        if (b == K - 1) tb[n_tb - 1] = (uint32_t)b;
-    }
-}
 
 // Output offsets [begin, end): bucket b = upper_bound(cumHistMul, o) (bucketize
 // right=True); o' = o - (cumHistMul[b] - histMul[b]); q = o' / R, r = o' % R;
@@ -529,10 +548,8 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         }
         P->perm_l = std::move(sl.perm32);
         P->perm_r = std::move(sr.perm32);
-        DevBuf<int64_t> scal(ctx, 4);   // U_l, U_r, K, out_size
-        DevBuf<int> ovf(ctx, 1);
+        DevBuf<int64_t> scal(ctx, 6);   // U_l, U_r, K, out_size, overflow flag, fp64 total: one readback
         scal.zero();
-        ovf.zero();
         const int64_t cap = std::min(nl, nr);
         P->mL.alloc(ctx, cap);
         P->mR.alloc(ctx, cap);
@@ -544,30 +561,28 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         const double kb = k32 ? 4.0 : 8.0;
         if (k32) rle_intersect<uint32_t>(ctx, P, sl, sr, scal.get());
         else rle_intersect<uint64_t>(ctx, P, sl, sr, scal.get());
-        {
-            const int64_t tiles = ceil_div(cap, JTILE);
-            DevBuf<uint64_t> status(ctx, tiles);
-            DevBuf<unsigned long long> counter(ctx, 1);
-            status.zero();
-            counter.zero();
-            launch(ctx, "tqp_smj_cumsum", cum_kernel, dim3((unsigned)tiles), dim3(JNT), 0, P->mL.get(), P->mR.get(),
-                   scal.get() + 2, P->mcum.get(), scal.get() + 3, ovf.get(), status.get(), counter.get());
-        }
-        int64_t h[4];
-        int o = 0;
-        read_back(ctx, h, scal.get(), 32);
-        read_back(ctx, &o, ovf.get(), 4);
-        if (o) fail(TQP_ERR_OVERFLOW, "smj: output size exceeds 2^62");
+        const int64_t ctiles = ceil_div(cap, JTILE);
+        DevBuf<uint64_t> tsum(ctx, ctiles), toff(ctx, ctiles + 1);
+        launch(ctx, "tqp_smj_cumsum", cum_tiles_kernel, dim3((unsigned)ctiles), dim3(JNT), 0, (const uint32_t*)P->mL.get(),
+               (const uint32_t*)P->mR.get(), (const int64_t*)(scal.get() + 2), tsum.get(), (double*)(scal.get() + 5),
+               (int*)(scal.get() + 4));
+        scan_add_u64_exclusive(ctx, tsum.get(), toff.get(), ctiles);
+        TQP_CUDA(cudaMemcpyAsync(scal.get() + 3, toff.get() + ctiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        int64_t h[6];
+        read_back(ctx, h, scal.get(), 48);
+        double dt;
+        memcpy(&dt, &h[5], 8);
+        if (h[4] || dt >= 4.6116860184273879e18 || (uint64_t)h[3] >= SUM_CAP)   // 2^62
+            fail(TQP_ERR_OVERFLOW, "smj: output size exceeds 2^62");
         ctx->add_bytes("tqp_smj_intersect", (kb + 4.0) * (double)std::min(nl, nr) + 16.0 * (double)h[2]);
-        ctx->add_bytes("tqp_smj_cumsum", 24.0 * (double)h[2]);
         P->K = h[2];
         P->out_size = h[2] > 0 ? h[3] : 0;
-        if (P->out_size > 0) {   // tile -> bucket table for expand
+        if (P->out_size > 0) {   // cumHistMul + the tile -> bucket table for expand
             const int64_t n_tb = ceil_div(P->out_size, ETILE) + 1;
             P->tb.alloc(ctx, n_tb);
-            const int g = (int)std::min<int64_t>(ceil_div(P->K, 256), (int64_t)ctx->num_sms * 8);
-            launch(ctx, "tqp_smj_cumsum", tile_bucket_kernel, dim3(g), dim3(256), 0, (const int64_t*)P->mcum.get(),
-                   (const uint32_t*)P->mL.get(), (const uint32_t*)P->mR.get(), P->K, P->tb.get(), n_tb);
+            launch(ctx, "tqp_smj_cumsum", cum_write_kernel, dim3((unsigned)ctiles), dim3(JNT), 0,
+                   (const uint32_t*)P->mL.get(), (const uint32_t*)P->mR.get(), (const int64_t*)(scal.get() + 2),
+                   (const uint64_t*)toff.get(), P->mcum.get(), P->tb.get(), n_tb);
             ctx->add_bytes("tqp_smj_cumsum", 16.0 * (double)P->K + 4.0 * (double)n_tb);
         }
         *out_size_host = P->out_size;

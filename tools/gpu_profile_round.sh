@@ -1,4 +1,6 @@
-# Round profiling: full bench line, ncu launch list, ncu --set full of the top kernels.
+# Round profiling: full bench line, reference line, ncu launch list, ncu --set full of the
+# top kernels, summarised on the box (gpurun_out/ copies back at most 64 MiB: the big
+# .ncu-rep files are reduced to their summaries and deleted).
 # Usage (on the GPU box via gpurun): bash tools/gpu_profile_round.sh <tag>
 TAG=${1:-r01}
 set -x
@@ -8,5 +10,17 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/$
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline"
 timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
-for K in gb_dense_kernel gb_phase1 scatter_tma probe_kernel emit_kernel expand_kernel filter_mask rle_write intersect_kernel common_kernel; do timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -c $([ $K = scatter_tma ] && echo 10 || echo 2) -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_full_$K.log 2>&1; done
+for K in gb_dense_kernel gb_phase1 scatter_tma probe_kernel emit_kernel expand_kernel filter_mask rle_write intersect_kernel common_kernel; do
+  C=2; S=0
+  if [ $K = scatter_tma ]; then C=6; S=0; fi   # one step's sorts: 3 passes of the 15M build sort, then the 60M ones
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c $C -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_full_$K.log 2>&1
+done
+python tools/profile_summary.py ${TAG} gpurun_out/${TAG}_summary
+mkdir -p gpurun_out/${TAG}_reps
+for K in gb_dense_kernel scatter_tma probe_kernel; do
+  ncu -i gpurun_out/${TAG}_full_$K.ncu-rep --page raw --csv > gpurun_out/${TAG}_reps/${K}_raw.csv 2>/dev/null
+  ncu -i gpurun_out/${TAG}_full_$K.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${TAG}_reps/${K}_source.csv 2>/dev/null
+done
+rm -f gpurun_out/${TAG}_full_*.ncu-rep
+du -sh gpurun_out
 echo done

@@ -4,6 +4,7 @@ markdown summary. Usage: python tools/profile_summary.py <tag>"""
 import csv, io, json, os, subprocess, sys, collections
 
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
+OUT = sys.argv[2] if len(sys.argv) > 2 else "profiles"   # the GPU box writes into gpurun_out/
 G = "gpurun_out"
 NAME = [("gb_phase1", "tqp_groupby_tile"), ("gb_dense_kernel", "tqp_groupby_dense"), ("gb_presence", "tqp_groupby_presence"),
         ("gb_dense_ids", "tqp_groupby_dense_ids"), ("key_range", "tqp_groupby_keyrange"), ("scatter_tma", "tqp_sort_scatter"), ("scatter_kernel", "tqp_sort_scatter"),
@@ -64,7 +65,7 @@ def full(rep):
     return res
 
 
-os.makedirs("profiles", exist_ok=True)
+os.makedirs(OUT, exist_ok=True)
 L = launches()
 tot = sum(v[0] for v in L.values())
 tq = sum(v[0] for k, v in L.items() if not k.startswith("torch"))
@@ -74,8 +75,8 @@ for rep in sorted(glob.glob(f"{G}/{TAG}_full*.ncu-rep")):
     for k, v in full(rep).items():
         F[k] += v
 traffic = {k: sum(x["dram_read"] + x["dram_write"] for x in v) / len(v) for k, v in F.items() if k}
-json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
-with open(f"profiles/ncu_summary_{TAG}.md", "w") as f:
+json.dump(traffic, open(f"{OUT}/ncu_traffic.json", "w"), indent=1)
+with open(f"{OUT}/ncu_summary_{TAG}.md", "w") as f:
     f.write(f"# ncu summary ({TAG})\n\nCommand: `python bench.py --steps 1 --warmup 1 --no-cpu-baseline` on one B200 "
             f"(ncu, `--clock-control none`; cold-cache serialised launches: compare shares, not absolutes).\n\n")
     f.write("## Launch list: device time by libtqp kernel (share of libtqp time)\n\n| kernel | us | launches | share |\n|---|---|---|---|\n")
@@ -88,4 +89,4 @@ with open(f"profiles/ncu_summary_{TAG}.md", "w") as f:
         for x in v:
             f.write(f"| {k} | {x['time_us']:.0f} | {x['dram_read']/1e6:.1f} | {x['dram_write']/1e6:.1f} | "
                     f"{x['warps_active_pct']:.1f} | {x['issue_active_pct']:.1f} | {x['regs']} | {x['grid']} |\n")
-print(open(f"profiles/ncu_summary_{TAG}.md").read())
+print(open(f"{OUT}/ncu_summary_{TAG}.md").read())
