@@ -58,6 +58,23 @@ __global__ void pack_records_kernel(const KT* __restrict__ keys, const uint32_t*
         rec[i] = (((uint32_t)(KT)(keys[i] - base) & lowmask) << pbits) | perm[i];
 }
 
+// Slot table: 8 u32 per bucket holding its packed records inline (unused entries
+// 0xFFFFFFFF), or, for a bucket of more than 8 records, 0x80000000 | its first record
+// index. Valid records have the top bit clear (residual + row bits <= 31).
+__global__ void fill_slots_kernel(const uint32_t* __restrict__ T, const uint32_t* __restrict__ rec, int64_t nbk,
+                                  uint32_t* __restrict__ slots) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nbk; b += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t lo = T[b], hi = T[b + 1], cnt = hi - lo;
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) w[j] = (uint32_t)j < cnt ? rec[lo + j] : 0xFFFFFFFFu;
+        if (cnt > 8) w[0] = 0x80000000u | lo;
+        uint4* p4 = reinterpret_cast<uint4*>(slots + b * 8);
+        p4[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        p4[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+}
+
 struct ProbeArgs {
     const void* probe;
     int64_t n_probe;
@@ -65,6 +82,7 @@ struct ProbeArgs {
     const uint32_t* bperm;    // their source rows
     const uint32_t* T;        // bracket table, 2^B + 1 entries
     const uint32_t* rec;      // packed records (PACKED)
+    const uint32_t* slots;    // PACKED, nullable: 8 u32 per bucket (records inline, or a pointer)
     uint32_t lowmask;         // 2^shift - 1
     int pbits;                // bits of the row number in a record
     uint64_t base;            // internal-domain base (= AND of all build keys)
@@ -96,6 +114,23 @@ __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint3
     KT rel = (KT)(k - (KT)a.base);
     if (k < (KT)a.base || (a.vbits < 64 && ((uint64_t)rel >> a.vbits) != 0)) return false;
     uint64_t b = (uint64_t)rel >> a.shift;
+    if (PACKED && a.slots) {   // one aligned 32-byte sector: the bucket's records inline
+        const uint32_t low = (uint32_t)rel & a.lowmask;
+        const uint4* p4 = reinterpret_cast<const uint4*>(a.slots + b * 8);
+        const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1);
+        const uint32_t w[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        if (!(w[0] >> 31) || w[0] == 0xFFFFFFFFu) {   // else: more than 8 records, w[0] points into rec
+            bool hit = false;
+#pragma unroll
+            for (int j = 0; j < 8; j++) {   // empty entries have the top bit set; residuals are distinct
+                if (!(w[j] >> 31) && (w[j] >> a.pbits) == low) {
+                    left = w[j] & ((1u << a.pbits) - 1u);
+                    hit = true;
+                }
+            }
+            return hit;
+        }
+    }
     uint32_t lo = __ldg(a.T + b), hi = __ldg(a.T + b + 1);
     if (PACKED) {
         const uint32_t low = (uint32_t)rel & a.lowmask;
@@ -292,6 +327,7 @@ __global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ 
 struct Built {
     SortOut so;
     DevBuf<uint32_t> TR;      // bracket table T, then (packed) the records, one allocation
+    DevBuf<uint32_t> slots;   // packed: per-bucket slot table (null when it would be much larger)
     uint32_t* T = nullptr;
     uint32_t* rec = nullptr;
     size_t tr_bytes = 0;
@@ -362,6 +398,14 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
             launch(ctx, "tqp_pkfk_records", pack_records_kernel<uint64_t>, dim3(g), dim3(256), 0, B.so.keys64.get(),
                    B.so.perm32.get(), nb, (uint64_t)B.base, lowmask, B.pbits, B.rec);
         ctx->add_bytes("tqp_pkfk_records", (double)nb * ((B.so.k32 ? 4 : 8) + 8));
+        // slot table when the top bit is free and it is at most ~2x the records
+        if (B.shift + B.pbits <= 31 && nbk * 8 <= 2 * nb + (int64_t(1) << 20) && (nbk >> 27) == 0) {
+            B.slots.alloc(ctx, nbk * 8);
+            const int gs = (int)std::min<int64_t>(ceil_div(nbk, 256), (int64_t)ctx->num_sms * 8);
+            launch(ctx, "tqp_pkfk_records", fill_slots_kernel, dim3(gs), dim3(256), 0, (const uint32_t*)B.T,
+                   (const uint32_t*)B.rec, nbk, B.slots.get());
+            ctx->add_bytes("tqp_pkfk_records", 4.0 * (double)nb + 32.0 * (double)nbk);
+        }
         B.so.keys32.release();
         B.so.keys64.release();
         B.so.perm32.release();
@@ -388,6 +432,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         a.bperm = B.so.perm32.get();
         a.T = B.T;
         a.rec = B.rec;
+        a.slots = B.slots.get();
         a.pbits = B.pbits;
         a.lowmask = B.shift >= 32 ? 0xFFFFFFFFu : ((1u << B.shift) - 1u);
         a.base = B.base;
