@@ -12,7 +12,7 @@ timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
 for K in gb_dense_kernel gb_phase1 scatter_tma probe_kernel emit_kernel expand_kernel filter_mask rle_write intersect_kernel common_kernel; do
   C=2; S=0
-  if [ $K = scatter_tma ]; then C=6; S=0; fi   # one step's sorts: 3 passes of the 15M build sort, then the 60M ones
+  if [ $K = scatter_tma ]; then C=9; S=0; fi   # every scatter launch of one step (the bench averages them all)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c $C -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_full_$K.log 2>&1
 done
 python tools/profile_summary.py ${TAG} gpurun_out/${TAG}_summary
