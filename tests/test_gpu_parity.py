@@ -612,7 +612,8 @@ def test_launch_counter_and_profiling(T):
     st = ctx.kernel_stats()
     ctx.set_profiling(False)
     assert ctx.launch_count() >= 3
-    assert "tqp_onesweep" in st and st["tqp_onesweep"][1] >= 1
+    assert "tqp_sort_scatter" in st and st["tqp_sort_scatter"][1] >= 1
+    assert all(v[1] >= 1 and v[0] > 0 for v in st.values())   # every launch timed
 
 
 def test_groupby_merge_partials(T):

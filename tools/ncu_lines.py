@@ -1,8 +1,11 @@
 """Top source lines by stall samples + stall-reason totals for an ncu report (dev tool)."""
 import csv, io, subprocess, sys
 rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 15
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+if rep.endswith(".csv"):   # a saved `--page source --csv --print-source cuda,sass` export
+    out = open(rep).read()
+else:
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+                         capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 cur = None; hdr = None; agg = {}; tot = {}
 for r in rows:
