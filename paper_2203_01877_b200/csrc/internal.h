@@ -25,10 +25,14 @@ struct SortOut {
 
 // andor (nullable): the AND / OR of the sort-domain keys, already read back by the caller
 // from sort_andor (so several sorts share one host sync); null = computed here.
+// th0 (nullable, sort_hist0_words(n) u32): the first-pass histogram sort_andor fused in.
 void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& out,
-                const uint64_t* andor = nullptr);
-// AND / OR of the sort-domain keys into ao[0..1] (device, stream-ordered; no sync)
-void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao);
+                const uint64_t* andor = nullptr, uint32_t* th0 = nullptr);
+// AND / OR of the sort-domain keys into ao[0..1] (device, stream-ordered; no sync); with
+// th0, also the speculative pass-0 tile histogram (9-bit digits at bit 0, 4096-key tiles)
+void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao,
+                uint32_t* th0 = nullptr);
+size_t sort_hist0_words(int64_t n);
 
 // Exclusive / inclusive scans over device arrays (decoupled look-back).
 void iota_i64(tqp_ctx* ctx, int64_t* p, int64_t n);

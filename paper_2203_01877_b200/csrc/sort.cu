@@ -60,6 +60,52 @@ __global__ void __launch_bounds__(NT) andor_kernel(const void* keys, int64_t n, 
     }
 }
 
+// AND / OR of the sort-domain keys fused with a speculative first-pass histogram: the
+// low 9 bits (digit 0 of the 9-bit plan that dense integer keys take) per tile of 4096
+// keys -- exactly what tile_hist_kernel<uint32_t, IN, 16, 9> would compute for pass 0
+// at shift 0. The host uses it only when the plan turns out to be that one.
+constexpr int H0_IPT = 16, H0_TILE = 256 * H0_IPT, H0_BINS = 512;
+template <int IN>
+__global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64_t n, bool desc,
+                                                         unsigned long long* out, uint32_t* __restrict__ th0) {
+    __shared__ uint32_t h[NW][H0_BINS];
+    __shared__ uint64_t sa[NW], so[NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int d = lane; d < H0_BINS; d += 32) h[warp][d] = 0;
+    __syncwarp();
+    const int64_t base = (int64_t)blockIdx.x * H0_TILE;
+    uint64_t a = ~0ull, o = 0;
+    uint64_t u[H0_IPT];
+#pragma unroll
+    for (int i = 0; i < H0_IPT; i++) {
+        const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
+        u[i] = pos < n ? load_u<IN>(keys, pos, desc) : 0;
+        if (pos < n) { a &= u[i]; o |= u[i]; }
+    }
+#pragma unroll
+    for (int i = 0; i < H0_IPT; i++) {
+        const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
+        if (pos < n) atomicAdd(&h[warp][(uint32_t)u[i] & (H0_BINS - 1u)], 1u);
+    }
+    for (int sft = 16; sft > 0; sft >>= 1) {
+        a &= __shfl_xor_sync(0xffffffffu, a, sft);
+        o |= __shfl_xor_sync(0xffffffffu, o, sft);
+    }
+    if (lane == 0) { sa[warp] = a; so[warp] = o; }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < NW; w++) { a &= sa[w]; o |= so[w]; }
+        atomicAnd(&out[0], (unsigned long long)a);
+        atomicOr(&out[1], (unsigned long long)o);
+    }
+    for (int d = tid; d < H0_BINS; d += NT) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) c += h[w][d];
+        th0[(int64_t)blockIdx.x * H0_BINS + d] = c;
+    }
+}
+
 // Exclusive scan of one value per thread across a 256-thread block.
 __device__ __forceinline__ uint32_t block_excl_scan256(uint32_t v, uint32_t* s_w) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -484,7 +530,7 @@ static void dispatch_in(int mode, F&& f) {
 
 template <typename KT, int RB>
 static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o,
-                       const int* shifts, int P) {
+                       const int* shifts, int P, uint32_t* th0 = nullptr) {
     constexpr int BINS = 1 << RB;
     constexpr int IPT = sizeof(KT) == 4 ? 16 : 12;   // 4096 / 3072 keys per tile
     constexpr int TILE = NT * IPT;
@@ -512,12 +558,15 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         const void* in = p == 0 ? keys : kb[(p - 1) % 2].get();
         const int mode = p == 0 ? mode0 : (int)IN_INTERNAL;
         const double kin = p == 0 ? (double)dtype_size(dtype) : (double)sizeof(KT);
-        dispatch_in(mode, [&](auto m) {
-            launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT, RB>,
-                   dim3((unsigned)tiles), dim3(NT), 0, in, n, shifts[p], desc, th.get());
-        });
-        ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
-        launch(ctx, "tqp_sort_scan", scan_tiles_kernel<RB>, dim3((unsigned)chunks, BINS / SNT), dim3(SNT), 0, th.get(),
+        uint32_t* thp = (p == 0 && th0) ? th0 : th.get();   // pass 0: histogram fused into the AND/OR pass
+        if (thp != th0) {
+            dispatch_in(mode, [&](auto m) {
+                launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT, RB>,
+                       dim3((unsigned)tiles), dim3(NT), 0, in, n, shifts[p], desc, thp);
+            });
+            ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
+        }
+        launch(ctx, "tqp_sort_scan", scan_tiles_kernel<RB>, dim3((unsigned)chunks, BINS / SNT), dim3(SNT), 0, thp,
                tiles, ct.get());
         launch(ctx, "tqp_sort_scan", scan_chunks_kernel<RB>, dim3(1), dim3(BINS), 0, ct.get(), chunks);
         ctx->add_bytes("tqp_sort_scan", 8.0 * BINS * (double)tiles + 12.0 * BINS * (double)chunks);
@@ -533,7 +582,7 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
             a.out_perm64 = o.perm64;
             a.out_u = o.sorted_u;
         }
-        a.th = th.get();
+        a.th = thp;
         a.ct = ct.get();
         a.n = n;
         a.shift = shifts[p];
@@ -565,30 +614,44 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
     if (need_perm_final) o.perm32 = std::move(pb[fb]);
 }
 
-void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao) {
+void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao,
+                uint32_t* th0) {
     TQP_CUDA(cudaMemsetAsync(ao, 0xFF, 8, ctx->stream));
     TQP_CUDA(cudaMemsetAsync(ao + 1, 0, 8, ctx->stream));
     if (n <= 0) return;
     const int mode = in_mode(dtype);
     const int grid = (int)std::min<int64_t>(ceil_div(n, NT * 8), (int64_t)ctx->num_sms * 4);
     dispatch_in(mode, [&](auto m) {
-        if constexpr (decltype(m)::value != IN_INTERNAL)
-            launch(ctx, "tqp_sort_andor", andor_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc, ao);
+        if constexpr (decltype(m)::value != IN_INTERNAL) {
+            if (th0)
+                launch(ctx, "tqp_sort_andor", andor_hist0_kernel<decltype(m)::value>, dim3((unsigned)ceil_div(n, H0_TILE)),
+                       dim3(NT), 0, keys, n, desc, ao, th0);
+            else
+                launch(ctx, "tqp_sort_andor", andor_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc, ao);
+        }
     });
-    ctx->add_bytes("tqp_sort_andor", (double)n * dtype_size(dtype));
+    ctx->add_bytes("tqp_sort_andor", (double)n * dtype_size(dtype) + (th0 ? 2048.0 * (double)ceil_div(n, H0_TILE) : 0.0));
 }
 
-void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o, const uint64_t* andor) {
+size_t sort_hist0_words(int64_t n) { return (size_t)ceil_div(n, H0_TILE) * H0_BINS; }
+
+void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o, const uint64_t* andor,
+                uint32_t* th0) {
     if (n < 0 || n >= (int64_t(1) << 30)) fail(TQP_ERR_INVALID_ARGUMENT, "sort: n must be in [0, 2^30)");
     if (n == 0) return;
     const int mode = in_mode(dtype);
     uint64_t h[2];
+    DevBuf<uint32_t> th0_own;
     if (andor) {   // the caller launched sort_andor and read the plan back (one sync for several sorts)
         h[0] = andor[0];
         h[1] = andor[1];
     } else {
         DevBuf<unsigned long long> ao(ctx, 2);
-        sort_andor(ctx, keys, dtype, n, desc, ao.get());
+        if (n >= (1 << 16) && mode != IN_INTERNAL) {   // large sorts: speculative pass-0 histogram
+            th0_own.alloc(ctx, sort_hist0_words(n));
+            th0 = th0_own.get();
+        }
+        sort_andor(ctx, keys, dtype, n, desc, ao.get(), th0);
         read_back(ctx, h, ao.get(), 16);
     }
     o.and_bits = h[0];
@@ -634,7 +697,9 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
         return;
     }
     if (o.k32) {
-        if (rb == 9) run_passes<uint32_t, 9>(ctx, keys, dtype, n, desc, o, shifts, P);
+        // the fused histogram is pass 0's when the plan is 9-bit digits from bit 0 on u32 keys
+        uint32_t* h0 = (th0 && rb == 9 && shifts[0] == 0) ? th0 : nullptr;
+        if (rb == 9) run_passes<uint32_t, 9>(ctx, keys, dtype, n, desc, o, shifts, P, h0);
         else run_passes<uint32_t, 8>(ctx, keys, dtype, n, desc, o, shifts, P);
     } else {
         if (rb == 9) run_passes<uint64_t, 9>(ctx, keys, dtype, n, desc, o, shifts, P);
