@@ -183,11 +183,19 @@ class HotPath:
 def run_gpu(args):
     import paper_2203_01877_b200 as T
     rank, world, local = env_rank()
+    # test-only overrides: a functional run of the multi-rank code path on a one-GPU box
+    # (gloo collectives, every rank on device 0); never used for a reported number
+    if os.environ.get("TQP_BENCH_DEVICE") is not None:
+        local = int(os.environ["TQP_BENCH_DEVICE"])
     dist = None
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("TQP_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -387,7 +395,7 @@ def run_gpu(args):
                             "algorithmic_GBps": (v[2] / v[0] / 1e6) if v[0] > 0 else None}
                         for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:   # the oracle baseline: rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(hp, args)
         print(json.dumps(line), flush=True)
     if dist:
