@@ -343,7 +343,12 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         const int64_t base = tile * TILE;
         KT key[IPT];
         uint32_t pm[IPT], rk[IPT];
-        for (int d = lane; d < BINS; d += 32) { s.u.whist[warp][d] = 0; s.u.match[warp][d] = 0; }
+        for (int d = lane * 4; d < BINS; d += 128) {   // 16-byte stores
+            *reinterpret_cast<uint4*>(&s.u.whist[warp][d]) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(&s.u.match[warp][d]) = make_uint4(0, 0, 0, 0);
+        }
+        // rows of this tile left from this thread's first slot on (32-bit compares below)
+        const int rem = (int)min((int64_t)TILE + 1, a.n - base - (int64_t)(warp * 32 * IPT + lane));
         uint32_t gs[BPT];   // this tile's global digit starts: loaded now, used after ranking
 #pragma unroll
         for (int j = 0; j < BPT; j++) {
@@ -387,7 +392,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         }
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
-            const bool valid = base + warp * 32 * IPT + i * 32 + lane < a.n;
+            const bool valid = i * 32 < rem;
             const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
             // peers = lanes of this warp with the same digit: every lane ORs its bit into
             // the digit's match word, reads the word back, and the leader clears it
@@ -442,7 +447,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
-            if (base + warp * 32 * IPT + i * 32 + lane < a.n) {
+            if (i * 32 < rem) {
                 const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
                 rk[i] = s.u.whist[warp][d] + rk[i];
             }
@@ -450,7 +455,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
-            if (base + warp * 32 * IPT + i * 32 + lane < a.n) {
+            if (i * 32 < rem) {
                 s.u.sorted.keys[rk[i]] = key[i];
                 s.u.sorted.perm[rk[i]] = pm[i];
             }
@@ -459,6 +464,25 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         for (int j = 0; j < BPT; j++) s.gstart[tid + j * NT] = gs[j] - s.tstart[tid + j * NT];   // global - tile start
         __syncthreads();
         const int tile_n = (int)min((int64_t)TILE, a.n - base);
+        if (!a.out_perm64 && !a.out_u && !a.out_orig) {   // intermediate passes / internal outputs
+            KT* ok = (KT*)a.out_keys;
+            uint32_t* op = a.out_perm;
+            if (ok && op) {
+                for (int j = tid; j < tile_n; j += NT) {
+                    const KT kk = s.u.sorted.keys[j];
+                    const uint32_t dst = s.gstart[(uint32_t)(kk >> a.shift) & DM] + (uint32_t)j;
+                    ok[dst] = kk;
+                    op[dst] = s.u.sorted.perm[j];
+                }
+            } else {
+                for (int j = tid; j < tile_n; j += NT) {
+                    const KT kk = s.u.sorted.keys[j];
+                    const uint32_t dst = s.gstart[(uint32_t)(kk >> a.shift) & DM] + (uint32_t)j;
+                    if (ok) ok[dst] = kk;
+                    if (op) op[dst] = s.u.sorted.perm[j];
+                }
+            }
+        } else
         for (int j = tid; j < tile_n; j += NT) {
             const KT kk = s.u.sorted.keys[j];
             const uint32_t p = s.u.sorted.perm[j];
