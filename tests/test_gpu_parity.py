@@ -538,6 +538,33 @@ def test_groupby_dense_path(T, card, wide, monkeypatch):
     assert "tqp_groupby_dense" not in st
 
 
+@pytest.mark.parametrize("seed", range(6))
+def test_groupby_dense_path_random(T, seed):
+    """Dense path over three key columns (u8, negative i32, u8), != / range predicates that
+    may empty some or all groups, and SUM / MIN / MAX / AVG / COUNT of signed expressions."""
+    rng = np.random.default_rng(100 + seed)
+    n = int(rng.choice([1, 511, 512, 513, 70_001, 400_000]))
+    k0 = rng.integers(0, 2, n).astype(np.uint8)
+    k1 = (rng.integers(-2, 1, n) * 3).astype(np.int32)
+    k2 = (rng.integers(0, 2, n) + 200).astype(np.uint8)
+    v = rng.integers(-10**9, 10**9, n)
+    w = rng.integers(-100, 100, n)
+    cols = [k0, k1, k2, v, w]
+    gcols = [cu(k0, torch.uint8), cu(k1, torch.int32), cu(k2, torch.uint8), cu(v), cu(w)]
+    aggs = [("sum", [(3, 0, 1), (4, 7, -1)]), ("min", [(3, 5, -1)]), ("max", [(4, 0, 1), (4, 0, 1)]),
+            ("avg", [(3, 0, 1)]), ("count", []), ("sum", [(4, 0, 1)])]
+    preds = [[], [(4, "ne", 0), (3, "gt", -5 * 10**8)], [(1, "ne", -3)], [(4, "gt", 200)]][seed % 4]
+    want = oracle.groupby_agg(cols, [0, 1, 2], aggs, preds)
+    ctx = T.context()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    got = ctx.groupby_agg(gcols, [0, 1, 2], aggs, preds)
+    st = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    check_groupby(T, got, want, aggs)
+    assert "tqp_groupby_dense" in st   # 12 possible keys, packed width 1 + 3 + 1 bits
+
+
 def test_groupby_dense_bound_fallback(T):
     """A product the dense path cannot prove exact re-runs on the general path."""
     rng = np.random.default_rng(3)
