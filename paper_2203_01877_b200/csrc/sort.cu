@@ -288,9 +288,14 @@ struct ScatterWork {
     uint64_t mbar[2];
 };
 
+// The stage carries the keys only; a later pass's permutation is loaded from global
+// memory straight into registers (issued before the stage wait, used after ranking),
+// which halves the stages and leaves room for 3 CTAs per SM.
+constexpr bool PERM_DIRECT = false;   // measured: 3 CTAs/SM with direct loads was slower (1.39 -> 1.50 ms, 60M keys; MIO-bound)
+
 template <typename KT, int IN, int IPT>
 constexpr int scatter_stage_bytes() {
-    return NT * IPT * (int)sizeof(typename InKey<IN, KT>::T) + (IN == IN_INTERNAL ? NT * IPT * 4 : 0);
+    return NT * IPT * (int)sizeof(typename InKey<IN, KT>::T) + (IN == IN_INTERNAL && !PERM_DIRECT ? NT * IPT * 4 : 0);
 }
 
 // Input stages per CTA: tile k+2's copy is in flight while tile k is ranked and written.
@@ -303,7 +308,7 @@ constexpr size_t scatter_tma_smem() {
 }
 
 template <typename KT, int IN, int IPT, int RB>
-__global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
+__global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT) == 4 ? 3 : 2))) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
     constexpr int TILE = NT * IPT, BINS = 1 << RB, BPT = BINS / NT;
     constexpr uint32_t DM = BINS - 1u;
     using KIN = typename InKey<IN, KT>::T;
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
         uint8_t* dst = stage_ptr(st);
         mbar_expect_tx(&s.mbar[st], (uint32_t)STAGE_BYTES);
         bulk_g2s(dst, (const KIN*)a.in_keys + t * TILE, TILE * (uint32_t)sizeof(KIN), &s.mbar[st]);
-        if (HAS_PERM) bulk_g2s(dst + TILE * sizeof(KIN), a.in_perm + t * TILE, TILE * 4u, &s.mbar[st]);
+        if (HAS_PERM && !PERM_DIRECT) bulk_g2s(dst + TILE * sizeof(KIN), a.in_perm + t * TILE, TILE * 4u, &s.mbar[st]);
     };
     uint32_t uses[SST];
     for (int st = 0; st < SST; st++) {
@@ -356,6 +361,10 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
             gs[j] = __ldg(a.ct + (tile / CHUNK) * BINS + d) + __ldg(a.th + tile * BINS + d);
         }
         if (full(tile)) {
+            if (HAS_PERM && PERM_DIRECT) {
+#pragma unroll
+                for (int i = 0; i < IPT; i++) pm[i] = __ldcs(a.in_perm + base + warp * 32 * IPT + i * 32 + lane);
+            }
             mbar_wait(&s.mbar[st], (uses[st] - 1) & 1);
             const uint8_t* sp = stage_ptr(st);
             const KIN* sk = reinterpret_cast<const KIN*>(sp);
@@ -364,7 +373,8 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : 2)) scatter_tma_kernel(Sca
             for (int i = 0; i < IPT; i++) {
                 const int q = warp * 32 * IPT + i * 32 + lane;
                 key[i] = conv_key<KT, IN>(sk[q], a.desc);
-                pm[i] = HAS_PERM ? spm[q] : (uint32_t)(base + q);
+                if (!HAS_PERM) pm[i] = (uint32_t)(base + q);
+                else if (!PERM_DIRECT) pm[i] = spm[q];
             }
         } else {
 #pragma unroll
