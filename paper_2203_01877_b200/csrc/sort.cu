@@ -463,11 +463,17 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             }
         }
         __syncthreads();
+        // tile staged in digit order; u32 keys as {key, perm} pairs (one 8-byte access each way)
+        uint2* kp = reinterpret_cast<uint2*>(&s.u.sorted);
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
             if (i * 32 < rem) {
-                s.u.sorted.keys[rk[i]] = key[i];
-                s.u.sorted.perm[rk[i]] = pm[i];
+                if (sizeof(KT) == 4) {
+                    kp[rk[i]] = make_uint2((uint32_t)key[i], pm[i]);
+                } else {
+                    s.u.sorted.keys[rk[i]] = key[i];
+                    s.u.sorted.perm[rk[i]] = pm[i];
+                }
             }
         }
 #pragma unroll
@@ -477,25 +483,26 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
         if (!a.out_perm64 && !a.out_u && !a.out_orig) {   // intermediate passes / internal outputs
             KT* ok = (KT*)a.out_keys;
             uint32_t* op = a.out_perm;
-            if (ok && op) {
+            if (sizeof(KT) == 4 && ok && op) {
                 for (int j = tid; j < tile_n; j += NT) {
-                    const KT kk = s.u.sorted.keys[j];
-                    const uint32_t dst = s.gstart[(uint32_t)(kk >> a.shift) & DM] + (uint32_t)j;
-                    ok[dst] = kk;
-                    op[dst] = s.u.sorted.perm[j];
+                    const uint2 v = kp[j];
+                    const uint32_t dst = s.gstart[(v.x >> a.shift) & DM] + (uint32_t)j;
+                    ok[dst] = (KT)v.x;
+                    op[dst] = v.y;
                 }
             } else {
                 for (int j = tid; j < tile_n; j += NT) {
-                    const KT kk = s.u.sorted.keys[j];
+                    const KT kk = sizeof(KT) == 4 ? (KT)kp[j].x : s.u.sorted.keys[j];
+                    const uint32_t p = sizeof(KT) == 4 ? kp[j].y : s.u.sorted.perm[j];
                     const uint32_t dst = s.gstart[(uint32_t)(kk >> a.shift) & DM] + (uint32_t)j;
                     if (ok) ok[dst] = kk;
-                    if (op) op[dst] = s.u.sorted.perm[j];
+                    if (op) op[dst] = p;
                 }
             }
         } else
         for (int j = tid; j < tile_n; j += NT) {
-            const KT kk = s.u.sorted.keys[j];
-            const uint32_t p = s.u.sorted.perm[j];
+            const KT kk = sizeof(KT) == 4 ? (KT)kp[j].x : s.u.sorted.keys[j];
+            const uint32_t p = sizeof(KT) == 4 ? kp[j].y : s.u.sorted.perm[j];
             const uint32_t d = (uint32_t)(kk >> a.shift) & DM;
             const int64_t dst = (int64_t)(uint32_t)(s.gstart[d] + (uint32_t)j);   // gdelta[d] + j (mod 2^32, n < 2^30)
             if (a.out_keys) ((KT*)a.out_keys)[dst] = kk;
