@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
     // the buckets' (L, R, startL, startR) so that walking across keys needs no global loads
     constexpr int MCAP = 1024;
     __shared__ __align__(16) int32_t s_buf[2 * ETILE + 2 + 3 * MCAP];
-    __shared__ uint32_t s_l[ETILE], s_r[ETILE];
+    __shared__ __align__(16) uint32_t s_l[ETILE], s_r[ETILE];
     const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
     const int64_t c1 = min(c0 + ETILE, end);
     // buckets of outputs c0 and c1 - 1 lie in [b0, b1]: at most two output tiles' worth
@@ -454,10 +454,12 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
         int64_t off = o0 - (mcum[b0 + bi] - L * R);
         int64_t q = off / R, r = off - q * R;
         const int cnt = (int)min((int64_t)EIPT, c1 - o0);
-        for (int j = 0; j < cnt; j++) {
-            const int o = threadIdx.x * EIPT + j;
-            s_l[o] = __ldg(perm_l + sL + q);
-            s_r[o] = __ldg(perm_r + sR + r);
+        uint32_t vl[EIPT], vr[EIPT];
+#pragma unroll
+        for (int j = 0; j < EIPT; j++) {
+            if (j >= cnt) break;
+            vl[j] = __ldg(perm_l + sL + q);
+            vr[j] = __ldg(perm_r + sR + r);
             if (++r == R) {
                 r = 0;
                 if (++q == L) {
@@ -466,14 +468,37 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
                 }
             }
         }
+        const int o = threadIdx.x * EIPT;
+        if (cnt == EIPT) {   // 16-byte shared stores
+            reinterpret_cast<uint4*>(s_l + o)[0] = make_uint4(vl[0], vl[1], vl[2], vl[3]);
+            reinterpret_cast<uint4*>(s_l + o)[1] = make_uint4(vl[4], vl[5], vl[6], vl[7]);
+            reinterpret_cast<uint4*>(s_r + o)[0] = make_uint4(vr[0], vr[1], vr[2], vr[3]);
+            reinterpret_cast<uint4*>(s_r + o)[1] = make_uint4(vr[4], vr[5], vr[6], vr[7]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < EIPT; j++)
+                if (j < cnt) { s_l[o + j] = vl[j]; s_r[o + j] = vr[j]; }
+        }
     }
     __syncthreads();
     const int n = (int)(c1 - c0);
     int64_t* lo_p = lo_out + (c0 - begin);
     int64_t* ro_p = ro_out + (c0 - begin);
-    for (int o = threadIdx.x; o < n; o += ENT) {   // coalesced, streamed (evict-first) stores
-        __stcs((long long*)lo_p + o, (long long)s_l[o]);
-        __stcs((long long*)ro_p + o, (long long)s_r[o]);
+    const bool vec = n == ETILE && (((uintptr_t)lo_p | (uintptr_t)ro_p) & 15) == 0;
+    if (vec) {   // 4 outputs per thread and step: one 16-byte shared load, two 16-byte stores per array
+        for (int o = threadIdx.x * 4; o < n; o += ENT * 4) {
+            const uint4 a = *reinterpret_cast<const uint4*>(s_l + o);
+            const uint4 b = *reinterpret_cast<const uint4*>(s_r + o);
+            __stcs(reinterpret_cast<longlong2*>(lo_p + o), make_longlong2(a.x, a.y));
+            __stcs(reinterpret_cast<longlong2*>(lo_p + o) + 1, make_longlong2(a.z, a.w));
+            __stcs(reinterpret_cast<longlong2*>(ro_p + o), make_longlong2(b.x, b.y));
+            __stcs(reinterpret_cast<longlong2*>(ro_p + o) + 1, make_longlong2(b.z, b.w));
+        }
+    } else {
+        for (int o = threadIdx.x; o < n; o += ENT) {   // coalesced, streamed (evict-first) stores
+            __stcs((long long*)lo_p + o, (long long)s_l[o]);
+            __stcs((long long*)ro_p + o, (long long)s_r[o]);
+        }
     }
 }
 
