@@ -93,8 +93,10 @@ tqp_status tqp_ctx_kernel_stats(tqp_ctx* ctx, char* names_host, size_t names_cap
  * (n x int64, caller-allocated). descending != 0 orders keys descending with
  * ties still in ascending row order (descending is NOT the reverse).
  * sorted_keys_out: nullable; if given, n elements of the input dtype = keys[perm].
- * Implementation: onesweep LSD radix sort; digits that are constant across all
- * keys are skipped. Synchronises once (pass plan). Requires n < 2^31. */
+ * Implementation: reduce-then-scan LSD radix sort (per-tile digit histograms,
+ * prefix scans, stable tile scatter); digits that are constant across all keys
+ * are skipped. Synchronises once (pass plan). Requires n < 2^30, else
+ * TQP_ERR_INVALID_ARGUMENT. */
 tqp_status tqp_sort(tqp_ctx* ctx, tqp_col keys, int64_t n, int descending,
                     void* sorted_keys_out, int64_t* perm_out);
 
@@ -202,6 +204,9 @@ tqp_status tqp_filter_compact(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols
  * Method: each tile of rows is radix-sorted by key in shared memory and reduced
  * per run (segment boundaries + segmented sums); the per-tile partials are
  * radix-sorted globally and reduced again (two-level sort-based aggregation).
+ * When at most 16 packed keys occur (packed width <= 16 bits), the keys get dense
+ * ids in key order from a presence pass instead and rows are reduced per id without
+ * a sort; without group keys the partials are reduced per block. Same results.
  * prepare synchronises and reports *n_groups_host = G; fetch writes:
  *   keys_out[k]   : G elements of key column k's dtype (nullable each)
  *   results_out[a]: G elements of the aggregate's result type (nullable each). */
