@@ -136,6 +136,14 @@ tqp_status tqp_pkfk_join_payload(tqp_ctx* ctx, tqp_col build_keys, int64_t n_bui
                                  int n_probe_payload, void* const* probe_payload_out_host, int64_t* left_out_idx,
                                  int64_t* right_out_idx, int64_t* n_out_host);
 
+/* Hash-join ablation (the comparison point of PAPER.md:1299,
+ * not the paper's method): the same PK-FK join contract and output (pairs in
+ * ascending probe row, TQP_ERR_DUPLICATE_BUILD_KEY on a repeated build key) from
+ * an open-addressing hash table (>= 2 n_build slots, linear probing) instead of
+ * the sorted build side. Requires n_build < 2^30. Synchronises once. */
+tqp_status tqp_pkfk_join_hash(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys,
+                              int64_t n_probe, int64_t* left_out_idx, int64_t* right_out_idx, int64_t* n_out_host);
+
 /* Probe-side outer join (the PK-FK match mask of
  * PAPER.md:81 kept for every row): every probe row i in order gets
  * left_out[i] = its build row, or -1 without a match (n_probe x int64,

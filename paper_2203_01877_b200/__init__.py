@@ -35,7 +35,7 @@ MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
 EXPORTED = [
     "tqp_abi_version", "tqp_ctx_create", "tqp_ctx_destroy", "tqp_ctx_set_stream", "tqp_last_error",
     "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_kernel_stats",
-    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
+    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_pkfk_join_hash", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
     "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge",
 ]
@@ -71,6 +71,7 @@ _sig = {
     "tqp_pkfk_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_semi": ([_vp, Col, _i64, Col, _i64, _int, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_outer": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
+    "tqp_pkfk_join_hash": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_join_payload": ([_vp, Col, _i64, Col, _i64, _P(Col), _int, _P(_vp), _P(Col), _int, _P(_vp), _vp, _vp,
                                _P(_i64)], _int),
     "tqp_smj_prepare": ([_vp, Col, _i64, Col, _i64, _P(_vp), _P(_i64)], _int),
@@ -249,6 +250,18 @@ class Context:
                                                len(pps), po, _ptr(lo), _ptr(ro), ctypes.byref(m)))
         n = m.value
         return ([t[:n] for t in bouts], [t[:n] for t in pouts], (lo[:n], ro[:n]) if indices else None)
+
+    def pkfk_join_hash(self, build_keys, probe_keys):
+        """Hash-join ablation of pkfk_join (same output; not the paper's method)."""
+        self._sync_stream()
+        b = _dev_tensor(build_keys, self.device)
+        p = _dev_tensor(probe_keys, self.device)
+        lo = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        ro = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_pkfk_join_hash(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(lo), _ptr(ro),
+                                            ctypes.byref(m)))
+        return lo[:m.value], ro[:m.value]
 
     def pkfk_outer(self, build_keys, probe_keys, return_mask=False):
         """Probe-side outer join: build row per probe row (-1 = no match), probe rows in order."""
@@ -456,6 +469,10 @@ def smj_join(left, right):
 
 def pkfk_join_payload(build_keys, probe_keys, build_payload=(), probe_payload=(), indices=True):
     return context().pkfk_join_payload(build_keys, probe_keys, build_payload, probe_payload, indices)
+
+
+def pkfk_join_hash(build_keys, probe_keys):
+    return context().pkfk_join_hash(build_keys, probe_keys)
 
 
 def pkfk_outer(build_keys, probe_keys, return_mask=False):

@@ -9,6 +9,7 @@ namespace tqp {
 void pkfk_join(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void pkfk_semi(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int, uint8_t*, int64_t*, int64_t*);
 void pkfk_outer(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, uint8_t*, int64_t*);
+void pkfk_join_hash(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void pkfk_join_payload(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, const tqp_col*, int, void* const*, const tqp_col*, int,
                        void* const*, int64_t*, int64_t*, int64_t*);
 void filter_compact(tqp_ctx*, const tqp_col*, int, int64_t, const tqp_pred*, int, uint8_t*, int64_t*, int64_t*);
@@ -227,6 +228,14 @@ tqp_status tqp_pkfk_join_payload(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, i
         if ((n_bp > 0 && (!bp || !bp_out)) || (n_pp > 0 && (!pp || !pp_out)))
             tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null payload arrays");
         tqp::pkfk_join_payload(c, b, nb, p, np, bp, n_bp, bp_out, pp, n_pp, pp_out, lo, ro, n_out_host);
+    });
+}
+
+tqp_status tqp_pkfk_join_hash(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int64_t* lo, int64_t* ro,
+                              int64_t* n_out_host) {
+    TQP_GUARD(c, {
+        if (!n_out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_hash: null n_out_host");
+        tqp::pkfk_join_hash(c, b, nb, p, np, lo, ro, n_out_host);
     });
 }
 

@@ -499,7 +499,136 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
                                                     : (right_out ? 8.0 * (double)h[0] : 0.0));
     }
 }
+// ---------------------------------------------------------- hash-join ablation
+// the generic hash join the paper compares against (OmniSciDB's
+// hash aggregation / join beat TQP's sort-based operators on Q1 / Q9), as a
+// comparison point for the sort-based PK-FK join on the same GPU. Open addressing, a
+// power-of-two table of >= 2 n_build slots, linear probing; the row slot is claimed by
+// CAS, then the key is written (build and probe are separate launches). The probe
+// writes the same per-row u32 build row as the sort-based probe, so the scan and the
+// order-preserving emit are shared and the output is identical.
+__device__ __forceinline__ uint64_t hmix(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdull;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ull;
+    x ^= x >> 33;
+    return x;
+}
+
+__global__ void hash_build_kernel(const void* keys, int dt, int64_t n, uint64_t mask, long long* tkey, uint32_t* trow,
+                                  int* dup) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = load_as_i64(keys, dt, i);
+        uint64_t slot = hmix((uint64_t)k) & mask;
+        while (true) {
+            const uint32_t prev = atomicCAS(&trow[slot], NOMATCH, (uint32_t)i);
+            if (prev == NOMATCH) {
+                tkey[slot] = k;
+                break;
+            }
+            slot = (slot + 1) & mask;
+        }
+    }
+    (void)dup;
+}
+
+// duplicate build keys: two slots of one probe chain holding the same key
+__global__ void hash_dup_kernel(const long long* tkey, const uint32_t* trow, uint64_t mask, int64_t size, int* dup) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < size; s += (int64_t)gridDim.x * blockDim.x) {
+        if (trow[s] == NOMATCH) continue;
+        const long long k = tkey[s];
+        uint64_t t = hmix((uint64_t)k) & mask;
+        while (t != (uint64_t)s) {   // earlier slots of k's chain
+            if (trow[t] != NOMATCH && tkey[t] == k) { *dup = 1; break; }
+            t = (t + 1) & mask;
+        }
+    }
+}
+
+template <int PDT>
+__global__ void __launch_bounds__(PNT) hash_probe_kernel(const void* probe, int64_t np, uint64_t mask,
+                                                         const long long* __restrict__ tkey,
+                                                         const uint32_t* __restrict__ trow, uint32_t* lft,
+                                                         uint32_t* tcnt) {
+    __shared__ uint32_t s_w[PNW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * PTILE;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < PIPT; i++) {
+        const int64_t row = base + i * PNT + tid;
+        if (row >= np) continue;
+        int64_t k;
+        if (PDT == TQP_I64) k = (int64_t)__ldcs((const long long*)probe + row);
+        else if (PDT == TQP_I32) k = (int64_t)__ldcs((const int*)probe + row);
+        else k = (int64_t)__ldcs((const unsigned char*)probe + row);
+        uint64_t slot = hmix((uint64_t)k) & mask;
+        uint32_t left = NOMATCH;
+        while (true) {
+            const uint32_t r = __ldg(trow + slot);
+            if (r == NOMATCH) break;
+            if (__ldg(tkey + slot) == k) { left = r; break; }
+            slot = (slot + 1) & mask;
+        }
+        __stcs(lft + row, left);
+        cnt += left != NOMATCH;
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < PNW; w++) t += s_w[w];
+        tcnt[blockIdx.x] = t;
+    }
+}
 }  // namespace
+
+void pkfk_join_hash(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int64_t* left_out,
+                    int64_t* right_out, int64_t* n_out_host) {
+    check_col(bk, nb, "hash build");
+    check_col(pk, np, "hash probe");
+    if (np > 0 && (!left_out || !right_out)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_hash: null output");
+    if (nb >= (int64_t(1) << 30) || np >= (int64_t(1) << 40)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_hash: too large");
+    int64_t size = 1;
+    while (size < 2 * std::max<int64_t>(nb, 1)) size <<= 1;
+    const uint64_t mask = (uint64_t)size - 1;
+    DevBuf<long long> tkey(ctx, size);
+    DevBuf<uint32_t> trow(ctx, size);
+    DevBuf<int64_t> pack(ctx, 2);   // [0] pairs, [1] duplicate flag
+    pack.zero();
+    TQP_CUDA(cudaMemsetAsync(trow.get(), 0xFF, (size_t)size * 4, ctx->stream));
+    const int g = (int)std::min<int64_t>(ceil_div(std::max<int64_t>(nb, 1), 256), (int64_t)ctx->num_sms * 8);
+    if (nb > 0) {
+        launch(ctx, "tqp_hash_build", hash_build_kernel, dim3(g), dim3(256), 0, bk.data, bk.dtype, nb, mask, tkey.get(),
+               trow.get(), (int*)(pack.get() + 1));
+        const int gd = (int)std::min<int64_t>(ceil_div(size, 256), (int64_t)ctx->num_sms * 8);
+        launch(ctx, "tqp_hash_build", hash_dup_kernel, dim3(gd), dim3(256), 0, (const long long*)tkey.get(),
+               (const uint32_t*)trow.get(), mask, size, (int*)(pack.get() + 1));
+        ctx->add_bytes("tqp_hash_build", (double)nb * (dtype_size(bk.dtype) + 12.0) + 12.0 * (double)size);
+    }
+    if (np > 0) {
+        const int64_t tiles = ceil_div(np, PTILE);
+        DevBuf<uint32_t> lft(ctx, np), tcnt(ctx, tiles);
+        DevBuf<uint64_t> toff(ctx, tiles + 1);
+        switch (pk.dtype) {
+            case TQP_I64: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_I64>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const long long*)tkey.get(), (const uint32_t*)trow.get(), lft.get(), tcnt.get()); break;
+            case TQP_I32: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_I32>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const long long*)tkey.get(), (const uint32_t*)trow.get(), lft.get(), tcnt.get()); break;
+            default: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_U8>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const long long*)tkey.get(), (const uint32_t*)trow.get(), lft.get(), tcnt.get()); break;
+        }
+        scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
+        launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)lft.get(),
+               (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out, Payload{});
+        TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
+        ctx->add_bytes("tqp_hash_probe", (double)np * dtype_size(pk.dtype));
+    }
+    int64_t h[2];
+    read_back(ctx, h, pack.get(), 16);
+    if (h[1]) fail(TQP_ERR_DUPLICATE_BUILD_KEY, "pkfk_hash: duplicate key on the build side");
+    if (n_out_host) *n_out_host = h[0];
+    if (np > 0) ctx->add_bytes("tqp_pkfk_emit", 16.0 * (double)h[0]);
+}
 
 void pkfk_join(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int64_t* left_out, int64_t* right_out,
                int64_t* n_out_host) {

@@ -109,6 +109,20 @@ def test_pkfk_random_parity(T, nb, np_, span, bd, pd):
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
 
 
+@pytest.mark.parametrize("nb,np_,span", [(0, 100, 10), (1, 5, 3), (5000, 100_001, 20_000), (300_000, 1_000_003, 10**6)])
+def test_pkfk_hash_ablation_parity(T, nb, np_, span):
+    """The hash-join ablation returns exactly the sort-based join's output (and the oracle's)."""
+    rng = np.random.default_rng(nb + np_ + 1)
+    build = (rng.permutation(span)[:nb] - span // 3).astype(np.int64)
+    probe = rng.integers(-span // 2, span, np_).astype(np.int64)
+    lo, ro = T.pkfk_join_hash(cu(build), cu(probe))
+    olo, oro = oracle.pkfk_join(build, probe)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    with pytest.raises(T.TqpError) as e:
+        T.pkfk_join_hash(cu(np.array([7, 3, 7])), cu(probe[:10]))
+    assert e.value.status == T.TQP_ERR_DUPLICATE_BUILD_KEY
+
+
 def test_pkfk_wide_and_extreme_keys(T):
     build = np.array([I64_MIN, I64_MAX, 0, -1, 1 << 40, -(1 << 50)], np.int64)
     probe = np.array([I64_MAX, 5, I64_MIN, -1, 1 << 40, 0, I64_MAX, -(1 << 50) + 1], np.int64)

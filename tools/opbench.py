@@ -31,6 +31,7 @@ def main():
         "cub_sort_probe_i32": lambda: torch.sort(lk32, stable=True),
         "pkfk_join": lambda: ctx.pkfk_join(ok, lk),
         "pkfk_small_build": lambda: ctx.pkfk_join(ok[:65536], lk),
+        "pkfk_hash_ablation": lambda: ctx.pkfk_join_hash(ok, lk),
         "smj_join": lambda: ctx.smj_join(ok, lk),
         "q1_groupby": lambda: ctx.groupby_agg(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS),
         "q6_filter": lambda: ctx.filter_compact(q6, Q6_PREDS),
