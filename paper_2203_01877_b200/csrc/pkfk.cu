@@ -516,31 +516,32 @@ __device__ __forceinline__ uint64_t hmix(uint64_t x) {
     return x;
 }
 
-__global__ void hash_build_kernel(const void* keys, int dt, int64_t n, uint64_t mask, long long* tkey, uint32_t* trow,
-                                  int* dup) {
+// one 16-byte slot per entry (key and row in one sector): words {key lo, key hi, row, pad}
+__global__ void hash_build_kernel(const void* keys, int dt, int64_t n, uint64_t mask, uint4* slots) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = load_as_i64(keys, dt, i);
         uint64_t slot = hmix((uint64_t)k) & mask;
         while (true) {
-            const uint32_t prev = atomicCAS(&trow[slot], NOMATCH, (uint32_t)i);
-            if (prev == NOMATCH) {
-                tkey[slot] = k;
+            uint32_t* row = &slots[slot].z;
+            if (atomicCAS(row, NOMATCH, (uint32_t)i) == NOMATCH) {
+                slots[slot].x = (uint32_t)k;
+                slots[slot].y = (uint32_t)((uint64_t)k >> 32);
                 break;
             }
             slot = (slot + 1) & mask;
         }
     }
-    (void)dup;
 }
 
 // duplicate build keys: two slots of one probe chain holding the same key
-__global__ void hash_dup_kernel(const long long* tkey, const uint32_t* trow, uint64_t mask, int64_t size, int* dup) {
+__global__ void hash_dup_kernel(const uint4* slots, uint64_t mask, int64_t size, int* dup) {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < size; s += (int64_t)gridDim.x * blockDim.x) {
-        if (trow[s] == NOMATCH) continue;
-        const long long k = tkey[s];
-        uint64_t t = hmix((uint64_t)k) & mask;
-        while (t != (uint64_t)s) {   // earlier slots of k's chain
-            if (trow[t] != NOMATCH && tkey[t] == k) { *dup = 1; break; }
+        const uint4 e = slots[s];
+        if (e.z == NOMATCH) continue;
+        uint64_t t = hmix(((uint64_t)e.y << 32) | e.x) & mask;
+        while (t != (uint64_t)s) {   // earlier slots of the key's chain
+            const uint4 f = slots[t];
+            if (f.z != NOMATCH && f.x == e.x && f.y == e.y) { *dup = 1; break; }
             t = (t + 1) & mask;
         }
     }
@@ -548,8 +549,7 @@ __global__ void hash_dup_kernel(const long long* tkey, const uint32_t* trow, uin
 
 template <int PDT>
 __global__ void __launch_bounds__(PNT) hash_probe_kernel(const void* probe, int64_t np, uint64_t mask,
-                                                         const long long* __restrict__ tkey,
-                                                         const uint32_t* __restrict__ trow, uint32_t* lft,
+                                                         const uint4* __restrict__ slots, uint32_t* lft,
                                                          uint32_t* tcnt) {
     __shared__ uint32_t s_w[PNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -565,10 +565,10 @@ __global__ void __launch_bounds__(PNT) hash_probe_kernel(const void* probe, int6
         else k = (int64_t)__ldcs((const unsigned char*)probe + row);
         uint64_t slot = hmix((uint64_t)k) & mask;
         uint32_t left = NOMATCH;
-        while (true) {
-            const uint32_t r = __ldg(trow + slot);
-            if (r == NOMATCH) break;
-            if (__ldg(tkey + slot) == k) { left = r; break; }
+        while (true) {   // one 16-byte load per slot visited
+            const uint4 e = __ldg(slots + slot);
+            if (e.z == NOMATCH) break;
+            if ((((uint64_t)e.y << 32) | e.x) == (uint64_t)k) { left = e.z; break; }
             slot = (slot + 1) & mask;
         }
         __stcs(lft + row, left);
@@ -594,28 +594,26 @@ void pkfk_join_hash(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np
     int64_t size = 1;
     while (size < 2 * std::max<int64_t>(nb, 1)) size <<= 1;
     const uint64_t mask = (uint64_t)size - 1;
-    DevBuf<long long> tkey(ctx, size);
-    DevBuf<uint32_t> trow(ctx, size);
+    DevBuf<uint4> slots(ctx, size);
     DevBuf<int64_t> pack(ctx, 2);   // [0] pairs, [1] duplicate flag
     pack.zero();
-    TQP_CUDA(cudaMemsetAsync(trow.get(), 0xFF, (size_t)size * 4, ctx->stream));
+    TQP_CUDA(cudaMemsetAsync(slots.get(), 0xFF, (size_t)size * 16, ctx->stream));
     const int g = (int)std::min<int64_t>(ceil_div(std::max<int64_t>(nb, 1), 256), (int64_t)ctx->num_sms * 8);
     if (nb > 0) {
-        launch(ctx, "tqp_hash_build", hash_build_kernel, dim3(g), dim3(256), 0, bk.data, bk.dtype, nb, mask, tkey.get(),
-               trow.get(), (int*)(pack.get() + 1));
+        launch(ctx, "tqp_hash_build", hash_build_kernel, dim3(g), dim3(256), 0, bk.data, bk.dtype, nb, mask, slots.get());
         const int gd = (int)std::min<int64_t>(ceil_div(size, 256), (int64_t)ctx->num_sms * 8);
-        launch(ctx, "tqp_hash_build", hash_dup_kernel, dim3(gd), dim3(256), 0, (const long long*)tkey.get(),
-               (const uint32_t*)trow.get(), mask, size, (int*)(pack.get() + 1));
-        ctx->add_bytes("tqp_hash_build", (double)nb * (dtype_size(bk.dtype) + 12.0) + 12.0 * (double)size);
+        launch(ctx, "tqp_hash_build", hash_dup_kernel, dim3(gd), dim3(256), 0, (const uint4*)slots.get(), mask, size,
+               (int*)(pack.get() + 1));
+        ctx->add_bytes("tqp_hash_build", (double)nb * (dtype_size(bk.dtype) + 16.0) + 16.0 * (double)size);
     }
     if (np > 0) {
         const int64_t tiles = ceil_div(np, PTILE);
         DevBuf<uint32_t> lft(ctx, np), tcnt(ctx, tiles);
         DevBuf<uint64_t> toff(ctx, tiles + 1);
         switch (pk.dtype) {
-            case TQP_I64: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_I64>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const long long*)tkey.get(), (const uint32_t*)trow.get(), lft.get(), tcnt.get()); break;
-            case TQP_I32: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_I32>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const long long*)tkey.get(), (const uint32_t*)trow.get(), lft.get(), tcnt.get()); break;
-            default: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_U8>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const long long*)tkey.get(), (const uint32_t*)trow.get(), lft.get(), tcnt.get()); break;
+            case TQP_I64: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_I64>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const uint4*)slots.get(), lft.get(), tcnt.get()); break;
+            case TQP_I32: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_I32>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const uint4*)slots.get(), lft.get(), tcnt.get()); break;
+            default: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_U8>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const uint4*)slots.get(), lft.get(), tcnt.get()); break;
         }
         scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
         launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)lft.get(),
