@@ -612,6 +612,18 @@ def test_groupby_high_cardinality(T):
     check_groupby(T, got, want, aggs)
 
 
+def test_groupby_high_cardinality_sf1(T):
+    """General (sorted-tile) path at SF1: ~1.5M groups over 6M lineitem rows, vs the oracle."""
+    _, li = tpch_orders_lineitem(1.0, seed=42, device="cuda")
+    cols = [li["l_orderkey"], li["l_quantity"], li["l_extendedprice"], li["l_shipdate"]]
+    aggs = [("sum", [(1, 0, 1), (2, 0, 1)]), ("count", []), ("min", [(3, 0, 1)]), ("max", [(2, 0, -1)]),
+            ("avg", [(1, 0, 1)])]
+    preds = [(3, "ge", 9000)]
+    got = T.groupby_agg(cols, [0], aggs, preds)
+    want = oracle.groupby_agg([npy(c) for c in cols], [0], aggs, preds)
+    check_groupby(T, got, want, aggs)
+
+
 def test_groupby_empty_and_global(T):
     e = cu(np.array([], np.int64))
     got = T.groupby_agg([e], [0], [("sum", [(0, 0, 1)])])
