@@ -927,7 +927,7 @@ __device__ void flush_nokey(const Phase1Args& a, NoKeyAcc& acc, Work& w) {
 // k * gridDim.x are streamed into NS shared-memory stages with TMA bulk copies
 // (mbarrier completion; stage s is refilled as soon as every thread is done with it);
 // tail tiles and unaligned columns take plain cooperative loads.
-template <int NT, typename F>
+template <int NT, bool ABORTABLE = false, typename F>
 __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem, uint64_t* mbar, F&& process) {
     constexpr int TR = NT * GPT;   // rows per tile
     const int NS = a.n_stages;
@@ -949,12 +949,25 @@ __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem
             uses[s]++;
         }
     }
+    uint32_t done[4] = {0, 0, 0, 0};
+    __shared__ int s_abort;
     for (int64_t k = 0;; k++) {
         const int64_t t = blockIdx.x + k * gridDim.x;
         if (t >= a.n_tiles) break;
         const int s = (int)(k % NS);
+        if (ABORTABLE) {   // partial capacity exceeded somewhere: stop (the host takes the sort path)
+            if (tid == 0) s_abort = (*reinterpret_cast<volatile int*>(a.overflow) & 2) != 0;
+            __syncthreads();
+            if (s_abort) {
+                if (tid == 0)   // bulk copies still landing in this CTA's stages complete first
+                    for (int st = 0; st < NS; st++)
+                        if (uses[st] > done[st]) mbar_wait(&mbar[st], (uses[st] - 1) & 1);
+                break;
+            }
+        }
         if (eligible(t)) {
             mbar_wait(&mbar[s], (uses[s] - 1) & 1);
+            done[s]++;
         } else {   // tail tile or unaligned columns: plain cooperative loads
             const int64_t row0 = t * TR;
             const int nrows = (int)min((int64_t)TR, a.n - row0);
@@ -1015,10 +1028,12 @@ __global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
     }
     nacc.count = 0;
     nacc.ovf = 0;
-    tile_pipeline<GNT>(a, smem, w.mbar, [&](const uint8_t* st, int64_t t) {
-        if (nokey) process_tile_nokey(a, st, t, nacc, reinterpret_cast<NoKeyWork&>(w));
-        else process_tile(a, st, w, t);
-    });
+    if (nokey)
+        tile_pipeline<GNT>(a, smem, w.mbar, [&](const uint8_t* st, int64_t t) {
+            process_tile_nokey(a, st, t, nacc, reinterpret_cast<NoKeyWork&>(w));
+        });
+    else
+        tile_pipeline<GNT, true>(a, smem, w.mbar, [&](const uint8_t* st, int64_t t) { process_tile(a, st, w, t); });
     if (nokey) flush_nokey(a, nacc, w);
 }
 
@@ -1657,6 +1672,146 @@ struct Partials {   // phase-1 output / phase-2 input
 };
 
 // Phase 2: global sort of partial keys, segment ids, exact accumulation.
+// ------------------------------------------------ sort path (high cardinality)
+// Alg. 2 as written: when tiles do not reduce (about as many keys
+// per tile as rows), the rows' packed keys are radix-sorted with their permutation,
+// segment heads give the groups (uniqueConsecutive), and every (op, expression) pair
+// is evaluated in sorted order from the original columns and reduced per segment.
+constexpr int SPT = 8;    // consecutive sorted positions per thread in the reduction
+struct SortPathArgs {
+    int64_t m;                        // selected rows
+    const int64_t* sel;               // selected rows (null: all rows)
+    const uint32_t* perm;             // sorted position -> index into the selection
+    const uint32_t* gid;              // sorted position -> group
+    int n_keys;
+    const void* kcol[TQP_MAX_KEYS];
+    int kdt[TQP_MAX_KEYS];
+    const unsigned long long* krange;
+    uint64_t* pk;                     // packed keys (key kernel output)
+    int n_pairs;
+    int pop[TQP_MAX_AGGS];
+    int pnf[TQP_MAX_AGGS];
+    const void* fcol[TQP_MAX_AGGS][3];
+    int fdt[TQP_MAX_AGGS][3];
+    int fsign[TQP_MAX_AGGS][3];
+    int64_t fadd[TQP_MAX_AGGS][3];
+    int64_t* gcount;
+    uint64_t* glo[TQP_MAX_AGGS];
+    int64_t* ghi[TQP_MAX_AGGS];
+    int* overflow;
+};
+
+__global__ void sp_keys_kernel(SortPathArgs a) {
+    __shared__ uint64_t s_kmin[TQP_MAX_KEYS];
+    __shared__ int s_sh[TQP_MAX_KEYS];
+    if (threadIdx.x == 0) {
+        int wd[TQP_MAX_KEYS];
+        key_layout(a.krange, a.n_keys, s_kmin, s_sh, wd);
+    }
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = a.sel ? a.sel[i] : i;
+        uint64_t k = 0;
+        for (int c = 0; c < a.n_keys; c++)
+            k |= (key_part(load_as_i64(a.kcol[c], a.kdt[c], row), a.kdt[c]) - s_kmin[c]) << s_sh[c];
+        a.pk[i] = k;
+    }
+}
+
+// per thread: SPT consecutive sorted positions; segments wholly inside the range are
+// stored directly, the (at most two) that continue into a neighbour use atomics
+__global__ void __launch_bounds__(256) sp_reduce_kernel(SortPathArgs a) {
+    const int64_t p0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * SPT;
+    if (p0 >= a.m) return;
+    const int64_t p1 = min(p0 + (int64_t)SPT, a.m);
+    const uint32_t gprev = p0 > 0 ? a.gid[p0 - 1] : 0xFFFFFFFFu;
+    const uint32_t gnext = p1 < a.m ? a.gid[p1] : 0xFFFFFFFFu;
+    int64_t rows[SPT];
+    uint32_t g[SPT];
+    const int cnt = (int)(p1 - p0);
+#pragma unroll
+    for (int i = 0; i < SPT; i++) {
+        if (i < cnt) {
+            g[i] = a.gid[p0 + i];
+            const uint32_t q = a.perm[p0 + i];
+            rows[i] = a.sel ? a.sel[q] : (int64_t)q;
+        }
+    }
+    // a segment is shared with a neighbour iff it is this range's first (gprev equal)
+    // or last (gnext equal) segment
+    auto shared_seg = [&](uint32_t gg) { return gg == gprev || gg == gnext; };
+    {   // counts
+        int64_t c = 0;
+        for (int i = 0; i < cnt; i++) {
+            c++;
+            if (i + 1 == cnt || g[i + 1] != g[i]) {
+                if (shared_seg(g[i])) atomicAdd((unsigned long long*)&a.gcount[g[i]], (unsigned long long)c);
+                else a.gcount[g[i]] = c;
+                c = 0;
+            }
+        }
+    }
+    bool ovf = false;
+    for (int j = 0; j < a.n_pairs; j++) {
+        const int op = a.pop[j];
+        unsigned __int128 acc = 0;
+        int64_t mm = op == P_MIN ? INT64_MAX : INT64_MIN;
+        // the expression for all rows of the range first: the gathers are independent and in flight together
+        int64_t vv[SPT];
+#pragma unroll
+        for (int i = 0; i < SPT; i++) vv[i] = 1;
+        for (int f = 0; f < a.pnf[j]; f++) {   // prod_f (add_f + sign_f * x_f), overflow-checked
+            const int64_t add = a.fadd[j][f];
+            const bool neg = a.fsign[j][f] < 0;
+            const void* col = a.fcol[j][f];
+            const int dt = a.fdt[j][f];
+            int64_t x[SPT];
+#pragma unroll
+            for (int i = 0; i < SPT; i++) x[i] = i < cnt ? load_as_i64(col, dt, rows[i]) : 0;
+#pragma unroll
+            for (int i = 0; i < SPT; i++) {
+                int64_t t;
+                if (neg) {
+                    t = (int64_t)((uint64_t)add - (uint64_t)x[i]);
+                    ovf |= i < cnt && ((add ^ x[i]) & (add ^ t)) < 0;
+                } else {
+                    t = (int64_t)((uint64_t)add + (uint64_t)x[i]);
+                    ovf |= i < cnt && ((add ^ t) & (x[i] ^ t)) < 0;
+                }
+                if (f == 0) {
+                    vv[i] = t;
+                } else {
+                    const int64_t lo = (int64_t)((uint64_t)vv[i] * (uint64_t)t);
+                    ovf |= i < cnt && __mul64hi(vv[i], t) != (lo >> 63);
+                    vv[i] = lo;
+                }
+            }
+        }
+        for (int i = 0; i < cnt; i++) {
+            const int64_t v = vv[i];
+            if (op == P_SUM) acc += (unsigned __int128)(__int128)v;
+            else mm = op == P_MIN ? min(mm, v) : max(mm, v);
+            if (i + 1 == cnt || g[i + 1] != g[i]) {
+                const uint32_t gg = g[i];
+                if (op == P_SUM) {
+                    if (shared_seg(gg)) atomic_add_i128(&a.glo[j][gg], &a.ghi[j][gg], acc);
+                    else { a.glo[j][gg] = (uint64_t)acc; a.ghi[j][gg] = (int64_t)(acc >> 64); }
+                    acc = 0;
+                } else {
+                    if (shared_seg(gg)) {
+                        if (op == P_MIN) atomicMin((long long*)&a.glo[j][gg], (long long)mm);
+                        else atomicMax((long long*)&a.glo[j][gg], (long long)mm);
+                    } else {
+                        a.glo[j][gg] = (uint64_t)mm;
+                    }
+                    mm = op == P_MIN ? INT64_MAX : INT64_MIN;
+                }
+            }
+        }
+    }
+    if (ovf) atomicOr(a.overflow, 1);
+}
+
 void phase2(tqp_ctx* ctx, tqp_groupby_plan* PL, Partials& pr, bool split) {
     const int64_t P = pr.P;
     SortOut so;
@@ -1714,6 +1869,100 @@ void phase2(tqp_ctx* ctx, tqp_groupby_plan* PL, Partials& pr, bool split) {
     int64_t G = 0;
     read_back(ctx, &G, Gd.get(), 8);
     PL->G = G;
+}
+
+// The sort path (see sp_reduce_kernel): selection, packed keys, global radix sort with
+// the permutation, segment ids, and one reduction pass over the sorted positions.
+void sort_path(tqp_ctx* ctx, tqp_groupby_plan* PL, const tqp_col* cols, int n_cols, int64_t n, const int32_t* key_idx,
+               int n_keys, const tqp_pred* preds, int n_preds, const int (*pf)[3], const int (*ps)[3],
+               const int64_t (*pa)[3], const int* pnf, int64_t* n_groups_host) {
+    DevBuf<int64_t> sel;
+    int64_t m = n;
+    if (n_preds > 0) {
+        sel.alloc(ctx, n);
+        filter_compact(ctx, cols, n_cols, n, preds, n_preds, nullptr, sel.get(), &m);
+    }
+    PL->empty_global = false;
+    if (m == 0) {
+        PL->G = 0;
+        *n_groups_host = 0;
+        return;
+    }
+    SortPathArgs a{};
+    a.m = m;
+    a.sel = n_preds > 0 ? sel.get() : nullptr;
+    a.n_keys = n_keys;
+    double kb = 0;
+    for (int k = 0; k < n_keys; k++) {
+        a.kcol[k] = cols[key_idx[k]].data;
+        a.kdt[k] = cols[key_idx[k]].dtype;
+        kb += (double)dtype_size(a.kdt[k]);
+    }
+    a.krange = PL->krange.get();
+    DevBuf<uint64_t> pk(ctx, m);
+    a.pk = pk.get();
+    const int g = (int)std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->num_sms * 8);
+    launch(ctx, "tqp_groupby_keys", sp_keys_kernel, dim3(g), dim3(256), 0, a);
+    ctx->add_bytes("tqp_groupby_keys", (kb + 8.0 + (a.sel ? 8.0 : 0.0)) * (double)m);
+    SortOut so;
+    so.want_perm32 = true;
+    DevBuf<uint64_t> sk(ctx, m);
+    so.sorted_u = sk.get();
+    radix_sort(ctx, pk.get(), DT_U64, m, false, so);
+    pk.release();
+    DevBuf<uint32_t> gid(ctx, m);
+    DevBuf<int64_t> hd(ctx, 2);   // [0] G, [1] overflow flag
+    hd.zero();
+    PL->gkey.alloc(ctx, m);
+    {
+        const int64_t t2 = ceil_div(m, QTILE);
+        DevBuf<uint64_t> status(ctx, t2);
+        DevBuf<unsigned long long> counter(ctx, 1);
+        status.zero();
+        counter.zero();
+        launch(ctx, "tqp_groupby_gid", gb_gid_kernel, dim3((unsigned)t2), dim3(QNT), 0, (const uint64_t*)sk.get(), m,
+               gid.get(), PL->gkey.get(), hd.get(), status.get(), counter.get(), t2);
+        ctx->add_bytes("tqp_groupby_gid", 12.0 * (double)m);
+    }
+    PL->gcount.alloc(ctx, m);
+    PL->gcount.zero();
+    a.n_pairs = PL->n_pairs;
+    const int ig = (int)std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->num_sms * 8);
+    double vb = 0;
+    for (int j = 0; j < PL->n_pairs; j++) {
+        a.pop[j] = PL->pop[j];
+        a.pnf[j] = pnf[j];
+        for (int f = 0; f < pnf[j]; f++) {
+            a.fcol[j][f] = cols[pf[j][f]].data;
+            a.fdt[j][f] = cols[pf[j][f]].dtype;
+            a.fsign[j][f] = ps[j][f];
+            a.fadd[j][f] = pa[j][f];
+            vb += 32.0;   // one gathered sector per value
+        }
+        PL->glo[j].alloc(ctx, m);
+        a.glo[j] = PL->glo[j].get();
+        if (PL->pop[j] == P_SUM) {
+            PL->ghi[j].alloc(ctx, m);
+            a.ghi[j] = PL->ghi[j].get();
+            PL->glo[j].zero();
+            PL->ghi[j].zero();
+        } else {
+            launch(ctx, "tqp_groupby_init", gb_init_kernel, dim3(ig), dim3(256), 0, PL->glo[j].get(), m,
+                   PL->pop[j] == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+        }
+    }
+    a.perm = so.perm32.get();
+    a.gid = gid.get();
+    a.gcount = PL->gcount.get();
+    a.overflow = (int*)(hd.get() + 1);
+    const int rg = (int)ceil_div(ceil_div(m, SPT), 256);
+    launch(ctx, "tqp_groupby_accumulate", sp_reduce_kernel, dim3(rg), dim3(256), 0, a);
+    ctx->add_bytes("tqp_groupby_accumulate", (8.0 + (a.sel ? 8.0 : 0.0) + vb) * (double)m);
+    int64_t h[2];
+    read_back(ctx, h, hd.get(), 16);
+    if (h[1]) fail(TQP_ERR_OVERFLOW, "groupby: int64 overflow in an aggregate expression");
+    PL->G = h[0];
+    *n_groups_host = PL->G;
 }
 
 // Key-column ranges on the device (no host sync): min in kr[0..7], max in kr[8..15].
@@ -2091,6 +2340,12 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             }
             pr.P = (int64_t)h[0];
             if (!(o & 2)) break;
+            if (n_keys > 0 && n < (int64_t(1) << 30)) {
+                // tiles do not reduce (more than 64 keys per 1024 rows on average):
+                // Alg. 2 directly -- global sort of the packed keys + segmented reduction
+                sort_path(ctx, PL, cols, n_cols, n, key_idx, n_keys, preds, n_preds, pf, ps, pa, pnf, n_groups_host);
+                return PL;
+            }
             cap = std::max<int64_t>(n, 1);   // more distinct keys per tile than estimated: full capacity
         }
         {   // algorithmic bytes: distinct referenced columns read once, partial records written

@@ -34,6 +34,10 @@ void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
                 uint32_t* th0 = nullptr);
 size_t sort_hist0_words(int64_t n);
 
+// Filter + compaction (filter.cu), used by the group-by sort path for its selection.
+void filter_compact(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, const tqp_pred* preds, int n_preds,
+                    uint8_t* mask_out, int64_t* sel_out, int64_t* n_sel_host);
+
 // Exclusive / inclusive scans over device arrays (decoupled look-back).
 void iota_i64(tqp_ctx* ctx, int64_t* p, int64_t n);
 void scan_max_u32_exclusive(tqp_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t n);

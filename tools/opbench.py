@@ -36,6 +36,9 @@ def main():
         "q1_groupby": lambda: ctx.groupby_agg(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS),
         "q6_filter": lambda: ctx.filter_compact(q6, Q6_PREDS),
         "q6_sum": lambda: ctx.groupby_agg(q6, [], Q6_AGGS, Q6_PREDS),
+        # high cardinality (general sorted-tile path): 15M groups
+        "gb_orderkey": lambda: ctx.groupby_agg([lk, li["l_quantity"], li["l_extendedprice"]], [0],
+                                               [("sum", [(1, 0, 1)]), ("count", []), ("max", [(2, 0, 1)])]),
     }
     out = {}
     only = sys.argv[2].split(",") if len(sys.argv) > 2 else None
