@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <map>
+#include <mutex>
+#include <tuple>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -142,9 +144,39 @@ inline void launch(tqp_ctx* ctx, const char* name, void (*k)(KArgs...), dim3 gri
     }
 }
 
+// Dynamic shared-memory limit and occupancy per (kernel, block size, bytes), cached: the
+// runtime queries cost host time while the GPU waits right after a readback.
+inline std::mutex& kcache_mutex() {
+    static std::mutex m;
+    return m;
+}
 template <typename K>
 inline void set_smem(K* k, size_t bytes) {
+    static std::map<std::pair<const void*, int>, size_t> done;   // (kernel, device) -> limit set
+    int dev = 0;
+    TQP_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> g(kcache_mutex());
+    size_t& cur = done[{(const void*)k, dev}];
+    if (bytes <= cur) return;
     TQP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    cur = bytes;
+}
+template <typename K>
+inline int occupancy(K* k, int nt, size_t smem) {
+    static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+    int dev = 0;
+    TQP_CUDA(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> g(kcache_mutex());
+        auto it = cache.find({(const void*)k, dev, nt, smem});
+        if (it != cache.end()) return it->second;
+    }
+    set_smem(k, smem);
+    int occ = 0;
+    TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nt, smem));
+    std::lock_guard<std::mutex> g(kcache_mutex());
+    cache[{(const void*)k, dev, nt, smem}] = occ;
+    return occ;
 }
 
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -2187,13 +2187,7 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
                         const size_t sm = (size_t)ns * stage + hdr + accb;
                         if (sm > 227 * 1024) continue;
                         int occ = 0;
-                        if (nt == 128) {
-                            set_smem(gb_dense_kernel<128>, sm);
-                            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_dense_kernel<128>, nt, sm));
-                        } else {
-                            set_smem(gb_dense_kernel<256>, sm);
-                            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_dense_kernel<256>, nt, sm));
-                        }
+                        occ = nt == 128 ? occupancy(gb_dense_kernel<128>, nt, sm) : occupancy(gb_dense_kernel<256>, nt, sm);
                         const int wps = occ * nt / 32, st = occ * ns;
                         if (occ > 0 && (wps > best_w || (wps == best_w && st > best_st))) {
                             best_w = wps;
@@ -2235,9 +2229,7 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
             // wants more bytes in flight; keyed tiles are compute-heavy and prefer 2 CTAs/SM
             a.n_stages = ((size_t)4 * a.stage_bytes + sizeof(NoKeyWork) <= 112 * 1024) ? 4 : 2;
             nokey_smem = (size_t)a.n_stages * a.stage_bytes + sizeof(NoKeyWork);
-            set_smem(gb_phase1_kernel, nokey_smem);
-            int occ = 1;
-            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_phase1_kernel, GNT, nokey_smem));
+            const int occ = occupancy(gb_phase1_kernel, GNT, nokey_smem);
             nokey_grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
         }
         for (int attempt = 0; attempt < 3; attempt++) {
@@ -2285,9 +2277,7 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
                 a.n_stages = 2;
                 const size_t smem = (size_t)a.n_stages * a.stage_bytes + sizeof(Work);
                 if (smem > 227 * 1024) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: referenced columns too wide");
-                set_smem(gb_phase1_kernel, smem);
-                int occ = 1;
-                TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gb_phase1_kernel, GNT, smem));
+                const int occ = occupancy(gb_phase1_kernel, GNT, smem);
                 const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
                 launch(ctx, "tqp_groupby_tile", gb_phase1_kernel, dim3((unsigned)grid), dim3(GNT), smem, a);
             }

@@ -640,9 +640,7 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
             constexpr int INM = decltype(m)::value;
             constexpr size_t smem = scatter_tma_smem<KT, INM, IPT, RB>();
             auto* kfn = scatter_tma_kernel<KT, INM, IPT, RB>;
-            set_smem(kfn, smem);
-            int occ = 1;
-            TQP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, NT, smem));
+            const int occ = occupancy(kfn, NT, smem);
             const int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
             launch(ctx, "tqp_sort_scatter", kfn, dim3((unsigned)grid), dim3(NT), smem, a, tiles, aligned);
         });
