@@ -1,0 +1,90 @@
+"""Per-configuration timings for every BASELINE.json config on one B200:
+small configs as latency (launch-bound), large ones as throughput. Not the driver's bench
+line (bench.py times the SF10 hot-path step); this is the context table in DESIGN.md §10.
+
+usage: python tools/configs_bench.py [--out profiles/configs_r01.json] [--skip-sf100]
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2203_01877_b200 as T                                   # noqa: E402
+from datagen import tpch_orders_lineitem, uniform_keys, zipf_keys   # noqa: E402
+from datagen.queries import (Q1_AGGS, Q1_COLS, Q1_KEYS, Q1_PREDS,   # noqa: E402
+                             Q6_AGGS, Q6_COLS, Q6_PREDS, columns)
+
+
+def timed(f, reps=20, warm=3):
+    """Median and min device time (ms) of f() over reps runs, CUDA events, one run each."""
+    for _ in range(warm):
+        f()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        f()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts), min(ts)
+
+
+def tpch_ops(sf, which, reps):
+    orders, li = tpch_orders_lineitem(sf, seed=42, device="cuda")
+    ok, lk = orders["o_orderkey"], li["l_orderkey"]
+    q1, q6 = columns(li, Q1_COLS), columns(li, Q6_COLS)
+    ops = {"pkfk_join": lambda: T.pkfk_join(ok, lk),
+           "q1_groupby": lambda: T.groupby_agg(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS),
+           "q6_filter": lambda: T.filter_compact(q6, Q6_PREDS),
+           "q6_sum": lambda: T.groupby_agg(q6, [], Q6_AGGS, Q6_PREDS)}
+    out = {"lineitem_rows": lk.numel(), "orders_rows": ok.numel()}
+    for name in which:
+        med, mn = timed(ops[name], reps)
+        out[name] = {"median_ms": round(med, 4), "min_ms": round(mn, 4),
+                     "rows_per_s": lk.numel() / (med * 1e-3)}
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--skip-sf100", action="store_true")
+    a = ap.parse_args()
+    res = {}
+    res["c0_sf0.01"] = tpch_ops(0.01, ["pkfk_join", "q1_groupby"], 50)
+    res["c1_sf1"] = tpch_ops(1.0, ["q6_filter", "q6_sum", "q1_groupby"], 30)
+    res["c2_sf10"] = tpch_ops(10.0, ["pkfk_join"], 20)
+    # c3: Zipf(s=1) left x uniform right, 100M x 100M: prepare + full expand
+    n = 100_000_000
+    left = zipf_keys(n, n, seed=42, device="cuda")
+    right = uniform_keys(n, n, seed=43, device="cuda")
+    ctx = T.context()
+
+    def smj():
+        plan = ctx.smj_prepare(left, right)
+        lo, ro = plan.expand(0, plan.size)
+        plan.release()
+        return plan.size
+    size = smj()
+    med, mn = timed(smj, 5, 1)
+    res["c3_zipf_smj_100m"] = {"pairs": size, "median_ms": round(med, 3), "min_ms": round(mn, 3),
+                               "pairs_per_s": size / (med * 1e-3), "input_rows_per_s": 2 * n / (med * 1e-3)}
+    del left, right
+    torch.cuda.empty_cache()
+    if not a.skip_sf100:
+        res["c4_sf100_one_gpu"] = tpch_ops(100.0, ["pkfk_join", "q1_groupby"], 5)
+    print(json.dumps(res, indent=1))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
