@@ -114,6 +114,13 @@ tqp_status tqp_sort(tqp_ctx* ctx, tqp_col keys, int64_t n, int descending,
 tqp_status tqp_pkfk_join(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
                          int64_t* left_out_idx, int64_t* right_out_idx, int64_t* n_out_host);
 
+/* tqp_pkfk_join with int32 index outputs (output-width
+ * variant): identical pairs and order, written as int32 (half the output bytes of
+ * the emit pass). Requires n_build < 2^31 and n_probe < 2^31, else
+ * TQP_ERR_INVALID_ARGUMENT. Synchronises twice. */
+tqp_status tqp_pkfk_join_i32(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
+                             int32_t* left_out_idx, int32_t* right_out_idx, int64_t* n_out_host);
+
 /* Left-semi / left-anti variant ("left-semi, and left-anti
  * joins"): match_out (nullable, n_probe x u8) = 1 iff the probe row has a build
  * match; sel_out (nullable, capacity n_probe x int64) = ascending probe rows
@@ -171,6 +178,10 @@ tqp_status tqp_smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t n_left, tqp_col r
                            tqp_smj_plan** plan, int64_t* out_size_host);
 tqp_status tqp_smj_expand(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin, int64_t end,
                           int64_t* left_out_idx, int64_t* right_out_idx);
+/* tqp_smj_expand writing int32 indices (same pairs, half the bytes). Requires
+ * n_left < 2^31 and n_right < 2^31, else TQP_ERR_INVALID_ARGUMENT. */
+tqp_status tqp_smj_expand_i32(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin, int64_t end,
+                              int32_t* left_out_idx, int32_t* right_out_idx);
 void tqp_smj_release(tqp_ctx* ctx, tqp_smj_plan* plan);
 /* prepare + expand of everything into caller buffers of `capacity` pairs.
  * If capacity < outSize: TQP_ERR_CAPACITY and *n_out_host = outSize. */

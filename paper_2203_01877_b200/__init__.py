@@ -35,7 +35,8 @@ MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
 EXPORTED = [
     "tqp_abi_version", "tqp_ctx_create", "tqp_ctx_destroy", "tqp_ctx_set_stream", "tqp_last_error",
     "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_kernel_stats",
-    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_pkfk_join_hash", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_release",
+    "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_pkfk_join_hash",
+    "tqp_pkfk_join_i32", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_expand_i32", "tqp_smj_release",
     "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge",
 ]
@@ -69,6 +70,7 @@ _sig = {
                               _P(ctypes.c_double), _int, _P(_int)], _int),
     "tqp_sort": ([_vp, Col, _i64, _int, _vp, _vp], _int),
     "tqp_pkfk_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
+    "tqp_pkfk_join_i32": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_semi": ([_vp, Col, _i64, Col, _i64, _int, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_outer": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_join_hash": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
@@ -76,6 +78,7 @@ _sig = {
                                _P(_i64)], _int),
     "tqp_smj_prepare": ([_vp, Col, _i64, Col, _i64, _P(_vp), _P(_i64)], _int),
     "tqp_smj_expand": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
+    "tqp_smj_expand_i32": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "tqp_smj_release": ([_vp, _vp], None),
     "tqp_smj_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _i64, _P(_i64)], _int),
     "tqp_filter_compact": ([_vp, _P(Col), _int, _i64, _P(Pred), _int, _vp, _vp, _P(_i64)], _int),
@@ -204,16 +207,19 @@ class Context:
         self._check(_lib.tqp_sort(self._h, _col(k), n, int(bool(descending)), _ptr(out), _ptr(perm)))
         return out, perm
 
-    def pkfk_join(self, build_keys, probe_keys):
-        """PK-FK join -> (left_idx, right_idx) int64, ascending probe row. PAPER.md:55-100."""
+    def pkfk_join(self, build_keys, probe_keys, index_dtype=torch.int64):
+        """PK-FK join -> (left_idx, right_idx), ascending probe row. PAPER.md:55-100.
+        index_dtype=torch.int32 selects tqp_pkfk_join_i32 (both sides < 2^31 rows)."""
         self._sync_stream()
         b = _dev_tensor(build_keys, self.device)
         p = _dev_tensor(probe_keys, self.device)
-        lo = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
-        ro = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        if index_dtype not in (torch.int64, torch.int32):
+            raise ValueError("index_dtype must be torch.int64 or torch.int32")
+        lo = torch.empty(p.numel(), dtype=index_dtype, device=self.device)
+        ro = torch.empty(p.numel(), dtype=index_dtype, device=self.device)
         m = ctypes.c_int64(0)
-        self._check(_lib.tqp_pkfk_join(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(lo), _ptr(ro),
-                                       ctypes.byref(m)))
+        fn = _lib.tqp_pkfk_join if index_dtype == torch.int64 else _lib.tqp_pkfk_join_i32
+        self._check(fn(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(lo), _ptr(ro), ctypes.byref(m)))
         return lo[:m.value], ro[:m.value]
 
     def pkfk_semi(self, build_keys, probe_keys, anti=False, return_mask=False):
@@ -386,15 +392,20 @@ class SmjPlan:
     def __init__(self, ctx, handle, size):
         self.ctx, self._h, self.size = ctx, handle, size
 
-    def expand(self, begin, end, out=None):
+    def expand(self, begin, end, out=None, index_dtype=torch.int64):
+        """Pairs [begin, end) as (left_idx, right_idx); int32 outputs (index_dtype or
+        the dtype of `out`) select tqp_smj_expand_i32."""
         self.ctx._sync_stream()
         k = end - begin
         if out is None:
-            lo = torch.empty(k, dtype=torch.int64, device=self.ctx.device)
-            ro = torch.empty(k, dtype=torch.int64, device=self.ctx.device)
+            lo = torch.empty(k, dtype=index_dtype, device=self.ctx.device)
+            ro = torch.empty(k, dtype=index_dtype, device=self.ctx.device)
         else:
             lo, ro = out
-        self.ctx._check(_lib.tqp_smj_expand(self.ctx._h, self._h, begin, end, _ptr(lo), _ptr(ro)))
+        if lo.dtype != ro.dtype or lo.dtype not in (torch.int64, torch.int32) or lo.numel() < k or ro.numel() < k:
+            raise ValueError("expand: outputs must be two int64 or two int32 tensors of >= end-begin elements")
+        fn = _lib.tqp_smj_expand if lo.dtype == torch.int64 else _lib.tqp_smj_expand_i32
+        self.ctx._check(fn(self.ctx._h, self._h, begin, end, _ptr(lo), _ptr(ro)))
         return lo, ro
 
     def release(self):
@@ -451,8 +462,8 @@ def sort(keys, descending=False, return_keys=True):
     return context().sort(keys, descending, return_keys)
 
 
-def pkfk_join(build_keys, probe_keys):
-    return context().pkfk_join(build_keys, probe_keys)
+def pkfk_join(build_keys, probe_keys, index_dtype=torch.int64):
+    return context().pkfk_join(build_keys, probe_keys, index_dtype)
 
 
 def pkfk_semi(build_keys, probe_keys, anti=False, return_mask=False):

@@ -7,6 +7,7 @@
 
 namespace tqp {
 void pkfk_join(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
+void pkfk_join_i32(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int32_t*, int32_t*, int64_t*);
 void pkfk_semi(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int, uint8_t*, int64_t*, int64_t*);
 void pkfk_outer(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, uint8_t*, int64_t*);
 void pkfk_join_hash(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
@@ -14,7 +15,7 @@ void pkfk_join_payload(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, const tqp_c
                        void* const*, int64_t*, int64_t*, int64_t*);
 void filter_compact(tqp_ctx*, const tqp_col*, int, int64_t, const tqp_pred*, int, uint8_t*, int64_t*, int64_t*);
 tqp_smj_plan* smj_prepare(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*);
-void smj_expand(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, int64_t*, int64_t*);
+void smj_expand(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, void*, void*, int);
 void smj_release(tqp_ctx*, tqp_smj_plan*);
 tqp_groupby_plan* groupby_prepare(tqp_ctx*, const tqp_col*, int, int64_t, const int32_t*, int, const tqp_pred*, int,
                                   const tqp_agg*, int, int64_t*);
@@ -215,6 +216,14 @@ tqp_status tqp_pkfk_join(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t n
     });
 }
 
+tqp_status tqp_pkfk_join_i32(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int32_t* lo, int32_t* ro,
+                             int64_t* n_out_host) {
+    TQP_GUARD(c, {
+        if (!n_out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_i32: null n_out_host");
+        tqp::pkfk_join_i32(c, b, nb, p, np, lo, ro, n_out_host);
+    });
+}
+
 tqp_status tqp_pkfk_semi(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int anti, uint8_t* match_out,
                          int64_t* sel_out, int64_t* n_sel_host) {
     TQP_GUARD(c, { tqp::pkfk_semi(c, b, nb, p, np, anti, match_out, sel_out, n_sel_host); });
@@ -256,7 +265,15 @@ tqp_status tqp_smj_expand(tqp_ctx* c, const tqp_smj_plan* plan, int64_t begin, i
                           int64_t* ro) {
     TQP_GUARD(c, {
         if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: null plan");
-        tqp::smj_expand(c, plan, begin, end, lo, ro);
+        tqp::smj_expand(c, plan, begin, end, lo, ro, 0);
+    });
+}
+
+tqp_status tqp_smj_expand_i32(tqp_ctx* c, const tqp_smj_plan* plan, int64_t begin, int64_t end, int32_t* lo,
+                              int32_t* ro) {
+    TQP_GUARD(c, {
+        if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_i32: null plan");
+        tqp::smj_expand(c, plan, begin, end, lo, ro, 1);
     });
 }
 
@@ -276,7 +293,7 @@ tqp_status tqp_smj_join(tqp_ctx* c, tqp_col l, int64_t nl, tqp_col r, int64_t nr
             tqp::fail(TQP_ERR_CAPACITY, "smj_join: capacity smaller than the join size");
         }
         try {
-            tqp::smj_expand(c, P, 0, size, lo, ro);
+            tqp::smj_expand(c, P, 0, size, lo, ro, 0);
         } catch (...) {
             tqp::smj_release(c, P);
             throw;

@@ -231,6 +231,7 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
 // GenerateOutput / createOutput of PAPER.md:89, :333 fused with the compaction).
 constexpr int MAXPAY = 8;
 struct Payload {
+    int idx32;                      // index outputs as int32 (tqp_pkfk_join_i32) instead of int64
     int nb, np;                     // build-side / probe-side payload columns
     const void* bsrc[MAXPAY];
     int bdt[MAXPAY];
@@ -315,8 +316,13 @@ __global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ 
     }
     __syncthreads();
     for (uint32_t k = tid; k < tot; k += PNT) {   // streamed (evict-first) coalesced stores
-        if (JOIN && left_out) __stcs((long long*)left_out + excl + k, (long long)s_l[k]);
-        if (right_out) __stcs((long long*)right_out + excl + k, (long long)(base + s_r[k]));
+        if (pay.idx32) {
+            if (JOIN && left_out) __stcs((int*)left_out + excl + k, (int)s_l[k]);
+            if (right_out) __stcs((int*)right_out + excl + k, (int)(base + s_r[k]));
+        } else {
+            if (JOIN && left_out) __stcs((long long*)left_out + excl + k, (long long)s_l[k]);
+            if (right_out) __stcs((long long*)right_out + excl + k, (long long)(base + s_r[k]));
+        }
         if (JOIN) {
             for (int c = 0; c < pay.nb; c++) copy_elem(pay.bsrc[c], pay.bdt[c], s_l[k], pay.bdst[c], excl + k);
             for (int c = 0; c < pay.np; c++) copy_elem(pay.psrc[c], pay.pdt[c], base + s_r[k], pay.pdst[c], excl + k);
@@ -495,7 +501,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         for (int c = 0; pay && c < pay->nb; c++) pb += 2.0 * (double)dtype_size(pay->bdt[c]);
         for (int c = 0; pay && c < pay->np; c++) pb += 2.0 * (double)dtype_size(pay->pdt[c]);
         if (mode != 2)
-            ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? ((left_out ? 8.0 : 0.0) + (right_out ? 8.0 : 0.0) + pb) * (double)h[0]
+            ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? ((pay && pay->idx32 ? 4.0 : 8.0) * ((left_out ? 1.0 : 0.0) + (right_out ? 1.0 : 0.0)) + pb) * (double)h[0]
                                                     : (right_out ? 8.0 * (double)h[0] : 0.0));
     }
 }
@@ -669,6 +675,23 @@ void pkfk_join_payload(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t
     Built B;
     build_side(ctx, bk, nb, B);
     run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host, &pay);
+}
+
+// PK-FK join with int32 index outputs (SURVEY §8(f) NEXT 4 variant): half the output
+// bytes; both sides must have fewer than 2^31 rows.
+void pkfk_join_i32(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int32_t* left_out, int32_t* right_out,
+                   int64_t* n_out_host) {
+    check_col(bk, nb, "pkfk build");
+    check_col(pk, np, "pkfk probe");
+    if (np > 0 && (!left_out || !right_out)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null output");
+    if (nb >= (int64_t(1) << 31) || np >= (int64_t(1) << 31))
+        fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_i32: row counts must be < 2^31");
+    Payload pay{};
+    pay.idx32 = 1;
+    Built B;
+    build_side(ctx, bk, nb, B);
+    run_probe(ctx, B, pk, np, 0, 0, reinterpret_cast<int64_t*>(left_out), reinterpret_cast<int64_t*>(right_out), nullptr,
+              n_out_host, &pay);
 }
 
 void pkfk_semi(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int anti, uint8_t* match_out,

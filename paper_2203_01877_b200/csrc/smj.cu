@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
                                                      const uint32_t* __restrict__ tb,
                                                      const uint32_t* __restrict__ perm_l,
                                                      const uint32_t* __restrict__ perm_r, int64_t begin, int64_t end,
-                                                     int64_t* __restrict__ lo_out, int64_t* __restrict__ ro_out) {
+                                                     void* __restrict__ lo_out, void* __restrict__ ro_out, int idx32) {
     // shared memory: the staged bucket ends, plus (when the CTA spans <= MCAP buckets)
     // the buckets' (L, R, startL, startR) so that walking across keys needs no global loads
     constexpr int MCAP = 1024;
@@ -482,8 +482,24 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
     }
     __syncthreads();
     const int n = (int)(c1 - c0);
-    int64_t* lo_p = lo_out + (c0 - begin);
-    int64_t* ro_p = ro_out + (c0 - begin);
+    if (idx32) {   // int32 indices (tqp_smj_expand_i32)
+        int* lo32 = (int*)lo_out + (c0 - begin);
+        int* ro32 = (int*)ro_out + (c0 - begin);
+        if (n == ETILE && (((uintptr_t)lo32 | (uintptr_t)ro32) & 15) == 0) {
+            for (int o = threadIdx.x * 4; o < n; o += ENT * 4) {
+                __stcs(reinterpret_cast<int4*>(lo32 + o), *reinterpret_cast<const int4*>(s_l + o));
+                __stcs(reinterpret_cast<int4*>(ro32 + o), *reinterpret_cast<const int4*>(s_r + o));
+            }
+        } else {
+            for (int o = threadIdx.x; o < n; o += ENT) {
+                __stcs(lo32 + o, (int)s_l[o]);
+                __stcs(ro32 + o, (int)s_r[o]);
+            }
+        }
+        return;
+    }
+    int64_t* lo_p = (int64_t*)lo_out + (c0 - begin);
+    int64_t* ro_p = (int64_t*)ro_out + (c0 - begin);
     const bool vec = n == ETILE && (((uintptr_t)lo_p | (uintptr_t)ro_p) & 15) == 0;
     if (vec) {   // 4 outputs per thread and step: one 16-byte shared load, two 16-byte stores per array
         for (int o = threadIdx.x * 4; o < n; o += ENT * 4) {
@@ -619,16 +635,18 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
     }
 }
 
-void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end, int64_t* lo, int64_t* ro) {
+void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end, void* lo, void* ro, int idx32) {
     if (begin < 0 || end < begin || end > P->out_size) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: bad window");
     if (end == begin) return;
     if (!lo || !ro) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: null output");
     const int64_t blocks = ceil_div(end - begin, ETILE);
     if (blocks >= (int64_t(1) << 31)) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: window too large");
-    ctx->add_bytes("tqp_smj_expand", 16.0 * (double)(end - begin));
+    if (idx32 && (P->n_left >= (int64_t(1) << 31) || P->n_right >= (int64_t(1) << 31)))
+        fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_i32: row counts must be < 2^31");
+    ctx->add_bytes("tqp_smj_expand", (idx32 ? 8.0 : 16.0) * (double)(end - begin));
     launch(ctx, "tqp_smj_expand", expand_kernel, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(), P->mR.get(),
            P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(), begin, end, lo,
-           ro);
+           ro, idx32);
 }
 
 void smj_release(tqp_ctx*, tqp_smj_plan* P) { delete P; }

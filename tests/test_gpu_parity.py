@@ -109,6 +109,18 @@ def test_pkfk_random_parity(T, nb, np_, span, bd, pd):
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
 
 
+@pytest.mark.parametrize("nb,np_,span", [(0, 0, 10), (1, 5, 3), (2047, 2049, 4096), (300_000, 1_000_003, 10**6)])
+def test_pkfk_join_i32_outputs(T, nb, np_, span):
+    """tqp_pkfk_join_i32: the oracle's pairs, written as int32."""
+    rng = np.random.default_rng(nb + np_ + 7)
+    build = (rng.permutation(span)[:nb] - span // 3).astype(np.int64)
+    probe = rng.integers(-span // 2, span, np_).astype(np.int64)
+    lo, ro = T.pkfk_join(cu(build), cu(probe), index_dtype=torch.int32)
+    assert lo.dtype == torch.int32 and ro.dtype == torch.int32
+    olo, oro = oracle.pkfk_join(build, probe)
+    assert np.array_equal(npy(lo).astype(np.int64), olo) and np.array_equal(npy(ro).astype(np.int64), oro)
+
+
 @pytest.mark.parametrize("nb,np_,span", [(0, 100, 10), (1, 5, 3), (5000, 100_001, 20_000), (300_000, 1_000_003, 10**6)])
 def test_pkfk_hash_ablation_parity(T, nb, np_, span):
     """The hash-join ablation returns exactly the sort-based join's output (and the oracle's)."""
@@ -305,6 +317,30 @@ def test_smj_zipf_uniform_parity(T):
         e = int(min(plan.size, b + rng.integers(1, 50_000)))
         wl, wr = plan.expand(b, e)
         assert np.array_equal(npy(wl), olo[b:e]) and np.array_equal(npy(wr), oro[b:e])
+    plan.release()
+
+
+def test_smj_expand_i32_outputs(T):
+    """tqp_smj_expand_i32: full expansion and ragged / unaligned windows match the oracle."""
+    left = zipf_keys(100_000, 100_000, seed=44, device="cuda")
+    right = uniform_keys(100_000, 100_000, seed=45, device="cuda")
+    plan = T.smj_prepare(left, right)
+    olo, oro = oracle.smj_join(npy(left), npy(right))
+    lo, ro = plan.expand(0, plan.size, index_dtype=torch.int32)
+    assert lo.dtype == torch.int32
+    assert np.array_equal(npy(lo).astype(np.int64), olo) and np.array_equal(npy(ro).astype(np.int64), oro)
+    rng = np.random.default_rng(5)
+    buf_l = torch.empty(60_001, dtype=torch.int32, device="cuda")
+    buf_r = torch.empty(60_001, dtype=torch.int32, device="cuda")
+    for _ in range(4):
+        b = int(rng.integers(0, plan.size))
+        e = int(min(plan.size, b + rng.integers(1, 50_000)))
+        off = int(rng.integers(0, 3))   # unaligned output start: scalar store path
+        plan.expand(b, e, out=(buf_l[off:], buf_r[off:]))
+        assert np.array_equal(npy(buf_l[off:off + e - b]).astype(np.int64), olo[b:e])
+        assert np.array_equal(npy(buf_r[off:off + e - b]).astype(np.int64), oro[b:e])
+    with pytest.raises(ValueError):
+        plan.expand(0, 10, out=(buf_l, buf_r.to(torch.int64)))
     plan.release()
 
 

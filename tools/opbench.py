@@ -30,6 +30,7 @@ def main():
         "cub_sort_probe_i64": lambda: torch.sort(lk, stable=True),
         "cub_sort_probe_i32": lambda: torch.sort(lk32, stable=True),
         "pkfk_join": lambda: ctx.pkfk_join(ok, lk),
+        "pkfk_join_i32": lambda: ctx.pkfk_join(ok, lk, index_dtype=torch.int32),
         "pkfk_small_build": lambda: ctx.pkfk_join(ok[:65536], lk),
         "pkfk_hash_ablation": lambda: ctx.pkfk_join_hash(ok, lk),
         "smj_join": lambda: ctx.smj_join(ok, lk),
