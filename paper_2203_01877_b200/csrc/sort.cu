@@ -65,6 +65,12 @@ __global__ void __launch_bounds__(NT) andor_kernel(const void* keys, int64_t n, 
 // keys -- exactly what tile_hist_kernel<uint32_t, IN, 16, 9> would compute for pass 0
 // at shift 0. The host uses it only when the plan turns out to be that one.
 constexpr int H0_IPT = 16, H0_TILE = 256 * H0_IPT, H0_BINS = 512;
+
+// Shared-memory slot of digit d in a per-warp digit array: the low 5 bits (the bank)
+// are XORed with a function of the high bits, a bijection on [0, 2^RB). Keys with
+// structure in their low bits (TPC-H order keys take 8 of every 32 values, keys that
+// are multiples of 2^k) otherwise pile their digits onto a few banks.
+__device__ __forceinline__ uint32_t dslot(uint32_t d) { return d ^ (((d >> 5) * 9u) & 31u); }
 template <int IN>
 __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64_t n, bool desc,
                                                          unsigned long long* out, uint32_t* __restrict__ th0) {
@@ -85,7 +91,7 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
 #pragma unroll
     for (int i = 0; i < H0_IPT; i++) {
         const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
-        if (pos < n) atomicAdd(&h[warp][(uint32_t)u[i] & (H0_BINS - 1u)], 1u);
+        if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
     }
     for (int sft = 16; sft > 0; sft >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, sft);
@@ -101,7 +107,7 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
     for (int d = tid; d < H0_BINS; d += NT) {
         uint32_t c = 0;
 #pragma unroll
-        for (int w = 0; w < NW; w++) c += h[w][d];
+        for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
         th0[(int64_t)blockIdx.x * H0_BINS + d] = c;
     }
 }
@@ -147,13 +153,13 @@ __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int6
 #pragma unroll
     for (int i = 0; i < IPT; i++) {
         const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        if (pos < n) atomicAdd(&h[warp][(uint32_t)(k[i] >> shift) & (BINS - 1u)], 1u);
+        if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
     }
     __syncthreads();
     for (int d = tid; d < BINS; d += NT) {
         uint32_t c = 0;
 #pragma unroll
-        for (int w = 0; w < NW; w++) c += h[w][d];
+        for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
         th[(int64_t)blockIdx.x * BINS + d] = c;
     }
 }
@@ -403,7 +409,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
             const bool valid = i * 32 < rem;
-            const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
+            const uint32_t d = dslot((uint32_t)(key[i] >> a.shift) & DM);
             // peers = lanes of this warp with the same digit: every lane ORs its bit into
             // the digit's match word, reads the word back, and the leader clears it
             uint32_t* mw = &s.u.match[warp][d];
@@ -430,7 +436,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             uint32_t c[BPT][NW], cnt[BPT], local = 0;
 #pragma unroll
             for (int j = 0; j < BPT; j++) {
-                const int d = tid * BPT + j;
+                const int d = dslot(tid * BPT + j);
                 uint32_t run = 0;
 #pragma unroll
                 for (int w = 0; w < NW; w++) {
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                 uint32_t run = ex;
 #pragma unroll
                 for (int w = 0; w < NW; w++) {
-                    s.u.whist[w][d] = run;
+                    s.u.whist[w][dslot(d)] = run;
                     run += c[j][w];
                 }
                 ex += cnt[j];
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
             if (i * 32 < rem) {
-                const uint32_t d = (uint32_t)(key[i] >> a.shift) & DM;
+                const uint32_t d = dslot((uint32_t)(key[i] >> a.shift) & DM);
                 rk[i] = s.u.whist[warp][d] + rk[i];
             }
         }
