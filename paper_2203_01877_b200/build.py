@@ -45,7 +45,8 @@ def build(force=False, verbose=False, jobs=None):
     os.makedirs(odir, exist_ok=True)
     for s in sources():
         o = os.path.join(odir, os.path.basename(s) + ".o")
-        cmd = [NVCC, *FLAGS, "-dc" if False else "-c", s, "-o", o]
+        # TQP_NVCC_EXTRA: extra nvcc flags for A/B experiments (e.g. "-DTQP_PEER_MATCH_ANY=0")
+        cmd = [NVCC, *FLAGS, *os.environ.get("TQP_NVCC_EXTRA", "").split(), "-c", s, "-o", o]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

@@ -3,17 +3,21 @@
 // Paper: the join sorts its keys (Alg. 1 l.2-3) and the
 // aggregation sorts the concatenated group keys with "radix sort" (PAPER.md:256,
 // prose :1148). The paper composes torch.sort; here:
-//   - one AND/OR pass finds the bits that vary; 8-bit digits that are constant
-//     across all keys are skipped, and when every varying bit lies in the low
-//     32 bits the passes carry 32-bit keys (half the traffic);
+//   - one AND/OR pass finds the bits that vary (fused with pass 0's histogram);
+//     the digit plan covers only those bits: 8-bit digits over the bytes that
+//     vary, or 9-bit digits over the varying span when that takes fewer passes;
+//     when every varying bit lies in the low 32 bits the passes carry 32-bit keys
+//     (half the traffic);
 //   - every digit pass is reduce-then-scan, with no inter-tile waiting:
-//       tile_hist   per tile of 4096 (u32) / 3072 (u64) keys: 256 digit counts
+//       tile_hist   per tile of 4096 (u32) / 3072 (u64) keys: the digit counts
 //       scan_tiles  per chunk of 128 tiles: exclusive prefix over tiles, per digit
 //       scan_chunks prefix over chunks + global bin bases (one CTA)
-//       scatter     stable tile ranking (one ballot per digit bit gives each
-//                   key's peers; warp counters claimed with shared atomics in item
-//                   order), keys staged in shared memory in digit order, written
-//                   out so consecutive threads write consecutive addresses.
+//       scatter     persistent, TMA double-buffered input tiles; stable tile
+//                   ranking (each key's peers by warp match, per-warp digit
+//                   counters claimed with shared atomics in item order, digit slots
+//                   bank-swizzled), the tile staged in shared memory in digit order
+//                   and written out so consecutive threads write consecutive
+//                   addresses.
 //     (A decoupled look-back "onesweep" variant was measured at 0.74 ms per
 //     60M-key pass on B200: its inclusive-prefix frontier serialises the tiles;
 //     see DESIGN.md.)
@@ -308,6 +312,14 @@ constexpr int scatter_stage_bytes() {
 // (One stage with 3 CTAs/SM was measured slower: 1.34 -> 1.53 ms per 60M-key sort.)
 constexpr int SCATTER_STAGES = 2;
 
+// Peer detection by __match_any_sync (one MATCH.ANY per item) instead of the shared
+// match words (atomicOr + read-back + clear): measured slower on B200 (60M-key sort
+// scatter 1.27 -> 1.79 ms), kept off.
+#ifndef TQP_PEER_MATCH_ANY
+#define TQP_PEER_MATCH_ANY 0
+#endif
+constexpr bool PEER_MATCH_ANY = TQP_PEER_MATCH_ANY;
+
 template <typename KT, int IN, int IPT, int RB>
 constexpr size_t scatter_tma_smem() {
     return SCATTER_STAGES * (size_t)scatter_stage_bytes<KT, IN, IPT>() + sizeof(ScatterWork<KT, IN, IPT, RB>);
@@ -412,16 +424,22 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             const uint32_t d = dslot((uint32_t)(key[i] >> a.shift) & DM);
             // peers = lanes of this warp with the same digit: every lane ORs its bit into
             // the digit's match word, reads the word back, and the leader clears it
+            unsigned peers;
             uint32_t* mw = &s.u.match[warp][d];
-            if (valid) atomicOr(mw, 1u << lane);
-            __syncwarp();
-            const unsigned peers = valid ? *reinterpret_cast<volatile uint32_t*>(mw) : 0u;
-            __syncwarp();
+            if (PEER_MATCH_ANY) {
+                peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
+                if (!valid) peers = 0;
+            } else {
+                if (valid) atomicOr(mw, 1u << lane);
+                __syncwarp();
+                peers = valid ? *reinterpret_cast<volatile uint32_t*>(mw) : 0u;
+                __syncwarp();
+            }
             const uint32_t leader = 31 - __clz(peers);
             uint32_t old = 0;
             if (valid && lane == leader) {
                 old = atomicAdd(&s.u.whist[warp][d], (uint32_t)__popc(peers));
-                *mw = 0;
+                if (!PEER_MATCH_ANY) *mw = 0;
             }
             rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
         }
