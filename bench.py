@@ -209,6 +209,17 @@ def run_gpu(args):
     for _ in range(args.warmup):
         hp.step()
     torch.cuda.synchronize()
+    # Per-kernel table from profiled, untimed steps (two events around every launch
+    # cost host time the GPU waits on after each readback, ~0.35 ms per step); the
+    # timed region then brackets only the dominant kernel's launches with events.
+    prof_steps = 3
+    hp.ctx.reset_counters()
+    hp.ctx.set_profiling(True)
+    for _ in range(prof_steps):
+        hp.step()
+    ktable = hp.ctx.kernel_stats()
+    hp.ctx.set_profiling(False)
+    dom_name = max(ktable.items(), key=lambda kv: kv[1][0])[0]
     hp._ev, hp.op_ms = [], {}
 
     # ---------------- device-timed region: inputs resident in HBM
@@ -217,7 +228,7 @@ def run_gpu(args):
     torch.cuda.synchronize()
     clk.start()
     hp.ctx.reset_counters()
-    hp.ctx.set_profiling(True)
+    hp.ctx.set_profiling(True, only=dom_name)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
@@ -347,8 +358,8 @@ def run_gpu(args):
 
     if rank == 0:
         peak, peak_src = peaks()
-        dom = max(kstats.items(), key=lambda kv: kv[1][0])
-        name, (kms, klaunch, kbytes) = dom
+        name = dom_name
+        kms, klaunch, kbytes = kstats[name]
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
@@ -391,9 +402,11 @@ def run_gpu(args):
             "operators_ms": op_ms,
             "probe_rows_per_s": hp.n / (op_ms.get("pkfk_join", float("nan")) / 1e3),
             "groupby_rows_per_s": hp.n / (op_ms.get("q1_groupby", float("nan")) / 1e3),
-            "kernels": {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+            "kernels_how": f"every launch bracketed by events over {prof_steps} untimed steps "
+                           "(the timed region brackets only the dominant kernel)",
+            "kernels": {k: {"ms_per_step": v[0] / prof_steps, "launches_per_step": v[1] / prof_steps,
                             "algorithmic_GBps": (v[2] / v[0] / 1e6) if v[0] > 0 else None}
-                        for k, v in sorted(kstats.items(), key=lambda kv: -kv[1][0])},
+                        for k, v in sorted(ktable.items(), key=lambda kv: -kv[1][0])},
         }
         if not args.no_cpu_baseline and world == 1:   # the oracle baseline: rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(hp, args)

@@ -82,6 +82,10 @@ int tqp_abi_version(void);
 int64_t tqp_ctx_launch_count(const tqp_ctx* ctx);
 void tqp_ctx_reset_counters(tqp_ctx* ctx);
 tqp_status tqp_ctx_set_profiling(tqp_ctx* ctx, int enable);
+/* Restrict profiling to kernels whose name starts with name_prefix (NULL or ""
+ * = every kernel). Two event records per profiled launch cost host time that the
+ * GPU waits for after each readback; the bench profiles only its dominant kernel. */
+tqp_status tqp_ctx_set_profiling_filter(tqp_ctx* ctx, const char* name_prefix);
 tqp_status tqp_ctx_kernel_stats(tqp_ctx* ctx, char* names_host, size_t names_cap, double* ms_host,
                                 int64_t* launches_host, double* bytes_host, int max_kernels, int* n_kernels_host);
 

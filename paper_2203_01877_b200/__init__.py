@@ -34,7 +34,8 @@ MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
 
 EXPORTED = [
     "tqp_abi_version", "tqp_ctx_create", "tqp_ctx_destroy", "tqp_ctx_set_stream", "tqp_last_error",
-    "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_kernel_stats",
+    "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_set_profiling_filter",
+    "tqp_ctx_kernel_stats",
     "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_pkfk_join_hash",
     "tqp_pkfk_join_i32", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_expand_i32", "tqp_smj_release",
     "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
@@ -66,6 +67,7 @@ _sig = {
     "tqp_ctx_launch_count": ([_vp], _i64),
     "tqp_ctx_reset_counters": ([_vp], None),
     "tqp_ctx_set_profiling": ([_vp, _int], _int),
+    "tqp_ctx_set_profiling_filter": ([_vp, ctypes.c_char_p], _int),
     "tqp_ctx_kernel_stats": ([_vp, ctypes.c_char_p, ctypes.c_size_t, _P(ctypes.c_double), _P(_i64),
                               _P(ctypes.c_double), _int, _P(_int)], _int),
     "tqp_sort": ([_vp, Col, _i64, _int, _vp, _vp], _int),
@@ -180,7 +182,9 @@ class Context:
     def reset_counters(self):
         _lib.tqp_ctx_reset_counters(self._h)
 
-    def set_profiling(self, on=True):
+    def set_profiling(self, on=True, only=None):
+        """Per-launch device timing; `only`: a kernel-name prefix to restrict it to."""
+        self._check(_lib.tqp_ctx_set_profiling_filter(self._h, only.encode() if only else None))
         self._check(_lib.tqp_ctx_set_profiling(self._h, int(bool(on))))
 
     def kernel_stats(self):

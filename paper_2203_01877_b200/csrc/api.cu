@@ -172,6 +172,10 @@ tqp_status tqp_ctx_set_profiling(tqp_ctx* c, int enable) {
     TQP_GUARD(c, { c->drain_profile(); c->profiling = enable != 0; });
 }
 
+tqp_status tqp_ctx_set_profiling_filter(tqp_ctx* c, const char* name_prefix) {
+    TQP_GUARD(c, { c->drain_profile(); c->prof_prefix = name_prefix ? name_prefix : ""; });
+}
+
 tqp_status tqp_ctx_kernel_stats(tqp_ctx* c, char* names, size_t names_cap, double* ms, int64_t* launches,
                                 double* bytes, int max_kernels, int* n_kernels) {
     TQP_GUARD(c, {

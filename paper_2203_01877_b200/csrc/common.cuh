@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -54,6 +55,10 @@ struct tqp_ctx {
     std::string err;
     int64_t launches = 0;
     bool profiling = false;
+    std::string prof_prefix;   // profile only kernels whose name starts with this (empty: all)
+    bool profiled(const char* name) const {
+        return profiling && (prof_prefix.empty() || strncmp(name, prof_prefix.c_str(), prof_prefix.size()) == 0);
+    }
     struct Pending { const char* name; cudaEvent_t a, b; };
     std::vector<Pending> pending;
     std::vector<cudaEvent_t> free_events;
@@ -129,7 +134,8 @@ inline void launch(tqp_ctx* ctx, const char* name, void (*k)(KArgs...), dim3 gri
                    Args... args) {
     if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
     cudaEvent_t a = nullptr, b = nullptr;
-    if (ctx->profiling) {
+    const bool prof = ctx->profiled(name);
+    if (prof) {
         a = ctx->get_event();
         b = ctx->get_event();
         TQP_CUDA(cudaEventRecord(a, ctx->stream));
@@ -138,7 +144,7 @@ inline void launch(tqp_ctx* ctx, const char* name, void (*k)(KArgs...), dim3 gri
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(TQP_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
     ctx->launches++;
-    if (ctx->profiling) {
+    if (prof) {
         TQP_CUDA(cudaEventRecord(b, ctx->stream));
         ctx->pending.push_back({name, a, b});
     }

@@ -703,6 +703,15 @@ def test_launch_counter_and_profiling(T):
     assert ctx.launch_count() >= 3
     assert "tqp_sort_scatter" in st and st["tqp_sort_scatter"][1] >= 1
     assert all(v[1] >= 1 and v[0] > 0 for v in st.values())   # every launch timed
+    # filtered: only the scatter launches are timed; the others still count and carry bytes
+    ctx.reset_counters()
+    ctx.set_profiling(True, only="tqp_sort_scatter")
+    T.sort(cu(np.arange(10_000)[::-1].copy()))
+    st = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    assert st["tqp_sort_scatter"][1] >= 1 and st["tqp_sort_scatter"][0] > 0
+    assert all(v[1] == 0 and v[0] == 0 for k, v in st.items() if k != "tqp_sort_scatter")
+    assert ctx.launch_count() >= 3
 
 
 def test_groupby_merge_partials(T):
