@@ -125,6 +125,15 @@ tqp_status tqp_pkfk_join(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_
 tqp_status tqp_pkfk_join_i32(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
                              int32_t* left_out_idx, int32_t* right_out_idx, int64_t* n_out_host);
 
+/* tqp_pkfk_join in the paper's output order (reading R7):
+ * the probe side is sorted descending first (stable radix sort) and
+ * the sorted keys are probed in order, so the same pairs come ordered by probe key
+ * descending, then by ascending probe row. Outputs as tqp_pkfk_join (capacity
+ * n_probe x int64 each). Requires n_probe < 2^30. Synchronises three times. */
+tqp_status tqp_pkfk_join_paper_order(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys,
+                                     int64_t n_probe, int64_t* left_out_idx, int64_t* right_out_idx,
+                                     int64_t* n_out_host);
+
 /* Left-semi / left-anti variant ("left-semi, and left-anti
  * joins"): match_out (nullable, n_probe x u8) = 1 iff the probe row has a build
  * match; sel_out (nullable, capacity n_probe x int64) = ascending probe rows
@@ -186,11 +195,38 @@ tqp_status tqp_smj_expand(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin,
  * n_left < 2^31 and n_right < 2^31, else TQP_ERR_INVALID_ARGUMENT. */
 tqp_status tqp_smj_expand_i32(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin, int64_t end,
                               int32_t* left_out_idx, int32_t* right_out_idx);
+/* Fused consumer of the expansion (for joins whose
+ * outSize cannot be materialised, e.g. both-Zipf config 4 with ~4.6e13 pairs):
+ * the pairs (l_j, r_j) at output positions j in [begin, end) -- exactly those
+ * tqp_smj_expand would write -- are consumed in registers, and
+ *   out_host[0] = sum_j mix64(mix64((l_j << 32) | r_j) ^ j)
+ *   out_host[1] = sum_j l_j,   out_host[2] = sum_j r_j        (all mod 2^64)
+ * with mix64(x): x ^= x >> 30; x *= 0xbf58476d1ce4e5b9; x ^= x >> 27;
+ * x *= 0x94d049bb133111eb; x ^= x >> 31 (the splitmix64 finaliser). out_host:
+ * 3 x uint64 host array. Synchronises once. */
+tqp_status tqp_smj_expand_checksum(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin, int64_t end,
+                                   uint64_t* out_host);
 void tqp_smj_release(tqp_ctx* ctx, tqp_smj_plan* plan);
 /* prepare + expand of everything into caller buffers of `capacity` pairs.
  * If capacity < outSize: TQP_ERR_CAPACITY and *n_out_host = outSize. */
 tqp_status tqp_smj_join(tqp_ctx* ctx, tqp_col left, int64_t n_left, tqp_col right, int64_t n_right,
                         int64_t* left_out_idx, int64_t* right_out_idx, int64_t capacity, int64_t* n_out_host);
+
+/* Multi-column join keys (the key packing of PAPER.md:350,
+ * column 0 most significant): the n_cols key columns of two relations a and b are
+ * packed into one int64 key per row with a layout shared by both sides:
+ *   out[row] = sum_c (u_c(row) - min_c) << shift_c,
+ * u_c = the order-preserving unsigned image of column c (value XOR 2^63 of the
+ * sign-extended int64), min_c / max_c over both sides, width_c = bits(max_c -
+ * min_c), shift_c = sum of the widths of columns c+1 .. n_cols-1. Equal tuples
+ * pack equal, different tuples differently, and packed order = lexicographic tuple
+ * order, so tqp_pkfk_join / tqp_smj_* on the packed columns join on the tuples.
+ * a_cols_host / b_cols_host: host arrays of n_cols columns (n_a / n_b rows; b may be
+ * NULL with n_b = 0); a_out / b_out: device int64 (n_a / n_b). *bits_host (nullable):
+ * total width. More than 63 bits, or n_cols outside 1..8: TQP_ERR_INVALID_ARGUMENT.
+ * Synchronises twice. */
+tqp_status tqp_pack_keys(tqp_ctx* ctx, const tqp_col* a_cols_host, int64_t n_a, const tqp_col* b_cols_host,
+                         int64_t n_b, int n_cols, int64_t* a_out, int64_t* b_out, int* bits_host);
 
 /* ---------------------------------------------------- filter/compaction */
 /* (4) Filter -- Listing 1 (bitmap) and Listing 2 (selection

@@ -148,6 +148,31 @@ def smj_window(left, right, begin, end):
     return lo[:end - begin].copy(), ro[:end - begin].copy()
 
 
+def mix64(x):
+    """splitmix64's finaliser on uint64 (the mix of the fused expansion consumer,
+    include/tqp.h tqp_smj_expand_checksum; a definition of ours, not the paper's).
+    Pinned by splitmix64's published outputs (tests/test_oracle_joins.py)."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = x ^ (x >> np.uint64(30))
+        x = x * np.uint64(0xBF58476D1CE4E5B9)
+        x = x ^ (x >> np.uint64(27))
+        x = x * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    return x
+
+
+def smj_checksum(left, right, begin, end):
+    """The fused consumer over output offsets [begin, end): the pairs of smj_window
+    (PAPER.md:310-330), then (sum_j mix64(mix64((l_j << 32) | r_j) ^ j), sum_j l_j,
+    sum_j r_j), each mod 2^64."""
+    lo, ro = smj_window(left, right, begin, end)
+    lu, ru = lo.astype(np.uint64), ro.astype(np.uint64)
+    j = np.arange(begin, end, dtype=np.uint64)
+    h = mix64(mix64((lu << np.uint64(32)) | ru) ^ j)
+    return (int(h.sum(dtype=np.uint64)), int(lu.sum(dtype=np.uint64)), int(ru.sum(dtype=np.uint64)))
+
+
 def _preds(preds):
     arr = (_Pred * max(len(preds), 1))()
     for i, (c, op, v) in enumerate(preds):

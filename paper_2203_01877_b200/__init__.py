@@ -37,8 +37,9 @@ EXPORTED = [
     "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_set_profiling_filter",
     "tqp_ctx_kernel_stats",
     "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_pkfk_join_hash",
-    "tqp_pkfk_join_i32", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_expand_i32", "tqp_smj_release",
-    "tqp_smj_join", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
+    "tqp_pkfk_join_i32", "tqp_pkfk_join_paper_order", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_expand_i32", "tqp_smj_expand_checksum",
+    "tqp_smj_release",
+    "tqp_smj_join", "tqp_pack_keys", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge",
 ]
 
@@ -73,6 +74,8 @@ _sig = {
     "tqp_sort": ([_vp, Col, _i64, _int, _vp, _vp], _int),
     "tqp_pkfk_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_join_i32": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
+    "tqp_pack_keys": ([_vp, _vp, _i64, _vp, _i64, _int, _vp, _vp, _P(_int)], _int),
+    "tqp_pkfk_join_paper_order": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_semi": ([_vp, Col, _i64, Col, _i64, _int, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_outer": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_pkfk_join_hash": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
@@ -81,6 +84,7 @@ _sig = {
     "tqp_smj_prepare": ([_vp, Col, _i64, Col, _i64, _P(_vp), _P(_i64)], _int),
     "tqp_smj_expand": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "tqp_smj_expand_i32": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
+    "tqp_smj_expand_checksum": ([_vp, _vp, _i64, _i64, _P(ctypes.c_uint64)], _int),
     "tqp_smj_release": ([_vp, _vp], None),
     "tqp_smj_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _i64, _P(_i64)], _int),
     "tqp_filter_compact": ([_vp, _P(Col), _int, _i64, _P(Pred), _int, _vp, _vp, _P(_i64)], _int),
@@ -224,6 +228,39 @@ class Context:
         m = ctypes.c_int64(0)
         fn = _lib.tqp_pkfk_join if index_dtype == torch.int64 else _lib.tqp_pkfk_join_i32
         self._check(fn(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(lo), _ptr(ro), ctypes.byref(m)))
+        return lo[:m.value], ro[:m.value]
+
+    def pack_keys(self, a_cols, b_cols=None):
+        """Composite keys (lists of columns, column 0 most significant) of one or two
+        relations packed into int64 keys with a shared layout; returns
+        (a_packed, b_packed or None, total_bits)."""
+        self._sync_stream()
+        a = [_dev_tensor(c, self.device) for c in a_cols]
+        b = [_dev_tensor(c, self.device) for c in b_cols] if b_cols is not None else []
+        if not a or (b and len(b) != len(a)):
+            raise ValueError("pack_keys: one or two lists of the same number of key columns")
+        na, nb = a[0].numel(), (b[0].numel() if b else 0)
+        if any(c.numel() != na for c in a) or any(c.numel() != nb for c in b):
+            raise ValueError("pack_keys: columns of one side must have equal length")
+        ca = (Col * len(a))(*[_col(c) for c in a])
+        cb = (Col * len(b))(*[_col(c) for c in b]) if b else None
+        oa = torch.empty(na, dtype=torch.int64, device=self.device)
+        ob = torch.empty(nb, dtype=torch.int64, device=self.device) if b else None
+        bits = ctypes.c_int(0)
+        self._check(_lib.tqp_pack_keys(self._h, ca, na, cb, nb, len(a), _ptr(oa), _ptr(ob), ctypes.byref(bits)))
+        return oa, ob, bits.value
+
+    def pkfk_join_paper_order(self, build_keys, probe_keys):
+        """PK-FK join pairs in the paper's order: probe key descending, then probe row
+        (reading R7)."""
+        self._sync_stream()
+        b = _dev_tensor(build_keys, self.device)
+        p = _dev_tensor(probe_keys, self.device)
+        lo = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        ro = torch.empty(p.numel(), dtype=torch.int64, device=self.device)
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_pkfk_join_paper_order(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(lo), _ptr(ro),
+                                                   ctypes.byref(m)))
         return lo[:m.value], ro[:m.value]
 
     def pkfk_semi(self, build_keys, probe_keys, anti=False, return_mask=False):
@@ -412,6 +449,14 @@ class SmjPlan:
         self.ctx._check(fn(self.ctx._h, self._h, begin, end, _ptr(lo), _ptr(ro)))
         return lo, ro
 
+    def checksum(self, begin, end):
+        """Fused consumer over pairs [begin, end) without materialising them:
+        (sum_j mix64(mix64((l_j << 32) | r_j) ^ j), sum_j l_j, sum_j r_j), all mod 2^64."""
+        self.ctx._sync_stream()
+        out = (ctypes.c_uint64 * 3)()
+        self.ctx._check(_lib.tqp_smj_expand_checksum(self.ctx._h, self._h, begin, end, out))
+        return tuple(int(x) for x in out)
+
     def release(self):
         if self._h:
             _lib.tqp_smj_release(self.ctx._h, self._h)
@@ -468,6 +513,14 @@ def sort(keys, descending=False, return_keys=True):
 
 def pkfk_join(build_keys, probe_keys, index_dtype=torch.int64):
     return context().pkfk_join(build_keys, probe_keys, index_dtype)
+
+
+def pack_keys(a_cols, b_cols=None):
+    return context().pack_keys(a_cols, b_cols)
+
+
+def pkfk_join_paper_order(build_keys, probe_keys):
+    return context().pkfk_join_paper_order(build_keys, probe_keys)
 
 
 def pkfk_semi(build_keys, probe_keys, anti=False, return_mask=False):

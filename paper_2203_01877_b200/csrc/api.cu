@@ -8,14 +8,17 @@
 namespace tqp {
 void pkfk_join(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void pkfk_join_i32(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int32_t*, int32_t*, int64_t*);
+void pkfk_join_paper_order(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void pkfk_semi(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int, uint8_t*, int64_t*, int64_t*);
 void pkfk_outer(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, uint8_t*, int64_t*);
 void pkfk_join_hash(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void pkfk_join_payload(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, const tqp_col*, int, void* const*, const tqp_col*, int,
                        void* const*, int64_t*, int64_t*, int64_t*);
 void filter_compact(tqp_ctx*, const tqp_col*, int, int64_t, const tqp_pred*, int, uint8_t*, int64_t*, int64_t*);
+int pack_keys(tqp_ctx*, const tqp_col*, int64_t, const tqp_col*, int64_t, int, int64_t*, int64_t*);
 tqp_smj_plan* smj_prepare(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*);
 void smj_expand(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, void*, void*, int);
+void smj_expand_checksum(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, uint64_t*);
 void smj_release(tqp_ctx*, tqp_smj_plan*);
 tqp_groupby_plan* groupby_prepare(tqp_ctx*, const tqp_col*, int, int64_t, const int32_t*, int, const tqp_pred*, int,
                                   const tqp_agg*, int, int64_t*);
@@ -228,6 +231,14 @@ tqp_status tqp_pkfk_join_i32(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64
     });
 }
 
+tqp_status tqp_pkfk_join_paper_order(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int64_t* lo,
+                                     int64_t* ro, int64_t* n_out_host) {
+    TQP_GUARD(c, {
+        if (!n_out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_paper_order: null n_out_host");
+        tqp::pkfk_join_paper_order(c, b, nb, p, np, lo, ro, n_out_host);
+    });
+}
+
 tqp_status tqp_pkfk_semi(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int anti, uint8_t* match_out,
                          int64_t* sel_out, int64_t* n_sel_host) {
     TQP_GUARD(c, { tqp::pkfk_semi(c, b, nb, p, np, anti, match_out, sel_out, n_sel_host); });
@@ -281,6 +292,14 @@ tqp_status tqp_smj_expand_i32(tqp_ctx* c, const tqp_smj_plan* plan, int64_t begi
     });
 }
 
+tqp_status tqp_smj_expand_checksum(tqp_ctx* c, const tqp_smj_plan* plan, int64_t begin, int64_t end,
+                                   uint64_t* out_host) {
+    TQP_GUARD(c, {
+        if (!plan || !out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_checksum: null argument");
+        tqp::smj_expand_checksum(c, plan, begin, end, out_host);
+    });
+}
+
 void tqp_smj_release(tqp_ctx* c, tqp_smj_plan* plan) {
     if (plan) tqp::smj_release(c, plan);
 }
@@ -303,6 +322,15 @@ tqp_status tqp_smj_join(tqp_ctx* c, tqp_col l, int64_t nl, tqp_col r, int64_t nr
             throw;
         }
         tqp::smj_release(c, P);
+    });
+}
+
+tqp_status tqp_pack_keys(tqp_ctx* c, const tqp_col* a_cols, int64_t n_a, const tqp_col* b_cols, int64_t n_b, int n_cols,
+                         int64_t* a_out, int64_t* b_out, int* bits_host) {
+    TQP_GUARD(c, {
+        if (!a_cols) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pack_keys: null columns");
+        const int bits = tqp::pack_keys(c, a_cols, n_a, b_cols, n_b, n_cols, a_out, b_out);
+        if (bits_host) *bits_host = bits;
     });
 }
 

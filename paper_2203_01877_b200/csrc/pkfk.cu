@@ -703,6 +703,36 @@ void pkfk_join_payload(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t
     run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host, &pay);
 }
 
+// The paper's output order (reading R7): the probe side sorted
+// descending first (Alg. 1 l.3 as written for the PK-FK macro), then the
+// sorted keys probed in order, so the pairs come by probe key descending and, among
+// equal probe keys, by ascending probe row (the sort is stable). The original probe row
+// of each pair is the sort permutation gathered by the emit pass as a payload column.
+void pkfk_join_paper_order(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int64_t* left_out,
+                           int64_t* right_out, int64_t* n_out_host) {
+    check_col(bk, nb, "pkfk build");
+    check_col(pk, np, "pkfk probe");
+    if (np > 0 && (!left_out || !right_out)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: null output");
+    if (np >= (int64_t(1) << 30)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_paper_order: probe must be < 2^30 rows");
+    if (np == 0 || nb == 0) {
+        pkfk_join(ctx, bk, nb, pk, np, left_out, right_out, n_out_host);
+        return;
+    }
+    DevBuf<uint8_t> sorted(ctx, (size_t)np * dtype_size(pk.dtype));
+    DevBuf<int64_t> perm(ctx, np);
+    SortOut so;
+    so.sorted_orig = sorted.get();
+    so.perm64 = perm.get();
+    radix_sort(ctx, pk.data, pk.dtype, np, true, so);
+    tqp_col spk = pk;
+    spk.data = sorted.get();
+    tqp_col pp{};
+    pp.data = perm.get();
+    pp.dtype = TQP_I64;
+    void* pp_out[1] = {right_out};
+    pkfk_join_payload(ctx, bk, nb, spk, np, nullptr, 0, nullptr, &pp, 1, pp_out, left_out, nullptr, n_out_host);
+}
+
 // PK-FK join with int32 index outputs (SURVEY §8(f) NEXT 4 variant): half the output
 // bytes; both sides must have fewer than 2^31 rows.
 void pkfk_join_i32(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int32_t* left_out, int32_t* right_out,

@@ -25,7 +25,8 @@ struct tqp_smj_plan {
     tqp::DevBuf<uint32_t> perm_l, perm_r;
     tqp::DevBuf<uint32_t> mL, mR, msL, msR;   // per common key: counts and run starts (< 2^30)
     tqp::DevBuf<int64_t> mcum;                 // cumHistMul (inclusive)
-    tqp::DevBuf<uint32_t> tb;                  // per output tile of ETILE: bucket of its first output (+ sentinel)
+    tqp::DevBuf<uint32_t> tb;                  // per output tile of ETILE << tg_shift: bucket of its first output (+ sentinel)
+    int tg_shift = 0;                          // > 0 when outSize is far larger than the keys (coarse table)
 };
 
 namespace tqp {
@@ -384,9 +385,50 @@ __global__ void __launch_bounds__(JNT) cum_write_kernel(const uint32_t* __restri
         run += v[i];
         mcum[b] = (int64_t)run;
         // output tiles whose first output falls inside this key's range [start, run)
+        if (!tb) continue;   // coarse table: tb_search_kernel
         for (int64_t c = (start + ETILE_C - 1) / ETILE_C; c * ETILE_C < (int64_t)run; c++) tb[c] = (uint32_t)b;
         if (b == K - 1) tb[n_tb - 1] = (uint32_t)b;
     }
+}
+
+// Coarse tile-bucket table (outSize >> number of keys, e.g. both-Zipf joins): entry c is
+// the bucket of output c * TG, found by a binary search over cumHistMul (one thread per
+// entry; the filling loop of cum_write_kernel would spend one thread per heavy key).
+__global__ void tb_search_kernel(const int64_t* __restrict__ mcum, int64_t K, int tg_shift_total, uint32_t* tb,
+                                 int64_t n_tb) {
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n_tb; c += (int64_t)gridDim.x * blockDim.x) {
+        if (c == n_tb - 1) {
+            tb[c] = (uint32_t)(K - 1);
+            continue;
+        }
+        const int64_t x = c << tg_shift_total;
+        int64_t lo = 0, hi = K - 1;   // first b with mcum[b] > x (mcum[K-1] = outSize > x)
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (mcum[mid] > x) hi = mid; else lo = mid + 1;
+        }
+        tb[c] = (uint32_t)lo;
+    }
+}
+
+// Warp-cooperative search: the first b in [lo, hi] with mcum[b] > x, given mcum[hi] > x
+// (32 probes per step).
+__device__ __forceinline__ int64_t warp_upper(const int64_t* __restrict__ mcum, int64_t lo, int64_t hi, int64_t x) {
+    const int lane = threadIdx.x & 31;
+    while (lo < hi) {
+        const int64_t step = (hi - lo + 32) / 32;
+        const int64_t idx = min(lo + lane * step, hi);
+        const unsigned bal = __ballot_sync(0xffffffffu, mcum[idx] > x);
+        if (bal == 0) {
+            lo = min(lo + 31 * step, hi) + 1;
+        } else {
+            const int f = __ffs(bal) - 1;
+            const int64_t nhi = min(lo + f * step, hi);
+            lo = f == 0 ? lo : min(lo + (f - 1) * step, hi) + 1;
+            hi = nhi;
+        }
+    }
+    return lo;
 }
 
 constexpr int ENT = 256;
@@ -401,13 +443,43 @@ static_assert(ETILE == ETILE_C, "cum_write_kernel's tile-bucket table uses expan
 // buckets come from the tile-bucket table (two loads); their cumulative ends,
 // clamped to the CTA's output window, are staged in shared memory where every
 // thread finds its first bucket.
+// Fused consumer (tqp_smj_expand_checksum): h_j = mix64(mix64((left << 32) | right) ^ j)
+// over output positions j, summed mod 2^64 with the left and right indices.
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+constexpr int CK_SLOTS = 1024;
+__global__ void ck_final_kernel(const unsigned long long* __restrict__ slots, unsigned long long* out) {
+    __shared__ unsigned long long s[3][32];
+    uint64_t v[3] = {0, 0, 0};
+    for (int i = threadIdx.x; i < CK_SLOTS; i += blockDim.x)
+        for (int k = 0; k < 3; k++) v[k] += slots[3 * i + k];
+    for (int k = 0; k < 3; k++) {
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+        if ((threadIdx.x & 31) == 0) s[k][threadIdx.x >> 5] = v[k];
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        uint64_t t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += s[threadIdx.x][w];
+        out[threadIdx.x] = t;
+    }
+}
+
+template <bool CK>
 __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
                                                      const uint32_t* __restrict__ msL, const uint32_t* __restrict__ msR,
                                                      const int64_t* __restrict__ mcum, int64_t K,
                                                      const uint32_t* __restrict__ tb,
                                                      const uint32_t* __restrict__ perm_l,
                                                      const uint32_t* __restrict__ perm_r, int64_t begin, int64_t end,
-                                                     void* __restrict__ lo_out, void* __restrict__ ro_out, int idx32) {
+                                                     void* __restrict__ lo_out, void* __restrict__ ro_out, int idx32,
+                                                     unsigned long long* __restrict__ ck, int tg_shift) {
     // shared memory: the staged bucket ends, plus (when the CTA spans <= MCAP buckets)
     // the buckets' (L, R, startL, startR) so that walking across keys needs no global loads
     constexpr int MCAP = 1024;
@@ -416,8 +488,23 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
     const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
     const int64_t c1 = min(c0 + ETILE, end);
     // buckets of outputs c0 and c1 - 1 lie in [b0, b1]: at most two output tiles' worth
-    const int64_t b0 = tb[c0 / ETILE];
-    const int64_t b1 = min((int64_t)tb[(c1 - 1) / ETILE + 1], K - 1);
+    int64_t b0, b1;
+    if (tg_shift == 0) {
+        b0 = tb[c0 / ETILE];
+        b1 = min((int64_t)tb[(c1 - 1) / ETILE + 1], K - 1);
+    } else {   // coarse table: narrow [tb[c0 / TG], tb[(c1 - 1) / TG + 1]] to this CTA's buckets
+        __shared__ int64_t s_b[2];
+        if (threadIdx.x < 32) {
+            const int64_t lo = tb[(c0 / ETILE) >> tg_shift];
+            const int64_t hi = min((int64_t)tb[(((c1 - 1) / ETILE) >> tg_shift) + 1], K - 1);
+            const int64_t x0 = warp_upper(mcum, lo, hi, c0);
+            const int64_t x1 = warp_upper(mcum, x0, hi, c1 - 1);
+            if (threadIdx.x == 0) { s_b[0] = x0; s_b[1] = x1; }
+        }
+        __syncthreads();
+        b0 = s_b[0];
+        b1 = s_b[1];
+    }
     const int nb = (int)(b1 - b0 + 1);
     const bool meta = nb <= MCAP;
     int32_t* s_cum = s_buf;
@@ -434,6 +521,7 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
     }
     __syncthreads();
     const int64_t o0 = c0 + (int64_t)threadIdx.x * EIPT;
+    uint64_t hs = 0, sl = 0, sr = 0;   // CK: this thread's share of the consumer sums
     if (o0 < c1) {   // thread: EIPT consecutive outputs, incremental (q, r)
         const int32_t rel = threadIdx.x * EIPT;
         int lo = 0, hi = nb;
@@ -460,6 +548,11 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
             if (j >= cnt) break;
             vl[j] = __ldg(perm_l + sL + q);
             vr[j] = __ldg(perm_r + sR + r);
+            if (CK) {
+                hs += mix64(mix64(((uint64_t)vl[j] << 32) | vr[j]) ^ (uint64_t)(o0 + j));
+                sl += vl[j];
+                sr += vr[j];
+            }
             if (++r == R) {
                 r = 0;
                 if (++q == L) {
@@ -469,7 +562,8 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
             }
         }
         const int o = threadIdx.x * EIPT;
-        if (cnt == EIPT) {   // 16-byte shared stores
+        if (CK) {
+        } else if (cnt == EIPT) {   // 16-byte shared stores
             reinterpret_cast<uint4*>(s_l + o)[0] = make_uint4(vl[0], vl[1], vl[2], vl[3]);
             reinterpret_cast<uint4*>(s_l + o)[1] = make_uint4(vl[4], vl[5], vl[6], vl[7]);
             reinterpret_cast<uint4*>(s_r + o)[0] = make_uint4(vr[0], vr[1], vr[2], vr[3]);
@@ -479,6 +573,26 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
             for (int j = 0; j < EIPT; j++)
                 if (j < cnt) { s_l[o + j] = vl[j]; s_r[o + j] = vr[j]; }
         }
+    }
+    if (CK) {   // CTA sums -> one of CK_SLOTS partial slots (mod 2^64; spread so that
+                // same-address atomics do not serialise), summed by ck_final_kernel
+        __shared__ unsigned long long s_ck[3];
+        if (threadIdx.x < 3) s_ck[threadIdx.x] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int sh = 16; sh > 0; sh >>= 1) {
+            hs += __shfl_xor_sync(0xffffffffu, hs, sh);
+            sl += __shfl_xor_sync(0xffffffffu, sl, sh);
+            sr += __shfl_xor_sync(0xffffffffu, sr, sh);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicAdd(&s_ck[0], (unsigned long long)hs);
+            atomicAdd(&s_ck[1], (unsigned long long)sl);
+            atomicAdd(&s_ck[2], (unsigned long long)sr);
+        }
+        __syncthreads();
+        if (threadIdx.x < 3) atomicAdd(ck + 3 * (blockIdx.x % CK_SLOTS) + threadIdx.x, s_ck[threadIdx.x]);
+        return;
     }
     __syncthreads();
     const int n = (int)(c1 - c0);
@@ -620,11 +734,24 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         P->K = h[2];
         P->out_size = h[2] > 0 ? h[3] : 0;
         if (P->out_size > 0) {   // cumHistMul + the tile -> bucket table for expand
-            const int64_t n_tb = ceil_div(P->out_size, ETILE) + 1;
+            // a table entry per output tile while that is comparable to the keys; coarser
+            // tiles (and a search per entry) when outSize dwarfs them
+            const int64_t tcap = 4 * P->K + (int64_t(1) << 22);
+            int sh = 0;
+            while (ceil_div(P->out_size, (int64_t)ETILE << sh) + 1 > tcap) sh++;
+            P->tg_shift = sh;
+            const int64_t n_tb = ceil_div(P->out_size, (int64_t)ETILE << sh) + 1;
             P->tb.alloc(ctx, n_tb);
             launch(ctx, "tqp_smj_cumsum", cum_write_kernel, dim3((unsigned)ctiles), dim3(JNT), 0,
                    (const uint32_t*)P->mL.get(), (const uint32_t*)P->mR.get(), (const int64_t*)(scal.get() + 2),
-                   (const uint64_t*)toff.get(), P->mcum.get(), P->tb.get(), n_tb);
+                   (const uint64_t*)toff.get(), P->mcum.get(), sh == 0 ? P->tb.get() : (uint32_t*)nullptr, n_tb);
+            if (sh > 0) {
+                static_assert((ETILE & (ETILE - 1)) == 0, "ETILE is a power of two");
+                const int lg = __builtin_ctz(ETILE) + sh;
+                const int g = (int)std::min<int64_t>(ceil_div(n_tb, 256), (int64_t)ctx->num_sms * 16);
+                launch(ctx, "tqp_smj_cumsum", tb_search_kernel, dim3(g), dim3(256), 0, (const int64_t*)P->mcum.get(), P->K,
+                       lg, P->tb.get(), n_tb);
+            }
             ctx->add_bytes("tqp_smj_cumsum", 16.0 * (double)P->K + 4.0 * (double)n_tb);
         }
         *out_size_host = P->out_size;
@@ -644,9 +771,28 @@ void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end,
     if (idx32 && (P->n_left >= (int64_t(1) << 31) || P->n_right >= (int64_t(1) << 31)))
         fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_i32: row counts must be < 2^31");
     ctx->add_bytes("tqp_smj_expand", (idx32 ? 8.0 : 16.0) * (double)(end - begin));
-    launch(ctx, "tqp_smj_expand", expand_kernel, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(), P->mR.get(),
+    launch(ctx, "tqp_smj_expand", expand_kernel<false>, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(), P->mR.get(),
            P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(), begin, end, lo,
-           ro, idx32);
+           ro, idx32, (unsigned long long*)nullptr, P->tg_shift);
+}
+
+// The expansion consumed in place (a fused consumer instead of
+// materialising pairs that cannot be stored): out[0] = sum_j mix64(mix64((l_j << 32) |
+// r_j) ^ j), out[1] = sum_j l_j, out[2] = sum_j r_j, mod 2^64, over j in [begin, end).
+void smj_expand_checksum(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end, uint64_t* out_host) {
+    if (begin < 0 || end < begin || end > P->out_size) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: bad window");
+    out_host[0] = out_host[1] = out_host[2] = 0;
+    if (end == begin) return;
+    const int64_t blocks = ceil_div(end - begin, ETILE);
+    if (blocks >= (int64_t(1) << 31)) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: window too large");
+    DevBuf<unsigned long long> ck(ctx, 3 * CK_SLOTS + 3);
+    ck.zero();
+    launch(ctx, "tqp_smj_expand_checksum", expand_kernel<true>, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(),
+           P->mR.get(), P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(),
+           begin, end, (void*)nullptr, (void*)nullptr, 0, ck.get(), P->tg_shift);
+    launch(ctx, "tqp_smj_expand_checksum", ck_final_kernel, dim3(1), dim3(1024), 0, (const unsigned long long*)ck.get(),
+           ck.get() + 3 * CK_SLOTS);
+    read_back(ctx, out_host, ck.get() + 3 * CK_SLOTS, 24);
 }
 
 void smj_release(tqp_ctx*, tqp_smj_plan* P) { delete P; }

@@ -121,6 +121,29 @@ def test_pkfk_join_i32_outputs(T, nb, np_, span):
     assert np.array_equal(npy(lo).astype(np.int64), olo) and np.array_equal(npy(ro).astype(np.int64), oro)
 
 
+@pytest.mark.parametrize("nb,np_,span,pd", [(0, 100, 10, torch.int64), (1, 5, 3, torch.int64), (50, 3000, 40, torch.int32),
+                                             (5000, 100_001, 20_000, torch.int64), (300_000, 1_000_003, 10**6, torch.int64)])
+def test_pkfk_join_paper_order(T, nb, np_, span, pd):
+    """Reading R7: the paper's order = the oracle's pairs re-sorted stably by probe key
+    descending (ties: ascending probe row)."""
+    rng = np.random.default_rng(nb + np_ + 11)
+    build = (rng.permutation(span)[:nb] - span // 3).astype(np.int64)
+    probe = rng.integers(-span // 2, span, np_).astype(np.int64)
+    lo, ro = T.pkfk_join_paper_order(cu(build), cu(probe, pd))
+    olo, oro = oracle.pkfk_join(build, probe)
+    order = np.lexsort((oro, -probe[oro]))
+    assert np.array_equal(npy(lo), olo[order]) and np.array_equal(npy(ro), oro[order])
+
+
+def test_pkfk_join_paper_order_extremes(T):
+    build = np.array([I64_MAX, I64_MIN, 0, -1, 5], np.int64)
+    probe = np.array([5, I64_MIN, I64_MAX, 7, 0, I64_MIN, -1, 5, I64_MAX], np.int64)
+    lo, ro = T.pkfk_join_paper_order(cu(build), cu(probe))
+    olo, oro = oracle.pkfk_join(build, probe)
+    order = sorted(range(olo.size), key=lambda j: (-int(probe[oro[j]]), int(oro[j])))
+    assert npy(lo).tolist() == olo[order].tolist() and npy(ro).tolist() == oro[order].tolist()
+
+
 @pytest.mark.parametrize("nb,np_,span", [(0, 100, 10), (1, 5, 3), (5000, 100_001, 20_000), (300_000, 1_000_003, 10**6)])
 def test_pkfk_hash_ablation_parity(T, nb, np_, span):
     """The hash-join ablation returns exactly the sort-based join's output (and the oracle's)."""
@@ -342,6 +365,103 @@ def test_smj_expand_i32_outputs(T):
     with pytest.raises(ValueError):
         plan.expand(0, 10, out=(buf_l, buf_r.to(torch.int64)))
     plan.release()
+
+
+def test_smj_expand_checksum(T):
+    """The fused consumer (no materialisation) equals the oracle's checksum on full and
+    ragged windows, including windows crossing the heavy Zipf key."""
+    left = zipf_keys(60_000, 60_000, seed=46, device="cuda")
+    right = uniform_keys(60_000, 60_000, seed=47, device="cuda")
+    plan = T.smj_prepare(left, right)
+    L, R = npy(left), npy(right)
+    rng = np.random.default_rng(6)
+    wins = [(0, plan.size), (0, 0), (5, 6), (plan.size - 1, plan.size)]
+    for _ in range(4):
+        b = int(rng.integers(0, plan.size))
+        wins.append((b, int(min(plan.size, b + rng.integers(1, 40_000)))))
+    for b, e in wins:
+        assert plan.checksum(b, e) == oracle.smj_checksum(L, R, b, e), (b, e)
+    plan.release()
+
+
+def test_smj_checksum_both_zipf_windows(T):
+    """Config-4 as stated (both Zipf, outSize not materialisable at full size): windowed
+    checksums against the oracle's per-offset route."""
+    left = zipf_keys(200_000, 10**6, seed=42, device="cuda")
+    right = zipf_keys(200_000, 10**6, seed=43, stream=101, device="cuda")
+    plan = T.smj_prepare(left, right)
+    rng = np.random.default_rng(8)
+    for b in [0] + [int(x) for x in rng.integers(0, plan.size - 100_000, 3)]:
+        assert plan.checksum(b, b + 100_000) == oracle.smj_checksum(npy(left), npy(right), b, b + 100_000)
+    plan.release()
+
+
+def test_smj_coarse_tile_table(T):
+    """outSize ~9.6e9 from two heavy keys (the coarse tile-bucket table path): windows
+    crossing the heavy-heavy and heavy-light boundaries, materialised and checksummed."""
+    left = np.concatenate([np.full(60_000, 1), np.full(60_000, 2), np.arange(3, 1003)]).astype(np.int64)
+    right = np.concatenate([np.arange(3, 1003), np.full(80_000, 2), np.full(80_000, 1)]).astype(np.int64)
+    rng = np.random.default_rng(10)
+    left, right = rng.permutation(left), rng.permutation(right)
+    plan = T.smj_prepare(cu(left), cu(right))
+    assert plan.size == oracle.smj_count(left, right) == 2 * 60_000 * 80_000 + 1000
+    h = 60_000 * 80_000
+    wins = [(0, 5000), (h - 3000, h + 3000), (2 * h - 10, plan.size), (plan.size - 7, plan.size)]
+    wins += [(int(b), int(b) + 20_000) for b in rng.integers(0, plan.size - 20_000, 3)]
+    for b, e in wins:
+        lo, ro = plan.expand(b, e)
+        olo, oro = oracle.smj_window(left, right, b, e)
+        assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro), (b, e)
+        assert plan.checksum(b, e) == oracle.smj_checksum(left, right, b, e), (b, e)
+    plan.release()
+
+
+def _dense_ids(a_cols, b_cols):
+    """Tuple -> id in lexicographic tuple order over both sides (numpy unique on rows)."""
+    ta = np.stack([np.asarray(c, np.int64) for c in a_cols], axis=1)
+    tb = np.stack([np.asarray(c, np.int64) for c in b_cols], axis=1)
+    _, inv = np.unique(np.concatenate([ta, tb]), axis=0, return_inverse=True)
+    inv = inv.reshape(-1)
+    return inv[:len(ta)], inv[len(ta):]
+
+
+def test_pack_keys_composite_joins(T):
+    """Composite keys (i32, u8, i64 with negatives): PK-FK and SMJ on the packed keys equal
+    the oracle's joins on the tuples' dense ids (independent densification)."""
+    rng = np.random.default_rng(12)
+    nb, np_ = 3000, 20_011
+    # unique build tuples over a small domain
+    dom = np.array([(a, b, c) for a in range(-20, 20) for b in range(0, 256, 37) for c in (-(1 << 40), 0, 77)])
+    bt = dom[rng.permutation(len(dom))[:nb]]
+    pt = dom[rng.integers(0, len(dom), np_)]
+    pt[::13, 2] = 5   # tuples absent from the build side
+    bcols = [cu(bt[:, 0], torch.int32), cu(bt[:, 1], torch.uint8), cu(bt[:, 2])]
+    pcols = [cu(pt[:, 0], torch.int32), cu(pt[:, 1], torch.uint8), cu(pt[:, 2])]
+    kb, kp, bits = T.pack_keys(bcols, pcols)
+    assert bits <= 63
+    ib, ip = _dense_ids([bt[:, 0], bt[:, 1], bt[:, 2]], [pt[:, 0], pt[:, 1], pt[:, 2]])
+    lo, ro = T.pkfk_join(kb, kp)
+    olo, oro = oracle.pkfk_join(ib, ip)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    # m:n join on composite keys: same pairs in the same (key, l, r) order
+    lt, rt = pt[:5000], pt[5000:9000]
+    kl, kr, _ = T.pack_keys([cu(lt[:, 0], torch.int32), cu(lt[:, 1], torch.uint8), cu(lt[:, 2])],
+                            [cu(rt[:, 0], torch.int32), cu(rt[:, 1], torch.uint8), cu(rt[:, 2])])
+    il, ir = _dense_ids([lt[:, 0], lt[:, 1], lt[:, 2]], [rt[:, 0], rt[:, 1], rt[:, 2]])
+    lo, ro = T.smj_join(kl, kr)
+    olo, oro = oracle.smj_join(il, ir)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+def test_pack_keys_edges(T):
+    one = cu(np.array([5, 5, 5]))
+    ka, kb, bits = T.pack_keys([one], [cu(np.array([5]))])
+    assert bits == 0 and npy(ka).tolist() == [0, 0, 0] and npy(kb).tolist() == [0]
+    ka, kb, bits = T.pack_keys([cu(np.array([3, 1, 2]))])   # one side only
+    assert kb is None and npy(ka).tolist() == [2, 0, 1] and bits == 2
+    wide = cu(np.array([I64_MIN, I64_MAX]))
+    with pytest.raises(T.TqpError):
+        T.pack_keys([wide, cu(np.array([0, 1]))])   # 64 + 1 bits
 
 
 def test_smj_both_zipf_windows(T):

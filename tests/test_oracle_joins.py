@@ -181,3 +181,27 @@ def test_smj_zipf_uniform_size_law():
     cl = np.bincount(left, minlength=5000)
     cr = np.bincount(right, minlength=5000)
     assert oracle.smj_count(left, right) == int((cl * cr).sum())
+
+
+def test_mix64_splitmix64_vectors():
+    """The consumer's mix is splitmix64's output function: state += 0x9E3779B97F4A7C15,
+    out = mix64(state). Published outputs for seed 0."""
+    g = 0x9E3779B97F4A7C15
+    assert int(oracle.mix64(g)) == 0xE220A8397B1DCDAF
+    assert int(oracle.mix64((2 * g) % (1 << 64))) == 0x6E789E6AA1B965F4
+
+
+def test_smj_checksum_definition():
+    """The checksum of a window equals the same sums over the oracle's full join."""
+    rng = np.random.default_rng(9)
+    left = rng.integers(0, 30, 400)
+    right = rng.integers(0, 30, 300)
+    lo, ro = oracle.smj_join(left, right)
+    n = lo.size
+    for b, e in [(0, n), (0, 0), (7, 8), (n // 3, n - 5)]:
+        h, sl, sr = oracle.smj_checksum(left, right, b, e)
+        exp_h = 0
+        for j in range(b, e):   # scalar route over Python ints, mod 2^64
+            exp_h = (exp_h + int(oracle.mix64(int(oracle.mix64((int(lo[j]) << 32) | int(ro[j]))) ^ j))) % (1 << 64)
+        assert h == exp_h
+        assert sl == int(lo[b:e].sum()) % (1 << 64) and sr == int(ro[b:e].sum()) % (1 << 64)
