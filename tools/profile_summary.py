@@ -16,7 +16,11 @@ NAME = [("gb_phase1", "tqp_groupby_tile"), ("gb_dense_kernel", "tqp_groupby_dens
         ("rle_kernel", "tqp_smj_rle"), ("intersect_kernel", "tqp_smj_intersect"), ("cum_kernel", "tqp_smj_cumsum"),
         ("andor_kernel", "tqp_sort_andor"), ("gb_gid", "tqp_groupby_gid"), ("gb_acc", "tqp_groupby_accumulate"),
         ("gb_finalize", "tqp_groupby_finalize"), ("bucket_ends", "tqp_pkfk_bucket_ends"), ("scan_max", "tqp_scan_max"),
-        ("pack_records", "tqp_pkfk_records"), ("trivial_sort", "tqp_sort_trivial"), ("gb_init", "tqp_groupby_init")]
+        ("pack_records", "tqp_pkfk_records"), ("trivial_sort", "tqp_sort_trivial"), ("gb_init", "tqp_groupby_init"),
+        ("andor_hist0", "tqp_sort_andor"), ("cum_tiles", "tqp_smj_cumsum"), ("cum_write", "tqp_smj_cumsum"),
+        ("tb_search", "tqp_smj_cumsum"), ("ck_final", "tqp_smj_expand_checksum"), ("pack_minmax", "tqp_pack_minmax"),
+        ("pack_kernel", "tqp_pack"), ("fill_slots", "tqp_pkfk_records"), ("gb_sp_keys", "tqp_groupby_sortpath"),
+        ("sp_keys", "tqp_groupby_sortpath"), ("sp_reduce", "tqp_groupby_sortpath")]
 
 
 def tqp_name(k):
