@@ -540,7 +540,15 @@ __global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict_
         int64_t L, R, sL, sR;
         load(bi, L, R, sL, sR);
         int64_t off = o0 - (mcum[b0 + bi] - L * R);
-        int64_t q = off / R, r = off - q * R;
+        int64_t q, r;
+        if (((uint64_t)off | (uint64_t)R) >> 32 == 0) {   // 32-bit division when it fits
+            const uint32_t q32 = (uint32_t)off / (uint32_t)R;
+            q = q32;
+            r = (int64_t)((uint32_t)off - q32 * (uint32_t)R);
+        } else {
+            q = off / R;
+            r = off - q * R;
+        }
         const int cnt = (int)min((int64_t)EIPT, c1 - o0);
         uint32_t vl[EIPT], vr[EIPT];
 #pragma unroll

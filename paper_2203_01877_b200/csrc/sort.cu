@@ -145,33 +145,44 @@ __device__ __forceinline__ KT load_key(const void* in_keys, int64_t pos, bool de
     return (KT)load_u<IN>(in_keys, pos, desc);
 }
 
-// (1) per-tile digit counts -> th[tile * BINS + d]
+// (1) per-tile digit counts -> th[tile * BINS + d]; persistent over tiles, the next
+// tile's keys loaded while this one's counts are reduced and written
 template <typename KT, int IN, int IPT, int RB>
 __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int64_t n, int shift, bool desc,
                                                        uint32_t* __restrict__ th) {
     constexpr int TILE = NT * IPT, BINS = 1 << RB;
     __shared__ uint32_t h[NW][BINS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int d = lane; d < BINS; d += 32) h[warp][d] = 0;
-    __syncwarp();
-    const int64_t base = (int64_t)blockIdx.x * TILE;
+    const int64_t tiles = (n + TILE - 1) / TILE;
     KT k[IPT];
+    auto load = [&](int64_t t) {
+        const int64_t base = t * TILE;
 #pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        k[i] = pos < n ? load_key<KT, IN>(in_keys, pos, desc) : (KT)0;
-    }
+        for (int i = 0; i < IPT; i++) {
+            const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+            k[i] = pos < n ? load_key<KT, IN>(in_keys, pos, desc) : (KT)0;
+        }
+    };
+    int64_t t = blockIdx.x;
+    if (t < tiles) load(t);
+    for (; t < tiles; t += gridDim.x) {
+        for (int d = lane; d < BINS; d += 32) h[warp][d] = 0;
+        __syncwarp();
+        const int64_t base = t * TILE;
 #pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
-    }
-    __syncthreads();
-    for (int d = tid; d < BINS; d += NT) {
-        uint32_t c = 0;
+        for (int i = 0; i < IPT; i++) {
+            const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+            if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
+        }
+        if (t + gridDim.x < tiles) load(t + gridDim.x);
+        __syncthreads();
+        for (int d = tid; d < BINS; d += NT) {
+            uint32_t c = 0;
 #pragma unroll
-        for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
-        th[(int64_t)blockIdx.x * BINS + d] = c;
+            for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
+            th[t * BINS + d] = c;
+        }
+        __syncthreads();
     }
 }
 
@@ -633,8 +644,9 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         uint32_t* thp = (p == 0 && th0) ? th0 : th.get();   // pass 0: histogram fused into the AND/OR pass
         if (thp != th0) {
             dispatch_in(mode, [&](auto m) {
-                launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT, RB>,
-                       dim3((unsigned)tiles), dim3(NT), 0, in, n, shifts[p], desc, thp);
+                auto* kfn = tile_hist_kernel<KT, decltype(m)::value, IPT, RB>;
+                const int64_t g = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(1, occupancy(kfn, NT, 0)));
+                launch(ctx, "tqp_sort_tile_hist", kfn, dim3((unsigned)g), dim3(NT), 0, in, n, shifts[p], desc, thp);
             });
             ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
         }
