@@ -78,37 +78,24 @@ __device__ __forceinline__ uint32_t dslot(uint32_t d) { return d ^ (((d >> 5) * 
 template <int IN>
 __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64_t n, bool desc,
                                                          unsigned long long* out, uint32_t* __restrict__ th0) {
-    // persistent over tiles: one AND / OR atomic pair per CTA (same-address atomics from
-    // one CTA per tile serialise in L2)
     __shared__ uint32_t h[NW][H0_BINS];
     __shared__ uint64_t sa[NW], so[NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tiles = (n + H0_TILE - 1) / H0_TILE;
+    for (int d = lane; d < H0_BINS; d += 32) h[warp][d] = 0;
+    __syncwarp();
+    const int64_t base = (int64_t)blockIdx.x * H0_TILE;
     uint64_t a = ~0ull, o = 0;
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        for (int d = lane; d < H0_BINS; d += 32) h[warp][d] = 0;
-        __syncwarp();
-        const int64_t base = t * H0_TILE;
-        uint64_t u[H0_IPT];
+    uint64_t u[H0_IPT];
 #pragma unroll
-        for (int i = 0; i < H0_IPT; i++) {
-            const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
-            u[i] = pos < n ? load_u<IN>(keys, pos, desc) : 0;
-            if (pos < n) { a &= u[i]; o |= u[i]; }
-        }
+    for (int i = 0; i < H0_IPT; i++) {
+        const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
+        u[i] = pos < n ? load_u<IN>(keys, pos, desc) : 0;
+        if (pos < n) { a &= u[i]; o |= u[i]; }
+    }
 #pragma unroll
-        for (int i = 0; i < H0_IPT; i++) {
-            const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
-            if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
-        }
-        __syncthreads();
-        for (int d = tid; d < H0_BINS; d += NT) {
-            uint32_t c = 0;
-#pragma unroll
-            for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
-            th0[t * H0_BINS + d] = c;
-        }
-        __syncthreads();   // h is zeroed again for the next tile
+    for (int i = 0; i < H0_IPT; i++) {
+        const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
+        if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
     }
     for (int sft = 16; sft > 0; sft >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, sft);
@@ -120,6 +107,12 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
         for (int w = 1; w < NW; w++) { a &= sa[w]; o |= so[w]; }
         atomicAnd(&out[0], (unsigned long long)a);
         atomicOr(&out[1], (unsigned long long)o);
+    }
+    for (int d = tid; d < H0_BINS; d += NT) {
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
+        th0[(int64_t)blockIdx.x * H0_BINS + d] = c;
     }
 }
 
@@ -145,44 +138,33 @@ __device__ __forceinline__ KT load_key(const void* in_keys, int64_t pos, bool de
     return (KT)load_u<IN>(in_keys, pos, desc);
 }
 
-// (1) per-tile digit counts -> th[tile * BINS + d]; persistent over tiles, the next
-// tile's keys loaded while this one's counts are reduced and written
+// (1) per-tile digit counts -> th[tile * BINS + d]
 template <typename KT, int IN, int IPT, int RB>
 __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int64_t n, int shift, bool desc,
                                                        uint32_t* __restrict__ th) {
     constexpr int TILE = NT * IPT, BINS = 1 << RB;
     __shared__ uint32_t h[NW][BINS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t tiles = (n + TILE - 1) / TILE;
+    for (int d = lane; d < BINS; d += 32) h[warp][d] = 0;
+    __syncwarp();
+    const int64_t base = (int64_t)blockIdx.x * TILE;
     KT k[IPT];
-    auto load = [&](int64_t t) {
-        const int64_t base = t * TILE;
 #pragma unroll
-        for (int i = 0; i < IPT; i++) {
-            const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-            k[i] = pos < n ? load_key<KT, IN>(in_keys, pos, desc) : (KT)0;
-        }
-    };
-    int64_t t = blockIdx.x;
-    if (t < tiles) load(t);
-    for (; t < tiles; t += gridDim.x) {
-        for (int d = lane; d < BINS; d += 32) h[warp][d] = 0;
-        __syncwarp();
-        const int64_t base = t * TILE;
+    for (int i = 0; i < IPT; i++) {
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        k[i] = pos < n ? load_key<KT, IN>(in_keys, pos, desc) : (KT)0;
+    }
 #pragma unroll
-        for (int i = 0; i < IPT; i++) {
-            const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-            if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
-        }
-        if (t + gridDim.x < tiles) load(t + gridDim.x);
-        __syncthreads();
-        for (int d = tid; d < BINS; d += NT) {
-            uint32_t c = 0;
+    for (int i = 0; i < IPT; i++) {
+        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+        if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
+    }
+    __syncthreads();
+    for (int d = tid; d < BINS; d += NT) {
+        uint32_t c = 0;
 #pragma unroll
-            for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
-            th[t * BINS + d] = c;
-        }
-        __syncthreads();
+        for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
+        th[(int64_t)blockIdx.x * BINS + d] = c;
     }
 }
 
@@ -644,9 +626,8 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         uint32_t* thp = (p == 0 && th0) ? th0 : th.get();   // pass 0: histogram fused into the AND/OR pass
         if (thp != th0) {
             dispatch_in(mode, [&](auto m) {
-                auto* kfn = tile_hist_kernel<KT, decltype(m)::value, IPT, RB>;
-                const int64_t g = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(1, occupancy(kfn, NT, 0)));
-                launch(ctx, "tqp_sort_tile_hist", kfn, dim3((unsigned)g), dim3(NT), 0, in, n, shifts[p], desc, thp);
+                launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT, RB>,
+                       dim3((unsigned)tiles), dim3(NT), 0, in, n, shifts[p], desc, thp);
             });
             ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
         }
@@ -705,12 +686,9 @@ void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     const int grid = (int)std::min<int64_t>(ceil_div(n, NT * 8), (int64_t)ctx->num_sms * 4);
     dispatch_in(mode, [&](auto m) {
         if constexpr (decltype(m)::value != IN_INTERNAL) {
-            if (th0) {
-                auto* kfn = andor_hist0_kernel<decltype(m)::value>;
-                const int64_t g = std::min<int64_t>(ceil_div(n, H0_TILE),
-                                                    (int64_t)ctx->num_sms * std::max(1, occupancy(kfn, NT, 0)));
-                launch(ctx, "tqp_sort_andor", kfn, dim3((unsigned)g), dim3(NT), 0, keys, n, desc, ao, th0);
-            }
+            if (th0)
+                launch(ctx, "tqp_sort_andor", andor_hist0_kernel<decltype(m)::value>, dim3((unsigned)ceil_div(n, H0_TILE)),
+                       dim3(NT), 0, keys, n, desc, ao, th0);
             else
                 launch(ctx, "tqp_sort_andor", andor_kernel<decltype(m)::value>, dim3(grid), dim3(NT), 0, keys, n, desc, ao);
         }
