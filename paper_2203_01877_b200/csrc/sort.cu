@@ -75,6 +75,13 @@ constexpr int H0_IPT = 16, H0_TILE = 256 * H0_IPT, H0_BINS = 512;
 // structure in their low bits (TPC-H order keys take 8 of every 32 values, keys that
 // are multiples of 2^k) otherwise pile their digits onto a few banks.
 __device__ __forceinline__ uint32_t dslot(uint32_t d) { return d ^ (((d >> 5) * 9u) & 31u); }
+
+// Slot of tile rank r in the digit-ordered staging buffer: the low 4 bits XORed with
+// bits 5..8, a bijection within each aligned group of 16. Consecutive ranks (the
+// write-out) keep distinct banks; ranks 32 apart -- what an already ordered input
+// produces, e.g. orders rows in key order, whose digits repeat every 128 rows --
+// no longer land on one bank (32-way conflicts on the staging stores otherwise).
+__device__ __forceinline__ uint32_t kslot(uint32_t r) { return r ^ ((r >> 5) & 15u); }
 template <int IN>
 __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64_t n, bool desc,
                                                          unsigned long long* out, uint32_t* __restrict__ th0) {
@@ -493,10 +500,10 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
         for (int i = 0; i < IPT; i++) {
             if (i * 32 < rem) {
                 if (sizeof(KT) == 4) {
-                    kp[rk[i]] = make_uint2((uint32_t)key[i], pm[i]);
+                    kp[kslot(rk[i])] = make_uint2((uint32_t)key[i], pm[i]);
                 } else {
-                    s.u.sorted.keys[rk[i]] = key[i];
-                    s.u.sorted.perm[rk[i]] = pm[i];
+                    s.u.sorted.keys[kslot(rk[i])] = key[i];
+                    s.u.sorted.perm[kslot(rk[i])] = pm[i];
                 }
             }
         }
@@ -509,15 +516,15 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             uint32_t* op = a.out_perm;
             if (sizeof(KT) == 4 && ok && op) {
                 for (int j = tid; j < tile_n; j += NT) {
-                    const uint2 v = kp[j];
+                    const uint2 v = kp[kslot(j)];
                     const uint32_t dst = s.gstart[(v.x >> a.shift) & DM] + (uint32_t)j;
                     ok[dst] = (KT)v.x;
                     op[dst] = v.y;
                 }
             } else {
                 for (int j = tid; j < tile_n; j += NT) {
-                    const KT kk = sizeof(KT) == 4 ? (KT)kp[j].x : s.u.sorted.keys[j];
-                    const uint32_t p = sizeof(KT) == 4 ? kp[j].y : s.u.sorted.perm[j];
+                    const KT kk = sizeof(KT) == 4 ? (KT)kp[kslot(j)].x : s.u.sorted.keys[kslot(j)];
+                    const uint32_t p = sizeof(KT) == 4 ? kp[kslot(j)].y : s.u.sorted.perm[kslot(j)];
                     const uint32_t dst = s.gstart[(uint32_t)(kk >> a.shift) & DM] + (uint32_t)j;
                     if (ok) ok[dst] = kk;
                     if (op) op[dst] = p;
@@ -525,8 +532,8 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             }
         } else
         for (int j = tid; j < tile_n; j += NT) {
-            const KT kk = sizeof(KT) == 4 ? (KT)kp[j].x : s.u.sorted.keys[j];
-            const uint32_t p = sizeof(KT) == 4 ? kp[j].y : s.u.sorted.perm[j];
+            const KT kk = sizeof(KT) == 4 ? (KT)kp[kslot(j)].x : s.u.sorted.keys[kslot(j)];
+            const uint32_t p = sizeof(KT) == 4 ? kp[kslot(j)].y : s.u.sorted.perm[kslot(j)];
             const uint32_t d = (uint32_t)(kk >> a.shift) & DM;
             const int64_t dst = (int64_t)(uint32_t)(s.gstart[d] + (uint32_t)j);   // gdelta[d] + j (mod 2^32, n < 2^30)
             if (a.out_keys) ((KT*)a.out_keys)[dst] = kk;
