@@ -425,31 +425,37 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                 uses[st]++;
             }
         }
+        // ranking, specialised for full tiles (every item valid: no per-item guards)
+        auto rank_items = [&](auto fullc) {
+            constexpr bool FULL = decltype(fullc)::value;
 #pragma unroll
-        for (int i = 0; i < IPT; i++) {
-            const bool valid = i * 32 < rem;
-            const uint32_t d = dslot((uint32_t)(key[i] >> a.shift) & DM);
-            // peers = lanes of this warp with the same digit: every lane ORs its bit into
-            // the digit's match word, reads the word back, and the leader clears it
-            unsigned peers;
-            uint32_t* mw = &s.u.match[warp][d];
-            if (PEER_MATCH_ANY) {
-                peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
-                if (!valid) peers = 0;
-            } else {
-                if (valid) atomicOr(mw, 1u << lane);
-                __syncwarp();
-                peers = valid ? *reinterpret_cast<volatile uint32_t*>(mw) : 0u;
-                __syncwarp();
+            for (int i = 0; i < IPT; i++) {
+                const bool valid = FULL || i * 32 < rem;
+                const uint32_t d = dslot((uint32_t)(key[i] >> a.shift) & DM);
+                // peers = lanes of this warp with the same digit: every lane ORs its bit into
+                // the digit's match word, reads the word back, and the leader clears it
+                unsigned peers;
+                uint32_t* mw = &s.u.match[warp][d];
+                if (PEER_MATCH_ANY) {
+                    peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
+                    if (!valid) peers = 0;
+                } else {
+                    if (valid) atomicOr(mw, 1u << lane);
+                    __syncwarp();
+                    peers = valid ? *reinterpret_cast<volatile uint32_t*>(mw) : 0u;
+                    __syncwarp();
+                }
+                const uint32_t leader = 31 - __clz(peers);
+                uint32_t old = 0;
+                if (valid && lane == leader) {
+                    old = atomicAdd(&s.u.whist[warp][d], (uint32_t)__popc(peers));
+                    if (!PEER_MATCH_ANY) *mw = 0;
+                }
+                rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
             }
-            const uint32_t leader = 31 - __clz(peers);
-            uint32_t old = 0;
-            if (valid && lane == leader) {
-                old = atomicAdd(&s.u.whist[warp][d], (uint32_t)__popc(peers));
-                if (!PEER_MATCH_ANY) *mw = 0;
-            }
-            rk[i] = old | (leader << 16) | ((uint32_t)__popc(peers & lt) << 24);
-        }
+        };
+        if (base + TILE <= a.n) rank_items(std::true_type{});
+        else rank_items(std::false_type{});
 #pragma unroll
         for (int i = 0; i < IPT; i++) {
             const uint32_t b = __shfl_sync(0xffffffffu, rk[i] & 0xFFFFu, (rk[i] >> 16) & 31u);
