@@ -52,7 +52,9 @@ typedef enum {
 /* Column element types ("§4.1 Data Representation": numeric
  * n x 1 tensors; 1-character strings as uint8 (reading R19); dates as int32 days
  * or int64 microseconds (reading R18)). Comparisons: u8 unsigned, ints signed. */
-typedef enum { TQP_U8 = 1, TQP_I32 = 2, TQP_I64 = 3 } tqp_dtype;
+/* TQP_F64: IEEE double value columns, accepted only as factor columns of group-by
+ * aggregates; every other use -> TQP_ERR_INVALID_ARGUMENT. */
+typedef enum { TQP_U8 = 1, TQP_I32 = 2, TQP_I64 = 3, TQP_F64 = 4 } tqp_dtype;
 
 /* A column: `data` points to n elements of `dtype`, contiguous. */
 typedef struct {

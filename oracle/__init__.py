@@ -243,3 +243,59 @@ def groupby_agg(cols, key_idx, aggs, preds=()):
         else:
             out.append([int(res[i, a, 0]) for i in range(g)])
     return {"n_groups": g, "keys": [keys[:, k].copy() for k in range(len(key_idx))], "results": out}
+
+
+_NP_OPS = {LT: np.less, LE: np.less_equal, GT: np.greater, GE: np.greater_equal, EQ: np.equal, NE: np.not_equal}
+
+
+def groupby_agg_f64(cols, key_idx, aggs, preds=()):
+    """Group-by whose aggregates take float64 factor columns (include/tqp.h TQP_F64;
+    SURVEY.md §8(f) NEXT 4), written out in numpy: rows passing the AND of the
+    predicates, grouped by the key tuple in ascending order (Alg. 2,
+    PAPER.md:340-367), value per row = prod_f (add_f + sign_f * x_f) in float64, left to
+    right. SUM = the correctly rounded sum of the group's values (math.fsum), MIN / MAX,
+    COUNT = rows, AVG = SUM / COUNT. Returns dict(keys, results, abs_sums) with
+    abs_sums[a][g] = sum of |v| (the scale of an unordered float sum's error bound)."""
+    import math
+    cols = [np.asarray(c) for c in cols]
+    n = cols[0].size if cols else 0
+    m = np.ones(n, dtype=bool)
+    for c, op, v in preds:
+        o = _OPS[op] if isinstance(op, str) else int(op)
+        m &= _NP_OPS[o](cols[c].astype(np.int64), np.int64(v))
+    rows = np.nonzero(m)[0]
+    if key_idx:
+        kt = np.stack([cols[k].astype(np.int64)[rows] for k in key_idx], axis=1)
+        uk, inv = np.unique(kt, axis=0, return_inverse=True)
+        inv = inv.reshape(-1)
+        G = uk.shape[0]
+        keys = [uk[:, j] for j in range(len(key_idx))]
+    else:
+        inv = np.zeros(rows.size, dtype=np.int64)
+        G = 1
+        keys = []
+    members = [rows[inv == g] for g in range(G)] if key_idx else [rows]
+    results, abs_sums = [], []
+    for op, factors in aggs:
+        o = _AGGS[op] if isinstance(op, str) else int(op)
+        v = np.ones(n, dtype=np.float64)
+        for f, (c, add, sign) in enumerate(factors):
+            t = np.float64(add) + np.float64(sign) * cols[c].astype(np.float64)
+            v = t if f == 0 else v * t
+        out = []
+        for mem in members:
+            x = v[mem]
+            if o == COUNT:
+                out.append(int(mem.size))
+            elif o == SUM:
+                out.append(math.fsum(x.tolist()))
+            elif o == AVG:
+                out.append(math.fsum(x.tolist()) / mem.size if mem.size else float("nan"))
+            elif o == MIN:
+                out.append(float(x.min()) if mem.size else float("inf"))
+            else:
+                out.append(float(x.max()) if mem.size else float("-inf"))
+        results.append(out)
+        abs_sums.append([math.fsum(np.abs(v[mem]).tolist()) for mem in members])
+    return {"keys": keys, "results": results, "abs_sums": abs_sums, "counts": [int(x.size) for x in members]}
+

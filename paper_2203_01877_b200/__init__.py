@@ -27,7 +27,7 @@ _lib = ctypes.CDLL(_LIB_PATH)
 
 TQP_OK, TQP_ERR_INVALID_ARGUMENT, TQP_ERR_DUPLICATE_BUILD_KEY, TQP_ERR_OUT_OF_MEMORY, TQP_ERR_CUDA, \
     TQP_ERR_OVERFLOW, TQP_ERR_CAPACITY = range(7)
-TQP_U8, TQP_I32, TQP_I64 = 1, 2, 3
+TQP_U8, TQP_I32, TQP_I64, TQP_F64 = 1, 2, 3, 4
 OPS = {"lt": 0, "le": 1, "gt": 2, "ge": 3, "eq": 4, "ne": 5, "<": 0, "<=": 1, ">": 2, ">=": 3, "==": 4, "!=": 5}
 AGGS = {"sum": 0, "count": 1, "min": 2, "max": 3, "avg": 4}
 MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
@@ -116,7 +116,8 @@ def abi_version():
     return _lib.tqp_abi_version()
 
 
-_DT = {torch.uint8: TQP_U8, torch.bool: TQP_U8, torch.int32: TQP_I32, torch.int64: TQP_I64}
+_DT = {torch.uint8: TQP_U8, torch.bool: TQP_U8, torch.int32: TQP_I32, torch.int64: TQP_I64,
+       torch.float64: TQP_F64}   # float64: group-by aggregate factor columns only
 
 
 def _dev_tensor(t, device):
@@ -359,7 +360,8 @@ class Context:
         """Sort-based group-by (Alg. 2) with fused pre-filter.
 
         aggs: [(op, [(col, add, sign), ...])]. Returns dict(n_groups, keys=[tensor per key col],
-        results=[SUM: int64 (G,2) = (lo, hi) of the int128 | COUNT/MIN/MAX: int64 | AVG: float64])."""
+        results=[SUM: int64 (G,2) = (lo, hi) of the int128 | COUNT/MIN/MAX: int64 | AVG: float64]);
+        an aggregate with a float64 factor column is evaluated in fp64 and returns float64 (G,)."""
         self._sync_stream()
         cs = [_dev_tensor(c, self.device) for c in cols]
         n = cs[0].numel() if cs else 0
@@ -376,9 +378,11 @@ class Context:
             keys = [torch.empty(g, dtype=cs[k].dtype if cs[k].dtype != torch.bool else torch.uint8,
                                 device=self.device) for k in key_idx]
             res = []
-            for op, _ in aggs:
+            for op, factors in aggs:
                 o = AGGS[op] if isinstance(op, str) else int(op)
-                if o == 0:
+                if o != 1 and any(cs[c].dtype == torch.float64 for c, _, _ in factors):
+                    res.append(torch.empty(g, dtype=torch.float64, device=self.device))
+                elif o == 0:
                     res.append(torch.empty((g, 2), dtype=torch.int64, device=self.device))
                 elif o == 4:
                     res.append(torch.empty(g, dtype=torch.float64, device=self.device))

@@ -209,6 +209,7 @@ inline size_t dtype_size(int dt) {
         case TQP_I32: return 4;
         case TQP_I64: return 8;
         case DT_U64: return 8;
+        case TQP_F64: return 8;
     }
     return 0;
 }

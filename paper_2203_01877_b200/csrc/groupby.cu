@@ -38,6 +38,13 @@ struct tqp_groupby_plan {
     tqp::DevBuf<int64_t> gcount;
     tqp::DevBuf<uint64_t> glo[TQP_MAX_AGGS];
     tqp::DevBuf<int64_t> ghi[TQP_MAX_AGGS];
+    // fp64 aggregates (TQP_F64 factor columns): computed beside the integer plan
+    bool has_f64 = false;
+    int n_user_aggs = 0;
+    int uop[TQP_MAX_AGGS];         // user aggregate op
+    int imap[TQP_MAX_AGGS];        // user aggregate -> integer aggregate index, or -1 (fp64)
+    tqp::DevBuf<double> gf[TQP_MAX_AGGS];   // fp64 aggregate per group: SUM (AVG: the sum) as double,
+                                            // MIN / MAX as order-preserving int64 bit patterns
 };
 
 namespace tqp {
@@ -2050,9 +2057,9 @@ void make_pairs(tqp_groupby_plan* PL, const tqp_agg* aggs, int n_aggs, int (*pf)
 }
 }  // namespace
 
-tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, const int32_t* key_idx,
-                                  int n_keys, const tqp_pred* preds, int n_preds, const tqp_agg* aggs, int n_aggs,
-                                  int64_t* n_groups_host) {
+static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n,
+                                             const int32_t* key_idx, int n_keys, const tqp_pred* preds, int n_preds,
+                                             const tqp_agg* aggs, int n_aggs, int64_t* n_groups_host) {
     if (n < 0 || n_cols < 0 || n_keys < 0 || n_keys > TQP_MAX_KEYS || n_preds < 0 || n_preds > TQP_MAX_PREDS ||
         n_aggs < 0 || n_aggs > TQP_MAX_AGGS)
         fail(TQP_ERR_INVALID_ARGUMENT, "groupby: bad sizes");
@@ -2360,7 +2367,8 @@ tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols,
     }
 }
 
-void groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* PL, void* const* keys_out, void* const* results_out) {
+static void groupby_fetch_int(tqp_ctx* ctx, const tqp_groupby_plan* PL, void* const* keys_out,
+                              void* const* results_out) {
     if (PL->G == 0) return;
     FinArgs f{};
     f.n_keys = PL->n_keys;
@@ -2497,6 +2505,270 @@ tqp_groupby_plan* groupby_merge(tqp_ctx* ctx, int64_t m, const tqp_col* key_cols
     } catch (...) {
         delete PL;
         throw;
+    }
+}
+
+// ------------------------------------------------------- fp64 aggregates
+// SURVEY.md §8(f) NEXT 4 ("fp64 value columns"): aggregates whose factors include a
+// TQP_F64 column are evaluated in fp64, value = prod_f (add_f + sign_f * x_f) left to
+// right, beside the integer plan: the plan's groups (sorted packed keys) are found by a
+// binary search of each passing row's packed key, and the values are reduced with
+// atomics -- per CTA in shared memory when the groups x aggregates fit, then once per
+// CTA into the global accumulators. SUM is therefore a float sum in an unspecified
+// order (|error| <= (m - 1) u sum|v| for a group of m rows, u = 2^-53); MIN / MAX are
+// exact (order-preserving int64 images of the doubles, NaN inputs unsupported).
+namespace {
+constexpr int F64_PRIV = 2048;   // groups x fp64 aggregates kept per CTA in shared memory
+
+struct F64Args {
+    int64_t n;
+    TermSet ts;
+    const void* tcol[TQP_MAX_PREDS];
+    int n_keys;
+    const void* kcol[TQP_MAX_KEYS];
+    int kdt[TQP_MAX_KEYS];
+    const unsigned long long* krange;
+    const uint64_t* gkey;
+    int64_t G;
+    int na;
+    int op[TQP_MAX_AGGS];          // P_SUM / P_MIN / P_MAX
+    int nf[TQP_MAX_AGGS];
+    const void* fcol[TQP_MAX_AGGS][3];
+    int fdt[TQP_MAX_AGGS][3];
+    double fadd[TQP_MAX_AGGS][3];
+    double fsign[TQP_MAX_AGGS][3];
+    unsigned long long* acc[TQP_MAX_AGGS];   // G slots each (double bits or ordered int64)
+    int priv;
+};
+
+__device__ __forceinline__ long long dord(double x) {   // order-preserving int64 image
+    const long long b = __double_as_longlong(x);
+    return b >= 0 ? b : b ^ 0x7FFFFFFFFFFFFFFFll;
+}
+__device__ __forceinline__ double dunord(long long o) {
+    return __longlong_as_double(o >= 0 ? o : o ^ 0x7FFFFFFFFFFFFFFFll);
+}
+
+__device__ __forceinline__ void f64_acc(unsigned long long* p, int op, double v) {
+    if (op == P_SUM) atomicAdd(reinterpret_cast<double*>(p), v);
+    else if (op == P_MIN) atomicMin(reinterpret_cast<long long*>(p), dord(v));
+    else atomicMax(reinterpret_cast<long long*>(p), dord(v));
+}
+
+__device__ __forceinline__ unsigned long long f64_init(int op) {
+    if (op == P_SUM) return 0ull;   // +0.0
+    return (unsigned long long)(op == P_MIN ? dord(__longlong_as_double(0x7FF0000000000000ll))
+                                            : dord(__longlong_as_double((long long)0xFFF0000000000000ull)));
+}
+
+__global__ void __launch_bounds__(256) gb_f64_init_kernel(F64Args a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.G * a.na; i += (int64_t)gridDim.x * blockDim.x)
+        a.acc[i % a.na][i / a.na] = f64_init(a.op[i % a.na]);
+}
+
+__global__ void __launch_bounds__(256) gb_f64_kernel(F64Args a) {
+    extern __shared__ unsigned long long s_acc[];   // [G][na] when a.priv
+    if (a.priv) {
+        for (int i = threadIdx.x; i < a.G * a.na; i += blockDim.x) s_acc[i] = f64_init(a.op[i % a.na]);
+        __syncthreads();
+    }
+    uint64_t kmin[TQP_MAX_KEYS];
+    int sh[TQP_MAX_KEYS], wd[TQP_MAX_KEYS];
+    key_layout(a.krange, a.n_keys, kmin, sh, wd);
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < a.n; r += (int64_t)gridDim.x * blockDim.x) {
+        bool pass = !a.ts.never;
+        for (int q = 0; q < a.ts.n && pass; q++) {
+            const Term& t = a.ts.t[q];
+            const int64_t x = load_as_i64(a.tcol[q], t.dt, r);
+            pass = t.dt == TQP_I64 ? term64((uint64_t)x, t.lo, t.width, t.neg)
+                                   : term32((uint32_t)x, (uint32_t)t.lo, (uint32_t)t.width, t.neg);
+        }
+        if (!pass) continue;
+        uint64_t key = 0;
+        for (int k = 0; k < a.n_keys; k++)
+            key |= (key_part(load_as_i64(a.kcol[k], a.kdt[k], r), a.kdt[k]) - kmin[k]) << sh[k];
+        int64_t lo = 0, hi = a.G - 1;   // the row's group: its packed key is one of gkey
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (a.gkey[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        for (int j = 0; j < a.na; j++) {
+            double v = 1.0;
+            for (int f = 0; f < a.nf[j]; f++) {
+                const double x = a.fdt[j][f] == TQP_F64 ? reinterpret_cast<const double*>(a.fcol[j][f])[r]
+                                                        : (double)load_as_i64(a.fcol[j][f], a.fdt[j][f], r);
+                const double t = a.fadd[j][f] + a.fsign[j][f] * x;
+                v = f == 0 ? t : v * t;
+            }
+            f64_acc(a.priv ? &s_acc[lo * a.na + j] : &a.acc[j][lo], a.op[j], v);
+        }
+    }
+    if (a.priv) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < a.G * a.na; i += blockDim.x) {
+            const int j = i % a.na;
+            if (s_acc[i] != f64_init(a.op[j])) {
+                if (a.op[j] == P_SUM) atomicAdd(reinterpret_cast<double*>(&a.acc[j][i / a.na]), __longlong_as_double((long long)s_acc[i]));
+                else if (a.op[j] == P_MIN) atomicMin(reinterpret_cast<long long*>(&a.acc[j][i / a.na]), (long long)s_acc[i]);
+                else atomicMax(reinterpret_cast<long long*>(&a.acc[j][i / a.na]), (long long)s_acc[i]);
+            }
+        }
+    }
+}
+
+struct F64Fin {
+    int64_t G;
+    int na;
+    int uop[TQP_MAX_AGGS];
+    const unsigned long long* acc[TQP_MAX_AGGS];
+    const int64_t* gcount;
+    double* out[TQP_MAX_AGGS];
+};
+
+__global__ void gb_f64_fetch_kernel(F64Fin f) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < f.G; g += (int64_t)gridDim.x * blockDim.x)
+        for (int j = 0; j < f.na; j++) {
+            if (!f.out[j]) continue;
+            const long long w = (long long)f.acc[j][g];
+            double v;
+            if (f.uop[j] == TQP_SUM) v = __longlong_as_double(w);
+            else if (f.uop[j] == TQP_AVG) v = __longlong_as_double(w) / (double)f.gcount[g];
+            else v = dunord(w);
+            f.out[j][g] = v;
+        }
+}
+}  // namespace
+
+tqp_groupby_plan* groupby_prepare(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, const int32_t* key_idx,
+                                  int n_keys, const tqp_pred* preds, int n_preds, const tqp_agg* aggs, int n_aggs,
+                                  int64_t* n_groups_host) {
+    if (n_cols < 0 || n_aggs < 0 || n_aggs > TQP_MAX_AGGS || n_keys < 0 || n_preds < 0)
+        fail(TQP_ERR_INVALID_ARGUMENT, "groupby: bad sizes");
+    bool is_f64[TQP_MAX_AGGS] = {};
+    bool any = false;
+    for (int g = 0; g < n_aggs; g++) {
+        if (aggs[g].op == TQP_COUNT || aggs[g].n_factors < 0 || aggs[g].n_factors > 3) continue;
+        for (int f = 0; f < aggs[g].n_factors; f++) {
+            const int c = aggs[g].col[f];
+            if (c >= 0 && c < n_cols && cols[c].dtype == TQP_F64) is_f64[g] = true;
+        }
+        any = any || is_f64[g];
+    }
+    bool f64_col = false;
+    for (int c = 0; c < n_cols; c++) f64_col = f64_col || cols[c].dtype == TQP_F64;
+    if (!f64_col) {
+        tqp_groupby_plan* P = groupby_prepare_int(ctx, cols, n_cols, n, key_idx, n_keys, preds, n_preds, aggs, n_aggs,
+                                                  n_groups_host);
+        P->n_user_aggs = n_aggs;
+        return P;
+    }
+    // fp64 columns: only as aggregate factors; the integer plan sees a never-read u8 view
+    for (int k = 0; k < n_keys; k++)
+        if (key_idx[k] >= 0 && key_idx[k] < n_cols && cols[key_idx[k]].dtype == TQP_F64)
+            fail(TQP_ERR_INVALID_ARGUMENT, "groupby: fp64 columns cannot be group keys");
+    for (int q = 0; q < n_preds; q++)
+        if (preds[q].col >= 0 && preds[q].col < n_cols && cols[preds[q].col].dtype == TQP_F64)
+            fail(TQP_ERR_INVALID_ARGUMENT, "groupby: fp64 columns cannot carry predicates");
+    std::vector<tqp_col> c2(cols, cols + n_cols);
+    for (auto& c : c2)
+        if (c.dtype == TQP_F64) {
+            if (n > 0 && !c.data) fail(TQP_ERR_INVALID_ARGUMENT, "groupby column: null data");
+            c.dtype = TQP_U8;
+        }
+    for (int g = 0; g < n_aggs; g++) {
+        if (!is_f64[g]) continue;
+        if (aggs[g].op < TQP_SUM || aggs[g].op > TQP_AVG) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: aggregate");
+        for (int f = 0; f < aggs[g].n_factors; f++)
+            if (aggs[g].col[f] < 0 || aggs[g].col[f] >= n_cols || (aggs[g].sign[f] != 1 && aggs[g].sign[f] != -1))
+                fail(TQP_ERR_INVALID_ARGUMENT, "groupby: aggregate factor");
+    }
+    std::vector<tqp_agg> ia;
+    int imap[TQP_MAX_AGGS];
+    for (int g = 0; g < n_aggs; g++) {
+        imap[g] = is_f64[g] ? -1 : (int)ia.size();
+        if (!is_f64[g]) ia.push_back(aggs[g]);
+    }
+    tqp_groupby_plan* P = groupby_prepare_int(ctx, c2.data(), n_cols, n, key_idx, n_keys, preds, n_preds,
+                                              ia.empty() ? nullptr : ia.data(), (int)ia.size(), n_groups_host);
+    try {
+        P->n_user_aggs = n_aggs;
+        P->has_f64 = any;
+        for (int g = 0; g < n_aggs; g++) {
+            P->uop[g] = aggs[g].op;
+            P->imap[g] = imap[g];
+        }
+        if (!any || P->G == 0) return P;
+        F64Args a{};
+        a.n = n;
+        a.ts = make_terms(preds, n_preds, [&](int c) { return cols[c].dtype; });
+        for (int q = 0; q < a.ts.n; q++) a.tcol[q] = cols[a.ts.t[q].col].data;
+        a.n_keys = n_keys;
+        for (int k = 0; k < n_keys; k++) {
+            a.kcol[k] = cols[key_idx[k]].data;
+            a.kdt[k] = cols[key_idx[k]].dtype;
+        }
+        a.krange = P->krange.get();
+        a.gkey = P->gkey.get();
+        a.G = P->G;
+        for (int g = 0; g < n_aggs; g++) {
+            if (!is_f64[g]) continue;
+            const int j = a.na++;
+            a.op[j] = aggs[g].op == TQP_MIN ? P_MIN : (aggs[g].op == TQP_MAX ? P_MAX : P_SUM);
+            a.nf[j] = aggs[g].n_factors;
+            for (int f = 0; f < aggs[g].n_factors; f++) {
+                const tqp_col& c = cols[aggs[g].col[f]];
+                a.fcol[j][f] = c.data;
+                a.fdt[j][f] = c.dtype;
+                a.fadd[j][f] = (double)aggs[g].add[f];
+                a.fsign[j][f] = (double)aggs[g].sign[f];
+            }
+            P->gf[g].alloc(ctx, P->G);
+            a.acc[j] = reinterpret_cast<unsigned long long*>(P->gf[g].get());
+        }
+        const int gi = (int)std::min<int64_t>(ceil_div(P->G * a.na, 256), (int64_t)ctx->num_sms * 8);
+        launch(ctx, "tqp_groupby_f64", gb_f64_init_kernel, dim3(gi), dim3(256), 0, a);
+        if (n > 0) {
+            a.priv = P->G * a.na <= F64_PRIV ? 1 : 0;
+            const size_t smem = a.priv ? (size_t)P->G * a.na * 8 : 0;
+            if (smem > 48 * 1024) set_smem(gb_f64_kernel, smem);
+            const int occ = std::max(1, occupancy(gb_f64_kernel, 256, smem));
+            const int g = (int)std::min<int64_t>(ceil_div(n, 256), (int64_t)ctx->num_sms * occ);
+            launch(ctx, "tqp_groupby_f64", gb_f64_kernel, dim3(g), dim3(256), smem, a);
+            double b = 0;
+            for (int c = 0; c < n_cols; c++) b += (double)dtype_size(cols[c].dtype);
+            ctx->add_bytes("tqp_groupby_f64", b * (double)n);
+        }
+        return P;
+    } catch (...) {
+        delete P;
+        throw;
+    }
+}
+
+void groupby_fetch(tqp_ctx* ctx, const tqp_groupby_plan* PL, void* const* keys_out, void* const* results_out) {
+    if (!PL->has_f64) {   // integer plans (and merge plans) as they are
+        groupby_fetch_int(ctx, PL, keys_out, results_out);
+        return;
+    }
+    void* iout[TQP_MAX_AGGS] = {};
+    F64Fin f{};
+    f.G = PL->G;
+    f.gcount = PL->gcount.get();
+    for (int g = 0; g < PL->n_user_aggs; g++) {
+        void* o = results_out ? results_out[g] : nullptr;
+        if (PL->imap[g] >= 0) {
+            iout[PL->imap[g]] = o;
+        } else {
+            const int j = f.na++;
+            f.uop[j] = PL->uop[g];
+            f.acc[j] = reinterpret_cast<const unsigned long long*>(PL->gf[g].get());
+            f.out[j] = static_cast<double*>(o);
+        }
+    }
+    groupby_fetch_int(ctx, PL, keys_out, iout);
+    if (f.na > 0 && PL->G > 0) {
+        const int g = (int)std::min<int64_t>(ceil_div(PL->G, 256), (int64_t)ctx->num_sms * 8);
+        launch(ctx, "tqp_groupby_f64", gb_f64_fetch_kernel, dim3(g), dim3(256), 0, f);
     }
 }
 

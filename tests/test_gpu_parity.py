@@ -202,6 +202,30 @@ def test_pkfk_sf10_full_size_closed_form(T):
         assert int(lo[i]) == int(blo[0])
 
 
+def test_smj_sf10_full_size_closed_form(T):
+    """The bench's SMJ (orders x lineitem at SF10, full size, same calls as bench.py): the
+    pairs are (parent[r], r) in (key, l, r) order; order keys ascend with the order row, so
+    that is lineitem rows stably sorted by parent (torch: a library route). Sampled pair
+    windows against the oracle's per-offset definition."""
+    orders, li = tpch_orders_lineitem(10.0, seed=42, device="cuda")
+    ok, lk = orders["o_orderkey"], li["l_orderkey"]
+    plan = T.smj_prepare(ok, lk)
+    assert plan.size == lk.numel()
+    lo, ro = plan.expand(0, plan.size)
+    want_ro = torch.sort(li["l_parent"], stable=True).indices
+    assert torch.equal(ro, want_ro)
+    assert torch.equal(lo, li["l_parent"][want_ro])
+    plan.release()
+    # windows: the oracle on the keys of a slice of orders (its pairs are a contiguous
+    # range of the full output, shifted by the lineitems of the preceding orders)
+    o0, o1 = 7_000_000, 7_000_400
+    sel = ((lk >= ok[o0]) & (lk <= ok[o1 - 1])).nonzero().flatten()
+    olo, oro = oracle.smj_join(npy(ok[o0:o1]), npy(lk[sel]))
+    start = int((lk < ok[o0]).sum())
+    assert np.array_equal(npy(lo[start:start + olo.size]) - o0, olo)
+    assert np.array_equal(npy(ro[start:start + oro.size]), npy(sel)[oro])
+
+
 @pytest.mark.parametrize("anti", [False, True])
 def test_pkfk_semi_anti(T, anti):
     rng = np.random.default_rng(5)
@@ -832,6 +856,81 @@ def test_launch_counter_and_profiling(T):
     assert st["tqp_sort_scatter"][1] >= 1 and st["tqp_sort_scatter"][0] > 0
     assert all(v[1] == 0 and v[0] == 0 for k, v in st.items() if k != "tqp_sort_scatter")
     assert ctx.launch_count() >= 3
+
+
+def _check_f64(got, want, aggs, f64_idx):
+    """fp64 aggregates against the oracle: MIN / MAX / COUNT exact; SUM / AVG within the
+    bound of an unordered float sum, |d| <= 2 m u sum|v| (u = 2^-53, m rows in the group)."""
+    u = 2.0 ** -53
+    for a in f64_idx:
+        op = aggs[a][0]
+        g = got["results"][a].cpu().numpy()
+        w = np.array(want["results"][a], dtype=np.float64)
+        if op in ("min", "max"):
+            assert np.array_equal(g, w), op
+            continue
+        m = np.array(want["counts"], dtype=np.float64)
+        bound = 2 * m * u * np.array(want["abs_sums"][a])
+        if op == "avg":
+            bound = bound / np.maximum(m, 1) + 4 * u * np.abs(w)
+            nan = np.isnan(w)
+            assert np.array_equal(np.isnan(g), nan)
+            g, w, bound = g[~nan], w[~nan], bound[~nan]
+        assert np.all(np.abs(g - w) <= bound + 1e-300), (op, np.max(np.abs(g - w) - bound))
+
+
+@pytest.mark.parametrize("ng", [1, 6, 300, 50_000])
+def test_groupby_f64_aggregates(T, ng):
+    """fp64 value columns (TQP_F64) beside integer aggregates, with a fused filter; shared-
+    memory accumulators (few groups) and global ones (50K groups)."""
+    rng = np.random.default_rng(ng)
+    n = 400_003
+    k = rng.integers(0, ng, n).astype(np.int32)
+    x = rng.normal(0.0, 1e4, n)
+    q = rng.integers(0, 5000, n).astype(np.int64)
+    d = rng.integers(0, 11, n).astype(np.uint8)
+    cols = [cu(k, torch.int32), torch.tensor(x, device="cuda"), cu(q), cu(d, torch.uint8)]
+    aggs = [("sum", [(1, 0, 1)]), ("sum", [(2, 0, 1)]), ("avg", [(1, 0, 1)]), ("min", [(1, 0, 1)]),
+            ("max", [(1, 0, 1), (3, 100, -1)]), ("sum", [(1, 0, 1), (3, 100, -1), (2, 1, 1)]), ("count", [])]
+    preds = [(2, "lt", 4500), (3, "ne", 7)]
+    got = T.groupby_agg(cols, [0], aggs, preds)
+    wf = oracle.groupby_agg_f64([k, x, q, d], [0], aggs, preds)
+    wi = oracle.groupby_agg([k, q, d], [0], [("sum", [(1, 0, 1)])], [(1, "lt", 4500), (2, "ne", 7)])
+    assert got["n_groups"] == len(wf["counts"])
+    assert npy(got["keys"][0]).tolist() == [int(v) for v in wf["keys"][0]]
+    assert T.int128_to_ints(got["results"][1]) == wi["results"][0]
+    assert npy(got["results"][6]).tolist() == wf["counts"]
+    _check_f64(got, wf, aggs, [0, 2, 3, 4, 5])
+
+
+def test_groupby_f64_exact_sums_and_global(T):
+    """Values on a 2^-4 grid with small magnitudes: every partial sum is exact, so SUM must
+    equal the oracle bit for bit whatever the order; no keys; empty global group."""
+    rng = np.random.default_rng(5)
+    n = 1_000_001
+    x = rng.integers(-4000, 4000, n) / 16.0
+    k = rng.integers(0, 3, n).astype(np.uint8)
+    cols = [cu(k, torch.uint8), torch.tensor(x, device="cuda")]
+    aggs = [("sum", [(1, 0, 1)]), ("sum", [(1, 2, -1)]), ("min", [(1, 0, 1)]), ("max", [(1, 0, 1)])]
+    for keys in ([0], []):
+        got = T.groupby_agg(cols, keys, aggs)
+        want = oracle.groupby_agg_f64([k, x], keys, aggs)
+        for a in range(4):
+            assert npy(got["results"][a]).tolist() == want["results"][a]
+    e = T.groupby_agg(cols, [], aggs + [("avg", [(1, 0, 1)]), ("count", [])], [(0, "gt", 5)])
+    r = [npy(t).tolist() for t in e["results"]]
+    assert r[0] == [0.0] and r[2] == [float("inf")] and r[3] == [float("-inf")] and np.isnan(r[4][0]) and r[5] == [0]
+
+
+def test_groupby_f64_rejects_f64_keys_and_predicates(T):
+    x = torch.randn(100, dtype=torch.float64, device="cuda")
+    k = torch.zeros(100, dtype=torch.int64, device="cuda")
+    with pytest.raises(T.TqpError):
+        T.groupby_agg([x, k], [0], [("count", [])])
+    with pytest.raises(T.TqpError):
+        T.groupby_agg([k, x], [0], [("count", [])], [(1, "lt", 0)])
+    with pytest.raises(T.TqpError):
+        T.filter_compact([x], [(0, "lt", 0)])
 
 
 def test_groupby_merge_partials(T):
