@@ -260,6 +260,12 @@ tqp_status tqp_filter_compact(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols
  * Results: SUM -> int128 (16 bytes, little-endian two's complement, exact);
  * COUNT -> int64 rows of the group (COUNT(*), n_factors ignored);
  * MIN / MAX -> int64; AVG -> double = rn((double)sum / (double)count) (R15/R17).
+ * fp64 aggregates: an aggregate with a TQP_F64 factor
+ * column is evaluated in fp64, prod_f (add_f + sign_f * x_f) left to right, and
+ * SUM / MIN / MAX / AVG return double (8 bytes): SUM in an unspecified order
+ * (|error| <= (m - 1) * 2^-53 * sum|v| for a group of m rows), MIN / MAX exact
+ * (no NaN inputs), AVG = SUM / COUNT; with no row: SUM 0, MIN +inf, MAX -inf.
+ * TQP_F64 columns may not be keys or predicate columns.
  * Groups come out in ascending key order. n_keys == 0 -> exactly one group even
  * if no row passes (SUM 0, COUNT 0, MIN INT64_MAX, MAX INT64_MIN, AVG NaN).
  * Method: each tile of rows is radix-sorted by key in shared memory and reduced
