@@ -226,7 +226,7 @@ tqp_status tqp_smj_join(tqp_ctx* ctx, tqp_col left, int64_t n_left, tqp_col righ
  * a_cols_host / b_cols_host: host arrays of n_cols columns (n_a / n_b rows; b may be
  * NULL with n_b = 0); a_out / b_out: device int64 (n_a / n_b). *bits_host (nullable):
  * total width. More than 63 bits, or n_cols outside 1..8: TQP_ERR_INVALID_ARGUMENT.
- * Synchronises twice. */
+ * Synchronises once. */
 tqp_status tqp_pack_keys(tqp_ctx* ctx, const tqp_col* a_cols_host, int64_t n_a, const tqp_col* b_cols_host,
                          int64_t n_b, int n_cols, int64_t* a_out, int64_t* b_out, int* bits_host);
 

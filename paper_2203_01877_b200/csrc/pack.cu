@@ -51,6 +51,11 @@ __global__ void __launch_bounds__(PKNT) pack_minmax_kernel(PackCols a, int64_t n
     }
 }
 
+__global__ void pack_mm_init_kernel(unsigned long long* mm, int n_cols) {
+    const int i = threadIdx.x;
+    if (i < 2 * n_cols) mm[i] = (i & 1) ? 0ull : ~0ull;
+}
+
 struct PackLayout {
     uint64_t min[TQP_MAX_KEYS];
     int shift[TQP_MAX_KEYS];
@@ -84,15 +89,7 @@ int pack_keys(tqp_ctx* ctx, const tqp_col* a_cols, int64_t na, const tqp_col* b_
     const PackCols A = pack_cols(a_cols, n_cols, na, "pack_keys side a");
     const PackCols B = nb > 0 || b_cols ? pack_cols(b_cols, n_cols, nb, "pack_keys side b") : PackCols{};
     DevBuf<unsigned long long> mm(ctx, 2 * n_cols);
-    {
-        unsigned long long init[2 * TQP_MAX_KEYS];
-        for (int c = 0; c < n_cols; c++) {
-            init[2 * c] = ~0ull;
-            init[2 * c + 1] = 0;
-        }
-        TQP_CUDA(cudaMemcpyAsync(mm.get(), init, 16 * (size_t)n_cols, cudaMemcpyHostToDevice, ctx->stream));
-        TQP_CUDA(cudaStreamSynchronize(ctx->stream));   // `init` is pageable stack memory
-    }
+    launch(ctx, "tqp_pack_minmax", pack_mm_init_kernel, dim3(1), dim3(32), 0, mm.get(), n_cols);
     auto grid = [&](int64_t n) { return (int)std::min<int64_t>(ceil_div(n, PKNT), (int64_t)ctx->num_sms * 8); };
     if (na > 0) launch(ctx, "tqp_pack_minmax", pack_minmax_kernel, dim3(grid(na)), dim3(PKNT), 0, A, na, mm.get());
     if (nb > 0) launch(ctx, "tqp_pack_minmax", pack_minmax_kernel, dim3(grid(nb)), dim3(PKNT), 0, B, nb, mm.get());
