@@ -1094,38 +1094,65 @@ __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
     for (int k = 0; k < a.n_keys; k++) vec = vec && (uintptr_t)a.kcol[k] % 16 == 0;
     const int64_t nb = vec ? a.n / R : 0;
     const int64_t gs = (int64_t)gridDim.x * GNT;
-    for (int64_t g = blockIdx.x * (int64_t)GNT + tid; g < nb; g += gs) {
-        uint32_t b[R];
+    // two row groups (g, g + gs) per step: their loads are in flight together
+    constexpr int U = 2;
+    for (int64_t g0 = blockIdx.x * (int64_t)GNT + tid; g0 < nb; g0 += U * gs) {
+        uint32_t b[U][R];
+        bool ok[U];
 #pragma unroll
-        for (int i = 0; i < R; i++) b[i] = 0;
+        for (int u = 0; u < U; u++) {
+            ok[u] = g0 + u * gs < nb;
+#pragma unroll
+            for (int i = 0; i < R; i++) b[u][i] = 0;
+        }
         for (int k = 0; k < a.n_keys; k++) {
             const int dt = a.kdt[k];
             const uint64_t mn = kmin[k];
             const int s = sh[k];
             if (dt == TQP_U8) {
-                const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g);
-                const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+                uint4 q[U];
 #pragma unroll
-                for (int i = 0; i < R; i++) b[i] |= (uint32_t)(((wv[i >> 2] >> (8 * (i & 3))) & 0xFFu) - (uint32_t)mn) << s;
+                for (int u = 0; u < U; u++)
+                    q[u] = ok[u] ? __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g0 + u * gs) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    const uint32_t wv[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+                    for (int i = 0; i < R; i++)
+                        b[u][i] |= (uint32_t)(((wv[i >> 2] >> (8 * (i & 3))) & 0xFFu) - (uint32_t)mn) << s;
+                }
             } else if (dt == TQP_I32) {
 #pragma unroll
-                for (int j = 0; j < R / 4; j++) {
-                    const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g * 4 + j);
-                    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+                for (int u = 0; u < U; u++) {
+                    if (!ok[u]) continue;
+                    const int64_t g = g0 + u * gs;
 #pragma unroll
-                    for (int i = 0; i < 4; i++) b[4 * j + i] |= ((wv[i] ^ 0x80000000u) - (uint32_t)mn) << s;
+                    for (int j = 0; j < R / 4; j++) {
+                        const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g * 4 + j);
+                        const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                        for (int i = 0; i < 4; i++) b[u][4 * j + i] |= ((wv[i] ^ 0x80000000u) - (uint32_t)mn) << s;
+                    }
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < R / 2; j++) {
-                    const ulonglong2 q = __ldcs(reinterpret_cast<const ulonglong2*>(a.kcol[k]) + g * 8 + j);
-                    b[2 * j] |= (uint32_t)((q.x ^ 0x8000000000000000ull) - mn) << s;
-                    b[2 * j + 1] |= (uint32_t)((q.y ^ 0x8000000000000000ull) - mn) << s;
+                for (int u = 0; u < U; u++) {
+                    if (!ok[u]) continue;
+                    const int64_t g = g0 + u * gs;
+#pragma unroll
+                    for (int j = 0; j < R / 2; j++) {
+                        const ulonglong2 q = __ldcs(reinterpret_cast<const ulonglong2*>(a.kcol[k]) + g * 8 + j);
+                        b[u][2 * j] |= (uint32_t)((q.x ^ 0x8000000000000000ull) - mn) << s;
+                        b[u][2 * j + 1] |= (uint32_t)((q.y ^ 0x8000000000000000ull) - mn) << s;
+                    }
                 }
             }
         }
 #pragma unroll
-        for (int i = 0; i < R; i++) mark(b[i]);
+        for (int u = 0; u < U; u++)
+            if (ok[u])
+#pragma unroll
+                for (int i = 0; i < R; i++) mark(b[u][i]);
     }
     for (int64_t r = nb * R + blockIdx.x * (int64_t)GNT + tid; r < a.n; r += gs) {   // tail / unaligned
         uint32_t b = 0;

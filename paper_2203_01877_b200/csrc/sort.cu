@@ -356,13 +356,11 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
         bulk_g2s(dst, (const KIN*)a.in_keys + t * TILE, TILE * (uint32_t)sizeof(KIN), &s.mbar[st]);
         if (HAS_PERM && !PERM_DIRECT) bulk_g2s(dst + TILE * sizeof(KIN), a.in_perm + t * TILE, TILE * 4u, &s.mbar[st]);
     };
-    uint32_t uses[SST];
+    uint32_t par = 0;   // bit st: phase parity of stage st's next wait (a register, not a local array)
     for (int st = 0; st < SST; st++) {
-        uses[st] = 0;
         const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
         if (t < n_tiles && full(t)) {
             if (tid == 0) issue(t, st);
-            uses[st]++;
         }
     }
     const unsigned lt = lanemask_lt();
@@ -390,7 +388,8 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
 #pragma unroll
                 for (int i = 0; i < IPT; i++) pm[i] = __ldcs(a.in_perm + base + warp * 32 * IPT + i * 32 + lane);
             }
-            mbar_wait(&s.mbar[st], (uses[st] - 1) & 1);
+            mbar_wait(&s.mbar[st], (par >> st) & 1u);
+            par ^= 1u << st;
             const uint8_t* sp = stage_ptr(st);
             const KIN* sk = reinterpret_cast<const KIN*>(sp);
             const uint32_t* spm = reinterpret_cast<const uint32_t*>(sp + TILE * sizeof(KIN));
@@ -422,7 +421,6 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                     fence_proxy_async();
                     issue(t2, st);
                 }
-                uses[st]++;
             }
         }
         // ranking, specialised for full tiles (every item valid: no per-item guards)
