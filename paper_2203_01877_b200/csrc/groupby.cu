@@ -1774,11 +1774,15 @@ __global__ void __launch_bounds__(256) sp_reduce_kernel(SortPathArgs a) {
     // a segment is shared with a neighbour iff it is this range's first (gprev equal)
     // or last (gnext equal) segment
     auto shared_seg = [&](uint32_t gg) { return gg == gprev || gg == gnext; };
+    // (the loops below are unrolled to SPT so g / vv stay in registers)
+    auto seg_end = [&](int i) { return i + 1 == cnt || (i + 1 < SPT && g[i + 1] != g[i]); };
     {   // counts
         int64_t c = 0;
-        for (int i = 0; i < cnt; i++) {
+#pragma unroll
+        for (int i = 0; i < SPT; i++) {
+            if (i >= cnt) break;
             c++;
-            if (i + 1 == cnt || g[i + 1] != g[i]) {
+            if (seg_end(i)) {
                 if (shared_seg(g[i])) atomicAdd((unsigned long long*)&a.gcount[g[i]], (unsigned long long)c);
                 else a.gcount[g[i]] = c;
                 c = 0;
@@ -1821,11 +1825,13 @@ __global__ void __launch_bounds__(256) sp_reduce_kernel(SortPathArgs a) {
                 }
             }
         }
-        for (int i = 0; i < cnt; i++) {
+#pragma unroll
+        for (int i = 0; i < SPT; i++) {
+            if (i >= cnt) break;
             const int64_t v = vv[i];
             if (op == P_SUM) acc += (unsigned __int128)(__int128)v;
             else mm = op == P_MIN ? min(mm, v) : max(mm, v);
-            if (i + 1 == cnt || g[i + 1] != g[i]) {
+            if (seg_end(i)) {
                 const uint32_t gg = g[i];
                 if (op == P_SUM) {
                     if (shared_seg(gg)) atomic_add_i128(&a.glo[j][gg], &a.ghi[j][gg], acc);
