@@ -948,15 +948,16 @@ __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem
             bulk_g2s(stage_ptr(s) + a.uoff[c], (const uint8_t*)a.ucol[c] + t * TR * es, TR * es, &mbar[s]);
         }
     };
-    uint32_t uses[4] = {0, 0, 0, 0};
+    // per stage, as register bit masks (dynamically indexed arrays would live in local
+    // memory): pend = a bulk copy is in flight, wpar = the phase parity of the next wait
+    uint32_t pend = 0, wpar = 0;
     for (int s = 0; s < NS; s++) {
         const int64_t t = blockIdx.x + (int64_t)s * gridDim.x;
         if (t < a.n_tiles && eligible(t)) {
             if (tid == 0) issue(t, s);
-            uses[s]++;
+            pend |= 1u << s;
         }
     }
-    uint32_t done[4] = {0, 0, 0, 0};
     __shared__ int s_abort;
     for (int64_t k = 0;; k++) {
         const int64_t t = blockIdx.x + k * gridDim.x;
@@ -968,13 +969,14 @@ __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem
             if (s_abort) {
                 if (tid == 0)   // bulk copies still landing in this CTA's stages complete first
                     for (int st = 0; st < NS; st++)
-                        if (uses[st] > done[st]) mbar_wait(&mbar[st], (uses[st] - 1) & 1);
+                        if ((pend >> st) & 1u) mbar_wait(&mbar[st], (wpar >> st) & 1u);
                 break;
             }
         }
         if (eligible(t)) {
-            mbar_wait(&mbar[s], (uses[s] - 1) & 1);
-            done[s]++;
+            mbar_wait(&mbar[s], (wpar >> s) & 1u);
+            wpar ^= 1u << s;
+            pend &= ~(1u << s);
         } else {   // tail tile or unaligned columns: plain cooperative loads
             const int64_t row0 = t * TR;
             const int nrows = (int)min((int64_t)TR, a.n - row0);
@@ -1006,7 +1008,7 @@ __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem
                 fence_proxy_async();
                 issue(t2, s);
             }
-            uses[s]++;
+            pend |= 1u << s;
         }
     }
 }
