@@ -93,16 +93,42 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
     const int64_t base = (int64_t)blockIdx.x * H0_TILE;
     uint64_t a = ~0ull, o = 0;
     uint64_t u[H0_IPT];
+    if ((IN == IN_I64 || IN == IN_I32) && base + H0_TILE <= n && ((uintptr_t)keys & 15) == 0) {
+        // full tile: 16-byte loads (which warp counts a key does not matter for the tile)
+        constexpr int PER = IN == IN_I64 ? 2 : 4;   // keys per 16-byte load
+        const uint4* p4 = reinterpret_cast<const uint4*>((const uint8_t*)keys + base * (IN == IN_I64 ? 8 : 4)) + tid;
 #pragma unroll
-    for (int i = 0; i < H0_IPT; i++) {
-        const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
-        u[i] = pos < n ? load_u<IN>(keys, pos, desc) : 0;
-        if (pos < n) { a &= u[i]; o |= u[i]; }
-    }
+        for (int j = 0; j < H0_IPT / PER; j++) {
+            const uint4 v = __ldg(p4 + j * NT);
+            if (IN == IN_I64) {
+                u[2 * j] = ordered_u64((int64_t)(((uint64_t)v.y << 32) | v.x));
+                u[2 * j + 1] = ordered_u64((int64_t)(((uint64_t)v.w << 32) | v.z));
+            } else {
+                u[4 * j] = ordered_u64((int64_t)(int32_t)v.x);
+                u[4 * j + 1] = ordered_u64((int64_t)(int32_t)v.y);
+                u[4 * j + 2] = ordered_u64((int64_t)(int32_t)v.z);
+                u[4 * j + 3] = ordered_u64((int64_t)(int32_t)v.w);
+            }
+        }
 #pragma unroll
-    for (int i = 0; i < H0_IPT; i++) {
-        const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
-        if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
+        for (int i = 0; i < H0_IPT; i++) {
+            if (desc) u[i] = ~u[i];
+            a &= u[i];
+            o |= u[i];
+            atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < H0_IPT; i++) {
+            const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
+            u[i] = pos < n ? load_u<IN>(keys, pos, desc) : 0;
+            if (pos < n) { a &= u[i]; o |= u[i]; }
+        }
+#pragma unroll
+        for (int i = 0; i < H0_IPT; i++) {
+            const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
+            if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
+        }
     }
     for (int sft = 16; sft > 0; sft >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, sft);
@@ -156,15 +182,28 @@ __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int6
     __syncwarp();
     const int64_t base = (int64_t)blockIdx.x * TILE;
     KT k[IPT];
+    if (IN == IN_INTERNAL && sizeof(KT) == 4 && IPT % 4 == 0 && base + TILE <= n) {
+        // full tile of internal u32 keys: 16-byte loads (which warp counts a key does
+        // not matter for the tile's histogram)
+        const uint4* p4 = reinterpret_cast<const uint4*>((const uint32_t*)in_keys + base) + tid;
 #pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        k[i] = pos < n ? load_key<KT, IN>(in_keys, pos, desc) : (KT)0;
-    }
+        for (int j = 0; j < IPT / 4; j++) {
+            const uint4 v = __ldg(p4 + j * NT);
+            k[4 * j] = (KT)v.x; k[4 * j + 1] = (KT)v.y; k[4 * j + 2] = (KT)v.z; k[4 * j + 3] = (KT)v.w;
+        }
 #pragma unroll
-    for (int i = 0; i < IPT; i++) {
-        const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
-        if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
+        for (int i = 0; i < IPT; i++) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
+    } else {
+#pragma unroll
+        for (int i = 0; i < IPT; i++) {
+            const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+            k[i] = pos < n ? load_key<KT, IN>(in_keys, pos, desc) : (KT)0;
+        }
+#pragma unroll
+        for (int i = 0; i < IPT; i++) {
+            const int64_t pos = base + warp * 32 * IPT + i * 32 + lane;
+            if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)(k[i] >> shift) & (BINS - 1u))], 1u);
+        }
     }
     __syncthreads();
     for (int d = tid; d < BINS; d += NT) {
