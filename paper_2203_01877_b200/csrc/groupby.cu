@@ -2008,12 +2008,27 @@ void sort_path(tqp_ctx* ctx, tqp_groupby_plan* PL, const tqp_col* cols, int n_co
 }
 
 // Key-column ranges on the device (no host sync): min in kr[0..7], max in kr[8..15].
+__global__ void u8_ranges_kernel(unsigned long long* kr, int n_keys) {
+    if (threadIdx.x < n_keys) {
+        kr[threadIdx.x] = 0;
+        kr[8 + threadIdx.x] = 255;
+    }
+}
+
 void key_ranges(tqp_ctx* ctx, const void* const* kcol, const int* kdt, int n_keys, int64_t n,
                 DevBuf<unsigned long long>& kr) {
     kr.alloc(ctx, 16);
     TQP_CUDA(cudaMemsetAsync(kr.get(), 0xFF, 8 * 8, ctx->stream));
     TQP_CUDA(cudaMemsetAsync(kr.get() + 8, 0, 8 * 8, ctx->stream));
     if (n_keys == 0 || n == 0) return;
+    // at most two u8 key columns: their whole domains pack into 16 bits (the dense path's
+    // presence bitmap), so the layout takes [0, 255] per column without a pass over the keys
+    bool u8only = n_keys <= 2;
+    for (int k = 0; k < n_keys; k++) u8only = u8only && kdt[k] == TQP_U8;
+    if (u8only) {
+        launch(ctx, "tqp_groupby_keyrange", u8_ranges_kernel, dim3(1), dim3(32), 0, kr.get(), n_keys);
+        return;
+    }
     KRArgs a{};
     a.n_keys = n_keys;
     a.n = n;
