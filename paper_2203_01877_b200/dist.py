@@ -200,6 +200,48 @@ def _splitters(sorted_keys_list, world, group=None, per_rank=64):
     return allv[torch.tensor(pos, dtype=torch.int64, device=dev)]
 
 
+def _output_splitters(lk, rk, world, group=None, per_rank=256):
+    """world - 1 splitters balancing rows + output pairs per rank (the SMJ's work). Keys
+    frequent in a sample are candidates; their exact global counts L_k, R_k are summed
+    over the ranks, and each candidate carries its L_k * R_k pairs as weight beside the
+    rows the samples stand for. Splitters sit at the weight quantiles, so a key heavier
+    than a rank's share recurs as consecutive splitters and spans several ranks."""
+    dev = lk.device
+    samples = []
+    for k in (lk, rk):
+        if k.numel():
+            sk = torch.sort(k)[0]
+            idx = torch.linspace(0, k.numel() - 1, per_rank, device=dev).round().to(torch.int64)
+            samples.append(sk[idx])
+    loc = torch.cat(samples) if samples else torch.empty(0, dtype=torch.int64, device=dev)
+    allv = torch.sort(_gather_rows(loc.reshape(-1, 1), group).reshape(-1))[0]
+    if allv.numel() == 0:
+        return torch.empty(0, dtype=torch.int64, device=dev)
+    uk, cnt = torch.unique_consecutive(allv, return_counts=True)
+    cand = uk[cnt >= 2]                      # identical on every rank
+    nrows = torch.tensor([lk.numel() + rk.numel()], dtype=torch.int64, device=dev)
+    dist.all_reduce(nrows, group=group)
+    def count_in(k):   # occurrences of each candidate key in k (candidates are sorted)
+        if cand.numel() == 0 or k.numel() == 0:
+            return torch.zeros(cand.numel(), dtype=torch.int64, device=dev)
+        pos = torch.searchsorted(cand, k)
+        hit = cand[pos.clamp(max=cand.numel() - 1)] == k
+        return torch.bincount(pos[hit], minlength=cand.numel()).to(torch.int64)
+    counts = torch.stack([count_in(lk), count_in(rk)])
+    dist.all_reduce(counts, group=group)
+    pairs = (counts[0] * counts[1]).to(torch.float64)
+    # weighted items: every sample stands for nrows / samples rows; candidates add their pairs
+    w_sample = float(nrows.item()) / allv.numel()
+    keys = torch.cat([allv, cand])
+    wts = torch.cat([torch.full((allv.numel(),), w_sample, dtype=torch.float64, device=dev), pairs])
+    order = torch.argsort(keys, stable=True)
+    keys, cum = keys[order], torch.cumsum(wts[order], 0)
+    total = float(cum[-1].item())
+    targets = torch.tensor([total * i / world for i in range(1, world)], dtype=torch.float64, device=dev)
+    pos = torch.searchsorted(cum, targets).clamp(max=keys.numel() - 1)
+    return keys[pos]
+
+
 def _range_dest(keys, splitters):
     """Rank owning each key: the number of splitters <= key (equal keys share a rank)."""
     return torch.searchsorted(splitters, keys.to(torch.int64), right=True)
@@ -222,19 +264,45 @@ def sort_samplesort(ctx, keys, global_rows, group=None, sort_fn=None):
 
 
 def smj_join_copartition(ctx, left_keys, left_rows, right_keys, right_rows, group=None, join_fn=None,
-                         sort_fn=None):
+                         sort_fn=None, n_left_total=None):
     """Distributed generic sort-merge join (Alg. 1) by key-range co-partitioning with
-    sampled splitters. Returns this rank's (global left row, global right row) pairs in
-    (key, left row, right row) order; the concatenation over ranks in rank order is the
-    single-GPU result. A key's pairs are produced by one rank (Zipf-heavy keys are not
-    split across ranks; output-range splitting of heavy keys is not implemented)."""
+    sampled splitters, with output-range splitting of heavy keys.
+    Returns this rank's (global left row, global right row) pairs in (key, left row,
+    right row) order; the concatenation over ranks in rank order is the single-GPU result.
+
+    A key equal to one or more splitters is heavy: it spans ranks lo..hi (lo = splitters
+    below it, hi = splitters up to it). Its left rows are split across those ranks by
+    global left row (row * (hi - lo + 1) // n_left_total: monotone, so each rank gets a
+    contiguous range of the key's left rows in order) and its right rows are replicated to
+    all of them, so each rank produces the key's pairs for its left rows and the pairs
+    still come out in (key, l, r) order across ranks. Light keys go to one rank."""
     join_fn = join_fn or ctx.smj_join
     if sort_fn is None and ctx is not None:
         sort_fn = lambda d: ctx.sort(d)[1]   # noqa: E731
     world = dist.get_world_size(group)
     lk, rk = left_keys.to(torch.int64), right_keys.to(torch.int64)
-    spl = _splitters([lk, rk], world, group, per_rank=256)
-    rl_key, rl_row = _exchange([lk, left_rows.to(torch.int64)], _range_dest(lk, spl), world, group, sort_fn)
-    rr_key, rr_row = _exchange([rk, right_rows.to(torch.int64)], _range_dest(rk, spl), world, group, sort_fn)
+    lrows, rrows = left_rows.to(torch.int64), right_rows.to(torch.int64)
+    if n_left_total is None:   # rows are global offsets into the left column: its length
+        t = torch.tensor([lrows.max().item() + 1 if lrows.numel() else 0], dtype=torch.int64, device=lk.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        n_left_total = max(int(t.item()), 1)
+    spl = _output_splitters(lk, rk, world, group)
+    # left: heavy keys' rows split across their ranks by global row, light rows to one rank
+    llo = torch.searchsorted(spl, lk, right=False)
+    lhi = torch.searchsorted(spl, lk, right=True)
+    dest_l = torch.where(lhi > llo, llo + (lrows * (lhi - llo + 1)) // n_left_total, lhi)
+    rl_key, rl_row = _exchange([lk, lrows], dest_l, world, group, sort_fn)
+    # right: heavy keys' rows replicated to every rank of the key's span
+    rlo = torch.searchsorted(spl, rk, right=False)
+    rhi = torch.searchsorted(spl, rk, right=True)
+    reps = rhi - rlo + 1
+    if bool((reps > 1).any()):
+        idx = torch.repeat_interleave(torch.arange(rk.numel(), device=rk.device), reps)
+        first = torch.repeat_interleave(torch.cumsum(reps, 0) - reps, reps)
+        dest_r = rlo[idx] + (torch.arange(idx.numel(), device=rk.device) - first)
+        rk_x, rrows_x = rk[idx], rrows[idx]
+    else:
+        dest_r, rk_x, rrows_x = rhi, rk, rrows
+    rr_key, rr_row = _exchange([rk_x, rrows_x], dest_r, world, group, sort_fn)
     lo, ro = join_fn(rl_key, rr_key)
     return rl_row[lo], rr_row[ro]

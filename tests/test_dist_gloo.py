@@ -217,6 +217,14 @@ def test_world2_copartition_join_and_cost_model():
         assert s == min(cost, key=cost.get)
 
 
+def _skewed(n, seed):
+    """Keys in [0, 400) with key 7 on about a quarter of the rows (a Zipf-like heavy key)."""
+    g = torch.Generator().manual_seed(seed)
+    k = torch.randint(0, 400, (n,), generator=g, dtype=torch.int64)
+    k[torch.rand(n, generator=g) < 0.25] = 7
+    return k
+
+
 def _worker_sort_smj(rank, world, port, out_q):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -244,7 +252,13 @@ def _worker_sort_smj(rank, world, port, out_q):
         sl = left[rank * n:(rank + 1) * n]
         sr2 = right[rank * n:(rank + 1) * n]
         gl, gr = D.smj_join_copartition(None, sl, rows, sr2, rows, join_fn=join_fn, sort_fn=None)
-        out_q.put((rank, sk.numpy(), sr.numpy(), gl.numpy(), gr.numpy()))
+        # skewed: one key holds ~25 % of each side (spans both ranks' key ranges)
+        m = 3_000
+        hl, hr = _skewed(world * m, 11), _skewed(world * m, 12)
+        hrows = torch.arange(rank * m, (rank + 1) * m, dtype=torch.int64)
+        hl_, hr_ = D.smj_join_copartition(None, hl[rank * m:(rank + 1) * m], hrows, hr[rank * m:(rank + 1) * m],
+                                          hrows, join_fn=join_fn, sort_fn=None)
+        out_q.put((rank, sk.numpy(), sr.numpy(), gl.numpy(), gr.numpy(), hl_.numpy(), hr_.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -273,6 +287,14 @@ def test_world2_samplesort_and_smj():
     assert np.array_equal(np.concatenate([o[2] for o in outs]), want_p)
     left = zipf_keys(world * n, 3_000, seed=7).numpy()
     right = uniform_keys(world * n, 3_000, seed=8).numpy()
+    # skewed case: exact single-process order, and the heavy key's pairs split over the ranks
+    m = 3_000
+    hl, hr = _skewed(world * m, 11).numpy(), _skewed(world * m, 12).numpy()
+    wl, wr = oracle.smj_join(hl, hr)
+    assert np.array_equal(np.concatenate([o[5] for o in outs]), wl)
+    assert np.array_equal(np.concatenate([o[6] for o in outs]), wr)
+    heavy = [int((hl[o[5]] == 7).sum()) for o in outs]
+    assert min(heavy) > 0.25 * sum(heavy), heavy
     olo, oro = oracle.smj_join(left, right)
     assert np.array_equal(np.concatenate([o[3] for o in outs]), olo)
     assert np.array_equal(np.concatenate([o[4] for o in outs]), oro)
