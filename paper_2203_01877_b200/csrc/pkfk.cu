@@ -22,6 +22,8 @@
 //      look-back left a tile's warps idle at the barrier (measured).
 // Duplicate build keys (adjacent equal sorted keys) -> TQP_ERR_DUPLICATE_BUILD_KEY.
 #include "internal.h"
+#include <cmath>
+#include <cstdlib>
 
 namespace tqp {
 
@@ -95,6 +97,7 @@ struct ProbeArgs {
     int64_t* left64;          // outer: per probe row, the build row or -1
     uint8_t* mask;            // semi: per probe row, 1 = the key is on the build side
     uint32_t* tcnt;           // per tile: rows selected (join: matches; semi: match != anti)
+    uint64_t blo, bhi;        // multi-pass probe: the bucket range this pass resolves
 };
 
 // L2 evict-last policy on the slot-table loads: measured no change at SF10
@@ -113,6 +116,46 @@ __device__ __forceinline__ uint4 ldg_hint(const uint4* ptr, uint64_t pol) {
     asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(ptr), "l"(pol));
     return v;
+}
+
+// Packed route: the bucket's records [T[b], T[b+1]) from the aligned 32-byte sector(s)
+// holding them (a few records), else a lower_bound over the residuals.
+__device__ __forceinline__ bool lookup_packed(const ProbeArgs& a, uint32_t rel_low, uint64_t b, uint32_t& left) {
+    uint32_t lo = __ldg(a.T + b), hi = __ldg(a.T + b + 1);
+    const uint32_t low = rel_low & a.lowmask;
+    const uint32_t target = low << a.pbits;
+    const uint32_t end = hi;
+    const uint32_t s0 = lo & ~7u;   // the bucket's records from the aligned 32-byte sector(s) holding it
+    if (hi <= s0 + 16u) {
+        const uint4* p4 = reinterpret_cast<const uint4*>(a.rec + s0);
+        const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1);
+        uint4 q2 = make_uint4(0, 0, 0, 0), q3 = q2;
+        if (hi > s0 + 8u) { q2 = __ldg(p4 + 2); q3 = __ldg(p4 + 3); }   // second sector only when needed
+        const uint32_t r16[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
+                                  q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
+        bool hit = false;
+#pragma unroll
+        for (int j = 0; j < 16; j++) {   // residuals are distinct: at most one match
+            const uint32_t pos = s0 + (uint32_t)j;
+            if (pos >= lo && pos < end && (r16[j] >> a.pbits) == low) {
+                left = r16[j] & ((1u << a.pbits) - 1u);
+                hit = true;
+            }
+        }
+        return hit;
+    }
+    while (lo < hi) {   // long bucket: lower_bound of the residual
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(a.rec + mid) < target) lo = mid + 1; else hi = mid;
+    }
+    if (lo < end) {
+        const uint32_t r = __ldg(a.rec + lo);
+        if ((r >> a.pbits) == low) {
+            left = r & ((1u << a.pbits) - 1u);
+            return true;
+        }
+    }
+    return false;
 }
 
 template <typename KT, int PDT, bool PACKED>
@@ -157,43 +200,8 @@ __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint3
             return hit;
         }
     }
+    if (PACKED) return lookup_packed(a, (uint32_t)rel, b, left);
     uint32_t lo = __ldg(a.T + b), hi = __ldg(a.T + b + 1);
-    if (PACKED) {
-        const uint32_t low = (uint32_t)rel & a.lowmask;
-        const uint32_t target = low << a.pbits;
-        const uint32_t end = hi;
-        const uint32_t s0 = lo & ~7u;   // the bucket's records from the aligned 32-byte sector(s) holding it
-        if (hi <= s0 + 16u) {
-            const uint4* p4 = reinterpret_cast<const uint4*>(a.rec + s0);
-            const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1);
-            uint4 q2 = make_uint4(0, 0, 0, 0), q3 = q2;
-            if (hi > s0 + 8u) { q2 = __ldg(p4 + 2); q3 = __ldg(p4 + 3); }   // second sector only when needed
-            const uint32_t r16[16] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w,
-                                      q2.x, q2.y, q2.z, q2.w, q3.x, q3.y, q3.z, q3.w};
-            bool hit = false;
-#pragma unroll
-            for (int j = 0; j < 16; j++) {   // residuals are distinct: at most one match
-                const uint32_t pos = s0 + (uint32_t)j;
-                if (pos >= lo && pos < end && (r16[j] >> a.pbits) == low) {
-                    left = r16[j] & ((1u << a.pbits) - 1u);
-                    hit = true;
-                }
-            }
-            return hit;
-        }
-        while (lo < hi) {   // long bucket: lower_bound of the residual
-            uint32_t mid = (lo + hi) >> 1;
-            if (__ldg(a.rec + mid) < target) lo = mid + 1; else hi = mid;
-        }
-        if (lo < end) {
-            const uint32_t r = __ldg(a.rec + lo);
-            if ((r >> a.pbits) == low) {
-                left = r & ((1u << a.pbits) - 1u);
-                return true;
-            }
-        }
-        return false;
-    }
     const KT* keys = (const KT*)a.bkeys;
     const uint32_t end = hi;
     while (lo < hi) {   // lower_bound inside the bucket (a few elements)
@@ -243,6 +251,120 @@ __global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
             cnt += m[i] != (a.anti != 0);
         }
     }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < PNW; w++) t += s_w[w];
+        a.tcnt[blockIdx.x] = t;
+    }
+}
+
+// Multi-pass probe (join mode, packed records) for build sides much larger than L2
+// (SF100: 150M orders -> 868 MB of bracket table + records). A single pass makes every
+// probe row a random HBM access into that structure (measured: 21.8 ms for 600M probes,
+// 3.7 TB/s of DRAM reads at ~131 B per probe). Instead the bucket range is split into P
+// slices of about one L2's worth of T + records; pass p resolves only the rows whose
+// bucket lies in slice p, so its lookups hit L2. The first pass turns each probe key
+// into a u32 code (0x80000000 | (key - base); keys outside the build domain resolve to
+// NOMATCH at once) stored in `lft`; later passes stream the codes (4 B per row) and
+// overwrite resolved rows in place with the build row (top bit clear) or NOMATCH; the
+// last pass also counts each tile's matches for the compaction. Needs vbits <= 30.
+// Thread t owns rows {t*4 .. t*4+3} and {1024 + t*4 .. +3} of its 2,048-row tile (two
+// 16-byte code vectors); the slice test is one subtract + compare per row on the code.
+__device__ __forceinline__ int64_t pass_row(int64_t base, int tid, int i) {
+    return base + (int64_t)(i >> 2) * (PTILE / 2) + (int64_t)tid * 4 + (i & 3);
+}
+
+template <typename KT, int PDT, bool FIRST, bool LAST>
+__global__ void __launch_bounds__(PNT) probe_pass_kernel(ProbeArgs a) {
+    static_assert(PIPT == 8 && PTILE == 2 * 4 * PNT, "two 4-row vectors per thread");
+    __shared__ uint32_t s_w[PNW];
+    __shared__ uint32_t s_c[PTILE];
+    __shared__ uint16_t s_q[PTILE];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * PTILE;
+    const bool full = base + PTILE <= a.n_probe;
+    uint32_t c[PIPT];
+    if (FIRST) {
+#pragma unroll
+        for (int i = 0; i < PIPT; i++) {
+            const int64_t row = pass_row(base, tid, i);
+            c[i] = NOMATCH;
+            if (row >= a.n_probe) continue;
+            int64_t v;
+            if (PDT == TQP_I64) v = (int64_t)__ldcs((const long long*)a.probe + row);
+            else if (PDT == TQP_I32) v = (int64_t)__ldcs((const int*)a.probe + row);
+            else v = (int64_t)__ldcs((const unsigned char*)a.probe + row);
+            const uint64_t u = ordered_u64(v);
+            bool ok = sizeof(KT) == 4 ? (u & 0xFFFFFFFF00000000ull) == a.hi_bits : true;
+            const KT k = (KT)u;
+            const KT rel = (KT)(k - (KT)a.base);
+            ok = ok && k >= (KT)a.base && ((uint64_t)rel >> a.vbits) == 0;
+            c[i] = ok ? (0x80000000u | (uint32_t)rel) : NOMATCH;
+        }
+    } else if (full) {
+        const uint4 v0 = __ldcs(reinterpret_cast<const uint4*>(a.lft + pass_row(base, tid, 0)));
+        const uint4 v1 = __ldcs(reinterpret_cast<const uint4*>(a.lft + pass_row(base, tid, 4)));
+        c[0] = v0.x; c[1] = v0.y; c[2] = v0.z; c[3] = v0.w;
+        c[4] = v1.x; c[5] = v1.y; c[6] = v1.z; c[7] = v1.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < PIPT; i++) {
+            const int64_t row = pass_row(base, tid, i);
+            c[i] = row < a.n_probe ? __ldcs(a.lft + row) : NOMATCH;
+        }
+    }
+    // codes of this slice: [0x80000000 + (blo << shift), 0x80000000 + (bhi << shift));
+    // resolved rows (top bit clear) and NOMATCH fall outside
+    const uint32_t clo = 0x80000000u + ((uint32_t)a.blo << a.shift);
+    const uint32_t cspan = (uint32_t)(a.bhi - a.blo) << a.shift;
+    uint32_t m = 0;
+#pragma unroll
+    for (int i = 0; i < PIPT; i++) m |= (uint32_t)(c[i] - clo < cspan) << i;
+    if (__any_sync(0xffffffffu, m)) {
+        // rows in the slice join a per-warp queue (local row indices) and the warp's
+        // lanes look them up densely: a few independent L2 lookups per lane instead of
+        // PIPT sparse rounds across the whole warp
+        uint32_t qn = 0;
+#pragma unroll
+        for (int i = 0; i < PIPT; i++) {
+            const bool in = (m >> i) & 1u;
+            const uint32_t li = (uint32_t)((i >> 2) * (PTILE / 2) + tid * 4 + (i & 3));
+            if (in) s_c[li] = c[i];
+            const uint32_t bal = __ballot_sync(0xffffffffu, in);
+            if (in) s_q[warp * 32 * PIPT + qn + __popc(bal & ((1u << lane) - 1u))] = (uint16_t)li;
+            qn += __popc(bal);
+        }
+        __syncwarp();
+        for (uint32_t j = lane; j < qn; j += 32) {
+            const uint32_t li = s_q[warp * 32 * PIPT + j];
+            const uint32_t rel = s_c[li] & 0x7FFFFFFFu;
+            uint32_t l = NOMATCH;
+            s_c[li] = lookup_packed(a, rel, (uint64_t)(rel >> a.shift), l) ? l : NOMATCH;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < PIPT; i++)
+            if ((m >> i) & 1u) c[i] = s_c[(i >> 2) * (PTILE / 2) + tid * 4 + (i & 3)];
+    }
+    if (full) {
+        if (FIRST || (m & 0xFu))
+            __stcs(reinterpret_cast<uint4*>(a.lft + pass_row(base, tid, 0)), make_uint4(c[0], c[1], c[2], c[3]));
+        if (FIRST || (m >> 4))
+            __stcs(reinterpret_cast<uint4*>(a.lft + pass_row(base, tid, 4)), make_uint4(c[4], c[5], c[6], c[7]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < PIPT; i++) {
+            const int64_t row = pass_row(base, tid, i);
+            if (row < a.n_probe && (FIRST || ((m >> i) & 1u))) __stcs(a.lft + row, c[i]);
+        }
+    }
+    if (!LAST) return;
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < PIPT; i++) cnt += c[i] != NOMATCH;   // rows past the end hold NOMATCH
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
     if (lane == 0) s_w[warp] = cnt;
     __syncthreads();
@@ -486,7 +608,37 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
                 default: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_U8, PK>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
             }
         };
-        if (B.so.k32) {
+        // slices of about one L2 of T + records (TQP_PROBE_SLICE_MB overrides, for A/B)
+        static const double slice_mb = [] {
+            const char* e = std::getenv("TQP_PROBE_SLICE_MB");
+            return e ? std::atof(e) : 128.0;
+        }();
+        int passes = 1;
+        if (mode == 0 && B.packed && !B.slots.get() && B.vbits <= 30 && np >= nb && slice_mb > 0)
+            passes = (int)std::min<double>(64.0, std::ceil((double)B.tr_bytes / (slice_mb * 1048576.0)));
+        if (passes > 1) {
+            const uint64_t nbk = uint64_t(1) << (B.vbits - B.shift);
+            auto gp = [&](auto kt, auto first, auto last) {
+                using KT = decltype(kt);
+                constexpr bool F = decltype(first)::value, L = decltype(last)::value;
+                switch (pk.dtype) {
+                    case TQP_I64: launch(ctx, "tqp_pkfk_probe", probe_pass_kernel<KT, TQP_I64, F, L>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                    case TQP_I32: launch(ctx, "tqp_pkfk_probe", probe_pass_kernel<KT, TQP_I32, F, L>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                    default: launch(ctx, "tqp_pkfk_probe", probe_pass_kernel<KT, TQP_U8, F, L>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                }
+            };
+            for (int p = 0; p < passes; p++) {
+                a.blo = nbk * (uint64_t)p / (uint64_t)passes;
+                a.bhi = p + 1 == passes ? nbk : nbk * (uint64_t)(p + 1) / (uint64_t)passes;
+                const bool first = p == 0, last = p + 1 == passes;
+                auto run = [&](auto kt) {
+                    if (first) gp(kt, std::true_type{}, std::false_type{});
+                    else if (last) gp(kt, std::false_type{}, std::true_type{});
+                    else gp(kt, std::false_type{}, std::false_type{});
+                };
+                if (B.so.k32) run(uint32_t{}); else run(uint64_t{});
+            }
+        } else if (B.so.k32) {
             if (B.packed) go(uint32_t{}, std::true_type{}); else go(uint32_t{}, std::false_type{});
         } else {
             if (B.packed) go(uint64_t{}, std::true_type{}); else go(uint64_t{}, std::false_type{});

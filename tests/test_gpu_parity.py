@@ -8,6 +8,7 @@ full-size cases (BASELINE configs[2]) use closed forms that hold at any size.
 """
 
 import math
+import os
 
 import numpy as np
 import pytest
@@ -109,6 +110,26 @@ def test_pkfk_random_parity(T, nb, np_, span, bd, pd):
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
 
 
+@pytest.mark.parametrize("bits", [29, 30])
+@pytest.mark.parametrize("clustered", [False, True])
+def test_pkfk_fine_bucket_slot_table(T, bits, clustered):
+    """Wide keys over few build rows (the SF100 shape scaled down: residual + row bits would
+    need 32): the build side takes finer buckets so the slot table applies; runs of 20
+    consecutive keys overflow their bucket's 8 slots (pointer route)."""
+    rng = np.random.default_rng(bits + 10 * clustered)
+    if clustered:
+        starts = np.unique(rng.integers(0, 2**bits - 64, 5000) // 64 * 64)
+        build = (starts[:, None] + np.arange(20)).ravel()
+    else:
+        build = np.unique(rng.integers(0, 2**bits, 110_000))
+    build = rng.permutation(build).astype(np.int64)
+    probe = np.concatenate([rng.choice(build, 150_000), rng.integers(-5, 2**bits + 5, 150_001)])
+    probe = rng.permutation(probe).astype(np.int64)
+    lo, ro = T.pkfk_join(cu(build), cu(probe))
+    olo, oro = oracle.pkfk_join(build, probe)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
 @pytest.mark.parametrize("nb,np_,span", [(0, 0, 10), (1, 5, 3), (2047, 2049, 4096), (300_000, 1_000_003, 10**6)])
 def test_pkfk_join_i32_outputs(T, nb, np_, span):
     """tqp_pkfk_join_i32: the oracle's pairs, written as int32."""
@@ -183,6 +204,18 @@ def test_pkfk_tpch_filtered_build(T):
     lo, ro = T.pkfk_join(bk, li["l_orderkey"])
     olo, oro = oracle.pkfk_join(npy(bk), npy(li["l_orderkey"]))
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+@pytest.mark.parametrize("slice_mb", ["0.004", "0.05"])
+def test_pkfk_multipass_probe(T, slice_mb):
+    """The multi-pass probe (build sides much larger than L2, e.g. SF100) run at small sizes
+    by shrinking its slice: several passes, ragged tiles, i32 keys, a sparse key domain."""
+    import subprocess
+    import sys
+    env = dict(os.environ, TQP_PROBE_SLICE_MB=slice_mb)
+    child = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_pkfk_multipass_child.py")
+    r = subprocess.run([sys.executable, child], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.startswith("ok"), r.stdout + r.stderr
 
 
 def test_pkfk_sf10_full_size_closed_form(T):
