@@ -23,8 +23,9 @@ struct SortOut {
     DevBuf<uint32_t> perm32;           // internal permutation
 };
 
-// andor (nullable): the AND / OR of the sort-domain keys, already read back by the caller
-// from sort_andor (so several sorts share one host sync); null = computed here.
+// andor (nullable, 3 words): the AND / OR of the sort-domain keys and an "out of order"
+// flag (0 = already sorted), read back by the caller from sort_andor (so several sorts
+// share one host sync); null = computed here.
 // th0 (nullable, sort_hist0_words(n) u32): the first-pass histogram sort_andor fused in.
 void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& out,
                 const uint64_t* andor = nullptr, uint32_t* th0 = nullptr);

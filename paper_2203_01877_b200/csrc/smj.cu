@@ -701,14 +701,14 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         SortOut sl, sr;
         sl.want_internal = sr.want_internal = true;
         {   // both digit plans with one host sync
-            DevBuf<unsigned long long> ao(ctx, 4);
+            DevBuf<unsigned long long> ao(ctx, 6);
             DevBuf<uint32_t> hl(ctx, sort_hist0_words(nl)), hr(ctx, sort_hist0_words(nr));
             sort_andor(ctx, left.data, left.dtype, nl, false, ao.get(), hl.get());
-            sort_andor(ctx, right.data, right.dtype, nr, false, ao.get() + 2, hr.get());
-            uint64_t h[4];
-            read_back(ctx, h, ao.get(), 32);
+            sort_andor(ctx, right.data, right.dtype, nr, false, ao.get() + 3, hr.get());
+            uint64_t h[6];
+            read_back(ctx, h, ao.get(), 48);
             radix_sort(ctx, left.data, left.dtype, nl, false, sl, h, hl.get());
-            radix_sort(ctx, right.data, right.dtype, nr, false, sr, h + 2, hr.get());
+            radix_sort(ctx, right.data, right.dtype, nr, false, sr, h + 3, hr.get());
         }
         P->perm_l = std::move(sl.perm32);
         P->perm_r = std::move(sr.perm32);

@@ -22,6 +22,7 @@
 //     60M-key pass on B200: its inclusive-prefix frontier serialises the tiles;
 //     see DESIGN.md.)
 #include "internal.h"
+#include <cstdlib>
 
 namespace tqp {
 
@@ -45,11 +46,14 @@ template <int IN>
 __global__ void __launch_bounds__(NT) andor_kernel(const void* keys, int64_t n, bool desc,
                                                    unsigned long long* out) {
     uint64_t a = ~0ull, o = 0;
+    bool uns = false;   // some adjacent pair out of order (else the stable order is the identity)
     for (int64_t i = blockIdx.x * (int64_t)NT + threadIdx.x; i < n; i += (int64_t)gridDim.x * NT) {
         uint64_t u = load_u<IN>(keys, i, desc);
         a &= u;
         o |= u;
+        if (i + 1 < n) uns |= u > load_u<IN>(keys, i + 1, desc);
     }
+    if (__any_sync(0xffffffffu, uns) && (threadIdx.x & 31) == 0) atomicOr(&out[2], 1ull);
     for (int s = 16; s > 0; s >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, s);
         o |= __shfl_xor_sync(0xffffffffu, o, s);
@@ -110,13 +114,21 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
                 u[4 * j + 3] = ordered_u64((int64_t)(int32_t)v.w);
             }
         }
+        bool uns = false;
 #pragma unroll
         for (int i = 0; i < H0_IPT; i++) {
             if (desc) u[i] = ~u[i];
             a &= u[i];
             o |= u[i];
             atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
+            if (i % PER != PER - 1) {
+                uns |= u[i] > u[i + 1];
+            } else {   // the key after this vector (next thread's first): an L1 hit
+                const int64_t nx = base + ((int64_t)(i / PER) * NT + tid + 1) * PER;
+                if (nx < n) uns |= u[i] > load_u<IN>(keys, nx, desc);
+            }
         }
+        if (__any_sync(0xffffffffu, uns) && lane == 0) atomicOr(&out[2], 1ull);
     } else {
 #pragma unroll
         for (int i = 0; i < H0_IPT; i++) {
@@ -124,11 +136,14 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
             u[i] = pos < n ? load_u<IN>(keys, pos, desc) : 0;
             if (pos < n) { a &= u[i]; o |= u[i]; }
         }
+        bool uns = false;
 #pragma unroll
         for (int i = 0; i < H0_IPT; i++) {
             const int64_t pos = base + warp * 32 * H0_IPT + i * 32 + lane;
             if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
+            if (pos + 1 < n) uns |= u[i] > load_u<IN>(keys, pos + 1, desc);
         }
+        if (__any_sync(0xffffffffu, uns) && lane == 0) atomicOr(&out[2], 1ull);
     }
     for (int sft = 16; sft > 0; sft >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, sft);
@@ -727,10 +742,19 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
     if (need_perm_final) o.perm32 = std::move(pb[fb]);
 }
 
+// TQP_SORT_NO_PRESORTED=1 disables the presorted shortcut (A/B and tests of the radix path).
+static bool force_radix() {
+    static const bool f = [] {
+        const char* e = std::getenv("TQP_SORT_NO_PRESORTED");
+        return e && std::atoi(e) != 0;
+    }();
+    return f;
+}
+
 void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao,
                 uint32_t* th0) {
     TQP_CUDA(cudaMemsetAsync(ao, 0xFF, 8, ctx->stream));
-    TQP_CUDA(cudaMemsetAsync(ao + 1, 0, 8, ctx->stream));
+    TQP_CUDA(cudaMemsetAsync(ao + 1, 0, 16, ctx->stream));
     if (n <= 0) return;
     const int mode = in_mode(dtype);
     const int grid = (int)std::min<int64_t>(ceil_div(n, NT * 8), (int64_t)ctx->num_sms * 4);
@@ -753,19 +777,20 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     if (n < 0 || n >= (int64_t(1) << 30)) fail(TQP_ERR_INVALID_ARGUMENT, "sort: n must be in [0, 2^30)");
     if (n == 0) return;
     const int mode = in_mode(dtype);
-    uint64_t h[2];
+    uint64_t h[3];
     DevBuf<uint32_t> th0_own;
     if (andor) {   // the caller launched sort_andor and read the plan back (one sync for several sorts)
         h[0] = andor[0];
         h[1] = andor[1];
+        h[2] = andor[2];
     } else {
-        DevBuf<unsigned long long> ao(ctx, 2);
+        DevBuf<unsigned long long> ao(ctx, 3);
         if (n >= (1 << 16) && mode != IN_INTERNAL) {   // large sorts: speculative pass-0 histogram
             th0_own.alloc(ctx, sort_hist0_words(n));
             th0 = th0_own.get();
         }
         sort_andor(ctx, keys, dtype, n, desc, ao.get(), th0);
-        read_back(ctx, h, ao.get(), 16);
+        read_back(ctx, h, ao.get(), 24);
     }
     o.and_bits = h[0];
     o.or_bits = h[1];
@@ -786,6 +811,10 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
         }
     }
     o.passes = P;
+    // Already in (key, row) order -- every adjacent pair non-decreasing in the sort domain,
+    // as TPC-H's orders table is by o_orderkey: the stable order is the identity, and one
+    // streaming pass writes the outputs (the digit passes would reproduce the input order).
+    if (P > 0 && h[2] == 0 && n >= 2 && mode != IN_INTERNAL && !force_radix()) P = 0;
     if (P == 0) {
         if (o.want_internal || o.want_perm32) o.perm32.alloc(ctx, n);
         if (o.want_internal) {

@@ -58,11 +58,17 @@ def _sort_keys(kind, n, seed):
         return torch.tensor([I64_MIN, I64_MAX, 0, -1], dtype=torch.int64)[random_small_keys(n, 0, 3, seed)]
     if kind == "const":
         return torch.full((n,), 42, dtype=torch.int64)
+    if kind == "sorted_dups":   # already in order (the presorted shortcut), with ties
+        return torch.sort(random_small_keys(n, -1000, 1000, seed)).values
+    if kind == "sorted_i32_desc":   # non-increasing: identity order when sorting descending
+        return torch.sort(random_small_keys(n, -(1 << 31), (1 << 31) - 1, seed, dtype=torch.int32),
+                          descending=True).values
     raise ValueError(kind)
 
 
 @pytest.mark.parametrize("n", [0, 1, 2, 31, 33, 3071, 3072, 3073, 4095, 4096, 4097, 100_003])
-@pytest.mark.parametrize("kind", ["i64_wide", "i64_narrow", "i64_33bit", "i32", "u8", "dups", "extremes", "const"])
+@pytest.mark.parametrize("kind", ["i64_wide", "i64_narrow", "i64_33bit", "i32", "u8", "dups", "extremes", "const",
+                                  "sorted_dups", "sorted_i32_desc"])
 @pytest.mark.parametrize("desc", [False, True])
 def test_sort_parity(T, n, kind, desc):
     k = _sort_keys(kind, n, seed=n + 7)
@@ -71,6 +77,23 @@ def test_sort_parity(T, n, kind, desc):
     assert np.array_equal(npy(p), op)
     assert np.array_equal(npy(s).astype(np.int64), os_)
     assert s.dtype == k.dtype
+
+
+@pytest.mark.parametrize("dtype", [torch.int64, torch.int32])
+@pytest.mark.parametrize("n", [2, 4097, 100_003, 1_000_000])
+def test_sort_presorted_and_one_pair_out_of_order(T, dtype, n):
+    """Sorted input takes the one-pass identity route; one adjacent pair swapped anywhere
+    (first pair, across a 4,096-key tile, inside a 16-byte vector, the last pair) must not."""
+    k = torch.sort(random_small_keys(n, -(1 << 30), 1 << 30, 5, dtype=dtype)).values
+    cases = [k] + [k.clone() for _ in range(4)]
+    for c, i in zip(cases[1:], [0, 4095, n // 2 * 2, n - 2]):
+        if 0 <= i < n - 1 and c[i] != c[i + 1]:
+            c[[i, i + 1]] = c[[i + 1, i]]
+    for c in cases:
+        for desc in (False, True):
+            s, p = T.sort(c.cuda(), descending=desc)
+            os_, op = oracle.sort(c.numpy(), descending=desc)
+            assert np.array_equal(npy(p), op) and np.array_equal(npy(s).astype(np.int64), os_)
 
 
 @pytest.mark.parametrize("kind,n", [("i64_narrow", 2_000_003), ("i64_wide", 1_000_001), ("i32", 1_500_000)])
