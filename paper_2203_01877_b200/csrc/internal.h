@@ -18,6 +18,7 @@ struct SortOut {
     bool k32 = false;                  // internal keys are the low 32 bits of u
     uint64_t and_bits = 0, or_bits = 0;   // AND / OR of all u (varying-bit mask = and ^ or)
     int passes = 0;
+    bool identity = false;             // the input was already in (key, row) order: perm = 0..n-1
     DevBuf<uint32_t> keys32;           // internal sorted keys (k32)
     DevBuf<uint64_t> keys64;           // internal sorted keys (!k32)
     DevBuf<uint32_t> perm32;           // internal permutation

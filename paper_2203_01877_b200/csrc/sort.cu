@@ -816,6 +816,7 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     // streaming pass writes the outputs (the digit passes would reproduce the input order).
     if (P > 0 && h[2] == 0 && n >= 2 && mode != IN_INTERNAL && !force_radix()) P = 0;
     if (P == 0) {
+        o.identity = true;
         if (o.want_internal || o.want_perm32) o.perm32.alloc(ctx, n);
         if (o.want_internal) {
             if (o.k32) o.keys32.alloc(ctx, n); else o.keys64.alloc(ctx, n);

@@ -229,6 +229,47 @@ def test_pkfk_tpch_filtered_build(T):
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
 
 
+@pytest.mark.parametrize("kind", ["dense", "sparse", "i32_negative", "block_edges", "one_key"])
+def test_pkfk_presorted_build_rank_bitmap(T, kind):
+    """Build sides already in key order take the rank-bitmap route (one 32-byte block of a
+    rank + 224 presence bits per probe): dense and sparse domains, negative i32 keys, keys
+    on 224-bit block edges; probe keys below, inside and above the domain."""
+    rng = np.random.default_rng(7)
+    if kind == "dense":
+        build = np.arange(-50_000, 250_000, dtype=np.int64)
+    elif kind == "sparse":
+        build = np.unique(rng.integers(0, 6_000_000, 400_000))
+    elif kind == "i32_negative":
+        build = np.unique(rng.integers(-(1 << 31), -(1 << 31) + 3_000_000, 200_000))
+    elif kind == "block_edges":
+        e = np.arange(1, 3000, dtype=np.int64) * 224
+        build = np.unique(np.concatenate([e - 1, e, e + 1, e + 31, e + 32, e + 95, e + 96]))
+    else:
+        build = np.array([123456789], dtype=np.int64)
+    dt = torch.int32 if kind == "i32_negative" else torch.int64
+    lo_, hi_ = int(build.min()), int(build.max())
+    probe = np.concatenate([rng.choice(build, 300_000), rng.integers(lo_ - 300, hi_ + 300, 300_001)])
+    if dt == torch.int32:
+        probe = np.clip(probe, -(1 << 31), (1 << 31) - 1)
+    probe = rng.permutation(probe).astype(np.int64)
+    lo, ro = T.pkfk_join(cu(build, dt), cu(probe, dt))
+    olo, oro = oracle.pkfk_join(build, probe)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    left, mask = T.pkfk_outer(cu(build, dt), cu(probe, dt), return_mask=True)   # probe-side outer join
+    want = np.full(probe.size, -1, np.int64)
+    want[oro] = olo
+    assert np.array_equal(npy(left), want) and np.array_equal(npy(mask).astype(bool), want >= 0)
+    dups = np.sort(np.concatenate([build, build[::3]]))   # semi / anti: duplicates allowed
+    for anti in (False, True):
+        sel = T.pkfk_semi(cu(dups, dt), cu(probe, dt), anti=anti)
+        member = np.isin(probe, build)
+        assert np.array_equal(npy(sel), np.nonzero(~member if anti else member)[0])
+    if build.size > 1:   # a duplicate in a presorted build side is still an error
+        with pytest.raises(T.TqpError) as e:
+            T.pkfk_join(cu(np.insert(build, 1, build[0]), dt), cu(probe[:10], dt))
+        assert e.value.status == T.TQP_ERR_DUPLICATE_BUILD_KEY
+
+
 @pytest.mark.parametrize("slice_mb", ["0.004", "0.05"])
 def test_pkfk_multipass_probe(T, slice_mb):
     """The multi-pass probe (build sides much larger than L2, e.g. SF100) run at small sizes
