@@ -102,8 +102,27 @@ __global__ void rank_bitmap_kernel(const uint32_t* __restrict__ keys, int64_t n,
     }
 }
 
+// One 256-bit load per lookup (LDG.256, new on sm_100; L1 not allocated: the bitmap
+// lives in L2 and random 16-byte pairs made the probe L1-wavefront bound).
+#ifndef TQP_RANK_LD256
+#define TQP_RANK_LD256 1
+#endif
 __device__ __forceinline__ bool lookup_rank(const uint4* rb, uint32_t rel, uint32_t& left) {
     const uint32_t blk = rel / RB_BITS, bit = rel % RB_BITS, w = bit >> 5;
+#if TQP_RANK_LD256
+    uint32_t v[8];
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(rb + 2 * (int64_t)blk));
+    uint32_t cnt = v[0], word = v[1];
+#pragma unroll
+    for (int j = 1; j < 7; j++)
+        if (w >= (uint32_t)j) { cnt += __popc(v[j]); word = v[j + 1]; }
+    const uint32_t m1 = 1u << (bit & 31);
+    if (!(word & m1)) return false;
+    left = cnt + __popc(word & (m1 - 1u));
+    return true;
+#else
     const uint4 q0 = __ldg(rb + 2 * (int64_t)blk);
     const uint32_t words[3] = {q0.y, q0.z, q0.w};
     uint32_t cnt = q0.x, word;
@@ -124,6 +143,7 @@ __device__ __forceinline__ bool lookup_rank(const uint4* rb, uint32_t rel, uint3
     if (!(word & m)) return false;
     left = cnt + __popc(word & (m - 1u));
     return true;
+#endif
 }
 
 struct ProbeArgs {
@@ -234,6 +254,11 @@ __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint3
             const uint64_t pol = l2_evict_last();
             q0 = ldg_hint(p4, pol);
             q1 = ldg_hint(p4 + 1, pol);
+        } else if (TQP_RANK_LD256) {   // the bucket's sector in one 256-bit load
+            asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(q0.x), "=r"(q0.y), "=r"(q0.z), "=r"(q0.w), "=r"(q1.x), "=r"(q1.y), "=r"(q1.z),
+                           "=r"(q1.w)
+                         : "l"(p4));
         } else {
             q0 = __ldg(p4);
             q1 = __ldg(p4 + 1);
