@@ -42,6 +42,18 @@ __device__ __forceinline__ uint64_t load_u(const void* p, int64_t i, bool desc) 
     return desc ? ~u : u;
 }
 
+// Fold one block's AND / OR / "out of order" into the three plan words. Every block of a
+// 60M-key input hitting the same L2 sector with atomics serialised the pass (shuffled
+// keys: one same-address atomic per warp, 240 us for 60M keys); the words settle after
+// a few blocks, so each block reads them first and only issues the atomics that change
+// something.
+__device__ __forceinline__ void andor_fold(unsigned long long* out, uint64_t a, uint64_t o, bool uns) {
+    const volatile unsigned long long* v = out;
+    if ((v[0] & a) != v[0]) atomicAnd(&out[0], (unsigned long long)a);
+    if ((v[1] | o) != v[1]) atomicOr(&out[1], (unsigned long long)o);
+    if (uns && v[2] == 0) atomicOr(&out[2], 1ull);
+}
+
 template <int IN>
 __global__ void __launch_bounds__(NT) andor_kernel(const void* keys, int64_t n, bool desc,
                                                    unsigned long long* out) {
@@ -53,7 +65,7 @@ __global__ void __launch_bounds__(NT) andor_kernel(const void* keys, int64_t n, 
         o |= u;
         if (i + 1 < n) uns |= u > load_u<IN>(keys, i + 1, desc);
     }
-    if (__any_sync(0xffffffffu, uns) && (threadIdx.x & 31) == 0) atomicOr(&out[2], 1ull);
+    uns = __syncthreads_or(uns);
     for (int s = 16; s > 0; s >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, s);
         o |= __shfl_xor_sync(0xffffffffu, o, s);
@@ -63,8 +75,7 @@ __global__ void __launch_bounds__(NT) andor_kernel(const void* keys, int64_t n, 
     __syncthreads();
     if (threadIdx.x == 0) {
         for (int w = 1; w < NW; w++) { a &= sa[w]; o |= so[w]; }
-        atomicAnd(&out[0], (unsigned long long)a);
-        atomicOr(&out[1], (unsigned long long)o);
+        andor_fold(out, a, o, uns);
     }
 }
 
@@ -97,6 +108,7 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
     const int64_t base = (int64_t)blockIdx.x * H0_TILE;
     uint64_t a = ~0ull, o = 0;
     uint64_t u[H0_IPT];
+    bool unsorted;
     if ((IN == IN_I64 || IN == IN_I32) && base + H0_TILE <= n && ((uintptr_t)keys & 15) == 0) {
         // full tile: 16-byte loads (which warp counts a key does not matter for the tile)
         constexpr int PER = IN == IN_I64 ? 2 : 4;   // keys per 16-byte load
@@ -123,12 +135,17 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
             atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
             if (i % PER != PER - 1) {
                 uns |= u[i] > u[i + 1];
-            } else {   // the key after this vector (next thread's first): an L1 hit
-                const int64_t nx = base + ((int64_t)(i / PER) * NT + tid + 1) * PER;
-                if (nx < n) uns |= u[i] > load_u<IN>(keys, nx, desc);
+            } else {   // the key after this vector: the next lane's first (a shuffle), lane 31 loads it
+                const uint64_t nxt = __shfl_down_sync(0xffffffffu, u[i + 1 - PER], 1);
+                if (lane != 31) {
+                    uns |= u[i] > nxt;
+                } else {
+                    const int64_t nx = base + ((int64_t)(i / PER) * NT + tid + 1) * PER;
+                    if (nx < n) uns |= u[i] > load_u<IN>(keys, nx, desc);
+                }
             }
         }
-        if (__any_sync(0xffffffffu, uns) && lane == 0) atomicOr(&out[2], 1ull);
+        unsorted = uns;
     } else {
 #pragma unroll
         for (int i = 0; i < H0_IPT; i++) {
@@ -143,8 +160,9 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
             if (pos < n) atomicAdd(&h[warp][dslot((uint32_t)u[i] & (H0_BINS - 1u))], 1u);
             if (pos + 1 < n) uns |= u[i] > load_u<IN>(keys, pos + 1, desc);
         }
-        if (__any_sync(0xffffffffu, uns) && lane == 0) atomicOr(&out[2], 1ull);
+        unsorted = uns;
     }
+    unsorted = __syncthreads_or(unsorted);
     for (int sft = 16; sft > 0; sft >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, sft);
         o |= __shfl_xor_sync(0xffffffffu, o, sft);
@@ -153,8 +171,7 @@ __global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64
     __syncthreads();
     if (tid == 0) {
         for (int w = 1; w < NW; w++) { a &= sa[w]; o |= so[w]; }
-        atomicAnd(&out[0], (unsigned long long)a);
-        atomicOr(&out[1], (unsigned long long)o);
+        andor_fold(out, a, o, unsorted);
     }
     for (int d = tid; d < H0_BINS; d += NT) {
         uint32_t c = 0;
