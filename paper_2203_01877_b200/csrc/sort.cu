@@ -97,8 +97,15 @@ __device__ __forceinline__ uint32_t dslot(uint32_t d) { return d ^ (((d >> 5) * 
 // produces, e.g. orders rows in key order, whose digits repeat every 128 rows --
 // no longer land on one bank (32-way conflicts on the staging stores otherwise).
 __device__ __forceinline__ uint32_t kslot(uint32_t r) { return r ^ ((r >> 5) & 15u); }
+// Blocks per SM the register budget must allow: at the default 72 registers only 3 fit
+// (37 % occupancy) and the one-tile blocks stalled on their loads (ncu: long scoreboard).
+// Measured, 60M shuffled int64 keys: 0.147 ms at 72 registers, 0.128 ms with 4 blocks,
+// 0.120 ms with 5 (16 bytes of spills), 6 spills ~250 bytes.
+#ifndef TQP_H0_MINB
+#define TQP_H0_MINB 5
+#endif
 template <int IN>
-__global__ void __launch_bounds__(NT) andor_hist0_kernel(const void* keys, int64_t n, bool desc,
+__global__ void __launch_bounds__(NT, TQP_H0_MINB) andor_hist0_kernel(const void* keys, int64_t n, bool desc,
                                                          unsigned long long* out, uint32_t* __restrict__ th0) {
     __shared__ uint32_t h[NW][H0_BINS];
     __shared__ uint64_t sa[NW], so[NW];
