@@ -46,7 +46,13 @@ __device__ __forceinline__ void load_rows(const T* c, int64_t r0, int64_t n, boo
 
 // Pass 1 (Listing 1, the bitmap): the conjunction per row -> u8 mask, and the number
 // of passing rows per tile. No inter-tile dependency.
-__global__ void __launch_bounds__(FNT) filter_mask_kernel(FilterArgs a) {
+// Blocks per SM the register budget must allow (72 registers held it to 3). Measured, Q6
+// mask at SF10: 0.263 ms at 72 registers, 0.253 ms with 4 blocks (56), 0.254 with 5,
+// 0.256 with 6 (spills).
+#ifndef TQP_FILTER_MINB
+#define TQP_FILTER_MINB 4
+#endif
+__global__ void __launch_bounds__(FNT, TQP_FILTER_MINB) filter_mask_kernel(FilterArgs a) {
     __shared__ uint32_t s_w[FNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * FTILE;
