@@ -472,7 +472,12 @@ __global__ void ck_final_kernel(const unsigned long long* __restrict__ slots, un
 }
 
 template <bool CK>
-__global__ void __launch_bounds__(ENT) expand_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
+// Blocks per SM forced by the register budget: measured no gain (SF10 expansion 0.435 ms
+// at 63 registers / 4 blocks, 0.443 with 5, 0.439 with 6, 0.494 with 8 -- spills), so off.
+#ifndef TQP_EXPAND_MINB
+#define TQP_EXPAND_MINB 0
+#endif
+__global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint32_t* __restrict__ mL, const uint32_t* __restrict__ mR,
                                                      const uint32_t* __restrict__ msL, const uint32_t* __restrict__ msR,
                                                      const int64_t* __restrict__ mcum, int64_t K,
                                                      const uint32_t* __restrict__ tb,
