@@ -297,7 +297,12 @@ constexpr uint32_t NOMATCH = 0xFFFFFFFFu;   // build rows are < 2^30
 // the matching build row (or NOMATCH) as u32, semi mode the match byte; each tile
 // counts its selected rows.
 template <typename KT, int PDT, bool PACKED>
-__global__ void __launch_bounds__(PNT) probe_kernel(ProbeArgs a) {
+// Blocks per SM forced by the register budget: measured slower at full occupancy (SF10
+// probe 0.327 ms at 40 registers / 6 blocks, 0.340 ms at 32 registers / 8 blocks), so off.
+#ifndef TQP_PROBE_MINB
+#define TQP_PROBE_MINB 0
+#endif
+__global__ void __launch_bounds__(PNT, TQP_PROBE_MINB) probe_kernel(ProbeArgs a) {
     __shared__ uint32_t s_w[PNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * PTILE;
