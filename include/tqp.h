@@ -171,8 +171,9 @@ tqp_status tqp_pkfk_join_hash(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build,
  * left_out[i] = its build row, or -1 without a match (n_probe x int64,
  * caller-allocated, required); the right index of row i is i itself.
  * match_out (nullable, n_probe x u8) = 1 iff matched; *n_match_host (nullable)
- * = matched rows. Duplicate build keys are not checked (each probe row takes
- * one of the equal build rows). Synchronises twice. */
+ * = matched rows. Duplicate build keys are not an error: each probe row takes
+ * one of the equal build rows. Synchronises twice (three times when the build
+ * side is already in key order: its duplicate flag is read before the probe). */
 tqp_status tqp_pkfk_outer(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
                           int64_t* left_out, uint8_t* match_out, int64_t* n_match_host);
 

@@ -29,8 +29,23 @@ def deps():
         [os.path.join(ROOT, "include", "tqp.h"), __file__]
 
 
+STAMP = LIB + ".flags"
+
+
+def _flag_stamp():
+    """The nvcc flags a build uses, TQP_NVCC_EXTRA included: an A/B build with extra flags
+    (tools/ab_*.sh) must not be mistaken for the default one."""
+    return " ".join(FLAGS + os.environ.get("TQP_NVCC_EXTRA", "").split())
+
+
 def needs_build():
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as f:
+            if f.read() != _flag_stamp():
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(d) > t for d in deps())
@@ -64,6 +79,8 @@ def build(force=False, verbose=False, jobs=None):
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, "-o", tmp,
                            "-lcudart"])
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(_flag_stamp())
     return LIB
 
 

@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary of libtqp (declared in include/tqp.h).
 // Every entry point converts internal exceptions into a tqp_status and a
 // message; nothing C++ crosses the ABI.
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.h"
@@ -39,6 +40,16 @@ static size_t round_block(size_t b) {
 
 void* tqp_ctx::dalloc(size_t bytes) {
     if (bytes == 0) return nullptr;
+    if (exact_alloc) {
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            tqp::fail(TQP_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+        }
+        live_blocks[p] = bytes;
+        return p;
+    }
     const size_t sz = round_block(bytes);
     auto it = free_blocks.lower_bound(sz);
     if (it != free_blocks.end() && it->first <= sz + sz / 4) {   // best fit within 25 %
@@ -67,6 +78,12 @@ void* tqp_ctx::dalloc(size_t bytes) {
 void tqp_ctx::dfree(void* p) {
     auto it = live_blocks.find(p);
     if (it == live_blocks.end()) return;
+    if (exact_alloc) {
+        cudaStreamSynchronize(stream);
+        cudaFree(p);
+        live_blocks.erase(it);
+        return;
+    }
     free_blocks.emplace(it->second, p);
     cached_bytes += it->second;
     live_blocks.erase(it);
@@ -130,6 +147,8 @@ tqp_status tqp_ctx_create(int device, void* stream, tqp_ctx** out) {
         TQP_CUDA(cudaSetDevice(device));
         TQP_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
         c->stream = static_cast<cudaStream_t>(stream);
+        const char* ex = getenv("TQP_ALLOC_EXACT");
+        c->exact_alloc = ex && ex[0] == '1';
         TQP_CUDA(cudaMallocHost(&c->pinned, 4096));
     } catch (const tqp::Error& e) {
         delete c;

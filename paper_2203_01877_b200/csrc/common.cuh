@@ -49,6 +49,10 @@ struct tqp_ctx {
     std::multimap<size_t, void*> free_blocks;
     std::unordered_map<void*, size_t> live_blocks;
     size_t cached_bytes = 0;
+    // TQP_ALLOC_EXACT=1 (sanitizer runs): every temporary is its own exact-size cudaMalloc,
+    // freed (after a stream sync) when released, so memcheck sees out-of-bounds accesses
+    // that a cached, rounded-up block would hide
+    bool exact_alloc = false;
     void* dalloc(size_t bytes);
     void dfree(void* p);
     void trim();

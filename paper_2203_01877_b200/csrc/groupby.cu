@@ -1068,6 +1068,7 @@ struct PresArgs {
     int64_t n;
     const unsigned long long* krange;
     uint32_t* bitmap;   // 2^PBITS bits
+    int64_t stride;     // > 1: a sample -- 16-row groups 0, stride, 2 * stride, ... (no tail)
 };
 
 __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
@@ -1094,7 +1095,8 @@ __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
     constexpr int R = 16;
     bool vec = true;
     for (int k = 0; k < a.n_keys; k++) vec = vec && (uintptr_t)a.kcol[k] % 16 == 0;
-    const int64_t nb = vec ? a.n / R : 0;
+    const int64_t stride = a.stride;
+    const int64_t nb = vec ? a.n / R / stride : 0;   // 16-row groups visited
     const int64_t gs = (int64_t)gridDim.x * GNT;
     // two row groups (g, g + gs) per step: their loads are in flight together
     constexpr int U = 2;
@@ -1115,7 +1117,7 @@ __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
                 uint4 q[U];
 #pragma unroll
                 for (int u = 0; u < U; u++)
-                    q[u] = ok[u] ? __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g0 + u * gs) : make_uint4(0, 0, 0, 0);
+                    q[u] = ok[u] ? __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + (g0 + u * gs) * stride) : make_uint4(0, 0, 0, 0);
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     const uint32_t wv[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
@@ -1127,7 +1129,7 @@ __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     if (!ok[u]) continue;
-                    const int64_t g = g0 + u * gs;
+                    const int64_t g = (g0 + u * gs) * stride;
 #pragma unroll
                     for (int j = 0; j < R / 4; j++) {
                         const uint4 q = __ldcs(reinterpret_cast<const uint4*>(a.kcol[k]) + g * 4 + j);
@@ -1140,7 +1142,7 @@ __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
 #pragma unroll
                 for (int u = 0; u < U; u++) {
                     if (!ok[u]) continue;
-                    const int64_t g = g0 + u * gs;
+                    const int64_t g = (g0 + u * gs) * stride;
 #pragma unroll
                     for (int j = 0; j < R / 2; j++) {
                         const ulonglong2 q = __ldcs(reinterpret_cast<const ulonglong2*>(a.kcol[k]) + g * 8 + j);
@@ -1156,7 +1158,7 @@ __global__ void __launch_bounds__(GNT) gb_presence_kernel(PresArgs a) {
 #pragma unroll
                 for (int i = 0; i < R; i++) mark(b[u][i]);
     }
-    for (int64_t r = nb * R + blockIdx.x * (int64_t)GNT + tid; r < a.n; r += gs) {   // tail / unaligned
+    for (int64_t r = nb * R + blockIdx.x * (int64_t)GNT + tid; stride == 1 && r < a.n; r += gs) {   // tail / unaligned
         uint32_t b = 0;
         for (int k = 0; k < a.n_keys; k++)
             b |= (uint32_t)(key_part(load_as_i64(a.kcol[k], a.kdt[k], r), a.kdt[k]) - kmin[k]) << sh[k];
@@ -1238,7 +1240,18 @@ __device__ __forceinline__ void load4(const uint8_t* col, int dt, int tid, int64
     }
 }
 
-template <int NT>
+// SPEC (dense kernels specialised on the column types, which removes a per-factor dtype
+// switch from every row): bit 0 = every factor column is int64 (fixed-point decimals),
+// bit 1 = every key column is u8 (1-character flags, reading R19).
+constexpr int SPEC_VI64 = 1, SPEC_KU8 = 2;
+
+__device__ __forceinline__ void load4_i64(const uint8_t* col, int tid, int64_t (&x)[GPT]) {
+    const longlong2 u0 = reinterpret_cast<const longlong2*>(col)[2 * tid];
+    const longlong2 u1 = reinterpret_cast<const longlong2*>(col)[2 * tid + 1];
+    x[0] = u0.x; x[1] = u0.y; x[2] = u1.x; x[3] = u1.y;
+}
+
+template <int NT, int SPEC>
 __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* st, int64_t t, const DenseHdr& h,
                                            int64_t* acc, uint32_t* cnt, uint64_t (&mt)[PCH][3]) {
     const int tid = threadIdx.x;
@@ -1264,15 +1277,29 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     uint32_t kb[GPT] = {0, 0, 0, 0};
     for (int c = 0; c < a.n_keys; c++) {
         const int u = a.kcol[c];
-        const int dt = a.udt[u];
-        int64_t x[GPT];
-        load4(st + a.uoff[u], dt, tid, x);
+        if (SPEC & SPEC_KU8) {
+            const uint32_t w = reinterpret_cast<const uint32_t*>(st + a.uoff[u])[tid];
+            const uint32_t mn = (uint32_t)h.kmin[c];
+            const int sh = h.kshift[c];
 #pragma unroll
-        for (int i = 0; i < GPT; i++) kb[i] |= (uint32_t)(key_part(x[i], dt) - h.kmin[c]) << h.kshift[c];
+            for (int i = 0; i < GPT; i++) kb[i] |= (((w >> (8 * i)) & 0xFFu) - mn) << sh;
+        } else {
+            const int dt = a.udt[u];
+            int64_t x[GPT];
+            load4(st + a.uoff[u], dt, tid, x);
+#pragma unroll
+            for (int i = 0; i < GPT; i++) kb[i] |= (uint32_t)(key_part(x[i], dt) - h.kmin[c]) << h.kshift[c];
+        }
     }
     int id[GPT];
+    bool unseen = false;   // a key the (sampled) presence bitmap missed: the host redoes it in full
 #pragma unroll
-    for (int i = 0; i < GPT; i++) id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
+    for (int i = 0; i < GPT; i++) {
+        id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
+        unseen |= id[i] >= a.D;
+        pass[i] &= id[i] < a.D;
+    }
+    if (unseen) atomicOr(a.overflow, 8);
 #pragma unroll
     for (int i = 0; i < GPT; i++)
         if (pass[i]) cnt[id[i] * NT + tid]++;
@@ -1290,7 +1317,8 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
             if (f < fx) continue;
             if (f >= a.pnf[jj]) break;
             int64_t x[GPT];
-            load4(st + a.poff[jj][f], a.pdtf[jj][f], tid, x);
+            if (SPEC & SPEC_VI64) load4_i64(st + a.poff[jj][f], tid, x);
+            else load4(st + a.poff[jj][f], a.pdtf[jj][f], tid, x);
             const uint64_t add = (uint64_t)a.padd[jj][f];
             const bool neg = a.psign[jj][f] < 0;
             uint64_t m2 = mt[jj][f];
@@ -1316,7 +1344,7 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     }
 }
 
-template <int NT>
+template <int NT, int SPEC>
 __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1347,7 +1375,7 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     for (int jj = 0; jj < PCH; jj++)
 #pragma unroll
         for (int f = 0; f < 3; f++) mt[jj][f] = 0;
-    tile_pipeline<NT>(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile<NT>(a, st, t, h, acc, cnt, mt); });
+    tile_pipeline<NT>(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile<NT, SPEC>(a, st, t, h, acc, cnt, mt); });
     bool bad = false;
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
@@ -1403,6 +1431,22 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
         const int64_t rec = h.drec[d];
         if (rec >= 0) { a.pkey[rec] = a.dkeys[d]; a.pcount[rec] = h.dcnt[d]; }
     }
+}
+
+// f(gb_dense_kernel<nt, spec>) for runtime (nt, spec)
+template <typename F>
+static void dense_call(int nt, int spec, F&& f) {
+    auto by_spec = [&](auto ntc) {
+        constexpr int NTc = decltype(ntc)::value;
+        switch (spec) {
+            case 0: f(gb_dense_kernel<NTc, 0>); break;
+            case 1: f(gb_dense_kernel<NTc, 1>); break;
+            case 2: f(gb_dense_kernel<NTc, 2>); break;
+            default: f(gb_dense_kernel<NTc, 3>); break;
+        }
+    };
+    if (nt == 128) by_spec(std::integral_constant<int, 128>{});
+    else by_spec(std::integral_constant<int, 256>{});
 }
 
 // Direct merge of fixed-slot partials (dense ids / no keys): record b * D + d holds CTA
@@ -2202,37 +2246,51 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
         DevBuf<uint64_t> dkeys;
         bool dense = false;
         size_t dense_smem = 0;
-        int dense_ns = 0, dense_nt = GNT;
+        int dense_ns = 0, dense_nt = GNT, dense_spec = 0;
         int64_t dense_grid = 0;
         const char* dz = getenv("TQP_GROUPBY_DENSE");
         bool small_add = true;   // the dense bound argument needs |add| < 2^61
         for (int j = 0; j < PL->n_pairs && j < PCH; j++)
             for (int f = 0; f < pnf[j]; f++) small_add = small_add && a.padd[j][f] < (1ll << 61) && a.padd[j][f] > -(1ll << 61);
-        if (n_keys > 0 && n > 0 && PL->n_pairs <= PCH && small_add && !(dz && dz[0] == '0')) {
+        // presence from a sample of the rows first (~1M rows: the keys cost a few microseconds
+        // instead of a pass); a row whose key the sample missed raises overflow bit 8 in the
+        // dense kernel, and the presence pass is redone over every row
+        bool key_cols_aligned = true;
+        for (int k = 0; k < n_keys; k++) key_cols_aligned = key_cols_aligned && (uintptr_t)kc[k] % 16 == 0;
+        int64_t pres_stride = key_cols_aligned ? std::max<int64_t>(1, n / (int64_t(1) << 20)) : 1;
+        auto setup_dense = [&](int64_t stride) {
+            dense = false;
             DevBuf<uint32_t> bitmap(ctx, 1 << (PBITS - 5));
             DevBuf<int> Dd(ctx, 1);
             bitmap.zero();
             dtab.alloc(ctx, 1 << PBITS);
+            TQP_CUDA(cudaMemsetAsync(dtab.get(), 0xFF, (size_t)1 << PBITS, ctx->stream));
             dkeys.alloc(ctx, DMAX);
             PresArgs pa{};
             pa.n_keys = n_keys;
             pa.n = n;
             pa.krange = PL->krange.get();
             pa.bitmap = bitmap.get();
+            pa.stride = stride;
             double kb = 0;
             for (int k = 0; k < n_keys; k++) {
                 pa.kcol[k] = kc[k];
                 pa.kdt[k] = kd[k];
                 kb += (double)dtype_size(kd[k]);
             }
-            const int g = (int)std::min<int64_t>(ceil_div(n, GNT * 16), (int64_t)ctx->num_sms * 8);
+            const int g = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n / stride, GNT * 16), (int64_t)ctx->num_sms * 8));
             launch(ctx, "tqp_groupby_presence", gb_presence_kernel, dim3(g), dim3(GNT), 0, pa);
-            ctx->add_bytes("tqp_groupby_presence", kb * (double)n);
+            ctx->add_bytes("tqp_groupby_presence", kb * (double)(n / stride));
             launch(ctx, "tqp_groupby_dense_ids", gb_dense_ids_kernel, dim3(1), dim3(1024), 0, (const uint32_t*)bitmap.get(),
                    dtab.get(), dkeys.get(), Dd.get());
             int D = 0;
             read_back(ctx, &D, Dd.get(), 4);
             if (D >= 1 && D <= DMAX) {
+                bool vi64 = true, ku8 = true;
+                for (int j = 0; j < PL->n_pairs && j < PCH; j++)
+                    for (int f = 0; f < pnf[j]; f++) vi64 = vi64 && a.pdtf[j][f] == TQP_I64;
+                for (int k = 0; k < n_keys; k++) ku8 = ku8 && kd[k] == TQP_U8;
+                dense_spec = (vi64 ? SPEC_VI64 : 0) | (ku8 ? SPEC_KU8 : 0);
                 // (threads per CTA, stages) with the most resident warps per SM; ties go to
                 // more stages per SM. Lane-private accumulators make occupancy smem-bound.
                 const size_t hdr = (sizeof(DenseHdr) + 15) & ~size_t(15);
@@ -2244,7 +2302,7 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                         const size_t sm = (size_t)ns * stage + hdr + accb;
                         if (sm > 227 * 1024) continue;
                         int occ = 0;
-                        occ = nt == 128 ? occupancy(gb_dense_kernel<128>, nt, sm) : occupancy(gb_dense_kernel<256>, nt, sm);
+                        dense_call(nt, dense_spec, [&](auto* kfn) { occ = occupancy(kfn, nt, sm); });
                         const int wps = occ * nt / 32, st = occ * ns;
                         if (occ > 0 && (wps > best_w || (wps == best_w && st > best_st))) {
                             best_w = wps;
@@ -2270,7 +2328,8 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                     dense = a.dense_bits >= 1;
                 }
             }
-        }
+        };
+        if (n_keys > 0 && n > 0 && PL->n_pairs <= PCH && small_add && !(dz && dz[0] == '0')) setup_dense(pres_stride);
 
         // ---- phase 1 (retried once with full capacity if the partial estimate is exceeded)
         Partials pr;
@@ -2289,7 +2348,7 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
             const int occ = occupancy(gb_phase1_kernel, GNT, nokey_smem);
             nokey_grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
         }
-        for (int attempt = 0; attempt < 3; attempt++) {
+        for (int attempt = 0; attempt < 4; attempt++) {
             // dense ids / no keys: fixed per-CTA slots merged directly (no phase-2 sort)
             const bool direct = n > 0 && (dense || nokey_path);
             const int64_t dD = dense ? a.D : 1;
@@ -2321,10 +2380,10 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                 for (int j = 0; j < PL->n_pairs && j < PCH; j++)
                     for (int f = 0; f < pnf[j]; f++) ad.poff[j][f] = ad.uoff[a.pfc[j][f]];
                 tile_name = "tqp_groupby_dense";
-                if (dense_nt == 128)
-                    launch(ctx, tile_name, gb_dense_kernel<128>, dim3((unsigned)dense_grid), dim3(128), dense_smem, ad);
-                else
-                    launch(ctx, tile_name, gb_dense_kernel<256>, dim3((unsigned)dense_grid), dim3(256), dense_smem, ad);
+                dense_call(dense_nt, dense_spec, [&](auto* kfn) {
+                    set_smem(kfn, dense_smem);
+                    launch(ctx, tile_name, kfn, dim3((unsigned)dense_grid), dim3(dense_nt), dense_smem, ad);
+                });
             } else if (n > 0 && nokey_path) {
                 tile_name = "tqp_groupby_tile";
                 if (nokey_smem > 227 * 1024) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: referenced columns too wide");
@@ -2370,6 +2429,11 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
             unsigned long long h[2] = {0, 0};
             read_back(ctx, h, Pc.get(), 16);
             const int o = (int)h[1];
+            if ((o & 8) && dense && pres_stride > 1) {   // a key outside the sampled presence: full pass
+                pres_stride = 1;
+                setup_dense(1);
+                continue;
+            }
             if (o & 4) {   // dense path could not prove a tile exact: general path
                 dense = false;
                 continue;

@@ -14,6 +14,9 @@ struct SortOut {
     uint64_t* sorted_u = nullptr;      // n x sort-domain values u (ascending)
     bool want_internal = false;        // keep internal sorted keys + u32 permutation below
     bool want_perm32 = false;          // keep the u32 permutation only
+    bool defer_identity = false;       // presorted input: return with identity = true and nothing
+                                       // written (the caller reads the input keys themselves or
+                                       // calls sort_materialize_identity)
     // results
     bool k32 = false;                  // internal keys are the low 32 bits of u
     uint64_t and_bits = 0, or_bits = 0;   // AND / OR of all u (varying-bit mask = and ^ or)
@@ -35,6 +38,9 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
 void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao,
                 uint32_t* th0 = nullptr);
 size_t sort_hist0_words(int64_t n);
+// The identity route's outputs (the trivial pass) for a sort that returned with
+// defer_identity and identity set.
+void sort_materialize_identity(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o);
 
 // Filter + compaction (filter.cu), used by the group-by sort path for its selection.
 void filter_compact(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, const tqp_pred* preds, int n_preds,

@@ -20,6 +20,12 @@
 //      rightOutputIndex = probe row in ascending probe-row order
 //      (reading R7). Two passes instead of one with a decoupled look-back: the
 //      look-back left a tile's warps idle at the barrier (measured).
+//   4. direct output: when every probe row matches (a foreign key always has its
+//      primary key: lineitem -> orders), the compacted pairs ARE the per-row pairs, so
+//      the probe writes (build row, probe row) straight into the outputs and the u32
+//      intermediate, the scan and the compaction pass disappear. A 2,048-row sample
+//      probed first (probe_sample_kernel) picks the layout on the device; the one
+//      readback (matched rows) tells the host whether a compaction is needed after all.
 // Duplicate build keys (adjacent equal sorted keys) -> TQP_ERR_DUPLICATE_BUILD_KEY.
 #include "internal.h"
 #include <cmath>
@@ -86,15 +92,17 @@ constexpr uint32_t RB_BITS = 224;
 
 // One thread per sorted key: set its bit; the first key of a block writes the block's
 // rank (its sorted position); equal neighbours flag a duplicate build key.
-__global__ void rank_bitmap_kernel(const uint32_t* __restrict__ keys, int64_t n, uint32_t base, int64_t nblk,
+// Reads the caller's build keys directly (the sort's identity route writes nothing): the
+// low 32 bits of the order-preserving key (all varying bits are there, k32).
+__global__ void rank_bitmap_kernel(const void* __restrict__ keys, int dt, int64_t n, uint32_t base, int64_t nblk,
                                    uint32_t* __restrict__ bm, int* __restrict__ dup) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t rel = keys[i] - base;
+        const uint32_t rel = (uint32_t)ordered_u64(load_as_i64(keys, dt, i)) - base;
         const uint32_t blk = rel / RB_BITS, bit = rel % RB_BITS;
         atomicOr(bm + (int64_t)blk * 8 + 1 + (bit >> 5), 1u << (bit & 31));
         int64_t prev = -1;
         if (i > 0) {
-            const uint32_t rp = keys[i - 1] - base;
+            const uint32_t rp = (uint32_t)ordered_u64(load_as_i64(keys, dt, i - 1)) - base;
             if (rp == rel) *dup = 1;
             prev = rp / RB_BITS;
         }
@@ -168,6 +176,15 @@ struct ProbeArgs {
     uint32_t* tcnt;           // per tile: rows selected (join: matches; semi: match != anti)
     uint64_t blo, bhi;        // multi-pass probe: the bucket range this pass resolves
     const uint4* rank_bm;     // nullable: rank bitmap of a presorted build side (RB_BITS bits per 32-byte block)
+    // join mode, direct output: when *direct == 0 (no sampled miss, probe_sample_kernel)
+    // the probe writes the final pairs at their probe row -- left = build row (or -1),
+    // right = row -- instead of the u32 build row for the compaction pass; exact when every
+    // probe row matches (then no compaction runs), else the host compacts afterwards
+    const int* direct;        // nullable: never direct; else the sample's miss flag
+    unsigned long long* total;   // direct-capable launches: matched rows (one atomic per tile)
+    void* out_l;              // int64 (or int32 when idx32) pairs, capacity n_probe
+    void* out_r;
+    int idx32;
 };
 
 // L2 evict-last policy on the slot-table loads: measured no change at SF10
@@ -228,12 +245,47 @@ __device__ __forceinline__ bool lookup_packed(const ProbeArgs& a, uint32_t rel_l
     return false;
 }
 
+template <int PDT>
+__device__ __forceinline__ int64_t load_probe_key(const void* probe, int64_t row) {
+    // probe keys are streamed once: evict-first
+    if (PDT == TQP_I64) return (int64_t)__ldcs((const long long*)probe + row);
+    if (PDT == TQP_I32) return (int64_t)__ldcs((const int*)probe + row);
+    return (int64_t)__ldcs((const unsigned char*)probe + row);
+}
+
+// The probe key's offset rel = k - base in the internal key domain, if the key can be on
+// the build side at all (its high word and its varying-bit span match).
+template <typename KT>
+__device__ __forceinline__ bool probe_rel(const ProbeArgs& a, int64_t v, KT& rel) {
+    const uint64_t u = ordered_u64(v);
+    if (sizeof(KT) == 4 && (u & 0xFFFFFFFF00000000ull) != a.hi_bits) return false;
+    const KT k = (KT)u;
+    rel = (KT)(k - (KT)a.base);
+    return k >= (KT)a.base && !(a.vbits < 64 && ((uint64_t)rel >> a.vbits) != 0);
+}
+
+__device__ __forceinline__ void ld256(const void* p, uint32_t (&v)[8]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(p));
+}
+
+// rank bitmap block (already loaded) -> hit and build row
+__device__ __forceinline__ bool rank_eval(const uint32_t (&v)[8], uint32_t rel, uint32_t& left) {
+    const uint32_t bit = rel % RB_BITS, w = bit >> 5;
+    uint32_t cnt = v[0], word = v[1];
+#pragma unroll
+    for (int j = 1; j < 7; j++)
+        if (w >= (uint32_t)j) { cnt += __popc(v[j]); word = v[j + 1]; }
+    const uint32_t m1 = 1u << (bit & 31);
+    if (!(word & m1)) return false;
+    left = cnt + __popc(word & (m1 - 1u));
+    return true;
+}
+
 template <typename KT, int PDT, bool PACKED>
 __device__ __forceinline__ bool probe_one(const ProbeArgs& a, int64_t row, uint32_t& left) {
-    int64_t v;   // probe keys are streamed once: evict-first
-    if (PDT == TQP_I64) v = (int64_t)__ldcs((const long long*)a.probe + row);
-    else if (PDT == TQP_I32) v = (int64_t)__ldcs((const int*)a.probe + row);
-    else v = (int64_t)__ldcs((const unsigned char*)a.probe + row);
+    const int64_t v = load_probe_key<PDT>(a.probe, row);
     uint64_t u = ordered_u64(v);
     KT k;
     if (sizeof(KT) == 4) {
@@ -306,6 +358,7 @@ __global__ void __launch_bounds__(PNT, TQP_PROBE_MINB) probe_kernel(ProbeArgs a)
     __shared__ uint32_t s_w[PNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * PTILE;
+    const bool direct = a.mode == 0 && a.direct && *a.direct == 0;
     bool m[PIPT];
     uint32_t left[PIPT];
 #pragma unroll
@@ -320,7 +373,16 @@ __global__ void __launch_bounds__(PNT, TQP_PROBE_MINB) probe_kernel(ProbeArgs a)
     for (int i = 0; i < PIPT; i++) {
         const int64_t row = base + i * PNT + tid;
         if (row >= a.n_probe) continue;
-        if (a.mode == 0) {
+        if (direct) {   // final pairs in place (streamed stores, coalesced across the warp)
+            if (a.idx32) {
+                __stcs((int*)a.out_l + row, m[i] ? (int)left[i] : -1);
+                __stcs((int*)a.out_r + row, (int)row);
+            } else {
+                __stcs((long long*)a.out_l + row, m[i] ? (long long)left[i] : -1ll);
+                __stcs((long long*)a.out_r + row, (long long)row);
+            }
+            cnt += m[i];
+        } else if (a.mode == 0) {
             __stcs(a.lft + row, m[i] ? left[i] : NOMATCH);
             cnt += m[i];
         } else if (a.mode == 2) {
@@ -339,6 +401,140 @@ __global__ void __launch_bounds__(PNT, TQP_PROBE_MINB) probe_kernel(ProbeArgs a)
         uint32_t t = 0;
         for (int w = 0; w < PNW; w++) t += s_w[w];
         a.tcnt[blockIdx.x] = t;
+        if (a.total) atomicAdd(a.total, (unsigned long long)t);
+    }
+}
+
+// One-sector routes (rank bitmap, slot table), straight-line per route: the PIPT probe
+// keys are loaded first (all in flight), then the 32-byte sectors (LDG.256 each) in
+// batches of SECTOR_BATCH, then evaluated. Measured at SF10 (probe ms, full / half
+// match): the per-row probe_one 0.418 / 0.326; batches of 1 / 2 / 4 sectors at the
+// natural register count (3 blocks/SM) 0.437 / 0.441 / 0.476 and 0.298 / 0.335 / 0.428;
+// batch 1 at 6 blocks/SM 0.409 / 0.309 (default); batch 2 at 4 blocks 0.417 / 0.310 --
+// occupancy counts, not per-thread batching. What bounds it is the random 32-byte
+// sector per probe row on top of the stream: a plain read-8 / write-16 bytes per row
+// kernel takes 0.236 ms for the same 60M rows (tools/membench.cu). ROUTE: 0 = rank
+// bitmap, 1 = slots. Same outputs as probe_kernel (join direct / u32 build row, semi, outer).
+#ifndef TQP_SECTOR_BATCH
+#define TQP_SECTOR_BATCH 1
+#endif
+constexpr int SECTOR_BATCH = TQP_SECTOR_BATCH;
+#ifndef TQP_SECTOR_MINB
+#define TQP_SECTOR_MINB 6
+#endif
+template <int PDT, int ROUTE>
+__global__ void __launch_bounds__(PNT, TQP_SECTOR_MINB) probe_sector_kernel(ProbeArgs a) {
+    __shared__ uint32_t s_w[PNW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * PTILE;
+    const bool direct = a.mode == 0 && a.direct && *a.direct == 0;
+    int64_t v[PIPT];
+#pragma unroll
+    for (int i = 0; i < PIPT; i++) {
+        const int64_t row = base + i * PNT + tid;
+        v[i] = row < a.n_probe ? load_probe_key<PDT>(a.probe, row) : 0;
+    }
+    uint32_t rel[PIPT];
+    bool ok[PIPT];
+#pragma unroll
+    for (int i = 0; i < PIPT; i++) {
+        const int64_t row = base + i * PNT + tid;
+        uint32_t r = 0;
+        ok[i] = row < a.n_probe && probe_rel<uint32_t>(a, v[i], r);
+        rel[i] = r;
+    }
+    bool m[PIPT];
+    uint32_t left[PIPT];
+#pragma unroll
+    for (int b = 0; b < PIPT; b += SECTOR_BATCH) {   // SECTOR_BATCH sectors in flight per thread
+        uint32_t w[SECTOR_BATCH][8];
+#pragma unroll
+        for (int ii = 0; ii < SECTOR_BATCH; ii++) {
+            const int i = b + ii;
+            if (ok[i]) {
+                const void* p = ROUTE == 0 ? (const void*)(a.rank_bm + 2 * (int64_t)(rel[i] / RB_BITS))
+                                           : (const void*)(a.slots + (int64_t)(rel[i] >> a.shift) * 8);
+                ld256(p, w[ii]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; j++) w[ii][j] = 0;
+            }
+        }
+#pragma unroll
+        for (int ii = 0; ii < SECTOR_BATCH; ii++) {
+            const int i = b + ii;
+            left[i] = NOMATCH;
+            m[i] = false;
+            if (!ok[i]) continue;
+            if (ROUTE == 0) {
+                m[i] = rank_eval(w[ii], rel[i], left[i]);
+            } else if (!(w[ii][0] >> 31) || w[ii][0] == 0xFFFFFFFFu) {   // records inline (residuals distinct)
+                const uint32_t low = rel[i] & a.lowmask;
+#pragma unroll
+                for (int j = 0; j < 8; j++)
+                    if (!(w[ii][j] >> 31) && (w[ii][j] >> a.pbits) == low) { left[i] = w[ii][j] & ((1u << a.pbits) - 1u); m[i] = true; }
+            } else {   // more than 8 records in the bucket: the bracket + record route
+                m[i] = lookup_packed(a, rel[i], (uint64_t)(rel[i] >> a.shift), left[i]);
+            }
+        }
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int i = 0; i < PIPT; i++) {
+        const int64_t row = base + i * PNT + tid;
+        if (row >= a.n_probe) continue;
+        if (direct) {
+            if (a.idx32) {
+                __stcs((int*)a.out_l + row, m[i] ? (int)left[i] : -1);
+                __stcs((int*)a.out_r + row, (int)row);
+            } else {
+                __stcs((long long*)a.out_l + row, m[i] ? (long long)left[i] : -1ll);
+                __stcs((long long*)a.out_r + row, (long long)row);
+            }
+            cnt += m[i];
+        } else if (a.mode == 0) {
+            __stcs(a.lft + row, m[i] ? left[i] : NOMATCH);
+            cnt += m[i];
+        } else if (a.mode == 2) {
+            __stcs((long long*)a.left64 + row, m[i] ? (long long)left[i] : -1ll);
+            if (a.mask) a.mask[row] = (uint8_t)m[i];
+            cnt += m[i];
+        } else {
+            a.mask[row] = (uint8_t)m[i];
+            cnt += m[i] != (a.anti != 0);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) s_w[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t t = 0;
+        for (int w2 = 0; w2 < PNW; w2++) t += s_w[w2];
+        a.tcnt[blockIdx.x] = t;
+        if (a.total) atomicAdd(a.total, (unsigned long long)t);
+    }
+}
+
+// Direct-output decision: one CTA looks up PSAMPLE probe rows spread over the column;
+// *direct = 1 iff all of them match (the full-match case -- every lineitem row has its
+// order -- writes final pairs in the probe pass and skips the compaction). A wrong guess
+// (a miss outside the sample) costs a host-side compaction afterwards, never a wrong result.
+constexpr int PSAMPLE = 2048;   // one row per thread of PSAMPLE / PNT CTAs
+template <typename KT, int PDT, bool PACKED>
+__global__ void __launch_bounds__(PNT) probe_sample_kernel(ProbeArgs a, int* miss) {
+    const int j = blockIdx.x * PNT + threadIdx.x;
+    const int64_t row = (int64_t)(((__int128)j * a.n_probe) / PSAMPLE);
+    uint32_t l;
+    const bool hit = probe_one<KT, PDT, PACKED>(a, row, l);
+    if (!__syncthreads_and(hit) && threadIdx.x == 0) atomicOr(miss, 1);
+}
+
+// Misprediction fallback of the direct output: the in-place pairs (left = -1 for a miss)
+// back to the per-row u32 build row that emit_kernel compacts.
+__global__ void direct_to_lft_kernel(const void* out_l, int idx32, int64_t n, uint32_t* __restrict__ lft) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t l = idx32 ? (int64_t)((const int*)out_l)[i] : ((const long long*)out_l)[i];
+        lft[i] = l < 0 ? NOMATCH : (uint32_t)l;
     }
 }
 
@@ -483,16 +679,16 @@ __device__ __forceinline__ void copy_elem(const void* src, int dt, int64_t from,
 // join pairs (leftOutputIndex = build row, rightOutputIndex = probe row)
 // or semi/anti rows are staged in shared memory and written coalesced.
 template <bool JOIN>
-__global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ lft, const uint8_t* __restrict__ mask,
-                                                   int anti, int64_t np, const uint64_t* __restrict__ toff,
-                                                   int64_t* left_out, int64_t* right_out, Payload pay) {
+__device__ __forceinline__ void emit_tile(int64_t t, const uint32_t* __restrict__ lft, const uint8_t* __restrict__ mask,
+                                          int anti, int64_t np, const uint64_t* __restrict__ toff, int64_t* left_out,
+                                          int64_t* right_out, const Payload& pay) {
     __shared__ uint32_t s_w[PNW];
     __shared__ uint32_t s_l[PTILE];
     __shared__ uint16_t s_r[PTILE];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t base = (int64_t)blockIdx.x * PTILE;
-    const int64_t excl = (int64_t)toff[blockIdx.x];
-    const uint32_t tot = (uint32_t)(toff[blockIdx.x + 1] - toff[blockIdx.x]);
+    const int64_t base = t * PTILE;
+    const int64_t excl = (int64_t)toff[t];
+    const uint32_t tot = (uint32_t)(toff[t + 1] - toff[t]);
     if (tot == 0) return;
     const int64_t r0 = base + (int64_t)tid * PIPT;
     const bool full = base + PTILE <= np;
@@ -559,6 +755,21 @@ __global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ 
     }
 }
 
+// Persistent over the tiles (grid = resident CTAs): when the probe wrote the pairs
+// directly (*direct set), every CTA exits at once instead of ~n/2048 of them.
+template <bool JOIN>
+__global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ lft, const uint8_t* __restrict__ mask,
+                                                   int anti, int64_t np, const uint64_t* __restrict__ toff,
+                                                   int64_t* left_out, int64_t* right_out, Payload pay,
+                                                   const int* direct) {
+    if (direct && *direct == 0) return;
+    const int64_t tiles = (np + PTILE - 1) / PTILE;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        emit_tile<JOIN>(t, lft, mask, anti, np, toff, left_out, right_out, pay);
+        __syncthreads();   // the staging buffers are reused by the next tile
+    }
+}
+
 struct Built {
     SortOut so;
     DevBuf<uint32_t> TR;      // bracket table T, then (packed) the records, one allocation
@@ -574,8 +785,12 @@ struct Built {
     DevBuf<uint32_t> rank_bm;   // presorted build side: rank bitmap (then T / records are unused)
 };
 
-void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
+// allow_rank = false: never the rank bitmap (its build row = rank + popcount of the
+// distinct keys below is only right without duplicate build keys; the outer join, which
+// tolerates duplicates, rebuilds without it when the duplicate flag is set).
+void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allow_rank = true) {
     B.so.want_internal = true;
+    B.so.defer_identity = true;   // a presorted build side may take the rank bitmap straight from the keys
     radix_sort(ctx, bk.data, bk.dtype, nb, false, B.so);
     B.dup.alloc(ctx, 1);
     B.dup.zero();
@@ -615,20 +830,19 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
         const char* e = std::getenv("TQP_PKFK_NO_RANK");
         return e && std::atoi(e) != 0;
     }();
-    if (B.so.identity && B.so.k32 && vbits > 0 && !no_rank) {
+    if (B.so.identity && B.so.k32 && vbits > 0 && !no_rank && allow_rank) {
         const int64_t nblk = (int64_t)(((uint64_t(1) << vbits) + RB_BITS - 1) / RB_BITS);
         if (nblk * 32 <= 8 * nb + (int64_t(1) << 20)) {
             B.rank_bm.alloc(ctx, nblk * 8);
             B.rank_bm.zero();
             const int g = (int)std::min<int64_t>(ceil_div(nb, 256), (int64_t)ctx->num_sms * 8);
-            launch(ctx, "tqp_pkfk_rank_bitmap", rank_bitmap_kernel, dim3(g), dim3(256), 0,
-                   (const uint32_t*)B.so.keys32.get(), nb, (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get());
-            ctx->add_bytes("tqp_pkfk_rank_bitmap", 4.0 * (double)nb + 32.0 * (double)nblk);
-            B.so.keys32.release();
-            B.so.perm32.release();
+            launch(ctx, "tqp_pkfk_rank_bitmap", rank_bitmap_kernel, dim3(g), dim3(256), 0, bk.data, (int)bk.dtype, nb,
+                   (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get());
+            ctx->add_bytes("tqp_pkfk_rank_bitmap", (double)dtype_size(bk.dtype) * (double)nb + 32.0 * (double)nblk);
             return;
         }
     }
+    if (B.so.identity) sort_materialize_identity(ctx, bk.data, bk.dtype, nb, false, B.so);
     const int64_t nbk = int64_t(1) << Bbits;
     DevBuf<uint32_t> H(ctx, nbk + 1);
     H.zero();
@@ -671,9 +885,11 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B) {
 
 void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, int anti, int64_t* left_out,
                int64_t* right_out, uint8_t* match_out, int64_t* n_out_host, const Payload* pay = nullptr) {
-    DevBuf<int64_t> pack(ctx, 2);   // [0] selected rows, [1] duplicate-build-key flag: one readback
+    // [0] selected rows, [1] duplicate-build-key flag, [2] direct-output flag: one readback
+    DevBuf<int64_t> pack(ctx, 3);
     pack.zero();
     const int64_t nb = B.nb;
+    bool direct_capable = false;
     if (np > 0 && nb > 0) {
         const int64_t tiles = ceil_div(np, PTILE);
         DevBuf<uint32_t> tcnt(ctx, tiles);
@@ -706,6 +922,21 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         auto go = [&](auto kt, auto pk_) {
             using KT = decltype(kt);
             constexpr bool PK = decltype(pk_)::value;
+            if constexpr (sizeof(KT) == 4) {
+                const int route = a.rank_bm ? 0 : ((PK && a.slots) ? 1 : -1);
+                if (route >= 0) {
+                    auto gr = [&](auto rc) {
+                        constexpr int R = decltype(rc)::value;
+                        switch (pk.dtype) {
+                            case TQP_I64: launch(ctx, "tqp_pkfk_probe", probe_sector_kernel<TQP_I64, R>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                            case TQP_I32: launch(ctx, "tqp_pkfk_probe", probe_sector_kernel<TQP_I32, R>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                            default: launch(ctx, "tqp_pkfk_probe", probe_sector_kernel<TQP_U8, R>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
+                        }
+                    };
+                    if (route == 0) gr(std::integral_constant<int, 0>{}); else gr(std::integral_constant<int, 1>{});
+                    return;
+                }
+            }
             switch (pk.dtype) {
                 case TQP_I64: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_I64, PK>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
                 case TQP_I32: launch(ctx, "tqp_pkfk_probe", probe_kernel<KT, TQP_I32, PK>, dim3((unsigned)tiles), dim3(PNT), 0, a); break;
@@ -720,6 +951,30 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         int passes = 1;
         if (mode == 0 && B.packed && !B.slots.get() && !B.rank_bm.get() && B.vbits <= 30 && np >= nb && slice_mb > 0)
             passes = (int)std::min<double>(64.0, std::ceil((double)B.tr_bytes / (slice_mb * 1048576.0)));
+        // direct output: plain index pairs (no payload columns), single-pass probe
+        direct_capable = mode == 0 && passes == 1 && left_out && right_out && (!pay || (pay->nb == 0 && pay->np == 0));
+        int* dflag = reinterpret_cast<int*>(pack.get() + 2);
+        if (direct_capable) {
+            a.direct = dflag;
+            a.total = reinterpret_cast<unsigned long long*>(pack.get());
+            a.out_l = left_out;
+            a.out_r = right_out;
+            a.idx32 = pay ? pay->idx32 : 0;
+            auto gs = [&](auto kt, auto pk_) {
+                using KT = decltype(kt);
+                constexpr bool PK = decltype(pk_)::value;
+                switch (pk.dtype) {
+                    case TQP_I64: launch(ctx, "tqp_pkfk_sample", probe_sample_kernel<KT, TQP_I64, PK>, dim3(PSAMPLE / PNT), dim3(PNT), 0, a, dflag); break;
+                    case TQP_I32: launch(ctx, "tqp_pkfk_sample", probe_sample_kernel<KT, TQP_I32, PK>, dim3(PSAMPLE / PNT), dim3(PNT), 0, a, dflag); break;
+                    default: launch(ctx, "tqp_pkfk_sample", probe_sample_kernel<KT, TQP_U8, PK>, dim3(PSAMPLE / PNT), dim3(PNT), 0, a, dflag); break;
+                }
+            };
+            if (B.so.k32) {
+                if (B.packed) gs(uint32_t{}, std::true_type{}); else gs(uint32_t{}, std::false_type{});
+            } else {
+                if (B.packed) gs(uint64_t{}, std::true_type{}); else gs(uint64_t{}, std::false_type{});
+            }
+        }
         if (passes > 1) {
             const uint64_t nbk = uint64_t(1) << (B.vbits - B.shift);
             auto gp = [&](auto kt, auto first, auto last) {
@@ -747,15 +1002,43 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         } else {
             if (B.packed) go(uint64_t{}, std::true_type{}); else go(uint64_t{}, std::false_type{});
         }
+        const int egrid = (int)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occupancy(emit_kernel<true>, PNT, 0), 1));
+        if (direct_capable) {
+            // one readback decides: every row matched in the direct layout -> done (no scan,
+            // no compaction); else scan the tile counts and compact (after a mispredicted
+            // direct layout, from the in-place pairs)
+            int64_t h[3];
+            if (B.dup.get()) TQP_CUDA(cudaMemcpyAsync(pack.get() + 1, B.dup.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            read_back(ctx, h, pack.get(), 24);
+            if (h[1]) fail(TQP_ERR_DUPLICATE_BUILD_KEY, "pkfk: duplicate key on the build side");
+            const bool direct = (int)h[2] == 0;
+            const double ib = a.idx32 ? 4.0 : 8.0;
+            if (!direct || h[0] < np) {
+                scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
+                if (direct) {
+                    const int g = (int)std::min<int64_t>(ceil_div(np, 256), (int64_t)ctx->num_sms * 8);
+                    launch(ctx, "tqp_pkfk_emit", direct_to_lft_kernel, dim3(g), dim3(256), 0, (const void*)left_out,
+                           a.idx32, np, lft.get());
+                    ctx->add_bytes("tqp_pkfk_emit", (ib + 4.0) * (double)np);
+                }
+                launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)egrid), dim3(PNT), 0,
+                       (const uint32_t*)lft.get(), (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out,
+                       right_out, pay ? *pay : Payload{}, (const int*)nullptr);
+                ctx->add_bytes("tqp_pkfk_emit", 2.0 * ib * (double)h[0]);
+            }
+            if (n_out_host) *n_out_host = h[0];
+            ctx->add_bytes("tqp_pkfk_probe", (double)np * dtype_size(pk.dtype) + (direct ? 2.0 * ib * (double)np : 0.0));
+            return;
+        }
         scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
         if (mode == 0)
-            launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)lft.get(),
+            launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)egrid), dim3(PNT), 0, (const uint32_t*)lft.get(),
                    (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out,
-                   pay ? *pay : Payload{});
+                   pay ? *pay : Payload{}, (const int*)nullptr);
         else if (mode == 1 && right_out)
-            launch(ctx, "tqp_pkfk_emit", emit_kernel<false>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)nullptr,
+            launch(ctx, "tqp_pkfk_emit", emit_kernel<false>, dim3((unsigned)egrid), dim3(PNT), 0, (const uint32_t*)nullptr,
                    (const uint8_t*)a.mask, anti, np, (const uint64_t*)toff.get(), (int64_t*)nullptr, right_out,
-                   Payload{});
+                   Payload{}, (const int*)nullptr);
         TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
     } else if (np > 0 && mode == 2) {
         // empty build side: no probe row matches
@@ -772,8 +1055,8 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         }
     }
     if (B.dup.get()) TQP_CUDA(cudaMemcpyAsync(pack.get() + 1, B.dup.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
-    int64_t h[2];
-    read_back(ctx, h, pack.get(), 16);
+    int64_t h[3];
+    read_back(ctx, h, pack.get(), 24);
     if (h[1] && mode == 0) fail(TQP_ERR_DUPLICATE_BUILD_KEY, "pkfk: duplicate key on the build side");
     if (n_out_host) *n_out_host = h[0];
     if (np > 0 && nb > 0) {   // probe keys in; pairs (join) or mask + selection vector (semi) out
@@ -904,8 +1187,10 @@ void pkfk_join_hash(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np
             default: launch(ctx, "tqp_hash_probe", hash_probe_kernel<TQP_U8>, dim3((unsigned)tiles), dim3(PNT), 0, pk.data, np, mask, (const uint4*)slots.get(), lft.get(), tcnt.get()); break;
         }
         scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
-        launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)tiles), dim3(PNT), 0, (const uint32_t*)lft.get(),
-               (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out, Payload{});
+        const int egrid = (int)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occupancy(emit_kernel<true>, PNT, 0), 1));
+        launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)egrid), dim3(PNT), 0, (const uint32_t*)lft.get(),
+               (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out, Payload{},
+               (const int*)nullptr);
         TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
         ctx->add_bytes("tqp_hash_probe", (double)np * dtype_size(pk.dtype));
     }
@@ -1026,6 +1311,14 @@ void pkfk_outer(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, in
     if (np >= (int64_t(1) << 40)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_outer: probe too large");
     Built B;
     build_side(ctx, bk, nb, B);
+    if (B.rank_bm.get()) {   // a presorted build side with duplicate keys: rank + popcount would be wrong
+        int dup = 0;
+        read_back(ctx, &dup, B.dup.get(), 4);
+        if (dup) {
+            B = Built();
+            build_side(ctx, bk, nb, B, false);
+        }
+    }
     int64_t m = 0;
     run_probe(ctx, B, pk, np, 2, 0, left_out, nullptr, match_out, &m);
     if (n_match_host) *n_match_host = m;

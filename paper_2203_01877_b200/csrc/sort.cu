@@ -818,6 +818,30 @@ void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
 
 size_t sort_hist0_words(int64_t n) { return (size_t)ceil_div(n, H0_TILE) * H0_BINS; }
 
+void sort_materialize_identity(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o) {
+        const int mode = in_mode(dtype);
+        if (o.want_internal || o.want_perm32) o.perm32.alloc(ctx, n);
+        if (o.want_internal) {
+            if (o.k32) o.keys32.alloc(ctx, n); else o.keys64.alloc(ctx, n);
+        }
+        const int g = (int)std::min<int64_t>(ceil_div(n, NT), (int64_t)ctx->num_sms * 8);
+        ctx->add_bytes("tqp_sort_trivial",
+                       (double)n * (dtype_size(dtype) + (o.sorted_orig ? dtype_size(dtype) : 0) + (o.perm64 ? 8 : 0) +
+                                    (o.sorted_u ? 8 : 0) + (o.perm32.n ? 4 : 0) + (o.want_internal ? (o.k32 ? 4 : 8) : 0)));
+        dispatch_in(mode, [&](auto m) {
+            if constexpr (decltype(m)::value != IN_INTERNAL) {
+                if (o.k32)
+                    launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint32_t, decltype(m)::value>, dim3(g),
+                           dim3(NT), 0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys32.get(),
+                           o.perm32.get());
+                else
+                    launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint64_t, decltype(m)::value>, dim3(g),
+                           dim3(NT), 0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys64.get(),
+                           o.perm32.get());
+            }
+        });
+}
+
 void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o, const uint64_t* andor,
                 uint32_t* th0) {
     if (n < 0 || n >= (int64_t(1) << 30)) fail(TQP_ERR_INVALID_ARGUMENT, "sort: n must be in [0, 2^30)");
@@ -863,26 +887,8 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     if (P > 0 && h[2] == 0 && n >= 2 && mode != IN_INTERNAL && !force_radix()) P = 0;
     if (P == 0) {
         o.identity = true;
-        if (o.want_internal || o.want_perm32) o.perm32.alloc(ctx, n);
-        if (o.want_internal) {
-            if (o.k32) o.keys32.alloc(ctx, n); else o.keys64.alloc(ctx, n);
-        }
-        const int g = (int)std::min<int64_t>(ceil_div(n, NT), (int64_t)ctx->num_sms * 8);
-        ctx->add_bytes("tqp_sort_trivial",
-                       (double)n * (dtype_size(dtype) + (o.sorted_orig ? dtype_size(dtype) : 0) + (o.perm64 ? 8 : 0) +
-                                    (o.sorted_u ? 8 : 0) + (o.perm32.n ? 4 : 0) + (o.want_internal ? (o.k32 ? 4 : 8) : 0)));
-        dispatch_in(mode, [&](auto m) {
-            if constexpr (decltype(m)::value != IN_INTERNAL) {
-                if (o.k32)
-                    launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint32_t, decltype(m)::value>, dim3(g),
-                           dim3(NT), 0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys32.get(),
-                           o.perm32.get());
-                else
-                    launch(ctx, "tqp_sort_trivial", trivial_sort_kernel<uint64_t, decltype(m)::value>, dim3(g),
-                           dim3(NT), 0, keys, n, desc, dtype, o.sorted_orig, o.perm64, o.sorted_u, o.keys64.get(),
-                           o.perm32.get());
-            }
-        });
+        if (o.defer_identity) return;
+        sort_materialize_identity(ctx, keys, dtype, n, desc, o);
         return;
     }
     if (o.k32) {

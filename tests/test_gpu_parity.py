@@ -372,6 +372,28 @@ def test_pkfk_outer(T, nb, np_, span):
     assert np.array_equal(npy(mask).astype(bool), want >= 0)
 
 
+@pytest.mark.parametrize("presorted", [True, False])
+def test_pkfk_outer_duplicate_build_keys(T, presorted):
+    """Outer join over a build side with duplicate keys (not an error for the outer join):
+    each probe row takes a build row with its key, or -1. A presorted build side is the
+    rank-bitmap route, whose rank + popcount row would be wrong with duplicates (ADVICE r01:
+    [5,5,6] probed with 6 gave row 1), so it must be rebuilt without it."""
+    rng = np.random.default_rng(11)
+    build = rng.integers(0, 50_000, 200_003).astype(np.int64)
+    build[:3] = [5, 5, 6]
+    if presorted:
+        build = np.sort(build)
+    probe = rng.integers(-100, 51_000, 300_001).astype(np.int64)
+    probe[:2] = [6, 5]
+    left, mask = T.pkfk_outer(cu(build), cu(probe), return_mask=True)
+    left = npy(left)
+    members = set(build.tolist())
+    want_match = np.array([p in members for p in probe.tolist()])
+    assert np.array_equal(npy(mask).astype(bool), want_match)
+    assert np.array_equal(left >= 0, want_match)
+    assert np.array_equal(build[left[want_match]], probe[want_match])   # a build row with the probe key
+
+
 def test_pkfk_semi_empty_build(T):
     sel = T.pkfk_semi(cu(np.array([], np.int64)), cu(np.arange(10)), anti=True)
     assert npy(sel).tolist() == list(range(10))
@@ -827,6 +849,25 @@ def test_groupby_dense_path(T, card, wide, monkeypatch):
     ctx.set_profiling(False)
     check_groupby(T, got, want, aggs)
     assert "tqp_groupby_dense" not in st
+
+
+@pytest.mark.parametrize("where", ["first_unsampled", "middle", "last_row"])
+def test_groupby_dense_sampled_presence_miss(T, where):
+    """The dense path takes key presence from a sample of 16-row groups (n > 2^21 rows here,
+    so every 3rd group); keys that occur only in unsampled rows are flagged by the dense
+    kernel and the presence pass is redone over every row, so no group is lost."""
+    rng = np.random.default_rng(21)
+    n = 4_000_003
+    k = rng.integers(0, 2, n).astype(np.uint8) * 3 + 65
+    row = {"first_unsampled": 19, "middle": 2_000_037, "last_row": n - 1}[where]
+    k[row] = 90                                  # a group of one row, outside the sample
+    k[row + 16 * 4 if row + 64 < n else 0] = 91  # another key in a different (unsampled) group
+    v = rng.integers(-10**6, 10**6, n)
+    aggs = [("sum", [(1, 0, 1)]), ("count", []), ("max", [(1, 0, 1)])]
+    got = T.groupby_agg([cu(k, torch.uint8), cu(v)], [0], aggs)
+    want = oracle.groupby_agg([k, v], [0], aggs)
+    check_groupby(T, got, want, aggs)
+    assert got["n_groups"] == 4
 
 
 @pytest.mark.parametrize("seed", range(6))

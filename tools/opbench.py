@@ -24,7 +24,12 @@ def main():
     q1, q6 = columns(li, Q1_COLS), columns(li, Q6_COLS)
     lk32 = lk.to(torch.int32)
     ctx = T.context()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    ok_shuf = ok[torch.randperm(ok.numel(), device="cuda", generator=g)]   # general route (slot table)
+    ok_half = ok[::2].contiguous()                                           # ~50 % of probe rows match
     ops = {
+        "pkfk_join_shuffled_build": lambda: ctx.pkfk_join(ok_shuf, lk),
+        "pkfk_join_half_match": lambda: ctx.pkfk_join(ok_half, lk),
         "sort_build": lambda: ctx.sort(ok),
         "sort_probe": lambda: ctx.sort(lk),
         "cub_sort_probe_i64": lambda: torch.sort(lk, stable=True),
