@@ -34,6 +34,21 @@ def orders_count(sf: float) -> int:
     return int(round(1_500_000 * sf))
 
 
+def orderkey(i):
+    """o_orderkey of global orders row i (TPC-H's sparse keys: 8 of every 32 values)."""
+    return (i // 8) * 32 + (i % 8) + 1
+
+
+def spread_orderkeys(l_parent, rank: int, world: int):
+    """Shuffled multi-rank layout: re-parent a rank's lineitem slice so
+    its rows' orders are spread over every rank's orders slice. Local parent j of rank
+    `rank` becomes global orders row j * world + rank (a bijection onto the orders rows of
+    all ranks, each rank owning a contiguous range of them). Returns (l_orderkey, global
+    parent row)."""
+    g = l_parent * world + rank
+    return orderkey(g), g
+
+
 def tpch_orders_lineitem(sf: float, seed: int = 42, device="cpu", layout: str = "shuffled",
                          order_range=None):
     """Generate orders and lineitem for scale factor `sf`.
@@ -49,7 +64,7 @@ def tpch_orders_lineitem(sf: float, seed: int = 42, device="cpu", layout: str = 
     dev = torch.device(device)
     i = torch.arange(lo, hi, dtype=torch.int64, device=dev)
 
-    o_orderkey = (i // 8) * 32 + (i % 8) + 1
+    o_orderkey = orderkey(i)
     o_orderdate = rand_uniform_int(seed, _S_ODATE, i, DAYS["1992-01-01"], DAYS["1998-08-02"])
     nlines = rand_uniform_int(seed, _S_NLINES, i, 1, 7)
 

@@ -209,6 +209,18 @@ tqp_status tqp_smj_expand_i32(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t be
  * 3 x uint64 host array. Synchronises once. */
 tqp_status tqp_smj_expand_checksum(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin, int64_t end,
                                    uint64_t* out_host);
+/* createOutput fused into the expansion (Alg. 1's return, PAPER.md:333;
+ * SURVEY.md §8(f) NEXT 2): for the pairs (l_j, r_j) of output positions j in
+ * [begin, end), left_payload_out[c][j - begin] = left_payload[c][l_j] and
+ * right_payload_out[c][j - begin] = right_payload[c][r_j]. Payload columns are
+ * device columns of the left (n_left rows) / right (n_right rows) relation, any
+ * dtype (u8 / i32 / i64 / f64), at most 8 per side (host arrays of columns and of
+ * device output pointers, each output end - begin elements of its column's dtype).
+ * left_out_idx / right_out_idx (nullable) also receive the index pairs. Asynchronous. */
+tqp_status tqp_smj_expand_payload(tqp_ctx* ctx, const tqp_smj_plan* plan, int64_t begin, int64_t end,
+                                  const tqp_col* left_payload_host, int n_left_payload, void* const* left_payload_out_host,
+                                  const tqp_col* right_payload_host, int n_right_payload,
+                                  void* const* right_payload_out_host, int64_t* left_out_idx, int64_t* right_out_idx);
 void tqp_smj_release(tqp_ctx* ctx, tqp_smj_plan* plan);
 /* prepare + expand of everything into caller buffers of `capacity` pairs.
  * If capacity < outSize: TQP_ERR_CAPACITY and *n_out_host = outSize. */
@@ -316,6 +328,33 @@ tqp_status tqp_groupby_agg(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols, i
                            const int32_t* key_idx_host, int n_keys, const tqp_pred* preds_host, int n_preds,
                            const tqp_agg* aggs_host, int n_aggs, void* const* keys_out_host,
                            void* const* results_out_host, int64_t capacity, int64_t* n_groups_host);
+
+/* ------------------------------------------- data-parallel exchange steps */
+/* Multi-GPU execution (the paper names data-parallel execution as
+ * future work): one process per GPU exchanges (key, global row)
+ * pairs with NCCL all_to_all. These calls are the on-GPU steps around that
+ * collective; none synchronises with the host.
+ *
+ * Stable partition by key range. dest(k) = the number of splitters <= k
+ * (splitters: device, n_parts - 1 sorted int64; keys compare as signed int64).
+ * keys_out (device, n elements of the key dtype) receives the keys grouped by
+ * destination 0..n_parts-1, in input order within a destination; rows_out
+ * (device int64, nullable) the matching row_base + input row; counts_out (device
+ * int64, n_parts) the rows per destination -- the send buffer and split sizes
+ * of one all_to_all_single. 1 <= n_parts <= 256; keys u8 / i32 / i64. */
+tqp_status tqp_partition(tqp_ctx* ctx, tqp_col keys, int64_t n, const int64_t* splitters, int n_parts,
+                         int64_t row_base, void* keys_out, int64_t* rows_out, int64_t* counts_out);
+/* lohi_out (device, 2 x int64) = [min, max] of the key column; an empty column
+ * gives [INT64_MAX, INT64_MIN] (so MIN / MAX all-reduces across ranks ignore it). */
+tqp_status tqp_minmax(tqp_ctx* ctx, tqp_col keys, int64_t n, int64_t* lohi_out);
+/* Equal-width key ranges from a device [lo, hi] (e.g. all-reduced tqp_minmax):
+ * width = (hi - lo) / n_parts + 1, splitters_out[j] = lo + (j + 1) * width
+ * (saturating at INT64_MAX), j < n_parts - 1: key k goes to (k - lo) / width. */
+tqp_status tqp_range_splitters(tqp_ctx* ctx, const int64_t* lohi, int n_parts, int64_t* splitters_out);
+/* out[i] = src[idx[i]] for i < n (device; src any column dtype, out the same
+ * dtype; idx device int64 in [0, len(src))). The row mapping of createOutput
+ * (PAPER.md:333): join indices into received blocks -> global row numbers. */
+tqp_status tqp_gather(tqp_ctx* ctx, tqp_col src, const int64_t* idx, int64_t n, void* out);
 
 #ifdef __cplusplus
 }

@@ -40,7 +40,8 @@ EXPORTED = [
     "tqp_pkfk_join_i32", "tqp_pkfk_join_paper_order", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_expand_i32", "tqp_smj_expand_checksum",
     "tqp_smj_release",
     "tqp_smj_join", "tqp_pack_keys", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
-    "tqp_groupby_agg", "tqp_groupby_merge",
+    "tqp_groupby_agg", "tqp_groupby_merge", "tqp_smj_expand_payload", "tqp_partition", "tqp_minmax",
+    "tqp_range_splitters", "tqp_gather",
 ]
 
 
@@ -86,6 +87,11 @@ _sig = {
     "tqp_smj_expand_i32": ([_vp, _vp, _i64, _i64, _vp, _vp], _int),
     "tqp_smj_expand_checksum": ([_vp, _vp, _i64, _i64, _P(ctypes.c_uint64)], _int),
     "tqp_smj_release": ([_vp, _vp], None),
+    "tqp_smj_expand_payload": ([_vp, _vp, _i64, _i64, _P(Col), _int, _P(_vp), _P(Col), _int, _P(_vp), _vp, _vp], _int),
+    "tqp_partition": ([_vp, Col, _i64, _vp, _int, _i64, _vp, _vp, _vp], _int),
+    "tqp_minmax": ([_vp, Col, _i64, _vp], _int),
+    "tqp_range_splitters": ([_vp, _vp, _int, _vp], _int),
+    "tqp_gather": ([_vp, Col, _vp, _i64, _vp], _int),
     "tqp_smj_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _i64, _P(_i64)], _int),
     "tqp_filter_compact": ([_vp, _P(Col), _int, _i64, _P(Pred), _int, _vp, _vp, _P(_i64)], _int),
     "tqp_groupby_prepare": ([_vp, _P(Col), _int, _i64, _P(ctypes.c_int32), _int, _P(Pred), _int, _P(Agg), _int,
@@ -342,6 +348,59 @@ class Context:
         finally:
             plan.release()
 
+    def smj_join_payload(self, left, right, left_payload=(), right_payload=(), indices=False):
+        """Alg. 1 with createOutput fused: the pairs' payload columns gathered
+        in (key, l, r) order -> (left payload outputs, right payload outputs, (l, r) or None)."""
+        plan = self.smj_prepare(left, right)
+        try:
+            return plan.expand_payload(0, plan.size, left_payload, right_payload, indices)
+        finally:
+            plan.release()
+
+    # ------------------------------------------------ data-parallel exchange steps
+    def partition(self, keys, splitters, row_base=0, rows=True):
+        """Stable partition by key range (tqp_partition): dest = #splitters <= key. Returns
+        (keys grouped by destination, their row_base + input row (int64) or None, device
+        int64 counts per destination). No host sync."""
+        self._sync_stream()
+        k = _dev_tensor(keys, self.device)
+        spl = _dev_tensor(torch.as_tensor(splitters, dtype=torch.int64) if not isinstance(splitters, torch.Tensor)
+                          else splitters.to(torch.int64), self.device)
+        parts = spl.numel() + 1
+        ko = torch.empty_like(k)
+        ro = torch.empty(k.numel(), dtype=torch.int64, device=self.device) if rows else None
+        counts = torch.empty(parts, dtype=torch.int64, device=self.device)
+        self._check(_lib.tqp_partition(self._h, _col(k), k.numel(), _ptr(spl), parts, int(row_base), _ptr(ko), _ptr(ro),
+                                       _ptr(counts)))
+        return ko, ro, counts
+
+    def minmax(self, keys):
+        """Device int64 [min, max] of a key column ([INT64_MAX, INT64_MIN] when empty). No host sync."""
+        self._sync_stream()
+        k = _dev_tensor(keys, self.device)
+        out = torch.empty(2, dtype=torch.int64, device=self.device)
+        self._check(_lib.tqp_minmax(self._h, _col(k), k.numel(), _ptr(out)))
+        return out
+
+    def range_splitters(self, lohi, parts):
+        """parts - 1 equal-width splitters over a device [lo, hi] (tqp_range_splitters)."""
+        self._sync_stream()
+        lh = _dev_tensor(lohi, self.device).to(torch.int64).contiguous()
+        out = torch.empty(max(parts - 1, 0), dtype=torch.int64, device=self.device)
+        self._check(_lib.tqp_range_splitters(self._h, _ptr(lh), int(parts), _ptr(out)))
+        return out
+
+    def gather(self, src, idx):
+        """out[i] = src[idx[i]] (tqp_gather; idx int64 on the device)."""
+        self._sync_stream()
+        s = _dev_tensor(src, self.device)
+        i = _dev_tensor(idx, self.device)
+        if i.dtype != torch.int64:
+            raise TypeError("gather: idx must be int64")
+        out = torch.empty(i.numel(), dtype=s.dtype, device=self.device)
+        self._check(_lib.tqp_gather(self._h, _col(s), _ptr(i), i.numel(), _ptr(out)))
+        return out
+
     def filter_compact(self, cols, preds, mask=True, sel=True):
         """Listing 1 bitmap and/or Listing 2 selection vector -> (mask u8 | None, sel int64 | None)."""
         self._sync_stream()
@@ -453,6 +512,26 @@ class SmjPlan:
         self.ctx._check(fn(self.ctx._h, self._h, begin, end, _ptr(lo), _ptr(ro)))
         return lo, ro
 
+    def expand_payload(self, begin, end, left_payload=(), right_payload=(), indices=False):
+        """Payload columns gathered by the pairs of [begin, end) (tqp_smj_expand_payload) ->
+        (left outputs, right outputs, (l, r) or None)."""
+        c = self.ctx
+        c._sync_stream()
+        lps = [_dev_tensor(t, c.device) for t in left_payload]
+        rps = [_dev_tensor(t, c.device) for t in right_payload]
+        m = end - begin
+        louts = [torch.empty(m, dtype=t.dtype, device=c.device) for t in lps]
+        routs = [torch.empty(m, dtype=t.dtype, device=c.device) for t in rps]
+        lo = torch.empty(m, dtype=torch.int64, device=c.device) if indices else None
+        ro = torch.empty(m, dtype=torch.int64, device=c.device) if indices else None
+        la = (Col * max(len(lps), 1))(*[_col(t) for t in lps])
+        ra = (Col * max(len(rps), 1))(*[_col(t) for t in rps])
+        lo_p = (_vp * max(len(louts), 1))(*[t.data_ptr() for t in louts])
+        ro_p = (_vp * max(len(routs), 1))(*[t.data_ptr() for t in routs])
+        c._check(_lib.tqp_smj_expand_payload(c._h, self._h, begin, end, la, len(lps), lo_p, ra, len(rps), ro_p,
+                                             _ptr(lo), _ptr(ro)))
+        return louts, routs, ((lo, ro) if indices else None)
+
     def checksum(self, begin, end):
         """Fused consumer over pairs [begin, end) without materialising them:
         (sum_j mix64(mix64((l_j << 32) | r_j) ^ j), sum_j l_j, sum_j r_j), all mod 2^64."""
@@ -549,6 +628,26 @@ def pkfk_join_hash(build_keys, probe_keys):
 
 def pkfk_outer(build_keys, probe_keys, return_mask=False):
     return context().pkfk_outer(build_keys, probe_keys, return_mask)
+
+
+def smj_join_payload(left, right, left_payload=(), right_payload=(), indices=False):
+    return context().smj_join_payload(left, right, left_payload, right_payload, indices)
+
+
+def partition(keys, splitters, row_base=0, rows=True):
+    return context().partition(keys, splitters, row_base, rows)
+
+
+def minmax(keys):
+    return context().minmax(keys)
+
+
+def range_splitters(lohi, parts):
+    return context().range_splitters(lohi, parts)
+
+
+def gather(src, idx):
+    return context().gather(src, idx)
 
 
 def filter_compact(cols, preds, mask=True, sel=True):

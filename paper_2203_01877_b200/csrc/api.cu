@@ -27,6 +27,12 @@ void groupby_fetch(tqp_ctx*, const tqp_groupby_plan*, void* const*, void* const*
 void groupby_release(tqp_ctx*, tqp_groupby_plan*);
 tqp_groupby_plan* groupby_merge(tqp_ctx*, int64_t, const tqp_col*, int, const tqp_agg*, int, const void* const*,
                                 const int64_t*, int64_t*);
+void smj_expand_payload(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, const tqp_col*, int, void* const*,
+                        const tqp_col*, int, void* const*, int64_t*, int64_t*);
+void partition(tqp_ctx*, tqp_col, int64_t, const int64_t*, int, int64_t, void*, int64_t*, int64_t*);
+void minmax(tqp_ctx*, tqp_col, int64_t, int64_t*);
+void range_splitters(tqp_ctx*, const int64_t*, int, int64_t*);
+void gather(tqp_ctx*, tqp_col, const int64_t*, int64_t, void*);
 }  // namespace tqp
 
 static_assert(sizeof(tqp_col) == 16, "tqp_col layout");
@@ -413,6 +419,37 @@ tqp_status tqp_groupby_agg(tqp_ctx* c, const tqp_col* cols, int n_cols, int64_t 
         }
         tqp::groupby_release(c, P);
     });
+}
+
+tqp_status tqp_smj_expand_payload(tqp_ctx* c, const tqp_smj_plan* plan, int64_t begin, int64_t end,
+                                  const tqp_col* left_payload, int n_left_payload, void* const* left_payload_out,
+                                  const tqp_col* right_payload, int n_right_payload, void* const* right_payload_out,
+                                  int64_t* left_out_idx, int64_t* right_out_idx) {
+    TQP_GUARD(c, {
+        if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_payload: null plan");
+        if ((n_left_payload && (!left_payload || !left_payload_out)) ||
+            (n_right_payload && (!right_payload || !right_payload_out)))
+            tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_payload: null payload array");
+        tqp::smj_expand_payload(c, plan, begin, end, left_payload, n_left_payload, left_payload_out, right_payload,
+                                n_right_payload, right_payload_out, left_out_idx, right_out_idx);
+    });
+}
+
+tqp_status tqp_partition(tqp_ctx* c, tqp_col keys, int64_t n, const int64_t* splitters, int n_parts, int64_t row_base,
+                         void* keys_out, int64_t* rows_out, int64_t* counts_out) {
+    TQP_GUARD(c, { tqp::partition(c, keys, n, splitters, n_parts, row_base, keys_out, rows_out, counts_out); });
+}
+
+tqp_status tqp_minmax(tqp_ctx* c, tqp_col keys, int64_t n, int64_t* lohi_out) {
+    TQP_GUARD(c, { tqp::minmax(c, keys, n, lohi_out); });
+}
+
+tqp_status tqp_range_splitters(tqp_ctx* c, const int64_t* lohi, int n_parts, int64_t* splitters_out) {
+    TQP_GUARD(c, { tqp::range_splitters(c, lohi, n_parts, splitters_out); });
+}
+
+tqp_status tqp_gather(tqp_ctx* c, tqp_col src, const int64_t* idx, int64_t n, void* out) {
+    TQP_GUARD(c, { tqp::gather(c, src, idx, n, out); });
 }
 
 }  // extern "C"

@@ -471,7 +471,28 @@ __global__ void ck_final_kernel(const unsigned long long* __restrict__ slots, un
     }
 }
 
-template <bool CK>
+// createOutput fused into the expansion (Alg. 1's return; SURVEY §8(f) NEXT
+// 2): payload columns gathered by the pairs' left / right rows as they are written.
+constexpr int SMJ_MAXPAY = 8;
+struct SmjPayload {
+    int nl, nr;
+    const void* lsrc[SMJ_MAXPAY];
+    int ldt[SMJ_MAXPAY];
+    void* ldst[SMJ_MAXPAY];
+    const void* rsrc[SMJ_MAXPAY];
+    int rdt[SMJ_MAXPAY];
+    void* rdst[SMJ_MAXPAY];
+};
+
+__device__ __forceinline__ void pay_copy(const void* src, int dt, int64_t from, void* dst, int64_t to) {
+    switch (dt) {
+        case TQP_U8: static_cast<uint8_t*>(dst)[to] = __ldg(static_cast<const uint8_t*>(src) + from); break;
+        case TQP_I32: __stcs(static_cast<int*>(dst) + to, __ldg(static_cast<const int*>(src) + from)); break;
+        default: __stcs(static_cast<long long*>(dst) + to, __ldg(static_cast<const long long*>(src) + from));
+    }
+}
+
+template <bool CK, bool PAY = false>
 // Blocks per SM forced by the register budget: measured no gain (SF10 expansion 0.435 ms
 // at 63 registers / 4 blocks, 0.443 with 5, 0.439 with 6, 0.494 with 8 -- spills), so off.
 #ifndef TQP_EXPAND_MINB
@@ -484,7 +505,8 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
                                                      const uint32_t* __restrict__ perm_l,
                                                      const uint32_t* __restrict__ perm_r, int64_t begin, int64_t end,
                                                      void* __restrict__ lo_out, void* __restrict__ ro_out, int idx32,
-                                                     unsigned long long* __restrict__ ck, int tg_shift) {
+                                                     unsigned long long* __restrict__ ck, int tg_shift,
+                                                     SmjPayload pay) {
     // shared memory: the staged bucket ends, plus (when the CTA spans <= MCAP buckets)
     // the buckets' (L, R, startL, startR) so that walking across keys needs no global loads
     constexpr int MCAP = 1024;
@@ -609,6 +631,17 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
     }
     __syncthreads();
     const int n = (int)(c1 - c0);
+    if (PAY) {   // index outputs optional; payload gathered per output, coalesced stores
+        for (int o = threadIdx.x; o < n; o += ENT) {
+            const int64_t j = c0 - begin + o;
+            const uint32_t l = s_l[o], r = s_r[o];
+            if (lo_out) __stcs((long long*)lo_out + j, (long long)l);
+            if (ro_out) __stcs((long long*)ro_out + j, (long long)r);
+            for (int c = 0; c < pay.nl; c++) pay_copy(pay.lsrc[c], pay.ldt[c], l, pay.ldst[c], j);
+            for (int c = 0; c < pay.nr; c++) pay_copy(pay.rsrc[c], pay.rdt[c], r, pay.rdst[c], j);
+        }
+        return;
+    }
     if (idx32) {   // int32 indices (tqp_smj_expand_i32)
         int* lo32 = (int*)lo_out + (c0 - begin);
         int* ro32 = (int*)ro_out + (c0 - begin);
@@ -786,7 +819,42 @@ void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end,
     ctx->add_bytes("tqp_smj_expand", (idx32 ? 8.0 : 16.0) * (double)(end - begin));
     launch(ctx, "tqp_smj_expand", expand_kernel<false>, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(), P->mR.get(),
            P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(), begin, end, lo,
-           ro, idx32, (unsigned long long*)nullptr, P->tg_shift);
+           ro, idx32, (unsigned long long*)nullptr, P->tg_shift, SmjPayload{});
+}
+
+void smj_expand_payload(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end, const tqp_col* lp, int n_lp,
+                        void* const* lp_out, const tqp_col* rp, int n_rp, void* const* rp_out, int64_t* lo,
+                        int64_t* ro) {
+    if (begin < 0 || end < begin || end > P->out_size) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: bad window");
+    if (n_lp < 0 || n_lp > SMJ_MAXPAY || n_rp < 0 || n_rp > SMJ_MAXPAY)
+        fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_payload: at most 8 payload columns per side");
+    SmjPayload pay{};
+    pay.nl = n_lp;
+    pay.nr = n_rp;
+    double pb = 0;
+    for (int c = 0; c < n_lp; c++) {
+        if ((end > begin && (!lp[c].data || !lp_out[c])) || lp[c].dtype < TQP_U8 || lp[c].dtype > TQP_F64)
+            fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_payload: bad left payload column");
+        pay.lsrc[c] = lp[c].data;
+        pay.ldt[c] = lp[c].dtype;
+        pay.ldst[c] = lp_out[c];
+        pb += 2.0 * (double)dtype_size(lp[c].dtype);
+    }
+    for (int c = 0; c < n_rp; c++) {
+        if ((end > begin && (!rp[c].data || !rp_out[c])) || rp[c].dtype < TQP_U8 || rp[c].dtype > TQP_F64)
+            fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_payload: bad right payload column");
+        pay.rsrc[c] = rp[c].data;
+        pay.rdt[c] = rp[c].dtype;
+        pay.rdst[c] = rp_out[c];
+        pb += 2.0 * (double)dtype_size(rp[c].dtype);
+    }
+    if (end == begin) return;
+    const int64_t blocks = ceil_div(end - begin, ETILE);
+    if (blocks >= (int64_t(1) << 31)) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: window too large");
+    ctx->add_bytes("tqp_smj_expand", ((lo ? 8.0 : 0.0) + (ro ? 8.0 : 0.0) + pb) * (double)(end - begin));
+    launch(ctx, "tqp_smj_expand", expand_kernel<false, true>, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(),
+           P->mR.get(), P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(),
+           begin, end, (void*)lo, (void*)ro, 0, (unsigned long long*)nullptr, P->tg_shift, pay);
 }
 
 // The expansion consumed in place (a fused consumer instead of
@@ -802,7 +870,7 @@ void smj_expand_checksum(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int
     ck.zero();
     launch(ctx, "tqp_smj_expand_checksum", expand_kernel<true>, dim3((unsigned)blocks), dim3(ENT), 0, P->mL.get(),
            P->mR.get(), P->msL.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(),
-           begin, end, (void*)nullptr, (void*)nullptr, 0, ck.get(), P->tg_shift);
+           begin, end, (void*)nullptr, (void*)nullptr, 0, ck.get(), P->tg_shift, SmjPayload{});
     launch(ctx, "tqp_smj_expand_checksum", ck_final_kernel, dim3(1), dim3(1024), 0, (const unsigned long long*)ck.get(),
            ck.get() + 3 * CK_SLOTS);
     read_back(ctx, out_host, ck.get() + 3 * CK_SLOTS, 24);

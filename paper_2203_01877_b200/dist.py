@@ -1,54 +1,147 @@
-"""Multi-GPU driver: one process per GPU, torch.distributed (NCCL) for the exchanges.
+"""Multi-GPU driver: one process per GPU, torch.distributed (NCCL) for the collectives.
 
-The hot path shards by row ranges (the paper lists data-parallel
-execution as future work):
-  * group-by: every rank aggregates its rows (tqp_groupby_agg) with AVG rewritten as
-    SUM + COUNT; the few partial groups are all-gathered and merged exactly by
-    tqp_groupby_merge (int128 sums, averages recomputed from merged SUM / COUNT, never
-    averaged);
-  * PK-FK join, co-partitioned layout (each rank holds its orders and exactly their
-    lineitems): purely local, no exchange;
-  * PK-FK join, shuffled layout: either the build side is all-gathered (broadcast
-    build) -- the gathered rank-ordered concatenation is the global
-    build table, so build rows come out as global row numbers with no remapping -- or
-    both sides are co-partitioned by key range (all_to_all of (key, global row)) and
-    joined locally; a byte cost model picks the cheaper exchange (pkfk_cost_bytes).
-Operators are injectable (`local_fn`, `merge_fn`, `join_fn`) so the exchange logic is
-tested on CPU with the gloo backend and the oracle as the local operator
-(tests/test_dist_gloo.py). The product path always uses the libtqp kernels.
+The hot path shards by rows (the paper lists data-parallel execution
+as future work). Every rank holds a slice of each column; "global row"
+means the position in the rank-ordered concatenation of the ranks' slices, so every
+distributed result is compared with -- and equals, bit for bit -- the single-GPU result
+over the concatenated table.
+
+  * group-by: local partial aggregation (tqp_groupby_agg, AVG rewritten as SUM + COUNT),
+    all-gather of the few partial groups, exact merge (tqp_groupby_merge: int128 sums,
+    averages recomputed from merged SUM / COUNT, never averaged);
+  * PK-FK join, shuffled layout, two exchanges:
+      broadcast build -- the build slices are all-gathered in rank order (the global
+      build table), the local probe rows join against it;
+      co-partition -- equal-width key ranges from an all-reduced device [min, max]
+      (tqp_minmax, tqp_range_splitters: no host round trip), both sides' (key, global
+      row) partitioned by key range on the GPU (tqp_partition: histogram, scan, stable
+      scatter), one all_to_all per column, the local join gathers the received global
+      rows as payload (tqp_pkfk_join_payload) -- pairs come out ascending by global
+      probe row because the partition is stable and blocks arrive in rank order;
+    a byte cost model (pkfk_cost_bytes) picks the cheaper one;
+  * sample sort and the generic SMJ: local libtqp sort,
+    splitters from sampled sorted keys, contiguous slices of the sorted columns sent
+    with all_to_all, local stable sort / Alg. 1 with createOutput fused
+    (tqp_smj_expand_payload). Heavy SMJ keys (a key equal to a splitter spans several
+    ranks) are split by output range: the key's left rows are divided among its ranks
+    by their ordinal within the key (global: the key's rows on lower ranks + the local
+    position), its right rows replicated to each of them.
+
+Collectives go through `_Comm`: NCCL on device tensors; with the gloo backend, device
+tensors are staged through host memory (the world-size-2 tests run two ranks on one
+GPU that way, and on CPU with the oracle as the local operators). The only host syncs
+are the ones a collective's split sizes need (one per exchange) and the tiny splitter
+/ heavy-key metadata. The local operators come from `ops` (default: the libtqp context,
+so every full-column step runs in libtqp's kernels; the CPU tests pass an oracle-backed
+stand-in with the same methods).
 """
 
 import torch
 import torch.distributed as dist
 
 
+# --------------------------------------------------------------------- plumbing
+
+class _Comm:
+    """Collectives on one process group; gloo gets host copies of device tensors."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _h(self, t):
+        return t.cpu() if self.stage and t.is_cuda else t
+
+    def _dev(self):
+        """Where small control tensors live: host for gloo, the current GPU for NCCL."""
+        return torch.device("cpu") if self.stage else torch.device("cuda", torch.cuda.current_device())
+
+    def all_reduce(self, t, op=dist.ReduceOp.SUM):
+        h = self._h(t)
+        dist.all_reduce(h, op=op, group=self.group)
+        if h is not t:
+            t.copy_(h)
+        return t
+
+    def all_gather_sizes(self, n):
+        """Every rank's element count (one tiny collective + host read)."""
+        x = torch.tensor([n], dtype=torch.int64, device=self._dev())
+        out = [torch.empty_like(x) for _ in range(self.world)]
+        dist.all_gather(out, x, group=self.group)
+        return torch.cat(out).tolist()
+
+    def all_gather_cat(self, t, sizes=None):
+        """Concatenation of every rank's 1-D tensor in rank order (uneven sizes): one
+        broadcast per rank into views of the output (no copy after the collective)."""
+        sizes = self.all_gather_sizes(t.numel()) if sizes is None else sizes
+        out = torch.empty(sum(sizes), dtype=t.dtype, device=t.device)
+        ho = self._h(out) if self.stage else out
+        o = 0
+        for r, s in enumerate(sizes):
+            view = ho[o:o + s]
+            if r == self.rank:
+                view.copy_(self._h(t))
+            if s:
+                dist.broadcast(view, src=r, group=self.group)
+            o += s
+        if ho is not out:
+            out.copy_(ho)
+        return out
+
+    def exchange_counts(self, counts):
+        """counts[d] = rows this rank sends to d (device or host int64, shape (world,) or
+        (world, k)) -> (send, recv) host lists; the one host sync of an exchange."""
+        hc = counts.to(device=self._dev(), dtype=torch.int64).reshape(self.world, -1).contiguous()
+        r = torch.empty_like(hc)
+        dist.all_to_all_single(r, hc, group=self.group)
+        both = torch.stack([hc, r]).cpu().tolist()
+        return both[0], both[1]
+
+    def all_to_all_v(self, t, send, recv):
+        """all_to_all_single of a 1-D tensor with host split sizes; blocks arrive in
+        source-rank order."""
+        out = torch.empty(sum(recv), dtype=t.dtype, device=t.device)
+        if self.stage and t.is_cuda:
+            ho = torch.empty(sum(recv), dtype=t.dtype)
+            dist.all_to_all_single(ho, t.cpu(), recv, send, group=self.group)
+            out.copy_(ho)
+        else:
+            dist.all_to_all_single(out, t.contiguous(), recv, send, group=self.group)
+        return out
+
+
+def _offset(comm, n):
+    """(global offset of this rank's slice, total rows) from every rank's row count."""
+    sizes = comm.all_gather_sizes(n)
+    return sum(sizes[:comm.rank]), sum(sizes)
+
+
+def _key_dtype_ok(t):
+    if t.dtype not in (torch.int64, torch.int32, torch.uint8):
+        raise TypeError(f"distributed operators take u8 / i32 / i64 key columns, not {t.dtype}")
+
+
+# ---------------------------------------------------------------------- group-by
+
 def _rewrite_aggs(aggs):
     """Per-rank aggregates: AVG -> SUM of the same expression; one COUNT(*) appended."""
     return [("sum", f) if op == "avg" else (op, f) for op, f in aggs] + [("count", [])]
 
 
-def _gather_rows(t, group=None):
-    """All-gather a (rows, W) int64 tensor with per-rank row counts; returns the concatenation
-    in rank order (valid rows only)."""
-    world = dist.get_world_size(group)
-    n = torch.tensor([t.shape[0]], dtype=torch.int64, device=t.device)
-    sizes = [torch.zeros_like(n) for _ in range(world)]
-    dist.all_gather(sizes, n, group=group)
-    sizes = [int(s.item()) for s in sizes]
-    mx = max(max(sizes), 1)
-    pad = torch.zeros((mx, t.shape[1]), dtype=t.dtype, device=t.device)
-    pad[:t.shape[0]] = t
-    parts = [torch.empty_like(pad) for _ in range(world)]
-    dist.all_gather(parts, pad, group=group)
-    return torch.cat([p[:s] for p, s in zip(parts, sizes)], dim=0)
-
-
-def groupby_agg(ctx, cols, key_idx, aggs, preds=(), group=None, local_fn=None, merge_fn=None):
+def groupby_agg(ops, cols, key_idx, aggs, preds=(), group=None, local_fn=None, merge_fn=None):
     """Distributed sort-based group-by over row-partitioned columns: local partial
     aggregation, all-gather of the partial groups, exact merge. Every rank returns the
-    merged result (same dict layout as Context.groupby_agg)."""
-    local_fn = local_fn or ctx.groupby_agg
-    merge_fn = merge_fn or ctx.groupby_merge
+    merged result (same dict layout as Context.groupby_agg). Aggregates over fp64 value
+    columns are rejected: the exact merge is integer (int128) only."""
+    for op, factors in aggs:
+        if op != "count" and any(cols[c].dtype == torch.float64 for c, _, _ in factors):
+            raise ValueError("distributed groupby_agg: fp64 aggregate columns are not supported "
+                             "(tqp_groupby_merge merges exact int128 partials only)")
+    local_fn = local_fn or ops.groupby_agg
+    merge_fn = merge_fn or ops.groupby_merge
+    comm = _Comm(group)
     raggs = _rewrite_aggs(aggs)
     loc = local_fn(cols, key_idx, raggs, preds)
     G = loc["n_groups"]
@@ -58,7 +151,8 @@ def groupby_agg(ctx, cols, key_idx, aggs, preds=(), group=None, local_fn=None, m
     for (op, _), r in zip(raggs, loc["results"]):
         pieces.append(r.reshape(G, 2) if op == "sum" else r.reshape(G, 1).to(torch.int64))
     mat = torch.cat(pieces, dim=1) if pieces else torch.zeros((G, 0), dtype=torch.int64, device=dev)
-    allm = _gather_rows(mat.contiguous(), group)
+    W = mat.shape[1]
+    allm = comm.all_gather_cat(mat.contiguous().reshape(-1)).reshape(-1, W)   # a few groups per rank
     c = 0
     keys = []
     for dt in key_dtypes:
@@ -77,232 +171,242 @@ def groupby_agg(ctx, cols, key_idx, aggs, preds=(), group=None, local_fn=None, m
     return merge_fn(keys, aggs, partials, counts)
 
 
-def pkfk_join_broadcast(ctx, build_keys, probe_keys, group=None, join_fn=None):
-    """Shuffled-layout PK-FK join: all-gather the build side (rank-ordered, so the
-    concatenation is the global build table), then join the local probe rows.
-    Returns (global build row, local probe row) pairs in probe-row order."""
-    join_fn = join_fn or ctx.pkfk_join
-    allb = _gather_rows(build_keys.reshape(-1, 1).to(torch.int64), group).reshape(-1)
-    return join_fn(allb.to(build_keys.dtype), probe_keys)
+# ------------------------------------------------------------------- PK-FK join
+
+def pkfk_join_broadcast(ops, build_keys, probe_keys, group=None):
+    """Shuffled-layout PK-FK join, broadcast build: the build slices all-gathered in rank
+    order are the global build table, so left rows come out global; the probe side does
+    not move. Returns (global build row, global probe row), ascending probe row."""
+    _key_dtype_ok(build_keys)
+    comm = _Comm(group)
+    poff, _ = _offset(comm, probe_keys.numel())
+    allb = comm.all_gather_cat(build_keys)
+    lo, ro = ops.pkfk_join(allb, probe_keys)
+    if poff:
+        ro += poff   # local -> global probe row (the probe side never moved)
+    return lo, ro
 
 
-def _stable_order(dest, sort_fn):
-    """Stable permutation grouping rows by destination rank (libtqp's radix sort on GPUs)."""
-    if sort_fn is not None:
-        return sort_fn(dest)
-    return torch.argsort(dest, stable=True)
-
-
-def _exchange(cols, dest, world, group=None, sort_fn=None):
-    """Send row i of every column to rank dest[i] (all_to_all_single). Received rows are
-    in source-rank order, and in source row order within a source."""
-    order = _stable_order(dest, sort_fn)
-    send_counts = torch.bincount(dest, minlength=world).to(torch.int64)
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    sc, rc = send_counts.tolist(), recv_counts.tolist()
-    out = []
-    for c in cols:
-        r = torch.empty(sum(rc), dtype=c.dtype, device=c.device)
-        dist.all_to_all_single(r, c[order].contiguous(), rc, sc, group=group)
-        out.append(r)
-    return out
-
-
-def _key_ranges(build_keys, probe_keys, world, group=None):
-    """Equal-width key ranges over the global [min, max] of both sides (the TPC-H key
-    domain is dense; a sampled splitter set would replace this for skewed keys)."""
-    dev = build_keys.device
-    big = torch.iinfo(torch.int64)
-    lo = torch.tensor([min(int(build_keys.min()) if build_keys.numel() else big.max,
-                           int(probe_keys.min()) if probe_keys.numel() else big.max)], dtype=torch.int64, device=dev)
-    hi = torch.tensor([max(int(build_keys.max()) if build_keys.numel() else big.min,
-                           int(probe_keys.max()) if probe_keys.numel() else big.min)], dtype=torch.int64, device=dev)
-    dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=group)
-    dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=group)
-    kmin, kmax = int(lo.item()), int(hi.item())
-    width = max((kmax - kmin) // world + 1, 1)
-    return kmin, width
-
-
-def pkfk_join_copartition(ctx, build_keys, build_rows, probe_keys, probe_rows, group=None, join_fn=None,
-                          sort_fn=None):
-    """Shuffled-layout PK-FK join by co-partitioning: both sides' (key, global row) are
-    sent to the rank owning the key's range, joined locally, and mapped back to global
-    rows. Returns (global build row, global probe row) pairs of this rank's key range,
-    ascending by global probe row (the union over ranks = the single-GPU result)."""
-    join_fn = join_fn or ctx.pkfk_join
-    if sort_fn is None and ctx is not None:
-        sort_fn = lambda d: ctx.sort(d)[1]   # noqa: E731
-    world = dist.get_world_size(group)
-    kmin, width = _key_ranges(build_keys, probe_keys, world, group)
-    bk, pk = build_keys.to(torch.int64), probe_keys.to(torch.int64)
-    dest_b = torch.clamp((bk - kmin) // width, 0, world - 1)
-    dest_p = torch.clamp((pk - kmin) // width, 0, world - 1)
-    rb_key, rb_row = _exchange([bk, build_rows.to(torch.int64)], dest_b, world, group, sort_fn)
-    rp_key, rp_row = _exchange([pk, probe_rows.to(torch.int64)], dest_p, world, group, sort_fn)
-    lo, ro = join_fn(rb_key, rp_key)
-    gl, gr = rb_row[lo], rp_row[ro]
-    order = _stable_order(gr, sort_fn)
-    return gl[order], gr[order]
+def pkfk_join_copartition(ops, build_keys, probe_keys, group=None, exchange=None):
+    """Shuffled-layout PK-FK join by co-partitioning on key ranges (all on the GPU up to the
+    all_to_all split sizes). Returns this rank's (global build row, global probe row) pairs
+    for its key range, ascending by global probe row; the union over ranks is the
+    single-GPU join of the concatenated tables. `exchange` (a dict, optional) receives
+    the bytes this rank sent / received."""
+    _key_dtype_ok(build_keys)
+    _key_dtype_ok(probe_keys)
+    comm = _Comm(group)
+    G = comm.world
+    sizes_b = comm.all_gather_sizes(build_keys.numel())
+    sizes_p = comm.all_gather_sizes(probe_keys.numel())
+    boff, poff = sum(sizes_b[:comm.rank]), sum(sizes_p[:comm.rank])
+    # key ranges: [min, max] of both sides, all-reduced as MIN of (min, ~max) -- ~ reverses order
+    mb, mp = ops.minmax(build_keys), ops.minmax(probe_keys)
+    lohi = torch.stack([torch.minimum(mb[0], mp[0]), torch.maximum(mb[1], mp[1])])
+    red = torch.stack([lohi[0], ~lohi[1]])
+    comm.all_reduce(red, op=dist.ReduceOp.MIN)
+    lohi = torch.stack([red[0], ~red[1]])
+    spl = ops.range_splitters(lohi, G)
+    bk, brow, bcnt = ops.partition(build_keys, spl, row_base=boff)
+    pk, prow, pcnt = ops.partition(probe_keys, spl, row_base=poff)
+    send, recv = comm.exchange_counts(torch.stack([bcnt, pcnt], dim=1))
+    sb, rb = [s[0] for s in send], [r[0] for r in recv]
+    sp, rp = [s[1] for s in send], [r[1] for r in recv]
+    rb_key = comm.all_to_all_v(bk, sb, rb)
+    rb_row = comm.all_to_all_v(brow, sb, rb)
+    rp_key = comm.all_to_all_v(pk, sp, rp)
+    rp_row = comm.all_to_all_v(prow, sp, rp)
+    if exchange is not None:
+        kb_b, kb_p = build_keys.element_size(), probe_keys.element_size()
+        me = comm.rank
+        exchange["sent_bytes"] = (sum(sb) - sb[me]) * (kb_b + 8) + (sum(sp) - sp[me]) * (kb_p + 8)
+        exchange["recv_bytes"] = (sum(rb) - rb[me]) * (kb_b + 8) + (sum(rp) - rp[me]) * (kb_p + 8)
+    (gl,), (gr,), _ = ops.pkfk_join_payload(rb_key, rp_key, [rb_row], [rp_row], indices=False)
+    return gl, gr
 
 
 def pkfk_cost_bytes(n_build, n_probe, world, key_bytes=8, row_bytes=8):
     """Bytes received per rank by each shuffled-layout strategy:
     broadcast = every other rank's build keys; co-partition = the (key, row) pairs of
-    both sides that belong to another rank's key range."""
+    both sides that belong to another rank's key range (uniform keys)."""
     f = (world - 1) / world
     return {"broadcast": n_build * key_bytes * f,
             "copartition": (n_build + n_probe) / world * (key_bytes + row_bytes) * f}
 
 
-def pkfk_join_shuffled(ctx, build_keys, build_rows, probe_keys, probe_rows, group=None, strategy="auto",
-                       join_fn=None, sort_fn=None):
+def pkfk_join_shuffled(ops, build_keys, probe_keys, group=None, strategy="auto", exchange=None):
     """Shuffled-layout PK-FK join with the cheaper exchange (or the one asked for).
     Returns (strategy, global build rows, global probe rows); broadcast pairs come in
     local probe order, co-partition pairs by global probe row within the rank's range."""
-    world = dist.get_world_size(group)
+    comm = _Comm(group)
     if strategy == "auto":
-        n = torch.tensor([build_keys.numel(), probe_keys.numel()], dtype=torch.int64, device=build_keys.device)
-        dist.all_reduce(n, group=group)
-        cost = pkfk_cost_bytes(int(n[0]), int(n[1]), world)
+        nb = sum(comm.all_gather_sizes(build_keys.numel()))
+        np_ = sum(comm.all_gather_sizes(probe_keys.numel()))
+        cost = pkfk_cost_bytes(nb, np_, comm.world)
         strategy = min(cost, key=cost.get)
     if strategy == "broadcast":
-        lo, ro = pkfk_join_broadcast(ctx, build_keys, probe_keys, group, join_fn)
-        return strategy, lo, probe_rows.to(torch.int64)[ro]
-    gl, gr = pkfk_join_copartition(ctx, build_keys, build_rows, probe_keys, probe_rows, group, join_fn, sort_fn)
+        lo, ro = pkfk_join_broadcast(ops, build_keys, probe_keys, group)
+        if exchange is not None:
+            sizes = comm.all_gather_sizes(build_keys.numel())
+            exchange["recv_bytes"] = (sum(sizes) - sizes[comm.rank]) * build_keys.element_size()
+            exchange["sent_bytes"] = sizes[comm.rank] * build_keys.element_size() * (comm.world - 1)
+        return strategy, lo, ro
+    gl, gr = pkfk_join_copartition(ops, build_keys, probe_keys, group, exchange)
     return strategy, gl, gr
 
 
-# ---------------------------------------------------------- distributed sort / SMJ
-# SURVEY.md §8(f) NEXT 3. Ranks hold contiguous global row ranges (rank order = global
-# row order). Keys are range-partitioned by splitters sampled from every rank's sorted
-# keys; (key, global row) pairs are exchanged with all_to_all and sorted / joined locally
-# with libtqp. Received blocks arrive in source-rank order, so a stable local sort (or
-# the SMJ's (key, left row, right row) order) reproduces the single-GPU order exactly:
-# the concatenation of the ranks' outputs, in rank order, is bit-identical to it.
+# ---------------------------------------------------------- sample sort / SMJ
 
-def _splitters(sorted_keys_list, world, group=None, per_rank=64):
-    """world - 1 splitters from evenly spaced samples of each rank's keys (exact local
-    quantiles when the keys are sorted, a position sample otherwise)."""
-    dev = sorted_keys_list[0].device
-    samples = []
-    for k in sorted_keys_list:
-        if k.numel():
-            idx = torch.linspace(0, k.numel() - 1, per_rank, device=dev).round().to(torch.int64)
-            samples.append(k.to(torch.int64)[idx])
-    loc = torch.cat(samples) if samples else torch.empty(0, dtype=torch.int64, device=dev)
-    allv = _gather_rows(loc.reshape(-1, 1), group).reshape(-1)
-    allv, _ = torch.sort(allv)   # a few thousand host-chosen samples: plumbing, not the operator
+def _sample_sorted(sk, per_rank):
+    """Evenly spaced samples of a sorted column (a few hundred values: plumbing)."""
+    n = sk.numel()
+    if n == 0:
+        return sk.new_empty(0, dtype=torch.int64)
+    idx = torch.linspace(0, n - 1, per_rank, device=sk.device).round().to(torch.int64)
+    return sk[idx].to(torch.int64)
+
+
+def _splitters(comm, sorted_keys, per_rank=64):
+    """world - 1 splitters at the quantiles of every rank's regular samples."""
+    allv = comm.all_gather_cat(_sample_sorted(sorted_keys, per_rank))
+    allv = torch.sort(allv)[0]
     if allv.numel() == 0:
-        return torch.empty(0, dtype=torch.int64, device=dev)
-    pos = [(i * allv.numel()) // world for i in range(1, world)]
-    return allv[torch.tensor(pos, dtype=torch.int64, device=dev)]
+        return allv
+    pos = torch.tensor([(i * allv.numel()) // comm.world for i in range(1, comm.world)], dtype=torch.int64,
+                       device=allv.device)
+    return allv[pos]
 
 
-def _output_splitters(lk, rk, world, group=None, per_rank=256):
+def _count_sorted(sk, vals):
+    """Occurrences of each value in a sorted column, and its first position (binary searches)."""
+    skl = sk.to(torch.int64)
+    lb = torch.searchsorted(skl, vals, right=False)
+    ub = torch.searchsorted(skl, vals, right=True)
+    return ub - lb, lb
+
+
+def _output_splitters(comm, slk, srk, per_rank=256):
     """world - 1 splitters balancing rows + output pairs per rank (the SMJ's work). Keys
-    frequent in a sample are candidates; their exact global counts L_k, R_k are summed
-    over the ranks, and each candidate carries its L_k * R_k pairs as weight beside the
-    rows the samples stand for. Splitters sit at the weight quantiles, so a key heavier
-    than a rank's share recurs as consecutive splitters and spans several ranks."""
-    dev = lk.device
-    samples = []
-    for k in (lk, rk):
-        if k.numel():
-            sk = torch.sort(k)[0]
-            idx = torch.linspace(0, k.numel() - 1, per_rank, device=dev).round().to(torch.int64)
-            samples.append(sk[idx])
-    loc = torch.cat(samples) if samples else torch.empty(0, dtype=torch.int64, device=dev)
-    allv = torch.sort(_gather_rows(loc.reshape(-1, 1), group).reshape(-1))[0]
+    frequent in the samples are candidates; their exact global counts L_k, R_k (binary
+    searches in the sorted columns, all-reduced) weigh L_k * R_k pairs beside the rows
+    the samples stand for. Splitters sit at the weight quantiles, so a key heavier than a
+    rank's share recurs as consecutive splitters and spans several ranks."""
+    loc = torch.cat([_sample_sorted(slk, per_rank), _sample_sorted(srk, per_rank)])
+    allv = torch.sort(comm.all_gather_cat(loc))[0]
+    dev = allv.device
     if allv.numel() == 0:
-        return torch.empty(0, dtype=torch.int64, device=dev)
+        return allv
     uk, cnt = torch.unique_consecutive(allv, return_counts=True)
     cand = uk[cnt >= 2]                      # identical on every rank
-    nrows = torch.tensor([lk.numel() + rk.numel()], dtype=torch.int64, device=dev)
-    dist.all_reduce(nrows, group=group)
-    def count_in(k):   # occurrences of each candidate key in k (candidates are sorted)
-        if cand.numel() == 0 or k.numel() == 0:
-            return torch.zeros(cand.numel(), dtype=torch.int64, device=dev)
-        pos = torch.searchsorted(cand, k)
-        hit = cand[pos.clamp(max=cand.numel() - 1)] == k
-        return torch.bincount(pos[hit], minlength=cand.numel()).to(torch.int64)
-    counts = torch.stack([count_in(lk), count_in(rk)])
-    dist.all_reduce(counts, group=group)
+    nrows = torch.tensor([slk.numel() + srk.numel()], dtype=torch.int64, device=dev)
+    comm.all_reduce(nrows)
+    counts = torch.stack([_count_sorted(slk, cand)[0], _count_sorted(srk, cand)[0]]).to(dev)
+    comm.all_reduce(counts)
     pairs = (counts[0] * counts[1]).to(torch.float64)
-    # weighted items: every sample stands for nrows / samples rows; candidates add their pairs
     w_sample = float(nrows.item()) / allv.numel()
     keys = torch.cat([allv, cand])
     wts = torch.cat([torch.full((allv.numel(),), w_sample, dtype=torch.float64, device=dev), pairs])
     order = torch.argsort(keys, stable=True)
     keys, cum = keys[order], torch.cumsum(wts[order], 0)
     total = float(cum[-1].item())
-    targets = torch.tensor([total * i / world for i in range(1, world)], dtype=torch.float64, device=dev)
+    targets = torch.tensor([total * i / comm.world for i in range(1, comm.world)], dtype=torch.float64, device=dev)
     pos = torch.searchsorted(cum, targets).clamp(max=keys.numel() - 1)
     return keys[pos]
 
 
-def _range_dest(keys, splitters):
-    """Rank owning each key: the number of splitters <= key (equal keys share a rank)."""
-    return torch.searchsorted(splitters, keys.to(torch.int64), right=True)
+def _global_rows(ops, perm, off):
+    rows = perm.to(torch.int64)
+    return rows + off if off else rows
 
 
-def sort_samplesort(ctx, keys, global_rows, group=None, sort_fn=None):
+def sort_samplesort(ops, keys, group=None):
     """Distributed stable sort. Returns this rank's (sorted keys, their global rows); the
     ranks' outputs concatenated in rank order are the stable (key, global row) order of
-    the whole column. sort_fn(k) -> (sorted keys, permutation); default libtqp."""
-    sort_fn = sort_fn or ctx.sort
-    world = dist.get_world_size(group)
-    sk, perm = sort_fn(keys)
-    rows = global_rows.to(torch.int64)[perm]
-    spl = _splitters([sk], world, group)
-    dest = _range_dest(sk, spl)
-    rk, rr = _exchange([sk.to(torch.int64), rows], dest, world, group,
-                       sort_fn=lambda d: torch.arange(d.numel(), device=d.device))   # sk is sorted: dest ascends
-    k2, p2 = sort_fn(rk)
-    return k2.to(keys.dtype), rr[p2]
+    the concatenated column."""
+    _key_dtype_ok(keys)
+    comm = _Comm(group)
+    off, _ = _offset(comm, keys.numel())
+    sk, perm = ops.sort(keys)
+    rows = _global_rows(ops, perm, off)
+    spl = _splitters(comm, sk).to(sk.device)
+    # dest(k) = #splitters <= k: the sorted column splits into contiguous slices
+    b = torch.searchsorted(sk.to(torch.int64), spl, right=True).tolist() if spl.numel() else []
+    cuts = [0] + b + [sk.numel()]
+    send = [cuts[d + 1] - cuts[d] for d in range(comm.world)]
+    send, recv = comm.exchange_counts(torch.tensor(send, dtype=torch.int64))
+    send, recv = [s[0] for s in send], [r[0] for r in recv]
+    rk = comm.all_to_all_v(sk, send, recv)
+    rr = comm.all_to_all_v(rows, send, recv)
+    k2, p2 = ops.sort(rk)     # stable: equal keys stay in source-rank, then source order
+    return k2, ops.gather(rr, p2)
 
 
-def smj_join_copartition(ctx, left_keys, left_rows, right_keys, right_rows, group=None, join_fn=None,
-                         sort_fn=None, n_left_total=None):
+def smj_join_copartition(ops, left_keys, right_keys, group=None):
     """Distributed generic sort-merge join (Alg. 1) by key-range co-partitioning with
-    sampled splitters, with output-range splitting of heavy keys.
+    output-aware splitters and output-range splitting of heavy keys.
     Returns this rank's (global left row, global right row) pairs in (key, left row,
-    right row) order; the concatenation over ranks in rank order is the single-GPU result.
+    right row) order; the concatenation over ranks in rank order is the single-GPU join
+    of the concatenated columns.
 
-    A key equal to one or more splitters is heavy: it spans ranks lo..hi (lo = splitters
-    below it, hi = splitters up to it). Its left rows are split across those ranks by
-    global left row (row * (hi - lo + 1) // n_left_total: monotone, so each rank gets a
-    contiguous range of the key's left rows in order) and its right rows are replicated to
-    all of them, so each rank produces the key's pairs for its left rows and the pairs
-    still come out in (key, l, r) order across ranks. Light keys go to one rank."""
-    join_fn = join_fn or ctx.smj_join
-    if sort_fn is None and ctx is not None:
-        sort_fn = lambda d: ctx.sort(d)[1]   # noqa: E731
-    world = dist.get_world_size(group)
-    lk, rk = left_keys.to(torch.int64), right_keys.to(torch.int64)
-    lrows, rrows = left_rows.to(torch.int64), right_rows.to(torch.int64)
-    if n_left_total is None:   # rows are global offsets into the left column: its length
-        t = torch.tensor([lrows.max().item() + 1 if lrows.numel() else 0], dtype=torch.int64, device=lk.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        n_left_total = max(int(t.item()), 1)
-    spl = _output_splitters(lk, rk, world, group)
-    # left: heavy keys' rows split across their ranks by global row, light rows to one rank
-    llo = torch.searchsorted(spl, lk, right=False)
-    lhi = torch.searchsorted(spl, lk, right=True)
-    dest_l = torch.where(lhi > llo, llo + (lrows * (lhi - llo + 1)) // n_left_total, lhi)
-    rl_key, rl_row = _exchange([lk, lrows], dest_l, world, group, sort_fn)
-    # right: heavy keys' rows replicated to every rank of the key's span
-    rlo = torch.searchsorted(spl, rk, right=False)
-    rhi = torch.searchsorted(spl, rk, right=True)
-    reps = rhi - rlo + 1
-    if bool((reps > 1).any()):
-        idx = torch.repeat_interleave(torch.arange(rk.numel(), device=rk.device), reps)
-        first = torch.repeat_interleave(torch.cumsum(reps, 0) - reps, reps)
-        dest_r = rlo[idx] + (torch.arange(idx.numel(), device=rk.device) - first)
-        rk_x, rrows_x = rk[idx], rrows[idx]
+    A key v equal to one or more splitters spans ranks lo..hi (lo = splitters below v,
+    hi = splitters up to v). Its L_v left rows are divided among those ranks by ordinal
+    within the key -- global ordinal = the key's rows on lower ranks + local position, so
+    rank lo + d' takes ordinals [ceil(d' L_v / span), ceil((d'+1) L_v / span)) -- and its
+    right rows are replicated to every one of them: each rank emits the key's pairs for
+    its left rows, in (l, r) order, and the ranks' outputs stay in global order."""
+    _key_dtype_ok(left_keys)
+    _key_dtype_ok(right_keys)
+    comm = _Comm(group)
+    G, me = comm.world, comm.rank
+    loff, _ = _offset(comm, left_keys.numel())
+    roff, _ = _offset(comm, right_keys.numel())
+    slk, pl = ops.sort(left_keys)
+    srk, pr = ops.sort(right_keys)
+    lrows, rrows = _global_rows(ops, pl, loff), _global_rows(ops, pr, roff)
+    spl = _output_splitters(comm, slk, srk).to(slk.device)
+    spl_h = spl.tolist()
+    nl, nr = slk.numel(), srk.numel()
+    if G > 1 and spl.numel():
+        # distinct splitter values: local count and first position in the sorted left keys
+        vals = torch.unique(spl)
+        c_loc, lb = _count_sorted(slk, vals)
+        c_all = comm.all_gather_cat(c_loc.to(torch.int64)).reshape(G, -1)          # (rank, value)
+        meta = torch.stack([c_loc, lb, c_all[:me].sum(0), c_all.sum(0)]).cpu().tolist()
+        info = {}
+        for j, v in enumerate(vals.tolist()):
+            lo_v = sum(1 for s in spl_h if s < v)
+            hi_v = sum(1 for s in spl_h if s <= v)
+            info[v] = dict(c=meta[0][j], lb=meta[1][j], base=meta[2][j], L=meta[3][j], lo=lo_v, span=hi_v - lo_v + 1)
+        # left: disjoint slices of the sorted column; boundary d splits key v = spl[d - 1]
+        cuts = [0]
+        for d in range(1, G):
+            f = info[spl_h[d - 1]]
+            q = -(-((d - f["lo"]) * f["L"]) // f["span"]) - f["base"]   # ceil division
+            cuts.append(f["lb"] + min(max(q, 0), f["c"]))
+        cuts.append(nl)
+        send_l = [cuts[d + 1] - cuts[d] for d in range(G)]
+        # right: slices [lb(spl[d - 1]), ub(spl[d])) -- overlapping on heavy keys (replicas)
+        srk64 = srk.to(torch.int64)
+        lbs = torch.searchsorted(srk64, spl, right=False).tolist()
+        ubs = torch.searchsorted(srk64, spl, right=True).tolist()
+        rs = [0] + lbs
+        re_ = ubs + [nr]
+        send_r = [re_[d] - rs[d] for d in range(G)]
+        overlap = any(re_[d] > rs[d + 1] for d in range(G - 1))
+        if overlap:   # replicated heavy-key runs: materialise the slices back to back
+            rk_send = torch.cat([srk[rs[d]:re_[d]] for d in range(G)])
+            rr_send = torch.cat([rrows[rs[d]:re_[d]] for d in range(G)])
+        else:
+            rk_send, rr_send = srk, rrows
     else:
-        dest_r, rk_x, rrows_x = rhi, rk, rrows
-    rr_key, rr_row = _exchange([rk_x, rrows_x], dest_r, world, group, sort_fn)
-    lo, ro = join_fn(rl_key, rr_key)
-    return rl_row[lo], rr_row[ro]
+        send_l, send_r = [nl] + [0] * (G - 1), [nr] + [0] * (G - 1)
+        rk_send, rr_send = srk, rrows
+    send, recv = comm.exchange_counts(torch.tensor([send_l, send_r], dtype=torch.int64).t())
+    sl_, rl_ = [s[0] for s in send], [r[0] for r in recv]
+    sr_, rr_ = [s[1] for s in send], [r[1] for r in recv]
+    rl_key = comm.all_to_all_v(slk, sl_, rl_)
+    rl_row = comm.all_to_all_v(lrows, sl_, rl_)
+    rr_key = comm.all_to_all_v(rk_send, sr_, rr_)
+    rr_row = comm.all_to_all_v(rr_send, sr_, rr_)
+    (gl,), (gr,), _ = ops.smj_join_payload(rl_key, rr_key, [rl_row], [rr_row])
+    return gl, gr

@@ -1090,3 +1090,89 @@ def test_groupby_merge_partials(T):
     got = T.context().groupby_merge(keys, aggs, partials, counts)
     want = oracle.groupby_agg([npy(c) for c in cols], Q1_KEYS, aggs, Q1_PREDS)
     check_groupby(T, got, want, aggs)
+
+
+# ------------------------------------------------- data-parallel exchange steps
+
+@pytest.mark.parametrize("n", [0, 1, 4095, 4096, 4097, 300_001])
+@pytest.mark.parametrize("parts", [1, 2, 3, 8, 256])
+@pytest.mark.parametrize("dtype", [torch.int64, torch.int32, torch.uint8])
+def test_partition_stable_by_key_range(T, n, parts, dtype):
+    """tqp_partition = a stable sort by destination (#splitters <= key): numpy's stable
+    argsort of the searchsorted destinations, plus bincount counts; keys equal to a
+    splitter go to the higher rank; duplicate splitters leave empty destinations."""
+    rng = np.random.default_rng(n + parts)
+    hi = {torch.int64: 1 << 40, torch.int32: 1 << 30, torch.uint8: 255}[dtype]
+    lo = 0 if dtype == torch.uint8 else -hi
+    keys = rng.integers(lo, hi, n)
+    spl = np.sort(rng.integers(lo, hi, parts - 1))
+    if parts > 3:
+        spl[1] = spl[2]                     # a duplicate splitter: destination 2 is empty
+        keys[: min(n, 5)] = spl[1]          # keys equal to a splitter
+    ko, ro, cnt = T.partition(cu(keys, dtype), cu(spl), row_base=1000)
+    dest = np.searchsorted(spl, keys, side="right")
+    order = np.argsort(dest, kind="stable")
+    assert np.array_equal(npy(ko).astype(np.int64), keys[order])
+    assert np.array_equal(npy(ro), order + 1000)
+    assert np.array_equal(npy(cnt), np.bincount(dest, minlength=parts))
+
+
+def test_minmax_and_range_splitters(T):
+    """Device [min, max] (empty -> [INT64_MAX, INT64_MIN]) and equal-width splitters:
+    key k goes to (k - lo) // width, width = (hi - lo) // parts + 1."""
+    rng = np.random.default_rng(3)
+    k = rng.integers(-(1 << 50), 1 << 50, 100_003)
+    mm = npy(T.minmax(cu(k)))
+    assert mm.tolist() == [int(k.min()), int(k.max())]
+    assert npy(T.minmax(cu(np.array([], np.int64)))).tolist() == [I64_MAX, I64_MIN]
+    for parts in (1, 2, 7, 256):
+        spl = npy(T.range_splitters(cu(mm), parts))
+        w = (int(k.max()) - int(k.min())) // parts + 1
+        assert spl.tolist() == [int(k.min()) + (j + 1) * w for j in range(parts - 1)]
+        dest = np.searchsorted(spl, k, side="right")
+        assert np.array_equal(dest, (k - int(k.min())) // w)
+    spl = npy(T.range_splitters(cu(np.array([I64_MIN, I64_MAX])), 4))   # full domain: no overflow
+    assert spl[-1] < I64_MAX and np.all(np.diff(spl) > 0)
+
+
+@pytest.mark.parametrize("dtype", [torch.int64, torch.int32, torch.uint8, torch.float64])
+def test_gather(T, dtype):
+    rng = np.random.default_rng(4)
+    src = rng.integers(0, 200, 50_001)
+    idx = rng.integers(0, src.size, 123_457)
+    s = torch.as_tensor(src).to(dtype).cuda()
+    out = T.gather(s, cu(idx))
+    assert torch.equal(out.cpu(), s.cpu()[torch.as_tensor(idx)])
+
+
+@pytest.mark.parametrize("case", ["random", "zipf", "coarse"])
+def test_smj_expand_payload(T, case):
+    """createOutput fused into the expansion: payload gathered by the
+    oracle's pairs, over the whole output and ragged windows, with and without indices."""
+    rng = np.random.default_rng(9)
+    if case == "random":
+        left, right = rng.integers(0, 3_000, 40_003), rng.integers(0, 3_000, 30_001)
+    elif case == "zipf":
+        left = zipf_keys(100_000, 20_000, seed=5).numpy()
+        right = uniform_keys(100_000, 20_000, seed=6).numpy()
+    else:   # heavy keys: the coarse tile-bucket table
+        left = rng.permutation(np.concatenate([np.full(30_000, 1), np.arange(3, 503)]))
+        right = rng.permutation(np.concatenate([np.arange(3, 503), np.full(40_000, 1)]))
+    lp = [cu(rng.integers(-10**12, 10**12, left.size)), cu(rng.integers(0, 255, left.size), torch.uint8)]
+    rp = [cu(rng.integers(-2**31, 2**31 - 1, right.size), torch.int32),
+          torch.tensor(rng.normal(size=right.size), device="cuda")]
+    plan = T.smj_prepare(cu(left), cu(right))
+    wl, wr = oracle.smj_join(left, right)
+    assert plan.size == len(wl)
+    wins = [(0, plan.size), (0, 0), (plan.size // 3, plan.size // 3 + 2049), (plan.size - 7, plan.size)]
+    for b, e in wins:
+        louts, routs, idx = plan.expand_payload(b, e, lp, rp, indices=(b == 0))
+        for c, o in zip(lp, louts):
+            assert torch.equal(o.cpu(), c.cpu()[torch.as_tensor(wl[b:e])])
+        for c, o in zip(rp, routs):
+            assert torch.equal(o.cpu(), c.cpu()[torch.as_tensor(wr[b:e])])
+        if b == 0:
+            assert np.array_equal(npy(idx[0]), wl[b:e]) and np.array_equal(npy(idx[1]), wr[b:e])
+    plan.release()
+    (g,), (h,), _ = T.smj_join_payload(cu(left), cu(right), [lp[0]], [rp[0]])
+    assert torch.equal(g.cpu(), lp[0].cpu()[torch.as_tensor(wl)])
