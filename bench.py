@@ -9,10 +9,14 @@ Step (per rank, BASELINE.json configs[2] size: SF10 = 15M orders / ~60M lineitem
   3. tqp_groupby_agg TPC-H Q1: filter + group by (returnflag, linestatus), 8 aggregates (a8-a10)
   4. tqp_filter_compact  TPC-H Q6 predicates -> bitmap + selection vector (a10)
   5. tqp_groupby_agg Q6 revenue: fused filter + sum (n_keys = 0)
-Multi-GPU (torchrun, one process per GPU): each rank holds an SF10-sized co-partitioned slice
-of an SF(10*N) dataset (lineitem range-partitioned with its orders), so the
-joins need no exchange; the Q1/Q6 partial aggregates are all-gathered over NCCL and merged by
-libtqp (tqp_groupby_merge). scaling = "weak".
+Multi-GPU (torchrun, one process per GPU): each rank holds an SF10-sized slice of an
+SF(10*N) dataset -- its orders rows and a lineitem slice whose orders are spread over every
+rank (--placement exchange, the default). The PK-FK join then exchanges
+over NCCL (co-partition all_to_all of (key, global row) by key range, or a broadcast build,
+whichever the byte model picks), the SMJ runs the distributed sort-merge join (sampled
+splitters, heavy keys split by output range), and the Q1/Q6 partial aggregates are
+all-gathered and merged by libtqp (tqp_groupby_merge). --placement local keeps each
+rank's lineitem with its own orders (no join exchange: the upper bound). scaling = "weak".
 
 value = lineitem rows processed per second by the whole job (all ranks), device-timed with
 CUDA events, max over ranks. Inputs (2.8 GB/rank) are larger than L2 (126 MB).
@@ -106,11 +110,32 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ data
 
-def make_data(rank, world, device, layout):
+def make_data(rank, world, device, layout, placement="local"):
     n_o = orders_count(SF_PER_RANK)
     orders, li = tpch_orders_lineitem(SF_PER_RANK * world, seed=42, device=device, layout=layout,
                                       order_range=(rank * n_o, (rank + 1) * n_o))
+    if placement == "exchange" and world > 1:   # lineitem's orders spread over every rank
+        from datagen.tpch import spread_orderkeys
+        li["l_orderkey"], _ = spread_orderkeys(li["l_parent"], rank, world)
     return orders, li
+
+
+def compulsory_bytes(hp, out):
+    """SURVEY.md §8(d) compulsory bytes per operator of one step (int64 keys and indices):
+    sort(n) = 24 n; PK-FK = sort(n_b) + 8 n_b + 8 n_p + 16 m; SMJ = sort(n_l) + sort(n_r)
+    + 8 (n_l + n_r) + 16 outSize; group-by / filter = the bytes of the columns read per row
+    (+ the bitmap and selection vector for the filter)."""
+    es = lambda cols: sum(c.element_size() for c in {id(c): c for c in cols}.values())   # noqa: E731
+    nb, npr, n = hp.ok.numel(), hp.lk.numel(), hp.n
+    m = out["pkfk"][0].numel()
+    osz = out["smj"][0].numel()
+    return {
+        "pkfk_join": 24 * nb + 8 * nb + 8 * npr + 16 * m,
+        "smj_join": 24 * nb + 24 * npr + 8 * (nb + npr) + 16 * osz,
+        "q1_groupby": es(hp.q1) * n,
+        "q6_filter": es(hp.q6[:3]) * n + n + 8 * out["q6_sel"].numel(),
+        "q6_sum": es(hp.q6) * n,
+    }
 
 
 def q_avg_rewrite(aggs):
@@ -125,10 +150,12 @@ def q_avg_rewrite(aggs):
 # ------------------------------------------------------------------ GPU step
 
 class HotPath:
-    def __init__(self, T, orders, li, world):
+    def __init__(self, T, orders, li, world, placement="local"):
         self.T = T
         self.ctx = T.context()
         self.world = world
+        self.exchange = placement == "exchange" and world > 1
+        self.strategy = None
         self.ok = orders["o_orderkey"]
         self.lk = li["l_orderkey"]
         self.q1 = columns(li, Q1_COLS)
@@ -156,12 +183,19 @@ class HotPath:
         q6 = self.q6 if q6 is None else q6
         c = self.ctx
         self._mark("start")
-        lo, ro = c.pkfk_join(ok, lk)
-        self._mark("pkfk_join")
-        plan = c.smj_prepare(ok, lk)
-        sl, sr = plan.expand(0, plan.size)
-        plan.release()
-        self._mark("smj_join")
+        if self.exchange:   # shuffled placement: the joins exchange over NCCL
+            from paper_2203_01877_b200 import dist
+            self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk)
+            self._mark("pkfk_join")
+            sl, sr = dist.smj_join_copartition(c, ok, lk)
+            self._mark("smj_join")
+        else:
+            lo, ro = c.pkfk_join(ok, lk)
+            self._mark("pkfk_join")
+            plan = c.smj_prepare(ok, lk)
+            sl, sr = plan.expand(0, plan.size)
+            plan.release()
+            self._mark("smj_join")
         r1 = self.groupby(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS)
         self._mark("q1_groupby")
         mask, sel = c.filter_compact(q6, Q6_PREDS)
@@ -199,16 +233,19 @@ def run_gpu(args):
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    orders, li = make_data(rank, world, dev, args.layout)
-    hp = HotPath(T, orders, li, world)
+    placement = args.placement or ("exchange" if world > 1 else "local")
+    orders, li = make_data(rank, world, dev, args.layout, placement)
+    hp = HotPath(T, orders, li, world, placement)
 
     def barrier():
         if dist:
             dist.barrier()
 
     for _ in range(args.warmup):
-        hp.step()
+        last = hp.step()
     torch.cuda.synchronize()
+    cbytes = compulsory_bytes(hp, last)
+    del last
     # Per-kernel table from profiled, untimed steps (two events around every launch
     # cost host time the GPU waits on after each readback, ~0.35 ms per step); the
     # timed region then brackets only the dominant kernel's launches with events.
@@ -231,6 +268,8 @@ def run_gpu(args):
     hp.ctx.set_profiling(True, only=dom_name)
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
+    from paper_2203_01877_b200 import dist as tdist
+    tdist.EXCHANGE_LOG = [] if hp.exchange else None
     t0.record()
     for _ in range(args.steps):
         hp.step()
@@ -238,12 +277,28 @@ def run_gpu(args):
     torch.cuda.synchronize()
     barrier()
     clocks = clk.stop()
+    exchange = None
+    if hp.exchange:
+        xl, tdist.EXCHANGE_LOG = tdist.EXCHANGE_LOG, None
+        x_ms = sum(a.elapsed_time(b) for a, b, _, _ in xl) / args.steps
+        x_recv = sum(r for _, _, r, _ in xl) / args.steps
+        x_sent = sum(sn for _, _, _, sn in xl) / args.steps
+        exchange = {"strategy_pkfk": hp.strategy, "all_to_all_ms_per_step": x_ms,
+                    "recv_bytes_per_step": x_recv, "sent_bytes_per_step": x_sent,
+                    "nvlink_recv_GBps": x_recv / (x_ms / 1e3) / 1e9 if x_ms > 0 else None,
+                    "how": "CUDA events around every all_to_all of the step's two joins on this rank (rank 0 shown)"}
     ms_local = t0.elapsed_time(t1)
     kstats = hp.ctx.kernel_stats()
     hp.ctx.set_profiling(False)
     launches = hp.ctx.launch_count()
     hp.collect_ops()
     op_ms = {k: v / args.steps for k, v in hp.op_ms.items()}
+    peak_gbs, _ = peaks()
+    operators = {k: {"ms": op_ms[k], "compulsory_bytes": b, "GBps": b / (op_ms[k] / 1e3) / 1e9,
+                     "frac_measured_peak": b / (op_ms[k] / 1e3) / 1e9 / peak_gbs,
+                     "frac_8TBps": b / (op_ms[k] / 1e3) / 1e9 / 8000.0}
+                 for k, b in cbytes.items() if op_ms.get(k)}
+    general = general_route_pkfk(hp) if world == 1 else None
 
     # ---------------- end to end: pinned host inputs -> device -> step -> pinned host results
     host_cols = {"o_orderkey": orders["o_orderkey"]}
@@ -383,7 +438,10 @@ def run_gpu(args):
                 "sf_per_rank": SF_PER_RANK,
                 "lineitem_rows_per_rank": hp.n,
                 "orders_rows_per_rank": hp.ok.numel(),
-                "layout": f"{args.layout}; ranks co-partitioned (lineitem range-partitioned with its orders)",
+                "layout": f"lineitem rows {args.layout}",
+                "placement": (placement + (": every rank's lineitem references orders on every rank; the "
+                              "joins exchange (key, global row) over NCCL" if placement == "exchange" else
+                              ": each rank's lineitem references only its own orders (no join exchange)")),
                 "parallelism": f"dp{world}",
                 "l2": "inputs larger than L2: 2.8 GB of columns per rank per step vs 126 MB L2 (no flush needed)",
             },
@@ -400,6 +458,11 @@ def run_gpu(args):
                          "avg_launch_ms": kms / max(klaunch, 1), "launches": klaunch,
                          "share_of_step": kms / ms_total if ms_total else None},
             "operators_ms": op_ms,
+            "operators": operators,
+            "operators_how": "per-operator CUDA events inside the timed steps; compulsory bytes per SURVEY.md "
+                             "§8(d) (sort 24 B/key, index pairs 16 B, columns read once); frac against the "
+                             "measured copy peak and against 8 TB/s",
+            "pkfk_general_route": general,
             "probe_rows_per_s": hp.n / (op_ms.get("pkfk_join", float("nan")) / 1e3),
             "groupby_rows_per_s": hp.n / (op_ms.get("q1_groupby", float("nan")) / 1e3),
             "kernels_how": f"every launch bracketed by events over {prof_steps} untimed steps "
@@ -408,12 +471,74 @@ def run_gpu(args):
                             "algorithmic_GBps": (v[2] / v[0] / 1e6) if v[0] > 0 else None}
                         for k, v in sorted(ktable.items(), key=lambda kv: -kv[1][0])},
         }
+        if exchange is not None:
+            line["exchange"] = exchange
         if not args.no_cpu_baseline and world == 1:   # the oracle baseline: rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(hp, args)
+        if world == 1 and not args.no_sf100:
+            del hp
+            line["sf100"] = sf100_ops(T, dev, peak_gbs)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _timed(f, reps):
+    f()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        f()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def general_route_pkfk(hp, reps=5):
+    """The PK-FK join when the build side is NOT already in key order (orders shuffled by a
+    seeded permutation, made outside the timed region): the radix-sorted build side and
+    the slot-table probe instead of the presorted rank-bitmap route of the main step."""
+    g = torch.Generator(device=hp.ok.device).manual_seed(7)
+    ok_shuf = hp.ok[torch.randperm(hp.ok.numel(), device=hp.ok.device, generator=g)]
+    ms = _timed(lambda: hp.ctx.pkfk_join(ok_shuf, hp.lk), reps)
+    nb, npr = ok_shuf.numel(), hp.lk.numel()
+    b = 24 * nb + 8 * nb + 8 * npr + 16 * npr
+    out = {"ms": ms, "compulsory_bytes": b, "GBps": b / (ms / 1e3) / 1e9, "probe_rows_per_s": npr / (ms / 1e3),
+           "how": "orders keys permuted (seed 7) outside the timing; median-free mean of 5 calls, CUDA events"}
+    del ok_shuf
+    return out
+
+
+def sf100_ops(T, dev, peak_gbs, reps=3):
+    """SF100 on one GPU (BASELINE configs[4]'s per-GPU size at N = 1; the north-star target
+    operators): PK-FK join (150M orders x ~600M lineitem) and Q1, CUDA events around each
+    call, after one untimed call."""
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    orders, li = tpch_orders_lineitem(100.0, seed=42, device=dev, layout="shuffled")
+    ok, lk = orders["o_orderkey"], li["l_orderkey"]
+    q1 = columns(li, Q1_COLS)
+    keep = set(Q1_COLS) | {"l_orderkey"}
+    for k in list(li):
+        if k not in keep:
+            del li[k]
+    ctx = T.context()
+    res = {}
+    ms = _timed(lambda: ctx.pkfk_join(ok, lk), reps)
+    nb, npr = ok.numel(), lk.numel()
+    b = 24 * nb + 8 * nb + 8 * npr + 16 * npr
+    res["pkfk_join"] = {"ms": ms, "compulsory_bytes": b, "GBps": b / (ms / 1e3) / 1e9,
+                        "frac_measured_peak": b / (ms / 1e3) / 1e9 / peak_gbs, "probe_rows_per_s": npr / (ms / 1e3)}
+    ms = _timed(lambda: ctx.groupby_agg(q1, Q1_KEYS, Q1_AGGS, Q1_PREDS), reps)
+    b = sum(c.element_size() for c in q1) * npr
+    res["q1_groupby"] = {"ms": ms, "compulsory_bytes": b, "GBps": b / (ms / 1e3) / 1e9,
+                         "frac_measured_peak": b / (ms / 1e3) / 1e9 / peak_gbs, "rows_per_s": npr / (ms / 1e3)}
+    res["rows"] = {"orders": nb, "lineitem": npr}
+    del orders, li, ok, lk, q1
+    torch.cuda.empty_cache()
+    return res
 
 
 # ------------------------------------------------------------ CPU oracle leg
@@ -486,7 +611,10 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (in-repo TPC-H-shaped generator, seed 42)",
         "config": {"workload": "tpch_sf10_hot_path: pkfk_join + smj_join(orders x lineitem) + Q1 groupby + "
-                               "Q6 filter/sum", "sf_per_rank": SF_PER_RANK, "parallelism": "host oracle"},
+                               "Q6 filter/sum", "sample_sf": sfs,
+                   "sample": f"each step runs the workload's operators on a bounded SF{sfs} sample "
+                             f"({n} lineitem rows), not the SF{SF_PER_RANK:g} batch",
+                   "parallelism": "host oracle, 1 core"},
         "cpu_baseline": {"value": v, "unit": "rows/s", "cores": 1, "kind": "oracle",
                          "sample": f"TPC-H-shaped SF{sfs} ({n} lineitem rows) per step; single-threaded C oracle"},
         "e2e": {"value": v, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -504,6 +632,10 @@ def main():
     # paper-torch: the paper's tensor programs as torch ops on the same GPU (comparison only)
     ap.add_argument("--impl", default="tqp", choices=["tqp", "reference", "paper-torch"])
     ap.add_argument("--layout", default="shuffled", choices=["shuffled", "clustered"])
+    # N > 1: exchange (default) = lineitem's orders spread over all ranks, joins exchange over
+    # NCCL; local = each rank's lineitem joins only its own orders
+    ap.add_argument("--placement", default=None, choices=["exchange", "local"])
+    ap.add_argument("--no-sf100", action="store_true", help="skip the SF100 single-GPU operator section")
     ap.add_argument("--cpu-sample-sf", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -42,6 +42,11 @@ import torch.distributed as dist
 
 # --------------------------------------------------------------------- plumbing
 
+# Exchange instrumentation (bench.py): when a list, every all_to_all_v appends
+# (start event, end event, bytes received from other ranks, bytes sent to other ranks).
+EXCHANGE_LOG = None
+
+
 class _Comm:
     """Collectives on one process group; gloo gets host copies of device tensors."""
 
@@ -103,12 +108,20 @@ class _Comm:
         """all_to_all_single of a 1-D tensor with host split sizes; blocks arrive in
         source-rank order."""
         out = torch.empty(sum(recv), dtype=t.dtype, device=t.device)
+        log = EXCHANGE_LOG is not None and t.is_cuda
+        if log:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
         if self.stage and t.is_cuda:
             ho = torch.empty(sum(recv), dtype=t.dtype)
             dist.all_to_all_single(ho, t.cpu(), recv, send, group=self.group)
             out.copy_(ho)
         else:
             dist.all_to_all_single(out, t.contiguous(), recv, send, group=self.group)
+        if log:
+            e1.record()
+            es = t.element_size()
+            EXCHANGE_LOG.append((e0, e1, (sum(recv) - recv[self.rank]) * es, (sum(send) - send[self.rank]) * es))
         return out
 
 
