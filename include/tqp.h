@@ -82,6 +82,10 @@ int tqp_abi_version(void);
  * (profiled launches), bytes_host[k] (algorithmic bytes, all launches).
  * names_host: '\n'-separated kernel names written into a caller buffer. */
 int64_t tqp_ctx_launch_count(const tqp_ctx* ctx);
+/* Checked mode (environment TQP_ALLOC_EXACT=1 at context creation; test builds):
+ * every temporary is its own cudaMalloc followed by 256 canary bytes, verified when
+ * the temporary is released; returns the number of overwritten canaries seen. */
+int64_t tqp_ctx_guard_violations(const tqp_ctx* ctx);
 void tqp_ctx_reset_counters(tqp_ctx* ctx);
 tqp_status tqp_ctx_set_profiling(tqp_ctx* ctx, int enable);
 /* Restrict profiling to kernels whose name starts with name_prefix (NULL or ""
@@ -176,6 +180,18 @@ tqp_status tqp_pkfk_join_hash(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build,
  * side is already in key order: its duplicate flag is read before the probe). */
 tqp_status tqp_pkfk_outer(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys, int64_t n_probe,
                           int64_t* left_out, uint8_t* match_out, int64_t* n_match_host);
+
+/* Outer join preserving the BUILD (primary-key) side -- TPC-H Q13's customer
+ * LEFT OUTER JOIN orders shape, where every customer appears with each of its
+ * orders or once with a NULL (PAPER.md:1218 names TQP's left outer join as slow;
+ * SURVEY.md §8(f) NEXT 1). Output: the inner pairs exactly as tqp_pkfk_join
+ * returns them (ascending probe row), followed by (b, -1) for every build row b
+ * that no probe row matches, ascending b; right_out = -1 is the match flag.
+ * left_out / right_out: device int64, capacity n_probe + n_build (caller-
+ * allocated); *n_out_host = pairs + unmatched build rows. Duplicate build keys ->
+ * TQP_ERR_DUPLICATE_BUILD_KEY. n_build < 2^32. Synchronises three times. */
+tqp_status tqp_pkfk_outer_build(tqp_ctx* ctx, tqp_col build_keys, int64_t n_build, tqp_col probe_keys,
+                                int64_t n_probe, int64_t* left_out, int64_t* right_out, int64_t* n_out_host);
 
 /* ------------------------------------------------ m:n sort-merge join */
 /* (3) Generic sort-merge join -- Alg. 1 (prose :1114-1137)

@@ -34,14 +34,14 @@ MAX_PREDS, MAX_KEYS, MAX_AGGS = 16, 8, 16
 
 EXPORTED = [
     "tqp_abi_version", "tqp_ctx_create", "tqp_ctx_destroy", "tqp_ctx_set_stream", "tqp_last_error",
-    "tqp_ctx_launch_count", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_set_profiling_filter",
+    "tqp_ctx_launch_count", "tqp_ctx_guard_violations", "tqp_ctx_reset_counters", "tqp_ctx_set_profiling", "tqp_ctx_set_profiling_filter",
     "tqp_ctx_kernel_stats",
     "tqp_sort", "tqp_pkfk_join", "tqp_pkfk_semi", "tqp_pkfk_outer", "tqp_pkfk_join_payload", "tqp_pkfk_join_hash",
     "tqp_pkfk_join_i32", "tqp_pkfk_join_paper_order", "tqp_smj_prepare", "tqp_smj_expand", "tqp_smj_expand_i32", "tqp_smj_expand_checksum",
     "tqp_smj_release",
     "tqp_smj_join", "tqp_pack_keys", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge", "tqp_smj_expand_payload", "tqp_partition", "tqp_minmax",
-    "tqp_range_splitters", "tqp_gather",
+    "tqp_range_splitters", "tqp_gather", "tqp_pkfk_outer_build",
 ]
 
 
@@ -67,6 +67,7 @@ _sig = {
     "tqp_ctx_set_stream": ([_vp, _vp], _int),
     "tqp_last_error": ([_vp], ctypes.c_char_p),
     "tqp_ctx_launch_count": ([_vp], _i64),
+    "tqp_ctx_guard_violations": ([_vp], _i64),
     "tqp_ctx_reset_counters": ([_vp], None),
     "tqp_ctx_set_profiling": ([_vp, _int], _int),
     "tqp_ctx_set_profiling_filter": ([_vp, ctypes.c_char_p], _int),
@@ -92,6 +93,7 @@ _sig = {
     "tqp_minmax": ([_vp, Col, _i64, _vp], _int),
     "tqp_range_splitters": ([_vp, _vp, _int, _vp], _int),
     "tqp_gather": ([_vp, Col, _vp, _i64, _vp], _int),
+    "tqp_pkfk_outer_build": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
     "tqp_smj_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _i64, _P(_i64)], _int),
     "tqp_filter_compact": ([_vp, _P(Col), _int, _i64, _P(Pred), _int, _vp, _vp, _P(_i64)], _int),
     "tqp_groupby_prepare": ([_vp, _P(Col), _int, _i64, _P(ctypes.c_int32), _int, _P(Pred), _int, _P(Agg), _int,
@@ -189,6 +191,10 @@ class Context:
 
     def launch_count(self):
         return _lib.tqp_ctx_launch_count(self._h)
+
+    def guard_violations(self):
+        """Overwritten canaries after temporaries (checked mode, TQP_ALLOC_EXACT=1)."""
+        return _lib.tqp_ctx_guard_violations(self._h)
 
     def reset_counters(self):
         _lib.tqp_ctx_reset_counters(self._h)
@@ -328,6 +334,20 @@ class Context:
         self._check(_lib.tqp_pkfk_outer(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(left), _ptr(mask),
                                         ctypes.byref(m)))
         return (left, mask) if return_mask else left
+
+    def pkfk_outer_build(self, build_keys, probe_keys):
+        """Outer join preserving the build side (Q13's customer LEFT OUTER JOIN orders):
+        the inner pairs (ascending probe row), then (b, -1) for each unmatched build row."""
+        self._sync_stream()
+        b = _dev_tensor(build_keys, self.device)
+        p = _dev_tensor(probe_keys, self.device)
+        cap = b.numel() + p.numel()
+        lo = torch.empty(cap, dtype=torch.int64, device=self.device)
+        ro = torch.empty(cap, dtype=torch.int64, device=self.device)
+        m = ctypes.c_int64(0)
+        self._check(_lib.tqp_pkfk_outer_build(self._h, _col(b), b.numel(), _col(p), p.numel(), _ptr(lo), _ptr(ro),
+                                              ctypes.byref(m)))
+        return lo[:m.value], ro[:m.value]
 
     def smj_prepare(self, left, right):
         """Alg. 1 lines 1-9: sort, histograms, products, prefix sums -> SmjPlan (size known)."""
@@ -632,6 +652,10 @@ def pkfk_outer(build_keys, probe_keys, return_mask=False):
 
 def smj_join_payload(left, right, left_payload=(), right_payload=(), indices=False):
     return context().smj_join_payload(left, right, left_payload, right_payload, indices)
+
+
+def pkfk_outer_build(build_keys, probe_keys):
+    return context().pkfk_outer_build(build_keys, probe_keys)
 
 
 def partition(keys, splitters, row_base=0, rows=True):

@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary of libtqp (declared in include/tqp.h).
 // Every entry point converts internal exceptions into a tqp_status and a
 // message; nothing C++ crosses the ABI.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -30,6 +31,7 @@ tqp_groupby_plan* groupby_merge(tqp_ctx*, int64_t, const tqp_col*, int, const tq
 void smj_expand_payload(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, const tqp_col*, int, void* const*,
                         const tqp_col*, int, void* const*, int64_t*, int64_t*);
 void partition(tqp_ctx*, tqp_col, int64_t, const int64_t*, int, int64_t, void*, int64_t*, int64_t*);
+void pkfk_outer_build(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
 void minmax(tqp_ctx*, tqp_col, int64_t, int64_t*);
 void range_splitters(tqp_ctx*, const int64_t*, int, int64_t*);
 void gather(tqp_ctx*, tqp_col, const int64_t*, int64_t, void*);
@@ -46,13 +48,14 @@ static size_t round_block(size_t b) {
 
 void* tqp_ctx::dalloc(size_t bytes) {
     if (bytes == 0) return nullptr;
-    if (exact_alloc) {
+    if (exact_alloc) {   // exact size + GUARD canary bytes (0xA5), checked at release
         void* p = nullptr;
-        cudaError_t e = cudaMalloc(&p, bytes);
+        cudaError_t e = cudaMalloc(&p, bytes + GUARD);
         if (e != cudaSuccess) {
             cudaGetLastError();
             tqp::fail(TQP_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
         }
+        TQP_CUDA(cudaMemsetAsync(static_cast<char*>(p) + bytes, 0xA5, GUARD, stream));
         live_blocks[p] = bytes;
         return p;
     }
@@ -85,7 +88,17 @@ void tqp_ctx::dfree(void* p) {
     auto it = live_blocks.find(p);
     if (it == live_blocks.end()) return;
     if (exact_alloc) {
+        unsigned char g[GUARD];
         cudaStreamSynchronize(stream);
+        if (cudaMemcpy(g, static_cast<char*>(p) + it->second, GUARD, cudaMemcpyDeviceToHost) == cudaSuccess) {
+            for (size_t i = 0; i < GUARD; i++)
+                if (g[i] != 0xA5) {
+                    guard_violations++;
+                    fprintf(stderr, "libtqp: guard bytes after a %zu-byte temporary overwritten (offset %zu)\n",
+                            it->second, i);
+                    break;
+                }
+        }
         cudaFree(p);
         live_blocks.erase(it);
         return;
@@ -188,6 +201,8 @@ tqp_status tqp_ctx_set_stream(tqp_ctx* c, void* stream) {
 const char* tqp_last_error(const tqp_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 int64_t tqp_ctx_launch_count(const tqp_ctx* c) { return c ? c->launches : 0; }
+
+int64_t tqp_ctx_guard_violations(const tqp_ctx* c) { return c ? c->guard_violations : 0; }
 
 void tqp_ctx_reset_counters(tqp_ctx* c) {
     if (!c) return;
@@ -432,6 +447,14 @@ tqp_status tqp_smj_expand_payload(tqp_ctx* c, const tqp_smj_plan* plan, int64_t 
             tqp::fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_payload: null payload array");
         tqp::smj_expand_payload(c, plan, begin, end, left_payload, n_left_payload, left_payload_out, right_payload,
                                 n_right_payload, right_payload_out, left_out_idx, right_out_idx);
+    });
+}
+
+tqp_status tqp_pkfk_outer_build(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, int64_t np, int64_t* left_out,
+                                int64_t* right_out, int64_t* n_out_host) {
+    TQP_GUARD(c, {
+        if (!n_out_host) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_outer_build: null n_out_host");
+        tqp::pkfk_outer_build(c, b, nb, p, np, left_out, right_out, n_out_host);
     });
 }
 

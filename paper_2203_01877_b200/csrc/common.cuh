@@ -20,6 +20,29 @@
 #error "libtqp is written for sm_100a (B200) only"
 #endif
 
+// Checked build (-DTQP_CHECKED=1; compute-sanitizer is not available on the GPU pool):
+// device-side bounds checks on the global stores whose index the kernel computes (scatter
+// destinations, compaction offsets, expansion positions, partial-record slots); a failed
+// check prints the condition and traps, so the test that ran it fails loudly.
+#ifndef TQP_CHECKED
+#define TQP_CHECKED 0
+#endif
+#if TQP_CHECKED
+#include <cstdio>
+#define TQP_DCHECK(c)                                                                          \
+    do {                                                                                       \
+        if (!(c)) {                                                                            \
+            printf("TQP_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,     \
+                   (int)blockIdx.x, (int)threadIdx.x, #c);                                     \
+            __trap();                                                                          \
+        }                                                                                      \
+    } while (0)
+#else
+#define TQP_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
+
 namespace tqp {
 
 struct Error {
@@ -53,6 +76,8 @@ struct tqp_ctx {
     // freed (after a stream sync) when released, so memcheck sees out-of-bounds accesses
     // that a cached, rounded-up block would hide
     bool exact_alloc = false;
+    static constexpr size_t GUARD = 256;   // exact mode: canary bytes after every temporary
+    int64_t guard_violations = 0;          // canaries found overwritten at release
     void* dalloc(size_t bytes);
     void dfree(void* p);
     void trim();

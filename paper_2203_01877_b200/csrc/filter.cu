@@ -149,6 +149,7 @@ __global__ void __launch_bounds__(FNT) filter_sel_kernel(const uint8_t* __restri
         if (m[i]) s_out[lp++] = r0 + i;
     __syncthreads();
     int64_t* dst = sel + excl;
+    TQP_DCHECK(excl + (int64_t)tot <= n && lp <= (uint32_t)FTILE);
     for (uint32_t k = tid; k < tot; k += FNT) __stcs(reinterpret_cast<long long*>(dst + k), (long long)s_out[k]);
 }
 }  // namespace

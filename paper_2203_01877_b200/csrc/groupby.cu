@@ -528,6 +528,7 @@ __device__ void process_tile(const Phase1Args& a, const uint8_t* st, Work& w, in
     // 5. partial records: key and count; per-run accumulators live in shared memory
     //    when the tile has few runs (the partial slots are private to this tile),
     //    else directly in the tile's global partial slots
+    TQP_DCHECK(pb + U <= a.cap);
     for (int u = tid; u < U; u += GNT) {
         a.pkey[pb + u] = sk[w.rstart[u]] + kmin;
         a.pcount[pb + u] = (int64_t)w.rstart[u + 1] - w.rstart[u];
@@ -1429,6 +1430,7 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     }
     for (int d = tid; d < D; d += NT) {
         const int64_t rec = h.drec[d];
+        TQP_DCHECK(rec < a.cap);
         if (rec >= 0) { a.pkey[rec] = a.dkeys[d]; a.pcount[rec] = h.dcnt[d]; }
     }
 }

@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(QNT) part_scatter_kernel(const void* __restric
         if (row >= n) continue;
         const int d = dd[s];
         const int64_t p = (int64_t)s_off[d] + s_wc[warp][d] + pos[s];
+        TQP_DCHECK(d < parts && p >= 0 && p < n);
         st_key<DT>(keys_out, p, k[s]);
         if (rows_out) __stcs((long long*)rows_out + p, (long long)(row_base + row));
     }

@@ -176,6 +176,7 @@ struct ProbeArgs {
     uint32_t* tcnt;           // per tile: rows selected (join: matches; semi: match != anti)
     uint64_t blo, bhi;        // multi-pass probe: the bucket range this pass resolves
     const uint4* rank_bm;     // nullable: rank bitmap of a presorted build side (RB_BITS bits per 32-byte block)
+    int64_t n_build;          // build rows (bounds checks of the checked build)
     // join mode, direct output: when *direct == 0 (no sampled miss, probe_sample_kernel)
     // the probe writes the final pairs at their probe row -- left = build row (or -1),
     // right = row -- instead of the u32 build row for the compaction pass; exact when every
@@ -483,6 +484,7 @@ __global__ void __launch_bounds__(PNT, TQP_SECTOR_MINB) probe_sector_kernel(Prob
     for (int i = 0; i < PIPT; i++) {
         const int64_t row = base + i * PNT + tid;
         if (row >= a.n_probe) continue;
+        TQP_DCHECK(!m[i] || (int64_t)left[i] < a.n_build);
         if (direct) {
             if (a.idx32) {
                 __stcs((int*)a.out_l + row, m[i] ? (int)left[i] : -1);
@@ -690,6 +692,7 @@ __device__ __forceinline__ void emit_tile(int64_t t, const uint32_t* __restrict_
     const int64_t excl = (int64_t)toff[t];
     const uint32_t tot = (uint32_t)(toff[t + 1] - toff[t]);
     if (tot == 0) return;
+    TQP_DCHECK(tot <= (uint32_t)PTILE && excl + (int64_t)tot <= np);
     const int64_t r0 = base + (int64_t)tid * PIPT;
     const bool full = base + PTILE <= np;
     uint32_t l[PIPT];
@@ -901,6 +904,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         ProbeArgs a{};
         a.probe = pk.data;
         a.n_probe = np;
+        a.n_build = nb;
         a.bkeys = B.so.k32 ? (const void*)B.so.keys32.get() : (const void*)B.so.keys64.get();
         a.bperm = B.so.perm32.get();
         a.T = B.T;
@@ -1070,6 +1074,15 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
                                                     : (right_out ? 8.0 * (double)h[0] : 0.0));
     }
 }
+// Marks the build rows that some pair references (idempotent byte stores).
+__global__ void mark_rows_kernel(const int64_t* __restrict__ left, int64_t m, int64_t nb, uint8_t* __restrict__ matched) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = __ldcs((const long long*)left + i);
+        TQP_DCHECK(b >= 0 && b < nb);
+        matched[b] = 1;
+    }
+}
+
 // ---------------------------------------------------------- hash-join ablation
 // the generic hash join the paper compares against (OmniSciDB's
 // hash aggregation / join beat TQP's sort-based operators on Q1 / Q9), as a
@@ -1322,6 +1335,45 @@ void pkfk_outer(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, in
     int64_t m = 0;
     run_probe(ctx, B, pk, np, 2, 0, left_out, nullptr, match_out, &m);
     if (n_match_host) *n_match_host = m;
+}
+
+// Outer join preserving the build (primary-key) side -- TPC-H Q13's customer LEFT OUTER
+// JOIN orders shape (the left outer join TQP found slow; SURVEY.md §8(f)
+// NEXT 1): the inner pairs exactly as tqp_pkfk_join returns them (ascending probe row),
+// then (b, -1) for every build row b that no probe row matches, ascending b. Capacity of
+// both outputs: n_probe + n_build.
+void pkfk_outer_build(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int64_t* left_out,
+                      int64_t* right_out, int64_t* n_out_host) {
+    check_col(bk, nb, "outer build");
+    check_col(pk, np, "outer probe");
+    if (nb + np > 0 && (!left_out || !right_out)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_outer_build: null output");
+    if (np >= (int64_t(1) << 40) || nb >= (int64_t(1) << 32)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk_outer_build: too large");
+    int64_t m = 0;
+    pkfk_join(ctx, bk, nb, pk, np, left_out, right_out, &m);
+    if (nb == 0) {
+        *n_out_host = m;
+        return;
+    }
+    DevBuf<uint8_t> matched(ctx, nb);
+    matched.zero();
+    if (m > 0) {
+        const int g = (int)std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->num_sms * 8);
+        launch(ctx, "tqp_pkfk_outer_mark", mark_rows_kernel, dim3(g), dim3(256), 0, (const int64_t*)left_out, m, nb,
+               matched.get());
+        ctx->add_bytes("tqp_pkfk_outer_mark", 9.0 * (double)m);
+    }
+    // unmatched build rows = the selection vector of (matched == 0), appended after the pairs
+    tqp_col mc{};
+    mc.data = matched.get();
+    mc.dtype = TQP_U8;
+    tqp_pred pr{};
+    pr.col = 0;
+    pr.op = TQP_EQ;
+    pr.value = 0;
+    int64_t u = 0;
+    filter_compact(ctx, &mc, 1, nb, &pr, 1, nullptr, left_out + m, &u);
+    if (u > 0) TQP_CUDA(cudaMemsetAsync(right_out + m, 0xFF, (size_t)u * 8, ctx->stream));
+    *n_out_host = m + u;
 }
 
 }  // namespace tqp

@@ -514,6 +514,7 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
     __shared__ __align__(16) uint32_t s_l[ETILE], s_r[ETILE];
     const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
     const int64_t c1 = min(c0 + ETILE, end);
+    TQP_DCHECK(c0 < c1);
     // buckets of outputs c0 and c1 - 1 lie in [b0, b1]: at most two output tiles' worth
     int64_t b0, b1;
     if (tg_shift == 0) {
@@ -557,6 +558,7 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
             if (s_cum[mid] <= rel) lo = mid + 1; else hi = mid;
         }
         int bi = lo;   // bucket index relative to b0
+        TQP_DCHECK(bi < nb && b0 + bi < K);
         auto load = [&](int i, int64_t& L, int64_t& R, int64_t& sL, int64_t& sR) {
             if (meta) {
                 L = s_m[i]; R = s_m[MCAP + i]; sL = s_m[2 * MCAP + i]; sR = s_m[3 * MCAP + i];
@@ -581,6 +583,7 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
 #pragma unroll
         for (int j = 0; j < EIPT; j++) {
             if (j >= cnt) break;
+            TQP_DCHECK(q < L && r < R);
             vl[j] = __ldg(perm_l + sL + q);
             vr[j] = __ldg(perm_r + sR + r);
             if (CK) {

@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                 for (int j = tid; j < tile_n; j += NT) {
                     const uint2 v = kp[kslot(j)];
                     const uint32_t dst = s.gstart[(v.x >> a.shift) & DM] + (uint32_t)j;
+                    TQP_DCHECK((int64_t)dst < a.n);
                     if (TQP_SCATTER_HINTS & 2) {
                         st_hint_u32(reinterpret_cast<uint32_t*>(ok + dst), (uint32_t)v.x, opol);
                         st_hint_u32(op + dst, v.y, opol);
@@ -630,6 +631,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                     const KT kk = sizeof(KT) == 4 ? (KT)kp[kslot(j)].x : s.u.sorted.keys[kslot(j)];
                     const uint32_t p = sizeof(KT) == 4 ? kp[kslot(j)].y : s.u.sorted.perm[kslot(j)];
                     const uint32_t dst = s.gstart[(uint32_t)(kk >> a.shift) & DM] + (uint32_t)j;
+                    TQP_DCHECK((int64_t)dst < a.n);
                     if (ok) ok[dst] = kk;
                     if (op) op[dst] = p;
                 }
@@ -640,6 +642,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             const uint32_t p = sizeof(KT) == 4 ? kp[kslot(j)].y : s.u.sorted.perm[kslot(j)];
             const uint32_t d = (uint32_t)(kk >> a.shift) & DM;
             const int64_t dst = (int64_t)(uint32_t)(s.gstart[d] + (uint32_t)j);   // gdelta[d] + j (mod 2^32, n < 2^30)
+            TQP_DCHECK(dst < a.n);
             if (a.out_keys) ((KT*)a.out_keys)[dst] = kk;
             if (a.out_perm) a.out_perm[dst] = p;
             if (a.out_perm64) a.out_perm64[dst] = (int64_t)p;

@@ -28,3 +28,13 @@ def sf001():
 
 
 Q1_SHIPDATE_MAX = 10471  # 1998-09-02 (TPC-H Q1: l_shipdate <= date '1998-12-01' - 90 days)
+
+
+@pytest.fixture(autouse=True)
+def _checked_mode_guards(request):
+    """Checked mode (TQP_ALLOC_EXACT=1, tools/gpu_checked.sh): after every GPU test, no
+    canary after a libtqp temporary may have been overwritten."""
+    yield
+    if os.environ.get("TQP_ALLOC_EXACT") == "1" and request.node.get_closest_marker("gpu"):
+        import paper_2203_01877_b200 as T
+        assert T.context().guard_violations() == 0, "libtqp wrote past the end of a temporary"

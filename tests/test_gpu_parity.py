@@ -1176,3 +1176,31 @@ def test_smj_expand_payload(T, case):
     plan.release()
     (g,), (h,), _ = T.smj_join_payload(cu(left), cu(right), [lp[0]], [rp[0]])
     assert torch.equal(g.cpu(), lp[0].cpu()[torch.as_tensor(wl)])
+
+
+@pytest.mark.parametrize("nb,np_,span,presorted", [(0, 100, 10, False), (100, 0, 10, False), (1, 1, 5, False),
+                                                   (5_000, 20_000, 20_000, False), (150_000, 1_500_000, 150_000, True),
+                                                   (300_001, 123_457, 2_000_000, True), (300_001, 1_000_003, 400_000, False)])
+def test_pkfk_outer_build_q13_shape(T, nb, np_, span, presorted):
+    """Outer join preserving the build side (Q13: customer LEFT OUTER JOIN orders): the
+    oracle's inner pairs in probe order, then every build row without a match, ascending,
+    with right = -1. TPC-H-like case: 150K customers, 1.5M orders over 2/3 of them."""
+    rng = np.random.default_rng(nb + np_)
+    build = rng.permutation(span)[:nb].astype(np.int64)
+    if presorted:
+        build = np.sort(build)
+    if span == 150_000:   # orders reference customers whose key is not 0 mod 3 (TPC-H rule)
+        probe = rng.integers(0, span // 3, np_) * 3 + rng.integers(1, 3, np_)
+    else:
+        probe = rng.integers(-5, span + 5, np_).astype(np.int64)
+    lo, ro = T.pkfk_outer_build(cu(build), cu(probe))
+    olo, oro = oracle.pkfk_join(build, probe)
+    unmatched = np.setdiff1d(np.arange(nb), olo)
+    assert np.array_equal(npy(lo), np.concatenate([olo, unmatched]))
+    assert np.array_equal(npy(ro), np.concatenate([oro, np.full(len(unmatched), -1)]))
+
+
+def test_pkfk_outer_build_duplicate_key(T):
+    with pytest.raises(T.TqpError) as e:
+        T.pkfk_outer_build(cu(np.array([4, 4, 1])), cu(np.array([4, 1])))
+    assert e.value.status == T.TQP_ERR_DUPLICATE_BUILD_KEY
