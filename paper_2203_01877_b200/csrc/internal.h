@@ -20,6 +20,7 @@ struct SortOut {
     // results
     bool k32 = false;                  // internal keys are the low 32 bits of u
     uint64_t and_bits = 0, or_bits = 0;   // AND / OR of all u (varying-bit mask = and ^ or)
+    uint64_t first_u = 0, last_u = 0;     // u of keys[0] and keys[n - 1] (= min / max when identity)
     int passes = 0;
     bool identity = false;             // the input was already in (key, row) order: perm = 0..n-1
     DevBuf<uint32_t> keys32;           // internal sorted keys (k32)
@@ -27,13 +28,16 @@ struct SortOut {
     DevBuf<uint32_t> perm32;           // internal permutation
 };
 
-// andor (nullable, 3 words): the AND / OR of the sort-domain keys and an "out of order"
-// flag (0 = already sorted), read back by the caller from sort_andor (so several sorts
-// share one host sync); null = computed here.
+// andor (nullable, SORT_PLAN_WORDS words): the AND / OR of the sort-domain keys, an "out
+// of order" flag (0 = already sorted) and the sort-domain values of the first and last
+// key, read back by the caller from sort_andor (so several sorts share one host sync);
+// null = computed here.
 // th0 (nullable, sort_hist0_words(n) u32): the first-pass histogram sort_andor fused in.
+constexpr int SORT_PLAN_WORDS = 5;
 void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& out,
                 const uint64_t* andor = nullptr, uint32_t* th0 = nullptr);
-// AND / OR of the sort-domain keys into ao[0..1] (device, stream-ordered; no sync); with
+// AND / OR of the sort-domain keys into ao[0..1], the unsorted flag into ao[2], the first /
+// last key's sort-domain value into ao[3..4] (device, stream-ordered; no sync); with
 // th0, also the speculative pass-0 tile histogram (9-bit digits at bit 0, 4096-key tiles)
 void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao,
                 uint32_t* th0 = nullptr);

@@ -800,12 +800,21 @@ static bool force_radix() {
     return f;
 }
 
+template <int IN>
+__global__ void first_last_kernel(const void* keys, int64_t n, bool desc, unsigned long long* out) {
+    out[threadIdx.x] = load_u<IN>(keys, threadIdx.x == 0 ? 0 : n - 1, desc);
+}
+
 void sort_andor(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, unsigned long long* ao,
                 uint32_t* th0) {
     TQP_CUDA(cudaMemsetAsync(ao, 0xFF, 8, ctx->stream));
-    TQP_CUDA(cudaMemsetAsync(ao + 1, 0, 16, ctx->stream));
+    TQP_CUDA(cudaMemsetAsync(ao + 1, 0, 32, ctx->stream));
     if (n <= 0) return;
     const int mode = in_mode(dtype);
+    dispatch_in(mode, [&](auto m) {
+        if constexpr (decltype(m)::value != IN_INTERNAL)
+            launch(ctx, "tqp_sort_andor", first_last_kernel<decltype(m)::value>, dim3(1), dim3(2), 0, keys, n, desc, ao + 3);
+    });
     const int grid = (int)std::min<int64_t>(ceil_div(n, NT * 8), (int64_t)ctx->num_sms * 4);
     dispatch_in(mode, [&](auto m) {
         if constexpr (decltype(m)::value != IN_INTERNAL) {
@@ -850,23 +859,23 @@ void radix_sort(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc,
     if (n < 0 || n >= (int64_t(1) << 30)) fail(TQP_ERR_INVALID_ARGUMENT, "sort: n must be in [0, 2^30)");
     if (n == 0) return;
     const int mode = in_mode(dtype);
-    uint64_t h[3];
+    uint64_t h[SORT_PLAN_WORDS];
     DevBuf<uint32_t> th0_own;
     if (andor) {   // the caller launched sort_andor and read the plan back (one sync for several sorts)
-        h[0] = andor[0];
-        h[1] = andor[1];
-        h[2] = andor[2];
+        for (int w = 0; w < SORT_PLAN_WORDS; w++) h[w] = andor[w];
     } else {
-        DevBuf<unsigned long long> ao(ctx, 3);
+        DevBuf<unsigned long long> ao(ctx, SORT_PLAN_WORDS);
         if (n >= (1 << 16) && mode != IN_INTERNAL) {   // large sorts: speculative pass-0 histogram
             th0_own.alloc(ctx, sort_hist0_words(n));
             th0 = th0_own.get();
         }
         sort_andor(ctx, keys, dtype, n, desc, ao.get(), th0);
-        read_back(ctx, h, ao.get(), 24);
+        read_back(ctx, h, ao.get(), 8 * SORT_PLAN_WORDS);
     }
     o.and_bits = h[0];
     o.or_bits = h[1];
+    o.first_u = h[3];
+    o.last_u = h[4];
     const uint64_t diff = h[0] ^ h[1];
     o.k32 = (diff >> 32) == 0;
     // digit plan: 8-bit digits over the bytes that vary, or 9-bit digits over the

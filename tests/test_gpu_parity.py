@@ -1178,7 +1178,7 @@ def test_smj_expand_payload(T, case):
     assert torch.equal(g.cpu(), lp[0].cpu()[torch.as_tensor(wl)])
 
 
-@pytest.mark.parametrize("nb,np_,span,presorted", [(0, 100, 10, False), (100, 0, 10, False), (1, 1, 5, False),
+@pytest.mark.parametrize("nb,np_,span,presorted", [(0, 100, 10, False), (100, 0, 1000, False), (1, 1, 5, False),
                                                    (5_000, 20_000, 20_000, False), (150_000, 1_500_000, 150_000, True),
                                                    (300_001, 123_457, 2_000_000, True), (300_001, 1_000_003, 400_000, False)])
 def test_pkfk_outer_build_q13_shape(T, nb, np_, span, presorted):
