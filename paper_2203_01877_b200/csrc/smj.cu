@@ -73,45 +73,54 @@ __device__ __forceinline__ int64_t bound_g(const KR* r, uint64_t hi_bits, int64_
     return lo;
 }
 
-template <typename KO>
-__device__ __forceinline__ int bound_s(const KO* s, int lo, int hi, KO k, bool upper) {
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (upper ? s[mid] <= k : s[mid] < k) lo = mid + 1; else hi = mid;
+// Galloping search from lo: probe lo, lo + 1, lo + 3, lo + 7, ... then bisect the last
+// gap. A sorted left tile's keys step through the right keys a few at a time (TPC-H: ~4
+// lineitems per order), so a search costs a couple of probes instead of log2(range).
+template <typename KR, typename KO>
+__device__ __forceinline__ int64_t gallop_g(const KR* r, uint64_t hi_bits, int64_t lo, int64_t hi, KO k, bool upper) {
+    int64_t step = 1, end = lo;
+    while (end < hi) {
+        const KO v = right_key<KR, KO>(r, hi_bits, end);
+        if (!(upper ? v <= k : v < k)) break;
+        lo = end + 1;
+        end = lo + step;
+        step <<= 1;
     }
-    return lo;
+    return bound_g<KR, KO>(r, hi_bits, lo, min(end, hi), k, upper);
 }
 
 // cumHistMul's input per bucket (= sorted left row b): R = count of right rows with the
-// row's key, startR = their first sorted position. Tile of JTILE left rows: the right
-// keys between the tile's first and last left key are staged in shared memory when they
-// fit (else the searches run in global memory); each thread takes JIPT consecutive rows,
-// equal keys reuse the previous bounds, a new key searches from the previous upper bound.
+// row's key, startR = their first sorted position. Tile of JTILE left rows, whose right
+// key range comes from tile_rbounds_kernel; each thread takes JIPT consecutive rows,
+// bisects the first key inside the tile's range, reuses the bounds for equal keys and
+// gallops from the previous upper bound for a new key (measured: staging the tile's right
+// range in shared memory held the kernel to 2 CTAs per SM, 0.29 ms at SF10).
 // Per tile: the sum of R (saturated at 2^62; an fp64 running total flags larger outSize).
-constexpr int BCAP = 8192;   // right keys staged per tile (32 KB of u32 / 64 KB of u64)
 constexpr uint64_t SUM_CAP = 1ull << 62;
+
+// Each tile's right key range [lower_bound(first left key), upper_bound(last left key)),
+// every tile's two searches in parallel (one thread each): a search at the head of the
+// bucket kernel itself put 2 x 26 dependent L2 round trips in front of every tile.
+template <typename KL, typename KR, typename KO>
+__global__ void tile_rbounds_kernel(LeftKeys lk, int64_t nl, const KR* __restrict__ rk, uint64_t rhi_bits, int64_t nr,
+                                    int64_t tiles, int64_t* __restrict__ rb) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= 2 * tiles) return;
+    const int64_t t = i >> 1;
+    if (i & 1) rb[i] = bound_g<KR, KO>(rk, rhi_bits, 0, nr, left_key<KL, KO>(lk, min((t + 1) * JTILE, nl) - 1), true);
+    else rb[i] = bound_g<KR, KO>(rk, rhi_bits, 0, nr, left_key<KL, KO>(lk, t * JTILE), false);
+}
 
 template <typename KL, typename KR, typename KO>
 __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, const KR* __restrict__ rk,
-                                                       uint64_t rhi_bits, int64_t nr, uint32_t* __restrict__ mR,
+                                                       uint64_t rhi_bits, int64_t nr, const int64_t* __restrict__ rb,
+                                                       uint32_t* __restrict__ mR,
                                                        uint32_t* __restrict__ msR, uint64_t* __restrict__ tsum,
                                                        double* dtot, int* overflow) {
-    extern __shared__ __align__(16) uint8_t smem_b[];
-    KO* s_r = reinterpret_cast<KO*>(smem_b);
-    __shared__ int64_t s_rng[2];
     __shared__ unsigned long long s_w[JNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * JTILE;
-    const int64_t last = min(base + JTILE, nl) - 1;
-    if (tid == 0) s_rng[0] = bound_g<KR, KO>(rk, rhi_bits, 0, nr, left_key<KL, KO>(lk, base), false);
-    if (tid == 32) s_rng[1] = bound_g<KR, KO>(rk, rhi_bits, 0, nr, left_key<KL, KO>(lk, last), true);
-    __syncthreads();
-    const int64_t rlo = s_rng[0], rhi = max(s_rng[1], rlo);
-    const bool staged = rhi - rlo <= BCAP;
-    if (staged) {
-        for (int64_t i = rlo + tid; i < rhi; i += JNT) s_r[i - rlo] = right_key<KR, KO>(rk, rhi_bits, i);
-    }
-    __syncthreads();
+    const int64_t rlo = rb[2 * blockIdx.x], rhi = max(rb[2 * blockIdx.x + 1], rlo);
     const int64_t r0 = base + (int64_t)tid * JIPT;
     uint64_t tot = 0;
     if (r0 < nl) {
@@ -123,15 +132,12 @@ __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, 
 #pragma unroll
         for (int i = 0; i < JIPT; i++) {
             if (r0 + i >= nl) { R[i] = 0; S[i] = 0; continue; }
-            if (i == 0 || k[i] != k[i - 1]) {   // sorted: a new key's bounds lie at or after the previous upper
-                const int64_t from = i == 0 ? rlo : ub;
-                if (staged) {
-                    lb = rlo + bound_s<KO>(s_r, (int)(from - rlo), (int)(rhi - rlo), k[i], false);
-                    ub = rlo + bound_s<KO>(s_r, (int)(lb - rlo), (int)(rhi - rlo), k[i], true);
-                } else {
-                    lb = bound_g<KR, KO>(rk, rhi_bits, from, rhi, k[i], false);
-                    ub = bound_g<KR, KO>(rk, rhi_bits, lb, rhi, k[i], true);
-                }
+            if (i == 0) {   // the thread's first key: bisect the tile's right range (L1-resident top levels)
+                lb = bound_g<KR, KO>(rk, rhi_bits, rlo, rhi, k[0], false);
+                ub = gallop_g<KR, KO>(rk, rhi_bits, lb, rhi, k[0], true);
+            } else if (k[i] != k[i - 1]) {   // sorted: a new key's bounds lie at or after the previous upper
+                lb = gallop_g<KR, KO>(rk, rhi_bits, ub, rhi, k[i], false);
+                ub = gallop_g<KR, KO>(rk, rhi_bits, lb, rhi, k[i], true);
             }
             R[i] = (uint32_t)(ub - lb);
             S[i] = (uint32_t)lb;
@@ -323,10 +329,13 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
                                                      void* __restrict__ lo_out, void* __restrict__ ro_out, int idx32,
                                                      unsigned long long* __restrict__ ck, int tg_shift,
                                                      SmjPayload pay) {
-    // shared memory: the staged bucket ends, plus (when the CTA spans <= MCAP buckets)
-    // the buckets' (R, startR) so that walking across buckets needs no global loads
-    constexpr int MCAP = 1024;
-    __shared__ __align__(16) int32_t s_buf[2 * ETILE + 2 + 3 * MCAP];
+    // shared memory: the staged bucket ends (when the CTA spans <= CCAP buckets), plus
+    // (when it spans <= MCAP) the buckets' (R, startR) so that walking across buckets
+    // needs no global loads. Empty buckets (R = 0: left rows without a partner) make the
+    // span unbounded, so both are optional and searches fall back to global memory.
+    constexpr int MCAP = 1024, CCAP = 2 * ETILE + 2;
+    __shared__ __align__(16) int32_t s_cum[CCAP];
+    __shared__ __align__(16) uint32_t s_m[2 * MCAP];
     __shared__ __align__(16) uint32_t s_l[ETILE], s_r[ETILE];
     const int64_t c0 = begin + (int64_t)blockIdx.x * ETILE;
     const int64_t c1 = min(c0 + ETILE, end);
@@ -349,11 +358,9 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
         b0 = s_b[0];
         b1 = s_b[1];
     }
-    const int nb = (int)(b1 - b0 + 1);
-    const bool meta = nb <= MCAP;
-    int32_t* s_cum = s_buf;
-    uint32_t* s_m = reinterpret_cast<uint32_t*>(s_buf + (meta ? MCAP : 0));   // [2][MCAP] when meta
-    for (int i = threadIdx.x; i < nb; i += ENT) {
+    const int64_t nb = b1 - b0 + 1;
+    const bool meta = nb <= MCAP, cst = nb <= CCAP;
+    for (int i = threadIdx.x; cst && i < nb; i += ENT) {
         const int64_t v = mcum[b0 + i] - c0;
         s_cum[i] = (int32_t)(v < 0 ? -1 : (v > ETILE ? ETILE + 1 : v));
         if (meta) {
@@ -362,18 +369,30 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
         }
     }
     __syncthreads();
+    // first bucket index i >= lo (relative to b0) whose cumulative end exceeds output o
+    // (bucketize right=True; empty buckets are skipped because their end equals the next's start)
+    auto find = [&](int64_t o, int64_t lo) {
+        int64_t hi = nb;
+        if (cst) {
+            const int32_t rel = (int32_t)(o - c0);
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (s_cum[mid] <= rel) lo = mid + 1; else hi = mid;
+            }
+        } else {
+            while (lo < hi) {
+                const int64_t mid = (lo + hi) >> 1;
+                if (mcum[b0 + mid] <= o) lo = mid + 1; else hi = mid;
+            }
+        }
+        return lo;
+    };
     const int64_t o0 = c0 + (int64_t)threadIdx.x * EIPT;
     uint64_t hs = 0, sl = 0, sr = 0;   // CK: this thread's share of the consumer sums
     if (o0 < c1) {   // thread: EIPT consecutive outputs, incremental offset inside the bucket
-        const int32_t rel = threadIdx.x * EIPT;
-        int lo = 0, hi = nb;
-        while (lo < hi) {   // upper_bound(rel) over the staged ends
-            const int mid = (lo + hi) >> 1;
-            if (s_cum[mid] <= rel) lo = mid + 1; else hi = mid;
-        }
-        int bi = lo;   // bucket index relative to b0 (bucket = sorted left row b0 + bi)
+        int64_t bi = find(o0, 0);   // bucket index relative to b0 (bucket = sorted left row b0 + bi)
         TQP_DCHECK(bi < nb && b0 + bi < K);
-        auto load = [&](int i, int64_t& R, int64_t& sR) {
+        auto load = [&](int64_t i, int64_t& R, int64_t& sR) {
             if (meta) {
                 R = s_m[i]; sR = s_m[MCAP + i];
             } else {
@@ -399,12 +418,14 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
                 sl += vl[j];
                 sr += vr[j];
             }
-            if (++r == R && j + 1 < cnt) {   // next non-empty bucket
+            if (++r == R && j + 1 < cnt) {   // next non-empty bucket: the next one, else a search
                 r = 0;
-                do {
-                    ++bi;
+                load(++bi, R, sR);
+                if (R == 0) {
+                    bi = find(o0 + j + 1, bi + 1);
                     load(bi, R, sR);
-                } while (R == 0);
+                }
+                TQP_DCHECK(bi < nb && R > 0);
                 b = b0 + bi;
                 lrow = perm_l ? __ldg(perm_l + b) : (uint32_t)b;
             }
@@ -494,11 +515,11 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
 template <typename KL, typename KR, typename KO>
 void launch_buckets(tqp_ctx* ctx, const LeftKeys& lk, int64_t nl, const KR* rk, uint64_t rhi, int64_t nr,
                     tqp_smj_plan* P, uint64_t* tsum, int64_t tiles, int64_t* scal) {
-    const size_t smem = (size_t)BCAP * sizeof(KO);
-    auto* k = bucket_r_kernel<KL, KR, KO>;
-    set_smem(k, smem);
-    launch(ctx, "tqp_smj_buckets", k, dim3((unsigned)tiles), dim3(JNT), smem, lk, nl, rk, rhi, nr, P->mR.get(),
-           P->msR.get(), tsum, (double*)(scal + 5), (int*)(scal + 4));
+    DevBuf<int64_t> rb(ctx, 2 * tiles);
+    launch(ctx, "tqp_smj_bounds", tile_rbounds_kernel<KL, KR, KO>, dim3((unsigned)ceil_div(2 * tiles, 128)), dim3(128),
+           0, lk, nl, rk, rhi, nr, tiles, rb.get());
+    launch(ctx, "tqp_smj_buckets", bucket_r_kernel<KL, KR, KO>, dim3((unsigned)tiles), dim3(JNT), 0, lk, nl, rk, rhi, nr,
+           (const int64_t*)rb.get(), P->mR.get(), P->msR.get(), tsum, (double*)(scal + 5), (int*)(scal + 4));
 }
 }  // namespace
 

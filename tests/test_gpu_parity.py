@@ -1204,3 +1204,19 @@ def test_pkfk_outer_build_duplicate_key(T):
     with pytest.raises(T.TqpError) as e:
         T.pkfk_outer_build(cu(np.array([4, 4, 1])), cu(np.array([4, 1])))
     assert e.value.status == T.TQP_ERR_DUPLICATE_BUILD_KEY
+
+
+@pytest.mark.parametrize("frac", [0.0005, 0.02, 0.5])
+def test_smj_sparse_matches_empty_buckets(T, frac):
+    """Most left rows without a partner: the expansion's buckets (one per sorted left row)
+    are mostly empty, spans of thousands of empty buckets per output tile; checked against
+    the oracle over the whole output and windows."""
+    rng = np.random.default_rng(int(frac * 1e4))
+    n = 400_003
+    left = rng.integers(0, 1 << 40, n)
+    right = rng.integers(0, 1 << 40, n)
+    pick = rng.random(n) < frac
+    right[pick] = left[rng.integers(0, n, int(pick.sum()))]
+    lo, ro = T.smj_join(cu(left), cu(right))
+    olo, oro = oracle.smj_join(left, right)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
