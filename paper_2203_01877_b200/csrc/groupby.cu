@@ -935,9 +935,9 @@ __device__ void flush_nokey(const Phase1Args& a, NoKeyAcc& acc, Work& w) {
 // k * gridDim.x are streamed into NS shared-memory stages with TMA bulk copies
 // (mbarrier completion; stage s is refilled as soon as every thread is done with it);
 // tail tiles and unaligned columns take plain cooperative loads.
-template <int NT, bool ABORTABLE = false, typename F>
+template <int NT, bool ABORTABLE = false, int RPT = GPT, typename F>
 __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem, uint64_t* mbar, F&& process) {
-    constexpr int TR = NT * GPT;   // rows per tile
+    constexpr int TR = NT * RPT;   // rows per tile
     const int NS = a.n_stages;
     const int tid = threadIdx.x;
     auto stage_ptr = [&](int s) { return smem + (size_t)s * a.stage_bytes; };
@@ -1241,6 +1241,40 @@ __device__ __forceinline__ void load4(const uint8_t* col, int dt, int tid, int64
     }
 }
 
+// DR consecutive rows (thread-contiguous) of a staged column, sign/zero-extended
+template <int DR>
+__device__ __forceinline__ void loadr(const uint8_t* col, int dt, int tid, int64_t (&x)[DR]) {
+    if (dt == TQP_I64) {
+#pragma unroll
+        for (int h = 0; h < DR / 2; h++) {
+            const longlong2 u = reinterpret_cast<const longlong2*>(col)[(DR / 2) * tid + h];
+            x[2 * h] = u.x; x[2 * h + 1] = u.y;
+        }
+    } else if (dt == TQP_I32) {
+#pragma unroll
+        for (int h = 0; h < DR / 4; h++) {
+            const int4 u = reinterpret_cast<const int4*>(col)[(DR / 4) * tid + h];
+            x[4 * h] = u.x; x[4 * h + 1] = u.y; x[4 * h + 2] = u.z; x[4 * h + 3] = u.w;
+        }
+    } else {
+#pragma unroll
+        for (int h = 0; h < DR / 4; h++) {
+            const uint32_t u = reinterpret_cast<const uint32_t*>(col)[(DR / 4) * tid + h];
+#pragma unroll
+            for (int i = 0; i < 4; i++) x[4 * h + i] = (int64_t)((u >> (8 * i)) & 0xFFu);
+        }
+    }
+}
+
+template <int DR>
+__device__ __forceinline__ void loadr_i64(const uint8_t* col, int tid, int64_t (&x)[DR]) {
+#pragma unroll
+    for (int h = 0; h < DR / 2; h++) {
+        const longlong2 u = reinterpret_cast<const longlong2*>(col)[(DR / 2) * tid + h];
+        x[2 * h] = u.x; x[2 * h + 1] = u.y;
+    }
+}
+
 // SPEC (dense kernels specialised on the column types, which removes a per-factor dtype
 // switch from every row): bit 0 = every factor column is int64 (fixed-point decimals),
 // bit 1 = every key column is u8 (1-character flags, reading R19).
@@ -1252,79 +1286,89 @@ __device__ __forceinline__ void load4_i64(const uint8_t* col, int tid, int64_t (
     x[0] = u0.x; x[1] = u0.y; x[2] = u1.x; x[3] = u1.y;
 }
 
-template <int NT, int SPEC>
+template <int NT, int SPEC, int DR>
 __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* st, int64_t t, const DenseHdr& h,
                                            int64_t* acc, uint32_t* cnt, uint64_t (&mt)[PCH][3]) {
     const int tid = threadIdx.x;
-    const int nrows = (int)min((int64_t)NT * GPT, a.n - t * NT * GPT);
-    const int r0 = tid * GPT;
-    bool pass[GPT];
+    const int nrows = (int)min((int64_t)NT * DR, a.n - t * NT * DR);
+    const int r0 = tid * DR;
+    bool pass[DR];
 #pragma unroll
-    for (int i = 0; i < GPT; i++) pass[i] = !a.ts.never && r0 + i < nrows;
+    for (int i = 0; i < DR; i++) pass[i] = !a.ts.never && r0 + i < nrows;
     for (int q = 0; q < a.ts.n; q++) {
         const Term& tm = a.ts.t[q];
-        int64_t x[GPT];
-        load4(st + a.uoff[tm.col], tm.dt, tid, x);
+        int64_t x[DR];
+        loadr<DR>(st + a.uoff[tm.col], tm.dt, tid, x);
         if (tm.dt == TQP_I64) {
 #pragma unroll
-            for (int i = 0; i < GPT; i++) pass[i] &= term64((uint64_t)x[i], tm.lo, tm.width, tm.neg);
+            for (int i = 0; i < DR; i++) pass[i] &= term64((uint64_t)x[i], tm.lo, tm.width, tm.neg);
         } else {
 #pragma unroll
-            for (int i = 0; i < GPT; i++) pass[i] &= term32((uint32_t)x[i], (uint32_t)tm.lo, (uint32_t)tm.width, tm.neg);
+            for (int i = 0; i < DR; i++) pass[i] &= term32((uint32_t)x[i], (uint32_t)tm.lo, (uint32_t)tm.width, tm.neg);
         }
     }
-    if (!(pass[0] | pass[1] | pass[2] | pass[3])) return;
+    bool anyp = false;
+#pragma unroll
+    for (int i = 0; i < DR; i++) anyp |= pass[i];
+    if (!anyp) return;
     // packed key (same layout as the general path) -> dense id
-    uint32_t kb[GPT] = {0, 0, 0, 0};
+    uint32_t kb[DR];
+#pragma unroll
+    for (int i = 0; i < DR; i++) kb[i] = 0;
     for (int c = 0; c < a.n_keys; c++) {
         const int u = a.kcol[c];
         if (SPEC & SPEC_KU8) {
-            const uint32_t w = reinterpret_cast<const uint32_t*>(st + a.uoff[u])[tid];
             const uint32_t mn = (uint32_t)h.kmin[c];
             const int sh = h.kshift[c];
 #pragma unroll
-            for (int i = 0; i < GPT; i++) kb[i] |= (((w >> (8 * i)) & 0xFFu) - mn) << sh;
+            for (int hh = 0; hh < DR / 4; hh++) {
+                const uint32_t w = reinterpret_cast<const uint32_t*>(st + a.uoff[u])[(DR / 4) * tid + hh];
+#pragma unroll
+                for (int i = 0; i < 4; i++) kb[4 * hh + i] |= (((w >> (8 * i)) & 0xFFu) - mn) << sh;
+            }
         } else {
             const int dt = a.udt[u];
-            int64_t x[GPT];
-            load4(st + a.uoff[u], dt, tid, x);
+            int64_t x[DR];
+            loadr<DR>(st + a.uoff[u], dt, tid, x);
 #pragma unroll
-            for (int i = 0; i < GPT; i++) kb[i] |= (uint32_t)(key_part(x[i], dt) - h.kmin[c]) << h.kshift[c];
+            for (int i = 0; i < DR; i++) kb[i] |= (uint32_t)(key_part(x[i], dt) - h.kmin[c]) << h.kshift[c];
         }
     }
-    int id[GPT];
+    int id[DR];
     bool unseen = false;   // a key the (sampled) presence bitmap missed: the host redoes it in full
 #pragma unroll
-    for (int i = 0; i < GPT; i++) {
+    for (int i = 0; i < DR; i++) {
         id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
         unseen |= id[i] >= a.D;
         pass[i] &= id[i] < a.D;
     }
     if (unseen) atomicOr(a.overflow, 8);
 #pragma unroll
-    for (int i = 0; i < GPT; i++)
+    for (int i = 0; i < DR; i++)
         if (pass[i]) cnt[id[i] * NT + tid]++;
     const int np = a.n_pairs;
-    int64_t vprev[GPT] = {1, 1, 1, 1};
+    int64_t vprev[DR];
+#pragma unroll
+    for (int i = 0; i < DR; i++) vprev[i] = 1;
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
         if (jj >= np) break;
         const int fx = a.pext[jj];   // factors already multiplied into the previous pair's value
-        int64_t vv[GPT];
+        int64_t vv[DR];
 #pragma unroll
-        for (int i = 0; i < GPT; i++) vv[i] = fx ? vprev[i] : 1;
+        for (int i = 0; i < DR; i++) vv[i] = fx ? vprev[i] : 1;
 #pragma unroll
         for (int f = 0; f < 3; f++) {
             if (f < fx) continue;
             if (f >= a.pnf[jj]) break;
-            int64_t x[GPT];
-            if (SPEC & SPEC_VI64) load4_i64(st + a.poff[jj][f], tid, x);
-            else load4(st + a.poff[jj][f], a.pdtf[jj][f], tid, x);
+            int64_t x[DR];
+            if (SPEC & SPEC_VI64) loadr_i64<DR>(st + a.poff[jj][f], tid, x);
+            else loadr<DR>(st + a.poff[jj][f], a.pdtf[jj][f], tid, x);
             const uint64_t add = (uint64_t)a.padd[jj][f];
             const bool neg = a.psign[jj][f] < 0;
             uint64_t m2 = mt[jj][f];
 #pragma unroll
-            for (int i = 0; i < GPT; i++) {
+            for (int i = 0; i < DR; i++) {
                 const int64_t tt = (int64_t)(neg ? add - (uint64_t)x[i] : add + (uint64_t)x[i]);   // mod 2^64
                 m2 |= (uint64_t)(tt ^ (tt >> 63));   // every staged row (tail rows are zero-filled)
                 vv[i] = f == 0 ? tt : (int64_t)((uint64_t)vv[i] * (uint64_t)tt);                  // mod 2^64
@@ -1332,10 +1376,10 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
             mt[jj][f] = m2;
         }
 #pragma unroll
-        for (int i = 0; i < GPT; i++) vprev[i] = vv[i];
+        for (int i = 0; i < DR; i++) vprev[i] = vv[i];
         const int op = a.prop[jj];
 #pragma unroll
-        for (int i = 0; i < GPT; i++) {
+        for (int i = 0; i < DR; i++) {
             if (!pass[i]) continue;
             int64_t* p = acc + ((size_t)(id[i] * np + jj) * NT + tid);
             if (op == P_SUM) *p += vv[i];
@@ -1345,7 +1389,7 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     }
 }
 
-template <int NT, int SPEC>
+template <int NT, int SPEC, int DR>
 __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1376,7 +1420,7 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     for (int jj = 0; jj < PCH; jj++)
 #pragma unroll
         for (int f = 0; f < 3; f++) mt[jj][f] = 0;
-    tile_pipeline<NT>(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile<NT, SPEC>(a, st, t, h, acc, cnt, mt); });
+    tile_pipeline<NT, false, DR>(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile<NT, SPEC, DR>(a, st, t, h, acc, cnt, mt); });
     bool bad = false;
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
@@ -1437,18 +1481,22 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
 
 // f(gb_dense_kernel<nt, spec>) for runtime (nt, spec)
 template <typename F>
-static void dense_call(int nt, int spec, F&& f) {
-    auto by_spec = [&](auto ntc) {
-        constexpr int NTc = decltype(ntc)::value;
+static void dense_call(int nt, int spec, int dr, F&& f) {
+    auto by_spec = [&](auto ntc, auto drc) {
+        constexpr int NTc = decltype(ntc)::value, DRc = decltype(drc)::value;
         switch (spec) {
-            case 0: f(gb_dense_kernel<NTc, 0>); break;
-            case 1: f(gb_dense_kernel<NTc, 1>); break;
-            case 2: f(gb_dense_kernel<NTc, 2>); break;
-            default: f(gb_dense_kernel<NTc, 3>); break;
+            case 0: f(gb_dense_kernel<NTc, 0, DRc>); break;
+            case 1: f(gb_dense_kernel<NTc, 1, DRc>); break;
+            case 2: f(gb_dense_kernel<NTc, 2, DRc>); break;
+            default: f(gb_dense_kernel<NTc, 3, DRc>); break;
         }
     };
-    if (nt == 128) by_spec(std::integral_constant<int, 128>{});
-    else by_spec(std::integral_constant<int, 256>{});
+    auto by_nt = [&](auto drc) {
+        if (nt == 128) by_spec(std::integral_constant<int, 128>{}, drc);
+        else by_spec(std::integral_constant<int, 256>{}, drc);
+    };
+    if (dr == 8) by_nt(std::integral_constant<int, 8>{});
+    else by_nt(std::integral_constant<int, 4>{});
 }
 
 // Direct merge of fixed-slot partials (dense ids / no keys): record b * D + d holds CTA
@@ -2249,6 +2297,13 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
         bool dense = false;
         size_t dense_smem = 0;
         int dense_ns = 0, dense_nt = GNT, dense_spec = 0;
+        // rows per thread per tile of the dense kernel (TQP_DENSE_RPT=8 for A/B). Measured, Q1:
+        // 4 rows 0.665 ms (SF10) / 6.44 ms (SF100), 8 rows 0.760 / 7.31 (110 registers: fewer
+        // warps hide less latency than the halved per-tile control overhead saves)
+        static const int dense_dr = [] {
+            const char* e = getenv("TQP_DENSE_RPT");
+            return e && atoi(e) == 8 ? 8 : 4;
+        }();
         int64_t dense_grid = 0;
         const char* dz = getenv("TQP_GROUPBY_DENSE");
         bool small_add = true;   // the dense bound argument needs |add| < 2^61
@@ -2298,13 +2353,13 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                 const size_t hdr = (sizeof(DenseHdr) + 15) & ~size_t(15);
                 int best_w = 0, best_st = 0;
                 for (int nt : {128, 256}) {
-                    const size_t stage = (size_t)a.stage_bytes * nt / GNT;
+                    const size_t stage = (size_t)a.stage_bytes * nt * dense_dr / (GNT * GPT);
                     const size_t accb = (size_t)D * PL->n_pairs * nt * 8 + (size_t)D * nt * 4;
                     for (int ns = 1; ns <= 4; ns++) {
                         const size_t sm = (size_t)ns * stage + hdr + accb;
                         if (sm > 227 * 1024) continue;
                         int occ = 0;
-                        dense_call(nt, dense_spec, [&](auto* kfn) { occ = occupancy(kfn, nt, sm); });
+                        dense_call(nt, dense_spec, dense_dr, [&](auto* kfn) { occ = occupancy(kfn, nt, sm); });
                         const int wps = occ * nt / 32, st = occ * ns;
                         if (occ > 0 && (wps > best_w || (wps == best_w && st > best_st))) {
                             best_w = wps;
@@ -2317,10 +2372,10 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                     }
                 }
                 if (best_w > 0) {
-                    const int64_t tr = (int64_t)dense_nt * GPT;
+                    const int64_t tr = (int64_t)dense_nt * dense_dr;
                     dense_grid = std::min<int64_t>(dense_grid, ceil_div(n, tr));
                     // rows per thread bound -> per-thread int64 sums of values <= 2^bits stay <= 2^62
-                    const int64_t rpt = ceil_div(ceil_div(n, tr), dense_grid) * GPT;
+                    const int64_t rpt = ceil_div(ceil_div(n, tr), dense_grid) * dense_dr;
                     int lg = 0;
                     while ((int64_t(1) << lg) < rpt) lg++;
                     a.dense_bits = 62 - lg;
@@ -2372,17 +2427,17 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
             a.P_counter = Pc.get();
             a.overflow = ovf;
             if (n > 0 && dense) {
-                // the stage layout scaled to tiles of dense_nt * GPT rows
+                // the stage layout scaled to tiles of dense_nt * dense_dr rows
                 Phase1Args ad = a;
-                const int64_t tr = (int64_t)dense_nt * GPT;
+                const int64_t tr = (int64_t)dense_nt * dense_dr;
                 ad.n_stages = dense_ns;
-                ad.stage_bytes = (int)((int64_t)a.stage_bytes * dense_nt / GNT);
+                ad.stage_bytes = (int)((int64_t)a.stage_bytes * tr / GTILE);
                 ad.n_tiles = ceil_div(n, tr);
-                for (int c = 0; c < a.n_ucols; c++) ad.uoff[c] = (int)((int64_t)a.uoff[c] * dense_nt / GNT);
+                for (int c = 0; c < a.n_ucols; c++) ad.uoff[c] = (int)((int64_t)a.uoff[c] * tr / GTILE);
                 for (int j = 0; j < PL->n_pairs && j < PCH; j++)
                     for (int f = 0; f < pnf[j]; f++) ad.poff[j][f] = ad.uoff[a.pfc[j][f]];
                 tile_name = "tqp_groupby_dense";
-                dense_call(dense_nt, dense_spec, [&](auto* kfn) {
+                dense_call(dense_nt, dense_spec, dense_dr, [&](auto* kfn) {
                     set_smem(kfn, dense_smem);
                     launch(ctx, tile_name, kfn, dim3((unsigned)dense_grid), dim3(dense_nt), dense_smem, ad);
                 });
