@@ -90,23 +90,38 @@ __global__ void fill_slots_kernel(const uint32_t* __restrict__ T, const uint32_t
 // below it. 224 domain values per 32 bytes: SF10 order keys (26 bits) -> 9.6 MB.
 constexpr uint32_t RB_BITS = 224;
 
-// One thread per sorted key: set its bit; the first key of a block writes the block's
-// rank (its sorted position); equal neighbours flag a duplicate build key.
+// Each thread takes RBK consecutive sorted keys: bits of the same 32-bit word are OR-ed in a
+// register and written with one atomic per word change (sorted keys: TPC-H order keys put
+// ~8 keys in a word, so about a quarter of the atomics of one per key); the first key of a
+// block writes the block's rank (its sorted position); equal neighbours flag a duplicate.
 // Reads the caller's build keys directly (the sort's identity route writes nothing): the
 // low 32 bits of the order-preserving key (all varying bits are there, k32).
+constexpr int RBK = 8;
 __global__ void rank_bitmap_kernel(const void* __restrict__ keys, int dt, int64_t n, uint32_t base, int64_t nblk,
                                    uint32_t* __restrict__ bm, int* __restrict__ dup) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t rel = (uint32_t)ordered_u64(load_as_i64(keys, dt, i)) - base;
-        const uint32_t blk = rel / RB_BITS, bit = rel % RB_BITS;
-        atomicOr(bm + (int64_t)blk * 8 + 1 + (bit >> 5), 1u << (bit & 31));
-        int64_t prev = -1;
-        if (i > 0) {
-            const uint32_t rp = (uint32_t)ordered_u64(load_as_i64(keys, dt, i - 1)) - base;
-            if (rp == rel) *dup = 1;
-            prev = rp / RB_BITS;
+    const int64_t nth = (n + RBK - 1) / RBK;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nth; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i0 = t * RBK;
+        uint32_t prev = i0 > 0 ? (uint32_t)ordered_u64(load_as_i64(keys, dt, i0 - 1)) - base : 0xFFFFFFFFu;
+        uint32_t cw = 0xFFFFFFFFu, cv = 0;   // current word index and its pending bits
+#pragma unroll
+        for (int j = 0; j < RBK; j++) {
+            const int64_t i = i0 + j;
+            if (i >= n) break;
+            const uint32_t rel = (uint32_t)ordered_u64(load_as_i64(keys, dt, i)) - base;
+            const uint32_t blk = rel / RB_BITS, bit = rel % RB_BITS;
+            const uint32_t w = blk * 8 + 1 + (bit >> 5);   // word index (nblk * 8 < 2^32)
+            if (w != cw) {
+                if (cv) atomicOr(bm + cw, cv);
+                cw = w;
+                cv = 0;
+            }
+            cv |= 1u << (bit & 31);
+            if (i > 0 && prev == rel) *dup = 1;
+            if (i == 0 || prev / RB_BITS != blk) bm[(int64_t)blk * 8] = (uint32_t)i;   // blocks without keys: rank unused
+            prev = rel;
         }
-        if (prev != (int64_t)blk) bm[(int64_t)blk * 8] = (uint32_t)i;   // blocks without keys: rank unused
+        if (cv) atomicOr(bm + cw, cv);
     }
 }
 
@@ -845,7 +860,7 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allo
             B.rank_span = (uint32_t)span;
             B.rank_bm.alloc(ctx, nblk * 8);
             B.rank_bm.zero();
-            const int g = (int)std::min<int64_t>(ceil_div(nb, 256), (int64_t)ctx->num_sms * 8);
+            const int g = (int)std::min<int64_t>(ceil_div(ceil_div(nb, RBK), 256), (int64_t)ctx->num_sms * 8);
             launch(ctx, "tqp_pkfk_rank_bitmap", rank_bitmap_kernel, dim3(g), dim3(256), 0, bk.data, (int)bk.dtype, nb,
                    (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get());
             ctx->add_bytes("tqp_pkfk_rank_bitmap", (double)dtype_size(bk.dtype) * (double)nb + 32.0 * (double)nblk);
