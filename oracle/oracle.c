@@ -5,8 +5,10 @@
  * the TQP hot path computes (He et al., "Query Processing on Tensor Computation
  * Runtimes", arXiv 2203.01877; PAPER.md = /root/reference/PAPER.md).
  * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
- * `--impl reference` legs may load this library. It shares no code, header,
- * table or constant with the CUDA path (paper_2203_01877_b200/csrc).
+ * `--impl reference` legs may load this library. It shares no code, header or
+ * table with the CUDA path (paper_2203_01877_b200/csrc); the only numbers both
+ * contain are public hash constants (murmur3's fmix64 here for the hash map, also
+ * in the CUDA hash-join ablation), which never influence a result.
  *
  * The method reaches exactly (integers are exact) the plain relational result,
  * so every entry point below is the PLAIN DEFINITION written out, not a

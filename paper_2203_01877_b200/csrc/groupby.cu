@@ -12,7 +12,7 @@
 //     while tile k is reduced). The tile's predicates are evaluated, key columns
 //     packed into one 64-bit key (column 0 most significant, reading R12), the
 //     passing rows radix-sorted in shared memory over the bits that vary in the
-//     tile (stable LSD, warp match_any ranking), segment boundaries marked (the
+//     tile (stable LSD, peers by one warp ballot per digit bit), segment boundaries marked (the
 //     uniqueConsecutive / inverse step) and every distinct (op, expression) pair
 //     reduced per segment in registers, reading the values in sorted order
 //     straight from the staged columns; one partial record per (tile, key);
@@ -263,7 +263,8 @@ static_assert(sizeof(WarpPart) <= sizeof(uint64_t) * 2 * GTILE, "WarpPart fits t
 
 
 // One stable LSD pass over positions [0, m) of the tile: rank by the 8-bit digit
-// at `shift` with warp match_any, then scatter to the other buffer.
+// at `shift` (a key's peers in its warp from one ballot per digit bit), then scatter to
+// the other buffer.
 __device__ __forceinline__ void tile_pass(Work& w, int src, int m, int shift) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int dst = src ^ 1;

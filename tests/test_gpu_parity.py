@@ -931,7 +931,8 @@ def test_groupby_high_cardinality(T):
 
 
 def test_groupby_high_cardinality_sf1(T):
-    """General (sorted-tile) path at SF1: ~1.5M groups over 6M lineitem rows, vs the oracle."""
+    """High cardinality at SF1 (~1.5M groups over 6M lineitem rows): the tiles do not
+    reduce, so the group-by takes the global-sort path (Alg. 2 literally); vs the oracle."""
     _, li = tpch_orders_lineitem(1.0, seed=42, device="cuda")
     cols = [li["l_orderkey"], li["l_quantity"], li["l_extendedprice"], li["l_shipdate"]]
     aggs = [("sum", [(1, 0, 1), (2, 0, 1)]), ("count", []), ("min", [(3, 0, 1)]), ("max", [(2, 0, -1)]),

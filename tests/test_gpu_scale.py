@@ -59,7 +59,6 @@ def test_smj_zipf_uniform_100m(T):
     assert bool(((lo[1:] >= lo[:-1]) | ~same).all())             # then left row ascending
     same_l = same & (lo[1:] == lo[:-1])
     assert bool(((ro[1:] > ro[:-1]) | ~same_l).all())            # then right row ascending
-    # sampled windows against the oracle's per-offset route on a key-restricted slice
     plan.release()
 
 
