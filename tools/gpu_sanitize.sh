@@ -1,3 +1,5 @@
+# NOTE: compute-sanitizer is refused on this GPU pool (profiles/sanitizer_refused_r02.txt);
+# tools/gpu_checked.sh is the substitute that runs.
 # compute-sanitizer over every libtqp kernel (SURVEY.md §5 / VERDICT r01 missing #5).
 # Runs the -m gpu parity tests at their small sizes (<= ~1M rows; the SF1/SF10/100M cases are
 # excluded) under memcheck, racecheck and synccheck, checking only libtqp's kernels
