@@ -389,7 +389,41 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
     };
     const int64_t o0 = c0 + (int64_t)threadIdx.x * EIPT;
     uint64_t hs = 0, sl = 0, sr = 0;   // CK: this thread's share of the consumer sums
-    if (o0 < c1) {   // thread: EIPT consecutive outputs, incremental offset inside the bucket
+    const int n_out = (int)(c1 - c0);
+    // Bucket-major when the tile's buckets are many and small (<= 16 outputs on average,
+    // e.g. a PK-FK-shaped join: ~4 lineitems per order): a thread takes whole buckets and
+    // fills their outputs in the staging buffer -- a gather and two shared stores per
+    // output instead of the per-output bucket walk. Few large buckets (skew) keep the
+    // output-major walk, which balances by output.
+    const bool bmajor = meta && cst && nb * 16 >= n_out;
+    if (bmajor) {
+        for (int i = threadIdx.x; i < nb; i += ENT) {
+            const int st = i == 0 ? 0 : min(max((int)s_cum[i - 1], 0), n_out);
+            const int en = min(max((int)s_cum[i], 0), n_out);
+            if (st >= en) continue;
+            const int64_t b = b0 + i;
+            const uint32_t R = s_m[i], sR = s_m[MCAP + i];
+            // offset of the tile's first output of this bucket inside the bucket: 0 unless the
+            // bucket started before the tile (only the first non-empty bucket)
+            const int64_t r0 = (i > 0 && s_cum[i - 1] >= 0) ? 0 : c0 - (mcum[b] - (int64_t)R);
+            TQP_DCHECK(r0 >= 0 && r0 + (en - st) <= (int64_t)R);
+            const uint32_t lrow = perm_l ? __ldg(perm_l + b) : (uint32_t)b;
+            const uint32_t* pr = perm_r + sR + r0;
+            for (int p = st; p < en; p++) {
+                s_l[p] = lrow;
+                s_r[p] = __ldg(pr + (p - st));
+            }
+        }
+        if (CK) {
+            __syncthreads();
+            for (int o = threadIdx.x; o < n_out; o += ENT) {
+                const uint32_t l = s_l[o], r = s_r[o];
+                hs += mix64(mix64(((uint64_t)l << 32) | r) ^ (uint64_t)(c0 + o));
+                sl += l;
+                sr += r;
+            }
+        }
+    } else if (o0 < c1) {   // thread: EIPT consecutive outputs, incremental offset inside the bucket
         int64_t bi = find(o0, 0);   // bucket index relative to b0 (bucket = sorted left row b0 + bi)
         TQP_DCHECK(bi < nb && b0 + bi < K);
         auto load = [&](int64_t i, int64_t& R, int64_t& sR) {
