@@ -6,7 +6,12 @@ import csv, io, json, os, subprocess, sys, collections
 TAG = sys.argv[1] if len(sys.argv) > 1 else "r01"
 OUT = sys.argv[2] if len(sys.argv) > 2 else "profiles"   # the GPU box writes into gpurun_out/
 G = "gpurun_out"
-NAME = [("gb_phase1", "tqp_groupby_tile"), ("gb_dense_kernel", "tqp_groupby_dense"), ("gb_presence", "tqp_groupby_presence"),
+NAME = [("probe_sector", "tqp_pkfk_probe"), ("probe_sample", "tqp_pkfk_sample"), ("rank_bitmap", "tqp_pkfk_rank_bitmap"),
+        ("direct_to_lft", "tqp_pkfk_emit"), ("mark_rows", "tqp_pkfk_outer_mark"), ("bucket_r", "tqp_smj_buckets"),
+        ("tile_rbounds", "tqp_smj_bounds"), ("part_hist", "tqp_partition_hist"), ("part_counts", "tqp_partition_hist"),
+        ("part_scatter", "tqp_partition"), ("first_last", "tqp_sort_andor"), ("minmax", "tqp_minmax"),
+        ("range_splitters", "tqp_range_splitters"), ("gather_kernel", "tqp_gather"),
+        ("gb_phase1", "tqp_groupby_tile"), ("gb_dense_kernel", "tqp_groupby_dense"), ("gb_presence", "tqp_groupby_presence"),
         ("gb_dense_ids", "tqp_groupby_dense_ids"), ("key_range", "tqp_groupby_keyrange"), ("scatter_tma", "tqp_sort_scatter"), ("scatter_kernel", "tqp_sort_scatter"),
         ("probe_kernel", "tqp_pkfk_probe"), ("emit_kernel", "tqp_pkfk_emit"), ("filter_mask", "tqp_filter"),
         ("filter_sel", "tqp_filter_select"), ("rle_count", "tqp_smj_rle"), ("rle_write", "tqp_smj_rle"),
