@@ -161,13 +161,17 @@ class HotPath:
         # joins (inter-operator parallelism: independent operators fill each other's
         # sync gaps and leave-over bandwidth); agg_group: their own process group at N > 1
         self.streams = streams
-        self.agg_group = agg_group
+        self.agg_group, self.join_group = agg_group if agg_group else (None, None)
         if streams > 1:
             import concurrent.futures
             self.s2 = torch.cuda.Stream()
             with torch.cuda.stream(self.s2):
                 self.ctx2 = T.Context()
-            self.pool = concurrent.futures.ThreadPoolExecutor(max_workers=1)
+            self.pool = concurrent.futures.ThreadPoolExecutor(max_workers=2)
+        if streams > 2:   # the PK-FK join on a third stream, concurrently with the SMJ
+            self.s3 = torch.cuda.Stream()
+            with torch.cuda.stream(self.s3):
+                self.ctx3 = T.Context()
         self.ok = orders["o_orderkey"]
         self.lk = li["l_orderkey"]
         self.q1 = columns(li, Q1_COLS)
@@ -196,6 +200,15 @@ class HotPath:
             r6 = self.groupby(q6, [], Q6_AGGS, Q6_PREDS, ctx=self.ctx2, group=self.agg_group)
         return r1, mask, sel, r6
 
+    def _pkfk(self, ok, lk):
+        with torch.cuda.stream(self.s3):
+            if self.exchange:
+                from paper_2203_01877_b200 import dist
+                self.strategy, lo, ro = dist.pkfk_join_shuffled(self.ctx3, ok, lk, group=self.join_group)
+            else:
+                lo, ro = self.ctx3.pkfk_join(ok, lk)
+        return lo, ro
+
     def step(self, ok=None, lk=None, q1=None, q6=None):
         ok = self.ok if ok is None else ok
         lk = self.lk if lk is None else lk
@@ -206,15 +219,23 @@ class HotPath:
             main = torch.cuda.current_stream()
             self.s2.wait_stream(main)
             fut = self.pool.submit(self._aggregations, q1, q6)
+            if self.streams > 2:
+                self.s3.wait_stream(main)
+                fut3 = self.pool.submit(self._pkfk, ok, lk)
             if self.exchange:
                 from paper_2203_01877_b200 import dist
-                self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk)
+                if self.streams == 2:
+                    self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk)
                 sl, sr = dist.smj_join_copartition(c, ok, lk)
             else:
-                lo, ro = c.pkfk_join(ok, lk)
+                if self.streams == 2:
+                    lo, ro = c.pkfk_join(ok, lk)
                 plan = c.smj_prepare(ok, lk)
                 sl, sr = plan.expand(0, plan.size)
                 plan.release()
+            if self.streams > 2:
+                lo, ro = fut3.result()
+                main.wait_stream(self.s3)
             r1, mask, sel, r6 = fut.result()
             main.wait_stream(self.s2)
             return {"pkfk": (lo, ro), "smj": (sl, sr), "q1": r1, "q6_mask": mask, "q6_sel": sel, "q6": r6}
@@ -271,7 +292,9 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     placement = args.placement or ("exchange" if world > 1 else "local")
     orders, li = make_data(rank, world, dev, args.layout, placement)
-    agg_group = dist.new_group(list(range(world))) if (dist and args.streams > 1) else None
+    # separate process groups (communicators) for the collectives issued from other threads
+    agg_group = ((dist.new_group(list(range(world))), dist.new_group(list(range(world))) if args.streams > 2 else None)
+                 if (dist and args.streams > 1) else None)
     hp = HotPath(T, orders, li, world, placement, streams=args.streams, agg_group=agg_group)
     hp.streams = 1   # warm-up, kernel table and per-operator timings: one stream
 
@@ -307,7 +330,7 @@ def run_gpu(args):
         for _ in range(2):   # warm the concurrent path (second context, worker thread)
             hp.step()
         torch.cuda.synchronize()
-    ctxs = [hp.ctx] + ([hp.ctx2] if args.streams > 1 else [])
+    ctxs = [hp.ctx] + ([hp.ctx2] if args.streams > 1 else []) + ([hp.ctx3] if args.streams > 2 else [])
 
     # ---------------- device-timed region: inputs resident in HBM
     clk = ClockSampler(local)
@@ -500,10 +523,12 @@ def run_gpu(args):
                               ": each rank's lineitem references only its own orders (no join exchange)")),
                 "parallelism": f"dp{world}",
                 "streams": args.streams,
-                "concurrency": ("timed steps: the aggregation queries (Q1, Q6 filter, Q6 sum) on a second CUDA stream "
-                                "with their own libtqp context, concurrently with the joins; per-operator times and the "
-                                "kernel table from sequential steps" if args.streams > 1 else
-                                "one stream, operators in sequence"),
+                "concurrency": ({1: "one stream, operators in sequence",
+                                 2: "timed steps: the aggregation queries (Q1, Q6 filter, Q6 sum) on a second CUDA stream "
+                                    "with their own libtqp context, concurrently with the joins",
+                                 3: "timed steps: the aggregation queries, the PK-FK join and the SMJ on three CUDA "
+                                    "streams with their own libtqp contexts, concurrently"}[args.streams] +
+                                ("; per-operator times and the kernel table from sequential steps" if args.streams > 1 else "")),
                 "l2": "inputs larger than L2: 2.8 GB of columns per rank per step vs 126 MB L2 (no flush needed)",
             },
             "clocks": clocks,
@@ -699,7 +724,7 @@ def main():
     ap.add_argument("--no-sf100", action="store_true", help="skip the SF100 single-GPU operator section")
     # 2: the aggregation queries run on a second stream concurrently with the joins in the
     # timed steps (per-operator times always come from sequential steps)
-    ap.add_argument("--streams", type=int, default=2, choices=[1, 2])
+    ap.add_argument("--streams", type=int, default=2, choices=[1, 2, 3])
     ap.add_argument("--cpu-sample-sf", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -1287,9 +1287,13 @@ __device__ __forceinline__ void load4_i64(const uint8_t* col, int tid, int64_t (
     x[0] = u0.x; x[1] = u0.y; x[2] = u1.x; x[3] = u1.y;
 }
 
-template <int NT, int SPEC, int DR>
+// DK > 0: the D <= DK present packed keys (ascending) are held in registers and a row's
+// dense id is the number of them below its key (DK compares) instead of a dependent
+// global lookup in the 64K-entry table; DK = 0: the table.
+template <int NT, int SPEC, int DR, int DK>
 __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* st, int64_t t, const DenseHdr& h,
-                                           int64_t* acc, uint32_t* cnt, uint64_t (&mt)[PCH][3]) {
+                                           int64_t* acc, uint32_t* cnt, uint64_t (&mt)[PCH][3],
+                                           const uint32_t (&dkr)[DK > 0 ? DK : 1]) {
     const int tid = threadIdx.x;
     const int nrows = (int)min((int64_t)NT * DR, a.n - t * NT * DR);
     const int r0 = tid * DR;
@@ -1339,7 +1343,18 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     bool unseen = false;   // a key the (sampled) presence bitmap missed: the host redoes it in full
 #pragma unroll
     for (int i = 0; i < DR; i++) {
-        id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
+        if (DK > 0) {
+            int c = 0;
+            bool eq = false;
+#pragma unroll
+            for (int j = 0; j < (DK > 0 ? DK : 1); j++) {   // unused slots hold 0xFFFFFFFF (> any 16-bit key)
+                c += dkr[j] < kb[i];
+                eq |= dkr[j] == kb[i];
+            }
+            id[i] = pass[i] ? (eq ? c : DMAX) : 0;
+        } else {
+            id[i] = pass[i] ? (int)__ldg(a.dtab + kb[i]) : 0;
+        }
         unseen |= id[i] >= a.D;
         pass[i] &= id[i] < a.D;
     }
@@ -1390,7 +1405,7 @@ __device__ __forceinline__ void dense_tile(const Phase1Args& a, const uint8_t* s
     }
 }
 
-template <int NT, int SPEC, int DR>
+template <int NT, int SPEC, int DR, int DK>
 __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     constexpr int NW = NT / 32;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1421,7 +1436,12 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
     for (int jj = 0; jj < PCH; jj++)
 #pragma unroll
         for (int f = 0; f < 3; f++) mt[jj][f] = 0;
-    tile_pipeline<NT, false, DR>(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) { dense_tile<NT, SPEC, DR>(a, st, t, h, acc, cnt, mt); });
+    uint32_t dkr[DK > 0 ? DK : 1];
+#pragma unroll
+    for (int j = 0; j < (DK > 0 ? DK : 1); j++) dkr[j] = (DK > 0 && j < D) ? (uint32_t)a.dkeys[j] : 0xFFFFFFFFu;
+    tile_pipeline<NT, false, DR>(a, smem, h.mbar, [&](const uint8_t* st, int64_t t) {
+        dense_tile<NT, SPEC, DR, DK>(a, st, t, h, acc, cnt, mt, dkr);
+    });
     bool bad = false;
 #pragma unroll
     for (int jj = 0; jj < PCH; jj++) {
@@ -1481,23 +1501,24 @@ __global__ void __launch_bounds__(NT) gb_dense_kernel(Phase1Args a) {
 }
 
 // f(gb_dense_kernel<nt, spec>) for runtime (nt, spec)
+// f(gb_dense_kernel<nt, spec, 4 rows, dk>) for runtime (nt, spec, dk in {0, 4})
 template <typename F>
-static void dense_call(int nt, int spec, int dr, F&& f) {
-    auto by_spec = [&](auto ntc, auto drc) {
-        constexpr int NTc = decltype(ntc)::value, DRc = decltype(drc)::value;
+static void dense_call(int nt, int spec, int dk, F&& f) {
+    auto by_spec = [&](auto ntc, auto dkc) {
+        constexpr int NTc = decltype(ntc)::value, DKc = decltype(dkc)::value;
         switch (spec) {
-            case 0: f(gb_dense_kernel<NTc, 0, DRc>); break;
-            case 1: f(gb_dense_kernel<NTc, 1, DRc>); break;
-            case 2: f(gb_dense_kernel<NTc, 2, DRc>); break;
-            default: f(gb_dense_kernel<NTc, 3, DRc>); break;
+            case 0: f(gb_dense_kernel<NTc, 0, 4, DKc>); break;
+            case 1: f(gb_dense_kernel<NTc, 1, 4, DKc>); break;
+            case 2: f(gb_dense_kernel<NTc, 2, 4, DKc>); break;
+            default: f(gb_dense_kernel<NTc, 3, 4, DKc>); break;
         }
     };
-    auto by_nt = [&](auto drc) {
-        if (nt == 128) by_spec(std::integral_constant<int, 128>{}, drc);
-        else by_spec(std::integral_constant<int, 256>{}, drc);
+    auto by_nt = [&](auto dkc) {
+        if (nt == 128) by_spec(std::integral_constant<int, 128>{}, dkc);
+        else by_spec(std::integral_constant<int, 256>{}, dkc);
     };
-    if (dr == 8) by_nt(std::integral_constant<int, 8>{});
-    else by_nt(std::integral_constant<int, 4>{});
+    if (dk == 4) by_nt(std::integral_constant<int, 4>{});
+    else by_nt(std::integral_constant<int, 0>{});
 }
 
 // Direct merge of fixed-slot partials (dense ids / no keys): record b * D + d holds CTA
@@ -2298,13 +2319,11 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
         bool dense = false;
         size_t dense_smem = 0;
         int dense_ns = 0, dense_nt = GNT, dense_spec = 0;
-        // rows per thread per tile of the dense kernel (TQP_DENSE_RPT=8 for A/B). Measured, Q1:
-        // 4 rows 0.665 ms (SF10) / 6.44 ms (SF100), 8 rows 0.760 / 7.31 (110 registers: fewer
-        // warps hide less latency than the halved per-tile control overhead saves)
-        static const int dense_dr = [] {
-            const char* e = getenv("TQP_DENSE_RPT");
-            return e && atoi(e) == 8 ? 8 : 4;
-        }();
+        // rows per thread per tile of the dense kernel: 4 (8 measured slower, Q1: 0.665 ->
+        // 0.760 ms at SF10, 6.44 -> 7.31 ms at SF100: 110 registers, fewer warps hide less
+        // latency than the halved per-tile control overhead saves)
+        constexpr int dense_dr = 4;
+        int dense_dk = 0;   // 4: the dense ids by compares against <= 4 keys in registers
         int64_t dense_grid = 0;
         const char* dz = getenv("TQP_GROUPBY_DENSE");
         bool small_add = true;   // the dense bound argument needs |add| < 2^61
@@ -2349,6 +2368,11 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                     for (int f = 0; f < pnf[j]; f++) vi64 = vi64 && a.pdtf[j][f] == TQP_I64;
                 for (int k = 0; k < n_keys; k++) ku8 = ku8 && kd[k] == TQP_U8;
                 dense_spec = (vi64 ? SPEC_VI64 : 0) | (ku8 ? SPEC_KU8 : 0);
+                static const bool dk_off = [] {   // TQP_DENSE_DK=0: always the id table (A/B)
+                    const char* e = getenv("TQP_DENSE_DK");
+                    return e && e[0] == '0';
+                }();
+                dense_dk = (D <= 4 && !dk_off) ? 4 : 0;
                 // (threads per CTA, stages) with the most resident warps per SM; ties go to
                 // more stages per SM. Lane-private accumulators make occupancy smem-bound.
                 const size_t hdr = (sizeof(DenseHdr) + 15) & ~size_t(15);
@@ -2360,7 +2384,7 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                         const size_t sm = (size_t)ns * stage + hdr + accb;
                         if (sm > 227 * 1024) continue;
                         int occ = 0;
-                        dense_call(nt, dense_spec, dense_dr, [&](auto* kfn) { occ = occupancy(kfn, nt, sm); });
+                        dense_call(nt, dense_spec, dense_dk, [&](auto* kfn) { occ = occupancy(kfn, nt, sm); });
                         const int wps = occ * nt / 32, st = occ * ns;
                         if (occ > 0 && (wps > best_w || (wps == best_w && st > best_st))) {
                             best_w = wps;
@@ -2438,7 +2462,7 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                 for (int j = 0; j < PL->n_pairs && j < PCH; j++)
                     for (int f = 0; f < pnf[j]; f++) ad.poff[j][f] = ad.uoff[a.pfc[j][f]];
                 tile_name = "tqp_groupby_dense";
-                dense_call(dense_nt, dense_spec, dense_dr, [&](auto* kfn) {
+                dense_call(dense_nt, dense_spec, dense_dk, [&](auto* kfn) {
                     set_smem(kfn, dense_smem);
                     launch(ctx, tile_name, kfn, dim3((unsigned)dense_grid), dim3(dense_nt), dense_smem, ad);
                 });
