@@ -420,6 +420,17 @@ constexpr size_t scatter_tma_smem() {
     return SCATTER_STAGES * (size_t)scatter_stage_bytes<KT, IN, IPT>() + sizeof(ScatterWork<KT, IN, IPT, RB>);
 }
 
+// Tile order of a persistent CTA: grid-stride (tile b + k*grid, default) or contiguous
+// (TQP_SCATTER_CONTIG=1: CTA b takes tiles [b*T, (b+1)*T), so the tile after t -- whose
+// digit-d run continues exactly where t's ends, sharing a half-written 32-byte sector --
+// is written by the same CTA while that sector is still in L2). Measured contiguous
+// slower (SMJ's 60M-key sort, 3 scatter passes: 1.15 -> 1.40 ms): with grid-stride the
+// CTAs' concurrent writes of a digit land next to each other (tiles t, t+1, ... are in
+// flight together), which DRAM serves better than 296 write fronts far apart.
+#ifndef TQP_SCATTER_CONTIG
+#define TQP_SCATTER_CONTIG 0
+#endif
+
 template <typename KT, int IN, int IPT, int RB>
 __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT) == 4 ? 3 : 2))) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
     constexpr int TILE = NT * IPT, BINS = 1 << RB, BPT = BINS / NT;
@@ -451,17 +462,24 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
         }
     };
     uint32_t par = 0;   // bit st: phase parity of stage st's next wait (a register, not a local array)
+    // this CTA's k-th tile and the number of its tiles
+    const int64_t per = (n_tiles + gridDim.x - 1) / gridDim.x;
+    const int64_t t_begin = TQP_SCATTER_CONTIG ? min((int64_t)blockIdx.x * per, n_tiles) : 0;
+    const int64_t t_end = TQP_SCATTER_CONTIG ? min(t_begin + per, n_tiles) : n_tiles;
+    auto tile_of = [&](int64_t k) -> int64_t {
+        return TQP_SCATTER_CONTIG ? t_begin + k : blockIdx.x + k * gridDim.x;
+    };
     for (int st = 0; st < SST; st++) {
-        const int64_t t = blockIdx.x + (int64_t)st * gridDim.x;
-        if (t < n_tiles && full(t)) {
+        const int64_t t = tile_of(st);
+        if (t < t_end && full(t)) {
             if (tid == 0) issue(t, st);
         }
     }
     const unsigned lt = lanemask_lt();
     const uint64_t opol = (TQP_SCATTER_HINTS & 2) ? policy_evict_last() : 0;
     for (int64_t k = 0;; k++) {
-        const int64_t tile = blockIdx.x + k * gridDim.x;
-        if (tile >= n_tiles) break;
+        const int64_t tile = tile_of(k);
+        if (tile >= t_end) break;
         const int st = (int)(k % SST);
         const int64_t base = tile * TILE;
         KT key[IPT];
@@ -510,8 +528,8 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
         }
         __syncthreads();   // stage st consumed by every thread; whist zeroed
         {
-            const int64_t t2 = tile + SST * (int64_t)gridDim.x;
-            if (t2 < n_tiles && full(t2)) {
+            const int64_t t2 = tile_of(k + SST);
+            if (t2 < t_end && full(t2)) {
                 if (tid == 0) {
                     fence_proxy_async();
                     issue(t2, st);
