@@ -315,10 +315,16 @@ __device__ __forceinline__ void pay_copy(const void* src, int dt, int64_t from, 
 }
 
 template <bool CK, bool PAY = false>
-// Blocks per SM forced by the register budget: measured no gain (SF10 expansion 0.435 ms
-// at 63 registers / 4 blocks, 0.443 with 5, 0.439 with 6, 0.494 with 8 -- spills), so off.
+// Occupancy: the staged bucket ends (CCAP, more: searches in global memory) and the blocks
+// per SM the register budget must allow. Measured, SF10 expansion: CCAP 4098 (40 KB of
+// shared memory, 4 blocks/SM) 0.367 ms; CCAP 1025 (28 KB) 0.326 ms; + 6 blocks/SM (40
+// registers, 16 bytes of spills) 0.301 ms; 7 / 8 blocks 0.299 / 0.299. (r01, before the
+// per-row buckets: 4/5/6/8 blocks 0.435/0.443/0.439/0.494 ms.)
 #ifndef TQP_EXPAND_MINB
-#define TQP_EXPAND_MINB 0
+#define TQP_EXPAND_MINB 6
+#endif
+#ifndef TQP_EXPAND_CCAP
+#define TQP_EXPAND_CCAP 1025
 #endif
 __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint32_t* __restrict__ mR,
                                                      const uint32_t* __restrict__ msR,
@@ -333,7 +339,7 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
     // (when it spans <= MCAP) the buckets' (R, startR) so that walking across buckets
     // needs no global loads. Empty buckets (R = 0: left rows without a partner) make the
     // span unbounded, so both are optional and searches fall back to global memory.
-    constexpr int MCAP = 1024, CCAP = 2 * ETILE + 2;
+    constexpr int MCAP = 1024, CCAP = TQP_EXPAND_CCAP;
     __shared__ __align__(16) int32_t s_cum[CCAP];
     __shared__ __align__(16) uint32_t s_m[2 * MCAP];
     __shared__ __align__(16) uint32_t s_l[ETILE], s_r[ETILE];
