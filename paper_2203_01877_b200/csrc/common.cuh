@@ -179,6 +179,44 @@ inline void launch(tqp_ctx* ctx, const char* name, void (*k)(KArgs...), dim3 gri
     }
 }
 
+// The same launch as a thread-block cluster of `cluster` CTAs along x (grid.x a multiple).
+template <typename... KArgs, typename... Args>
+inline void launch_cluster(tqp_ctx* ctx, const char* name, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                           unsigned cluster, Args... args) {
+    if (cluster <= 1) {
+        launch(ctx, name, k, grid, block, smem, args...);
+        return;
+    }
+    if (grid.x == 0 || grid.y == 0 || grid.z == 0) return;
+    cudaEvent_t a = nullptr, b = nullptr;
+    const bool prof = ctx->profiled(name);
+    if (prof) {
+        a = ctx->get_event();
+        b = ctx->get_event();
+        TQP_CUDA(cudaEventRecord(a, ctx->stream));
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) fail(TQP_ERR_CUDA, std::string("launch ") + name + ": " + cudaGetErrorString(e));
+    ctx->launches++;
+    if (prof) {
+        TQP_CUDA(cudaEventRecord(b, ctx->stream));
+        ctx->pending.push_back({name, a, b});
+    }
+}
+
 // Dynamic shared-memory limit and occupancy per (kernel, block size, bytes), cached: the
 // runtime queries cost host time while the GPU waits right after a readback.
 inline std::mutex& kcache_mutex() {
