@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * JTILE;
     const int64_t rlo = rb[2 * blockIdx.x], rhi = max(rb[2 * blockIdx.x + 1], rlo);
+    const KO kfirst = left_key<KL, KO>(lk, base), klast = left_key<KL, KO>(lk, min(base + JTILE, nl) - 1);
     const int64_t r0 = base + (int64_t)tid * JIPT;
     uint64_t tot = 0;
     if (r0 < nl) {
@@ -132,9 +133,11 @@ __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, 
 #pragma unroll
         for (int i = 0; i < JIPT; i++) {
             if (r0 + i >= nl) { R[i] = 0; S[i] = 0; continue; }
-            if (i == 0) {   // the thread's first key: bisect the tile's right range (L1-resident top levels)
-                lb = bound_g<KR, KO>(rk, rhi_bits, rlo, rhi, k[0], false);
-                ub = gallop_g<KR, KO>(rk, rhi_bits, lb, rhi, k[0], true);
+            if (i == 0) {   // the thread's first key: bisect the tile's right range (L1-resident top levels);
+                            // the tile's first / last key has the range's own bounds (a heavy key
+                            // spanning tiles costs no search at all)
+                lb = k[0] == kfirst ? rlo : bound_g<KR, KO>(rk, rhi_bits, rlo, rhi, k[0], false);
+                ub = k[0] == klast ? rhi : gallop_g<KR, KO>(rk, rhi_bits, lb, rhi, k[0], true);
             } else if (k[i] != k[i - 1]) {   // sorted: a new key's bounds lie at or after the previous upper
                 lb = gallop_g<KR, KO>(rk, rhi_bits, ub, rhi, k[i], false);
                 ub = gallop_g<KR, KO>(rk, rhi_bits, lb, rhi, k[i], true);
@@ -314,9 +317,9 @@ __device__ __forceinline__ void pay_copy(const void* src, int dt, int64_t from, 
     }
 }
 
-template <bool CK, bool PAY = false>
 // Occupancy: the staged bucket ends (CCAP, more: searches in global memory) and the blocks
-// per SM the register budget must allow. Measured, SF10 expansion: CCAP 4098 (40 KB of
+// per SM the register budget must allow (sparse buckets -- more than ~700 per output tile,
+// e.g. Zipf x uniform where most left rows have no partner -- take CC = 4098 at 4 blocks/SM). Measured, SF10 expansion: CCAP 4098 (40 KB of
 // shared memory, 4 blocks/SM) 0.367 ms; CCAP 1025 (28 KB) 0.326 ms; + 6 blocks/SM (40
 // registers, 16 bytes of spills) 0.301 ms; 7 / 8 blocks 0.299 / 0.299. (r01, before the
 // per-row buckets: 4/5/6/8 blocks 0.435/0.443/0.439/0.494 ms.)
@@ -326,7 +329,8 @@ template <bool CK, bool PAY = false>
 #ifndef TQP_EXPAND_CCAP
 #define TQP_EXPAND_CCAP 1025
 #endif
-__global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint32_t* __restrict__ mR,
+template <bool CK, bool PAY = false, int CC = TQP_EXPAND_CCAP>
+__global__ void __launch_bounds__(ENT, CC <= 1025 ? TQP_EXPAND_MINB : 4) expand_kernel(const uint32_t* __restrict__ mR,
                                                      const uint32_t* __restrict__ msR,
                                                      const int64_t* __restrict__ mcum, int64_t K,
                                                      const uint32_t* __restrict__ tb,
@@ -339,7 +343,7 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
     // (when it spans <= MCAP) the buckets' (R, startR) so that walking across buckets
     // needs no global loads. Empty buckets (R = 0: left rows without a partner) make the
     // span unbounded, so both are optional and searches fall back to global memory.
-    constexpr int MCAP = 1024, CCAP = TQP_EXPAND_CCAP;
+    constexpr int MCAP = 1024, CCAP = CC;
     __shared__ __align__(16) int32_t s_cum[CCAP];
     __shared__ __align__(16) uint32_t s_m[2 * MCAP];
     __shared__ __align__(16) uint32_t s_l[ETILE], s_r[ETILE];
@@ -401,17 +405,20 @@ __global__ void __launch_bounds__(ENT, TQP_EXPAND_MINB) expand_kernel(const uint
     // fills their outputs in the staging buffer -- a gather and two shared stores per
     // output instead of the per-output bucket walk. Few large buckets (skew) keep the
     // output-major walk, which balances by output.
-    const bool bmajor = meta && cst && nb * 16 >= n_out;
+    const bool bmajor = meta && cst && nb * 16 >= n_out;   // (unstaged sparse buckets measured slower: 1.15 -> 1.91 ms, Zipf x uniform)
     if (bmajor) {
-        for (int i = threadIdx.x; i < nb; i += ENT) {
-            const int st = i == 0 ? 0 : min(max((int)s_cum[i - 1], 0), n_out);
-            const int en = min(max((int)s_cum[i], 0), n_out);
+        // end of bucket i relative to the tile, unclamped below (-1 / negative: before the tile)
+        auto rend = [&](int64_t i) -> int64_t { return cst ? (int64_t)s_cum[i] : mcum[b0 + i] - c0; };
+        for (int64_t i = threadIdx.x; i < nb; i += ENT) {
+            const int64_t pe = i == 0 ? -1 : rend(i - 1);
+            const int st = (int)min(max(pe, (int64_t)0), (int64_t)n_out);
+            const int en = (int)min(max(rend(i), (int64_t)0), (int64_t)n_out);
             if (st >= en) continue;
             const int64_t b = b0 + i;
-            const uint32_t R = s_m[i], sR = s_m[MCAP + i];
+            const uint32_t R = meta ? s_m[i] : mR[b], sR = meta ? s_m[MCAP + i] : msR[b];
             // offset of the tile's first output of this bucket inside the bucket: 0 unless the
             // bucket started before the tile (only the first non-empty bucket)
-            const int64_t r0 = (i > 0 && s_cum[i - 1] >= 0) ? 0 : c0 - (mcum[b] - (int64_t)R);
+            const int64_t r0 = (i > 0 && pe >= 0) ? 0 : c0 - (mcum[b] - (int64_t)R);
             TQP_DCHECK(r0 >= 0 && r0 + (en - st) <= (int64_t)R);
             const uint32_t lrow = perm_l ? __ldg(perm_l + b) : (uint32_t)b;
             const uint32_t* pr = perm_r + sR + r0;
@@ -641,9 +648,12 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
             fail(TQP_ERR_OVERFLOW, "smj: output size exceeds 2^62");
         P->out_size = h[3];
         if (P->out_size > 0) {   // cumHistMul + the tile -> bucket table for expand
-            // a table entry per output tile while that is comparable to the buckets; coarser
-            // tiles (and a search per entry) when outSize dwarfs them
-            const int64_t tcap = 4 * P->K + (int64_t(1) << 22);
+            // a table entry per output tile while that stays small; coarser tiles (and a search
+            // per entry) when outSize dwarfs the buckets. The cap is K / 8 + 2^22 entries: with
+            // one bucket per left row, 4K entries (the r01 cap for keys) meant 400M binary
+            // searches for the both-Zipf config (8.9 ms); a coarser table only widens the
+            // range each expansion CTA narrows with its warp-cooperative search.
+            const int64_t tcap = P->K / 8 + (int64_t(1) << 22);
             int sh = 0;
             while (ceil_div(P->out_size, (int64_t)ETILE << sh) + 1 > tcap) sh++;
             P->tg_shift = sh;
@@ -669,6 +679,11 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
     }
 }
 
+// more than ~700 buckets per output tile on average: the larger staging of bucket ends
+static bool expand_sparse(const tqp_smj_plan* P) {
+    return P->out_size > 0 && (double)P->K * ETILE > 700.0 * (double)P->out_size;
+}
+
 void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end, void* lo, void* ro, int idx32) {
     if (begin < 0 || end < begin || end > P->out_size) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: bad window");
     if (end == begin) return;
@@ -678,7 +693,8 @@ void smj_expand(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int64_t end,
     if (idx32 && (P->n_left >= (int64_t(1) << 31) || P->n_right >= (int64_t(1) << 31)))
         fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand_i32: row counts must be < 2^31");
     ctx->add_bytes("tqp_smj_expand", (idx32 ? 8.0 : 16.0) * (double)(end - begin));
-    launch(ctx, "tqp_smj_expand", expand_kernel<false>, dim3((unsigned)blocks), dim3(ENT), 0, P->mR.get(),
+    auto* kf = expand_sparse(P) ? expand_kernel<false, false, 4098> : expand_kernel<false, false, TQP_EXPAND_CCAP>;
+    launch(ctx, "tqp_smj_expand", kf, dim3((unsigned)blocks), dim3(ENT), 0, P->mR.get(),
            P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(), begin, end, lo,
            ro, idx32, (unsigned long long*)nullptr, P->tg_shift, SmjPayload{});
 }
@@ -713,7 +729,8 @@ void smj_expand_payload(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int6
     const int64_t blocks = ceil_div(end - begin, ETILE);
     if (blocks >= (int64_t(1) << 31)) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: window too large");
     ctx->add_bytes("tqp_smj_expand", ((lo ? 8.0 : 0.0) + (ro ? 8.0 : 0.0) + pb) * (double)(end - begin));
-    launch(ctx, "tqp_smj_expand", expand_kernel<false, true>, dim3((unsigned)blocks), dim3(ENT), 0,
+    auto* kf = expand_sparse(P) ? expand_kernel<false, true, 4098> : expand_kernel<false, true, TQP_EXPAND_CCAP>;
+    launch(ctx, "tqp_smj_expand", kf, dim3((unsigned)blocks), dim3(ENT), 0,
            P->mR.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(),
            begin, end, (void*)lo, (void*)ro, 0, (unsigned long long*)nullptr, P->tg_shift, pay);
 }
@@ -729,7 +746,8 @@ void smj_expand_checksum(tqp_ctx* ctx, const tqp_smj_plan* P, int64_t begin, int
     if (blocks >= (int64_t(1) << 31)) fail(TQP_ERR_INVALID_ARGUMENT, "smj_expand: window too large");
     DevBuf<unsigned long long> ck(ctx, 3 * CK_SLOTS + 3);
     ck.zero();
-    launch(ctx, "tqp_smj_expand_checksum", expand_kernel<true>, dim3((unsigned)blocks), dim3(ENT), 0,
+    auto* kf = expand_sparse(P) ? expand_kernel<true, false, 4098> : expand_kernel<true, false, TQP_EXPAND_CCAP>;
+    launch(ctx, "tqp_smj_expand_checksum", kf, dim3((unsigned)blocks), dim3(ENT), 0,
            P->mR.get(), P->msR.get(), P->mcum.get(), P->K, P->tb.get(), P->perm_l.get(), P->perm_r.get(),
            begin, end, (void*)nullptr, (void*)nullptr, 0, ck.get(), P->tg_shift, SmjPayload{});
     launch(ctx, "tqp_smj_expand_checksum", ck_final_kernel, dim3(1), dim3(1024), 0, (const unsigned long long*)ck.get(),
