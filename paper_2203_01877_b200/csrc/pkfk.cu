@@ -97,8 +97,12 @@ constexpr uint32_t RB_BITS = 224;
 // Reads the caller's build keys directly (the sort's identity route writes nothing): the
 // low 32 bits of the order-preserving key (all varying bits are there, k32).
 constexpr int RBK = 8;
+// Speculative route (unsorted != null): the caller only knows the first and the last key;
+// a key out of order, outside [first, last] or with another high word sets *unsorted and
+// the host rebuilds the build side by the sort (the bitmap is then garbage, never used).
 __global__ void rank_bitmap_kernel(const void* __restrict__ keys, int dt, int64_t n, uint32_t base, int64_t nblk,
-                                   uint32_t* __restrict__ bm, int* __restrict__ dup) {
+                                   uint32_t* __restrict__ bm, int* __restrict__ dup, int* __restrict__ unsorted,
+                                   uint32_t hi32, uint32_t span) {
     const int64_t nth = (n + RBK - 1) / RBK;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nth; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i0 = t * RBK;
@@ -108,7 +112,12 @@ __global__ void rank_bitmap_kernel(const void* __restrict__ keys, int dt, int64_
         for (int j = 0; j < RBK; j++) {
             const int64_t i = i0 + j;
             if (i >= n) break;
-            const uint32_t rel = (uint32_t)ordered_u64(load_as_i64(keys, dt, i)) - base;
+            const uint64_t u = ordered_u64(load_as_i64(keys, dt, i));
+            const uint32_t rel = (uint32_t)u - base;
+            if (unsorted && ((uint32_t)(u >> 32) != hi32 || rel > span || (i > 0 && rel < prev))) {
+                *unsorted = 1;
+                return;
+            }
             const uint32_t blk = rel / RB_BITS, bit = rel % RB_BITS;
             const uint32_t w = blk * 8 + 1 + (bit >> 5);   // word index (nblk * 8 < 2^32)
             if (w != cw) {
@@ -192,6 +201,7 @@ struct ProbeArgs {
     uint64_t blo, bhi;        // multi-pass probe: the bucket range this pass resolves
     const uint4* rank_bm;     // nullable: rank bitmap of a presorted build side (RB_BITS bits per 32-byte block)
     int64_t n_build;          // build rows (bounds checks of the checked build)
+    const int* unsorted;      // nullable: the speculative build side turned out unsorted -> do nothing
     uint32_t rank_span;       // rank bitmap route: rel must be <= rank_span
     // join mode, direct output: when *direct == 0 (no sampled miss, probe_sample_kernel)
     // the probe writes the final pairs at their probe row -- left = build row (or -1),
@@ -373,6 +383,7 @@ template <typename KT, int PDT, bool PACKED>
 #endif
 __global__ void __launch_bounds__(PNT, TQP_PROBE_MINB) probe_kernel(ProbeArgs a) {
     __shared__ uint32_t s_w[PNW];
+    if (a.unsorted && *a.unsorted) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * PTILE;
     const bool direct = a.mode == 0 && a.direct && *a.direct == 0;
@@ -442,6 +453,7 @@ constexpr int SECTOR_BATCH = TQP_SECTOR_BATCH;
 template <int PDT, int ROUTE>
 __global__ void __launch_bounds__(PNT, TQP_SECTOR_MINB) probe_sector_kernel(ProbeArgs a) {
     __shared__ uint32_t s_w[PNW];
+    if (a.unsorted && *a.unsorted) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * PTILE;
     const bool direct = a.mode == 0 && a.direct && *a.direct == 0;
@@ -803,12 +815,75 @@ struct Built {
     int64_t nb = 0;
     DevBuf<uint32_t> rank_bm;   // presorted build side: rank bitmap (then T / records are unused)
     uint32_t rank_span = 0;     // rank bitmap: keys - base lie in [0, rank_span]
+    DevBuf<int> unsorted;       // speculative rank route: set when the build side was not in key order
 };
+
+// out[0] / out[1] = the first / last key (order-preserving images); out[2] = 1 if 2,049
+// evenly spaced keys (first and last included) are not in order -- a shuffled build side
+// never takes the speculative route.
+constexpr int SPEC_SAMPLE = 2048;
+__global__ void __launch_bounds__(1024) first_last_kernel(const void* keys, int dt, int64_t n, unsigned long long* out) {
+    bool bad = false;
+    for (int j = threadIdx.x; j < SPEC_SAMPLE; j += blockDim.x) {
+        const int64_t a = (int64_t)(((__int128)j * (n - 1)) / SPEC_SAMPLE);
+        const int64_t b = (int64_t)(((__int128)(j + 1) * (n - 1)) / SPEC_SAMPLE);
+        bad |= ordered_u64(load_as_i64(keys, dt, a)) > ordered_u64(load_as_i64(keys, dt, b));
+    }
+    bad = __syncthreads_or(bad);
+    if (threadIdx.x < 2) out[threadIdx.x] = ordered_u64(load_as_i64(keys, dt, threadIdx.x == 0 ? 0 : n - 1));
+    if (threadIdx.x == 0) out[2] = bad ? 1ull : 0ull;
+}
 
 // allow_rank = false: never the rank bitmap (its build row = rank + popcount of the
 // distinct keys below is only right without duplicate build keys; the outer join, which
 // tolerates duplicates, rebuilds without it when the duplicate flag is set).
-void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allow_rank = true) {
+void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allow_rank = true, bool spec = true) {
+    static const bool no_rank = [] {
+        const char* e = std::getenv("TQP_PKFK_NO_RANK");
+        return e && std::atoi(e) != 0;
+    }();
+    // Speculative rank route (TQP_PKFK_NO_SPEC=1 disables it): primary-key columns are
+    // usually stored in key order, so read only the first and the last key (one 16-byte
+    // sync instead of the sort's plan pass over the column), size the rank bitmap by them
+    // and build it in one pass that also verifies the order; the probe's single readback
+    // carries the verdict and an unsorted build side is redone the ordinary way.
+    static const bool no_spec = [] {
+        const char* e = std::getenv("TQP_PKFK_NO_SPEC");
+        return e && std::atoi(e) != 0;
+    }();
+    if (spec && allow_rank && !no_rank && !no_spec && nb >= (1 << 16) &&
+        (bk.dtype == TQP_I64 || bk.dtype == TQP_I32)) {
+        DevBuf<unsigned long long> fl(ctx, 3);
+        launch(ctx, "tqp_sort_andor", first_last_kernel, dim3(1), dim3(1024), 0, bk.data, (int)bk.dtype, nb, fl.get());
+        uint64_t h[3];
+        read_back(ctx, h, fl.get(), 24);
+        const uint64_t lo = h[0], hi = h[1];
+        if (!h[2] && hi > lo && (lo >> 32) == (hi >> 32)) {
+            const uint64_t span = hi - lo;
+            const int64_t nblk = (int64_t)((span + RB_BITS) / RB_BITS);
+            if (nblk * 32 <= 8 * nb + (int64_t(1) << 20)) {
+                B.nb = nb;
+                B.so.k32 = true;
+                B.so.identity = true;
+                B.base = lo & 0xFFFFFFFFull;
+                B.hi_bits = lo & 0xFFFFFFFF00000000ull;
+                B.vbits = 32;   // the probe's range test is rank_span
+                B.rank_span = (uint32_t)span;
+                B.dup.alloc(ctx, 1);
+                B.dup.zero();
+                B.unsorted.alloc(ctx, 1);
+                B.unsorted.zero();
+                B.rank_bm.alloc(ctx, nblk * 8);
+                B.rank_bm.zero();
+                const int g = (int)std::min<int64_t>(ceil_div(ceil_div(nb, RBK), 256), (int64_t)ctx->num_sms * 8);
+                launch(ctx, "tqp_pkfk_rank_bitmap", rank_bitmap_kernel, dim3(g), dim3(256), 0, bk.data, (int)bk.dtype,
+                       nb, (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get(), B.unsorted.get(),
+                       (uint32_t)(lo >> 32), (uint32_t)span);
+                ctx->add_bytes("tqp_pkfk_rank_bitmap", (double)dtype_size(bk.dtype) * (double)nb + 32.0 * (double)nblk);
+                return;
+            }
+        }
+    }
     B.so.want_internal = true;
     B.so.defer_identity = true;   // a presorted build side may take the rank bitmap straight from the keys
     radix_sort(ctx, bk.data, bk.dtype, nb, false, B.so);
@@ -846,10 +921,6 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allo
     // Build side already in key order (the sort's identity route) over a domain of at most
     // ~8 bytes of bitmap per build row: the rank bitmap replaces T + records (one sector
     // per probe, 9.6 MB at SF10 instead of 64 MB). TQP_PKFK_NO_RANK=1 disables it (A/B).
-    static const bool no_rank = [] {
-        const char* e = std::getenv("TQP_PKFK_NO_RANK");
-        return e && std::atoi(e) != 0;
-    }();
     if (B.so.identity && B.so.k32 && vbits > 0 && !no_rank && allow_rank) {
         // in key order: the keys span [first, last]; the bitmap covers exactly that range
         // (SF100 orders: 6e8 values -> 86 MB, L2-resident, where 2^vbits values took 153 MB)
@@ -862,7 +933,7 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allo
             B.rank_bm.zero();
             const int g = (int)std::min<int64_t>(ceil_div(ceil_div(nb, RBK), 256), (int64_t)ctx->num_sms * 8);
             launch(ctx, "tqp_pkfk_rank_bitmap", rank_bitmap_kernel, dim3(g), dim3(256), 0, bk.data, (int)bk.dtype, nb,
-                   (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get());
+                   (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get(), (int*)nullptr, 0u, 0u);
             ctx->add_bytes("tqp_pkfk_rank_bitmap", (double)dtype_size(bk.dtype) * (double)nb + 32.0 * (double)nblk);
             return;
         }
@@ -908,10 +979,12 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allo
     }
 }
 
-void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, int anti, int64_t* left_out,
+// false: the build side taken as sorted was not (speculative rank route) -- nothing the
+// probe wrote may be used; the caller rebuilds with spec = false and probes again.
+bool run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, int anti, int64_t* left_out,
                int64_t* right_out, uint8_t* match_out, int64_t* n_out_host, const Payload* pay = nullptr) {
     // [0] selected rows, [1] duplicate-build-key flag, [2] direct-output flag: one readback
-    DevBuf<int64_t> pack(ctx, 3);
+    DevBuf<int64_t> pack(ctx, 4);   // + [3] the speculative route's unsorted flag
     pack.zero();
     const int64_t nb = B.nb;
     bool direct_capable = false;
@@ -927,6 +1000,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         a.probe = pk.data;
         a.n_probe = np;
         a.n_build = nb;
+        a.unsorted = B.unsorted.get();
         a.bkeys = B.so.k32 ? (const void*)B.so.keys32.get() : (const void*)B.so.keys64.get();
         a.bperm = B.so.perm32.get();
         a.T = B.T;
@@ -1034,9 +1108,12 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
             // one readback decides: every row matched in the direct layout -> done (no scan,
             // no compaction); else scan the tile counts and compact (after a mispredicted
             // direct layout, from the in-place pairs)
-            int64_t h[3];
+            int64_t h[4];
             if (B.dup.get()) TQP_CUDA(cudaMemcpyAsync(pack.get() + 1, B.dup.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
-            read_back(ctx, h, pack.get(), 24);
+            if (B.unsorted.get())
+                TQP_CUDA(cudaMemcpyAsync(pack.get() + 3, B.unsorted.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
+            read_back(ctx, h, pack.get(), 32);
+            if (h[3]) return false;
             if (h[1]) fail(TQP_ERR_DUPLICATE_BUILD_KEY, "pkfk: duplicate key on the build side");
             const bool direct = (int)h[2] == 0;
             const double ib = a.idx32 ? 4.0 : 8.0;
@@ -1055,7 +1132,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
             }
             if (n_out_host) *n_out_host = h[0];
             ctx->add_bytes("tqp_pkfk_probe", (double)np * dtype_size(pk.dtype) + (direct ? 2.0 * ib * (double)np : 0.0));
-            return;
+            return true;
         }
         scan_add_u32_to_u64_exclusive(ctx, tcnt.get(), toff.get(), tiles);
         if (mode == 0)
@@ -1082,8 +1159,11 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         }
     }
     if (B.dup.get()) TQP_CUDA(cudaMemcpyAsync(pack.get() + 1, B.dup.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
-    int64_t h[3];
-    read_back(ctx, h, pack.get(), 24);
+    if (B.unsorted.get())
+        TQP_CUDA(cudaMemcpyAsync(pack.get() + 3, B.unsorted.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
+    int64_t h[4];
+    read_back(ctx, h, pack.get(), 32);
+    if (h[3]) return false;
     if (h[1] && mode == 0) fail(TQP_ERR_DUPLICATE_BUILD_KEY, "pkfk: duplicate key on the build side");
     if (n_out_host) *n_out_host = h[0];
     if (np > 0 && nb > 0) {   // probe keys in; pairs (join) or mask + selection vector (semi) out
@@ -1096,6 +1176,7 @@ void run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
             ctx->add_bytes("tqp_pkfk_emit", mode == 0 ? ((pay && pay->idx32 ? 4.0 : 8.0) * ((left_out ? 1.0 : 0.0) + (right_out ? 1.0 : 0.0)) + pb) * (double)h[0]
                                                     : (right_out ? 8.0 * (double)h[0] : 0.0));
     }
+    return true;
 }
 // Marks the build rows that some pair references (idempotent byte stores).
 __global__ void mark_rows_kernel(const int64_t* __restrict__ left, int64_t m, int64_t nb, uint8_t* __restrict__ matched) {
@@ -1245,7 +1326,11 @@ void pkfk_join(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int
     if (np >= (int64_t(1) << 40)) fail(TQP_ERR_INVALID_ARGUMENT, "pkfk: probe too large");
     Built B;
     build_side(ctx, bk, nb, B);
-    run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host);
+    if (!run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host)) {
+        B = Built();
+        build_side(ctx, bk, nb, B, true, false);
+        run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host);
+    }
 }
 
 // PK-FK join with payload columns gathered into the output (one row per matching probe
@@ -1277,7 +1362,11 @@ void pkfk_join_payload(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t
     }
     Built B;
     build_side(ctx, bk, nb, B);
-    run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host, &pay);
+    if (!run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host, &pay)) {
+        B = Built();
+        build_side(ctx, bk, nb, B, true, false);
+        run_probe(ctx, B, pk, np, 0, 0, left_out, right_out, nullptr, n_out_host, &pay);
+    }
 }
 
 // The paper's output order (reading R7): the probe side sorted
@@ -1323,8 +1412,13 @@ void pkfk_join_i32(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np,
     pay.idx32 = 1;
     Built B;
     build_side(ctx, bk, nb, B);
-    run_probe(ctx, B, pk, np, 0, 0, reinterpret_cast<int64_t*>(left_out), reinterpret_cast<int64_t*>(right_out), nullptr,
-              n_out_host, &pay);
+    if (!run_probe(ctx, B, pk, np, 0, 0, reinterpret_cast<int64_t*>(left_out), reinterpret_cast<int64_t*>(right_out),
+                   nullptr, n_out_host, &pay)) {
+        B = Built();
+        build_side(ctx, bk, nb, B, true, false);
+        run_probe(ctx, B, pk, np, 0, 0, reinterpret_cast<int64_t*>(left_out), reinterpret_cast<int64_t*>(right_out), nullptr,
+                  n_out_host, &pay);
+    }
 }
 
 void pkfk_semi(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int anti, uint8_t* match_out,
@@ -1333,7 +1427,11 @@ void pkfk_semi(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, int
     check_col(pk, np, "semi probe");
     Built B;
     build_side(ctx, bk, nb, B);
-    run_probe(ctx, B, pk, np, 1, anti, nullptr, sel_out, match_out, n_sel_host);
+    if (!run_probe(ctx, B, pk, np, 1, anti, nullptr, sel_out, match_out, n_sel_host)) {
+        B = Built();
+        build_side(ctx, bk, nb, B, true, false);
+        run_probe(ctx, B, pk, np, 1, anti, nullptr, sel_out, match_out, n_sel_host);
+    }
 }
 
 // Probe-side outer join ("outer = inner pairs + unmatched rows
@@ -1348,9 +1446,13 @@ void pkfk_outer(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np, in
     Built B;
     build_side(ctx, bk, nb, B);
     if (B.rank_bm.get()) {   // a presorted build side with duplicate keys: rank + popcount would be wrong
-        int dup = 0;
-        read_back(ctx, &dup, B.dup.get(), 4);
-        if (dup) {
+        int flags[2] = {0, 0};   // duplicate, speculative route found the build side unsorted
+        DevBuf<int> f(ctx, 2);
+        f.zero();
+        TQP_CUDA(cudaMemcpyAsync(f.get(), B.dup.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        if (B.unsorted.get()) TQP_CUDA(cudaMemcpyAsync(f.get() + 1, B.unsorted.get(), 4, cudaMemcpyDeviceToDevice, ctx->stream));
+        read_back(ctx, flags, f.get(), 8);
+        if (flags[0] || flags[1]) {
             B = Built();
             build_side(ctx, bk, nb, B, false);
         }

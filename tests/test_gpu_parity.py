@@ -1221,3 +1221,36 @@ def test_smj_sparse_matches_empty_buckets(T, frac):
     lo, ro = T.smj_join(cu(left), cu(right))
     olo, oro = oracle.smj_join(left, right)
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+@pytest.mark.parametrize("case", ["one_swap", "shuffled_middle", "out_of_range", "sorted", "sorted_i32"])
+def test_pkfk_speculative_rank_route(T, case):
+    """The build side is taken as sorted from its first and last key alone (the speculative
+    rank-bitmap route); a build side that is not in key order after all -- one adjacent swap,
+    a shuffled middle, a key outside [first, last] -- must be detected and redone, in join,
+    semi and outer mode. Checked against the oracle."""
+    rng = np.random.default_rng(len(case))
+    nb = 300_017
+    build = np.sort(rng.choice(4 * nb, nb, replace=False)).astype(np.int64) + 1000
+    if case == "one_swap":
+        j = nb // 2
+        build[j], build[j + 1] = build[j + 1], build[j]
+    elif case == "shuffled_middle":
+        mid = build[1:-1].copy()
+        rng.shuffle(mid)
+        build[1:-1] = mid
+    elif case == "out_of_range":
+        build[nb // 3] = build[-1] + 5   # above the last key: not sorted, outside [first, last]
+        build = np.concatenate([build[: nb // 3], build[nb // 3:]])
+    dt = torch.int32 if case == "sorted_i32" else torch.int64
+    probe = rng.choice(build, 1_000_003).astype(np.int64)
+    probe[::7] = rng.integers(0, 5 * nb, probe[::7].size)   # some misses
+    lo, ro = T.pkfk_join(cu(build, dt), cu(probe, dt))
+    olo, oro = oracle.pkfk_join(build, probe)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    sel = T.pkfk_semi(cu(build, dt), cu(probe, dt))
+    assert np.array_equal(npy(sel), np.unique(oro))
+    left = T.pkfk_outer(cu(build, dt), cu(probe, dt))
+    want = np.full(probe.size, -1, np.int64)
+    want[oro] = olo
+    assert np.array_equal(npy(left), want)
