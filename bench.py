@@ -156,6 +156,7 @@ class HotPath:
         self.world = world
         self.exchange = placement == "exchange" and world > 1
         self.strategy = None
+        self.transport = "nccl"   # co-partition exchange: NCCL all_to_all, or "p2p" (fused partition + peer stores)
         # streams = 2: the aggregation queries (Q1, Q6 filter, Q6 sum) run on a second
         # stream from a worker thread with their own libtqp context, concurrently with the
         # joins (inter-operator parallelism: independent operators fill each other's
@@ -204,7 +205,8 @@ class HotPath:
         with torch.cuda.stream(self.s3):
             if self.exchange:
                 from paper_2203_01877_b200 import dist
-                self.strategy, lo, ro = dist.pkfk_join_shuffled(self.ctx3, ok, lk, group=self.join_group)
+                self.strategy, lo, ro = dist.pkfk_join_shuffled(self.ctx3, ok, lk, group=self.join_group,
+                                                                transport=self.transport)
             else:
                 lo, ro = self.ctx3.pkfk_join(ok, lk)
         return lo, ro
@@ -225,7 +227,7 @@ class HotPath:
             if self.exchange:
                 from paper_2203_01877_b200 import dist
                 if self.streams == 2:
-                    self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk)
+                    self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk, transport=self.transport)
                 sl, sr = dist.smj_join_copartition(c, ok, lk)
             else:
                 if self.streams == 2:
@@ -242,7 +244,7 @@ class HotPath:
         self._mark("start")
         if self.exchange:   # shuffled placement: the joins exchange over NCCL
             from paper_2203_01877_b200 import dist
-            self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk)
+            self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk, transport=self.transport)
             self._mark("pkfk_join")
             sl, sr = dist.smj_join_copartition(c, ok, lk)
             self._mark("smj_join")
@@ -297,6 +299,7 @@ def run_gpu(args):
                  if (dist and args.streams > 1) else None)
     hp = HotPath(T, orders, li, world, placement, streams=args.streams, agg_group=agg_group)
     hp.streams = 1   # warm-up, kernel table and per-operator timings: one stream
+    hp.transport = args.transport
 
     def barrier():
         if dist:
@@ -357,7 +360,7 @@ def run_gpu(args):
         x_ms = sum(a.elapsed_time(b) for a, b, _, _ in xl) / args.steps
         x_recv = sum(r for _, _, r, _ in xl) / args.steps
         x_sent = sum(sn for _, _, _, sn in xl) / args.steps
-        exchange = {"strategy_pkfk": hp.strategy, "all_to_all_ms_per_step": x_ms,
+        exchange = {"strategy_pkfk": hp.strategy, "transport": args.transport, "all_to_all_ms_per_step": x_ms,
                     "recv_bytes_per_step": x_recv, "sent_bytes_per_step": x_sent,
                     "nvlink_recv_GBps": x_recv / (x_ms / 1e3) / 1e9 if x_ms > 0 else None,
                     "how": "CUDA events around every all_to_all of the step's two joins on this rank (rank 0 shown)"}
@@ -725,6 +728,9 @@ def main():
     # 2: the aggregation queries run on a second stream concurrently with the joins in the
     # timed steps (per-operator times always come from sequential steps)
     ap.add_argument("--streams", type=int, default=2, choices=[1, 2, 3])
+    # N > 1, co-partitioned PK-FK join: NCCL all_to_all, or the fused partition kernel storing
+    # straight into the peers' receive buffers (CUDA IPC / NVLink P2P)
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"])
     ap.add_argument("--cpu-sample-sf", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

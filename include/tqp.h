@@ -360,6 +360,34 @@ tqp_status tqp_groupby_agg(tqp_ctx* ctx, const tqp_col* cols_host, int n_cols, i
  * of one all_to_all_single. 1 <= n_parts <= 256; keys u8 / i32 / i64. */
 tqp_status tqp_partition(tqp_ctx* ctx, tqp_col keys, int64_t n, const int64_t* splitters, int n_parts,
                          int64_t row_base, void* keys_out, int64_t* rows_out, int64_t* counts_out);
+/* The same partition as a fused exchange: no local send buffer, each destination's
+ * block written straight into that destination's receive buffer (a peer GPU's memory
+ * mapped with tqp_ipc_open -- NVLink P2P stores -- or local memory), so the partition's
+ * stores are the all-to-all. Two steps around the count exchange:
+ *   tqp_partition_plan_create: the destination histogram + scan; counts_out (device
+ *     int64, n_parts) = rows per destination; keys and splitters must stay valid until
+ *     the plan is released;
+ *   tqp_partition_scatter: destination d's rows (input order kept) go to
+ *     dst_keys_host[d] + dst_base_host[d] (elements of the key dtype) and, if
+ *     dst_rows_host is not NULL, dst_rows_host[d] + dst_base_host[d] (int64 row_base +
+ *     input row). The pointers (host arrays of n_parts device pointers) may be peers'.
+ * The caller orders the exchange (all destinations' buffers ready before the scatter,
+ * the scatter finished -- device sync + barrier -- before a destination reads). */
+typedef struct tqp_partition_plan tqp_partition_plan;
+tqp_status tqp_partition_plan_create(tqp_ctx* ctx, tqp_col keys, int64_t n, const int64_t* splitters, int n_parts,
+                                     int64_t* counts_out, tqp_partition_plan** plan);
+tqp_status tqp_partition_scatter(tqp_ctx* ctx, tqp_partition_plan* plan, int64_t row_base,
+                                 void* const* dst_keys_host, int64_t* const* dst_rows_host,
+                                 const int64_t* dst_base_host);
+void tqp_partition_release(tqp_ctx* ctx, tqp_partition_plan* plan);
+/* Receive buffers shared between processes (CUDA IPC): tqp_ipc_alloc = an exact
+ * cudaMalloc of `bytes` and its 64-byte IPC handle (handle_out: host, 64 bytes);
+ * tqp_ipc_open maps a peer process's handle (peer access enabled lazily: NVLink P2P
+ * between GPUs, or the same GPU); tqp_ipc_close unmaps; tqp_ipc_free frees. */
+tqp_status tqp_ipc_alloc(tqp_ctx* ctx, size_t bytes, void** dev_ptr_out, void* handle_out);
+tqp_status tqp_ipc_free(tqp_ctx* ctx, void* dev_ptr);
+tqp_status tqp_ipc_open(tqp_ctx* ctx, const void* handle, void** dev_ptr_out);
+tqp_status tqp_ipc_close(tqp_ctx* ctx, void* dev_ptr);
 /* lohi_out (device, 2 x int64) = [min, max] of the key column; an empty column
  * gives [INT64_MAX, INT64_MIN] (so MIN / MAX all-reduces across ranks ignore it). */
 tqp_status tqp_minmax(tqp_ctx* ctx, tqp_col keys, int64_t n, int64_t* lohi_out);

@@ -41,7 +41,8 @@ EXPORTED = [
     "tqp_smj_release",
     "tqp_smj_join", "tqp_pack_keys", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge", "tqp_smj_expand_payload", "tqp_partition", "tqp_minmax",
-    "tqp_range_splitters", "tqp_gather", "tqp_pkfk_outer_build",
+    "tqp_range_splitters", "tqp_gather", "tqp_pkfk_outer_build", "tqp_partition_plan_create", "tqp_partition_scatter",
+    "tqp_partition_release", "tqp_ipc_alloc", "tqp_ipc_free", "tqp_ipc_open", "tqp_ipc_close",
 ]
 
 
@@ -94,6 +95,13 @@ _sig = {
     "tqp_range_splitters": ([_vp, _vp, _int, _vp], _int),
     "tqp_gather": ([_vp, Col, _vp, _i64, _vp], _int),
     "tqp_pkfk_outer_build": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _P(_i64)], _int),
+    "tqp_partition_plan_create": ([_vp, Col, _i64, _vp, _int, _vp, _P(_vp)], _int),
+    "tqp_partition_scatter": ([_vp, _vp, _i64, _P(_vp), _P(_vp), _P(_i64)], _int),
+    "tqp_partition_release": ([_vp, _vp], None),
+    "tqp_ipc_alloc": ([_vp, ctypes.c_size_t, _P(_vp), _vp], _int),
+    "tqp_ipc_free": ([_vp, _vp], _int),
+    "tqp_ipc_open": ([_vp, _vp, _P(_vp)], _int),
+    "tqp_ipc_close": ([_vp, _vp], _int),
     "tqp_smj_join": ([_vp, Col, _i64, Col, _i64, _vp, _vp, _i64, _P(_i64)], _int),
     "tqp_filter_compact": ([_vp, _P(Col), _int, _i64, _P(Pred), _int, _vp, _vp, _P(_i64)], _int),
     "tqp_groupby_prepare": ([_vp, _P(Col), _int, _i64, _P(ctypes.c_int32), _int, _P(Pred), _int, _P(Agg), _int,
@@ -394,6 +402,38 @@ class Context:
                                        _ptr(counts)))
         return ko, ro, counts
 
+    def partition_plan(self, keys, splitters):
+        """Fused-exchange partition, step 1 (tqp_partition_plan_create): -> (PartitionPlan,
+        device int64 counts per destination). Keep `keys` and `splitters` alive."""
+        self._sync_stream()
+        k = _dev_tensor(keys, self.device)
+        spl = _dev_tensor(splitters, self.device).to(torch.int64).contiguous()
+        parts = spl.numel() + 1
+        counts = torch.empty(parts, dtype=torch.int64, device=self.device)
+        h = ctypes.c_void_p()
+        self._check(_lib.tqp_partition_plan_create(self._h, _col(k), k.numel(), _ptr(spl), parts, _ptr(counts),
+                                                   ctypes.byref(h)))
+        return PartitionPlan(self, h, parts, (k, spl)), counts
+
+    def ipc_alloc(self, nbytes):
+        """A cudaMalloc'd buffer shareable with other processes -> (device pointer, 64-byte handle)."""
+        p = ctypes.c_void_p()
+        hb = ctypes.create_string_buffer(64)
+        self._check(_lib.tqp_ipc_alloc(self._h, int(nbytes), ctypes.byref(p), hb))
+        return p.value, hb.raw
+
+    def ipc_free(self, ptr):
+        self._check(_lib.tqp_ipc_free(self._h, ctypes.c_void_p(ptr)))
+
+    def ipc_open(self, handle):
+        """Map another process's buffer (64-byte handle) -> device pointer."""
+        p = ctypes.c_void_p()
+        self._check(_lib.tqp_ipc_open(self._h, ctypes.create_string_buffer(bytes(handle), 64), ctypes.byref(p)))
+        return p.value
+
+    def ipc_close(self, ptr):
+        self._check(_lib.tqp_ipc_close(self._h, ctypes.c_void_p(ptr)))
+
     def minmax(self, keys):
         """Device int64 [min, max] of a key column ([INT64_MAX, INT64_MIN] when empty). No host sync."""
         self._sync_stream()
@@ -508,6 +548,45 @@ class Context:
         self._check(_lib.tqp_groupby_merge(self._h, m, ca, len(ks), aa, len(aggs), pp, _ptr(cnt),
                                            ctypes.byref(plan), ctypes.byref(G)))
         return self._fetch(plan, G.value, [k.dtype for k in ks], aggs)
+
+
+class PartitionPlan:
+    """Step 2 of the fused exchange: scatter(row_base, key_ptrs, row_ptrs, bases) writes
+    destination d's rows at key_ptrs[d] + bases[d] (and row_ptrs[d] + bases[d]); the
+    pointers may be peers' receive buffers (Context.ipc_open)."""
+
+    def __init__(self, ctx, handle, parts, keep):
+        self.ctx, self._h, self.parts, self._keep = ctx, handle, parts, keep
+
+    def scatter(self, row_base, key_ptrs, row_ptrs, bases):
+        c = self.ctx
+        c._sync_stream()
+        n = self.parts
+        kp = (_vp * n)(*key_ptrs)
+        rp = (_vp * n)(*row_ptrs) if row_ptrs is not None else None
+        bp = (ctypes.c_int64 * n)(*bases)
+        c._check(_lib.tqp_partition_scatter(c._h, self._h, int(row_base), kp, rp, bp))
+
+    def release(self):
+        if self._h:
+            _lib.tqp_partition_release(self.ctx._h, self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:
+            pass
+
+
+def device_view(ptr, n, dtype, device):
+    """A torch tensor over n elements of raw device memory at ptr (no copy, not owning)."""
+    typestr = {torch.int64: "<i8", torch.int32: "<i4", torch.uint8: "|u1", torch.float64: "<f8"}[dtype]
+
+    class _A:
+        __cuda_array_interface__ = {"shape": (int(n),), "typestr": typestr, "data": (int(ptr) if n else 0, False),
+                                    "version": 3, "strides": None}
+    return torch.as_tensor(_A(), device=device) if n else torch.empty(0, dtype=dtype, device=device)
 
 
 class SmjPlan:

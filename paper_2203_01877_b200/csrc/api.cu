@@ -32,6 +32,11 @@ void smj_expand_payload(tqp_ctx*, const tqp_smj_plan*, int64_t, int64_t, const t
                         const tqp_col*, int, void* const*, int64_t*, int64_t*);
 void partition(tqp_ctx*, tqp_col, int64_t, const int64_t*, int, int64_t, void*, int64_t*, int64_t*);
 void pkfk_outer_build(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
+tqp_partition_plan* partition_plan(tqp_ctx*, tqp_col, int64_t, const int64_t*, int, int64_t*);
+void partition_scatter(tqp_ctx*, tqp_partition_plan*, int64_t, void* const*, int64_t* const*, const int64_t*);
+void partition_release(tqp_ctx*, tqp_partition_plan*);
+void* ipc_alloc(size_t, void*);
+void* ipc_open(const void*);
 void minmax(tqp_ctx*, tqp_col, int64_t, int64_t*);
 void range_splitters(tqp_ctx*, const int64_t*, int, int64_t*);
 void gather(tqp_ctx*, tqp_col, const int64_t*, int64_t, void*);
@@ -461,6 +466,48 @@ tqp_status tqp_pkfk_outer_build(tqp_ctx* c, tqp_col b, int64_t nb, tqp_col p, in
 tqp_status tqp_partition(tqp_ctx* c, tqp_col keys, int64_t n, const int64_t* splitters, int n_parts, int64_t row_base,
                          void* keys_out, int64_t* rows_out, int64_t* counts_out) {
     TQP_GUARD(c, { tqp::partition(c, keys, n, splitters, n_parts, row_base, keys_out, rows_out, counts_out); });
+}
+
+tqp_status tqp_partition_plan_create(tqp_ctx* c, tqp_col keys, int64_t n, const int64_t* splitters, int n_parts,
+                                     int64_t* counts_out, tqp_partition_plan** plan) {
+    TQP_GUARD(c, {
+        if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "partition_plan: null plan");
+        *plan = tqp::partition_plan(c, keys, n, splitters, n_parts, counts_out);
+    });
+}
+
+tqp_status tqp_partition_scatter(tqp_ctx* c, tqp_partition_plan* plan, int64_t row_base, void* const* dst_keys_host,
+                                 int64_t* const* dst_rows_host, const int64_t* dst_base_host) {
+    TQP_GUARD(c, {
+        if (!plan) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "partition_scatter: null plan");
+        tqp::partition_scatter(c, plan, row_base, dst_keys_host, dst_rows_host, dst_base_host);
+    });
+}
+
+void tqp_partition_release(tqp_ctx* c, tqp_partition_plan* plan) {
+    if (c && plan) tqp::partition_release(c, plan);
+}
+
+tqp_status tqp_ipc_alloc(tqp_ctx* c, size_t bytes, void** dev_ptr_out, void* handle_out) {
+    TQP_GUARD(c, {
+        if (!dev_ptr_out || !handle_out) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "ipc_alloc: null output");
+        *dev_ptr_out = tqp::ipc_alloc(bytes, handle_out);
+    });
+}
+
+tqp_status tqp_ipc_free(tqp_ctx* c, void* dev_ptr) {
+    TQP_GUARD(c, { TQP_CUDA(cudaFree(dev_ptr)); });
+}
+
+tqp_status tqp_ipc_open(tqp_ctx* c, const void* handle, void** dev_ptr_out) {
+    TQP_GUARD(c, {
+        if (!handle || !dev_ptr_out) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "ipc_open: null argument");
+        *dev_ptr_out = tqp::ipc_open(handle);
+    });
+}
+
+tqp_status tqp_ipc_close(tqp_ctx* c, void* dev_ptr) {
+    TQP_GUARD(c, { TQP_CUDA(cudaIpcCloseMemHandle(dev_ptr)); });
 }
 
 tqp_status tqp_minmax(tqp_ctx* c, tqp_col keys, int64_t n, int64_t* lohi_out) {

@@ -79,19 +79,31 @@ __device__ __forceinline__ void st_key(void* out, int64_t pos, int64_t k) {
     else ((unsigned char*)out)[pos] = (unsigned char)k;
 }
 
+// Per-destination output (the fused exchange): destination d's block is written at
+// keys[d] + base[d] / rows[d] + base[d] -- device pointers that may be a peer GPU's
+// receive buffer (CUDA IPC / NVLink P2P), so the partition's stores ARE the all-to-all.
+struct PartDest {
+    void* keys[QMAXP];
+    int64_t* rows[QMAXP];
+    int64_t base[QMAXP];
+};
+
 template <int DT>
 __global__ void __launch_bounds__(QNT) part_scatter_kernel(const void* __restrict__ keys, int64_t n,
                                                            const int64_t* __restrict__ splitters, int parts,
                                                            int64_t tiles, const uint64_t* __restrict__ off,
-                                                           int64_t row_base, void* keys_out, int64_t* rows_out) {
+                                                           int64_t row_base, void* keys_out, int64_t* rows_out,
+                                                           const PartDest* __restrict__ dest) {
     __shared__ int64_t s_spl[QMAXP];
     __shared__ uint64_t s_off[QMAXP];
+    __shared__ int64_t s_dbase[QMAXP];   // dest: base[d] - start of d's block in the local layout
     __shared__ uint32_t s_wc[QNW][QMAXP];   // per-warp counts -> per-warp offsets per destination
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t t = blockIdx.x;
     for (int j = tid; j < parts; j += QNT) {
         if (j < parts - 1) s_spl[j] = splitters[j];
         s_off[j] = off[(int64_t)j * tiles + t];
+        if (dest) s_dbase[j] = dest->base[j] - (int64_t)off[(int64_t)j * tiles];
 #pragma unroll
         for (int w = 0; w < QNW; w++) s_wc[w][j] = 0;
     }
@@ -131,8 +143,14 @@ __global__ void __launch_bounds__(QNT) part_scatter_kernel(const void* __restric
         const int d = dd[s];
         const int64_t p = (int64_t)s_off[d] + s_wc[warp][d] + pos[s];
         TQP_DCHECK(d < parts && p >= 0 && p < n);
-        st_key<DT>(keys_out, p, k[s]);
-        if (rows_out) __stcs((long long*)rows_out + p, (long long)(row_base + row));
+        if (dest) {   // straight into destination d's (possibly remote) receive buffer
+            const int64_t q = s_dbase[d] + p;
+            st_key<DT>(dest->keys[d], q, k[s]);
+            if (dest->rows[d]) __stcs((long long*)dest->rows[d] + q, (long long)(row_base + row));
+        } else {
+            st_key<DT>(keys_out, p, k[s]);
+            if (rows_out) __stcs((long long*)rows_out + p, (long long)(row_base + row));
+        }
     }
 }
 
@@ -214,13 +232,107 @@ void partition(tqp_ctx* ctx, tqp_col keys, int64_t n, const int64_t* splitters, 
     ctx->add_bytes("tqp_partition_hist", (double)n * dtype_size(keys.dtype) + 4.0 * (double)ncnt);
     scan_add_u32_to_u64_exclusive(ctx, cnt.get(), off.get(), ncnt);
     switch (keys.dtype) {
-        case TQP_I64: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_I64>, dim3((unsigned)tiles), dim3(QNT), 0, keys.data, n, splitters, parts, tiles, (const uint64_t*)off.get(), row_base, keys_out, rows_out); break;
-        case TQP_I32: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_I32>, dim3((unsigned)tiles), dim3(QNT), 0, keys.data, n, splitters, parts, tiles, (const uint64_t*)off.get(), row_base, keys_out, rows_out); break;
-        default: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_U8>, dim3((unsigned)tiles), dim3(QNT), 0, keys.data, n, splitters, parts, tiles, (const uint64_t*)off.get(), row_base, keys_out, rows_out); break;
+        case TQP_I64: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_I64>, dim3((unsigned)tiles), dim3(QNT), 0, keys.data, n, splitters, parts, tiles, (const uint64_t*)off.get(), row_base, keys_out, rows_out, (const PartDest*)nullptr); break;
+        case TQP_I32: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_I32>, dim3((unsigned)tiles), dim3(QNT), 0, keys.data, n, splitters, parts, tiles, (const uint64_t*)off.get(), row_base, keys_out, rows_out, (const PartDest*)nullptr); break;
+        default: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_U8>, dim3((unsigned)tiles), dim3(QNT), 0, keys.data, n, splitters, parts, tiles, (const uint64_t*)off.get(), row_base, keys_out, rows_out, (const PartDest*)nullptr); break;
     }
     ctx->add_bytes("tqp_partition", (double)n * (2.0 * dtype_size(keys.dtype) + (rows_out ? 8.0 : 0.0)));
     launch(ctx, "tqp_partition_hist", part_counts_kernel, dim3(1), dim3(256), 0, (const uint64_t*)off.get(), tiles, parts,
            counts);
+}
+
+}  // namespace tqp
+
+struct tqp_partition_plan {
+    tqp_col keys{};
+    int64_t n = 0, tiles = 0;
+    int parts = 1;
+    const int64_t* splitters = nullptr;
+    tqp::DevBuf<uint64_t> off;
+    tqp::DevBuf<tqp::PartDest> dest;
+};
+
+namespace tqp {
+
+// Pass 1 of the fused exchange: the destination histogram and its scan (counts_out: device
+// int64 per destination); the caller exchanges the counts, then scatters into the
+// destinations' buffers with partition_scatter.
+tqp_partition_plan* partition_plan(tqp_ctx* ctx, tqp_col keys, int64_t n, const int64_t* splitters, int parts,
+                                   int64_t* counts) {
+    check_col(keys, n, "partition keys");
+    if (keys.dtype == TQP_F64) fail(TQP_ERR_INVALID_ARGUMENT, "partition: keys must be integer columns");
+    if (parts < 1 || parts > QMAXP) fail(TQP_ERR_INVALID_ARGUMENT, "partition: parts must be in [1, 256]");
+    if (!counts || (parts > 1 && !splitters)) fail(TQP_ERR_INVALID_ARGUMENT, "partition: null splitters / counts");
+    auto* P = new tqp_partition_plan();
+    try {
+        P->keys = keys;
+        P->n = n;
+        P->parts = parts;
+        P->splitters = splitters;
+        P->tiles = ceil_div(n, QTILE);
+        if (n == 0) {
+            TQP_CUDA(cudaMemsetAsync(counts, 0, (size_t)parts * 8, ctx->stream));
+            return P;
+        }
+        const int64_t ncnt = P->tiles * parts;
+        DevBuf<uint32_t> cnt(ctx, ncnt);
+        P->off.alloc(ctx, ncnt + 1);
+        launch(ctx, "tqp_partition_hist", part_hist_kernel, dim3((unsigned)P->tiles), dim3(QNT), 0, keys.data,
+               (int)keys.dtype, n, splitters, parts, P->tiles, cnt.get());
+        ctx->add_bytes("tqp_partition_hist", (double)n * dtype_size(keys.dtype) + 4.0 * (double)ncnt);
+        scan_add_u32_to_u64_exclusive(ctx, cnt.get(), P->off.get(), ncnt);
+        launch(ctx, "tqp_partition_hist", part_counts_kernel, dim3(1), dim3(256), 0, (const uint64_t*)P->off.get(),
+               P->tiles, parts, counts);
+        return P;
+    } catch (...) {
+        delete P;
+        throw;
+    }
+}
+
+void partition_scatter(tqp_ctx* ctx, tqp_partition_plan* P, int64_t row_base, void* const* dkeys, int64_t* const* drows,
+                       const int64_t* dbase) {
+    if (P->n == 0) return;
+    if (!dkeys || !dbase) fail(TQP_ERR_INVALID_ARGUMENT, "partition_scatter: null destination arrays");
+    PartDest h{};
+    for (int d = 0; d < P->parts; d++) {
+        h.keys[d] = dkeys[d];
+        h.rows[d] = drows ? drows[d] : nullptr;
+        h.base[d] = dbase[d];
+    }
+    // the table (6 KB) in device memory: a pageable-source copy returns once the source is
+    // staged, and the buffer's reuse by the next call is stream-ordered after this kernel
+    P->dest.alloc(ctx, 1);
+    TQP_CUDA(cudaMemcpyAsync(P->dest.get(), &h, sizeof(PartDest), cudaMemcpyHostToDevice, ctx->stream));
+    const PartDest* dp = P->dest.get();
+    switch (P->keys.dtype) {
+        case TQP_I64: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_I64>, dim3((unsigned)P->tiles), dim3(QNT), 0, P->keys.data, P->n, P->splitters, P->parts, P->tiles, (const uint64_t*)P->off.get(), row_base, (void*)nullptr, (int64_t*)nullptr, dp); break;
+        case TQP_I32: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_I32>, dim3((unsigned)P->tiles), dim3(QNT), 0, P->keys.data, P->n, P->splitters, P->parts, P->tiles, (const uint64_t*)P->off.get(), row_base, (void*)nullptr, (int64_t*)nullptr, dp); break;
+        default: launch(ctx, "tqp_partition", part_scatter_kernel<TQP_U8>, dim3((unsigned)P->tiles), dim3(QNT), 0, P->keys.data, P->n, P->splitters, P->parts, P->tiles, (const uint64_t*)P->off.get(), row_base, (void*)nullptr, (int64_t*)nullptr, dp); break;
+    }
+    ctx->add_bytes("tqp_partition", (double)P->n * (2.0 * dtype_size(P->keys.dtype) + (drows ? 8.0 : 0.0)));
+}
+
+void partition_release(tqp_ctx*, tqp_partition_plan* P) { delete P; }
+
+// Receive buffers shared across processes (CUDA IPC; peers on NVLink map them over P2P):
+// an exact cudaMalloc (an IPC handle names a whole allocation), its handle, and the
+// importer's mapping of a peer's handle.
+void* ipc_alloc(size_t bytes, void* handle) {
+    void* p = nullptr;
+    TQP_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    cudaIpcMemHandle_t h;
+    TQP_CUDA(cudaIpcGetMemHandle(&h, p));
+    memcpy(handle, &h, sizeof(h));
+    return p;
+}
+
+void* ipc_open(const void* handle) {
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* p = nullptr;
+    TQP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    return p;
 }
 
 void minmax(tqp_ctx* ctx, tqp_col keys, int64_t n, int64_t* lohi) {

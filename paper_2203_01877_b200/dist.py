@@ -70,6 +70,9 @@ class _Comm:
             t.copy_(h)
         return t
 
+    def barrier(self):
+        dist.barrier(group=self.group)
+
     def all_gather_sizes(self, n):
         """Every rank's element count (one tiny collective + host read)."""
         x = torch.tensor([n], dtype=torch.int64, device=self._dev())
@@ -200,7 +203,7 @@ def pkfk_join_broadcast(ops, build_keys, probe_keys, group=None):
     return lo, ro
 
 
-def pkfk_join_copartition(ops, build_keys, probe_keys, group=None, exchange=None):
+def pkfk_join_copartition(ops, build_keys, probe_keys, group=None, exchange=None, transport="nccl"):
     """Shuffled-layout PK-FK join by co-partitioning on key ranges (all on the GPU up to the
     all_to_all split sizes). Returns this rank's (global build row, global probe row) pairs
     for its key range, ascending by global probe row; the union over ranks is the
@@ -220,6 +223,11 @@ def pkfk_join_copartition(ops, build_keys, probe_keys, group=None, exchange=None
     comm.all_reduce(red, op=dist.ReduceOp.MIN)
     lohi = torch.stack([red[0], ~red[1]])
     spl = ops.range_splitters(lohi, G)
+    if transport == "p2p":   # the fused partition + exchange over peer memory
+        rb_key, rb_row, rp_key, rp_row = _pkfk_exchange_p2p(ops, comm, build_keys, probe_keys, spl, boff, poff,
+                                                            exchange)
+        (gl,), (gr,), _ = ops.pkfk_join_payload(rb_key, rp_key, [rb_row], [rp_row], indices=False)
+        return gl, gr
     bk, brow, bcnt = ops.partition(build_keys, spl, row_base=boff)
     pk, prow, pcnt = ops.partition(probe_keys, spl, row_base=poff)
     send, recv = comm.exchange_counts(torch.stack([bcnt, pcnt], dim=1))
@@ -238,6 +246,118 @@ def pkfk_join_copartition(ops, build_keys, probe_keys, group=None, exchange=None
     return gl, gr
 
 
+# ------------------------------------------- fused exchange over peer memory (P2P)
+
+class _Arena:
+    """This process's receive arena, shared with the other ranks by CUDA IPC (grow-only),
+    and the mappings of the other ranks' arenas. With GPUs on NVLink the mappings are P2P
+    windows: a partition kernel's stores into them travel over NVLink (the fused
+    partition + all-to-all); ranks on one GPU map each other's memory on that GPU."""
+
+    def __init__(self, ops):
+        self.ops, self.ptr, self.cap, self.handle, self.gen = ops, None, 0, bytes(64), 0
+        self.peers = {}    # rank -> (gen, mapped pointer)
+
+    def sync(self, comm, need):
+        """Grow to `need` bytes if necessary, exchange (generation, handle) with every rank,
+        (re)map the peers whose arena changed. Returns {rank: base pointer}."""
+        old = None
+        if need > self.cap:
+            old = self.ptr
+            self.cap = max(need, 2 * self.cap, 1 << 20)
+            self.ptr, self.handle = self.ops.ipc_alloc(self.cap)
+            self.gen += 1
+        mine = torch.tensor(list(self.gen.to_bytes(8, "little")) + list(self.handle) + [int(old is not None)],
+                            dtype=torch.uint8)
+        allb = comm.all_gather_cat(mine.to(comm._dev())).cpu().reshape(comm.world, 73)
+        bases = {}
+        for r in range(comm.world):
+            if r == comm.rank:
+                bases[r] = self.ptr
+                continue
+            gen = int.from_bytes(bytes(allb[r, :8].tolist()), "little")
+            if r not in self.peers or self.peers[r][0] != gen:
+                if r in self.peers:
+                    self.ops.ipc_close(self.peers[r][1])
+                self.peers[r] = (gen, self.ops.ipc_open(bytes(allb[r, 8:72].tolist())))
+            bases[r] = self.peers[r][1]
+        if int(allb[:, 72].sum()) > 0:   # some arena moved: once every rank has closed the old
+            comm.barrier()               # mappings (above), the owners free the old arenas
+            if old is not None:
+                self.ops.ipc_free(old)
+        return bases
+
+
+_ARENAS = {}
+
+
+def _arena(ops):
+    key = (id(ops), torch.cuda.current_device())
+    if key not in _ARENAS:
+        _ARENAS[key] = _Arena(ops)
+    return _ARENAS[key]
+
+
+def _align(x, a=256):
+    return (x + a - 1) // a * a
+
+
+def _pkfk_exchange_p2p(ops, comm, bk, pk, spl, boff, poff, exchange=None):
+    """Co-partition exchange by the fused partition: each rank's scatter writes its rows
+    straight into the owner ranks' arenas (no send buffer, no NCCL). Returns the received
+    (build key, build row, probe key, probe row) as views of this rank's arena, in
+    source-rank order like all_to_all."""
+    G, me = comm.world, comm.rank
+    plan_b, cnt_b = ops.partition_plan(bk, spl)
+    plan_p, cnt_p = ops.partition_plan(pk, spl)
+    M = comm.all_gather_cat(torch.stack([cnt_b, cnt_p]).reshape(-1).to(comm._dev())).cpu().reshape(G, 2, G).tolist()
+    kbs, kps = bk.element_size(), pk.element_size()
+
+    def layout(d):   # byte offsets of rank d's four sections, and its need
+        rb = sum(M[s][0][d] for s in range(G))
+        rp = sum(M[s][1][d] for s in range(G))
+        o_bk = 0
+        o_br = _align(o_bk + rb * kbs)
+        o_pk = _align(o_br + rb * 8)
+        o_pr = _align(o_pk + rp * kps)
+        return (o_bk, o_br, o_pk, o_pr), _align(o_pr + rp * 8), rb, rp
+
+    lays = [layout(d) for d in range(G)]
+    torch.cuda.synchronize()
+    comm.barrier()   # every rank is done reading its arena from the previous exchange
+    bases = _arena(ops).sync(comm, lays[me][1])
+    log = EXCHANGE_LOG is not None
+    if log:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+    for side, plan, off, es in ((0, plan_b, boff, kbs), (1, plan_p, poff, kps)):
+        kptr, rptr, base = [], [], []
+        for d in range(G):
+            o = lays[d][0]
+            kptr.append(bases[d] + o[2 * side])
+            rptr.append(bases[d] + o[2 * side + 1])
+            base.append(sum(M[s][side][d] for s in range(me)))   # this source's slot in d's block
+        plan.scatter(off, kptr, rptr, base)
+    if log:   # the fused partition + transfer kernels (bytes: what crossed to other ranks)
+        e1.record()
+        EXCHANGE_LOG.append((e0, e1, sum((kbs + 8) * M[s][0][me] + (kps + 8) * M[s][1][me] for s in range(G) if s != me),
+                             sum((kbs + 8) * M[me][0][d] + (kps + 8) * M[me][1][d] for d in range(G) if d != me)))
+    torch.cuda.synchronize()
+    comm.barrier()   # every block has landed in its destination
+    plan_b.release()
+    plan_p.release()
+    (o_bk, o_br, o_pk, o_pr), _, rb, rp = lays[me]
+    a = bases[me]
+    dev = bk.device
+    from paper_2203_01877_b200 import device_view
+    if exchange is not None:
+        exchange["sent_bytes"] = sum((kbs + 8) * M[me][0][d] + (kps + 8) * M[me][1][d] for d in range(G) if d != me)
+        exchange["recv_bytes"] = sum((kbs + 8) * M[s][0][me] + (kps + 8) * M[s][1][me] for s in range(G) if s != me)
+        exchange["transport"] = "p2p"
+    return (device_view(a + o_bk, rb, bk.dtype, dev), device_view(a + o_br, rb, torch.int64, dev),
+            device_view(a + o_pk, rp, pk.dtype, dev), device_view(a + o_pr, rp, torch.int64, dev))
+
+
 def pkfk_cost_bytes(n_build, n_probe, world, key_bytes=8, row_bytes=8):
     """Bytes received per rank by each shuffled-layout strategy:
     broadcast = every other rank's build keys; co-partition = the (key, row) pairs of
@@ -247,7 +367,7 @@ def pkfk_cost_bytes(n_build, n_probe, world, key_bytes=8, row_bytes=8):
             "copartition": (n_build + n_probe) / world * (key_bytes + row_bytes) * f}
 
 
-def pkfk_join_shuffled(ops, build_keys, probe_keys, group=None, strategy="auto", exchange=None):
+def pkfk_join_shuffled(ops, build_keys, probe_keys, group=None, strategy="auto", exchange=None, transport="nccl"):
     """Shuffled-layout PK-FK join with the cheaper exchange (or the one asked for).
     Returns (strategy, global build rows, global probe rows); broadcast pairs come in
     local probe order, co-partition pairs by global probe row within the rank's range."""
@@ -264,7 +384,7 @@ def pkfk_join_shuffled(ops, build_keys, probe_keys, group=None, strategy="auto",
             exchange["recv_bytes"] = (sum(sizes) - sizes[comm.rank]) * build_keys.element_size()
             exchange["sent_bytes"] = sizes[comm.rank] * build_keys.element_size() * (comm.world - 1)
         return strategy, lo, ro
-    gl, gr = pkfk_join_copartition(ops, build_keys, probe_keys, group, exchange)
+    gl, gr = pkfk_join_copartition(ops, build_keys, probe_keys, group, exchange, transport)
     return strategy, gl, gr
 
 

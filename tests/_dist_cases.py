@@ -162,7 +162,7 @@ def _slice(t, rank, world):
 
 # ------------------------------------------------------------------------- worker
 
-def worker(rank, world, port, use_gpu, out_q):
+def worker(rank, world, port, use_gpu, out_q, transport="nccl"):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -190,12 +190,18 @@ def worker(rank, world, port, use_gpu, out_q):
         # PK-FK join, shuffled layout, both exchanges
         for strategy in ("copartition", "broadcast", "auto"):
             ex = {}
-            s, gl, gr = D.pkfk_join_shuffled(ops, orders["o_orderkey"], lk, strategy=strategy, exchange=ex)
+            s, gl, gr = D.pkfk_join_shuffled(ops, orders["o_orderkey"], lk, strategy=strategy, exchange=ex,
+                                             transport=transport)
             out["pkfk_" + strategy] = (s, h(gl), h(gr), ex)
+        if transport == "p2p":   # twice more: the arenas are reused (and grow once for the int32 case)
+            for _ in range(2):
+                s, gl, gr = D.pkfk_join_shuffled(ops, orders["o_orderkey"], lk, strategy="copartition",
+                                                 transport=transport)
+                assert (h(gl) == out["pkfk_copartition"][1]).all() and (h(gr) == out["pkfk_copartition"][2]).all()
         out["parent"] = h(parent)
         # int32 keys through the partition (co-partition) path
         s, gl, gr = D.pkfk_join_shuffled(ops, orders["o_orderkey"].to(torch.int32), lk.to(torch.int32),
-                                         strategy="copartition")
+                                         strategy="copartition", transport=transport)
         out["pkfk_i32"] = (h(gl), h(gr))
         # sample sort and SMJ on slices of global columns
         inp = smj_inputs(world)
@@ -216,12 +222,12 @@ def worker(rank, world, port, use_gpu, out_q):
         dist.destroy_process_group()
 
 
-def run(world, use_gpu):
+def run(world, use_gpu, transport="nccl"):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, world, port, use_gpu, q)) for r in range(world)]
+    procs = [ctx.Process(target=worker, args=(r, world, port, use_gpu, q, transport)) for r in range(world)]
     for p in procs:
         p.start()
     outs = sorted([q.get(timeout=600) for _ in range(world)], key=lambda o: o["rank"])
