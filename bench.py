@@ -157,6 +157,7 @@ class HotPath:
         self.exchange = placement == "exchange" and world > 1
         self.strategy = None
         self.transport = "nccl"   # co-partition exchange: NCCL all_to_all, or "p2p" (fused partition + peer stores)
+        self.pkfk_strategy = "auto"
         # streams = 2: the aggregation queries (Q1, Q6 filter, Q6 sum) run on a second
         # stream from a worker thread with their own libtqp context, concurrently with the
         # joins (inter-operator parallelism: independent operators fill each other's
@@ -206,7 +207,7 @@ class HotPath:
             if self.exchange:
                 from paper_2203_01877_b200 import dist
                 self.strategy, lo, ro = dist.pkfk_join_shuffled(self.ctx3, ok, lk, group=self.join_group,
-                                                                transport=self.transport)
+                                                                strategy=self.pkfk_strategy, transport=self.transport)
             else:
                 lo, ro = self.ctx3.pkfk_join(ok, lk)
         return lo, ro
@@ -227,7 +228,7 @@ class HotPath:
             if self.exchange:
                 from paper_2203_01877_b200 import dist
                 if self.streams == 2:
-                    self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk, transport=self.transport)
+                    self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk, strategy=self.pkfk_strategy, transport=self.transport)
                 sl, sr = dist.smj_join_copartition(c, ok, lk)
             else:
                 if self.streams == 2:
@@ -244,7 +245,7 @@ class HotPath:
         self._mark("start")
         if self.exchange:   # shuffled placement: the joins exchange over NCCL
             from paper_2203_01877_b200 import dist
-            self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk, transport=self.transport)
+            self.strategy, lo, ro = dist.pkfk_join_shuffled(c, ok, lk, strategy=self.pkfk_strategy, transport=self.transport)
             self._mark("pkfk_join")
             sl, sr = dist.smj_join_copartition(c, ok, lk)
             self._mark("smj_join")
@@ -300,6 +301,7 @@ def run_gpu(args):
     hp = HotPath(T, orders, li, world, placement, streams=args.streams, agg_group=agg_group)
     hp.streams = 1   # warm-up, kernel table and per-operator timings: one stream
     hp.transport = args.transport
+    hp.pkfk_strategy = args.pkfk_strategy
 
     def barrier():
         if dist:
@@ -363,7 +365,8 @@ def run_gpu(args):
         exchange = {"strategy_pkfk": hp.strategy, "transport": args.transport, "all_to_all_ms_per_step": x_ms,
                     "recv_bytes_per_step": x_recv, "sent_bytes_per_step": x_sent,
                     "nvlink_recv_GBps": x_recv / (x_ms / 1e3) / 1e9 if x_ms > 0 else None,
-                    "how": "CUDA events around every all_to_all of the step's two joins on this rank (rank 0 shown)"}
+                    "how": "CUDA events around every all_to_all (NCCL) or fused partition-scatter (p2p) of the step's two "
+                           "joins on this rank (rank 0 shown)"}
     ms_local = t0.elapsed_time(t1)
     kstats, launches = {}, 0
     for c in ctxs:   # the dominant kernel may run on either context
@@ -731,6 +734,7 @@ def main():
     # N > 1, co-partitioned PK-FK join: NCCL all_to_all, or the fused partition kernel storing
     # straight into the peers' receive buffers (CUDA IPC / NVLink P2P)
     ap.add_argument("--transport", default="nccl", choices=["nccl", "p2p"])
+    ap.add_argument("--pkfk-strategy", default="auto", choices=["auto", "broadcast", "copartition"])
     ap.add_argument("--cpu-sample-sf", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
