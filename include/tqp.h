@@ -87,6 +87,13 @@ int64_t tqp_ctx_launch_count(const tqp_ctx* ctx);
  * the temporary is released; returns the number of overwritten canaries seen. */
 int64_t tqp_ctx_guard_violations(const tqp_ctx* ctx);
 void tqp_ctx_reset_counters(tqp_ctx* ctx);
+/* Plan-compiled kernels (process-wide, all contexts): the dense group-by kernel of
+ * tqp_groupby_agg is compiled at run time for each distinct aggregation plan (NVRTC,
+ * sm_100a; environment TQP_JIT=0 disables it, TQP_JIT_MIN_ROWS (default 2^20) is the
+ * smallest input that uses it). Writes the number of plans compiled successfully, the
+ * compilations that failed (the generic kernel ran instead) and the launches of compiled
+ * kernels; any pointer may be NULL. Returns 1 if the runtime compiler was found, else 0. */
+int tqp_jit_counters(int64_t* compiled_host, int64_t* failed_host, int64_t* launches_host);
 tqp_status tqp_ctx_set_profiling(tqp_ctx* ctx, int enable);
 /* Restrict profiling to kernels whose name starts with name_prefix (NULL or ""
  * = every kernel). Two event records per profiled launch cost host time that the

@@ -42,7 +42,7 @@ EXPORTED = [
     "tqp_smj_join", "tqp_pack_keys", "tqp_filter_compact", "tqp_groupby_prepare", "tqp_groupby_fetch", "tqp_groupby_release",
     "tqp_groupby_agg", "tqp_groupby_merge", "tqp_smj_expand_payload", "tqp_partition", "tqp_minmax",
     "tqp_range_splitters", "tqp_gather", "tqp_pkfk_outer_build", "tqp_partition_plan_create", "tqp_partition_scatter",
-    "tqp_partition_release", "tqp_ipc_alloc", "tqp_ipc_free", "tqp_ipc_open", "tqp_ipc_close",
+    "tqp_partition_release", "tqp_ipc_alloc", "tqp_ipc_free", "tqp_ipc_open", "tqp_ipc_close", "tqp_jit_counters",
 ]
 
 
@@ -69,6 +69,7 @@ _sig = {
     "tqp_last_error": ([_vp], ctypes.c_char_p),
     "tqp_ctx_launch_count": ([_vp], _i64),
     "tqp_ctx_guard_violations": ([_vp], _i64),
+    "tqp_jit_counters": ([_vp, _vp, _vp], ctypes.c_int),
     "tqp_ctx_reset_counters": ([_vp], None),
     "tqp_ctx_set_profiling": ([_vp, _int], _int),
     "tqp_ctx_set_profiling_filter": ([_vp, ctypes.c_char_p], _int),
@@ -130,6 +131,14 @@ def lib_path():
 
 def abi_version():
     return _lib.tqp_abi_version()
+
+
+def jit_counters():
+    """Plan-compiled dense group-by kernels (process-wide): {"available", "compiled",
+    "failed", "launches"} -- include/tqp.h tqp_jit_counters."""
+    c, f, l = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    ok = _lib.tqp_jit_counters(ctypes.byref(c), ctypes.byref(f), ctypes.byref(l))
+    return {"available": bool(ok), "compiled": c.value, "failed": f.value, "launches": l.value}
 
 
 _DT = {torch.uint8: TQP_U8, torch.bool: TQP_U8, torch.int32: TQP_I32, torch.int64: TQP_I64,

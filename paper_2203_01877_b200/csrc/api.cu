@@ -6,6 +6,7 @@
 #include <cstring>
 
 #include "internal.h"
+#include "jit.h"
 
 namespace tqp {
 void pkfk_join(tqp_ctx*, tqp_col, int64_t, tqp_col, int64_t, int64_t*, int64_t*, int64_t*);
@@ -208,6 +209,14 @@ const char* tqp_last_error(const tqp_ctx* c) { return c ? c->err.c_str() : "null
 int64_t tqp_ctx_launch_count(const tqp_ctx* c) { return c ? c->launches : 0; }
 
 int64_t tqp_ctx_guard_violations(const tqp_ctx* c) { return c ? c->guard_violations : 0; }
+
+int tqp_jit_counters(int64_t* compiled, int64_t* failed, int64_t* launches) {
+    const tqp::JitCounters c = tqp::jit_counters();
+    if (compiled) *compiled = c.compiled;
+    if (failed) *failed = c.failed;
+    if (launches) *launches = c.launches;
+    return tqp::jit_available() ? 1 : 0;
+}
 
 void tqp_ctx_reset_counters(tqp_ctx* c) {
     if (!c) return;

@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "jit.h"
 
 struct tqp_groupby_plan {
     int64_t G = 0;
@@ -2325,6 +2326,9 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
         constexpr int dense_dr = 4;
         int dense_dk = 0;   // 4: the dense ids by compares against <= 4 keys in registers
         int64_t dense_grid = 0;
+        bool dense_jit = false;     // launch the kernel compiled for this plan (jit.cu)
+        DenseJitSpec jit_spec;
+        size_t dense_jit_smem = 0;
         const char* dz = getenv("TQP_GROUPBY_DENSE");
         bool small_add = true;   // the dense bound argument needs |add| < 2^61
         for (int j = 0; j < PL->n_pairs && j < PCH; j++)
@@ -2396,6 +2400,55 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                         }
                     }
                 }
+                // the kernel compiled for this plan (jit.cu) in the chosen configuration; its
+                // own occupancy sizes the grid
+                dense_jit = false;
+                const char* jm = getenv("TQP_JIT_MIN_ROWS");
+                const int64_t jit_min = jm ? atoll(jm) : (int64_t(1) << 20);
+                if (best_w > 0 && n >= jit_min && jit_enabled()) {
+                    const int64_t tr = (int64_t)dense_nt * dense_dr;
+                    DenseJitSpec& js = jit_spec;
+                    js = DenseJitSpec{};
+                    js.nt = dense_nt;
+                    js.ns = dense_ns;
+                    js.stage_bytes = (int)((int64_t)a.stage_bytes * tr / GTILE);
+                    js.n_ucols = a.n_ucols;
+                    for (int c = 0; c < a.n_ucols; c++) {
+                        js.udt[c] = a.udt[c];
+                        js.uoff[c] = (int)((int64_t)a.uoff[c] * tr / GTILE);
+                    }
+                    js.n_terms = a.ts.n;
+                    js.never = a.ts.never;
+                    for (int q = 0; q < a.ts.n; q++) {
+                        js.tcol[q] = a.ts.t[q].col;
+                        js.tdt[q] = a.ts.t[q].dt;
+                        js.tneg[q] = a.ts.t[q].neg;
+                        js.tlo[q] = a.ts.t[q].lo;
+                        js.twidth[q] = a.ts.t[q].width;
+                    }
+                    js.n_keys = n_keys;
+                    for (int k = 0; k < n_keys; k++) js.kslot[k] = a.kcol[k];
+                    js.n_pairs = PL->n_pairs;
+                    for (int j = 0; j < PL->n_pairs; j++) {
+                        js.prop[j] = a.prop[j];
+                        js.pnf[j] = a.pnf[j];
+                        js.pext[j] = a.pext[j];
+                        for (int f = 0; f < a.pnf[j]; f++) {
+                            js.pslot[j][f] = a.pfc[j][f];
+                            js.psign[j][f] = a.psign[j][f];
+                            js.padd[j][f] = a.padd[j][f];
+                        }
+                    }
+                    js.dk = dense_dk;
+                    const size_t accb = (size_t)D * PL->n_pairs * dense_nt * 8 + (size_t)D * dense_nt * 4;
+                    const size_t sm = (size_t)dense_ns * js.stage_bytes + DENSE_JIT_HDR + accb;
+                    const int occ = sm <= 227 * 1024 ? dense_jit_occupancy(js, sm) : 0;
+                    if (occ > 0) {
+                        dense_jit = true;
+                        dense_jit_smem = sm;
+                        dense_grid = (int64_t)ctx->num_sms * occ;
+                    }
+                }
                 if (best_w > 0) {
                     const int64_t tr = (int64_t)dense_nt * dense_dr;
                     dense_grid = std::min<int64_t>(dense_grid, ceil_div(n, tr));
@@ -2462,10 +2515,32 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                 for (int j = 0; j < PL->n_pairs && j < PCH; j++)
                     for (int f = 0; f < pnf[j]; f++) ad.poff[j][f] = ad.uoff[a.pfc[j][f]];
                 tile_name = "tqp_groupby_dense";
-                dense_call(dense_nt, dense_spec, dense_dk, [&](auto* kfn) {
-                    set_smem(kfn, dense_smem);
-                    launch(ctx, tile_name, kfn, dim3((unsigned)dense_grid), dim3(dense_nt), dense_smem, ad);
-                });
+                bool done = false;
+                if (dense_jit) {
+                    DenseJitArgs ja{};
+                    for (int c = 0; c < a.n_ucols; c++) ja.ucol[c] = a.ucol[c];
+                    ja.n = n;
+                    ja.n_tiles = ad.n_tiles;
+                    ja.D = a.D;
+                    ja.dense_bits = a.dense_bits;
+                    ja.bulk_ok = a.bulk_ok;
+                    ja.krange = a.krange;
+                    ja.dkeys = reinterpret_cast<const unsigned long long*>(a.dkeys);
+                    ja.dtab = a.dtab;
+                    ja.overflow = a.overflow;
+                    for (int j = 0; j < PL->n_pairs; j++) {
+                        ja.plo[j] = reinterpret_cast<unsigned long long*>(a.plo[j]);
+                        ja.phi[j] = reinterpret_cast<long long*>(a.phi[j]);
+                    }
+                    ja.pkey = reinterpret_cast<unsigned long long*>(a.pkey);
+                    ja.pcount = reinterpret_cast<long long*>(a.pcount);
+                    done = dense_jit_launch(ctx, jit_spec, ja, dense_grid, dense_jit_smem, tile_name);
+                }
+                if (!done)
+                    dense_call(dense_nt, dense_spec, dense_dk, [&](auto* kfn) {
+                        set_smem(kfn, dense_smem);
+                        launch(ctx, tile_name, kfn, dim3((unsigned)dense_grid), dim3(dense_nt), dense_smem, ad);
+                    });
             } else if (n > 0 && nokey_path) {
                 tile_name = "tqp_groupby_tile";
                 if (nokey_smem > 227 * 1024) fail(TQP_ERR_INVALID_ARGUMENT, "groupby: referenced columns too wide");

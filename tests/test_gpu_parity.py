@@ -751,13 +751,27 @@ def test_groupby_spec_example(T):
     assert T.int128_to_ints(got["results"][0]) == g["sums"]
 
 
+@pytest.fixture(params=["jit", "generic"])
+def dense_kernel(request, monkeypatch):
+    """The dense group-by kernel compiled for the plan (jit.cu; TQP_JIT_MIN_ROWS=0 so every
+    size uses it) or the generic one (TQP_JIT=0): both must give the oracle's result."""
+    if request.param == "jit":
+        monkeypatch.setenv("TQP_JIT_MIN_ROWS", "0")
+    else:
+        monkeypatch.setenv("TQP_JIT", "0")
+    return request.param
+
+
 @pytest.mark.parametrize("sf", [0.01, 1.0])
-def test_groupby_q1_parity(T, sf):
+def test_groupby_q1_parity(T, sf, dense_kernel):
     _, li = tpch_orders_lineitem(sf, seed=42, device="cuda")
     cols = columns(li, Q1_COLS)
+    jit0 = T.jit_counters()
     got = T.groupby_agg(cols, Q1_KEYS, Q1_AGGS, Q1_PREDS)
     want = oracle.groupby_agg([npy(c) for c in cols], Q1_KEYS, Q1_AGGS, Q1_PREDS)
     check_groupby(T, got, want, Q1_AGGS)
+    if dense_kernel == "jit":   # Q1's four (returnflag, linestatus) groups: the compiled kernel
+        assert T.jit_counters()["launches"] > jit0["launches"]
 
 
 def test_groupby_q6_fused_sum(T):
@@ -814,8 +828,10 @@ def test_groupby_sum_magnitude_tiers(T, e, card):
     check_groupby(T, got, want, aggs)
 
 
+
+
 @pytest.mark.parametrize("card,wide", [(1, False), (2, False), (5, False), (6, False), (5, True)])
-def test_groupby_dense_path(T, card, wide, monkeypatch):
+def test_groupby_dense_path(T, card, wide, monkeypatch, dense_kernel):
     """Few distinct packed keys (<= 16, packed width <= 16 bits) take the sort-free dense
     kernel; both it and the general tile path (TQP_GROUPBY_DENSE=0) match the oracle."""
     rng = np.random.default_rng(card)
@@ -852,7 +868,7 @@ def test_groupby_dense_path(T, card, wide, monkeypatch):
 
 
 @pytest.mark.parametrize("where", ["first_unsampled", "middle", "last_row"])
-def test_groupby_dense_sampled_presence_miss(T, where):
+def test_groupby_dense_sampled_presence_miss(T, where, dense_kernel):
     """The dense path takes key presence from a sample of 16-row groups (n > 2^21 rows here,
     so every 3rd group); keys that occur only in unsampled rows are flagged by the dense
     kernel and the presence pass is redone over every row, so no group is lost."""
@@ -871,7 +887,7 @@ def test_groupby_dense_sampled_presence_miss(T, where):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_groupby_dense_path_random(T, seed):
+def test_groupby_dense_path_random(T, seed, dense_kernel):
     """Dense path over three key columns (u8, negative i32, u8), != / range predicates that
     may empty some or all groups, and SUM / MIN / MAX / AVG / COUNT of signed expressions."""
     rng = np.random.default_rng(100 + seed)
@@ -887,6 +903,7 @@ def test_groupby_dense_path_random(T, seed):
             ("avg", [(3, 0, 1)]), ("count", []), ("sum", [(4, 0, 1)])]
     preds = [[], [(4, "ne", 0), (3, "gt", -5 * 10**8)], [(1, "ne", -3)], [(4, "gt", 200)]][seed % 4]
     want = oracle.groupby_agg(cols, [0, 1, 2], aggs, preds)
+    jit0 = T.jit_counters()
     ctx = T.context()
     ctx.reset_counters()
     ctx.set_profiling(True)
@@ -895,9 +912,12 @@ def test_groupby_dense_path_random(T, seed):
     ctx.set_profiling(False)
     check_groupby(T, got, want, aggs)
     assert "tqp_groupby_dense" in st   # 12 possible keys, packed width 1 + 3 + 1 bits
+    if dense_kernel == "jit":
+        jc = T.jit_counters()
+        assert jc["available"] and jc["launches"] > jit0["launches"] and jc["failed"] == 0
 
 
-def test_groupby_dense_bound_fallback(T):
+def test_groupby_dense_bound_fallback(T, dense_kernel):
     """A product the dense path cannot prove exact re-runs on the general path."""
     rng = np.random.default_rng(3)
     n = 100_000
