@@ -10,14 +10,14 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/$
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-sf100"
 timeout 600 $CMD > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launch.log 2>&1
-for K in gb_dense_kernel gb_phase1 scatter_tma probe_sector expand_kernel filter_mask bucket_r rank_bitmap andor_hist0 tile_hist; do
+for K in tqp_groupby_dense_jit gb_phase1 scatter_tma probe_sector expand_kernel filter_mask bucket_r rank_bitmap andor_hist0 tile_hist; do
   C=2; S=0
   if [ $K = scatter_tma ]; then C=9; S=0; fi   # every scatter launch of one step (the bench averages them all)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c $C -o gpurun_out/${TAG}_full_$K $CMD > gpurun_out/${TAG}_ncu_full_$K.log 2>&1
 done
 python tools/profile_summary.py ${TAG} gpurun_out/${TAG}_summary
 mkdir -p gpurun_out/${TAG}_reps
-for K in gb_dense_kernel scatter_tma probe_sector expand_kernel; do
+for K in tqp_groupby_dense_jit scatter_tma probe_sector expand_kernel; do
   ncu -i gpurun_out/${TAG}_full_$K.ncu-rep --page raw --csv > gpurun_out/${TAG}_reps/${K}_raw.csv 2>/dev/null
   ncu -i gpurun_out/${TAG}_full_$K.ncu-rep --page source --csv --print-source cuda,sass > gpurun_out/${TAG}_reps/${K}_source.csv 2>/dev/null
 done

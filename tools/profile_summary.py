@@ -11,7 +11,7 @@ NAME = [("probe_sector", "tqp_pkfk_probe"), ("probe_sample", "tqp_pkfk_sample"),
         ("tile_rbounds", "tqp_smj_bounds"), ("part_hist", "tqp_partition_hist"), ("part_counts", "tqp_partition_hist"),
         ("part_scatter", "tqp_partition"), ("first_last", "tqp_sort_andor"), ("minmax", "tqp_minmax"),
         ("range_splitters", "tqp_range_splitters"), ("gather_kernel", "tqp_gather"),
-        ("gb_phase1", "tqp_groupby_tile"), ("gb_dense_kernel", "tqp_groupby_dense"), ("gb_presence", "tqp_groupby_presence"),
+        ("gb_phase1", "tqp_groupby_tile"), ("tqp_groupby_dense_jit", "tqp_groupby_dense"), ("gb_dense_kernel", "tqp_groupby_dense"), ("gb_presence", "tqp_groupby_presence"),
         ("gb_dense_ids", "tqp_groupby_dense_ids"), ("key_range", "tqp_groupby_keyrange"), ("scatter_tma", "tqp_sort_scatter"), ("scatter_kernel", "tqp_sort_scatter"),
         ("probe_kernel", "tqp_pkfk_probe"), ("emit_kernel", "tqp_pkfk_emit"), ("filter_mask", "tqp_filter"),
         ("filter_sel", "tqp_filter_select"), ("rle_count", "tqp_smj_rle"), ("rle_write", "tqp_smj_rle"),
