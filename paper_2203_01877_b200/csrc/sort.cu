@@ -367,19 +367,20 @@ __device__ __forceinline__ KT conv_key(typename InKey<IN, KT>::T v, bool desc) {
     return (KT)(desc ? ~u : u);
 }
 
-template <typename KT, int IN, int IPT, int RB>
+template <typename KT, int IN, int IPT, int RB, int SNT = NT>
 struct ScatterWork {
+    static constexpr int SNW = SNT / 32;
     union {
         struct {
-            uint32_t whist[NW][1 << RB];
-            uint32_t match[NW][1 << RB];   // per-warp digit -> lane bitmask (peer detection)
+            uint32_t whist[SNW][1 << RB];
+            uint32_t match[SNW][1 << RB];   // per-warp digit -> lane bitmask (peer detection)
         };
         struct {
-            KT keys[NT * IPT];
-            uint32_t perm[NT * IPT];
+            KT keys[SNT * IPT];
+            uint32_t perm[SNT * IPT];
         } sorted;
     } u;
-    uint32_t tstart[1 << RB], gstart[1 << RB], w[NW];
+    uint32_t tstart[1 << RB], gstart[1 << RB], w[SNW];
     uint64_t mbar[2];
 };
 
@@ -388,9 +389,9 @@ struct ScatterWork {
 // which halves the stages and leaves room for 3 CTAs per SM.
 constexpr bool PERM_DIRECT = false;   // measured: 3 CTAs/SM with direct loads was slower (1.39 -> 1.50 ms, 60M keys; MIO-bound)
 
-template <typename KT, int IN, int IPT>
+template <typename KT, int IN, int IPT, int SNT = NT>
 constexpr int scatter_stage_bytes() {
-    return NT * IPT * (int)sizeof(typename InKey<IN, KT>::T) + (IN == IN_INTERNAL && !PERM_DIRECT ? NT * IPT * 4 : 0);
+    return SNT * IPT * (int)sizeof(typename InKey<IN, KT>::T) + (IN == IN_INTERNAL && !PERM_DIRECT ? SNT * IPT * 4 : 0);
 }
 
 // Input stages per CTA: tile k+2's copy is in flight while tile k is ranked and written.
@@ -407,6 +408,14 @@ constexpr int SCATTER_STAGES = TQP_SCATTER_STAGES;
 #define TQP_PEER_MATCH_ANY 0
 #endif
 constexpr bool PEER_MATCH_ANY = TQP_PEER_MATCH_ANY;
+// Peer detection by RB ballots (one per digit bit; peers = lanes agreeing on every bit)
+// and a plain read-modify-write of the warp's digit counter by the peers' leader: no
+// shared atomics, no match words to clear. Measured slower (60M u32 keys, 3 passes:
+// 1.108 -> 1.331 ms in the SMJ, 1.188 -> 1.415 ms int64 sort), kept off.
+#ifndef TQP_PEER_BALLOT
+#define TQP_PEER_BALLOT 0
+#endif
+constexpr bool PEER_BALLOT = TQP_PEER_BALLOT;
 
 // L2 hints in the scatter: bit 0 = the TMA input copies evict_first (read once), bit 1 =
 // the u32 key/perm output stores evict_last (run ends share sectors with the neighbouring
@@ -418,9 +427,9 @@ constexpr bool PEER_MATCH_ANY = TQP_PEER_MATCH_ANY;
 #define TQP_SCATTER_HINTS 0
 #endif
 
-template <typename KT, int IN, int IPT, int RB>
+template <typename KT, int IN, int IPT, int RB, int SNT = NT>
 constexpr size_t scatter_tma_smem() {
-    return SCATTER_STAGES * (size_t)scatter_stage_bytes<KT, IN, IPT>() + sizeof(ScatterWork<KT, IN, IPT, RB>);
+    return SCATTER_STAGES * (size_t)scatter_stage_bytes<KT, IN, IPT, SNT>() + sizeof(ScatterWork<KT, IN, IPT, RB, SNT>);
 }
 
 // Tile order of a persistent CTA: grid-stride (tile b + k*grid, default) or contiguous
@@ -443,20 +452,34 @@ constexpr size_t scatter_tma_smem() {
 #define TQP_SCATTER_CLUSTER 2
 #endif
 
-template <typename KT, int IN, int IPT, int RB>
+// Threads per scatter CTA for 9-bit digits on u32 keys: 512 = one CTA per SM ranking
+// 8192-key tiles (16 keys per digit run instead of 8: fewer half-written sectors).
+// Measured (60M keys, 3 passes; SMJ / int64 sort): 256 threads in cluster pairs 1.083 /
+// 1.156 ms, 512 threads 1.058 / 1.113 ms.
+#ifndef TQP_SCATTER_NT
+#define TQP_SCATTER_NT 512
+#endif
+constexpr int SCATTER_NT = TQP_SCATTER_NT;
+// cluster size of a scatter launch: the 512-thread CTA already holds the adjacent runs the
+// clusters pair up (measured 1.083 -> 1.058 ms with clusters off, 1.095 with pairs)
+__host__ __device__ constexpr int scatter_cluster(int snt) { return snt > NT ? 1 : TQP_SCATTER_CLUSTER; }
+template <typename KT, int IN, int IPT, int RB, int SNT>
 #ifndef TQP_SCATTER_MINB
 #define TQP_SCATTER_MINB 2
 #endif
-__global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT) == 4 ? 3 : TQP_SCATTER_MINB))) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
-    constexpr int TILE = NT * IPT, BINS = 1 << RB, BPT = BINS / NT;
+__global__ void __launch_bounds__(SNT, (SNT > NT ? 1 : IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT) == 4 ? 3 : TQP_SCATTER_MINB))) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
+    constexpr int TILE = SNT * IPT, BINS = 1 << RB, BPT = BINS / SNT, SNW = SNT / 32;
+    constexpr int HR = SNT / NT;   // histogram tiles (NT * IPT keys) per scatter tile
+    static_assert(BPT >= 1, "one digit per thread at least");
+    constexpr int CLS = scatter_cluster(SNT);
     constexpr uint32_t DM = BINS - 1u;
     using KIN = typename InKey<IN, KT>::T;
     constexpr bool HAS_PERM = IN == IN_INTERNAL;
-    constexpr int STAGE_BYTES = scatter_stage_bytes<KT, IN, IPT>();
+    constexpr int STAGE_BYTES = scatter_stage_bytes<KT, IN, IPT, SNT>();
     extern __shared__ __align__(128) uint8_t smem[];
     constexpr int SST = SCATTER_STAGES;
     auto stage_ptr = [&](int st) { return smem + (size_t)st * STAGE_BYTES; };
-    ScatterWork<KT, IN, IPT, RB>& s = *reinterpret_cast<ScatterWork<KT, IN, IPT, RB>*>(smem + SST * STAGE_BYTES);
+    ScatterWork<KT, IN, IPT, RB, SNT>& s = *reinterpret_cast<ScatterWork<KT, IN, IPT, RB, SNT>*>(smem + SST * STAGE_BYTES);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) {
         for (int st = 0; st < SST; st++) mbar_init(&s.mbar[st], 1);
@@ -495,7 +518,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
     // with clusters every CTA of a cluster runs as many iterations as its first CTA (the one
     // with the most tiles), idling through its own missing ones, so the barriers match
     int64_t kmax = INT64_MAX;
-    if (TQP_SCATTER_CLUSTER > 1) {
+    if (CLS > 1) {
         unsigned rank;
         asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
         const int64_t first = (int64_t)blockIdx.x - rank;
@@ -504,7 +527,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
     for (int64_t k = 0; k < kmax; k++) {
         const int64_t tile = tile_of(k);
         if (tile >= t_end) {
-            if (TQP_SCATTER_CLUSTER > 1) {
+            if (CLS > 1) {
                 asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
                 continue;
             }
@@ -516,15 +539,15 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
         uint32_t pm[IPT], rk[IPT];
         for (int d = lane * 4; d < BINS; d += 128) {   // 16-byte stores
             *reinterpret_cast<uint4*>(&s.u.whist[warp][d]) = make_uint4(0, 0, 0, 0);
-            *reinterpret_cast<uint4*>(&s.u.match[warp][d]) = make_uint4(0, 0, 0, 0);
+            if (!PEER_BALLOT) *reinterpret_cast<uint4*>(&s.u.match[warp][d]) = make_uint4(0, 0, 0, 0);
         }
         // rows of this tile left from this thread's first slot on (32-bit compares below)
         const int rem = (int)min((int64_t)TILE + 1, a.n - base - (int64_t)(warp * 32 * IPT + lane));
         uint32_t gs[BPT];   // this tile's global digit starts: loaded now, used after ranking
 #pragma unroll
         for (int j = 0; j < BPT; j++) {
-            const int d = tid + j * NT;
-            gs[j] = __ldg(a.ct + (tile / CHUNK) * BINS + d) + __ldg(a.th + tile * BINS + d);
+            const int d = tid + j * SNT;
+            gs[j] = __ldg(a.ct + (tile * HR / CHUNK) * BINS + d) + __ldg(a.th + tile * HR * BINS + d);
         }
         if (full(tile)) {
             if (HAS_PERM && PERM_DIRECT) {
@@ -577,7 +600,16 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                 // the digit's match word, reads the word back, and the leader clears it
                 unsigned peers;
                 uint32_t* mw = &s.u.match[warp][d];
-                if (PEER_MATCH_ANY) {
+                if (PEER_BALLOT) {
+                    peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+                    for (int b = 0; b < RB; b++) {
+                        const bool bit = (d >> b) & 1u;
+                        const unsigned bb = __ballot_sync(0xffffffffu, bit);
+                        peers &= bit ? bb : ~bb;
+                    }
+                    if (!valid) peers = 0;
+                } else if (PEER_MATCH_ANY) {
                     peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu);
                     if (!valid) peers = 0;
                 } else {
@@ -588,7 +620,13 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                 }
                 const uint32_t leader = 31 - __clz(peers);
                 uint32_t old = 0;
-                if (valid && lane == leader) {
+                if (PEER_BALLOT) {
+                    if (valid && lane == leader) {
+                        old = s.u.whist[warp][d];
+                        s.u.whist[warp][d] = old + (uint32_t)__popc(peers);
+                    }
+                    __syncwarp();
+                } else if (valid && lane == leader) {
                     old = atomicAdd(&s.u.whist[warp][d], (uint32_t)__popc(peers));
                     if (!PEER_MATCH_ANY) *mw = 0;
                 }
@@ -605,13 +643,13 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
         __syncthreads();
         {   // per digit: tile-local digit start + exclusive prefix over warps, folded into
             // whist[w][d] (thread owns BPT digits); gdelta[d] = global - tile digit start
-            uint32_t c[BPT][NW], cnt[BPT], local = 0;
+            uint32_t c[BPT][SNW], cnt[BPT], local = 0;
 #pragma unroll
             for (int j = 0; j < BPT; j++) {
                 const int d = dslot(tid * BPT + j);
                 uint32_t run = 0;
 #pragma unroll
-                for (int w = 0; w < NW; w++) {
+                for (int w = 0; w < SNW; w++) {
                     c[j][w] = s.u.whist[w][d];
                     run += c[j][w];
                 }
@@ -625,7 +663,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                 s.tstart[d] = ex;
                 uint32_t run = ex;
 #pragma unroll
-                for (int w = 0; w < NW; w++) {
+                for (int w = 0; w < SNW; w++) {
                     s.u.whist[w][dslot(d)] = run;
                     run += c[j][w];
                 }
@@ -655,14 +693,14 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             }
         }
 #pragma unroll
-        for (int j = 0; j < BPT; j++) s.gstart[tid + j * NT] = gs[j] - s.tstart[tid + j * NT];   // global - tile start
+        for (int j = 0; j < BPT; j++) s.gstart[tid + j * SNT] = gs[j] - s.tstart[tid + j * SNT];   // global - tile start
         __syncthreads();
         const int tile_n = (int)min((int64_t)TILE, a.n - base);
         if (!a.out_perm64 && !a.out_u && !a.out_orig) {   // intermediate passes / internal outputs
             KT* ok = (KT*)a.out_keys;
             uint32_t* op = a.out_perm;
             if (sizeof(KT) == 4 && ok && op) {
-                for (int j = tid; j < tile_n; j += NT) {
+                for (int j = tid; j < tile_n; j += SNT) {
                     const uint2 v = kp[kslot(j)];
                     const uint32_t dst = s.gstart[(v.x >> a.shift) & DM] + (uint32_t)j;
                     TQP_DCHECK((int64_t)dst < a.n);
@@ -675,7 +713,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                     }
                 }
             } else {
-                for (int j = tid; j < tile_n; j += NT) {
+                for (int j = tid; j < tile_n; j += SNT) {
                     const KT kk = sizeof(KT) == 4 ? (KT)kp[kslot(j)].x : s.u.sorted.keys[kslot(j)];
                     const uint32_t p = sizeof(KT) == 4 ? kp[kslot(j)].y : s.u.sorted.perm[kslot(j)];
                     const uint32_t dst = s.gstart[(uint32_t)(kk >> a.shift) & DM] + (uint32_t)j;
@@ -685,7 +723,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
                 }
             }
         } else
-        for (int j = tid; j < tile_n; j += NT) {
+        for (int j = tid; j < tile_n; j += SNT) {
             const KT kk = sizeof(KT) == 4 ? (KT)kp[kslot(j)].x : s.u.sorted.keys[kslot(j)];
             const uint32_t p = sizeof(KT) == 4 ? kp[kslot(j)].y : s.u.sorted.perm[kslot(j)];
             const uint32_t d = (uint32_t)(kk >> a.shift) & DM;
@@ -709,7 +747,7 @@ __global__ void __launch_bounds__(NT, (IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT)
             }
         }
         __syncthreads();   // sorted/whist/gstart reused by the next tile
-        if (TQP_SCATTER_CLUSTER > 1) {   // the cluster's CTAs (adjacent tiles) stay in step
+        if (CLS > 1) {   // the cluster's CTAs (adjacent tiles) stay in step
             asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
         }
     }
@@ -827,16 +865,19 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         const bool aligned = ((uintptr_t)in % 16 == 0) && (p == 0 || (uintptr_t)a.in_perm % 16 == 0);
         dispatch_in(mode, [&](auto m) {
             constexpr int INM = decltype(m)::value;
-            constexpr size_t smem = scatter_tma_smem<KT, INM, IPT, RB>();
-            auto* kfn = scatter_tma_kernel<KT, INM, IPT, RB>;
-            const int occ = occupancy(kfn, NT, smem);
-            int64_t grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
-            if (TQP_SCATTER_CLUSTER > 1) {   // a whole number of clusters (the kernel needs them)
-                grid -= grid % TQP_SCATTER_CLUSTER;
-                if (grid < TQP_SCATTER_CLUSTER) grid = TQP_SCATTER_CLUSTER;
+            constexpr int SNTc = (RB == 9 && sizeof(KT) == 4) ? SCATTER_NT : NT;
+            constexpr size_t smem = scatter_tma_smem<KT, INM, IPT, RB, SNTc>();
+            auto* kfn = scatter_tma_kernel<KT, INM, IPT, RB, SNTc>;
+            const int occ = occupancy(kfn, SNTc, smem);
+            const int64_t stiles = ceil_div(n, (int64_t)SNTc * IPT);
+            int64_t grid = std::min<int64_t>(stiles, (int64_t)ctx->num_sms * std::max(occ, 1));
+            constexpr int CL = scatter_cluster(SNTc);
+            if (CL > 1) {   // a whole number of clusters (the kernel needs them)
+                grid -= grid % CL;
+                if (grid < CL) grid = CL;
             }
-            launch_cluster(ctx, "tqp_sort_scatter", kfn, dim3((unsigned)grid), dim3(NT), smem,
-                           (unsigned)TQP_SCATTER_CLUSTER, a, tiles, aligned);
+            launch_cluster(ctx, "tqp_sort_scatter", kfn, dim3((unsigned)grid), dim3(SNTc), smem, (unsigned)CL, a,
+                           stiles, aligned);
         });
     }
     const int fb = (P - 1) % 2;
