@@ -394,6 +394,8 @@ constexpr int scatter_stage_bytes() {
     return SNT * IPT * (int)sizeof(typename InKey<IN, KT>::T) + (IN == IN_INTERNAL && !PERM_DIRECT ? SNT * IPT * 4 : 0);
 }
 
+// (Writing the digit-ordered tile into the tile's own input stage, which saves a barrier
+// and refills the stage after the write-out, measured no faster: 1.059 -> 1.064 ms.)
 // Input stages per CTA: tile k+2's copy is in flight while tile k is ranked and written.
 // (One stage with 3 CTAs/SM was measured slower: 1.34 -> 1.53 ms per 60M-key sort.)
 #ifndef TQP_SCATTER_STAGES
