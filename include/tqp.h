@@ -82,7 +82,10 @@ int tqp_abi_version(void);
  * (profiled launches), bytes_host[k] (algorithmic bytes, all launches).
  * names_host: '\n'-separated kernel names written into a caller buffer. */
 int64_t tqp_ctx_launch_count(const tqp_ctx* ctx);
-/* Checked mode (environment TQP_ALLOC_EXACT=1 at context creation; test builds):
+/* Poisoned temporaries (environment TQP_ALLOC_POISON=1 at context creation; tests): every
+ * libtqp temporary is filled with 0xA5 bytes when handed out, so reads of never-written
+ * temporary memory give garbage deterministically instead of a fresh allocation's zeros.
+ * Checked mode (environment TQP_ALLOC_EXACT=1 at context creation; test builds):
  * every temporary is its own cudaMalloc followed by 256 canary bytes, verified when
  * the temporary is released; returns the number of overwritten canaries seen. */
 int64_t tqp_ctx_guard_violations(const tqp_ctx* ctx);

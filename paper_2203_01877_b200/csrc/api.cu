@@ -62,6 +62,7 @@ void* tqp_ctx::dalloc(size_t bytes) {
             tqp::fail(TQP_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
         }
         TQP_CUDA(cudaMemsetAsync(static_cast<char*>(p) + bytes, 0xA5, GUARD, stream));
+        if (poison) TQP_CUDA(cudaMemsetAsync(p, 0xA5, bytes, stream));
         live_blocks[p] = bytes;
         return p;
     }
@@ -73,6 +74,7 @@ void* tqp_ctx::dalloc(size_t bytes) {
         free_blocks.erase(it);
         cached_bytes -= have;
         live_blocks[p] = have;
+        if (poison) TQP_CUDA(cudaMemsetAsync(p, 0xA5, bytes, stream));
         return p;
     }
     void* p = nullptr;
@@ -87,6 +89,7 @@ void* tqp_ctx::dalloc(size_t bytes) {
         tqp::fail(TQP_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
     }
     live_blocks[p] = sz;
+    if (poison) TQP_CUDA(cudaMemsetAsync(p, 0xA5, bytes, stream));
     return p;
 }
 
@@ -174,6 +177,8 @@ tqp_status tqp_ctx_create(int device, void* stream, tqp_ctx** out) {
         c->stream = static_cast<cudaStream_t>(stream);
         const char* ex = getenv("TQP_ALLOC_EXACT");
         c->exact_alloc = ex && ex[0] == '1';
+        const char* po = getenv("TQP_ALLOC_POISON");
+        c->poison = po && po[0] == '1';
         TQP_CUDA(cudaMallocHost(&c->pinned, 4096));
     } catch (const tqp::Error& e) {
         delete c;

@@ -76,6 +76,9 @@ struct tqp_ctx {
     // freed (after a stream sync) when released, so memcheck sees out-of-bounds accesses
     // that a cached, rounded-up block would hide
     bool exact_alloc = false;
+    // TQP_ALLOC_POISON=1 (tests): every temporary handed out is filled with 0xA5 bytes first,
+    // so a kernel that reads a temporary it never wrote sees garbage, not a lucky zero
+    bool poison = false;
     static constexpr size_t GUARD = 256;   // exact mode: canary bytes after every temporary
     int64_t guard_violations = 0;          // canaries found overwritten at release
     void* dalloc(size_t bytes);

@@ -792,8 +792,9 @@ template <bool JOIN>
 __global__ void __launch_bounds__(PNT) emit_kernel(const uint32_t* __restrict__ lft, const uint8_t* __restrict__ mask,
                                                    int anti, int64_t np, const uint64_t* __restrict__ toff,
                                                    int64_t* left_out, int64_t* right_out, Payload pay,
-                                                   const int* direct) {
+                                                   const int* direct, const int* unsorted) {
     if (direct && *direct == 0) return;
+    if (unsorted && *unsorted) return;   // speculative build side not in key order: redone by the caller
     const int64_t tiles = (np + PTILE - 1) / PTILE;
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         emit_tile<JOIN>(t, lft, mask, anti, np, toff, left_out, right_out, pay);
@@ -1127,7 +1128,7 @@ bool run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
                 }
                 launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)egrid), dim3(PNT), 0,
                        (const uint32_t*)lft.get(), (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out,
-                       right_out, pay ? *pay : Payload{}, (const int*)nullptr);
+                       right_out, pay ? *pay : Payload{}, (const int*)nullptr, (const int*)B.unsorted.get());
                 ctx->add_bytes("tqp_pkfk_emit", 2.0 * ib * (double)h[0]);
             }
             if (n_out_host) *n_out_host = h[0];
@@ -1138,11 +1139,11 @@ bool run_probe(tqp_ctx* ctx, Built& B, const tqp_col& pk, int64_t np, int mode, 
         if (mode == 0)
             launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)egrid), dim3(PNT), 0, (const uint32_t*)lft.get(),
                    (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out,
-                   pay ? *pay : Payload{}, (const int*)nullptr);
+                   pay ? *pay : Payload{}, (const int*)nullptr, (const int*)B.unsorted.get());
         else if (mode == 1 && right_out)
             launch(ctx, "tqp_pkfk_emit", emit_kernel<false>, dim3((unsigned)egrid), dim3(PNT), 0, (const uint32_t*)nullptr,
                    (const uint8_t*)a.mask, anti, np, (const uint64_t*)toff.get(), (int64_t*)nullptr, right_out,
-                   Payload{}, (const int*)nullptr);
+                   Payload{}, (const int*)nullptr, (const int*)B.unsorted.get());
         TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
     } else if (np > 0 && mode == 2) {
         // empty build side: no probe row matches
@@ -1307,7 +1308,7 @@ void pkfk_join_hash(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t np
         const int egrid = (int)std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occupancy(emit_kernel<true>, PNT, 0), 1));
         launch(ctx, "tqp_pkfk_emit", emit_kernel<true>, dim3((unsigned)egrid), dim3(PNT), 0, (const uint32_t*)lft.get(),
                (const uint8_t*)nullptr, 0, np, (const uint64_t*)toff.get(), left_out, right_out, Payload{},
-               (const int*)nullptr);
+               (const int*)nullptr, (const int*)nullptr);
         TQP_CUDA(cudaMemcpyAsync(pack.get(), toff.get() + tiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
         ctx->add_bytes("tqp_hash_probe", (double)np * dtype_size(pk.dtype));
     }

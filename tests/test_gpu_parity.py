@@ -1274,3 +1274,59 @@ def test_pkfk_speculative_rank_route(T, case):
     want = np.full(probe.size, -1, np.int64)
     want[oro] = olo
     assert np.array_equal(npy(left), want)
+
+
+@pytest.mark.parametrize("case", ["one_swap", "shuffled_middle", "out_of_range", "sorted"])
+def test_poisoned_temporaries(T, case, monkeypatch):
+    """Every libtqp temporary filled with garbage when handed out (TQP_ALLOC_POISON=1): a
+    kernel reading temporary memory nobody wrote -- e.g. tile counts of probe tiles that
+    exited early because the speculative build side was not sorted -- gives wrong results
+    or faults here deterministically, not only when the caching allocator happens to hand
+    back a used block. The operators' retry and fallback paths against the oracle."""
+    monkeypatch.setenv("TQP_ALLOC_POISON", "1")
+    ctx = T.Context()
+    rng = np.random.default_rng(7 + len(case))
+    nb = 200_003
+    build = np.sort(rng.choice(4 * nb, nb, replace=False)).astype(np.int64) + 17
+    if case == "one_swap":
+        build[nb // 2], build[nb // 2 + 1] = build[nb // 2 + 1], build[nb // 2]
+    elif case == "shuffled_middle":
+        mid = build[1:-1].copy()
+        rng.shuffle(mid)
+        build[1:-1] = mid
+    elif case == "out_of_range":
+        build[nb // 3] = build[-1] + 5
+    probe = rng.choice(build, 700_001).astype(np.int64)
+    probe[::5] = rng.integers(0, 5 * nb, probe[::5].size)
+    olo, oro = oracle.pkfk_join(build, probe)
+    lo, ro = ctx.pkfk_join(cu(build), cu(probe))
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    lo, ro = ctx.pkfk_join(cu(build), cu(probe), index_dtype=torch.int32)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    sel = ctx.pkfk_semi(cu(build), cu(probe))
+    assert np.array_equal(npy(sel), np.unique(oro))
+    anti = ctx.pkfk_semi(cu(build), cu(probe), anti=True)
+    assert np.array_equal(npy(anti), np.setdiff1d(np.arange(probe.size), oro))
+    left = ctx.pkfk_outer(cu(build), cu(probe))
+    want = np.full(probe.size, -1, np.int64)
+    want[oro] = olo
+    assert np.array_equal(npy(left), want)
+    bo, po, idx = ctx.pkfk_join_payload(cu(build), cu(probe), build_payload=(cu(build * 3),),
+                                        probe_payload=(cu(probe + 1),))
+    assert np.array_equal(npy(idx[0]), olo) and np.array_equal(npy(idx[1]), oro)
+    assert np.array_equal(npy(bo[0]), build[olo] * 3) and np.array_equal(npy(po[0]), probe[oro] + 1)
+    # the other operators' temporaries under the same poisoning
+    slo, sro = ctx.smj_join(cu(build), cu(probe))
+    xlo, xro = oracle.smj_join(build, probe)
+    assert np.array_equal(npy(slo), xlo) and np.array_equal(npy(sro), xro)
+    k = (probe % 5).astype(np.uint8)
+    aggs = [("sum", [(1, 0, 1)]), ("count", []), ("min", [(1, 0, 1)]), ("max", [(1, 3, -1)])]
+    got = ctx.groupby_agg([cu(k, torch.uint8), cu(probe)], [0], aggs, [(1, "gt", 1000)])
+    check_groupby(T, got, oracle.groupby_agg([k, probe], [0], aggs, [(1, "gt", 1000)]), aggs)
+    got = ctx.groupby_agg([cu(probe), cu(k, torch.uint8)], [0], [("count", []), ("sum", [(1, 0, 1)])])
+    check_groupby(T, got, oracle.groupby_agg([probe, k], [0], [("count", []), ("sum", [(1, 0, 1)])]),
+                  [("count", []), ("sum", [(1, 0, 1)])])
+    mask, sel = ctx.filter_compact([cu(probe)], [(0, "lt", 3 * nb)])
+    assert np.array_equal(npy(sel), np.flatnonzero(probe < 3 * nb))
+    s = ctx.sort(cu(probe))
+    assert np.array_equal(npy(s[0]), np.sort(probe, kind="stable"))
