@@ -1330,3 +1330,81 @@ def test_poisoned_temporaries(T, case, monkeypatch):
     assert np.array_equal(npy(sel), np.flatnonzero(probe < 3 * nb))
     s = ctx.sort(cu(probe))
     assert np.array_equal(npy(s[0]), np.sort(probe, kind="stable"))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_groupby_dense_compiled_plan_fuzz(T, seed, monkeypatch):
+    """Random aggregation plans through the plan-compiled dense kernel (jit.cu), each one a
+    different generated source: 1-3 key columns of mixed dtypes (u8 / i32 / i64, negative
+    values), 1-4 distinct keys (register compares) or 5-16 (id table), 0-4 predicates of
+    every comparison kind (folded into interval and != terms, possibly unsatisfiable),
+    1-8 (op, expression) pairs with 0-3 factors of mixed dtypes, signs and constants, pairs
+    that extend the previous pair's factor list, row counts around the tile edges. Each
+    result against the oracle."""
+    monkeypatch.setenv("TQP_JIT_MIN_ROWS", "0")
+    rng = np.random.default_rng(9000 + seed)
+    n = int(rng.choice([1, 511, 512, 513, 2048, 9_999, 65_537, 300_001]))
+    n_keys = int(rng.integers(1, 4))
+    d_target = int(rng.choice([1, 2, 3, 4, 5, 9, 16]))
+    dts = [torch.uint8, torch.int32, torch.int64]
+    cols, gcols, kidx = [], [], []
+    # key columns: a small domain each, their product near d_target distinct tuples
+    per = max(1, round(d_target ** (1.0 / n_keys)))
+    width = 0   # the key columns' dtypes fit one 64-bit packed key (the API's limit)
+    size = {torch.uint8: 1, torch.int32: 4, torch.int64: 8}
+    for k in range(n_keys):
+        dt = dts[int(rng.integers(0, 3))]
+        if width + size[dt] > 8:
+            dt = torch.int32 if width + 4 <= 8 else torch.uint8
+        if width + size[dt] > 8:
+            break
+        width += size[dt]
+        lo = 0 if dt == torch.uint8 else int(rng.integers(-50, 50))
+        step = int(rng.integers(1, 4))
+        v = lo + step * rng.integers(0, per, n)
+        cols.append(v.astype(np.int64))
+        gcols.append(cu(v, dt))
+        kidx.append(len(cols) - 1)
+    # value columns
+    for _ in range(int(rng.integers(1, 4))):
+        dt = dts[int(rng.integers(0, 3))]
+        hi = {torch.uint8: 255, torch.int32: 1 << 16, torch.int64: 1 << 18}[dt]   # 3 factors stay < 2^63
+        lo = 0 if dt == torch.uint8 else -hi
+        v = rng.integers(lo, hi + 1, n)
+        cols.append(v.astype(np.int64))
+        gcols.append(cu(v, dt))
+    vidx = list(range(len(kidx), len(cols)))
+    ops = ["lt", "le", "gt", "ge", "eq", "ne"]
+    preds = []
+    for _ in range(int(rng.integers(0, 5))):
+        c = int(rng.integers(0, len(cols)))
+        x = int(rng.choice(cols[c])) if n else 0
+        preds.append((c, ops[int(rng.integers(0, 6))], x + int(rng.integers(-2, 3))))
+    aggs = []
+    prev = None
+    for _ in range(int(rng.integers(1, 9))):
+        op = ["sum", "count", "min", "max", "avg"][int(rng.integers(0, 5))]
+        if op == "count":
+            aggs.append(("count", []))
+            prev = None
+            continue
+        if prev is not None and len(prev) < 3 and rng.random() < 0.4:   # extends the previous pair's factors
+            fs = prev + [(int(rng.choice(vidx)), int(rng.integers(-5, 6)), int(rng.choice([1, -1])))]
+        else:
+            fs = [(int(rng.choice(vidx)), int(rng.integers(-100, 101)), int(rng.choice([1, -1])))
+                  for _ in range(int(rng.integers(0, 3)))]
+        aggs.append((op, fs))
+        prev = fs if op in ("sum", "avg") else None
+    want = oracle.groupby_agg(cols, kidx, aggs, preds)
+    jit0 = T.jit_counters()
+    ctx = T.context()
+    ctx.reset_counters()
+    ctx.set_profiling(True)
+    got = ctx.groupby_agg(gcols, kidx, aggs, preds)
+    st = ctx.kernel_stats()
+    ctx.set_profiling(False)
+    check_groupby(T, got, want, aggs)
+    jit1 = T.jit_counters()
+    assert jit1["failed"] == jit0["failed"]
+    # every dense launch of a plan is the compiled kernel
+    assert ("tqp_groupby_dense" in st) == (jit1["launches"] > jit0["launches"])
