@@ -70,6 +70,27 @@ typedef struct tqp_ctx tqp_ctx;
 tqp_status tqp_ctx_create(int device, void* stream, tqp_ctx** out);
 void tqp_ctx_destroy(tqp_ctx* ctx);
 tqp_status tqp_ctx_set_stream(tqp_ctx* ctx, void* stream);
+
+/* Device memory for the context's temporaries (SURVEY.md §8(b) tqp_alloc_fn /
+ * tqp_free_fn): by default cudaMalloc / cudaFree; with tqp_ctx_set_allocator, the
+ * caller's allocator (e.g. the framework's caching allocator, so both draw on one pool
+ * of HBM). `stream` is the context stream (a cudaStream_t), `device` its device.
+ * alloc returns NULL when out of memory; it must not call back into libtqp.
+ * libtqp keeps the blocks it releases in a per-context cache in front of the allocator
+ * (reused stream-ordered on the context stream), so the callbacks run on a cache miss,
+ * at tqp_ctx_trim and at tqp_ctx_destroy only; on an allocation failure the cache is
+ * returned to the allocator and the allocation retried once.
+ * tqp_ctx_set_allocator: both callbacks or neither (NULL, NULL = cudaMalloc / cudaFree);
+ * call it before the context's first operator -- with live temporaries it returns
+ * TQP_ERR_INVALID_ARGUMENT; cached blocks of the previous allocator are returned to it
+ * first. `user` is passed through to the callbacks (not owned). */
+typedef void* (*tqp_alloc_fn)(void* user, size_t bytes, int device, void* stream);
+typedef void (*tqp_free_fn)(void* user, void* ptr, int device, void* stream);
+tqp_status tqp_ctx_set_allocator(tqp_ctx* ctx, tqp_alloc_fn alloc, tqp_free_fn free_fn, void* user);
+/* Return every cached temporary block to the allocator (synchronises the context stream). */
+tqp_status tqp_ctx_trim(tqp_ctx* ctx);
+/* Bytes held in the context's cache of released temporaries. */
+size_t tqp_ctx_cached_bytes(const tqp_ctx* ctx);
 const char* tqp_last_error(const tqp_ctx* ctx);
 int tqp_abi_version(void);
 

@@ -12,6 +12,7 @@ Operators (same names as the C ABI, PAPER.md citations in include/tqp.h):
 """
 
 import ctypes
+import sys
 import os
 
 import torch
@@ -43,6 +44,7 @@ EXPORTED = [
     "tqp_groupby_agg", "tqp_groupby_merge", "tqp_smj_expand_payload", "tqp_partition", "tqp_minmax",
     "tqp_range_splitters", "tqp_gather", "tqp_pkfk_outer_build", "tqp_partition_plan_create", "tqp_partition_scatter",
     "tqp_partition_release", "tqp_ipc_alloc", "tqp_ipc_free", "tqp_ipc_open", "tqp_ipc_close", "tqp_jit_counters",
+    "tqp_ctx_set_allocator", "tqp_ctx_trim", "tqp_ctx_cached_bytes",
 ]
 
 
@@ -70,6 +72,9 @@ _sig = {
     "tqp_ctx_launch_count": ([_vp], _i64),
     "tqp_ctx_guard_violations": ([_vp], _i64),
     "tqp_jit_counters": ([_vp, _vp, _vp], ctypes.c_int),
+    "tqp_ctx_set_allocator": ([_vp, _vp, _vp, _vp], _int),
+    "tqp_ctx_trim": ([_vp], _int),
+    "tqp_ctx_cached_bytes": ([_vp], ctypes.c_size_t),
     "tqp_ctx_reset_counters": ([_vp], None),
     "tqp_ctx_set_profiling": ([_vp, _int], _int),
     "tqp_ctx_set_profiling_filter": ([_vp, ctypes.c_char_p], _int),
@@ -169,10 +174,34 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr() if t is not None and t.numel() else None)
 
 
-class Context:
-    """A libtqp context bound to one CUDA device; work goes on torch's current stream."""
+# libtqp's temporaries from torch's caching allocator (include/tqp.h tqp_ctx_set_allocator):
+# one pool of HBM for both; called only when libtqp's own cache misses, and at trim/destroy
+_ALLOC_T = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p)
+_FREE_T = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p)
 
-    def __init__(self, device=None):
+
+@_ALLOC_T
+def _torch_alloc(user, nbytes, device, stream):
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0))
+    except Exception:   # out of memory: libtqp returns its cache and retries once, then reports it
+        return None
+
+
+@_FREE_T
+def _torch_free(user, ptr, device, stream):
+    try:
+        torch.cuda.caching_allocator_delete(ptr)
+    except Exception:
+        pass
+
+
+class Context:
+    """A libtqp context bound to one CUDA device; work goes on torch's current stream.
+    allocator="torch" (default): libtqp's temporaries come from torch's caching allocator
+    (one HBM pool; ctx.trim() hands libtqp's cached blocks back to it); "cuda": cudaMalloc."""
+
+    def __init__(self, device=None, allocator="torch"):
         if not torch.cuda.is_available():
             raise RuntimeError("libtqp needs a CUDA device (B200); no CPU fallback exists")
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
@@ -183,10 +212,16 @@ class Context:
             self._check(_lib.tqp_ctx_create(self.device.index, ctypes.c_void_p(s), ctypes.byref(h)), None)
         self._h = h
         self._stream = s
+        if allocator == "torch":
+            self._check(_lib.tqp_ctx_set_allocator(self._h, ctypes.cast(_torch_alloc, ctypes.c_void_p),
+                                                   ctypes.cast(_torch_free, ctypes.c_void_p), None))
+        elif allocator != "cuda":
+            raise ValueError("allocator must be 'torch' or 'cuda'")
+        self.allocator = allocator
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and _lib is not None:
+        if h and _lib is not None and not sys.is_finalizing():   # at exit the process frees it all
             try:
                 _lib.tqp_ctx_destroy(h)
             except Exception:
@@ -208,6 +243,13 @@ class Context:
 
     def launch_count(self):
         return _lib.tqp_ctx_launch_count(self._h)
+
+    def trim(self):
+        """Return libtqp's cached temporary blocks to the allocator (synchronises)."""
+        self._check(_lib.tqp_ctx_trim(self._h))
+
+    def cached_bytes(self):
+        return _lib.tqp_ctx_cached_bytes(self._h)
 
     def guard_violations(self):
         """Overwritten canaries after temporaries (checked mode, TQP_ALLOC_EXACT=1)."""

@@ -52,15 +52,27 @@ static size_t round_block(size_t b) {
     return (b + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
 }
 
+void* tqp_ctx::raw_alloc(size_t bytes) {
+    if (alloc_fn) return alloc_fn(alloc_user, bytes, device, stream);
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void tqp_ctx::raw_free(void* p) {
+    if (!p) return;
+    if (free_fn) free_fn(alloc_user, p, device, stream);
+    else cudaFree(p);
+}
+
 void* tqp_ctx::dalloc(size_t bytes) {
     if (bytes == 0) return nullptr;
     if (exact_alloc) {   // exact size + GUARD canary bytes (0xA5), checked at release
-        void* p = nullptr;
-        cudaError_t e = cudaMalloc(&p, bytes + GUARD);
-        if (e != cudaSuccess) {
-            cudaGetLastError();
-            tqp::fail(TQP_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-        }
+        void* p = raw_alloc(bytes + GUARD);
+        if (!p) tqp::fail(TQP_ERR_OUT_OF_MEMORY, "device allocation of a temporary failed");
         TQP_CUDA(cudaMemsetAsync(static_cast<char*>(p) + bytes, 0xA5, GUARD, stream));
         if (poison) TQP_CUDA(cudaMemsetAsync(p, 0xA5, bytes, stream));
         live_blocks[p] = bytes;
@@ -77,17 +89,12 @@ void* tqp_ctx::dalloc(size_t bytes) {
         if (poison) TQP_CUDA(cudaMemsetAsync(p, 0xA5, bytes, stream));
         return p;
     }
-    void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, sz);
-    if (e == cudaErrorMemoryAllocation) {
-        cudaGetLastError();
+    void* p = raw_alloc(sz);
+    if (!p) {   // out of memory: give the cached blocks back and retry once
         trim();
-        e = cudaMalloc(&p, sz);
+        p = raw_alloc(sz);
     }
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        tqp::fail(TQP_ERR_OUT_OF_MEMORY, std::string("cudaMalloc: ") + cudaGetErrorString(e));
-    }
+    if (!p) tqp::fail(TQP_ERR_OUT_OF_MEMORY, "device allocation of a temporary failed (" + std::to_string(sz) + " bytes)");
     live_blocks[p] = sz;
     if (poison) TQP_CUDA(cudaMemsetAsync(p, 0xA5, bytes, stream));
     return p;
@@ -108,7 +115,7 @@ void tqp_ctx::dfree(void* p) {
                     break;
                 }
         }
-        cudaFree(p);
+        raw_free(p);
         live_blocks.erase(it);
         return;
     }
@@ -119,7 +126,7 @@ void tqp_ctx::dfree(void* p) {
 
 void tqp_ctx::trim() {
     cudaStreamSynchronize(stream);
-    for (auto& kv : free_blocks) cudaFree(kv.second);
+    for (auto& kv : free_blocks) raw_free(kv.second);
     free_blocks.clear();
     cached_bytes = 0;
 }
@@ -196,9 +203,26 @@ void tqp_ctx_destroy(tqp_ctx* c) {
     for (auto e : c->free_events) cudaEventDestroy(e);
     if (c->pinned) cudaFreeHost(c->pinned);
     c->trim();
-    for (auto& kv : c->live_blocks) cudaFree(kv.first);
+    for (auto& kv : c->live_blocks) c->raw_free(kv.first);
     delete c;
 }
+
+tqp_status tqp_ctx_set_allocator(tqp_ctx* c, tqp_alloc_fn alloc, tqp_free_fn free_, void* user) {
+    TQP_GUARD(c, {
+        if ((alloc == nullptr) != (free_ == nullptr)) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "allocator: both callbacks or neither");
+        if (!c->live_blocks.empty()) tqp::fail(TQP_ERR_INVALID_ARGUMENT, "allocator: the context holds live temporaries");
+        c->trim();   // cached blocks go back to the allocator they came from
+        c->alloc_fn = alloc;
+        c->free_fn = free_;
+        c->alloc_user = user;
+    });
+}
+
+tqp_status tqp_ctx_trim(tqp_ctx* c) {
+    TQP_GUARD(c, { c->trim(); });
+}
+
+size_t tqp_ctx_cached_bytes(const tqp_ctx* c) { return c ? c->cached_bytes : 0; }
 
 tqp_status tqp_ctx_set_stream(tqp_ctx* c, void* stream) {
     // cached blocks were last used on the old stream: order the switch

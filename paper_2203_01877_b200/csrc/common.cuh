@@ -84,6 +84,13 @@ struct tqp_ctx {
     void* dalloc(size_t bytes);
     void dfree(void* p);
     void trim();
+    // device memory under the cache: the caller's allocator (tqp_ctx_set_allocator) or
+    // cudaMalloc / cudaFree
+    void* (*alloc_fn)(void*, size_t, int, void*) = nullptr;
+    void (*free_fn)(void*, void*, int, void*) = nullptr;
+    void* alloc_user = nullptr;
+    void* raw_alloc(size_t bytes);   // nullptr when out of memory
+    void raw_free(void* p);
     std::string err;
     int64_t launches = 0;
     bool profiling = false;

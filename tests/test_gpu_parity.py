@@ -1408,3 +1408,48 @@ def test_groupby_dense_compiled_plan_fuzz(T, seed, monkeypatch):
     assert jit1["failed"] == jit0["failed"]
     # every dense launch of a plan is the compiled kernel
     assert ("tqp_groupby_dense" in st) == (jit1["launches"] > jit0["launches"])
+
+
+def test_context_allocator_hooks(T):
+    """tqp_ctx_set_allocator (SURVEY §8(b) tqp_alloc_fn / tqp_free_fn): the default Python
+    context draws libtqp's temporaries from torch's caching allocator (one HBM pool) and
+    trim hands them back; cudaMalloc contexts work the same; an allocator that fails makes
+    the operator fail with TQP_ERR_OUT_OF_MEMORY, nothing else; the callbacks come in pairs."""
+    import ctypes
+    rng = np.random.default_rng(5)
+    build = np.sort(rng.choice(10**7, 300_000, replace=False)).astype(np.int64)
+    rng.shuffle(build)   # the sort route: plenty of temporaries
+    probe = rng.choice(build, 2_000_000)
+    olo, oro = oracle.pkfk_join(build, probe)
+    b, p = cu(build), cu(probe)
+    torch.cuda.synchronize()
+    ctx = T.Context(allocator="torch")
+    before = torch.cuda.memory_allocated()
+    lo, ro = ctx.pkfk_join(b, p)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    held = ctx.cached_bytes()
+    assert held > 0
+    # libtqp's cached blocks are torch allocations (outputs lo / ro come on top)
+    assert torch.cuda.memory_allocated() - before >= held
+    ctx.trim()
+    assert ctx.cached_bytes() == 0
+    del lo, ro
+    torch.cuda.synchronize()
+    assert torch.cuda.memory_allocated() <= before + 4096
+    c2 = T.Context(allocator="cuda")
+    lo, ro = c2.pkfk_join(b, p)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+    # an allocator that is always out of memory
+    fails = T._ALLOC_T(lambda user, n, dev, s: None)
+    frees = T._FREE_T(lambda user, ptr, dev, s: None)
+    c3 = T.Context(allocator="cuda")
+    assert T._lib.tqp_ctx_set_allocator(c3._h, ctypes.cast(fails, ctypes.c_void_p), None, None) == T.TQP_ERR_INVALID_ARGUMENT
+    assert T._lib.tqp_ctx_set_allocator(c3._h, ctypes.cast(fails, ctypes.c_void_p),
+                                        ctypes.cast(frees, ctypes.c_void_p), None) == T.TQP_OK
+    with pytest.raises(T.TqpError) as e:
+        c3.pkfk_join(b, p)
+    assert e.value.status == T.TQP_ERR_OUT_OF_MEMORY
+    # back to cudaMalloc: the context is still usable
+    assert T._lib.tqp_ctx_set_allocator(c3._h, None, None, None) == T.TQP_OK
+    lo, ro = c3.pkfk_join(b, p)
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
