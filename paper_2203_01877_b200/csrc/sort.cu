@@ -418,6 +418,9 @@ constexpr bool PEER_MATCH_ANY = TQP_PEER_MATCH_ANY;
 #define TQP_PEER_BALLOT 0
 #endif
 constexpr bool PEER_BALLOT = TQP_PEER_BALLOT;
+// (A single 64-bit word per (warp, digit) -- peer mask low, warp digit count high, one
+// 64-bit shared atomicOr per key, the leader's plain store replacing the atomic add and
+// the clear, no leader shuffle -- measured much slower: 1.059 -> 1.502 ms.)
 
 // L2 hints in the scatter: bit 0 = the TMA input copies evict_first (read once), bit 1 =
 // the u32 key/perm output stores evict_last (run ends share sectors with the neighbouring
