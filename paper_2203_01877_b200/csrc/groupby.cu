@@ -2408,7 +2408,7 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
                 if (best_w > 0 && n >= jit_min && jit_enabled()) {
                     const int64_t tr = (int64_t)dense_nt * dense_dr;
                     DenseJitSpec& js = jit_spec;
-                    js = DenseJitSpec{};
+                    memset(&js, 0, sizeof(js));   // padding too: the compiled-kernel cache keys on the bytes
                     js.nt = dense_nt;
                     js.ns = dense_ns;
                     js.stage_bytes = (int)((int64_t)a.stage_bytes * tr / GTILE);

@@ -285,6 +285,7 @@ struct JitKernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t k = nullptr;
     size_t smem_set = 0;
+    std::map<size_t, int> occ;   // resident CTAs per SM by dynamic shared memory bytes
 };
 std::mutex& jit_mutex() {
     static std::mutex m;
@@ -296,13 +297,15 @@ std::map<std::string, JitKernel>& jit_cache() {
     return c;
 }
 
-// the compiled kernel for the plan (cached per source text); null when unavailable
+// the compiled kernel for the plan (cached by the plan's bytes -- the caller zero-fills the
+// spec, padding included -- so a hit costs no source generation); null when unavailable
 JitKernel* dense_jit_kernel(const DenseJitSpec& s) {
-    std::string src = dense_jit_source(s);
+    std::string key(reinterpret_cast<const char*>(&s), sizeof(s));
     std::lock_guard<std::mutex> g(jit_mutex());
     auto& cache = jit_cache();
-    auto it = cache.find(src);
+    auto it = cache.find(key);
     if (it != cache.end()) return it->second.k ? &it->second : nullptr;
+    const std::string src = dense_jit_source(s);
     JitKernel jk;
     Nvrtc& nv = nvrtc();
     nvrtcProg prog = nullptr;
@@ -330,7 +333,7 @@ JitKernel* dense_jit_kernel(const DenseJitSpec& s) {
         nv.destroy(&prog);
     }
     (jk.k ? g_counters.compiled : g_counters.failed)++;
-    auto& slot = cache[std::move(src)];
+    auto& slot = cache[std::move(key)];
     slot = jk;
     return slot.k ? &slot : nullptr;
 }
@@ -363,12 +366,15 @@ int dense_jit_occupancy(const DenseJitSpec& s, size_t smem) {
     JitKernel* jk = dense_jit_kernel(s);
     if (!jk) return 0;
     std::lock_guard<std::mutex> g(jit_mutex());
+    auto it = jk->occ.find(smem);
+    if (it != jk->occ.end()) return it->second;
     if (!set_jit_smem(jk, smem)) return 0;
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)jk->k, s.nt, smem) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
+    jk->occ[smem] = occ;
     return occ;
 }
 

@@ -30,6 +30,8 @@ namespace tqp {
 struct DenseJitArgs TQP_DENSE_JIT_ARGS_BODY;
 
 // Everything the generated source fixes as literals (groupby.cu's Phase1Args, dense part).
+// Compiled kernels are cached by the struct's bytes: zero-fill it (memset) before filling
+// it in, so the padding is deterministic.
 struct DenseJitSpec {
     int nt = 128;            // threads per CTA (4 rows each per tile)
     int ns = 1;              // TMA stages
