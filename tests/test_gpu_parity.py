@@ -1453,3 +1453,20 @@ def test_context_allocator_hooks(T):
     assert T._lib.tqp_ctx_set_allocator(c3._h, None, None, None) == T.TQP_OK
     lo, ro = c3.pkfk_join(b, p)
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
+
+
+@pytest.mark.parametrize("offset", [1, 3])
+def test_groupby_dense_unaligned_columns(T, offset, dense_kernel):
+    """Columns starting off a 16-byte boundary (views into larger tensors) cannot be staged
+    with bulk copies: both dense kernels take the plain cooperative loads for every tile."""
+    rng = np.random.default_rng(40 + offset)
+    n = 123_457
+    k = (rng.integers(0, 3, n + offset) + 65).astype(np.uint8)
+    d = rng.integers(-5000, 5000, n + offset).astype(np.int32)
+    v = rng.integers(-10**9, 10**9, n + offset)
+    cols = [k[offset:], d[offset:], v[offset:]]
+    gcols = [cu(k, torch.uint8)[offset:], cu(d, torch.int32)[offset:], cu(v)[offset:]]
+    aggs = [("sum", [(2, 0, 1), (1, 7, -1)]), ("count", []), ("min", [(1, 0, 1)]), ("max", [(2, 0, -1)])]
+    preds = [(1, "ge", -4000)]
+    got = T.groupby_agg(gcols, [0], aggs, preds)
+    check_groupby(T, got, oracle.groupby_agg(cols, [0], aggs, preds), aggs)
