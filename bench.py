@@ -110,9 +110,12 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ data
 
+SEED = 42
+
+
 def make_data(rank, world, device, layout, placement="local"):
     n_o = orders_count(SF_PER_RANK)
-    orders, li = tpch_orders_lineitem(SF_PER_RANK * world, seed=42, device=device, layout=layout,
+    orders, li = tpch_orders_lineitem(SF_PER_RANK * world, seed=SEED, device=device, layout=layout,
                                       order_range=(rank * n_o, (rank + 1) * n_o))
     if placement == "exchange" and world > 1:   # lineitem's orders spread over every rank
         from datagen.tpch import spread_orderkeys
@@ -517,9 +520,10 @@ def run_gpu(args):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "int64",
-            "data": "synthetic (in-repo TPC-H-shaped generator, seed 42; dbgen unavailable offline)",
+            "data": f"synthetic (in-repo TPC-H-shaped generator, seed {SEED}; dbgen unavailable offline)",
             "config": {
-                "workload": "tpch_sf10_hot_path: pkfk_join + smj_join(orders x lineitem) + Q1 groupby + Q6 filter/sum",
+                "workload": f"tpch_sf{SF_PER_RANK:g}_hot_path: pkfk_join + smj_join(orders x lineitem) + Q1 groupby + "
+                            "Q6 filter/sum",
                 "sf_per_rank": SF_PER_RANK,
                 "lineitem_rows_per_rank": hp.n,
                 "orders_rows_per_rank": hp.ok.numel(),
@@ -737,7 +741,13 @@ def main():
     ap.add_argument("--pkfk-strategy", default="auto", choices=["auto", "broadcast", "copartition"])
     ap.add_argument("--cpu-sample-sf", type=float, default=0.25)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # the workload: TPC-H scale factor per rank (BASELINE.json's metric is quoted at 10) and
+    # the generator seed
+    ap.add_argument("--sf", type=float, default=10.0)
+    ap.add_argument("--seed", type=int, default=42)
     args = ap.parse_args()
+    global SF_PER_RANK, SEED
+    SF_PER_RANK, SEED = args.sf, args.seed
     if args.warmup < 3 and args.impl == "tqp":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
     if args.impl == "reference":
