@@ -5,6 +5,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 #include "jit.h"
 
@@ -146,9 +148,17 @@ void tqp_ctx::drain_profile() {
     pending.clear();
 }
 
+// Every entry point is an NVTX range named after it (nsys / ncu --nvtx timelines; nvtx3
+// is header-only and costs a null check without a tool attached).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+
 #define TQP_GUARD(ctx, body)                                                   \
     do {                                                                       \
         if (!(ctx)) return TQP_ERR_INVALID_ARGUMENT;                           \
+        NvtxRange nvtx_range_(__func__);                                       \
         try {                                                                  \
             int cur_ = -1;                                                     \
             cudaGetDevice(&cur_);                                              \
