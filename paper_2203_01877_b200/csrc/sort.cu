@@ -334,8 +334,9 @@ struct ScatterArgs {
     int orig_dtype;
     int64_t* out_perm64;          // last pass
     uint64_t* out_u;              // last pass: sort-domain values
-    const uint32_t* th;           // per tile, per digit: exclusive prefix within the chunk
+    const uint32_t* th;           // per histogram tile, per digit: exclusive prefix within the chunk
     const uint32_t* ct;           // per chunk, per digit: global start
+    int hr;                       // histogram tiles per scatter tile (th's tile is smaller)
     int64_t n;
     int shift;
     bool desc;
@@ -474,7 +475,6 @@ template <typename KT, int IN, int IPT, int RB, int SNT>
 #endif
 __global__ void __launch_bounds__(SNT, (SNT > NT ? 1 : IPT <= 8 ? 4 : (PERM_DIRECT && sizeof(KT) == 4 ? 3 : TQP_SCATTER_MINB))) scatter_tma_kernel(ScatterArgs a, int64_t n_tiles, bool use_tma) {
     constexpr int TILE = SNT * IPT, BINS = 1 << RB, BPT = BINS / SNT, SNW = SNT / 32;
-    constexpr int HR = SNT / NT;   // histogram tiles (NT * IPT keys) per scatter tile
     static_assert(BPT >= 1, "one digit per thread at least");
     constexpr int CLS = scatter_cluster(SNT);
     constexpr uint32_t DM = BINS - 1u;
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(SNT, (SNT > NT ? 1 : IPT <= 8 ? 4 : (PERM_DIRE
 #pragma unroll
         for (int j = 0; j < BPT; j++) {
             const int d = tid + j * SNT;
-            gs[j] = __ldg(a.ct + (tile * HR / CHUNK) * BINS + d) + __ldg(a.th + tile * HR * BINS + d);
+            gs[j] = __ldg(a.ct + (tile * a.hr / CHUNK) * BINS + d) + __ldg(a.th + tile * a.hr * BINS + d);
         }
         if (full(tile)) {
             if (HAS_PERM && PERM_DIRECT) {
@@ -805,10 +805,15 @@ template <typename KT, int RB>
 static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o,
                        const int* shifts, int P, uint32_t* th0 = nullptr) {
     constexpr int BINS = 1 << RB;
-    constexpr int IPT = sizeof(KT) == 4 ? 16 : 12;   // 4096 / 3072 keys per tile
+    constexpr int IPT = sizeof(KT) == 4 ? 16 : 12;   // 4096 / 3072 keys per NT-thread tile
     constexpr int TILE = NT * IPT;
+    // the scatter's CTA width and tile; the tile histograms of passes after the first are
+    // per scatter tile (the fused pass-0 histogram of sort_andor is per TILE keys)
+    constexpr int SNTs = (RB == 9 && sizeof(KT) == 4) ? SCATTER_NT : NT;
+    constexpr int HR0 = SNTs / NT;
     const int64_t tiles = ceil_div(n, TILE);
-    const int64_t chunks = ceil_div(tiles, CHUNK);
+    const int64_t stiles = ceil_div(n, (int64_t)SNTs * IPT);
+    const int64_t chunks_max = ceil_div(tiles, CHUNK);
     DevBuf<KT> kb[2];
     DevBuf<uint32_t> pb[2];
     const bool need_key_final = o.want_internal;
@@ -824,25 +829,28 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         if (kused) kb[b].alloc(ctx, n);
         if (pused) pb[b].alloc(ctx, n);
     }
-    DevBuf<uint32_t> th(ctx, (size_t)tiles * BINS);
-    DevBuf<uint32_t> ct(ctx, (size_t)chunks * BINS);
+    DevBuf<uint32_t> th(ctx, (size_t)stiles * BINS);
+    DevBuf<uint32_t> ct(ctx, (size_t)chunks_max * BINS);
     const int mode0 = in_mode(dtype);
     for (int p = 0; p < P; p++) {
         const void* in = p == 0 ? keys : kb[(p - 1) % 2].get();
         const int mode = p == 0 ? mode0 : (int)IN_INTERNAL;
         const double kin = p == 0 ? (double)dtype_size(dtype) : (double)sizeof(KT);
-        uint32_t* thp = (p == 0 && th0) ? th0 : th.get();   // pass 0: histogram fused into the AND/OR pass
-        if (thp != th0) {
+        const bool fused = p == 0 && th0;   // pass 0: histogram fused into the AND/OR pass
+        uint32_t* thp = fused ? th0 : th.get();
+        const int64_t htiles = fused ? tiles : stiles;
+        const int64_t chunks = ceil_div(htiles, CHUNK);
+        if (!fused) {
             dispatch_in(mode, [&](auto m) {
-                launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT, RB>,
-                       dim3((unsigned)tiles), dim3(NT), 0, in, n, shifts[p], desc, thp);
+                launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT * HR0, RB>,
+                       dim3((unsigned)stiles), dim3(NT), 0, in, n, shifts[p], desc, thp);
             });
-            ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)tiles);
+            ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)stiles);
         }
         launch(ctx, "tqp_sort_scan", scan_tiles_kernel<RB>, dim3((unsigned)chunks, BINS / SNT), dim3(SNT), 0, thp,
-               tiles, ct.get());
+               htiles, ct.get());
         launch(ctx, "tqp_sort_scan", scan_chunks_kernel<RB>, dim3(1), dim3(BINS), 0, ct.get(), chunks);
-        ctx->add_bytes("tqp_sort_scan", 8.0 * BINS * (double)tiles + 12.0 * BINS * (double)chunks);
+        ctx->add_bytes("tqp_sort_scan", 8.0 * BINS * (double)htiles + 12.0 * BINS * (double)chunks);
         ScatterArgs a{};
         a.in_keys = in;
         a.in_perm = p == 0 ? nullptr : pb[(p - 1) % 2].get();
@@ -857,6 +865,7 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         }
         a.th = thp;
         a.ct = ct.get();
+        a.hr = fused ? HR0 : 1;
         a.n = n;
         a.shift = shifts[p];
         a.desc = desc;
@@ -874,7 +883,6 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
             constexpr size_t smem = scatter_tma_smem<KT, INM, IPT, RB, SNTc>();
             auto* kfn = scatter_tma_kernel<KT, INM, IPT, RB, SNTc>;
             const int occ = occupancy(kfn, SNTc, smem);
-            const int64_t stiles = ceil_div(n, (int64_t)SNTc * IPT);
             int64_t grid = std::min<int64_t>(stiles, (int64_t)ctx->num_sms * std::max(occ, 1));
             constexpr int CL = scatter_cluster(SNTc);
             if (CL > 1) {   // a whole number of clusters (the kernel needs them)
