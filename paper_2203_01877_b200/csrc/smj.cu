@@ -37,7 +37,14 @@ namespace tqp {
 namespace {
 constexpr int JNT = 256;
 constexpr int JNW = JNT / 32;
-constexpr int JIPT = 8;
+#ifndef TQP_SMJ_JIPT
+#define TQP_SMJ_JIPT 4
+#endif
+// left rows (buckets) per thread of the bucket / cumsum kernels; measured at SF10 (buckets +
+// cumsum ms): 4 -> 0.166 + 0.070, 8 -> 0.195 + 0.073, 16 -> 0.270 + 0.105 (fewer searches per
+// thread in flight matter less than more threads searching)
+constexpr int JIPT = TQP_SMJ_JIPT;
+static_assert(JIPT % 4 == 0, "16-byte stores");
 constexpr int JTILE = JNT * JIPT;
 
 constexpr uint32_t NOMATCH = 0xFFFFFFFFu;
@@ -149,10 +156,11 @@ __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, 
             tot += R[i];
         }
         if (r0 + JIPT <= nl) {   // 16-byte stores
-            reinterpret_cast<uint4*>(mR + r0)[0] = make_uint4(R[0], R[1], R[2], R[3]);
-            reinterpret_cast<uint4*>(mR + r0)[1] = make_uint4(R[4], R[5], R[6], R[7]);
-            reinterpret_cast<uint4*>(msR + r0)[0] = make_uint4(S[0], S[1], S[2], S[3]);
-            reinterpret_cast<uint4*>(msR + r0)[1] = make_uint4(S[4], S[5], S[6], S[7]);
+#pragma unroll
+            for (int q = 0; q < JIPT / 4; q++) {
+                reinterpret_cast<uint4*>(mR + r0)[q] = make_uint4(R[4 * q], R[4 * q + 1], R[4 * q + 2], R[4 * q + 3]);
+                reinterpret_cast<uint4*>(msR + r0)[q] = make_uint4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < JIPT; i++)
