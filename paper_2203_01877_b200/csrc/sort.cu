@@ -211,11 +211,11 @@ __device__ __forceinline__ KT load_key(const void* in_keys, int64_t pos, bool de
 }
 
 // (1) per-tile digit counts -> th[tile * BINS + d]
-template <typename KT, int IN, int IPT, int RB>
-__global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int64_t n, int shift, bool desc,
+template <typename KT, int IN, int IPT, int RB, int TNT = NT>
+__global__ void __launch_bounds__(TNT) tile_hist_kernel(const void* in_keys, int64_t n, int shift, bool desc,
                                                        uint32_t* __restrict__ th) {
-    constexpr int TILE = NT * IPT, BINS = 1 << RB;
-    __shared__ uint32_t h[NW][BINS];
+    constexpr int TILE = TNT * IPT, BINS = 1 << RB;
+    __shared__ uint32_t h[(TNT / 32)][BINS];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int d = lane; d < BINS; d += 32) h[warp][d] = 0;
     __syncwarp();
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int6
         const uint4* p4 = reinterpret_cast<const uint4*>((const uint32_t*)in_keys + base) + tid;
 #pragma unroll
         for (int j = 0; j < IPT / 4; j++) {
-            const uint4 v = __ldg(p4 + j * NT);
+            const uint4 v = __ldg(p4 + j * TNT);
             k[4 * j] = (KT)v.x; k[4 * j + 1] = (KT)v.y; k[4 * j + 2] = (KT)v.z; k[4 * j + 3] = (KT)v.w;
         }
 #pragma unroll
@@ -245,10 +245,10 @@ __global__ void __launch_bounds__(NT) tile_hist_kernel(const void* in_keys, int6
         }
     }
     __syncthreads();
-    for (int d = tid; d < BINS; d += NT) {
+    for (int d = tid; d < BINS; d += TNT) {
         uint32_t c = 0;
 #pragma unroll
-        for (int w = 0; w < NW; w++) c += h[w][dslot(d)];
+        for (int w = 0; w < (TNT / 32); w++) c += h[w][dslot(d)];
         th[(int64_t)blockIdx.x * BINS + d] = c;
     }
 }
@@ -842,8 +842,9 @@ static void run_passes(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, boo
         const int64_t chunks = ceil_div(htiles, CHUNK);
         if (!fused) {
             dispatch_in(mode, [&](auto m) {
-                launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT * HR0, RB>,
-                       dim3((unsigned)stiles), dim3(NT), 0, in, n, shifts[p], desc, thp);
+                // one CTA of the scatter's width per scatter tile
+                launch(ctx, "tqp_sort_tile_hist", tile_hist_kernel<KT, decltype(m)::value, IPT, RB, SNTs>,
+                       dim3((unsigned)stiles), dim3(SNTs), 0, in, n, shifts[p], desc, thp);
             });
             ctx->add_bytes("tqp_sort_tile_hist", kin * (double)n + 4.0 * BINS * (double)stiles);
         }
