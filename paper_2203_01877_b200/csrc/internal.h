@@ -46,6 +46,10 @@ size_t sort_hist0_words(int64_t n);
 // defer_identity and identity set.
 void sort_materialize_identity(tqp_ctx* ctx, const void* keys, int dtype, int64_t n, bool desc, SortOut& o);
 
+// First / last key (order-preserving images) and an order check of 2,049 evenly spaced
+// keys (pkfk.cu): out[0] = first, out[1] = last, out[2] = 1 if the sample is not in order.
+void sample_first_last(tqp_ctx* ctx, const void* keys, int dt, int64_t n, unsigned long long* out);
+
 // Filter + compaction (filter.cu), used by the group-by sort path for its selection.
 void filter_compact(tqp_ctx* ctx, const tqp_col* cols, int n_cols, int64_t n, const tqp_pred* preds, int n_preds,
                     uint8_t* mask_out, int64_t* sel_out, int64_t* n_sel_host);

@@ -1503,4 +1503,10 @@ void pkfk_outer_build(tqp_ctx* ctx, tqp_col bk, int64_t nb, tqp_col pk, int64_t 
     *n_out_host = m + u;
 }
 
+// The sampled first / last / order check of a key column (first_last_kernel): out[0..2]
+// on the device, stream-ordered (the SMJ's speculative presorted left side uses it too).
+void sample_first_last(tqp_ctx* ctx, const void* keys, int dt, int64_t n, unsigned long long* out) {
+    launch(ctx, "tqp_sort_andor", first_last_kernel, dim3(1), dim3(1024), 0, keys, dt, n, out);
+}
+
 }  // namespace tqp

@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, 
                                                        uint64_t rhi_bits, int64_t nr, const int64_t* __restrict__ rb,
                                                        uint32_t* __restrict__ mR,
                                                        uint32_t* __restrict__ msR, uint64_t* __restrict__ tsum,
-                                                       double* dtot, int* overflow) {
+                                                       double* dtot, int* overflow, int* unsorted) {
     __shared__ unsigned long long s_w[JNW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = (int64_t)blockIdx.x * JTILE;
@@ -137,6 +137,20 @@ __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, 
         KO k[JIPT];
 #pragma unroll
         for (int i = 0; i < JIPT; i++) k[i] = r0 + i < nl ? left_key<KL, KO>(lk, r0 + i) : KO(0);
+        if (unsorted) {   // speculative presorted left side (the caller's column, lk.dt != 0): verify
+                          // the order of the full 64-bit keys, each adjacent pair once (a key outside
+                          // [first, last] cannot pass as a truncated 32-bit key)
+            bool bad = false;
+            uint64_t up = ordered_u64(load_as_i64(lk.p, lk.dt, r0));
+#pragma unroll
+            for (int i = 1; i <= JIPT; i++) {
+                if (r0 + i >= nl) break;
+                const uint64_t u = ordered_u64(load_as_i64(lk.p, lk.dt, r0 + i));
+                bad |= up > u;
+                up = u;
+            }
+            if (bad) *unsorted = 1;
+        }
         uint32_t R[JIPT], S[JIPT];
         int64_t lb = 0, ub = 0;
 #pragma unroll
@@ -571,18 +585,22 @@ __global__ void __launch_bounds__(ENT, CC <= 1025 ? TQP_EXPAND_MINB : 4) expand_
 
 template <typename KL, typename KR, typename KO>
 void launch_buckets(tqp_ctx* ctx, const LeftKeys& lk, int64_t nl, const KR* rk, uint64_t rhi, int64_t nr,
-                    tqp_smj_plan* P, uint64_t* tsum, int64_t tiles, int64_t* scal) {
+                    tqp_smj_plan* P, uint64_t* tsum, int64_t tiles, int64_t* scal, bool verify) {
     DevBuf<int64_t> rb(ctx, 2 * tiles);
     launch(ctx, "tqp_smj_bounds", tile_rbounds_kernel<KL, KR, KO>, dim3((unsigned)ceil_div(2 * tiles, 128)), dim3(128),
            0, lk, nl, rk, rhi, nr, tiles, rb.get());
     launch(ctx, "tqp_smj_buckets", bucket_r_kernel<KL, KR, KO>, dim3((unsigned)tiles), dim3(JNT), 0, lk, nl, rk, rhi, nr,
-           (const int64_t*)rb.get(), P->mR.get(), P->msR.get(), tsum, (double*)(scal + 5), (int*)(scal + 4));
+           (const int64_t*)rb.get(), P->mR.get(), P->msR.get(), tsum, (double*)(scal + 5), (int*)(scal + 4),
+           verify ? (int*)(scal + 2) : (int*)nullptr);
 }
 }  // namespace
 
-tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right, int64_t nr, int64_t* out_size_host) {
-    check_col(left, nl, "smj left");
-    check_col(right, nr, "smj right");
+// spec: take a left side whose first / last / sampled keys are in order as sorted without
+// the plan pass over it (primary-key columns are usually stored in key order); the bucket
+// kernel, which reads every left key anyway, verifies the order and a left side that is
+// not sorted after all is prepared again the ordinary way (returns nullptr).
+static tqp_smj_plan* smj_prepare_impl(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right, int64_t nr,
+                                      int64_t* out_size_host, bool spec) {
     auto* P = new tqp_smj_plan();
     try {
         P->n_left = nl;
@@ -595,14 +613,32 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         SortOut sl, sr;
         sl.want_internal = sr.want_internal = true;
         sl.defer_identity = true;   // a left side in key order is read as it is (no identity pass)
+        bool verify = false;   // the left side was taken as sorted on a sample: the bucket kernel checks it
         {   // both digit plans with one host sync
             constexpr int W = SORT_PLAN_WORDS;
             DevBuf<unsigned long long> ao(ctx, 2 * W);
-            DevBuf<uint32_t> hl(ctx, sort_hist0_words(nl)), hr(ctx, sort_hist0_words(nr));
-            sort_andor(ctx, left.data, left.dtype, nl, false, ao.get(), hl.get());
+            DevBuf<uint32_t> hl, hr(ctx, sort_hist0_words(nr));
+            if (spec) sample_first_last(ctx, left.data, left.dtype, nl, ao.get());
+            else {
+                hl.alloc(ctx, sort_hist0_words(nl));
+                sort_andor(ctx, left.data, left.dtype, nl, false, ao.get(), hl.get());
+            }
             sort_andor(ctx, right.data, right.dtype, nr, false, ao.get() + W, hr.get());
             uint64_t h[2 * W];
             read_back(ctx, h, ao.get(), 16 * W);
+            if (spec && h[2]) {   // the sample is out of order: the left side's own plan pass
+                hl.alloc(ctx, sort_hist0_words(nl));
+                sort_andor(ctx, left.data, left.dtype, nl, false, ao.get(), hl.get());
+                read_back(ctx, h, ao.get(), 8 * W);
+            } else if (spec) {   // plan words of a side in key order: its keys lie in [first, last]
+                const uint64_t first = h[0], last = h[1];
+                h[0] = first;    // AND / OR stand-ins whose XOR has a high word iff the keys' high words differ
+                h[1] = last;
+                h[2] = 0;
+                h[3] = first;
+                h[4] = last;
+                verify = true;
+            }
             radix_sort(ctx, left.data, left.dtype, nl, false, sl, h, hl.get());
             radix_sort(ctx, right.data, right.dtype, nr, false, sr, h + W, hr.get());
         }
@@ -633,8 +669,8 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
             using KL = decltype(kl);
             using KR = decltype(kr);
             const KR* rk = sizeof(KR) == 4 ? (const KR*)sr.keys32.get() : (const KR*)sr.keys64.get();
-            if (k32) launch_buckets<KL, KR, uint32_t>(ctx, lk, nl, rk, rhi, nr, P, tsum.get(), ctiles, scal.get());
-            else launch_buckets<KL, KR, uint64_t>(ctx, lk, nl, rk, rhi, nr, P, tsum.get(), ctiles, scal.get());
+            if (k32) launch_buckets<KL, KR, uint32_t>(ctx, lk, nl, rk, rhi, nr, P, tsum.get(), ctiles, scal.get(), verify);
+            else launch_buckets<KL, KR, uint64_t>(ctx, lk, nl, rk, rhi, nr, P, tsum.get(), ctiles, scal.get(), verify);
         };
         if (sl.k32 || lid) {
             if (sr.k32) go(uint32_t{}, uint32_t{}); else go(uint32_t{}, uint64_t{});
@@ -652,6 +688,10 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         TQP_CUDA(cudaMemcpyAsync(scal.get() + 3, toff.get() + ctiles, 8, cudaMemcpyDeviceToDevice, ctx->stream));
         int64_t h[6];
         read_back(ctx, h, scal.get(), 48);
+        if (verify && (int)h[2]) {   // not sorted after all
+            delete P;
+            return nullptr;
+        }
         double dt;
         memcpy(&dt, &h[5], 8);
         if (h[4] || dt >= 4.6116860184273879e18 || (uint64_t)h[3] >= SUM_CAP)   // 2^62
@@ -687,6 +727,22 @@ tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right,
         delete P;
         throw;
     }
+}
+
+tqp_smj_plan* smj_prepare(tqp_ctx* ctx, tqp_col left, int64_t nl, tqp_col right, int64_t nr, int64_t* out_size_host) {
+    check_col(left, nl, "smj left");
+    check_col(right, nr, "smj right");
+    // TQP_SMJ_NO_SPEC=1 (and TQP_SORT_NO_PRESORTED, whose radix route needs the true plan)
+    // always runs the left side's plan pass
+    static const bool no_spec = [] {
+        const char* e = std::getenv("TQP_SMJ_NO_SPEC");
+        const char* f = std::getenv("TQP_SORT_NO_PRESORTED");
+        return (e && std::atoi(e) != 0) || (f && std::atoi(f) != 0);
+    }();
+    const bool spec = !no_spec && nl >= (1 << 16) && nr > 0 && (left.dtype == TQP_I64 || left.dtype == TQP_I32);
+    if (spec)
+        if (tqp_smj_plan* P = smj_prepare_impl(ctx, left, nl, right, nr, out_size_host, true)) return P;
+    return smj_prepare_impl(ctx, left, nl, right, nr, out_size_host, false);
 }
 
 // more than ~700 buckets per output tile on average: the larger staging of bucket ends

@@ -1470,3 +1470,37 @@ def test_groupby_dense_unaligned_columns(T, offset, dense_kernel):
     preds = [(1, "ge", -4000)]
     got = T.groupby_agg(gcols, [0], aggs, preds)
     check_groupby(T, got, oracle.groupby_agg(cols, [0], aggs, preds), aggs)
+
+
+@pytest.mark.parametrize("case", ["sorted", "one_swap", "shuffled_middle", "high_word", "sorted_dups", "sorted_i32"])
+def test_smj_speculative_sorted_left(T, case, monkeypatch):
+    """The SMJ takes a left side whose first / last / 2,049 sampled keys are in order as
+    sorted without its plan pass; the bucket kernel verifies the order of every adjacent
+    pair in the full 64-bit key domain and a left side that is not sorted after all -- one
+    adjacent swap, a shuffled middle, a key with another high word that a 32-bit key
+    domain would truncate into order -- is prepared again with the sort. Against the
+    oracle, with the poisoned allocator (the retry must not read the first attempt's
+    temporaries)."""
+    monkeypatch.setenv("TQP_ALLOC_POISON", "1")
+    ctx = T.Context()
+    rng = np.random.default_rng(31 + len(case))
+    nl = 150_007
+    left = np.sort(rng.choice(4 * nl, nl, replace=not case.endswith("dups"))).astype(np.int64) + 10
+    if case == "one_swap":
+        j = nl // 2
+        left[j], left[j + 1] = left[j + 1], left[j]
+    elif case == "shuffled_middle":
+        mid = left[1:-1].copy()
+        rng.shuffle(mid)
+        left[1:-1] = mid
+    elif case == "high_word":   # sample-invisible: (1 << 40) + key looks in order when truncated to 32 bits
+        j = nl // 2 + 3
+        left[j] = (1 << 40) + (left[j - 1] + left[j + 1]) // 2 if left[j + 1] - left[j - 1] > 1 else left[j] + (1 << 40)
+    dt = torch.int32 if case == "sorted_i32" else torch.int64
+    right = rng.choice(left, 600_001).astype(np.int64)
+    right[::9] = rng.integers(0, 5 * nl, right[::9].size)
+    if dt == torch.int32:
+        left, right = left.astype(np.int32), right.astype(np.int32)
+    lo, ro = ctx.smj_join(cu(left, dt), cu(right, dt))
+    olo, oro = oracle.smj_join(left.astype(np.int64), right.astype(np.int64))
+    assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
