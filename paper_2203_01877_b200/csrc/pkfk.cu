@@ -96,7 +96,15 @@ constexpr uint32_t RB_BITS = 224;
 // block writes the block's rank (its sorted position); equal neighbours flag a duplicate.
 // Reads the caller's build keys directly (the sort's identity route writes nothing): the
 // low 32 bits of the order-preserving key (all varying bits are there, k32).
-constexpr int RBK = 8;
+// keys per thread of rank_bitmap_kernel and its grid (CTAs per SM at most); measured, SF10
+// orders: 8 keys / 8 per SM 0.047 ms, 16 / 8 0.079, 4 / 8 0.042, 8 / 32 0.048, 4 / 32 0.039
+#ifndef TQP_RBK
+#define TQP_RBK 4
+#endif
+#ifndef TQP_RB_GRID
+#define TQP_RB_GRID 32
+#endif
+constexpr int RBK = TQP_RBK;
 // Speculative route (unsorted != null): the caller only knows the first and the last key;
 // a key out of order, outside [first, last] or with another high word sets *unsorted and
 // the host rebuilds the build side by the sort (the bitmap is then garbage, never used).
@@ -877,7 +885,7 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allo
                 B.unsorted.zero();
                 B.rank_bm.alloc(ctx, nblk * 8);
                 B.rank_bm.zero();
-                const int g = (int)std::min<int64_t>(ceil_div(ceil_div(nb, RBK), 256), (int64_t)ctx->num_sms * 8);
+                const int g = (int)std::min<int64_t>(ceil_div(ceil_div(nb, RBK), 256), (int64_t)ctx->num_sms * TQP_RB_GRID);
                 launch(ctx, "tqp_pkfk_rank_bitmap", rank_bitmap_kernel, dim3(g), dim3(256), 0, bk.data, (int)bk.dtype,
                        nb, (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get(), B.unsorted.get(),
                        (uint32_t)(lo >> 32), (uint32_t)span);
@@ -933,7 +941,7 @@ void build_side(tqp_ctx* ctx, const tqp_col& bk, int64_t nb, Built& B, bool allo
             B.rank_span = (uint32_t)span;
             B.rank_bm.alloc(ctx, nblk * 8);
             B.rank_bm.zero();
-            const int g = (int)std::min<int64_t>(ceil_div(ceil_div(nb, RBK), 256), (int64_t)ctx->num_sms * 8);
+            const int g = (int)std::min<int64_t>(ceil_div(ceil_div(nb, RBK), 256), (int64_t)ctx->num_sms * TQP_RB_GRID);
             launch(ctx, "tqp_pkfk_rank_bitmap", rank_bitmap_kernel, dim3(g), dim3(256), 0, bk.data, (int)bk.dtype, nb,
                    (uint32_t)B.base, nblk, B.rank_bm.get(), B.dup.get(), (int*)nullptr, 0u, 0u);
             ctx->add_bytes("tqp_pkfk_rank_bitmap", (double)dtype_size(bk.dtype) * (double)nb + 32.0 * (double)nblk);
