@@ -1016,7 +1016,14 @@ __device__ __forceinline__ void tile_pipeline(const Phase1Args& a, uint8_t* smem
     }
 }
 
-__global__ void __launch_bounds__(GNT) gb_phase1_kernel(Phase1Args a) {
+// Blocks per SM the register budget must allow (78 registers, no spills): measured, Q6's
+// fused filter + sum at SF10 (the no-key tiles), 116 registers / 2 blocks 0.337 ms, 3 blocks
+// 0.277-0.281 ms, 4 blocks (64 registers) 0.308 ms; an explicit minimum of 1 let ptxas take
+// 138 registers (1 block, 0.549 ms).
+#ifndef TQP_PHASE1_MINB
+#define TQP_PHASE1_MINB 3
+#endif
+__global__ void __launch_bounds__(GNT, TQP_PHASE1_MINB) gb_phase1_kernel(Phase1Args a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int NS = a.n_stages;   // 2..4 stages in flight per CTA
     Work& w = *reinterpret_cast<Work*>(smem + (size_t)NS * a.stage_bytes);
@@ -2478,7 +2485,10 @@ static tqp_groupby_plan* groupby_prepare_int(tqp_ctx* ctx, const tqp_col* cols, 
         if (nokey_path && n > 0) {
             // pipeline depth: light per-row work (no group keys) is bandwidth-bound and
             // wants more bytes in flight; keyed tiles are compute-heavy and prefer 2 CTAs/SM
-            a.n_stages = ((size_t)4 * a.stage_bytes + sizeof(NoKeyWork) <= 112 * 1024) ? 4 : 2;
+#ifndef TQP_NOKEY_STAGES   // (3 stages at 3 blocks per SM: 0.349 ms; 2: 0.278)
+#define TQP_NOKEY_STAGES 4
+#endif
+            a.n_stages = ((size_t)TQP_NOKEY_STAGES * a.stage_bytes + sizeof(NoKeyWork) <= 112 * 1024) ? TQP_NOKEY_STAGES : 2;
             nokey_smem = (size_t)a.n_stages * a.stage_bytes + sizeof(NoKeyWork);
             const int occ = occupancy(gb_phase1_kernel, GNT, nokey_smem);
             nokey_grid = std::min<int64_t>(tiles, (int64_t)ctx->num_sms * std::max(occ, 1));
