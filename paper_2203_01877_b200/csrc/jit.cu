@@ -284,8 +284,8 @@ namespace {
 struct JitKernel {
     cudaLibrary_t lib = nullptr;
     cudaKernel_t k = nullptr;
-    size_t smem_set = 0;
-    std::map<size_t, int> occ;   // resident CTAs per SM by dynamic shared memory bytes
+    std::map<int, size_t> smem_set;   // per device: the dynamic shared memory limit set so far
+    std::map<size_t, int> occ;        // resident CTAs per SM by dynamic shared memory bytes
 };
 std::mutex& jit_mutex() {
     static std::mutex m;
@@ -339,12 +339,15 @@ JitKernel* dense_jit_kernel(const DenseJitSpec& s) {
 }
 
 bool set_jit_smem(JitKernel* jk, size_t smem) {
-    if (smem <= jk->smem_set) return true;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    size_t& cur = jk->smem_set[dev];
+    if (smem <= cur) return true;
     if (cudaFuncSetAttribute((const void*)jk->k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
         cudaGetLastError();
         return false;
     }
-    jk->smem_set = smem;
+    cur = smem;
     return true;
 }
 }  // namespace
