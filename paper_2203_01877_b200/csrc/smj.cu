@@ -209,9 +209,17 @@ __global__ void __launch_bounds__(JNT) cum_write_kernel(const uint32_t* __restri
     const int64_t base = (int64_t)blockIdx.x * JTILE + (int64_t)tid * JIPT;
     if ((int64_t)blockIdx.x * JTILE >= K) return;
     uint64_t v[JIPT], t = 0;
+    const bool fullv = base + JIPT <= K;   // whole rows: 16-byte loads / stores
+    if (fullv) {
+#pragma unroll
+        for (int q = 0; q < JIPT / 4; q++) {
+            const uint4 u = reinterpret_cast<const uint4*>(mR + base)[q];
+            v[4 * q] = u.x; v[4 * q + 1] = u.y; v[4 * q + 2] = u.z; v[4 * q + 3] = u.w;
+        }
+    }
 #pragma unroll
     for (int i = 0; i < JIPT; i++) {
-        v[i] = base + i < K ? (uint64_t)mR[base + i] : 0;
+        if (!fullv) v[i] = base + i < K ? (uint64_t)mR[base + i] : 0;
         t += v[i];
     }
     uint64_t x = t;
@@ -226,13 +234,22 @@ __global__ void __launch_bounds__(JNT) cum_write_kernel(const uint32_t* __restri
 #pragma unroll
     for (int w = 0; w < JNW; w++)
         if (w < warp) run += s_w[w];
+    if (fullv) {
+        uint64_t c[JIPT];
+        uint64_t r2 = run;
+#pragma unroll
+        for (int i = 0; i < JIPT; i++) { r2 += v[i]; c[i] = r2; }
+#pragma unroll
+        for (int q = 0; q < JIPT / 2; q++)
+            reinterpret_cast<longlong2*>(mcum + base)[q] = make_longlong2((long long)c[2 * q], (long long)c[2 * q + 1]);
+    }
 #pragma unroll
     for (int i = 0; i < JIPT; i++) {
         const int64_t b = base + i;
         if (b >= K) break;
         const int64_t start = (int64_t)run;
         run += v[i];
-        mcum[b] = (int64_t)run;
+        if (!fullv) mcum[b] = (int64_t)run;
         // output tiles whose first output falls inside this key's range [start, run)
         if (!tb) continue;   // coarse table: tb_search_kernel
         for (int64_t c = (start + ETILE_C - 1) / ETILE_C; c * ETILE_C < (int64_t)run; c++) tb[c] = (uint32_t)b;
