@@ -135,8 +135,24 @@ __global__ void __launch_bounds__(JNT) bucket_r_kernel(LeftKeys lk, int64_t nl, 
     uint64_t tot = 0;
     if (r0 < nl) {
         KO k[JIPT];
+        if (r0 + JIPT <= nl && lk.dt == TQP_I64 && ((uintptr_t)lk.p & 15) == 0) {   // the caller's int64 column:
+#pragma unroll                                                                      // 16-byte loads
+            for (int q = 0; q < JIPT / 2; q++) {
+                const longlong2 u = __ldg(reinterpret_cast<const longlong2*>((const long long*)lk.p + r0) + q);
+                k[2 * q] = (KO)ordered_u64(u.x);
+                k[2 * q + 1] = (KO)ordered_u64(u.y);
+            }
+        } else if (r0 + JIPT <= nl && lk.dt == 0 && sizeof(KL) == 4) {   // internal u32 keys
 #pragma unroll
-        for (int i = 0; i < JIPT; i++) k[i] = r0 + i < nl ? left_key<KL, KO>(lk, r0 + i) : KO(0);
+            for (int q = 0; q < JIPT / 4; q++) {
+                const uint4 u = __ldg(reinterpret_cast<const uint4*>((const uint32_t*)lk.p + r0) + q);
+                k[4 * q] = (KO)(lk.hi | u.x); k[4 * q + 1] = (KO)(lk.hi | u.y);
+                k[4 * q + 2] = (KO)(lk.hi | u.z); k[4 * q + 3] = (KO)(lk.hi | u.w);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < JIPT; i++) k[i] = r0 + i < nl ? left_key<KL, KO>(lk, r0 + i) : KO(0);
+        }
         if (unsorted) {   // speculative presorted left side (the caller's column, lk.dt != 0): verify
                           // the order of the full 64-bit keys, each adjacent pair once (a key outside
                           // [first, last] cannot pass as a truncated 32-bit key)
