@@ -116,11 +116,30 @@ __global__ void rank_bitmap_kernel(const void* __restrict__ keys, int dt, int64_
         const int64_t i0 = t * RBK;
         uint32_t prev = i0 > 0 ? (uint32_t)ordered_u64(load_as_i64(keys, dt, i0 - 1)) - base : 0xFFFFFFFFu;
         uint32_t cw = 0xFFFFFFFFu, cv = 0;   // current word index and its pending bits
+        uint64_t uk[RBK];   // this thread's keys (order-preserving): 16-byte loads when whole and aligned
+        if (dt == TQP_I64 && RBK % 2 == 0 && i0 + RBK <= n && ((uintptr_t)keys & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < RBK / 2; q++) {
+                const longlong2 v = __ldg(reinterpret_cast<const longlong2*>((const long long*)keys + i0) + q);
+                uk[2 * q] = ordered_u64(v.x);
+                uk[2 * q + 1] = ordered_u64(v.y);
+            }
+        } else if (dt == TQP_I32 && RBK % 4 == 0 && i0 + RBK <= n && ((uintptr_t)keys & 15) == 0) {
+#pragma unroll
+            for (int q = 0; q < RBK / 4; q++) {
+                const int4 v = __ldg(reinterpret_cast<const int4*>((const int*)keys + i0) + q);
+                uk[4 * q] = ordered_u64(v.x); uk[4 * q + 1] = ordered_u64(v.y);
+                uk[4 * q + 2] = ordered_u64(v.z); uk[4 * q + 3] = ordered_u64(v.w);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < RBK; j++) uk[j] = i0 + j < n ? ordered_u64(load_as_i64(keys, dt, i0 + j)) : 0;
+        }
 #pragma unroll
         for (int j = 0; j < RBK; j++) {
             const int64_t i = i0 + j;
             if (i >= n) break;
-            const uint64_t u = ordered_u64(load_as_i64(keys, dt, i));
+            const uint64_t u = uk[j];
             const uint32_t rel = (uint32_t)u - base;
             if (unsorted && ((uint32_t)(u >> 32) != hi32 || rel > span || (i > 0 && rel < prev))) {
                 *unsorted = 1;
