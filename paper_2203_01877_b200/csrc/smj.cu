@@ -599,14 +599,12 @@ __global__ void __launch_bounds__(ENT, CC <= 1025 ? TQP_EXPAND_MINB : 4) expand_
     int64_t* lo_p = (int64_t*)lo_out + (c0 - begin);
     int64_t* ro_p = (int64_t*)ro_out + (c0 - begin);
     const bool vec = n == ETILE && (((uintptr_t)lo_p | (uintptr_t)ro_p) & 15) == 0;
-    if (vec) {   // 4 outputs per thread and step: one 16-byte shared load, two 16-byte stores per array
-        for (int o = threadIdx.x * 4; o < n; o += ENT * 4) {
-            const uint4 a = *reinterpret_cast<const uint4*>(s_l + o);
-            const uint4 b = *reinterpret_cast<const uint4*>(s_r + o);
+    if (vec) {   // 2 outputs per thread and store: every warp store covers 512 contiguous bytes
+        for (int o = threadIdx.x * 2; o < n; o += ENT * 2) {
+            const uint2 a = *reinterpret_cast<const uint2*>(s_l + o);
+            const uint2 b = *reinterpret_cast<const uint2*>(s_r + o);
             __stcs(reinterpret_cast<longlong2*>(lo_p + o), make_longlong2(a.x, a.y));
-            __stcs(reinterpret_cast<longlong2*>(lo_p + o) + 1, make_longlong2(a.z, a.w));
             __stcs(reinterpret_cast<longlong2*>(ro_p + o), make_longlong2(b.x, b.y));
-            __stcs(reinterpret_cast<longlong2*>(ro_p + o) + 1, make_longlong2(b.z, b.w));
         }
     } else {
         for (int o = threadIdx.x; o < n; o += ENT) {   // coalesced, streamed (evict-first) stores
