@@ -386,6 +386,13 @@ __device__ __forceinline__ void pay_copy(const void* src, int dt, int64_t from, 
 #ifndef TQP_EXPAND_CCAP
 #define TQP_EXPAND_CCAP 1025
 #endif
+// Bucket-major fill: 1 = the threads write each output's sorted right position, then the
+// CTA gathers perm_r for consecutive outputs (warp-coalesced: consecutive buckets own
+// consecutive sorted right rows); 0 = each thread gathers its own buckets' rows.
+// Measured (SF10 orders x lineitem expansion): 0.273 -> 0.256 ms.
+#ifndef TQP_EXPAND_COOP
+#define TQP_EXPAND_COOP 1
+#endif
 template <bool CK, bool PAY = false, int CC = TQP_EXPAND_CCAP>
 __global__ void __launch_bounds__(ENT, CC <= 1025 ? TQP_EXPAND_MINB : 4) expand_kernel(const uint32_t* __restrict__ mR,
                                                      const uint32_t* __restrict__ msR,
@@ -478,11 +485,23 @@ __global__ void __launch_bounds__(ENT, CC <= 1025 ? TQP_EXPAND_MINB : 4) expand_
             const int64_t r0 = (i > 0 && pe >= 0) ? 0 : c0 - (mcum[b] - (int64_t)R);
             TQP_DCHECK(r0 >= 0 && r0 + (en - st) <= (int64_t)R);
             const uint32_t lrow = perm_l ? __ldg(perm_l + b) : (uint32_t)b;
-            const uint32_t* pr = perm_r + sR + r0;
-            for (int p = st; p < en; p++) {
-                s_l[p] = lrow;
-                s_r[p] = __ldg(pr + (p - st));
+            if (TQP_EXPAND_COOP) {   // the right row's sorted position; gathered below, warp-coalesced
+                const uint32_t q0 = sR + (uint32_t)r0;
+                for (int p = st; p < en; p++) {
+                    s_l[p] = lrow;
+                    s_r[p] = q0 + (uint32_t)(p - st);
+                }
+            } else {
+                const uint32_t* pr = perm_r + sR + r0;
+                for (int p = st; p < en; p++) {
+                    s_l[p] = lrow;
+                    s_r[p] = __ldg(pr + (p - st));
+                }
             }
+        }
+        if (TQP_EXPAND_COOP) {   // consecutive outputs of consecutive buckets: consecutive sorted right rows
+            __syncthreads();
+            for (int o = threadIdx.x; o < n_out; o += ENT) s_r[o] = __ldg(perm_r + s_r[o]);
         }
         if (CK) {
             __syncthreads();
