@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(ENT, CC <= 1025 ? TQP_EXPAND_MINB : 4) expand_
             if (j >= cnt) break;
             TQP_DCHECK(r < R);
             vl[j] = lrow;
-            vr[j] = __ldg(perm_r + sR + r);
+            // (COOP, stored outputs: the sorted right position, gathered below warp-coalesced)
+            vr[j] = (TQP_EXPAND_COOP && !CK) ? (uint32_t)(sR + r) : __ldg(perm_r + sR + r);
             if (CK) {
                 hs += mix64(mix64(((uint64_t)vl[j] << 32) | vr[j]) ^ (uint64_t)(o0 + j));
                 sl += vl[j];
@@ -588,6 +589,10 @@ __global__ void __launch_bounds__(ENT, CC <= 1025 ? TQP_EXPAND_MINB : 4) expand_
     }
     __syncthreads();
     const int n = (int)(c1 - c0);
+    if (TQP_EXPAND_COOP && !bmajor) {   // output-major staging holds sorted right positions
+        for (int o = threadIdx.x; o < n; o += ENT) s_r[o] = __ldg(perm_r + s_r[o]);
+        __syncthreads();
+    }
     if (PAY) {   // index outputs optional; payload gathered per output, coalesced stores
         for (int o = threadIdx.x; o < n; o += ENT) {
             const int64_t j = c0 - begin + o;
