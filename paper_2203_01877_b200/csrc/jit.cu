@@ -89,9 +89,37 @@ std::string u64lit(unsigned long long v) {
 const char* ctype(int dt) { return dt == TQP_U8 ? "u8" : dt == TQP_I32 ? "int" : "i64"; }
 int esize(int dt) { return dt == TQP_U8 ? 1 : dt == TQP_I32 ? 4 : 8; }
 
+// Rows of a thread in the tile: paired (default) = rows 2 tid, 2 tid + 1, 2 NT + 2 tid,
+// 2 NT + 2 tid + 1, so each shared-memory vector load of a warp is contiguous (no bank
+// conflicts); else 4 tid .. 4 tid + 3 (lanes 32 bytes apart in an int64 column: 2-way
+// conflicts on every 16-byte load). Aggregation does not care which thread takes a row.
+#ifndef TQP_JIT_PAIRED
+#define TQP_JIT_PAIRED 1
+#endif
+
 // the 4 rows of stage slot u for this thread, sign / zero extended: x<u>_<i>
 void emit_load(std::ostringstream& o, const DenseJitSpec& s, int u) {
     const int off = s.uoff[u];
+    if (TQP_JIT_PAIRED) {
+        const int NT = s.nt;
+        if (s.udt[u] == TQP_I64) {
+            o << "      const longlong2 a" << u << " = reinterpret_cast<const longlong2*>(st + " << off << ")[tid];\n"
+              << "      const longlong2 b" << u << " = reinterpret_cast<const longlong2*>(st + " << off << ")[" << NT << " + tid];\n"
+              << "      const i64 x" << u << "_0 = a" << u << ".x, x" << u << "_1 = a" << u << ".y, x" << u << "_2 = b" << u
+              << ".x, x" << u << "_3 = b" << u << ".y;\n";
+        } else if (s.udt[u] == TQP_I32) {
+            o << "      const int2 a" << u << " = reinterpret_cast<const int2*>(st + " << off << ")[tid];\n"
+              << "      const int2 b" << u << " = reinterpret_cast<const int2*>(st + " << off << ")[" << NT << " + tid];\n"
+              << "      const i64 x" << u << "_0 = a" << u << ".x, x" << u << "_1 = a" << u << ".y, x" << u << "_2 = b" << u
+              << ".x, x" << u << "_3 = b" << u << ".y;\n";
+        } else {
+            o << "      const u32 a" << u << " = reinterpret_cast<const unsigned short*>(st + " << off << ")[tid];\n"
+              << "      const u32 b" << u << " = reinterpret_cast<const unsigned short*>(st + " << off << ")[" << NT << " + tid];\n"
+              << "      const i64 x" << u << "_0 = (i64)(a" << u << " & 0xFFu), x" << u << "_1 = (i64)(a" << u << " >> 8), x" << u
+              << "_2 = (i64)(b" << u << " & 0xFFu), x" << u << "_3 = (i64)(b" << u << " >> 8);\n";
+        }
+        return;
+    }
     if (s.udt[u] == TQP_I64) {
         o << "      const longlong2 a" << u << " = reinterpret_cast<const longlong2*>(st + " << off << ")[2 * tid];\n"
           << "      const longlong2 b" << u << " = reinterpret_cast<const longlong2*>(st + " << off << ")[2 * tid + 1];\n"
@@ -172,8 +200,15 @@ std::string dense_jit_source(const DenseJitSpec& s) {
     }
     o << "      __syncthreads();\n    }\n";
     // ---- one tile: 4 consecutive rows per thread
-    o << "    {\n      const int r0 = tid * 4;\n";
-    for (int i = 0; i < 4; i++) o << "      bool p" << i << " = " << (s.never ? "false && " : "") << "r0 + " << i << " < nrows;\n";
+    if (TQP_JIT_PAIRED) {
+        o << "    {\n";
+        for (int i = 0; i < 4; i++)
+            o << "      bool p" << i << " = " << (s.never ? "false && " : "") << "(" << (i < 2 ? 0 : 2 * NT) << " + 2 * tid + "
+              << (i & 1) << ") < nrows;\n";
+    } else {
+        o << "    {\n      const int r0 = tid * 4;\n";
+        for (int i = 0; i < 4; i++) o << "      bool p" << i << " = " << (s.never ? "false && " : "") << "r0 + " << i << " < nrows;\n";
+    }
     std::vector<bool> used(s.n_ucols, false);
     for (int q = 0; q < s.n_terms; q++) used[s.tcol[q]] = true;
     for (int k = 0; k < NK; k++) used[s.kslot[k]] = true;
