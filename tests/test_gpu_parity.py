@@ -1427,10 +1427,11 @@ def test_context_allocator_hooks(T):
     before = torch.cuda.memory_allocated()
     lo, ro = ctx.pkfk_join(b, p)
     assert np.array_equal(npy(lo), olo) and np.array_equal(npy(ro), oro)
-    held = ctx.cached_bytes()
-    assert held > 0
-    # libtqp's cached blocks are torch allocations (outputs lo / ro come on top)
-    assert torch.cuda.memory_allocated() - before >= held
+    if os.environ.get("TQP_ALLOC_EXACT") != "1":   # checked mode frees every temporary at once: no cache
+        held = ctx.cached_bytes()
+        assert held > 0
+        # libtqp's cached blocks are torch allocations (outputs lo / ro come on top)
+        assert torch.cuda.memory_allocated() - before >= held
     ctx.trim()
     assert ctx.cached_bytes() == 0
     del lo, ro
