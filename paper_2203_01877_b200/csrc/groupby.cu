@@ -1859,7 +1859,37 @@ struct SortPathArgs {
     uint64_t* glo[TQP_MAX_AGGS];
     int64_t* ghi[TQP_MAX_AGGS];
     int* overflow;
+    // nullable: the distinct factor columns interleaved per selected row (aos[q * astride + u],
+    // int64), so the reduction's random gather of a row fetches one sector, not one per column
+    const int64_t* aos;
+    int astride;
+    int fu[TQP_MAX_AGGS][3];          // factor (pair, f) -> its column's slot in a row's record
 };
+
+// the AoS copy: row q of the selection, every distinct factor column as int64
+struct AosArgs {
+    int64_t m;
+    const int64_t* sel;
+    int nu, stride;
+    const void* col[4];
+    int dt[4];
+    int64_t* aos;
+};
+__global__ void sp_aos_kernel(AosArgs a) {
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.m; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = a.sel ? a.sel[q] : q;
+        int64_t v[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int u = 0; u < 4; u++)
+            if (u < a.nu) v[u] = load_as_i64(a.col[u], a.dt[u], row);
+        if (a.stride == 2) {
+            reinterpret_cast<longlong2*>(a.aos)[q] = make_longlong2(v[0], v[1]);
+        } else {
+            reinterpret_cast<longlong2*>(a.aos)[2 * q] = make_longlong2(v[0], v[1]);
+            reinterpret_cast<longlong2*>(a.aos)[2 * q + 1] = make_longlong2(v[2], v[3]);
+        }
+    }
+}
 
 __global__ void sp_keys_kernel(SortPathArgs a) {
     __shared__ uint64_t s_kmin[TQP_MAX_KEYS];
@@ -1889,12 +1919,27 @@ __global__ void __launch_bounds__(256) sp_reduce_kernel(SortPathArgs a) {
     int64_t rows[SPT];
     uint32_t g[SPT];
     const int cnt = (int)(p1 - p0);
+    int64_t rec[SPT][4];   // AoS: each row's factor columns, one random sector per row
 #pragma unroll
     for (int i = 0; i < SPT; i++) {
         if (i < cnt) {
             g[i] = a.gid[p0 + i];
             const uint32_t q = a.perm[p0 + i];
-            rows[i] = a.sel ? a.sel[q] : (int64_t)q;
+            if (a.aos) {
+                const longlong2 u0 = __ldg(reinterpret_cast<const longlong2*>(a.aos + (int64_t)q * a.astride));
+                rec[i][0] = u0.x;
+                rec[i][1] = u0.y;
+                if (a.astride == 4) {
+                    const longlong2 u1 = __ldg(reinterpret_cast<const longlong2*>(a.aos + (int64_t)q * a.astride) + 1);
+                    rec[i][2] = u1.x;
+                    rec[i][3] = u1.y;
+                } else {
+                    rec[i][2] = rec[i][3] = 0;
+                }
+                rows[i] = 0;
+            } else {
+                rows[i] = a.sel ? a.sel[q] : (int64_t)q;
+            }
         }
     }
     // a segment is shared with a neighbour iff it is this range's first (gprev equal)
@@ -1930,8 +1975,14 @@ __global__ void __launch_bounds__(256) sp_reduce_kernel(SortPathArgs a) {
             const void* col = a.fcol[j][f];
             const int dt = a.fdt[j][f];
             int64_t x[SPT];
+            if (a.aos) {
+                const int fu = a.fu[j][f];
 #pragma unroll
-            for (int i = 0; i < SPT; i++) x[i] = i < cnt ? load_as_i64(col, dt, rows[i]) : 0;
+                for (int i = 0; i < SPT; i++) x[i] = i < cnt ? (fu == 0 ? rec[i][0] : fu == 1 ? rec[i][1] : fu == 2 ? rec[i][2] : rec[i][3]) : 0;
+            } else {
+#pragma unroll
+                for (int i = 0; i < SPT; i++) x[i] = i < cnt ? load_as_i64(col, dt, rows[i]) : 0;
+            }
 #pragma unroll
             for (int i = 0; i < SPT; i++) {
                 int64_t t;
@@ -2115,6 +2166,47 @@ void sort_path(tqp_ctx* ctx, tqp_groupby_plan* PL, const tqp_col* cols, int n_co
         } else {
             launch(ctx, "tqp_groupby_init", gb_init_kernel, dim3(ig), dim3(256), 0, PL->glo[j].get(), m,
                    PL->pop[j] == P_MIN ? (uint64_t)INT64_MAX : (uint64_t)INT64_MIN);
+        }
+    }
+    // 2-4 distinct factor columns: interleave them per selected row first (a sequential pass),
+    // so the reduction's random gather of a row fetches one sector instead of one per column
+    DevBuf<int64_t> aos;
+    {
+        const void* uc[4];
+        int ud[4], nu = 0;
+        bool fits = true;
+        for (int j = 0; j < PL->n_pairs && fits; j++)
+            for (int f = 0; f < pnf[j]; f++) {
+                int u = 0;
+                while (u < nu && uc[u] != a.fcol[j][f]) u++;
+                if (u == nu) {
+                    if (nu == 4) { fits = false; break; }
+                    uc[nu] = a.fcol[j][f];
+                    ud[nu] = a.fdt[j][f];
+                    nu++;
+                }
+                a.fu[j][f] = u;
+            }
+        static const bool aos_off = [] {   // TQP_SORTPATH_AOS=0: gather each column (A/B)
+            const char* e = getenv("TQP_SORTPATH_AOS");
+            return e && e[0] == '0';
+        }();
+        if (fits && nu >= 2 && m >= (int64_t(1) << 20) && !aos_off) {
+            AosArgs aa{};
+            aa.m = m;
+            aa.sel = a.sel;
+            aa.nu = nu;
+            aa.stride = nu <= 2 ? 2 : 4;
+            for (int u = 0; u < nu; u++) { aa.col[u] = uc[u]; aa.dt[u] = ud[u]; }
+            aos.alloc(ctx, (size_t)m * aa.stride);
+            aa.aos = aos.get();
+            const int ag = (int)std::min<int64_t>(ceil_div(m, 256), (int64_t)ctx->num_sms * 8);
+            launch(ctx, "tqp_groupby_sortpath", sp_aos_kernel, dim3(ag), dim3(256), 0, aa);
+            double cb = 0;
+            for (int u = 0; u < nu; u++) cb += (double)dtype_size(ud[u]);
+            ctx->add_bytes("tqp_groupby_sortpath", (cb + 8.0 * aa.stride + (a.sel ? 8.0 : 0.0)) * (double)m);
+            a.aos = aos.get();
+            a.astride = aa.stride;
         }
     }
     a.perm = so.perm32.get();
