@@ -467,7 +467,9 @@ __global__ void __launch_bounds__(PNT, TQP_PROBE_MINB) probe_kernel(ProbeArgs a)
 // natural register count (3 blocks/SM) 0.437 / 0.441 / 0.476 and 0.298 / 0.335 / 0.428;
 // batch 1 at 6 blocks/SM 0.409 / 0.309 (default); batch 2 at 4 blocks 0.417 / 0.310 --
 // occupancy counts, not per-thread batching. All of a thread's sectors fetched at once
-// with cp.async into shared memory (64 KB per CTA, 3 CTAs/SM) measured 0.417 -> 0.660 ms. What bounds it is the random 32-byte
+// with cp.async into shared memory (64 KB per CTA, 3 CTAs/SM) measured 0.417 -> 0.660 ms;
+// an L2 evict-last policy on the sector loads left SF10 / SF100 unchanged (0.418 / 5.354
+// -> 0.411 / 5.360 ms). What bounds it is the random 32-byte
 // sector per probe row on top of the stream: a plain read-8 / write-16 bytes per row
 // kernel takes 0.236 ms for the same 60M rows (tools/membench.cu). ROUTE: 0 = rank
 // bitmap, 1 = slots. Same outputs as probe_kernel (join direct / u32 build row, semi, outer).
