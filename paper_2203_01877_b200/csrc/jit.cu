@@ -340,6 +340,10 @@ JitKernel* dense_jit_kernel(const DenseJitSpec& s) {
     auto& cache = jit_cache();
     auto it = cache.find(key);
     if (it != cache.end()) return it->second.k ? &it->second : nullptr;
+    // a bounded number of compiled plans per process (each holds a loaded module); past it,
+    // new plans run on the generic kernel
+    constexpr size_t MAX_PLANS = 256;
+    if (cache.size() >= MAX_PLANS) return nullptr;
     const std::string src = dense_jit_source(s);
     JitKernel jk;
     Nvrtc& nv = nvrtc();
