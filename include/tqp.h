@@ -114,7 +114,8 @@ void tqp_ctx_reset_counters(tqp_ctx* ctx);
 /* Plan-compiled kernels (process-wide, all contexts): the dense group-by kernel of
  * tqp_groupby_agg is compiled at run time for each distinct aggregation plan (NVRTC,
  * sm_100a; environment TQP_JIT=0 disables it, TQP_JIT_MIN_ROWS (default 2^20) is the
- * smallest input that uses it). Writes the number of plans compiled successfully, the
+ * smallest input that uses it; at most 256 plans are compiled per process, later ones run
+ * on the generic kernel). Writes the number of plans compiled successfully, the
  * compilations that failed (the generic kernel ran instead) and the launches of compiled
  * kernels; any pointer may be NULL. Returns 1 if the runtime compiler was found, else 0. */
 int tqp_jit_counters(int64_t* compiled_host, int64_t* failed_host, int64_t* launches_host);
