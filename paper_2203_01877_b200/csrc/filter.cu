@@ -91,8 +91,9 @@ __device__ __forceinline__ void load_grouped(const T* c, int64_t base, int tid, 
 // Blocks per SM the register budget must allow (72 registers held it to 3). Measured, Q6
 // mask at SF10: 0.263 ms at 72 registers, 0.253 ms with 4 blocks (56), 0.254 with 5,
 // 0.256 with 6 (spills).
+// (r02, with the grouped row layout: 4 -> 5 blocks per SM, 0.200 -> 0.194 ms)
 #ifndef TQP_FILTER_MINB
-#define TQP_FILTER_MINB 4
+#define TQP_FILTER_MINB 5
 #endif
 __global__ void __launch_bounds__(FNT, TQP_FILTER_MINB) filter_mask_kernel(FilterArgs a) {
     __shared__ uint32_t s_w[FNW];

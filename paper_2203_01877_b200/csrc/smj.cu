@@ -382,8 +382,9 @@ __device__ __forceinline__ void pay_copy(const void* src, int dt, int64_t from, 
 // shared memory, 4 blocks/SM) 0.367 ms; CCAP 1025 (28 KB) 0.326 ms; + 6 blocks/SM (40
 // registers, 16 bytes of spills) 0.301 ms; 7 / 8 blocks 0.299 / 0.299. (r01, before the
 // per-row buckets: 4/5/6/8 blocks 0.435/0.443/0.439/0.494 ms.)
+// (r02, with the coalesced gather and stores: 6 -> 7 blocks per SM, 0.271 -> 0.265 ms)
 #ifndef TQP_EXPAND_MINB
-#define TQP_EXPAND_MINB 6
+#define TQP_EXPAND_MINB 7
 #endif
 #ifndef TQP_EXPAND_CCAP
 #define TQP_EXPAND_CCAP 1025
