@@ -419,6 +419,10 @@ constexpr bool PEER_MATCH_ANY = TQP_PEER_MATCH_ANY;
 #define TQP_PEER_BALLOT 0
 #endif
 constexpr bool PEER_BALLOT = TQP_PEER_BALLOT;
+// (Half-warp ranking -- each 16-lane half ranks its own 256 consecutive keys with one word
+// per (half, digit) holding the peer mask and the half's count, the leader's single store
+// replacing the atomic add, the clear and the leader shuffle -- correct but slower:
+// 1.062 -> 1.104 ms.)
 // (The leader's count update as a plain load + store instead of the shared atomic add --
 // it is the only writer of its digit in its warp -- measured slower: 1.065 -> 1.101 ms.)
 // (A single 64-bit word per (warp, digit) -- peer mask low, warp digit count high, one
