@@ -963,6 +963,31 @@ def test_groupby_high_cardinality_sf1(T):
     check_groupby(T, got, want, aggs)
 
 
+@pytest.mark.parametrize("ncols", [2, 4])
+def test_groupby_sort_path_interleaved_gather(T, ncols):
+    """The high-cardinality sort path with 2 / 4 distinct factor columns of mixed dtypes
+    over 2M rows (above the 2^20-row threshold): the columns are interleaved per row
+    (16- / 32-byte records) before the reduction gathers them; no predicate, so the records
+    are indexed by row directly. Against the oracle."""
+    rng = np.random.default_rng(77 + ncols)
+    n = 2_000_003
+    k = rng.integers(0, 700_000, n)
+    cols = [k]
+    gcols = [cu(k)]
+    dts = [torch.int64, torch.int32, torch.uint8, torch.int64]
+    for c in range(ncols):
+        dt = dts[c]
+        hi = {torch.uint8: 255, torch.int32: 1 << 20, torch.int64: 1 << 30}[dt]
+        v = rng.integers(0 if dt == torch.uint8 else -hi, hi + 1, n)
+        cols.append(v.astype(np.int64))
+        gcols.append(cu(v, dt))
+    aggs = [("sum", [(1, 0, 1)]), ("count", []), ("max", [(2, 3, -1)]), ("sum", [(1, 0, 1), (2, 1, 1)])]
+    if ncols == 4:
+        aggs += [("min", [(3, 0, 1)]), ("avg", [(4, 0, 1)])]
+    got = T.groupby_agg(gcols, [0], aggs)
+    check_groupby(T, got, oracle.groupby_agg(cols, [0], aggs), aggs)
+
+
 def test_groupby_empty_and_global(T):
     e = cu(np.array([], np.int64))
     got = T.groupby_agg([e], [0], [("sum", [(0, 0, 1)])])
