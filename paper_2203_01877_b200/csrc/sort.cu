@@ -28,7 +28,7 @@ namespace tqp {
 
 constexpr int NT = 256;   // threads per CTA in the sort kernels
 constexpr int NW = NT / 32;
-constexpr int CHUNK = 128;   // tiles per scan chunk
+constexpr int CHUNK = 128;   // tiles per scan chunk (64 / 32 measured slower: 0.083 / 0.118 ms vs 0.071 for the SMJ sort)
 
 enum InMode { IN_INTERNAL = 0, IN_I64 = 1, IN_I32 = 2, IN_U8 = 3, IN_U64 = 4 };
 
